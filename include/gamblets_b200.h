@@ -1,0 +1,186 @@
+/* C ABI of libgamblets_b200.so -- the drop-in boundary of the B200 gamblet
+ * hot path (arXiv 1503.03467; reference: /root/reference/pkg/src/gamblets).
+ *
+ * The reference is a pure-Python package with no FFI of its own; its boundary
+ * is the Python API re-exported in gamblets/__init__.py:10-94.  This library
+ * sits *under* a Python shim (paper_1503_03467_b200) that keeps those
+ * signatures and binds these symbols with ctypes.  Each
+ * entry point below names the reference call site it replaces.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer (cudaMalloc / torch storage) unless
+ *     named host_*; sizes are plain ints; `stream` is a cudaStream_t passed
+ *     as void*; calls are asynchronous on that stream.
+ *   - return value: GB_OK, GB_ERR_INVALID (bad argument, the shim raises
+ *     InvalidArgumentError) or GB_ERR_CUDA (launch failure; message in
+ *     gb_last_error()).  Numerical failures found on the device (nonpositive
+ *     diagonal, non-SPD patch, CG breakdown) are written to the caller's
+ *     int64 status block {code, detail}; the shim raises NumericalError.
+ *   - box-stencil layout of every level operator: see
+ *     paper_1503_03467_b200/csrc/gb_common.cuh and DESIGN.md section 3.
+ */
+#ifndef GAMBLETS_B200_H
+#define GAMBLETS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GB_OK 0
+#define GB_ERR_INVALID 1
+#define GB_ERR_NUMERICAL 2
+#define GB_ERR_CUDA 3
+
+/* device status codes (status[0]) */
+#define GB_ST_NONPOS_DIAG 1
+#define GB_ST_NOT_SPD 2
+#define GB_ST_OUTSIDE_BOX 3
+#define GB_ST_CG_BREAKDOWN 4
+
+/* CSR export kinds */
+#define GB_EXP_SQUARE 0
+#define GB_EXP_CHILD 1
+#define GB_EXP_PSI 2
+#define GB_EXP_TDT 3
+
+int gb_abi_version(void);
+const char* gb_last_error(void);
+int gb_device_count(void);
+
+/* ---- input conversion: canonical CSR (fine grid side n) -> box ----------
+ * replaces as_csr(M)/as_csr(A) in fast_transform (gamblet_fast.py:645-646)
+ * and the implicit 9-point stencil of grid_fem._assemble (grid_fem.py:205-214) */
+int gb_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,
+                     int32_t* out_w, void* stream);
+int gb_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
+                  const double* data, double* box, int64_t* status, void* stream);
+
+/* ---- unit-diagonal congruence s = diag^-1/2 (gamblet_fast.py:123-139) ---- */
+int gb_box_scale(int64_t rows, int nr, int w, const double* box, double* s,
+                 int64_t* status, void* stream);
+
+/* ---- symmetrize + dead-tail drop (gamblet_exact.py:95-103,
+ *      gamblet_fast.py:154-169); dmin preset to +inf, stats to 0 ------------ */
+int gb_box_diag_min(int64_t rows, int nr, int w, const double* box, double* dmin,
+                    void* stream);
+int gb_box_sym_drop(int L, int nr, int w, const double* raw, double* out,
+                    const double* dmin, double* stats, void* stream);
+/* row-tail drop (gamblet_fast.py:172-190) on dense row windows */
+int gb_row_tail_drop(int64_t rows, int64_t S, double* v, void* stream);
+
+/* ---- K1 mass patches: local_mass_inverse (gamblet_fast.py:464-498) ------- */
+size_t gb_mass_patch_workspace(int rho, int blocks);
+int gb_mass_patches(int n, int wM, const double* M, const double* s, int rho, int wd,
+                    double* psi, int64_t* status, double* workspace, int blocks,
+                    void* stream);
+
+/* ---- K2 A^(q) = psi A psi^T (gamblet_fast.py:658-665) -------------------- */
+int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
+                   const double* A, int wX, double* X, void* stream);
+int gb_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
+                    const double* X, int wR, double* raw, void* stream);
+
+/* ---- K3 B = W A W^T, G = W A pibar^T, P A P^T (gamblet_fast.py:520-544,
+ *      597-601); w12 = the 3x4 null-basis template (hierarchy.py:31-42) ----- */
+int gb_level_diag(int Lk, int wA, const double* A, const double* host_w12,
+                  double* bdiag, double* dmin, void* stream);
+int gb_level_blocks(int Lk, int wA, const double* A, const double* host_w12, int wB,
+                    const double* bdiag, const double* dmin, double* B, double* G,
+                    double* PAPt, double* stats, void* stream);
+
+/* ---- K4 correction patches (gamblet_fast.py:546-591) --------------------- */
+size_t gb_correction_workspace(int rho, int blocks);
+int gb_correction_patches(int Lp, int wB, const double* B, const double* sB, int wG,
+                          const double* G, int rho, double* Dt, int64_t* status,
+                          double* workspace, int blocks, void* stream);
+
+/* ---- K6 R, split triple product, psi^(k-1) (gamblet_fast.py:587-624) ----- */
+int gb_restriction(int Lp, int rho, const double* Dt, const double* host_w12,
+                   double* R, void* stream);
+int gb_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
+          double* BD, void* stream);
+int gb_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
+           double* GtD, void* stream);
+int gb_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
+                  int rho, const double* Dt, int wBD, const double* BD, int wA2,
+                  double* raw, void* stream);
+int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double* psi,
+            int wdw, double* Wpsi, void* stream);
+int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                double* psi_next, void* stream);
+
+/* ---- K7/K8 Krylov (sparse_core.py:126-165, 232-278;
+ *      gamblet_fast.py:380-387, 717-760) ---------------------------------- */
+size_t gb_kstate_bytes(void);
+int gb_red_blocks(void);
+int gb_state_reset(void* state, int max_iter, void* stream);
+int gb_cg_init(int64_t n, const double* b, const double* x0, const double* Ax0,
+               double* x, double* r, double* p, double rel_tol, int max_iter,
+               void* state, double* partials, void* stream);
+int gb_cg_iterations(int L, int nr, int w, const double* B, const double* s, int mode,
+                     double* x, double* r, double* p, double* Ap, int iters,
+                     void* state, double* partials, void* stream);
+int gb_pow_iterations(int L, int nr, int w, const double* B, const double* s, int mode,
+                      double* x, double* y, double tol, int iters, void* state,
+                      double* partials, void* stream);
+int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
+            void* state, double* partials, void* stream);
+int gb_scale_by_norm(int64_t n, const double* a, const double* norm2, int which,
+                     double* y, double* y2, void* stream);
+int gb_box_apply(int L, int nr, int w, const double* B, const double* s, int mode,
+                 const double* x, double* y, void* stream);
+
+/* ---- K9 load-dependent transfers (gamblet_fast.py:726-765) --------------- */
+int gb_apply_w(int Lp, const double* host_w12, const double* g, const double* s,
+               double* out, void* stream);
+int gb_apply_wt(int Lp, const double* host_w12, const double* w, double* v,
+                void* stream);
+int gb_apply_r(int Lp, int rho, const double* R, const double* g, double* out,
+               void* stream);
+int gb_psi_t_apply(int n, int L, int lo, int wd, const double* psi, const double* v,
+                   double* inc, void* stream);
+int gb_psi_apply(int n, int L, int lo, int wd, const double* psi, const double* b,
+                 double* out, void* stream);
+int gb_axpby(int64_t n, double a, const double* x, double b, const double* y,
+             double* out, void* stream);
+int gb_vmul(int64_t n, const double* a, const double* b, double* out, void* stream);
+int gb_vadd(int64_t n, const double* a, const double* b, double* out, void* stream);
+
+/* ---- CSR export at the API edge (the .stiffness/.subband/... attributes,
+ *      gamblet_fast.py:626-632; canonical form of sparse_core.py:47-67) ---- */
+int gb_export_count(int kind, int L, int nr, int w, int nc, int n, int lo, int wd,
+                    const double* val, int64_t rows, int64_t S, int64_t* counts,
+                    void* stream);
+int gb_exclusive_scan(const int64_t* counts, int64_t* indptr, int64_t n, void* tmp,
+                      size_t* tmp_bytes, void* stream);
+int gb_export_emit(int kind, int L, int nr, int w, int nc, int n, int lo, int wd,
+                   const double* val, int64_t rows, int64_t S, const int64_t* indptr,
+                   int32_t* indices, double* data, void* stream);
+
+/* ---- K10 exact path, dense (gamblet_exact.py:115-263) -------------------- */
+int gb_dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta,
+                  const double* B, int ldb, int tb, double beta, double* C, int ldc,
+                  void* stream);
+int gb_dense_potrf(int n, double* A, int lda, int64_t* status, void* stream);
+int gb_dense_potrs(int n, int nrhs, const double* L, int lda, double* B, int ldb,
+                   void* stream);
+int gb_dense_sym(int n, const double* X, int ldx, double* out, double* stats,
+                 void* stream);
+
+int gb_csr_to_dense(int nrows, int ncols, const int32_t* indptr, const int32_t* indices,
+                    const double* data, double* out, void* stream);
+int gb_eye(int n, double* out, void* stream);
+int gb_dense_build_w(int Lk, const double* host_w12, double* out, void* stream);
+int gb_dense_build_p(int Lk, double* out, double scale, void* stream);
+
+/* ---- FP64 peak probes (DFMA / DMMA) used for the roofline denominators --- */
+int gb_fp64_peak_probe(int kind, int iters, double* sink, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAMBLETS_B200_H */

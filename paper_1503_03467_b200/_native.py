@@ -1,0 +1,124 @@
+"""ctypes binding of libgamblets_b200.so (the C ABI in include/gamblets_b200.h).
+
+There is no fallback: if the library is missing or no CUDA device is present
+every entry point raises.  Device buffers are torch tensors (ownership and
+the caching allocator only); the kernels see raw pointers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import InvalidArgumentError, NumericalError
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libgamblets_b200.so"
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_D = ctypes.c_double
+_Z = ctypes.c_size_t
+
+# name -> (argtypes, restype)
+_SIGS = {
+    "gb_abi_version": ([], _I),
+    "gb_last_error": ([], ctypes.c_char_p),
+    "gb_device_count": ([], _I),
+    "gb_csr_halfwidth": ([_I, _P, _P, _P, _P], _I),
+    "gb_csr_to_box": ([_I, _I, _P, _P, _P, _P, _P, _P], _I),
+    "gb_box_scale": ([_L, _I, _I, _P, _P, _P, _P], _I),
+    "gb_box_diag_min": ([_L, _I, _I, _P, _P, _P], _I),
+    "gb_box_sym_drop": ([_I, _I, _I, _P, _P, _P, _P, _P], _I),
+    "gb_row_tail_drop": ([_L, _L, _P, _P], _I),
+    "gb_mass_patch_workspace": ([_I, _I], _Z),
+    "gb_mass_patches": ([_I, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P], _I),
+    "gb_psi_stencil": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb_psi_galerkin": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb_level_diag": ([_I, _I, _P, _P, _P, _P, _P], _I),
+    "gb_level_blocks": ([_I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
+    "gb_correction_workspace": ([_I, _I], _Z),
+    "gb_correction_patches": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _P, _I, _P], _I),
+    "gb_restriction": ([_I, _I, _P, _P, _P, _P], _I),
+    "gb_bd": ([_I, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb_gtd": ([_I, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb_coarse_raw": ([_I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb_wpsi": ([_I, _I, _I, _I, _P, _P, _I, _P, _P], _I),
+    "gb_psi_next": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P, _P], _I),
+    "gb_kstate_bytes": ([], _Z),
+    "gb_red_blocks": ([], _I),
+    "gb_state_reset": ([_P, _I, _P], _I),
+    "gb_cg_init": ([_L, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_cg_iterations": ([_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P], _I),
+    "gb_pow_iterations": ([_I, _I, _I, _P, _P, _I, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
+    "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),
+    "gb_box_apply": ([_I, _I, _I, _P, _P, _I, _P, _P, _P], _I),
+    "gb_apply_w": ([_I, _P, _P, _P, _P, _P], _I),
+    "gb_apply_wt": ([_I, _P, _P, _P, _P], _I),
+    "gb_apply_r": ([_I, _I, _P, _P, _P, _P], _I),
+    "gb_psi_t_apply": ([_I, _I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_psi_apply": ([_I, _I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_axpby": ([_L, _D, _P, _D, _P, _P, _P], _I),
+    "gb_vmul": ([_L, _P, _P, _P, _P], _I),
+    "gb_vadd": ([_L, _P, _P, _P, _P], _I),
+    "gb_export_count": ([_I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _L, _P, _P], _I),
+    "gb_exclusive_scan": ([_P, _P, _L, _P, _P, _P], _I),
+    "gb_export_emit": ([_I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _L, _P, _P, _P, _P], _I),
+    "gb_dense_gemm": ([_I, _I, _I, _D, _P, _I, _I, _P, _I, _I, _D, _P, _I, _P], _I),
+    "gb_dense_potrf": ([_I, _P, _I, _P, _P], _I),
+    "gb_dense_potrs": ([_I, _I, _P, _I, _P, _I, _P], _I),
+    "gb_dense_sym": ([_I, _P, _I, _P, _P, _P], _I),
+    "gb_dense_build_w": ([_I, _P, _P, _P], _I),
+    "gb_dense_build_p": ([_I, _P, _D, _P], _I),
+    "gb_csr_to_dense": ([_I, _I, _P, _P, _P, _P, _P], _I),
+    "gb_eye": ([_I, _P, _P], _I),
+    "gb_fp64_peak_probe": ([_I, _I, _P, _P], _I),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path=None):
+    """Load (once) and return the ctypes library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA library first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = ctypes.CDLL(str(p), mode=ctypes.RTLD_GLOBAL)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error():
+    msg = load().gb_last_error()
+    return msg.decode() if msg else ""
+
+
+def call(name, *args):
+    """Invoke one C entry point and map its status to the API exceptions."""
+    rc = getattr(load(), name)(*args)
+    if rc == 0:
+        return 0
+    if rc == 1:
+        raise InvalidArgumentError(f"{name}: {last_error()}")
+    if rc == 2:
+        raise NumericalError(f"{name}: {last_error()}")
+    raise RuntimeError(f"{name} failed: {last_error()}")
+
+
+def query(name, *args):
+    """Entry points that return a value instead of a status."""
+    return getattr(load(), name)(*args)

@@ -1,0 +1,357 @@
+// Box-stencil plumbing: CSR input -> box, diagonal scaling, symmetrize + tail
+// drop, row-tail drop and the box -> canonical CSR export at the API edge.
+#include <cub/cub.cuh>
+
+#include "gb_common.cuh"
+#include "gb_kernels.h"
+
+namespace gb {
+
+// ---------------------------------------------------------------------------
+// CSR (fine grid, side n) -> box of half-width w
+// ---------------------------------------------------------------------------
+__global__ void k_csr_halfwidth(int n, const int32_t* __restrict__ indptr,
+                                const int32_t* __restrict__ indices,
+                                int* __restrict__ out) {
+  const long long N = (long long)n * n;
+  int m = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < N;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int rs = (int)(r / n), rt = (int)(r % n);
+    for (int e = indptr[r]; e < indptr[r + 1]; ++e) {
+      const int c = indices[e];
+      const int ds = c / n - rs, dt = c % n - rt;
+      m = imax(m, imax(ds < 0 ? -ds : ds, dt < 0 ? -dt : dt));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = imax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_csr_to_box(int n, int w, const int32_t* __restrict__ indptr,
+                             const int32_t* __restrict__ indices,
+                             const double* __restrict__ data,
+                             double* __restrict__ box, long long* status) {
+  const long long N = (long long)n * n;
+  const int S = box_slots(w, 1);
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < N;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int rs = (int)(r / n), rt = (int)(r % n);
+    for (int e = indptr[r]; e < indptr[r + 1]; ++e) {
+      const int c = indices[e];
+      const int ds = c / n - rs, dt = c % n - rt;
+      if (ds < -w || ds > w || dt < -w || dt > w) {
+        raise_status(status, ST_OUTSIDE_BOX, r);
+        continue;
+      }
+      box[r * S + slot_of(w, 1, ds, dt, 0)] += data[e];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// s = diag^-1/2 (gamblet_fast.py:123-139), nonpositive diagonal -> status
+// ---------------------------------------------------------------------------
+__global__ void k_box_scale(long long rows, int nr, int w,
+                            const double* __restrict__ box,
+                            double* __restrict__ s, long long* status) {
+  const int S = box_slots(w, nr);
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(r % nr);
+    const double d = box[r * S + slot_of(w, nr, 0, 0, c)];
+    if (!(d > 0.0)) {
+      raise_status(status, ST_NONPOS_DIAG, r);
+      s[r] = 0.0;
+    } else {
+      s[r] = 1.0 / sqrt(d);
+    }
+  }
+}
+
+// min of the diagonal (the tail drop is skipped when it is <= 0,
+// gamblet_fast.py:157-159); dmin must be pre-set to +inf by the caller.
+__global__ void k_box_diag_min(long long rows, int nr, int w,
+                               const double* __restrict__ box,
+                               double* __restrict__ dmin) {
+  const int S = box_slots(w, nr);
+  double m = __longlong_as_double(0x7ff0000000000000ll);
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    m = fmin(m, box[r * S + slot_of(w, nr, 0, 0, (int)(r % nr))]);
+  }
+  m = warp_min(m);
+  if ((threadIdx.x & 31) == 0) {
+    // atomic min on doubles via CAS (values may be negative)
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(dmin);
+    unsigned long long old = *a, assumed;
+    do {
+      assumed = old;
+      if (__longlong_as_double((long long)assumed) <= m) break;
+      old = atomicCAS(a, assumed, (unsigned long long)__double_as_longlong(m));
+    } while (assumed != old);
+  }
+}
+
+// (X + X^T) * 0.5 with the repair statistics, then the symmetric dead-tail
+// drop |x| < 1e-12 sqrt(d_i d_j) off the diagonal (gamblet_exact.py:95-103,
+// gamblet_fast.py:154-169).  stats[0] = max|x_ij - x_ji|, stats[1] = max|x|.
+__global__ void k_box_sym_drop(int L, int nr, int w, const double* __restrict__ raw,
+                               double* __restrict__ out,
+                               const double* __restrict__ dmin,
+                               double* __restrict__ stats) {
+  const int S = box_slots(w, nr);
+  const long long total = (long long)L * L * nr * S;
+  const bool do_drop = *dmin > 0.0;
+  double mdiff = 0.0, mabs = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / S;
+    const int sl = (int)(e - r * S);
+    const int cp = sl % nr;
+    const int bs = sl / nr;
+    const int ds = bs / (2 * w + 1) - w, dt = bs % (2 * w + 1) - w;
+    const long long p = r / nr;
+    const int c = (int)(r - p * nr);
+    const int ps = (int)(p / L), pt = (int)(p % L);
+    const int qs = ps + ds, qt = pt + dt;
+    double v = 0.0;
+    if (qs >= 0 && qs < L && qt >= 0 && qt < L) {
+      const long long r2 = ((long long)qs * L + qt) * nr + cp;
+      const double a = raw[e];
+      const double b = raw[r2 * S + slot_of(w, nr, -ds, -dt, c)];
+      mdiff = fmax(mdiff, fabs(a - b));
+      mabs = fmax(mabs, fabs(a));
+      v = (a + b) * 0.5;
+      const bool diag = (r2 == r);
+      if (do_drop && !diag) {
+        const double di = raw[r * S + slot_of(w, nr, 0, 0, c)];
+        const double dj = raw[r2 * S + slot_of(w, nr, 0, 0, cp)];
+        if (!(fabs(v) >= 1e-12 * sqrt(di * dj))) v = 0.0;
+      }
+    }
+    out[e] = v;
+  }
+  mdiff = warp_max(mdiff);
+  mabs = warp_max(mabs);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&stats[0], mdiff);
+    atomic_max_nonneg(&stats[1], mabs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row-tail drop |x| < 1e-11 * rowmax (gamblet_fast.py:172-190) on a dense row
+// layout (one block per row; used for psi^(k) windows)
+// ---------------------------------------------------------------------------
+__global__ void k_row_tail_drop(long long rows, long long S, double* __restrict__ v) {
+  __shared__ double sh[32];
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    double* row = v + r * S;
+    double m = 0.0;
+    for (long long j = threadIdx.x; j < S; j += blockDim.x) m = fmax(m, fabs(row[j]));
+    m = block_max(m, sh);
+    const double thr = 1e-11 * m;
+    for (long long j = threadIdx.x; j < S; j += blockDim.x) {
+      const double x = row[j];
+      if (!(fabs(x) >= thr)) row[j] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR export.  `kind` selects the slot enumeration in ascending global column
+// order and the column map:
+//   EXP_SQUARE : rows (p,c) on LxL x nr, cols (p+d, c') x nc
+//   EXP_CHILD  : rows i on LxL, cols children of (i+d) on (2L)x(2L); slot (d, b)
+//   EXP_PSI    : rows of level side L, fine window (n, lo, wd, h = n/L)
+//   EXP_TDT    : D = Dt^T; rows (p,c) on LxL x3, cols i with Dt[i][(p-i, c)]
+// ---------------------------------------------------------------------------
+struct ExportDesc {
+  int kind, L, nr, w, nc;  // box geometry (for EXP_TDT: Dt's half-width w)
+  int n, lo, wd;           // psi window geometry
+};
+
+__device__ __forceinline__ bool export_entry(const ExportDesc& d,
+                                             const double* __restrict__ val,
+                                             long long r, long long j, double* v,
+                                             int* col) {
+  if (d.kind == EXP_SQUARE) {
+    const int S = box_slots(d.w, d.nc);
+    const int cp = (int)(j % d.nc);
+    const int bs = (int)(j / d.nc);
+    const int ds = bs / (2 * d.w + 1) - d.w, dt = bs % (2 * d.w + 1) - d.w;
+    const long long p = r / d.nr;
+    const int qs = (int)(p / d.L) + ds, qt = (int)(p % d.L) + dt;
+    if (qs < 0 || qs >= d.L || qt < 0 || qt >= d.L) return false;
+    *v = val[r * S + j];
+    *col = (qs * d.L + qt) * d.nc + cp;
+    return *v != 0.0;
+  } else if (d.kind == EXP_CHILD) {
+    const int W2 = 2 * d.w + 1;
+    const int beta = (int)(j & 1);
+    long long t = j >> 1;
+    const int dti = (int)(t % W2);
+    t /= W2;
+    const int alpha = (int)(t & 1);
+    const int dsi = (int)(t >> 1);
+    const int ds = dsi - d.w, dt = dti - d.w;
+    const int qs = (int)(r / d.L) + ds, qt = (int)(r % d.L) + dt;
+    if (qs < 0 || qs >= d.L || qt < 0 || qt >= d.L) return false;
+    const int S = W2 * W2 * 4;
+    *v = val[r * S + (dsi * W2 + dti) * 4 + 2 * alpha + beta];
+    *col = (2 * qs + alpha) * (2 * d.L) + 2 * qt + beta;
+    return *v != 0.0;
+  } else if (d.kind == EXP_PSI) {
+    const int h = d.n / d.L;
+    const int os = clampi((int)(r / d.L) * h + d.lo, 0, d.n - d.wd);
+    const int ot = clampi((int)(r % d.L) * h + d.lo, 0, d.n - d.wd);
+    const int a = (int)(j / d.wd), b = (int)(j % d.wd);
+    *v = val[r * (long long)d.wd * d.wd + j];
+    *col = (os + a) * d.n + (ot + b);
+    return *v != 0.0;
+  } else {  // EXP_TDT
+    const int W2 = 2 * d.w + 1;
+    const long long p = r / 3;
+    const int c = (int)(r % 3);
+    const int dis = (int)(j / W2) - d.w, dit = (int)(j % W2) - d.w;
+    const int is = (int)(p / d.L) + dis, it = (int)(p % d.L) + dit;
+    if (is < 0 || is >= d.L || it < 0 || it >= d.L) return false;
+    const long long i = (long long)is * d.L + it;
+    *v = val[i * (W2 * W2 * 3) + slot_of(d.w, 3, -dis, -dit, c)];
+    *col = (int)i;
+    return *v != 0.0;
+  }
+}
+
+__global__ void k_export_count(ExportDesc d, const double* __restrict__ val,
+                               long long rows, long long S,
+                               long long* __restrict__ counts) {
+  __shared__ double sh[32];
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    double c = 0.0;
+    for (long long j = threadIdx.x; j < S; j += blockDim.x) {
+      double v;
+      int col;
+      if (export_entry(d, val, r, j, &v, &col)) c += 1.0;
+    }
+    c = block_sum(c, sh);
+    if (threadIdx.x == 0) counts[r] = (long long)c;
+    __syncthreads();
+  }
+}
+
+__global__ void k_export_emit(ExportDesc d, const double* __restrict__ val,
+                              long long rows, long long S,
+                              const long long* __restrict__ indptr,
+                              int32_t* __restrict__ indices,
+                              double* __restrict__ data) {
+  typedef cub::BlockScan<int, 256> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const long long base = indptr[r];
+    for (long long j0 = 0; j0 < S; j0 += 256) {
+      const long long j = j0 + threadIdx.x;
+      double v = 0.0;
+      int col = 0;
+      const int keep = (j < S) && export_entry(d, val, r, j, &v, &col);
+      int pos, tot;
+      Scan(tmp).ExclusiveSum(keep, pos, tot);
+      if (keep) {
+        indices[base + carry + pos] = col;
+        data[base + carry + pos] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) carry += tot;
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace gb
+
+// ===========================================================================
+// host launchers
+// ===========================================================================
+using namespace gb;
+
+static inline int grid_for(long long work, int block, int cap = 148 * 64) {
+  long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+int gbk_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,
+                      int* out, cudaStream_t s) {
+  const long long N = (long long)n * n;
+  k_csr_halfwidth<<<grid_for(N, 256), 256, 0, s>>>(n, indptr, indices, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
+                   const double* data, double* box, long long* status,
+                   cudaStream_t s) {
+  const long long N = (long long)n * n;
+  k_csr_to_box<<<grid_for(N, 256), 256, 0, s>>>(n, w, indptr, indices, data, box,
+                                                status);
+  return (int)cudaGetLastError();
+}
+
+int gbk_box_scale(long long rows, int nr, int w, const double* box, double* sv,
+                  long long* status, cudaStream_t s) {
+  k_box_scale<<<grid_for(rows, 256), 256, 0, s>>>(rows, nr, w, box, sv, status);
+  return (int)cudaGetLastError();
+}
+
+int gbk_box_diag_min(long long rows, int nr, int w, const double* box,
+                     double* dmin, cudaStream_t s) {
+  k_box_diag_min<<<grid_for(rows, 256), 256, 0, s>>>(rows, nr, w, box, dmin);
+  return (int)cudaGetLastError();
+}
+
+int gbk_box_sym_drop(int L, int nr, int w, const double* raw, double* out,
+                     const double* dmin, double* stats, cudaStream_t s) {
+  const long long total = (long long)L * L * nr * box_slots(w, nr);
+  k_box_sym_drop<<<grid_for(total, 256), 256, 0, s>>>(L, nr, w, raw, out, dmin,
+                                                      stats);
+  return (int)cudaGetLastError();
+}
+
+int gbk_row_tail_drop(long long rows, long long S, double* v, cudaStream_t s) {
+  const int g = (int)(rows < 65535 * 4 ? rows : 65535 * 4);
+  k_row_tail_drop<<<g, 256, 0, s>>>(rows, S, v);
+  return (int)cudaGetLastError();
+}
+
+int gbk_export_count(int kind, int L, int nr, int w, int nc, int n, int lo,
+                     int wd, const double* val, long long rows, long long S,
+                     long long* counts, cudaStream_t s) {
+  ExportDesc d{kind, L, nr, w, nc, n, lo, wd};
+  const int g = (int)(rows < (1ll << 30) ? rows : (1ll << 30));
+  k_export_count<<<g, 256, 0, s>>>(d, val, rows, S, counts);
+  return (int)cudaGetLastError();
+}
+
+int gbk_exclusive_scan(const long long* counts, long long* indptr, long long n,
+                       void* tmp, size_t* tmp_bytes, cudaStream_t s) {
+  // indptr has n+1 entries: exclusive scan of counts over n+1 inputs where the
+  // caller guarantees counts[n] == 0.
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, counts, indptr,
+                                                (int)(n + 1), s);
+  return (int)e;
+}
+
+int gbk_export_emit(int kind, int L, int nr, int w, int nc, int n, int lo,
+                    int wd, const double* val, long long rows, long long S,
+                    const long long* indptr, int32_t* indices, double* data,
+                    cudaStream_t s) {
+  ExportDesc d{kind, L, nr, w, nc, n, lo, wd};
+  const int g = (int)(rows < (1ll << 30) ? rows : (1ll << 30));
+  k_export_emit<<<g, 256, 0, s>>>(d, val, rows, S, indptr, indices, data);
+  return (int)cudaGetLastError();
+}

@@ -1,0 +1,348 @@
+// K10: dense FP64 kernels for the exact (global-gamblet) path,
+// gamblet_exact.py:115-263 (config 0).  Row-major storage throughout.
+//
+//   - tiled DGEMM  C = alpha op(A) op(B) + beta C  (64x64 tiles, DFMA)
+//   - blocked right-looking Cholesky (panel in one CTA + DGEMM trailing update)
+//   - blocked triangular solves L L^T X = B (diagonal blocks by one CTA,
+//     off-diagonal updates by DGEMM)
+//   - (X + X^T)/2 with the repair statistics of gamblet_exact.py:95-103
+//   - FP64 peak probes (DFMA chains, DMMA m8n8k4) for the roofline
+//
+// config 0 is launch/latency bound (6.4 GFlop total); these
+// kernels aim for correctness and reasonable DFMA use, not peak.
+#include "gb_common.cuh"
+
+namespace gb {
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+__global__ void __launch_bounds__(256) k_dgemm(int m, int n, int k, double alpha,
+                                               const double* __restrict__ A, int lda,
+                                               int ta, const double* __restrict__ B,
+                                               int ldb, int tb, double beta,
+                                               double* __restrict__ C, int ldc) {
+  __shared__ double As[TK][TM + 1];
+  __shared__ double Bs[TK][TN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int row0 = blockIdx.y * TM, col0 = blockIdx.x * TN;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < k; k0 += TK) {
+    for (int e = threadIdx.x; e < TM * TK; e += 256) {
+      const int r = e / TK, kk = e % TK;
+      const int gr = row0 + r, gk = k0 + kk;
+      double v = 0.0;
+      if (gr < m && gk < k) v = ta ? A[(long long)gk * lda + gr] : A[(long long)gr * lda + gk];
+      As[kk][r] = v;
+    }
+    for (int e = threadIdx.x; e < TK * TN; e += 256) {
+      const int kk = e / TN, c = e % TN;
+      const int gk = k0 + kk, gc = col0 + c;
+      double v = 0.0;
+      if (gk < k && gc < n) v = tb ? B[(long long)gc * ldb + gk] : B[(long long)gk * ldb + gc];
+      Bs[kk][c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = row0 + ty + 16 * i;
+    if (gr >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = col0 + tx + 16 * j;
+      if (gc >= n) continue;
+      double* c = C + (long long)gr * ldc + gc;
+      *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[i][j];
+    }
+  }
+}
+
+// unblocked Cholesky of the nb x nb diagonal block at (j0, j0) by one CTA;
+// then the panel below it: L21 = A21 L11^-T (rows independent)
+__global__ void k_potrf_panel(int n, int j0, int nb, double* __restrict__ A, int lda,
+                              long long* status) {
+  __shared__ double colj[256];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* a = A + (long long)j0 * lda + j0;
+  for (int j = 0; j < nb; ++j) {
+    const double d = a[(long long)j * lda + j];
+    if (!(d > 0.0)) {
+      if (tid == 0) raise_status(status, ST_NOT_SPD, j0 + j);
+      return;
+    }
+    const double l = sqrt(d);
+    for (int i = j + 1 + tid; i < nb; i += nt) {
+      const double v = a[(long long)i * lda + j] / l;
+      a[(long long)i * lda + j] = v;
+      colj[i] = v;
+    }
+    __syncthreads();
+    if (tid == 0) a[(long long)j * lda + j] = l;
+    for (int e = tid; e < nb * nb; e += nt) {
+      const int i = e / nb, kk = e % nb;
+      if (i > j && kk > j && kk <= i) a[(long long)i * lda + kk] -= colj[i] * colj[kk];
+    }
+    __syncthreads();
+  }
+  // panel rows i >= j0+nb: solve x L11^T = a_i (forward substitution)
+  for (int i = j0 + nb + tid; i < n; i += nt) {
+    double* ai = A + (long long)i * lda + j0;
+    for (int j = 0; j < nb; ++j) {
+      double v = ai[j];
+      for (int kk = 0; kk < j; ++kk) v -= ai[kk] * a[(long long)j * lda + kk];
+      ai[j] = v / a[(long long)j * lda + j];
+    }
+  }
+}
+
+// zero the strict upper triangle (A becomes L)
+__global__ void k_tril(int n, double* A, int lda) {
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    if (j > i) A[(long long)i * lda + j] = 0.0;
+  }
+}
+
+// diagonal-block triangular solves on rows [j0, j0+nb) for all nrhs columns
+// forward (L y = b) when fwd, else backward (L^T z = y); one thread per column
+__global__ void k_trsv_block(int j0, int nb, int nrhs, const double* __restrict__ L,
+                             int lda, double* __restrict__ X, int ldx, int fwd) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nrhs;
+       c += gridDim.x * blockDim.x) {
+    if (fwd) {
+      for (int i = 0; i < nb; ++i) {
+        double v = X[(long long)(j0 + i) * ldx + c];
+        for (int kk = 0; kk < i; ++kk)
+          v -= L[(long long)(j0 + i) * lda + j0 + kk] * X[(long long)(j0 + kk) * ldx + c];
+        X[(long long)(j0 + i) * ldx + c] = v / L[(long long)(j0 + i) * lda + j0 + i];
+      }
+    } else {
+      for (int i = nb - 1; i >= 0; --i) {
+        double v = X[(long long)(j0 + i) * ldx + c];
+        for (int kk = i + 1; kk < nb; ++kk)
+          v -= L[(long long)(j0 + kk) * lda + j0 + i] * X[(long long)(j0 + kk) * ldx + c];
+        X[(long long)(j0 + i) * ldx + c] = v / L[(long long)(j0 + i) * lda + j0 + i];
+      }
+    }
+  }
+}
+
+__global__ void k_dense_sym(int n, const double* __restrict__ X, int ldx,
+                            double* __restrict__ out, double* __restrict__ stats) {
+  const long long total = (long long)n * n;
+  double md = 0.0, ma = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    const double a = X[(long long)i * ldx + j], b = X[(long long)j * ldx + i];
+    md = fmax(md, fabs(a - b));
+    ma = fmax(ma, fabs(a));
+    out[(long long)i * n + j] = (a + b) * 0.5;
+  }
+  md = warp_max(md);
+  ma = warp_max(ma);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&stats[0], md);
+    atomic_max_nonneg(&stats[1], ma);
+  }
+}
+
+// dense W^(k) (3*4^(k-1) x 4^k) from the template, and dense s * pi^(k-1,k)
+__global__ void k_dense_build_w(int Lk, WTemplate W, double* __restrict__ out) {
+  const int Lp = Lk / 2;
+  const long long cols = (long long)Lk * Lk;
+  const long long total = (long long)Lp * Lp * 3 * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols, c = e % cols;
+    const long long p = r / 3;
+    const int comp = (int)(r % 3);
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    const int cs = (int)(c / Lk), ct = (int)(c % Lk);
+    double v = 0.0;
+    if (cs / 2 == ps && ct / 2 == pt) v = W.w[comp][2 * (cs & 1) + (ct & 1)];
+    out[e] = v;
+  }
+}
+
+__global__ void k_dense_build_p(int Lk, double scale, double* __restrict__ out) {
+  const int Lp = Lk / 2;
+  const long long cols = (long long)Lk * Lk;
+  const long long total = (long long)Lp * Lp * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / cols, c = e % cols;
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    const int cs = (int)(c / Lk), ct = (int)(c % Lk);
+    out[e] = (cs / 2 == ps && ct / 2 == pt) ? scale : 0.0;
+  }
+}
+
+// dense row-major copy of a CSR matrix (input conversion for the exact path)
+__global__ void k_csr_to_dense(int nrows, int ncols, const int32_t* __restrict__ indptr,
+                               const int32_t* __restrict__ indices,
+                               const double* __restrict__ data, double* __restrict__ out) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nrows;
+       r += (long long)gridDim.x * blockDim.x) {
+    double* row = out + r * ncols;
+    for (int c = 0; c < ncols; ++c) row[c] = 0.0;
+    for (int e = indptr[r]; e < indptr[r + 1]; ++e) row[indices[e]] += data[e];
+  }
+}
+
+__global__ void k_eye(int n, double* __restrict__ out) {
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+// ---- FP64 peak probes -------------------------------------------------------
+__global__ void k_dfma_probe(int iters, double* sink) {
+  double a0 = threadIdx.x * 1e-7, a1 = a0 + 1e-7, a2 = a0 + 2e-7, a3 = a0 + 3e-7;
+  double a4 = a0 + 4e-7, a5 = a0 + 5e-7, a6 = a0 + 6e-7, a7 = a0 + 7e-7;
+  const double b = 0.999999, c = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+      a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) sink[0] = s;
+}
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void k_dmma_probe(int iters, double* sink) {
+  double c[8][2] = {};
+  const double a = 1e-3 * (threadIdx.x & 31), b = 0.5;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dmma884(c[u][0], c[u][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += c[u][0] + c[u][1];
+  if (s == 12345.678) sink[0] = s;
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+int gbk_dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta,
+                   const double* B, int ldb, int tb, double beta, double* C, int ldc,
+                   cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  dim3 grid((n + TN - 1) / TN, (m + TM - 1) / TM);
+  k_dgemm<<<grid, 256, 0, s>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
+  return (int)cudaGetLastError();
+}
+
+int gbk_dense_potrf(int n, double* A, int lda, long long* status, cudaStream_t s) {
+  const int nb = 64;
+  for (int j0 = 0; j0 < n; j0 += nb) {
+    const int b = (n - j0) < nb ? (n - j0) : nb;
+    k_potrf_panel<<<1, 256, 0, s>>>(n, j0, b, A, lda, status);
+    const int r0 = j0 + b, m = n - r0;
+    if (m > 0) {
+      // A22 -= L21 L21^T  (full trailing block; upper part is ignored)
+      int e = gbk_dense_gemm(m, m, b, -1.0, A + (long long)r0 * lda + j0, lda, 0,
+                             A + (long long)r0 * lda + j0, lda, 1, 1.0,
+                             A + (long long)r0 * lda + r0, lda, s);
+      if (e) return e;
+    }
+  }
+  k_tril<<<148 * 4, 256, 0, s>>>(n, A, lda);
+  return (int)cudaGetLastError();
+}
+
+int gbk_dense_potrs(int n, int nrhs, const double* L, int lda, double* X, int ldx,
+                    cudaStream_t s) {
+  const int nb = 64;
+  const int g = (nrhs + 127) / 128;
+  // forward: L Y = B
+  for (int j0 = 0; j0 < n; j0 += nb) {
+    const int b = (n - j0) < nb ? (n - j0) : nb;
+    k_trsv_block<<<g, 128, 0, s>>>(j0, b, nrhs, L, lda, X, ldx, 1);
+    const int r0 = j0 + b, m = n - r0;
+    if (m > 0) {
+      int e = gbk_dense_gemm(m, nrhs, b, -1.0, L + (long long)r0 * lda + j0, lda, 0,
+                             X + (long long)j0 * ldx, ldx, 0, 1.0,
+                             X + (long long)r0 * ldx, ldx, s);
+      if (e) return e;
+    }
+  }
+  // backward: L^T Z = Y
+  const int nblk = (n + nb - 1) / nb;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int j0 = bi * nb;
+    const int b = (n - j0) < nb ? (n - j0) : nb;
+    k_trsv_block<<<g, 128, 0, s>>>(j0, b, nrhs, L, lda, X, ldx, 0);
+    if (j0 > 0) {
+      // X[0:j0] -= L[j0:j0+b, 0:j0]^T X[j0:j0+b]
+      int e = gbk_dense_gemm(j0, nrhs, b, -1.0, L + (long long)j0 * lda, lda, 1,
+                             X + (long long)j0 * ldx, ldx, 0, 1.0, X, ldx, s);
+      if (e) return e;
+    }
+  }
+  return (int)cudaGetLastError();
+}
+
+int gbk_dense_sym(int n, const double* X, int ldx, double* out, double* stats,
+                  cudaStream_t s) {
+  k_dense_sym<<<148 * 4, 256, 0, s>>>(n, X, ldx, out, stats);
+  return (int)cudaGetLastError();
+}
+
+int gbk_dense_build_w(int Lk, const double* w12, double* out, cudaStream_t s) {
+  WTemplate W;
+  for (int c = 0; c < 3; ++c)
+    for (int a = 0; a < 4; ++a) W.w[c][a] = w12[c * 4 + a];
+  k_dense_build_w<<<148 * 4, 256, 0, s>>>(Lk, W, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_dense_build_p(int Lk, double scale, double* out, cudaStream_t s) {
+  k_dense_build_p<<<148 * 4, 256, 0, s>>>(Lk, scale, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_csr_to_dense(int nrows, int ncols, const int32_t* indptr, const int32_t* indices,
+                     const double* data, double* out, cudaStream_t s) {
+  k_csr_to_dense<<<(nrows + 127) / 128, 128, 0, s>>>(nrows, ncols, indptr, indices, data, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_eye(int n, double* out, cudaStream_t s) {
+  k_eye<<<148 * 4, 256, 0, s>>>(n, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_fp64_peak_probe(int kind, int iters, double* sink, cudaStream_t s) {
+  if (kind == 0) k_dfma_probe<<<148 * 8, 256, 0, s>>>(iters, sink);
+  else k_dmma_probe<<<148 * 8, 256, 0, s>>>(iters, sink);
+  return (int)cudaGetLastError();
+}

@@ -1,0 +1,98 @@
+// Internal launcher prototypes (C++ linkage); the public C ABI wraps these in
+// gb_capi.cu and is declared in include/gamblets_b200.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+enum { EXP_SQUARE = 0, EXP_CHILD = 1, EXP_PSI = 2, EXP_TDT = 3 };
+
+// gb_box.cu
+int gbk_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices, int* out,
+                      cudaStream_t s);
+int gbk_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
+                   const double* data, double* box, long long* status, cudaStream_t s);
+int gbk_box_scale(long long rows, int nr, int w, const double* box, double* sv,
+                  long long* status, cudaStream_t s);
+int gbk_box_diag_min(long long rows, int nr, int w, const double* box, double* dmin,
+                     cudaStream_t s);
+int gbk_box_sym_drop(int L, int nr, int w, const double* raw, double* out,
+                     const double* dmin, double* stats, cudaStream_t s);
+int gbk_row_tail_drop(long long rows, long long S, double* v, cudaStream_t s);
+int gbk_export_count(int kind, int L, int nr, int w, int nc, int n, int lo, int wd,
+                     const double* val, long long rows, long long S, long long* counts,
+                     cudaStream_t s);
+int gbk_exclusive_scan(const long long* counts, long long* indptr, long long n, void* tmp,
+                       size_t* tmp_bytes, cudaStream_t s);
+int gbk_export_emit(int kind, int L, int nr, int w, int nc, int n, int lo, int wd,
+                    const double* val, long long rows, long long S,
+                    const long long* indptr, int32_t* indices, double* data,
+                    cudaStream_t s);
+
+// gb_patch.cu
+size_t gbk_mass_patch_workspace(int rho, int blocks);
+int gbk_mass_patches(int n, int wM, const double* M, const double* s, int rho, int wd,
+                     double* psi, long long* status, double* gws, int blocks,
+                     cudaStream_t st);
+size_t gbk_correction_workspace(int rho, int blocks);
+int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB, int wG,
+                           const double* G, int rho, double* Dt, long long* status,
+                           double* gws, int blocks, cudaStream_t st);
+
+// gb_products.cu
+int gbk_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
+                    const double* A, int wX, double* X, cudaStream_t s);
+int gbk_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
+                     const double* X, int wR, double* raw, cudaStream_t s);
+int gbk_level_diag(int Lk, int wA, const double* A, const double* w12, double* bdiag,
+                   double* dmin, cudaStream_t s);
+int gbk_level_blocks(int Lk, int wA, const double* A, const double* w12, int wB,
+                     const double* bdiag, const double* dmin, double* B, double* G,
+                     double* PAPt, double* stats, cudaStream_t s);
+int gbk_restriction(int Lp, int rho, const double* Dt, const double* w12, double* R,
+                    cudaStream_t s);
+int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
+           double* BD, cudaStream_t s);
+int gbk_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
+            double* GtD, cudaStream_t s);
+int gbk_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
+                   int rho, const double* Dt, int wBD, const double* BD, int wA2,
+                   double* raw, cudaStream_t s);
+int gbk_wpsi(int n, int Lk, int lo, int wd, const double* w12, const double* psi,
+             int wdw, double* Wpsi, cudaStream_t s);
+int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                 double* psi_next, cudaStream_t s);
+
+// gb_krylov.cu
+size_t gbk_kstate_bytes();
+int gbk_red_blocks();
+int gbk_state_reset(void* st, int max_iter, cudaStream_t s);
+int gbk_cg_init(long long n, const double* b, const double* x0, const double* Ax0,
+                double* x, double* r, double* p, double rel_tol, int max_iter, void* st,
+                double* part, cudaStream_t s);
+int gbk_cg_iterations(int L, int nr, int w, const double* B, const double* sv, int mode,
+                      double* x, double* r, double* p, double* Ap, int iters, void* st,
+                      double* part, cudaStream_t s);
+int gbk_pow_iterations(int L, int nr, int w, const double* B, const double* sv, int mode,
+                       double* x, double* y, double tol, int iters, void* st,
+                       double* part, cudaStream_t s);
+int gbk_dot2(long long n, const double* a, const double* b, const double* c, double* out,
+             void* st, double* part, cudaStream_t s);
+int gbk_scale_by_norm(long long n, const double* a, const double* norm2, int which,
+                      double* y, double* y2, cudaStream_t s);
+int gbk_box_apply(int L, int nr, int w, const double* B, const double* sv, int mode,
+                  const double* x, double* y, cudaStream_t s);
+int gbk_apply_w(int Lp, const double* w12, const double* g, const double* sv, double* out,
+                cudaStream_t s);
+int gbk_apply_wt(int Lp, const double* w12, const double* w, double* v, cudaStream_t s);
+int gbk_apply_r(int Lp, int rho, const double* R, const double* g, double* out,
+                cudaStream_t s);
+int gbk_psi_t_apply(int n, int L, int lo, int wd, const double* psi, const double* v,
+                    double* inc, cudaStream_t s);
+int gbk_axpby(long long n, double a, const double* x, double b, const double* y,
+              double* out, cudaStream_t s);
+int gbk_vmul(long long n, const double* a, const double* b, double* out, cudaStream_t s);
+int gbk_vadd(long long n, const double* a, const double* b, double* out, cudaStream_t s);
+int gbk_psi_apply(int n, int L, int lo, int wd, const double* psi, const double* b,
+                  double* out, cudaStream_t s);

@@ -1,0 +1,676 @@
+// Solve-phase kernels: subband / coarse CG (K8), the spectral-estimate
+// building blocks (K7) and the load-dependent transfers (K9).
+//
+// CG follows sparse_core.py:126-165 step for step (zero start or warm start,
+// stop when ||r|| <= tol ||b||, breakdown on p^T A p <= 0, max_iter reported
+// not fatal).  The iteration state lives in device memory; the kernels read it
+// at entry and return immediately once `done` is set, so the host can enqueue
+// chunks of iterations without a round trip per step.  Reductions are two
+// level with a fixed order (per-block partials summed by the last block), so
+// every run is bitwise reproducible.
+#include "gb_common.cuh"
+#include "gb_kernels.h"
+
+namespace gb {
+
+struct KState {
+  double rs, pAp, alpha, beta, bnorm, tol_abs, rnorm, lam;
+  double ynorm, res, aux0, aux1;
+  int it, done, converged, max_iter, breakdown, pad0, pad1, pad2;
+  unsigned int counter, pad3;
+};
+
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  return am_last;
+}
+
+// deterministic sum of gridDim.x partials (pairs) by the last block
+__device__ __forceinline__ void final_sum2(const double* part, int nb, double* o0,
+                                          double* o1, double* sh) {
+  double a = 0.0, b = 0.0;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+    a += part[2 * j];
+    b += part[2 * j + 1];
+  }
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  *o0 = a;
+  *o1 = b;
+}
+
+// y_r = Op(x)_r for a square box (nr = nc), one warp per row.
+// mode 0: sum ((B s_r) s_c) x_c        (materialized congruence S B S)
+// mode 1: s_r * sum B (s_c x_c)        (_RescaledOperator, gamblet_fast.py:142-151)
+__device__ __forceinline__ double box_row_apply(int L, int nr, int w,
+                                                const double* __restrict__ B,
+                                                const double* __restrict__ s, int mode,
+                                                const double* __restrict__ x,
+                                                long long r, int lane) {
+  const int W2 = 2 * w + 1;
+  const int S = W2 * W2 * nr;
+  const long long p = r / nr;
+  const int ps = (int)(p / L), pt = (int)(p % L);
+  const int s0 = imax(ps - w, 0) - ps, s1 = imin(ps + w, L - 1) - ps;
+  const int t0 = imax(pt - w, 0) - pt, t1 = imin(pt + w, L - 1) - pt;
+  const int nt = (t1 - t0 + 1) * nr;
+  const int cnt = (s1 - s0 + 1) * nt;
+  const double* row = B + r * S;
+  const double sr = s[r];
+  double acc = 0.0;
+  for (int j = lane; j < cnt; j += 32) {
+    const int a = j / nt, rem = j - a * nt;
+    const int ds = s0 + a;
+    const int dt = t0 + rem / nr, c = rem % nr;
+    const double bv = row[((ds + w) * W2 + (dt + w)) * nr + c];
+    const long long col = ((long long)(ps + ds) * L + (pt + dt)) * nr + c;
+    if (mode == 0) acc += (bv * sr) * s[col] * x[col];
+    else acc += bv * (s[col] * x[col]);
+  }
+  acc = warp_sum(acc);
+  return mode == 0 ? acc : sr * acc;
+}
+
+// Ap = Op(p); partial (p.Ap, 0); last block: pAp, alpha, breakdown
+__global__ void k_cg_spmv(int L, int nr, int w, const double* __restrict__ B,
+                          const double* __restrict__ s, int mode,
+                          const double* __restrict__ p, double* __restrict__ Ap,
+                          KState* st, double* part) {
+  __shared__ double sh[32];
+  if (st->done) return;
+  const long long rows = (long long)L * L * nr;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  double dot = 0.0;
+  for (long long r = wid; r < rows; r += nwarps) {
+    const double y = box_row_apply(L, nr, w, B, s, mode, p, r, lane);
+    if (lane == 0) {
+      Ap[r] = y;
+      dot += p[r] * y;
+    }
+  }
+  dot = block_sum(dot, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = dot;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->pAp = a;
+      if (!(a > 0.0)) {
+        st->breakdown = st->it + 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rs / a;
+      }
+    }
+  }
+}
+
+// x += alpha p; r -= alpha Ap; rs_new; convergence; beta
+__global__ void k_cg_update(long long n, double* __restrict__ x, double* __restrict__ r,
+                            const double* __restrict__ p, const double* __restrict__ Ap,
+                            KState* st, double* part) {
+  __shared__ double sh[32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  double rr = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * Ap[i];
+    r[i] = ri;
+    rr += ri * ri;
+  }
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = rr;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->it += 1;
+      const double rn = sqrt(a);
+      st->rnorm = rn;
+      if (rn <= st->tol_abs) {
+        st->done = 1;
+        st->converged = 1;
+      } else if (st->it >= st->max_iter) {
+        st->done = 1;
+        st->converged = 0;
+      } else {
+        st->beta = a / st->rs;
+        st->rs = a;
+      }
+    }
+  }
+}
+
+__global__ void k_cg_dir(long long n, const double* __restrict__ r, double* __restrict__ p,
+                         const KState* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = r[i] + beta * p[i];
+}
+
+// init: r = b - Ax0 (Ax0 may be null => x0 = 0), x = x0 or 0, p = r;
+// bnorm, rnorm, early exits of sparse_core.py:138-148
+__global__ void k_cg_init(long long n, const double* __restrict__ b,
+                          const double* __restrict__ x0, const double* __restrict__ Ax0,
+                          double* __restrict__ x, double* __restrict__ r,
+                          double* __restrict__ p, double rel_tol, int max_iter,
+                          KState* st, double* part) {
+  __shared__ double sh[32];
+  double bb = 0.0, rr = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double bi = b[i];
+    const double ri = Ax0 ? bi - Ax0[i] : bi;
+    x[i] = x0 ? x0[i] : 0.0;
+    r[i] = ri;
+    p[i] = ri;
+    bb += bi * bi;
+    rr += ri * ri;
+  }
+  bb = block_sum(bb, sh);
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = bb;
+    part[2 * blockIdx.x + 1] = rr;
+  }
+  if (last_block(&st->counter)) {
+    double a, c;
+    final_sum2(part, gridDim.x, &a, &c, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->it = 0;
+      st->breakdown = 0;
+      st->max_iter = max_iter;
+      const double bn = sqrt(a);
+      st->bnorm = bn;
+      st->tol_abs = rel_tol * bn;
+      const double rn = sqrt(c);
+      st->rnorm = rn;
+      st->rs = rn * rn;
+      st->done = 0;
+      st->converged = 0;
+      if (bn == 0.0) {
+        st->done = 1;
+        st->converged = 1;
+        st->rnorm = 0.0;
+        st->aux0 = 1.0;  // x must be zeroed (zero rhs)
+      } else if (rn <= rel_tol * bn) {
+        st->done = 1;
+        st->converged = 1;
+        st->aux0 = 0.0;
+      } else {
+        st->aux0 = 0.0;
+      }
+    }
+  }
+}
+
+// zero rhs => x = 0 (sparse_core.py:140-141)
+__global__ void k_cg_zero_if(long long n, double* __restrict__ x, const KState* st) {
+  if (st->aux0 == 0.0) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// spectral building blocks (sparse_core.py:232-278)
+// ---------------------------------------------------------------------------
+// y = Op(x); (x.y, y.y) -> st->lam, st->ynorm
+__global__ void k_pow_apply(int L, int nr, int w, const double* __restrict__ B,
+                            const double* __restrict__ s, int mode,
+                            const double* __restrict__ x, double* __restrict__ y,
+                            KState* st, double* part) {
+  __shared__ double sh[32];
+  if (st->done) return;
+  const long long rows = (long long)L * L * nr;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  double xy = 0.0, yy = 0.0;
+  for (long long r = wid; r < rows; r += nwarps) {
+    const double v = box_row_apply(L, nr, w, B, s, mode, x, r, lane);
+    if (lane == 0) {
+      y[r] = v;
+      xy += x[r] * v;
+      yy += v * v;
+    }
+  }
+  xy = block_sum(xy, sh);
+  yy = block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = xy;
+    part[2 * blockIdx.x + 1] = yy;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->lam = a;
+      st->ynorm = sqrt(b);
+      if (st->ynorm == 0.0) {
+        st->lam = 0.0;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+// res = ||y - lam x||; x = y / ynorm; stop test res <= 0.5 tol |lam|
+__global__ void k_pow_step(long long n, double* __restrict__ x, const double* __restrict__ y,
+                           double tol, KState* st, double* part) {
+  __shared__ double sh[32];
+  if (st->done) return;
+  const double lam = st->lam, yn = st->ynorm;
+  double rr = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double d = y[i] - lam * x[i];
+    rr += d * d;
+  }
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = rr;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  // every block must finish reading x before anyone rescales it: the rescale
+  // happens in k_pow_scale after this kernel completes
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->res = sqrt(a);
+      st->it += 1;
+      st->aux1 = (st->res <= 0.5 * tol * fabs(lam) || st->it >= st->max_iter) ? 1.0 : 0.0;
+    }
+  }
+}
+
+__global__ void k_pow_scale(long long n, double* __restrict__ x, const double* __restrict__ y,
+                            KState* st) {
+  if (st->done) return;
+  const double yn = st->ynorm;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = y[i] / yn;
+  // the stop flag is committed by the last thread to leave (any thread may
+  // set it: the kernel boundary orders it before the next launch)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->aux1 != 0.0) st->done = 1;
+}
+
+// generic dot products: out[0] = a.b, out[1] = c.c  (c may be null)
+__global__ void k_dot2(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                       const double* __restrict__ c, double* out, KState* st,
+                       double* part) {
+  __shared__ double sh[32];
+  double s0 = 0.0, s1 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    s0 += a[i] * b[i];
+    if (c) s1 += c[i] * c[i];
+  }
+  s0 = block_sum(s0, sh);
+  s1 = block_sum(s1, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s0;
+    part[2 * blockIdx.x + 1] = s1;
+  }
+  if (last_block(&st->counter)) {
+    double x0, x1;
+    final_sum2(part, gridDim.x, &x0, &x1, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      out[0] = x0;
+      out[1] = x1;
+    }
+  }
+}
+
+// y = a / sqrt(norm2[0]) ; also copies into y2 when given
+__global__ void k_scale_by_norm(long long n, const double* __restrict__ a,
+                                const double* __restrict__ norm2, int which,
+                                double* __restrict__ y, double* __restrict__ y2) {
+  const double nv = sqrt(norm2[which]);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = a[i] / nv;
+    y[i] = v;
+    if (y2) y2[i] = v;
+  }
+}
+
+// plain y = Op(x)
+__global__ void k_box_apply(int L, int nr, int w, const double* __restrict__ B,
+                            const double* __restrict__ s, int mode,
+                            const double* __restrict__ x, double* __restrict__ y) {
+  const long long rows = (long long)L * L * nr;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nwarps) {
+    const double v = box_row_apply(L, nr, w, B, s, mode, x, r, lane);
+    if (lane == 0) y[r] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K9 transfers
+// ---------------------------------------------------------------------------
+// out[(p,c)] = s[(p,c)] * sum_a W[c][a] g[child_a(p)]   (s may be null)
+__global__ void k_apply_w(int Lp, WTemplate W, const double* __restrict__ g,
+                          const double* __restrict__ s, double* __restrict__ out) {
+  const long long P = (long long)Lp * Lp;
+  const int Lk = 2 * Lp;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    double gv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      gv[a] = g[(long long)(2 * ps + (a >> 1)) * Lk + 2 * pt + (a & 1)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (W.w[c][a] != 0.0) acc += W.w[c][a] * gv[a];
+      out[p * 3 + c] = s ? s[p * 3 + c] * acc : acc;
+    }
+  }
+}
+
+// v[child_a(p)] = sum_c W[c][a] w[(p,c)]   (W^T w, csc scatter order)
+__global__ void k_apply_wt(int Lp, WTemplate W, const double* __restrict__ w,
+                           double* __restrict__ v) {
+  const long long P = (long long)Lp * Lp;
+  const int Lk = 2 * Lp;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    const double w0 = w[p * 3], w1 = w[p * 3 + 1], w2 = w[p * 3 + 2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double acc = 0.0;
+      if (W.w[0][a] != 0.0) acc += W.w[0][a] * w0;
+      if (W.w[1][a] != 0.0) acc += W.w[1][a] * w1;
+      if (W.w[2][a] != 0.0) acc += W.w[2][a] * w2;
+      v[(long long)(2 * ps + (a >> 1)) * Lk + 2 * pt + (a & 1)] = acc;
+    }
+  }
+}
+
+// g'[i] = sum over R row i in ascending column order (ds, alpha, dt, beta)
+__global__ void k_apply_r(int Lp, int rho, const double* __restrict__ R,
+                          const double* __restrict__ g, double* __restrict__ out) {
+  const long long P = (long long)Lp * Lp;
+  const int W2 = 2 * rho + 1, Lk = 2 * Lp;
+  const int S = W2 * W2 * 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int is = (int)(i / Lp), it = (int)(i % Lp);
+    const double* row = R + i * S;
+    double acc = 0.0;
+    for (int dsi = 0; dsi < W2; ++dsi) {
+      const int qs = is + dsi - rho;
+      if (qs < 0 || qs >= Lp) continue;
+      for (int alpha = 0; alpha < 2; ++alpha) {
+        for (int dti = 0; dti < W2; ++dti) {
+          const int qt = it + dti - rho;
+          if (qt < 0 || qt >= Lp) continue;
+          for (int beta = 0; beta < 2; ++beta) {
+            const double rv = row[(dsi * W2 + dti) * 4 + 2 * alpha + beta];
+            if (rv != 0.0)
+              acc += rv * g[(long long)(2 * qs + alpha) * Lk + 2 * qt + beta];
+          }
+        }
+      }
+    }
+    out[i] = acc;
+  }
+}
+
+// inc[f] = sum_{j asc} psi[j][f] v[j]   (psi^T v, csc scatter order)
+__global__ void k_psi_t_apply(int n, int L, int lo, int wd, const double* __restrict__ psi,
+                              const double* __restrict__ v, double* __restrict__ inc) {
+  const long long N = (long long)n * n;
+  const int h = n / L;
+  const int hi = lo + wd - 1;  // only meaningful when the window is unclipped
+  const long long per = (long long)wd * wd;
+  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < N;
+       f += (long long)gridDim.x * blockDim.x) {
+    const int fs = (int)(f / n), ft = (int)(f % n);
+    // rows j whose window covers f; windows are monotone in j, use a safe range
+    int j0s, j1s, j0t, j1t;
+    if (wd >= n) {
+      j0s = 0; j1s = L - 1; j0t = 0; j1t = L - 1;
+    } else {
+      j0s = imax(0, (fs - hi) / h - 1); j1s = imin(L - 1, (fs - lo) / h + 1);
+      j0t = imax(0, (ft - hi) / h - 1); j1t = imin(L - 1, (ft - lo) / h + 1);
+    }
+    double acc = 0.0;
+    for (int js = j0s; js <= j1s; ++js) {
+      const int ls = fs - clampi(js * h + lo, 0, n - wd);
+      if (ls < 0 || ls >= wd) continue;
+      for (int jt = j0t; jt <= j1t; ++jt) {
+        const int lt = ft - clampi(jt * h + lo, 0, n - wd);
+        if (lt < 0 || lt >= wd) continue;
+        const long long j = (long long)js * L + jt;
+        const double pv = psi[j * per + ls * wd + lt];
+        if (pv != 0.0) acc += pv * v[j];
+      }
+    }
+    inc[f] = acc;
+  }
+}
+
+// out[i] = sum over row i's window (ascending) psi[i][f] b[f]   (psi @ b)
+__global__ void k_psi_apply(int n, int L, int lo, int wd, const double* __restrict__ psi,
+                            const double* __restrict__ b, double* __restrict__ out) {
+  const long long rows = (long long)L * L;
+  const int h = n / L;
+  const long long per = (long long)wd * wd;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = wid; i < rows; i += nwarps) {
+    const int os = clampi((int)(i / L) * h + lo, 0, n - wd);
+    const int ot = clampi((int)(i % L) * h + lo, 0, n - wd);
+    const double* row = psi + i * per;
+    double acc = 0.0;
+    for (long long e = lane; e < per; e += 32) {
+      const double v = row[e];
+      if (v != 0.0) acc += v * b[(long long)(os + e / wd) * n + ot + e % wd];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+__global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = (y ? a * x[i] + b * y[i] : a * x[i]);
+}
+
+__global__ void k_vmul(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                       double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+
+__global__ void k_vadd(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                       double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+static const int kRedBlocks = 592;  // 4 per SM on 148 SMs; partials sized by the caller
+
+static inline int grid_for(long long work, int block, int cap) {
+  long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+static inline WTemplate mkW(const double* w12) {
+  WTemplate W;
+  for (int c = 0; c < 3; ++c)
+    for (int a = 0; a < 4; ++a) W.w[c][a] = w12[c * 4 + a];
+  return W;
+}
+
+size_t gbk_kstate_bytes() { return sizeof(KState); }
+int gbk_red_blocks() { return kRedBlocks; }
+
+namespace gb {
+__global__ void k_state_reset(KState* st, int max_iter) {
+  KState z = {};
+  z.max_iter = max_iter;
+  *st = z;
+}
+}  // namespace gb
+
+int gbk_state_reset(void* st, int max_iter, cudaStream_t s) {
+  k_state_reset<<<1, 1, 0, s>>>((KState*)st, max_iter);
+  return (int)cudaGetLastError();
+}
+
+int gbk_cg_init(long long n, const double* b, const double* x0, const double* Ax0,
+                double* x, double* r, double* p, double rel_tol, int max_iter,
+                void* st, double* part, cudaStream_t s) {
+  const int g = grid_for(n, 256, kRedBlocks);
+  k_cg_init<<<g, 256, 0, s>>>(n, b, x0, Ax0, x, r, p, rel_tol, max_iter, (KState*)st,
+                              part);
+  k_cg_zero_if<<<grid_for(n, 256, kRedBlocks), 256, 0, s>>>(n, x, (KState*)st);
+  return (int)cudaGetLastError();
+}
+
+int gbk_cg_iterations(int L, int nr, int w, const double* B, const double* sv,
+                      int mode, double* x, double* r, double* p, double* Ap,
+                      int iters, void* st, double* part, cudaStream_t s) {
+  const long long n = (long long)L * L * nr;
+  const int gs = grid_for(n * 32, 256, kRedBlocks);
+  const int gv = grid_for(n, 256, kRedBlocks);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    k_cg_spmv<<<gs, 256, 0, s>>>(L, nr, w, B, sv, mode, p, Ap, k, part);
+    k_cg_update<<<gv, 256, 0, s>>>(n, x, r, p, Ap, k, part);
+    k_cg_dir<<<gv, 256, 0, s>>>(n, r, p, k);
+  }
+  return (int)cudaGetLastError();
+}
+
+int gbk_pow_iterations(int L, int nr, int w, const double* B, const double* sv,
+                       int mode, double* x, double* y, double tol, int iters,
+                       void* st, double* part, cudaStream_t s) {
+  const long long n = (long long)L * L * nr;
+  const int gs = grid_for(n * 32, 256, kRedBlocks);
+  const int gv = grid_for(n, 256, kRedBlocks);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    k_pow_apply<<<gs, 256, 0, s>>>(L, nr, w, B, sv, mode, x, y, k, part);
+    k_pow_step<<<gv, 256, 0, s>>>(n, x, y, tol, k, part);
+    k_pow_scale<<<gv, 256, 0, s>>>(n, x, y, k);
+  }
+  return (int)cudaGetLastError();
+}
+
+int gbk_dot2(long long n, const double* a, const double* b, const double* c,
+             double* out, void* st, double* part, cudaStream_t s) {
+  k_dot2<<<grid_for(n, 256, kRedBlocks), 256, 0, s>>>(n, a, b, c, out, (KState*)st, part);
+  return (int)cudaGetLastError();
+}
+
+int gbk_scale_by_norm(long long n, const double* a, const double* norm2, int which,
+                      double* y, double* y2, cudaStream_t s) {
+  k_scale_by_norm<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, a, norm2, which, y, y2);
+  return (int)cudaGetLastError();
+}
+
+int gbk_box_apply(int L, int nr, int w, const double* B, const double* sv, int mode,
+                  const double* x, double* y, cudaStream_t s) {
+  const long long n = (long long)L * L * nr;
+  k_box_apply<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(L, nr, w, B, sv, mode, x, y);
+  return (int)cudaGetLastError();
+}
+
+int gbk_apply_w(int Lp, const double* w12, const double* g, const double* sv, double* out,
+                cudaStream_t s) {
+  const long long P = (long long)Lp * Lp;
+  k_apply_w<<<grid_for(P, 256, 148 * 16), 256, 0, s>>>(Lp, mkW(w12), g, sv, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_apply_wt(int Lp, const double* w12, const double* w, double* v, cudaStream_t s) {
+  const long long P = (long long)Lp * Lp;
+  k_apply_wt<<<grid_for(P, 256, 148 * 16), 256, 0, s>>>(Lp, mkW(w12), w, v);
+  return (int)cudaGetLastError();
+}
+
+int gbk_apply_r(int Lp, int rho, const double* R, const double* g, double* out,
+                cudaStream_t s) {
+  const long long P = (long long)Lp * Lp;
+  k_apply_r<<<grid_for(P, 128, 148 * 16), 128, 0, s>>>(Lp, rho, R, g, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_psi_t_apply(int n, int L, int lo, int wd, const double* psi, const double* v,
+                    double* inc, cudaStream_t s) {
+  const long long N = (long long)n * n;
+  k_psi_t_apply<<<grid_for(N, 128, 148 * 32), 128, 0, s>>>(n, L, lo, wd, psi, v, inc);
+  return (int)cudaGetLastError();
+}
+
+int gbk_psi_apply(int n, int L, int lo, int wd, const double* psi, const double* b,
+                  double* out, cudaStream_t s) {
+  const long long rows = (long long)L * L;
+  k_psi_apply<<<grid_for(rows * 32, 256, 148 * 16), 256, 0, s>>>(n, L, lo, wd, psi, b, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_axpby(long long n, double a, const double* x, double b, const double* y,
+              double* out, cudaStream_t s) {
+  k_axpby<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, a, x, b, y, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_vmul(long long n, const double* a, const double* b, double* out, cudaStream_t s) {
+  k_vmul<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, a, b, out);
+  return (int)cudaGetLastError();
+}
+
+int gbk_vadd(long long n, const double* a, const double* b, double* out, cudaStream_t s) {
+  k_vadd<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, a, b, out);
+  return (int)cudaGetLastError();
+}

@@ -1,0 +1,283 @@
+// Batched SPD patch solves (Algorithm 2 lines 2a/3 and 11).
+//
+// K1 mass patches  (gamblet_fast.py:464-498): per fine node i,
+//     (S M S)[i^rho, i^rho] z = s_i e_i,   psi^(q)_i = s[i^rho] * z.
+// K4 correction patches (gamblet_fast.py:546-591): per coarse index i,
+//     (S B S)[chi_i, chi_i] z = s[chi_i] * (-G)[chi_i, i],
+//     D[chi_i, i] = s[chi_i] * z, then the row-tail trim of D^T
+//     (gamblet_fast.py:172-190) fused in.
+//
+// The reference solves every patch by CG to a relative residual that tight
+// mode clamps at 1e-14; these kernels factor each patch exactly (Cholesky in
+// shared memory, one CTA per patch), which matches tight mode to 1e-13
+// (SURVEY.md 8(c)).  Patches that do not fit shared memory use a per-CTA
+// global-memory workspace with the same code.
+#include "gb_common.cuh"
+#include "gb_kernels.h"
+
+namespace gb {
+
+// Right-looking Cholesky of the n x n row-major matrix `a` (lower triangle
+// used) by the whole CTA.  `colj` is an n-vector scratch.  Returns false (CTA
+// uniform) when a pivot is not positive.
+__device__ bool cta_cholesky(double* a, int ld, int n, double* colj) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int j = 0; j < n; ++j) {
+    const double d = a[(long long)j * ld + j];
+    if (!(d > 0.0)) return false;
+    const double l = sqrt(d);
+    for (int i = j + 1 + tid; i < n; i += nt) {
+      const double v = a[(long long)i * ld + j] / l;
+      a[(long long)i * ld + j] = v;
+      colj[i] = v;
+    }
+    __syncthreads();
+    if (tid == 0) a[(long long)j * ld + j] = l;
+    for (int i = j + 1 + warp; i < n; i += nw) {
+      const double lij = colj[i];
+      double* ai = a + (long long)i * ld;
+      for (int k = j + 1 + lane; k <= i; k += 32) ai[k] -= lij * colj[k];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// Solves L L^T z = b in place with the factor from cta_cholesky.
+__device__ void cta_chol_solve(const double* a, int ld, int n, double* b) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int j = 0; j < n; ++j) {
+    __syncthreads();
+    const double yj = b[j] / a[(long long)j * ld + j];
+    __syncthreads();
+    if (tid == 0) b[j] = yj;
+    for (int i = j + 1 + tid; i < n; i += nt) b[i] -= a[(long long)i * ld + j] * yj;
+  }
+  for (int j = n - 1; j >= 0; --j) {
+    __syncthreads();
+    const double zj = b[j] / a[(long long)j * ld + j];
+    __syncthreads();
+    if (tid == 0) b[j] = zj;
+    for (int i = tid; i < j; i += nt) b[i] -= a[(long long)j * ld + i] * zj;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// K1: mass patches.  M is a box (w = wM) on the n x n fine grid, s = diag^-1/2.
+// psi window: lo = -rho, width wd (= min(2 rho + 1, n)).
+// ---------------------------------------------------------------------------
+__global__ void k_mass_patches(int n, int wM, const double* __restrict__ M,
+                               const double* __restrict__ s, int rho, int wd,
+                               double* __restrict__ psi, long long* status,
+                               double* __restrict__ gws, int use_gmem) {
+  extern __shared__ double sm[];
+  const int side = 2 * rho + 1;
+  const int nmax = side * side;
+  double* a;
+  if (use_gmem) a = gws + (long long)blockIdx.x * nmax * nmax;
+  else a = sm;
+  double* b = sm + (use_gmem ? 0 : nmax * nmax);
+  double* colj = b + nmax;
+  const int SM = box_slots(wM, 1);
+  const long long N = (long long)n * n;
+  for (long long i = blockIdx.x; i < N; i += gridDim.x) {
+    const int si = (int)(i / n), ti = (int)(i % n);
+    const int s0 = imax(0, si - rho), s1 = imin(n - 1, si + rho);
+    const int t0 = imax(0, ti - rho), t1 = imin(n - 1, ti + rho);
+    const int ns = s1 - s0 + 1, nt = t1 - t0 + 1, m = ns * nt;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int l1 = e / m, l2 = e % m;
+      const int r1s = s0 + l1 / nt, r1t = t0 + l1 % nt;
+      const int r2s = s0 + l2 / nt, r2t = t0 + l2 % nt;
+      const int ds = r2s - r1s, dt = r2t - r1t;
+      double v = 0.0;
+      if (ds >= -wM && ds <= wM && dt >= -wM && dt <= wM) {
+        const long long r1 = (long long)r1s * n + r1t, r2 = (long long)r2s * n + r2t;
+        v = M[r1 * SM + slot_of(wM, 1, ds, dt, 0)] * s[r1] * s[r2];
+      }
+      a[(long long)l1 * m + l2] = v;
+    }
+    const int li = (si - s0) * nt + (ti - t0);
+    for (int l = threadIdx.x; l < m; l += blockDim.x) b[l] = (l == li) ? s[i] : 0.0;
+    __syncthreads();
+    const bool ok = cta_cholesky(a, m, m, colj);
+    if (!ok) {
+      if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
+      __syncthreads();
+      continue;
+    }
+    cta_chol_solve(a, m, m, b);
+    // scatter into the origin-clamped window of row i
+    const int os = clampi(si - rho, 0, n - wd), ot = clampi(ti - rho, 0, n - wd);
+    double* row = psi + i * (long long)wd * wd;
+    for (int e = threadIdx.x; e < wd * wd; e += blockDim.x) {
+      const int fs = os + e / wd, ft = ot + e % wd;
+      double v = 0.0;
+      if (fs >= s0 && fs <= s1 && ft >= t0 && ft <= t1) {
+        const int l = (fs - s0) * nt + (ft - t0);
+        v = s[(long long)fs * n + ft] * b[l];
+      }
+      row[e] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: correction patches on the parent grid (side Lp).  B: box nr=nc=3,
+// half-width wB; G: box nr=3, nc=1, half-width wG; sB = diag(B)^-1/2.
+// Output Dt: box on the parent grid, nr=1, nc=3, half-width rho (row i holds
+// D[:, i] after the row-tail trim).
+// ---------------------------------------------------------------------------
+__global__ void k_correction_patches(int Lp, int wB, const double* __restrict__ B,
+                                     const double* __restrict__ sB,
+                                     int wG, const double* __restrict__ G,
+                                     int rho, double* __restrict__ Dt,
+                                     long long* status, double* __restrict__ gws,
+                                     int use_gmem, int nmax) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  double* a;
+  if (use_gmem) a = gws + (long long)blockIdx.x * nmax * nmax;
+  else a = sm;
+  double* b = sm + (use_gmem ? 0 : (long long)nmax * nmax);
+  double* colj = b + nmax;
+  const int SB = box_slots(wB, 3), SG = box_slots(wG, 1), SD = box_slots(rho, 3);
+  const long long P = (long long)Lp * Lp;
+  for (long long i = blockIdx.x; i < P; i += gridDim.x) {
+    const int si = (int)(i / Lp), ti = (int)(i % Lp);
+    const int s0 = imax(0, si - rho), s1 = imin(Lp - 1, si + rho);
+    const int t0 = imax(0, ti - rho), t1 = imin(Lp - 1, ti + rho);
+    const int nbt = t1 - t0 + 1;
+    const int m = 3 * (s1 - s0 + 1) * nbt;
+    // right-hand side s * (-G[:, i]) and its norm
+    double nrm = 0.0;
+    for (int l = threadIdx.x; l < m; l += blockDim.x) {
+      const int pl = l / 3, c = l % 3;
+      const int ps = s0 + pl / nbt, pt = t0 + pl % nbt;
+      const long long r = ((long long)ps * Lp + pt) * 3 + c;
+      const int ds = si - ps, dt = ti - pt;
+      double g = 0.0;
+      if (ds >= -wG && ds <= wG && dt >= -wG && dt <= wG)
+        g = G[r * SG + slot_of(wG, 1, ds, dt, 0)];
+      const double v = sB[r] * (-g);
+      b[l] = v;
+      nrm += v * v;
+    }
+    nrm = block_sum(nrm, red);
+    double* drow = Dt + i * SD;
+    if (nrm == 0.0) {  // gamblet_fast.py:561-562: empty correction column
+      for (int e = threadIdx.x; e < SD; e += blockDim.x) drow[e] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+      const int l1 = (int)(e / m), l2 = (int)(e % m);
+      const int p1 = l1 / 3, c1 = l1 % 3, p2 = l2 / 3, c2 = l2 % 3;
+      const int p1s = s0 + p1 / nbt, p1t = t0 + p1 % nbt;
+      const int p2s = s0 + p2 / nbt, p2t = t0 + p2 % nbt;
+      const int ds = p2s - p1s, dt = p2t - p1t;
+      double v = 0.0;
+      if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB) {
+        const long long r1 = ((long long)p1s * Lp + p1t) * 3 + c1;
+        const long long r2 = ((long long)p2s * Lp + p2t) * 3 + c2;
+        v = B[r1 * SB + slot_of(wB, 3, ds, dt, c2)] * sB[r1] * sB[r2];
+      }
+      a[(long long)l1 * m + l2] = v;
+    }
+    __syncthreads();
+    const bool ok = cta_cholesky(a, m, m, colj);
+    if (!ok) {
+      if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
+      __syncthreads();
+      continue;
+    }
+    cta_chol_solve(a, m, m, b);
+    // D values s * z and the row-tail trim of this column of D
+    double mx = 0.0;
+    for (int l = threadIdx.x; l < m; l += blockDim.x) {
+      const int pl = l / 3, c = l % 3;
+      const int ps = s0 + pl / nbt, pt = t0 + pl % nbt;
+      const long long r = ((long long)ps * Lp + pt) * 3 + c;
+      const double v = sB[r] * b[l];
+      b[l] = v;
+      mx = fmax(mx, fabs(v));
+    }
+    mx = block_max(mx, red);
+    const double thr = 1e-11 * mx;
+    for (int e = threadIdx.x; e < SD; e += blockDim.x) {
+      const int c = e % 3, bs = e / 3;
+      const int ps = si + bs / (2 * rho + 1) - rho, pt = ti + bs % (2 * rho + 1) - rho;
+      double v = 0.0;
+      if (ps >= s0 && ps <= s1 && pt >= t0 && pt <= t1) {
+        v = b[((ps - s0) * nbt + (pt - t0)) * 3 + c];
+        if (!(fabs(v) >= thr)) v = 0.0;
+      }
+      drow[e] = v;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+static const int kMaxSmem = 227 * 1024;
+
+size_t gbk_mass_patch_workspace(int rho, int blocks) {
+  const int nmax = (2 * rho + 1) * (2 * rho + 1);
+  const size_t smem = ((size_t)nmax * nmax + 2 * nmax) * 8;
+  if (smem <= (size_t)kMaxSmem) return 0;
+  return (size_t)blocks * nmax * nmax * 8;
+}
+
+int gbk_mass_patches(int n, int wM, const double* M, const double* s, int rho,
+                     int wd, double* psi, long long* status, double* gws,
+                     int blocks, cudaStream_t st) {
+  const int nmax = (2 * rho + 1) * (2 * rho + 1);
+  size_t smem = ((size_t)nmax * nmax + 2 * nmax) * 8;
+  int use_gmem = 0;
+  if (smem > (size_t)kMaxSmem) {
+    use_gmem = 1;
+    smem = (size_t)2 * nmax * 8;
+    if (gws == nullptr) return 1;
+  }
+  cudaFuncSetAttribute(k_mass_patches, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const long long N = (long long)n * n;
+  int g = blocks > 0 ? blocks : (int)(N < 148 * 64 ? N : 148 * 64);
+  k_mass_patches<<<g, nmax <= 64 ? 64 : 256, smem, st>>>(n, wM, M, s, rho, wd, psi,
+                                                         status, gws, use_gmem);
+  return (int)cudaGetLastError();
+}
+
+size_t gbk_correction_workspace(int rho, int blocks) {
+  const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
+  const size_t smem = ((size_t)nmax * nmax + 2 * nmax) * 8;
+  if (smem <= (size_t)kMaxSmem) return 0;
+  return (size_t)blocks * nmax * nmax * 8;
+}
+
+int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB,
+                           int wG, const double* G, int rho, double* Dt,
+                           long long* status, double* gws, int blocks,
+                           cudaStream_t st) {
+  const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
+  size_t smem = ((size_t)nmax * nmax + 2 * nmax) * 8;
+  int use_gmem = 0;
+  if (smem > (size_t)kMaxSmem) {
+    use_gmem = 1;
+    smem = (size_t)2 * nmax * 8;
+    if (gws == nullptr) return 1;
+  }
+  cudaFuncSetAttribute(k_correction_patches,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const long long P = (long long)Lp * Lp;
+  int g = blocks > 0 ? blocks : (int)(P < 148 * 8 ? P : 148 * 8);
+  k_correction_patches<<<g, 256, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt, status,
+                                             gws, use_gmem, nmax);
+  return (int)cudaGetLastError();
+}

@@ -1,0 +1,622 @@
+// Structured (box-stencil) sparse products of the localized transform.
+//
+// Every product below reproduces the reference's scipy SpGEMM accumulation
+// order (row of the left factor, its stored columns ascending, sums starting
+// at 0.0), so identical inputs give bitwise identical outputs wherever the
+// reference itself is order-deterministic.
+//
+//   K2  X = psi A, raw = X psi^T              gamblet_fast.py:658-665
+//   K3  B = W A W^T (sym fused), G = W A pibar^T, PAPt = P A P^T
+//                                             gamblet_fast.py:520-544, 597-601
+//   K6  R = pibar + Dt W                      gamblet_fast.py:587-590
+//       BD = B D, GtD = G^T D, DtBD, raw A^(k-1) gamblet_fast.py:602-611
+//       psi^(k-1) = 0.25 P psi + Dt (W psi)   gamblet_fast.py:615-622
+#include "gb_common.cuh"
+#include "gb_kernels.h"
+
+namespace gb {
+
+// psi window helpers --------------------------------------------------------
+struct PsiWin {
+  int n, L, lo, wd;  // fine side, level side, window offset, window width
+  int hi;            // unclipped support bound: row support in [c+lo, c+hi]
+  __device__ __forceinline__ int h() const { return n / L; }
+  __device__ __forceinline__ int origin(int s) const {
+    return clampi(s * (n / L) + lo, 0, n - wd);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K2a: X = psi A (fine grid), X box half-width wX = rho + wA
+// ---------------------------------------------------------------------------
+__global__ void k_psi_stencil(PsiWin pw, int rho, const double* __restrict__ psi,
+                              int wA, const double* __restrict__ A, int wX,
+                              double* __restrict__ X) {
+  const int n = pw.n;
+  const int SX = box_slots(wX, 1), SA = box_slots(wA, 1);
+  const long long total = (long long)n * n * SX;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / SX;
+    const int sl = (int)(e - i * SX);
+    const int si = (int)(i / n), ti = (int)(i % n);
+    const int us = si + sl / (2 * wX + 1) - wX, ut = ti + sl % (2 * wX + 1) - wX;
+    double acc = 0.0;
+    if (us >= 0 && us < n && ut >= 0 && ut < n) {
+      const int os = pw.origin(si), ot = pw.origin(ti);
+      const double* prow = psi + i * (long long)pw.wd * pw.wd;
+      // v over psi row support (true support [i-rho, i+rho] in the window)
+      const int vs0 = imax(imax(os, si - rho), us - wA);
+      const int vs1 = imin(imin(os + pw.wd - 1, si + rho), us + wA);
+      const int vt0 = imax(imax(ot, ti - rho), ut - wA);
+      const int vt1 = imin(imin(ot + pw.wd - 1, ti + rho), ut + wA);
+      for (int vs = vs0; vs <= vs1; ++vs) {
+        for (int vt = vt0; vt <= vt1; ++vt) {
+          const double pv = prow[(vs - os) * pw.wd + (vt - ot)];
+          if (pv == 0.0) continue;
+          const long long v = (long long)vs * n + vt;
+          acc += pv * A[v * SA + slot_of(wA, 1, us - vs, ut - vt, 0)];
+        }
+      }
+    }
+    X[e] = acc;
+  }
+}
+
+// K2b: raw[i][j] = sum_m X[i][m] psi[j][m], box half-width wR = wX + rho
+__global__ void k_psi_galerkin(PsiWin pw, int rho, const double* __restrict__ psi,
+                               int wX, const double* __restrict__ X, int wR,
+                               double* __restrict__ raw) {
+  const int n = pw.n;
+  const int SX = box_slots(wX, 1), SR = box_slots(wR, 1);
+  const long long total = (long long)n * n * SR;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / SR;
+    const int sl = (int)(e - i * SR);
+    const int si = (int)(i / n), ti = (int)(i % n);
+    const int js = si + sl / (2 * wR + 1) - wR, jt = ti + sl % (2 * wR + 1) - wR;
+    double acc = 0.0;
+    if (js >= 0 && js < n && jt >= 0 && jt < n) {
+      const int os = pw.origin(js), ot = pw.origin(jt);
+      const double* prow = psi + ((long long)js * n + jt) * pw.wd * pw.wd;
+      const double* xrow = X + i * SX;
+      const int ms0 = imax(imax(si - wX, 0), imax(os, js - rho));
+      const int ms1 = imin(imin(si + wX, n - 1), imin(os + pw.wd - 1, js + rho));
+      const int mt0 = imax(imax(ti - wX, 0), imax(ot, jt - rho));
+      const int mt1 = imin(imin(ti + wX, n - 1), imin(ot + pw.wd - 1, jt + rho));
+      for (int ms = ms0; ms <= ms1; ++ms) {
+        for (int mt = mt0; mt <= mt1; ++mt) {
+          const double xv = xrow[slot_of(wX, 1, ms - si, mt - ti, 0)];
+          if (xv == 0.0) continue;
+          acc += xv * prow[(ms - os) * pw.wd + (mt - ot)];
+        }
+      }
+    }
+    raw[e] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: level blocks.  A: box on Lk x Lk (wA).  Parent grid Lp = Lk/2.
+// ---------------------------------------------------------------------------
+struct Blk {
+  double T[4][4];
+};
+
+__device__ __forceinline__ void load_T(int Lk, int wA, const double* __restrict__ A,
+                                       int ps, int pt, int qs, int qt, Blk& t) {
+  const int SA = box_slots(wA, 1);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int as = 2 * ps + (a >> 1), at = 2 * pt + (a & 1);
+    const long long ra = (long long)as * Lk + at;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int bs = 2 * qs + (b >> 1), bt = 2 * qt + (b & 1);
+      const int ds = bs - as, dt = bt - at;
+      t.T[a][b] = (ds >= -wA && ds <= wA && dt >= -wA && dt <= wA)
+                      ? A[ra * SA + slot_of(wA, 1, ds, dt, 0)]
+                      : 0.0;
+    }
+  }
+}
+
+// B_ij[c][c'] = sum_b (sum_a W[c][a] T[a][b]) W[c'][b]   (X = W A, then X W^T)
+// B_ji[c'][c] = sum_a (sum_b W[c'][b] T[a][b]) W[c][a]   (same from the other side)
+__device__ __forceinline__ void block_products(const WTemplate& W, const Blk& t,
+                                               double X[3][4], double Bij[3][3],
+                                               double Bji[3][3]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (W.w[c][a] != 0.0) acc += W.w[c][a] * t.T[a][b];
+      X[c][b] = acc;
+    }
+  }
+  double Xp[3][4];  // Xp[c'][a] = sum_b W[c'][b] T[a][b]
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (W.w[c][b] != 0.0) acc += W.w[c][b] * t.T[a][b];
+      Xp[c][a] = acc;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int cp = 0; cp < 3; ++cp) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (W.w[cp][b] != 0.0) acc += X[c][b] * W.w[cp][b];
+      Bij[c][cp] = acc;
+      double acc2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (W.w[c][a] != 0.0) acc2 += Xp[cp][a] * W.w[c][a];
+      Bji[cp][c] = acc2;
+    }
+  }
+}
+
+__global__ void k_level_diag(int Lk, int wA, const double* __restrict__ A,
+                             WTemplate W, double* __restrict__ bdiag,
+                             double* __restrict__ dmin) {
+  const int Lp = Lk / 2;
+  const long long P = (long long)Lp * Lp;
+  double m = __longlong_as_double(0x7ff0000000000000ll);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    Blk t;
+    load_T(Lk, wA, A, ps, pt, ps, pt, t);
+    double X[3][4], Bij[3][3], Bji[3][3];
+    block_products(W, t, X, Bij, Bji);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double d = (Bij[c][c] + Bji[c][c]) * 0.5;
+      bdiag[p * 3 + c] = d;
+      m = fmin(m, d);
+    }
+  }
+  m = warp_min(m);
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(dmin);
+    unsigned long long old = *a, assumed;
+    do {
+      assumed = old;
+      if (__longlong_as_double((long long)assumed) <= m) break;
+      old = atomicCAS(a, assumed, (unsigned long long)__double_as_longlong(m));
+    } while (assumed != old);
+  }
+}
+
+// B (nr=nc=3, wB), G (nr=3, nc=1, wB), PAPt (nr=nc=1, wB).  One thread per
+// (parent, offset).  stats[0..1] = B repair max|Bij-Bji|, max|Bij|.
+__global__ void k_level_blocks(int Lk, int wA, const double* __restrict__ A,
+                               WTemplate W, int wB,
+                               const double* __restrict__ bdiag,
+                               const double* __restrict__ dmin,
+                               double* __restrict__ B, double* __restrict__ G,
+                               double* __restrict__ PAPt,
+                               double* __restrict__ stats) {
+  const int Lp = Lk / 2;
+  const int W2 = 2 * wB + 1, NB = W2 * W2;
+  const long long total = (long long)Lp * Lp * NB;
+  const bool do_drop = *dmin > 0.0;
+  const int SB = NB * 9 / 3;  // slots per B row: NB * 3
+  double mdiff = 0.0, mabs = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / NB;
+    const int bs = (int)(e - p * NB);
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    const int ds = bs / W2 - wB, dt = bs % W2 - wB;
+    const int qs = ps + ds, qt = pt + dt;
+    double* Bout = B + p * 3 * SB;
+    if (qs < 0 || qs >= Lp || qt < 0 || qt >= Lp) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int cp = 0; cp < 3; ++cp) Bout[c * SB + bs * 3 + cp] = 0.0;
+        G[(p * 3 + c) * NB + bs] = 0.0;
+      }
+      PAPt[p * NB + bs] = 0.0;
+      continue;
+    }
+    Blk t;
+    load_T(Lk, wA, A, ps, pt, qs, qt, t);
+    double X[3][4], Bij[3][3], Bji[3][3];
+    block_products(W, t, X, Bij, Bji);
+    const long long q = (long long)qs * Lp + qt;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int cp = 0; cp < 3; ++cp) {
+        const double a = Bij[c][cp], b = Bji[c][cp];
+        mdiff = fmax(mdiff, fabs(a - b));
+        mabs = fmax(mabs, fabs(a));
+        double v = (a + b) * 0.5;
+        const bool diag = (ds == 0 && dt == 0 && c == cp);
+        if (do_drop && !diag) {
+          if (!(fabs(v) >= 1e-12 * sqrt(bdiag[p * 3 + c] * bdiag[q * 3 + cp]))) v = 0.0;
+        }
+        Bout[c * SB + bs * 3 + cp] = v;
+      }
+      // G = X pibar^T: children of q ascending, each X * 0.25
+      double g = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) g += X[c][b] * 0.25;
+      G[(p * 3 + c) * NB + bs] = g;
+    }
+    // PAPt: PA[b] = sum_a T[a][b] (a ascending), then sum_b PA[b]
+    double pap = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double pa = ((t.T[0][b] + t.T[1][b]) + t.T[2][b]) + t.T[3][b];
+      pap += pa;
+    }
+    PAPt[p * NB + bs] = pap;
+  }
+  mdiff = warp_max(mdiff);
+  mabs = warp_max(mabs);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&stats[0], mdiff);
+    atomic_max_nonneg(&stats[1], mabs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: R = 0.25 P + Dt W.  R box on the parent grid, nc = 4 children, w = rho.
+// ---------------------------------------------------------------------------
+__global__ void k_restriction(int Lp, int rho, const double* __restrict__ Dt,
+                              WTemplate W, double* __restrict__ R) {
+  const int W2 = 2 * rho + 1, NB = W2 * W2;
+  const long long total = (long long)Lp * Lp * NB;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / NB;
+    const int bs = (int)(e - i * NB);
+    const int si = (int)(i / Lp), ti = (int)(i % Lp);
+    const int ds = bs / W2 - rho, dt = bs % W2 - rho;
+    const int qs = si + ds, qt = ti + dt;
+    double* out = R + e * 4;
+    if (qs < 0 || qs >= Lp || qt < 0 || qt >= Lp) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[b] = 0.0;
+      continue;
+    }
+    const double* d = Dt + i * (NB * 3) + bs * 3;
+    const double d0 = d[0], d1 = d[1], d2 = d[2];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double acc = 0.0;
+      if (W.w[0][b] != 0.0 && d0 != 0.0) acc += d0 * W.w[0][b];
+      if (W.w[1][b] != 0.0 && d1 != 0.0) acc += d1 * W.w[1][b];
+      if (W.w[2][b] != 0.0 && d2 != 0.0) acc += d2 * W.w[2][b];
+      out[b] = (ds == 0 && dt == 0) ? 0.25 + acc : acc;
+    }
+  }
+}
+
+// BD[(p,c)][j] = sum_{r' asc} B[(p,c)][r'] * Dt[j][(p'-j, c')],  w = wB + rho
+__global__ void k_bd(int Lp, int wB, const double* __restrict__ B, int rho,
+                     const double* __restrict__ Dt, int wBD, double* __restrict__ BD) {
+  const int SB = box_slots(wB, 3), SD = box_slots(rho, 3), SBD = box_slots(wBD, 1);
+  const long long total = (long long)Lp * Lp * 3 * SBD;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / SBD;
+    const int sl = (int)(e - r * SBD);
+    const long long p = r / 3;
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    const int js = ps + sl / (2 * wBD + 1) - wBD, jt = pt + sl % (2 * wBD + 1) - wBD;
+    double acc = 0.0;
+    if (js >= 0 && js < Lp && jt >= 0 && jt < Lp) {
+      const double* brow = B + r * SB;
+      const double* drow = Dt + ((long long)js * Lp + jt) * SD;
+      const int a0 = imax(imax(ps - wB, js - rho), 0), a1 = imin(imin(ps + wB, js + rho), Lp - 1);
+      const int b0 = imax(imax(pt - wB, jt - rho), 0), b1 = imin(imin(pt + wB, jt + rho), Lp - 1);
+      for (int qs = a0; qs <= a1; ++qs) {
+        for (int qt = b0; qt <= b1; ++qt) {
+          const double* bb = brow + slot_of(wB, 3, qs - ps, qt - pt, 0);
+          const double* dd = drow + slot_of(rho, 3, qs - js, qt - jt, 0);
+#pragma unroll
+          for (int cp = 0; cp < 3; ++cp) {
+            const double bv = bb[cp], dv = dd[cp];
+            if (bv != 0.0 && dv != 0.0) acc += bv * dv;
+          }
+        }
+      }
+    }
+    BD[e] = acc;
+  }
+}
+
+// GtD[i][j] = sum_{r asc} G[r][i] * Dt[j][r],  box nr=nc=1, w = wG + rho
+__global__ void k_gtd(int Lp, int wG, const double* __restrict__ G, int rho,
+                      const double* __restrict__ Dt, int wGD, double* __restrict__ GtD) {
+  const int SG = box_slots(wG, 1), SD = box_slots(rho, 3), SO = box_slots(wGD, 1);
+  const long long total = (long long)Lp * Lp * SO;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / SO;
+    const int sl = (int)(e - i * SO);
+    const int is = (int)(i / Lp), it = (int)(i % Lp);
+    const int js = is + sl / (2 * wGD + 1) - wGD, jt = it + sl % (2 * wGD + 1) - wGD;
+    double acc = 0.0;
+    if (js >= 0 && js < Lp && jt >= 0 && jt < Lp) {
+      const double* drow = Dt + ((long long)js * Lp + jt) * SD;
+      const int a0 = imax(imax(is - wG, js - rho), 0), a1 = imin(imin(is + wG, js + rho), Lp - 1);
+      const int b0 = imax(imax(it - wG, jt - rho), 0), b1 = imin(imin(it + wG, jt + rho), Lp - 1);
+      for (int ps = a0; ps <= a1; ++ps) {
+        for (int pt = b0; pt <= b1; ++pt) {
+          const long long p = (long long)ps * Lp + pt;
+          const int gsl = slot_of(wG, 1, is - ps, it - pt, 0);
+          const double* dd = drow + slot_of(rho, 3, ps - js, pt - jt, 0);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double gv = G[(p * 3 + c) * SG + gsl], dv = dd[c];
+            if (gv != 0.0 && dv != 0.0) acc += gv * dv;
+          }
+        }
+      }
+    }
+    GtD[e] = acc;
+  }
+}
+
+// raw A^(k-1)[i][j] = ((0.0625 PAPt + GtD_ij) + GtD_ji) + DtBD_ij,
+// DtBD_ij = sum_{r asc} Dt[i][r] BD[r][j].  Box w = wA2 (>= 2 rho + wB).
+__global__ void k_coarse_raw(int Lp, int wB, const double* __restrict__ PAPt,
+                             int wGD, const double* __restrict__ GtD, int rho,
+                             const double* __restrict__ Dt, int wBD,
+                             const double* __restrict__ BD, int wA2,
+                             double* __restrict__ raw) {
+  const int SP = box_slots(wB, 1), SGD = box_slots(wGD, 1), SD = box_slots(rho, 3),
+            SBD = box_slots(wBD, 1), SO = box_slots(wA2, 1);
+  const long long total = (long long)Lp * Lp * SO;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / SO;
+    const int sl = (int)(e - i * SO);
+    const int is = (int)(i / Lp), it = (int)(i % Lp);
+    const int ds = sl / (2 * wA2 + 1) - wA2, dt = sl % (2 * wA2 + 1) - wA2;
+    const int js = is + ds, jt = it + dt;
+    double v = 0.0;
+    if (js >= 0 && js < Lp && jt >= 0 && jt < Lp) {
+      const long long j = (long long)js * Lp + jt;
+      double pap = 0.0, gij = 0.0, gji = 0.0;
+      if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
+        pap = PAPt[i * SP + slot_of(wB, 1, ds, dt, 0)];
+      if (ds >= -wGD && ds <= wGD && dt >= -wGD && dt <= wGD) {
+        gij = GtD[i * SGD + slot_of(wGD, 1, ds, dt, 0)];
+        gji = GtD[j * SGD + slot_of(wGD, 1, -ds, -dt, 0)];
+      }
+      double acc = 0.0;
+      const double* drow = Dt + i * SD;
+      const int a0 = imax(imax(is - rho, js - wBD), 0), a1 = imin(imin(is + rho, js + wBD), Lp - 1);
+      const int b0 = imax(imax(it - rho, jt - wBD), 0), b1 = imin(imin(it + rho, jt + wBD), Lp - 1);
+      for (int ps = a0; ps <= a1; ++ps) {
+        for (int pt = b0; pt <= b1; ++pt) {
+          const double* dd = drow + slot_of(rho, 3, ps - is, pt - it, 0);
+          const long long p = (long long)ps * Lp + pt;
+          const int bsl = slot_of(wBD, 1, js - ps, jt - pt, 0);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double dv = dd[c];
+            if (dv == 0.0) continue;
+            const double bv = BD[(p * 3 + c) * SBD + bsl];
+            if (bv != 0.0) acc += dv * bv;
+          }
+        }
+      }
+      v = ((0.0625 * pap + gij) + gji) + acc;
+    }
+    raw[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// psi^(k-1) = drop_row(0.25 P psi + Dt (W psi))
+// Wpsi rows (p, c) on the parent grid, window (lo_k, wdw = min(wd_k + h, n))
+// with parent spacing 2h.
+// ---------------------------------------------------------------------------
+__global__ void k_wpsi(PsiWin child, WTemplate W, const double* __restrict__ psi,
+                       PsiWin par, double* __restrict__ Wpsi) {
+  // par.L = child.L / 2, par.lo = child.lo, par.wd = wdw
+  const int Lp = par.L;
+  const long long per = (long long)par.wd * par.wd;
+  const long long total = (long long)Lp * Lp * per;
+  const long long cper = (long long)child.wd * child.wd;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / per;
+    const int f = (int)(e - p * per);
+    const int ps = (int)(p / Lp), pt = (int)(p % Lp);
+    const int fs = par.origin(ps) + f / par.wd, ft = par.origin(pt) + f % par.wd;
+    double cv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int cs = 2 * ps + (a >> 1), ct = 2 * pt + (a & 1);
+      const int os = child.origin(cs), ot = child.origin(ct);
+      const int ls = fs - os, lt = ft - ot;
+      cv[a] = (ls >= 0 && ls < child.wd && lt >= 0 && lt < child.wd)
+                  ? psi[((long long)cs * child.L + ct) * cper + ls * child.wd + lt]
+                  : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (W.w[c][a] != 0.0 && cv[a] != 0.0) acc += W.w[c][a] * cv[a];
+      Wpsi[(p * 3 + c) * per + f] = acc;
+    }
+  }
+}
+
+// raw psi^(k-1) rows; the row-tail drop runs afterwards (k_row_tail_drop)
+__global__ void k_psi_next(PsiWin child, const double* __restrict__ psi,
+                           PsiWin par, const double* __restrict__ Wpsi, int rho,
+                           const double* __restrict__ Dt, PsiWin out,
+                           double* __restrict__ psi_next) {
+  const int Lp = out.L;
+  const long long per = (long long)out.wd * out.wd;
+  const long long total = (long long)Lp * Lp * per;
+  const long long cper = (long long)child.wd * child.wd;
+  const long long wper = (long long)par.wd * par.wd;
+  const int SD = box_slots(rho, 3);
+  const int h = child.h();  // child spacing in fine units; parent spacing 2h
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / per;
+    const int f = (int)(e - i * per);
+    const int is = (int)(i / Lp), it = (int)(i % Lp);
+    const int fs = out.origin(is) + f / out.wd, ft = out.origin(it) + f % out.wd;
+    // P psi: the 4 children of i
+    double pv = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int cs = 2 * is + (a >> 1), ct = 2 * it + (a & 1);
+      const int ls = fs - child.origin(cs), lt = ft - child.origin(ct);
+      if (ls >= 0 && ls < child.wd && lt >= 0 && lt < child.wd)
+        pv += psi[((long long)cs * child.L + ct) * cper + ls * child.wd + lt];
+    }
+    // Dt (W psi): parents p in ball(i, rho) whose Wpsi support covers f.
+    // support of Wpsi row p: fine [2p h + lo, (2p+1) h + hi] with
+    // hi = lo + wd_child - 1 (unclamped), so 2p h in [f - h - hi, f - lo]
+    const int lo = child.lo, hi = child.hi;
+    double acc = 0.0;
+    const double* drow = Dt + i * SD;
+    const int a0 = imax(imax(is - rho, 0), (fs - h - hi + 2 * h - 1) / (2 * h) - 1);
+    const int a1 = imin(imin(is + rho, Lp - 1), (fs - lo) / (2 * h) + 1);
+    const int b0 = imax(imax(it - rho, 0), (ft - h - hi + 2 * h - 1) / (2 * h) - 1);
+    const int b1 = imin(imin(it + rho, Lp - 1), (ft - lo) / (2 * h) + 1);
+    for (int ps = a0; ps <= a1; ++ps) {
+      const int ls = fs - par.origin(ps);
+      if (ls < 0 || ls >= par.wd) continue;
+      for (int pt = b0; pt <= b1; ++pt) {
+        const int lt = ft - par.origin(pt);
+        if (lt < 0 || lt >= par.wd) continue;
+        const double* dd = drow + slot_of(rho, 3, ps - is, pt - it, 0);
+        const long long p = (long long)ps * Lp + pt;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double dv = dd[c];
+          if (dv == 0.0) continue;
+          const double wv = Wpsi[(p * 3 + c) * wper + ls * par.wd + lt];
+          if (wv != 0.0) acc += dv * wv;
+        }
+      }
+    }
+    psi_next[e] = 0.25 * pv + acc;
+  }
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+static inline int grid_for(long long work, int block, int cap = 148 * 32) {
+  long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+static inline WTemplate mkW(const double* w12) {
+  WTemplate W;
+  for (int c = 0; c < 3; ++c)
+    for (int a = 0; a < 4; ++a) W.w[c][a] = w12[c * 4 + a];
+  return W;
+}
+
+int gbk_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
+                    const double* A, int wX, double* X, cudaStream_t s) {
+  PsiWin pw{n, n, lo, wd, -lo};
+  const long long total = (long long)n * n * box_slots(wX, 1);
+  k_psi_stencil<<<grid_for(total, 256), 256, 0, s>>>(pw, rho, psi, wA, A, wX, X);
+  return (int)cudaGetLastError();
+}
+
+int gbk_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
+                     const double* X, int wR, double* raw, cudaStream_t s) {
+  PsiWin pw{n, n, lo, wd, -lo};
+  const long long total = (long long)n * n * box_slots(wR, 1);
+  k_psi_galerkin<<<grid_for(total, 256), 256, 0, s>>>(pw, rho, psi, wX, X, wR, raw);
+  return (int)cudaGetLastError();
+}
+
+int gbk_level_diag(int Lk, int wA, const double* A, const double* w12,
+                   double* bdiag, double* dmin, cudaStream_t s) {
+  const long long P = (long long)(Lk / 2) * (Lk / 2);
+  k_level_diag<<<grid_for(P, 128), 128, 0, s>>>(Lk, wA, A, mkW(w12), bdiag, dmin);
+  return (int)cudaGetLastError();
+}
+
+int gbk_level_blocks(int Lk, int wA, const double* A, const double* w12, int wB,
+                     const double* bdiag, const double* dmin, double* B, double* G,
+                     double* PAPt, double* stats, cudaStream_t s) {
+  const long long total = (long long)(Lk / 2) * (Lk / 2) * box_slots(wB, 1);
+  k_level_blocks<<<grid_for(total, 128), 128, 0, s>>>(Lk, wA, A, mkW(w12), wB, bdiag,
+                                                      dmin, B, G, PAPt, stats);
+  return (int)cudaGetLastError();
+}
+
+int gbk_restriction(int Lp, int rho, const double* Dt, const double* w12, double* R,
+                    cudaStream_t s) {
+  const long long total = (long long)Lp * Lp * box_slots(rho, 1);
+  k_restriction<<<grid_for(total, 256), 256, 0, s>>>(Lp, rho, Dt, mkW(w12), R);
+  return (int)cudaGetLastError();
+}
+
+int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
+           double* BD, cudaStream_t s) {
+  const long long total = (long long)Lp * Lp * 3 * box_slots(wBD, 1);
+  k_bd<<<grid_for(total, 256), 256, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD);
+  return (int)cudaGetLastError();
+}
+
+int gbk_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
+            double* GtD, cudaStream_t s) {
+  const long long total = (long long)Lp * Lp * box_slots(wGD, 1);
+  k_gtd<<<grid_for(total, 256), 256, 0, s>>>(Lp, wG, G, rho, Dt, wGD, GtD);
+  return (int)cudaGetLastError();
+}
+
+int gbk_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
+                   int rho, const double* Dt, int wBD, const double* BD, int wA2,
+                   double* raw, cudaStream_t s) {
+  const long long total = (long long)Lp * Lp * box_slots(wA2, 1);
+  k_coarse_raw<<<grid_for(total, 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt,
+                                                    wBD, BD, wA2, raw);
+  return (int)cudaGetLastError();
+}
+
+int gbk_wpsi(int n, int Lk, int lo, int wd, const double* w12, const double* psi,
+             int wdw, double* Wpsi, cudaStream_t s) {
+  PsiWin child{n, Lk, lo, wd, 0}, par{n, Lk / 2, lo, wdw, 0};
+  const long long total = (long long)(Lk / 2) * (Lk / 2) * wdw * wdw;
+  k_wpsi<<<grid_for(total, 256), 256, 0, s>>>(child, mkW(w12), psi, par, Wpsi);
+  return (int)cudaGetLastError();
+}
+
+int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                 double* psi_next, cudaStream_t s) {
+  PsiWin child{n, Lk, lo, wd, hi}, par{n, Lk / 2, lo, wdw, 0}, out{n, Lk / 2, lo2, wd2, 0};
+  const long long total = (long long)(Lk / 2) * (Lk / 2) * wd2 * wd2;
+  k_psi_next<<<grid_for(total, 256), 256, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out,
+                                                  psi_next);
+  return (int)cudaGetLastError();
+}

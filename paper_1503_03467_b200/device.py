@@ -1,0 +1,203 @@
+"""Device-resident operators in box-stencil layout and their lazy CSR export.
+
+torch owns the memory (caching allocator, streams); every computation is a
+call into libgamblets_b200.so.  A level operator lives on the GPU as a
+`BoxMatrix` or `PsiWindows`; the scipy CSR the reference API exposes is
+produced on first access by the export kernels (count -> scan -> emit) and
+cached on the host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _native as nat
+from .errors import InvalidArgumentError
+
+EXP_SQUARE, EXP_CHILD, EXP_PSI, EXP_TDT = 0, 1, 2, 3
+
+_DEV = None
+
+
+def device():
+    """The CUDA device the package runs on; raises when there is none."""
+    global _DEV
+    if _DEV is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_1503_03467_b200 needs a CUDA device (B200, sm_100a); "
+                "there is no CPU fallback")
+        nat.load()
+        _DEV = torch.device("cuda", torch.cuda.current_device())
+    return _DEV
+
+
+def stream():
+    return torch.cuda.current_stream(device()).cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def empty(n, dtype=torch.float64):
+    return torch.empty(int(n), dtype=dtype, device=device())
+
+
+def zeros(n, dtype=torch.float64):
+    return torch.zeros(int(n), dtype=dtype, device=device())
+
+
+def to_dev(arr, dtype=None):
+    a = np.ascontiguousarray(arr)
+    t = torch.from_numpy(a)
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(device(), non_blocking=False)
+
+
+def box_slots(w, nc):
+    return (2 * w + 1) ** 2 * nc
+
+
+class _Exportable:
+    """Mixin: CSR export through the device kernels, cached."""
+
+    _csr = None
+
+    def _export_args(self):
+        raise NotImplementedError
+
+    def to_csr(self):
+        if self._csr is not None:
+            return self._csr
+        kind, L, nr, w, nc, n, lo, wd, rows, S, shape = self._export_args()
+        s = stream()
+        counts = zeros(rows + 1, torch.int64)
+        nat.call("gb_export_count", kind, L, nr, w, nc, n, lo, wd, ptr(self.vals),
+                 rows, S, ptr(counts), s)
+        indptr = empty(rows + 1, torch.int64)
+        tmp_bytes = nat.ctypes.c_size_t(0)
+        nat.call("gb_exclusive_scan", ptr(counts), ptr(indptr), rows, None,
+                 nat.ctypes.byref(tmp_bytes), s)
+        tmp = empty(max(1, tmp_bytes.value), torch.uint8)
+        nat.call("gb_exclusive_scan", ptr(counts), ptr(indptr), rows, ptr(tmp),
+                 nat.ctypes.byref(tmp_bytes), s)
+        nnz = int(indptr[rows].item())
+        indices = empty(max(nnz, 1), torch.int32)
+        data = empty(max(nnz, 1), torch.float64)
+        nat.call("gb_export_emit", kind, L, nr, w, nc, n, lo, wd, ptr(self.vals), rows,
+                 S, ptr(indptr), ptr(indices), ptr(data), s)
+        ip = indptr.cpu().numpy()
+        if nnz < 2 ** 31 - 1:
+            ip = ip.astype(np.int32)
+        out = sp.csr_array((data[:nnz].cpu().numpy(), indices[:nnz].cpu().numpy(), ip),
+                           shape=shape)
+        out.has_sorted_indices = True
+        self._csr = out
+        return out
+
+
+class BoxMatrix(_Exportable):
+    """Box-stencil operator.
+
+    kind EXP_SQUARE: rows (p, c) on an L x L grid with nr components, columns
+    (p + d, c') with nc components, |d| <= w.  kind EXP_CHILD: rows on L x L,
+    columns are the 4 children of (p + d) on the 2L x 2L grid (R).  kind
+    EXP_TDT: the stored rows are D^T (nr=1, nc=3) and the exported matrix is
+    D = (D^T)^T with shape (3 L^2, L^2).
+    """
+
+    def __init__(self, vals, L, nr, w, nc, kind=EXP_SQUARE):
+        self.vals, self.L, self.nr, self.w, self.nc, self.kind = vals, L, nr, w, nc, kind
+        self._csr = None
+
+    @property
+    def rows(self):
+        return self.L * self.L * self.nr
+
+    @property
+    def slots(self):
+        return box_slots(self.w, self.nc)
+
+    def _export_args(self):
+        L, w = self.L, self.w
+        if self.kind == EXP_SQUARE:
+            shape = (L * L * self.nr, L * L * self.nc)
+            return (EXP_SQUARE, L, self.nr, w, self.nc, 0, 0, 0, self.rows,
+                    self.slots, shape)
+        if self.kind == EXP_CHILD:
+            shape = (L * L, 4 * L * L)
+            return (EXP_CHILD, L, 1, w, 4, 0, 0, 0, self.rows, self.slots, shape)
+        if self.kind == EXP_TDT:
+            shape = (3 * L * L, L * L)
+            return (EXP_TDT, L, 3, w, 3, 0, 0, 0, 3 * L * L, (2 * w + 1) ** 2, shape)
+        raise InvalidArgumentError(f"unknown box kind {self.kind}")
+
+    def diagonal_host(self):
+        S = self.slots
+        c = np.arange(self.rows) % self.nr
+        center = (self.w * (2 * self.w + 1) + self.w) * self.nc + c
+        v = self.vals.view(self.rows, S)
+        idx = torch.as_tensor(center, device=v.device).view(-1, 1)
+        return v.gather(1, idx).view(-1).cpu().numpy()
+
+
+class PsiWindows(_Exportable):
+    """Rows of psi^(k) over the fine grid in origin-clamped square windows.
+
+    Row i of level side L (h = n / L) has support in [c + lo, c + hi] per
+    dimension (c = (s h, t h)); the stored window has width wd = min(hi - lo
+    + 1, n) and origin clamp(c + lo, 0, n - wd).
+    """
+
+    def __init__(self, vals, n, L, lo, hi):
+        self.vals, self.n, self.L, self.lo, self.hi = vals, n, L, lo, hi
+        self.wd = min(hi - lo + 1, n)
+        self._csr = None
+
+    @staticmethod
+    def window(n, lo, hi):
+        return min(hi - lo + 1, n)
+
+    def _export_args(self):
+        rows = self.L * self.L
+        return (EXP_PSI, self.L, 1, 0, 1, self.n, self.lo, self.wd, rows,
+                self.wd * self.wd, (rows, self.n * self.n))
+
+
+def csr_to_box(mat, L):
+    """Canonical CSR on an L x L grid -> BoxMatrix (half-width from the data).
+    Host CSR (scipy) is uploaded; this is the API entry of M and A."""
+    s = stream()
+    indptr = to_dev(mat.indptr.astype(np.int32, copy=False))
+    indices = to_dev(mat.indices.astype(np.int32, copy=False))
+    data = to_dev(mat.data.astype(np.float64, copy=False))
+    wbuf = zeros(1, torch.int32)
+    nat.call("gb_csr_halfwidth", L, ptr(indptr), ptr(indices), ptr(wbuf), s)
+    w = int(wbuf.item())
+    box = zeros(L * L * box_slots(w, 1))
+    status = zeros(2, torch.int64)
+    nat.call("gb_csr_to_box", L, w, ptr(indptr), ptr(indices), ptr(data), ptr(box),
+             ptr(status), s)
+    return BoxMatrix(box, L, 1, w, 1), status
+
+
+def csr_to_psi(mat, n, L):
+    """Host CSR rows of psi^(k) (level side L over the fine n x n grid) into
+    the window layout (used only when a caller hands in its own psi)."""
+    mat = sp.csr_array(mat)
+    h = n // L
+    rows = np.repeat(np.arange(mat.shape[0]), np.diff(mat.indptr))
+    rs, rt = rows // L * h, rows % L * h
+    fs, ft = mat.indices // n, mat.indices % n
+    lo = int(min((fs - rs).min(initial=0), (ft - rt).min(initial=0)))
+    hi = int(max((fs - rs).max(initial=0), (ft - rt).max(initial=0)))
+    wd = PsiWindows.window(n, lo, hi)
+    os_ = np.clip(rs + lo, 0, n - wd)
+    ot_ = np.clip(rt + lo, 0, n - wd)
+    buf = np.zeros((L * L, wd, wd))
+    buf[rows, fs - os_, ft - ot_] = mat.data
+    return PsiWindows(to_dev(buf.ravel()), n, L, lo, hi)

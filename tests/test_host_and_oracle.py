@@ -1,0 +1,155 @@
+"""CPU tests: the oracle pinned against the reference's golden outputs, the
+package's host-side input builders and index maps against the reference
+(bitwise), and the C ABI library's exported symbols (no GPU needed)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1503_03467_b200 as gb
+from oracle import gamblets_oracle as O
+from oracle.make_goldens import digest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+# --- oracle pinned to the reference -----------------------------------------
+
+@pytest.mark.parametrize("name,q,coeff", [
+    ("fast_q4_example1", 4, "example1"),
+    ("fast_q5_checker", 5, "checker"),
+])
+def test_oracle_fast_matches_reference(golden, problem, oracle_fast, name, q, coeff):
+    G = golden(name)
+    sol, lv, radii = oracle_fast(q, coeff)
+    assert tuple(radii) == tuple(G["radii"])
+    for k in range(q, 0, -1):
+        assert O.rel_fro(lv[k]["stiffness"], G[f"A{k}"]) <= 1e-12
+        assert O.same_pattern(lv[k]["stiffness"], G[f"A{k}"])
+        assert O.rel_fro(lv[k]["psi"], G[f"psi{k}"]) <= 1e-12
+        assert O.same_pattern(lv[k]["psi"], G[f"psi{k}"])
+        if k >= 2:
+            for key, g in (("subband", "B"), ("restriction", "R"), ("correction", "D")):
+                assert O.rel_fro(lv[k][key], G[f"{g}{k}"]) <= 1e-12, (key, k)
+                assert O.same_pattern(lv[k][key], G[f"{g}{k}"]), (key, k)
+            np.testing.assert_allclose([lv[k]["lambda_min"], lv[k]["lambda_max"]],
+                                       G[f"lam{k}"], rtol=1e-9)
+    p = problem(q, coeff)
+    assert O.rel_energy(p.A, sol["u"], G["u"]) <= 1e-12
+
+
+def test_oracle_exact_matches_reference(golden, problem):
+    G = golden("exact_q3_example1")
+    p = problem(3)
+    sol, lv = O.exact_solve(p.M, p.A, p.load.b, 3)
+    for k in range(3, 0, -1):
+        assert O.rel_fro(lv[k]["stiffness"], G[f"A{k}"]) <= 1e-12
+        assert O.rel_fro(lv[k]["psi"], G[f"psi{k}"]) <= 1e-12
+    assert O.rel_energy(p.A, sol["u"], G["u"]) <= 1e-12
+
+
+def test_oracle_reproduces_reference_goldens_json(problem):
+    """The reference's own pinned values (pkg/tests/golden/goldens.json:
+    fast/q4/relerr and fast/q4/biorth_defect, rtol 1e-3), reproduced by the
+    oracle at the reference's default schedule."""
+    gold_relerr = [9.597639903617125e-4, 8.017142494668527e-6]
+    gold_biorth = [2.6573471127002216e-5, 7.159738350518316e-6]
+    p = problem(4)
+    ex, _ = O.exact_solve(p.M, p.A, p.load.b, 4)
+    errs, defs = [], []
+    for eps in (1e-3, 1e-4):
+        sol, lv, _ = O.fast_solve(p.M, p.A, p.load.g_nodal, 4, eps, spectral=False)
+        errs.append(O.rel_energy(p.A, sol["u"], ex["u"]))
+        worst = 0.0
+        for k in (1, 2, 3, 4):
+            Gm = (O.phi(k, 4, p.M) @ lv[k]["psi"].T).toarray()
+            worst = max(worst, float(np.abs(Gm - np.eye(Gm.shape[0])).max()))
+        defs.append(worst)
+    np.testing.assert_allclose(errs, gold_relerr, rtol=1e-3)
+    np.testing.assert_allclose(defs, gold_biorth, rtol=1e-3)
+
+
+def test_pinned_index_maps_and_schedules(golden):
+    P = golden("pins")
+    tree = gb.IndexTree(3)
+    np.testing.assert_array_equal(tree.chi_neighborhood(3, 5, 1), P["chi_q3_k3_c5_r1"])
+    np.testing.assert_array_equal(O.chi_indices(3, 5, 1), P["chi_q3_k3_c5_r1"])
+    assert gb.make_schedule(1e-3, 5).radii == tuple(P["radii_1e-3_q5"])
+    assert gb.make_schedule(1e-4, 5).radii == tuple(P["radii_1e-4_q5"])
+    assert gb.make_schedule(1e-3, 7).radii == tuple(P["radii_1e-3_q7"])
+    assert gb.make_schedule(1e-3, 4, uniform_rho=3).radii == tuple(P["radii_u3_q4"])
+    assert O.make_radii(1e-3, 7) == tuple(P["radii_1e-3_q7"])
+
+
+# --- host-side builders reproduce the reference bitwise --------------------
+
+@pytest.mark.parametrize("q", [3, 5, 7, 10])
+def test_assembly_is_bitwise_reference(golden, q):
+    P = golden("pins")
+    grid = gb.build_grid(q)
+    assert digest(gb.assemble_mass(grid)) == str(P[f"digest_M_q{q}"])
+    assert digest(gb.assemble_stiffness(grid, gb.coefficient_example1(grid))) == \
+        str(P[f"digest_Aex1_q{q}"])
+    assert digest(gb.assemble_stiffness(grid, gb.coefficient_checkerboard(grid, 1e4, 0))) \
+        == str(P[f"digest_Achk_q{q}"])
+
+
+def test_load_and_coefficient_pins(golden):
+    P = golden("pins")
+    grid = gb.build_grid(6)
+    load = gb.assemble_load(grid, gb.example_load(grid))
+    assert np.linalg.norm(load.b) == P["load_q6_norm"]
+    assert np.abs(load.b).sum() == P["load_q6_abs"]
+    coef = gb.coefficient_example1(grid)
+    np.testing.assert_array_equal([coef.lambda_min, coef.lambda_max], P["ex1_q6_minmax"])
+
+
+def test_hierarchy_maps_match_oracle():
+    tree = gb.IndexTree(5)
+    for k in range(2, 6):
+        for variant in ("orthonormal", "chain"):
+            W = tree.null_basis(k, variant)
+            assert O.same_pattern(W, O.null_basis(k, variant))
+            assert O.rel_fro(W, O.null_basis(k, variant)) == 0.0
+        P = tree.pi_step(k - 1)
+        assert O.rel_fro(P, O.pi_step(k - 1)) == 0.0
+        for i in sorted({0, min(7, 4 ** (k - 1) - 1), 4 ** (k - 1) - 1}):
+            np.testing.assert_array_equal(tree.neighborhood(k - 1, i, 3),
+                                          O.box_indices(2 ** (k - 1), i, 3))
+            np.testing.assert_array_equal(tree.chi_neighborhood(k, i, 3),
+                                          O.chi_indices(k, i, 3))
+    W = tree.null_basis(4)
+    assert np.all(np.abs((W @ np.ones(W.shape[1]))) == 0.0)
+    assert np.allclose((W @ W.T).toarray(), np.eye(W.shape[0]))
+
+
+def test_tree_and_schedule_guards():
+    for bad in (0, -2, 1.5, True, "3"):
+        with pytest.raises(gb.InvalidArgumentError):
+            gb.IndexTree(bad)
+    for eps in (0.0, 1.0, -0.5):
+        with pytest.raises(gb.InvalidArgumentError):
+            gb.make_schedule(eps, 4)
+    with pytest.raises(gb.InvalidArgumentError):
+        gb.make_schedule(1e-3, 4, uniform_rho=0)
+    with pytest.raises(gb.InvalidArgumentError):
+        gb.make_schedule(1e-3, 4).rho(5)
+    with pytest.raises(gb.InvalidArgumentError):
+        gb.build_grid(13)
+
+
+# --- the C ABI ----------------------------------------------------------------
+
+def test_library_exports_every_header_symbol():
+    from paper_1503_03467_b200 import _native
+    header = (ROOT / "include" / "gamblets_b200.h").read_text()
+    declared = set(re.findall(r"^(?:int|size_t|const char\*)\s+(gb_\w+)\(", header, re.M))
+    assert len(declared) > 40
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_native.EXPORTED)
+    assert lib.gb_abi_version() == 1
