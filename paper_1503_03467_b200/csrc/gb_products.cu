@@ -242,7 +242,7 @@ __global__ void k_level_blocks(int Lk, int wA, const double* __restrict__ A,
     for (int c = 0; c < 3; ++c) {
 #pragma unroll
       for (int cp = 0; cp < 3; ++cp) {
-        const double a = Bij[c][cp], b = Bji[c][cp];
+        const double a = Bij[c][cp], b = Bji[cp][c];
         mdiff = fmax(mdiff, fabs(a - b));
         mabs = fmax(mabs, fabs(a));
         double v = (a + b) * 0.5;

@@ -57,6 +57,11 @@ DENSE_PATCH_CUTOFF = 2048
 SYMMETRY_REPAIR_TOL = 1e-12
 _H = 0.5
 
+# debugging switches: skip the lambda estimates (fields stay None); report
+# device status words instead of raising
+SPECTRAL = True
+STRICT = True
+
 _KSTATE = np.dtype([
     ("rs", "f8"), ("pAp", "f8"), ("alpha", "f8"), ("beta", "f8"), ("bnorm", "f8"),
     ("tol_abs", "f8"), ("rnorm", "f8"), ("lam", "f8"), ("ynorm", "f8"), ("res", "f8"),
@@ -280,6 +285,12 @@ class _Ctx:
     def check(self):
         if self.n == 0:
             return
+        if not STRICT:
+            self._check()
+            return
+        self._check(raise_=True)
+
+    def _check(self, raise_=False):
         st = self.status[: 2 * self.n].cpu().numpy().reshape(-1, 2)
         stats = self.stats[: 2 * self.n].cpu().numpy().reshape(-1, 2)
         for i, kind, what, detail in self.labels:
@@ -288,10 +299,16 @@ class _Ctx:
                 md, ma = stats[i]
                 rep = 0.0 if ma == 0.0 else float(md / ma)
                 self.repair_of[i] = rep
+                if not raise_ and (rep >= SYMMETRY_REPAIR_TOL or code):
+                    print(f"[ctx] {what}: repair {rep:.3e} status {code}/{det}")
+                    continue
                 if rep >= SYMMETRY_REPAIR_TOL:
                     raise NumericalError(
                         f"{what} lost symmetry beyond rounding: relative repair {rep:.3e}")
             if code == 0:
+                continue
+            if not raise_:
+                print(f"[ctx] {kind} {what}: status {code} detail {det}")
                 continue
             if kind == "scale":
                 raise NumericalError(f"{what}: nonpositive diagonal entry (row {det})")
@@ -321,6 +338,7 @@ class _Krylov:
         self.state = dv.empty(nat.query("gb_kstate_bytes"), torch.uint8)
         self.part = dv.empty(2 * nat.query("gb_red_blocks"))
         self.dots = dv.empty(4)
+        nat.call("gb_state_reset", dv.ptr(self.state), 0, dv.stream())
 
     def read(self):
         return self.state.cpu().numpy().view(_KSTATE)[0]
@@ -568,7 +586,11 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         counter.add("scaling", 2 * J * dv.box_slots(wB, 3) + J)
 
         # K7: spectral extremes of S B S (gamblet_fast.py:531-534)
-        lam_min, lam_max, calls = _eig_extremes(B, sB)
+        if SPECTRAL:
+            lam_min, lam_max, calls = _eig_extremes(B, sB)
+        else:
+            lam_min = lam_max = None
+            calls = 0
         counter.add("spectral", 2 * J * dv.box_slots(wB, 3) * calls)
 
         # K4: correction patches -> D^T with the row-tail trim fused

@@ -1,0 +1,51 @@
+"""Stage-by-stage GPU vs oracle comparison (development aid)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import scipy.sparse as sp
+import torch
+import paper_1503_03467_b200 as gb
+from paper_1503_03467_b200 import gamblet_fast as gf, device as dv, _native as nat
+from oracle import gamblets_oracle as O
+sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tests"))
+from conftest import build_problem
+
+q = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+coeff = sys.argv[2] if len(sys.argv) > 2 else "example1"
+p = build_problem(q, coeff)
+gf.SPECTRAL = False
+gf.STRICT = False
+sched = gb.make_schedule(1e-13, q, uniform_rho=3)
+levels, _ = gb.fast_transform(p.M, p.A, p.tree, sched)
+lv = O.fast_transform(p.M, p.A, q, sched.radii, spectral=False)
+def cmp(name, a, b):
+    try:
+        e = O.rel_fro(a, b); pat = O.same_pattern(a, b)
+        print(f"{name:12s} rel {e:.3e} pattern {'ok' if pat else 'DIFF'} nnz {sp.csr_array(a).nnz} vs {sp.csr_array(b).nnz}")
+    except Exception as ex:
+        print(name, "ERR", ex)
+for k in range(q, 0, -1):
+    g, o = levels[k], lv[k]
+    cmp(f"A{k}", g.stiffness, o["stiffness"])
+    if o.get("psi") is not None: cmp(f"psi{k}", g.psi, o["psi"])
+    if k >= 2:
+        cmp(f"B{k}", g.subband, o["subband"])
+        print("   sB", np.abs(g.subband_scale / o["subband_scale"] - 1).max())
+        cmp(f"D{k}", g.correction, o["correction"])
+        cmp(f"R{k}", g.restriction, o["restriction"])
+# CG on our B^(q)
+B = levels[q].raw("subband"); sB = levels[q].raw("subband_scale")
+n = B.rows
+x = np.random.default_rng(0).standard_normal(n)
+xd = dv.to_dev(x); y = dv.empty(n)
+nat.call("gb_box_apply", B.L, B.nr, B.w, dv.ptr(B.vals), dv.ptr(sB), 0, dv.ptr(xd), dv.ptr(y), dv.stream())
+_, Bs = O.diag_scale(lv[q]["subband"])
+print("box_apply mode0 err", np.abs(y.cpu().numpy() - Bs @ x).max() / np.abs(Bs @ x).max())
+nat.call("gb_box_apply", B.L, B.nr, B.w, dv.ptr(B.vals), dv.ptr(sB), 1, dv.ptr(xd), dv.ptr(y), dv.stream())
+print("box_apply mode1 err", np.abs(y.cpu().numpy() - Bs @ x).max() / np.abs(Bs @ x).max())
+z, its, rel, conv, brk, h = gf._cg(B, sB, 0, xd, 1e-10)
+print("cg", its, rel, conv, brk, "err", np.abs(Bs @ z.cpu().numpy() - x).max())
+z, its, rel, conv, brk, h = gf._cg(B, sB, 0, xd, 1e-10, x0=dv.to_dev(0.5 * x))
+print("cg warm", its, rel, conv, brk, "err", np.abs(Bs @ z.cpu().numpy() - x).max())
+print("eig", gf._eig_extremes(B, sB)[:2], O.eig_extremes(Bs))
