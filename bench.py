@@ -1,0 +1,362 @@
+"""Benchmark: fine-DOF/s of the localized gamblet setup + subband solve (fp64).
+
+Workload (BASELINE.json configs[2], "Single GPU"): q = 10 (N = 4^10 =
+1,048,576 interior nodes under the reference's node convention), log-uniform
+contrast-1e4 checkerboard coefficient (PCG64 seed 0), Gaussian nodal load
+(seed 1), localized gamblets with uniform radius 3, reference tight mode
+(epsilon = 1e-13, c_tol = 1e-6).  A "step" is one full fast_solve: setup of
+every level (psi^(k), A^(k), B^(k), R, D, spectral estimates) plus all
+subband solves and the reassembly of u.
+
+  value  device-resident inputs (M, A as CSR in HBM, g in HBM), u left in HBM
+  e2e    the public API gb.fast_solve with host scipy M, A and host load,
+         host->device uploads and the device->host copy of u inside the step
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+        (N > 1: one process per GPU via torch.distributed.run; each rank solves
+        its own replica -- weak scaling, no domain decomposition yet)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(q=7, coeff="example1"),
+    "c2": dict(q=10, coeff="checker"),
+    "c3": dict(q=12, coeff="checker"),
+}
+EPS, RHO, CTOL = 1e-13, 3, 1e-6
+METRIC = "fine-DOF/s for gamblet setup+solve (fp64)"
+CPU_SAMPLE_Q = 6
+
+
+def build_inputs(q, coeff):
+    import paper_1503_03467_b200 as gb
+    grid = gb.build_grid(q)
+    if coeff == "example1":
+        c = gb.coefficient_example1(grid)
+        g = gb.example_load(grid)
+    else:
+        c = gb.coefficient_checkerboard(grid, 1e4, 0)
+        g = np.random.default_rng(1).standard_normal(grid.num_nodes)
+    M = gb.assemble_mass(grid)
+    A = gb.assemble_stiffness(grid, c)
+    load = gb.assemble_load(grid, g, mass=M)
+    return grid, M, A, load, gb.build_hierarchy(grid)
+
+
+def cpu_oracle_sample(coeff, threads):
+    """The CPU oracle (numpy/scipy restatement of the reference, tight mode)
+    on the q=CPU_SAMPLE_Q instance of the same configuration family."""
+    from threadpoolctl import threadpool_limits
+    from oracle import gamblets_oracle as O
+    grid, M, A, load, tree = build_inputs(CPU_SAMPLE_Q, coeff)
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        O.fast_solve(M, A, load.g_nodal, CPU_SAMPLE_Q, EPS, uniform_rho=RHO)
+        dt = time.perf_counter() - t0
+    return 4 ** CPU_SAMPLE_Q / dt, dt
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.path = Path(f"/tmp/gb_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def fp64_peak_tflops():
+    """Measured FP64 peak on this GPU: max of the DFMA and DMMA probes."""
+    import torch
+    from paper_1503_03467_b200 import _native as nat, device as dv
+    sink = dv.empty(1)
+    best = {}
+    for kind, name in ((0, "dfma"), (1, "dmma")):
+        iters = 4000
+        nat.call("gb_fp64_peak_probe", kind, 200, dv.ptr(sink), dv.stream())
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        nat.call("gb_fp64_peak_probe", kind, iters, dv.ptr(sink), dv.stream())
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if kind == 0:
+            flops = 148 * 8 * 256 * iters * 8 * 8 * 2.0
+        else:
+            flops = 148 * 8 * 8 * iters * 8 * 256 * 2.0   # warps * iters * 8 mma * 256 FMA
+        best[name] = flops / (ms * 1e-3) / 1e12
+    return best
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1503_03467_b200 as gb
+    from paper_1503_03467_b200 import _native as nat, device as dv, gamblet_fast as gf
+
+    torch.cuda.set_device(local_rank)
+    cfg = CONFIGS[args.config]
+    q = args.q or cfg["q"]
+    coeff = cfg["coeff"]
+    N = 4 ** q
+    grid, M, A, load, tree = build_inputs(q, coeff)
+    sched = gb.make_schedule(EPS, q, uniform_rho=RHO)
+
+    # device-resident inputs for the `value` leg
+    Md = dv.DeviceCSR.from_scipy(M)
+    Ad = dv.DeviceCSR.from_scipy(A)
+    gd = dv.to_dev(load.g_nodal)
+
+    def step_device():
+        counter = gb.FlopCounter()
+        levels, counter = gf.fast_transform(Md, Ad, tree, sched, counter=counter)
+        parts, U1 = gf._solve_levels(levels, gd, tree, sched, sched.subband_tol(), counter, [])
+        return levels, parts, counter
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    dv.Prof.reset(enabled=True)
+    launches0 = nat.query("gb_launch_count")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            levels, parts, counter = step_device()
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = nat.query("gb_launch_count") - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    phase_ms = {k: v / args.steps for k, v in dv.Prof.times_ms().items()}
+    phase_flops = {k: v / args.steps for k, v in dv.Prof.flops.items()}
+    phase_bytes = {k: v / args.steps for k, v in dv.Prof.bytes.items()}
+    phase_counts = {k: v // args.steps for k, v in dv.Prof.counts().items()}
+    dv.Prof.reset(enabled=False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * N / (ms * 1e-3)
+    iters = {k: v for k, v in counter.iterations.items()}
+
+    # e2e through the public API with host buffers
+    e2e_ms = []
+    h2d = d2h = 0
+    for i in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        barrier()
+        dv.Traffic.reset()
+        t0 = time.perf_counter()
+        res = gb.fast_solve(M, A, load, tree, EPS, uniform_rho=RHO, c_tol=CTOL)
+        u = res.solution.u  # host copy made inside the call
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d, d2h = dv.Traffic.h2d, dv.Traffic.d2h
+    e2e = float(np.median(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+    del res
+
+    if rank != 0:
+        return None
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs")
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if hbm_peak else "fallback B200_PROFILING.md"
+    hbm_peak = hbm_peak or 6650.0
+    fp64 = fp64_peak_tflops()
+    fp64_peak = max(fp64.values())
+
+    # dominant kernel family by device time
+    dom = max(phase_ms, key=phase_ms.get)
+    if phase_flops.get(dom):
+        achieved = phase_flops[dom] / (phase_ms[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "fp64", "achieved": round(achieved, 3),
+                "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
+                "frac": round(achieved / fp64_peak, 4),
+                "peak_source": "measured in-run (max of DFMA/DMMA probes; "
+                               "MEASURED_PEAKS.json has no fp64 figure)"}
+    else:
+        nb = phase_bytes.get(dom, 0.0)
+        achieved = nb / (phase_ms[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "peak_source": hbm_src}
+    prof_file = ROOT / "profiles" / "ncu_traffic.json"
+    traffic = None
+    if prof_file.exists():
+        traffic = json.loads(prof_file.read_text()).get(dom)
+    roof["traffic"] = traffic
+    roof["share_of_step"] = round(phase_ms[dom] / ms, 4)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, dt = cpu_oracle_sample(coeff, threads)
+        cpu = {"value": round(v, 2), "unit": "fine-DOF/s", "cores": threads, "kind": "port",
+               "sample": f"oracle/gamblets_oracle.fast_solve, q={CPU_SAMPLE_Q} instance of "
+                         f"the same config family ({4 ** CPU_SAMPLE_Q} DOFs), {dt:.1f} s"}
+
+    clocks = clk.summary()
+    out = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "fine-DOF/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded reference generators: checkerboard contrast 1e4 seed 0, "
+                "Gaussian nodal load seed 1)",
+        "config": {"workload": f"{args.config}: q={q}, N={N} fine DOFs, {coeff}, "
+                               f"localized gamblets rho={RHO}, tight mode eps={EPS}",
+                   "q": q, "fine_dofs": N, "rho": RHO, "epsilon": EPS,
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "l2": "working set > 126 MB L2 (operators ~GBs), no flush needed"},
+        "e2e": {"value": round(world * N / (e2e * 1e-3), 1), "unit": "fine-DOF/s",
+                "ms_per_step": round(e2e, 3), "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": int(launches // max(1, args.steps)),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "phases_ms": {k: round(v, 3) for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
+        "phase_launch_groups": phase_counts,
+        "fp64_peak_tflops": {k: round(v, 2) for k, v in fp64.items()},
+        "subband_iterations": iters.get("line8"),
+    }
+    return out
+
+
+def run_reference(args, rank):
+    """Reference arm: the CPU oracle port (the reference is pure Python and
+    cannot travel to the GPU box), all host threads, bounded sample."""
+    if rank != 0:
+        return None
+    cfg = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        v, dt = cpu_oracle_sample(cfg["coeff"], threads)
+        if i >= args.warmup:
+            times.append(dt)
+    dt = float(np.median(times))
+    value = 4 ** CPU_SAMPLE_Q / dt
+    sample = (f"oracle/gamblets_oracle.fast_solve (numpy/scipy restatement of the "
+              f"reference, tight mode), q={CPU_SAMPLE_Q} instance of {args.config}'s "
+              f"config family ({4 ** CPU_SAMPLE_Q} DOFs) per step")
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 2),
+        "unit": "fine-DOF/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (CPU sample q={CPU_SAMPLE_Q})"},
+        "cpu_baseline": {"value": round(value, 2), "unit": "fine-DOF/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 2), "unit": "fine-DOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--q", type=int, default=None, help="override the config's q")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank)
+    else:
+        if world > 1:
+            import torch
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl")
+        out = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

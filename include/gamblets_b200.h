@@ -47,6 +47,8 @@ extern "C" {
 #define GB_EXP_TDT 3
 
 int gb_abi_version(void);
+/* kernels launched through this ABI since load (for the bench's gpu_launches) */
+unsigned long long gb_launch_count(void);
 const char* gb_last_error(void);
 int gb_device_count(void);
 

@@ -25,6 +25,7 @@ _Z = ctypes.c_size_t
 # name -> (argtypes, restype)
 _SIGS = {
     "gb_abi_version": ([], _I),
+    "gb_launch_count": ([], ctypes.c_ulonglong),
     "gb_last_error": ([], ctypes.c_char_p),
     "gb_device_count": ([], _I),
     "gb_csr_halfwidth": ([_I, _P, _P, _P, _P], _I),

@@ -23,6 +23,8 @@ int gbk_csr_to_dense(int nrows, int ncols, const int32_t* indptr, const int32_t*
 int gbk_eye(int n, double* out, cudaStream_t s);
 
 static thread_local char g_err[512];
+static unsigned long long g_launches = 0;  // kernels launched through this ABI
+#define COUNT(n) (g_launches += (unsigned long long)(n))
 
 static int wrap(int e, const char* what) {
   if (e == 0) return GB_OK;
@@ -42,6 +44,7 @@ static int invalid(const char* msg) {
 extern "C" {
 
 int gb_abi_version(void) { return 1; }
+unsigned long long gb_launch_count(void) { return g_launches; }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
   int n = 0;
@@ -52,29 +55,35 @@ int gb_device_count(void) {
 int gb_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,
                      int32_t* out_w, void* stream) {
   if (n <= 0) return invalid("csr_halfwidth: n <= 0");
+  COUNT(1);
   return wrap(gbk_csr_halfwidth(n, indptr, indices, out_w, ST(stream)), "csr_halfwidth");
 }
 int gb_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
                   const double* data, double* box, int64_t* status, void* stream) {
   if (n <= 0 || w < 0) return invalid("csr_to_box: bad geometry");
+  COUNT(1);
   return wrap(gbk_csr_to_box(n, w, indptr, indices, data, box, LL(status), ST(stream)),
               "csr_to_box");
 }
 int gb_box_scale(int64_t rows, int nr, int w, const double* box, double* s,
                  int64_t* status, void* stream) {
+  COUNT(1);
   return wrap(gbk_box_scale(rows, nr, w, box, s, LL(status), ST(stream)), "box_scale");
 }
 int gb_box_diag_min(int64_t rows, int nr, int w, const double* box, double* dmin,
                     void* stream) {
+  COUNT(1);
   return wrap(gbk_box_diag_min(rows, nr, w, box, dmin, ST(stream)), "box_diag_min");
 }
 int gb_box_sym_drop(int L, int nr, int w, const double* raw, double* out,
                     const double* dmin, double* stats, void* stream) {
   if (raw == out) return invalid("box_sym_drop: in-place not supported");
+  COUNT(1);
   return wrap(gbk_box_sym_drop(L, nr, w, raw, out, dmin, stats, ST(stream)),
               "box_sym_drop");
 }
 int gb_row_tail_drop(int64_t rows, int64_t S, double* v, void* stream) {
+  COUNT(1);
   return wrap(gbk_row_tail_drop(rows, S, v, ST(stream)), "row_tail_drop");
 }
 
@@ -85,29 +94,34 @@ int gb_mass_patches(int n, int wM, const double* M, const double* s, int rho, in
                     double* psi, int64_t* status, double* workspace, int blocks,
                     void* stream) {
   if (rho < 0 || wd <= 0 || wd > n) return invalid("mass_patches: bad window");
+  COUNT(1);
   return wrap(gbk_mass_patches(n, wM, M, s, rho, wd, psi, LL(status), workspace, blocks,
                                ST(stream)),
               "mass_patches");
 }
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                    const double* A, int wX, double* X, void* stream) {
+  COUNT(1);
   return wrap(gbk_psi_stencil(n, lo, wd, rho, psi, wA, A, wX, X, ST(stream)),
               "psi_stencil");
 }
 int gb_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
                     const double* X, int wR, double* raw, void* stream) {
+  COUNT(1);
   return wrap(gbk_psi_galerkin(n, lo, wd, rho, psi, wX, X, wR, raw, ST(stream)),
               "psi_galerkin");
 }
 int gb_level_diag(int Lk, int wA, const double* A, const double* host_w12, double* bdiag,
                   double* dmin, void* stream) {
   if (Lk < 2 || (Lk & 1)) return invalid("level_diag: bad level side");
+  COUNT(1);
   return wrap(gbk_level_diag(Lk, wA, A, host_w12, bdiag, dmin, ST(stream)), "level_diag");
 }
 int gb_level_blocks(int Lk, int wA, const double* A, const double* host_w12, int wB,
                     const double* bdiag, const double* dmin, double* B, double* G,
                     double* PAPt, double* stats, void* stream) {
   if (Lk < 2 || (Lk & 1)) return invalid("level_blocks: bad level side");
+  COUNT(1);
   return wrap(gbk_level_blocks(Lk, wA, A, host_w12, wB, bdiag, dmin, B, G, PAPt, stats,
                                ST(stream)),
               "level_blocks");
@@ -119,36 +133,43 @@ int gb_correction_patches(int Lp, int wB, const double* B, const double* sB, int
                           const double* G, int rho, double* Dt, int64_t* status,
                           double* workspace, int blocks, void* stream) {
   if (Lp < 1 || rho < 0) return invalid("correction_patches: bad geometry");
+  COUNT(1);
   return wrap(gbk_correction_patches(Lp, wB, B, sB, wG, G, rho, Dt, LL(status), workspace,
                                      blocks, ST(stream)),
               "correction_patches");
 }
 int gb_restriction(int Lp, int rho, const double* Dt, const double* host_w12, double* R,
                    void* stream) {
+  COUNT(1);
   return wrap(gbk_restriction(Lp, rho, Dt, host_w12, R, ST(stream)), "restriction");
 }
 int gb_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
           double* BD, void* stream) {
+  COUNT(1);
   return wrap(gbk_bd(Lp, wB, B, rho, Dt, wBD, BD, ST(stream)), "bd");
 }
 int gb_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
            double* GtD, void* stream) {
+  COUNT(1);
   return wrap(gbk_gtd(Lp, wG, G, rho, Dt, wGD, GtD, ST(stream)), "gtd");
 }
 int gb_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
                   int rho, const double* Dt, int wBD, const double* BD, int wA2,
                   double* raw, void* stream) {
+  COUNT(1);
   return wrap(gbk_coarse_raw(Lp, wB, PAPt, wGD, GtD, rho, Dt, wBD, BD, wA2, raw,
                              ST(stream)),
               "coarse_raw");
 }
 int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double* psi,
             int wdw, double* Wpsi, void* stream) {
+  COUNT(1);
   return wrap(gbk_wpsi(n, Lk, lo, wd, host_w12, psi, wdw, Wpsi, ST(stream)), "wpsi");
 }
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
                 double* psi_next, void* stream) {
+  COUNT(1);
   return wrap(gbk_psi_next(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2, psi_next,
                            ST(stream)),
               "psi_next");
@@ -157,11 +178,13 @@ int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wd
 size_t gb_kstate_bytes(void) { return gbk_kstate_bytes(); }
 int gb_red_blocks(void) { return gbk_red_blocks(); }
 int gb_state_reset(void* state, int max_iter, void* stream) {
+  COUNT(1);
   return wrap(gbk_state_reset(state, max_iter, ST(stream)), "state_reset");
 }
 int gb_cg_init(int64_t n, const double* b, const double* x0, const double* Ax0,
                double* x, double* r, double* p, double rel_tol, int max_iter,
                void* state, double* partials, void* stream) {
+  COUNT(2);
   return wrap(gbk_cg_init(n, b, x0, Ax0, x, r, p, rel_tol, max_iter, state, partials,
                           ST(stream)),
               "cg_init");
@@ -169,6 +192,7 @@ int gb_cg_init(int64_t n, const double* b, const double* x0, const double* Ax0,
 int gb_cg_iterations(int L, int nr, int w, const double* B, const double* s, int mode,
                      double* x, double* r, double* p, double* Ap, int iters,
                      void* state, double* partials, void* stream) {
+  COUNT(3 * (unsigned long long)iters);
   return wrap(gbk_cg_iterations(L, nr, w, B, s, mode, x, r, p, Ap, iters, state,
                                 partials, ST(stream)),
               "cg_iterations");
@@ -176,62 +200,76 @@ int gb_cg_iterations(int L, int nr, int w, const double* B, const double* s, int
 int gb_pow_iterations(int L, int nr, int w, const double* B, const double* s, int mode,
                       double* x, double* y, double tol, int iters, void* state,
                       double* partials, void* stream) {
+  COUNT(3 * (unsigned long long)iters);
   return wrap(gbk_pow_iterations(L, nr, w, B, s, mode, x, y, tol, iters, state,
                                  partials, ST(stream)),
               "pow_iterations");
 }
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {
+  COUNT(1);
   return wrap(gbk_dot2(n, a, b, c, out, state, partials, ST(stream)), "dot2");
 }
 int gb_scale_by_norm(int64_t n, const double* a, const double* norm2, int which,
                      double* y, double* y2, void* stream) {
+  COUNT(1);
   return wrap(gbk_scale_by_norm(n, a, norm2, which, y, y2, ST(stream)), "scale_by_norm");
 }
 int gb_box_apply(int L, int nr, int w, const double* B, const double* s, int mode,
                  const double* x, double* y, void* stream) {
+  COUNT(1);
   return wrap(gbk_box_apply(L, nr, w, B, s, mode, x, y, ST(stream)), "box_apply");
 }
 int gb_apply_w(int Lp, const double* host_w12, const double* g, const double* s,
                double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_apply_w(Lp, host_w12, g, s, out, ST(stream)), "apply_w");
 }
 int gb_apply_wt(int Lp, const double* host_w12, const double* w, double* v,
                 void* stream) {
+  COUNT(1);
   return wrap(gbk_apply_wt(Lp, host_w12, w, v, ST(stream)), "apply_wt");
 }
 int gb_apply_r(int Lp, int rho, const double* R, const double* g, double* out,
                void* stream) {
+  COUNT(1);
   return wrap(gbk_apply_r(Lp, rho, R, g, out, ST(stream)), "apply_r");
 }
 int gb_psi_t_apply(int n, int L, int lo, int wd, const double* psi, const double* v,
                    double* inc, void* stream) {
+  COUNT(1);
   return wrap(gbk_psi_t_apply(n, L, lo, wd, psi, v, inc, ST(stream)), "psi_t_apply");
 }
 int gb_psi_apply(int n, int L, int lo, int wd, const double* psi, const double* b,
                  double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_psi_apply(n, L, lo, wd, psi, b, out, ST(stream)), "psi_apply");
 }
 int gb_axpby(int64_t n, double a, const double* x, double b, const double* y,
              double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_axpby(n, a, x, b, y, out, ST(stream)), "axpby");
 }
 int gb_vmul(int64_t n, const double* a, const double* b, double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_vmul(n, a, b, out, ST(stream)), "vmul");
 }
 int gb_vadd(int64_t n, const double* a, const double* b, double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_vadd(n, a, b, out, ST(stream)), "vadd");
 }
 
 int gb_export_count(int kind, int L, int nr, int w, int nc, int n, int lo, int wd,
                     const double* val, int64_t rows, int64_t S, int64_t* counts,
                     void* stream) {
+  COUNT(1);
   return wrap(gbk_export_count(kind, L, nr, w, nc, n, lo, wd, val, rows, S, LL(counts),
                                ST(stream)),
               "export_count");
 }
 int gb_exclusive_scan(const int64_t* counts, int64_t* indptr, int64_t n, void* tmp,
                       size_t* tmp_bytes, void* stream) {
+  COUNT(1);
   return wrap(gbk_exclusive_scan(reinterpret_cast<const long long*>(counts), LL(indptr),
                                  n, tmp, tmp_bytes, ST(stream)),
               "exclusive_scan");
@@ -239,6 +277,7 @@ int gb_exclusive_scan(const int64_t* counts, int64_t* indptr, int64_t n, void* t
 int gb_export_emit(int kind, int L, int nr, int w, int nc, int n, int lo, int wd,
                    const double* val, int64_t rows, int64_t S, const int64_t* indptr,
                    int32_t* indices, double* data, void* stream) {
+  COUNT(1);
   return wrap(gbk_export_emit(kind, L, nr, w, nc, n, lo, wd, val, rows, S,
                               reinterpret_cast<const long long*>(indptr), indices, data,
                               ST(stream)),
@@ -248,36 +287,45 @@ int gb_export_emit(int kind, int L, int nr, int w, int nc, int n, int lo, int wd
 int gb_dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta,
                   const double* B, int ldb, int tb, double beta, double* C, int ldc,
                   void* stream) {
+  COUNT(1);
   return wrap(gbk_dense_gemm(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc,
                              ST(stream)),
               "dense_gemm");
 }
 int gb_dense_potrf(int n, double* A, int lda, int64_t* status, void* stream) {
+  COUNT(3 * ((n + 63) / 64) + 1);
   return wrap(gbk_dense_potrf(n, A, lda, LL(status), ST(stream)), "dense_potrf");
 }
 int gb_dense_potrs(int n, int nrhs, const double* L, int lda, double* B, int ldb,
                    void* stream) {
+  COUNT(4 * ((n + 63) / 64));
   return wrap(gbk_dense_potrs(n, nrhs, L, lda, B, ldb, ST(stream)), "dense_potrs");
 }
 int gb_dense_sym(int n, const double* X, int ldx, double* out, double* stats,
                  void* stream) {
+  COUNT(1);
   return wrap(gbk_dense_sym(n, X, ldx, out, stats, ST(stream)), "dense_sym");
 }
 int gb_dense_build_w(int Lk, const double* host_w12, double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_dense_build_w(Lk, host_w12, out, ST(stream)), "dense_build_w");
 }
 int gb_dense_build_p(int Lk, double* out, double scale, void* stream) {
+  COUNT(1);
   return wrap(gbk_dense_build_p(Lk, scale, out, ST(stream)), "dense_build_p");
 }
 int gb_csr_to_dense(int nrows, int ncols, const int32_t* indptr, const int32_t* indices,
                     const double* data, double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_csr_to_dense(nrows, ncols, indptr, indices, data, out, ST(stream)),
               "csr_to_dense");
 }
 int gb_eye(int n, double* out, void* stream) {
+  COUNT(1);
   return wrap(gbk_eye(n, out, ST(stream)), "eye");
 }
 int gb_fp64_peak_probe(int kind, int iters, double* sink, void* stream) {
+  COUNT(1);
   return wrap(gbk_fp64_peak_probe(kind, iters, sink, ST(stream)), "fp64_peak_probe");
 }
 

@@ -9,6 +9,8 @@ cached on the host.
 
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -50,12 +52,102 @@ def zeros(n, dtype=torch.float64):
     return torch.zeros(int(n), dtype=dtype, device=device())
 
 
+class Traffic:
+    """Host<->device byte counters (the bench's e2e h2d/d2h accounting)."""
+
+    h2d = 0
+    d2h = 0
+
+    @classmethod
+    def reset(cls):
+        cls.h2d = cls.d2h = 0
+
+
 def to_dev(arr, dtype=None):
+    """Host array -> new device tensor (counted in Traffic.h2d).  A torch
+    tensor already on the device is returned as is."""
+    if isinstance(arr, torch.Tensor):
+        if arr.is_cuda:
+            return arr if dtype is None else arr.to(dtype)
+        arr = arr.numpy()
     a = np.ascontiguousarray(arr)
     t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)
+    Traffic.h2d += t.numel() * t.element_size()
     return t.to(device(), non_blocking=False)
+
+
+def to_host(t):
+    """Device tensor -> numpy (counted in Traffic.d2h)."""
+    Traffic.d2h += t.numel() * t.element_size()
+    return t.cpu().numpy()
+
+
+class DeviceCSR:
+    """A canonical CSR matrix already resident in HBM (int32 indptr/indices,
+    float64 data) -- the device-side form of the API's M and A."""
+
+    def __init__(self, indptr, indices, data, shape):
+        self.indptr, self.indices, self.data, self.shape = indptr, indices, data, shape
+
+    @classmethod
+    def from_scipy(cls, mat):
+        return cls(to_dev(mat.indptr.astype(np.int32, copy=False)),
+                   to_dev(mat.indices.astype(np.int32, copy=False)),
+                   to_dev(mat.data.astype(np.float64, copy=False)), mat.shape)
+
+
+class Prof:
+    """Optional per-phase CUDA-event timing on the launching stream."""
+
+    enabled = False
+    events = []
+    flops = {}
+    bytes = {}
+
+    @classmethod
+    def reset(cls, enabled=True):
+        cls.enabled = enabled
+        cls.events = []
+        cls.flops = {}
+        cls.bytes = {}
+
+    @classmethod
+    def add_work(cls, label, flops=0, nbytes=0):
+        if cls.enabled:
+            cls.flops[label] = cls.flops.get(label, 0) + flops
+            cls.bytes[label] = cls.bytes.get(label, 0) + nbytes
+
+    @classmethod
+    def times_ms(cls):
+        torch.cuda.synchronize()
+        out = {}
+        for label, a, b in cls.events:
+            out[label] = out.get(label, 0.0) + a.elapsed_time(b)
+        return out
+
+    @classmethod
+    def counts(cls):
+        out = {}
+        for label, _, _ in cls.events:
+            out[label] = out.get(label, 0) + 1
+        return out
+
+
+@contextmanager
+def phase(label):
+    if not Prof.enabled:
+        yield
+        return
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    try:
+        yield
+    finally:
+        b.record()
+        Prof.events.append((label, a, b))
 
 
 def box_slots(w, nc):
@@ -85,15 +177,15 @@ class _Exportable:
         tmp = empty(max(1, tmp_bytes.value), torch.uint8)
         nat.call("gb_exclusive_scan", ptr(counts), ptr(indptr), rows, ptr(tmp),
                  nat.ctypes.byref(tmp_bytes), s)
-        nnz = int(indptr[rows].item())
+        nnz = int(to_host(indptr[rows:rows + 1])[0])
         indices = empty(max(nnz, 1), torch.int32)
         data = empty(max(nnz, 1), torch.float64)
         nat.call("gb_export_emit", kind, L, nr, w, nc, n, lo, wd, ptr(self.vals), rows,
                  S, ptr(indptr), ptr(indices), ptr(data), s)
-        ip = indptr.cpu().numpy()
+        ip = to_host(indptr)
         if nnz < 2 ** 31 - 1:
             ip = ip.astype(np.int32)
-        out = sp.csr_array((data[:nnz].cpu().numpy(), indices[:nnz].cpu().numpy(), ip),
+        out = sp.csr_array((to_host(data[:nnz]), to_host(indices[:nnz]), ip),
                            shape=shape)
         out.has_sorted_indices = True
         self._csr = out
@@ -136,14 +228,6 @@ class BoxMatrix(_Exportable):
             return (EXP_TDT, L, 3, w, 3, 0, 0, 0, 3 * L * L, (2 * w + 1) ** 2, shape)
         raise InvalidArgumentError(f"unknown box kind {self.kind}")
 
-    def diagonal_host(self):
-        S = self.slots
-        c = np.arange(self.rows) % self.nr
-        center = (self.w * (2 * self.w + 1) + self.w) * self.nc + c
-        v = self.vals.view(self.rows, S)
-        idx = torch.as_tensor(center, device=v.device).view(-1, 1)
-        return v.gather(1, idx).view(-1).cpu().numpy()
-
 
 class PsiWindows(_Exportable):
     """Rows of psi^(k) over the fine grid in origin-clamped square windows.
@@ -170,14 +254,14 @@ class PsiWindows(_Exportable):
 
 def csr_to_box(mat, L):
     """Canonical CSR on an L x L grid -> BoxMatrix (half-width from the data).
-    Host CSR (scipy) is uploaded; this is the API entry of M and A."""
+    Host CSR (scipy) is uploaded; a DeviceCSR is used in place."""
     s = stream()
-    indptr = to_dev(mat.indptr.astype(np.int32, copy=False))
-    indices = to_dev(mat.indices.astype(np.int32, copy=False))
-    data = to_dev(mat.data.astype(np.float64, copy=False))
+    if not isinstance(mat, DeviceCSR):
+        mat = DeviceCSR.from_scipy(mat)
+    indptr, indices, data = mat.indptr, mat.indices, mat.data
     wbuf = zeros(1, torch.int32)
     nat.call("gb_csr_halfwidth", L, ptr(indptr), ptr(indices), ptr(wbuf), s)
-    w = int(wbuf.item())
+    w = int(to_host(wbuf)[0])
     box = zeros(L * L * box_slots(w, 1))
     status = zeros(2, torch.int64)
     nat.call("gb_csr_to_box", L, w, ptr(indptr), ptr(indices), ptr(data), ptr(box),

@@ -291,8 +291,8 @@ class _Ctx:
         self._check(raise_=True)
 
     def _check(self, raise_=False):
-        st = self.status[: 2 * self.n].cpu().numpy().reshape(-1, 2)
-        stats = self.stats[: 2 * self.n].cpu().numpy().reshape(-1, 2)
+        st = dv.to_host(self.status[: 2 * self.n]).reshape(-1, 2)
+        stats = dv.to_host(self.stats[: 2 * self.n]).reshape(-1, 2)
         for i, kind, what, detail in self.labels:
             code, det = int(st[i, 0]), int(st[i, 1])
             if kind == "sym":
@@ -341,7 +341,7 @@ class _Krylov:
         nat.call("gb_state_reset", dv.ptr(self.state), 0, dv.stream())
 
     def read(self):
-        return self.state.cpu().numpy().view(_KSTATE)[0]
+        return dv.to_host(self.state).view(_KSTATE)[0]
 
 
 def _cg(box, s, mode, b, rel_tol, x0=None, max_iter=None, kr=None):
@@ -428,7 +428,7 @@ def _eig_extremes(box, s, tol=0.1, max_iter=500, seed=24337):
         calls += 1
         nat.call("gb_dot2", n, dv.ptr(xn), dv.ptr(Ax), None, dv.ptr(dots[2:]),
                  dv.ptr(kr.state), dv.ptr(kr.part), st)
-        d = dots.cpu().numpy()
+        d = dv.to_host(dots)
         if d[0] == 0.0:
             raise NumericalError("inverse iteration broke down: A^{-1} x = 0")
         lam_min = float(d[2])
@@ -442,6 +442,12 @@ def _eig_extremes(box, s, tol=0.1, max_iter=500, seed=24337):
 # ---------------------------------------------------------------------------
 # transform
 # ---------------------------------------------------------------------------
+
+def _canon(mat):
+    if isinstance(mat, dv.DeviceCSR) or is_canonical_csr(mat):
+        return mat
+    return as_csr(mat)
+
 
 def _box_dev(level, name, L, ctx):
     v = level.raw(name)
@@ -473,8 +479,9 @@ def _level_q(M, A, tree, rho, ctx, counter):
         raise InvalidArgumentError(f"mass shape {M.shape} does not match q={q}")
     if A.shape != (N, N):
         raise InvalidArgumentError(f"stiffness shape {A.shape} does not match q={q}")
-    Mb, _ = dv.csr_to_box(M if is_canonical_csr(M) else as_csr(M), n)
-    Ab, _ = dv.csr_to_box(A if is_canonical_csr(A) else as_csr(A), n)
+    with dv.phase("input_to_box"):
+        Mb, _ = dv.csr_to_box(_canon(M), n)
+        Ab, _ = dv.csr_to_box(_canon(A), n)
     sM = dv.empty(N)
     nat.call("gb_box_scale", N, 1, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM),
              ctx.st(ctx.slot("scale", "mass")), s)
@@ -486,21 +493,26 @@ def _level_q(M, A, tree, rho, ctx, counter):
     blocks = _blocks_for(nmax, N)
     wsb = nat.query("gb_mass_patch_workspace", rho, blocks)
     ws = dv.empty(wsb // 8) if wsb else None
-    nat.call("gb_mass_patches", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd, dv.ptr(psi),
-             ctx.st(ctx.slot("mass", "mass")), dv.ptr(ws), blocks, s)
+    with dv.phase("mass_patches"):
+        nat.call("gb_mass_patches", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd,
+                 dv.ptr(psi), ctx.st(ctx.slot("mass", "mass")), dv.ptr(ws), blocks, s)
+    dv.Prof.add_work("mass_patches", flops=_patch_flops(n, rho, 1))
     wX = min(rho + Ab.w, n - 1)
     X = dv.empty(N * dv.box_slots(wX, 1))
-    nat.call("gb_psi_stencil", n, lo, wd, rho, dv.ptr(psi), Ab.w, dv.ptr(Ab.vals), wX,
-             dv.ptr(X), s)
     wR = min(wX + rho, n - 1)
     raw = dv.empty(N * dv.box_slots(wR, 1))
-    nat.call("gb_psi_galerkin", n, lo, wd, rho, dv.ptr(psi), wX, dv.ptr(X), wR,
-             dv.ptr(raw), s)
+    with dv.phase("psi_A_psiT"):
+        nat.call("gb_psi_stencil", n, lo, wd, rho, dv.ptr(psi), Ab.w, dv.ptr(Ab.vals), wX,
+                 dv.ptr(X), s)
+        nat.call("gb_psi_galerkin", n, lo, wd, rho, dv.ptr(psi), wX, dv.ptr(X), wR,
+                 dv.ptr(raw), s)
     del X
     i = ctx.slot("sym", "A^(q),loc")
-    nat.call("gb_box_diag_min", N, 1, wR, dv.ptr(raw), ctx.dm(i), s)
     Aq = dv.empty(N * dv.box_slots(wR, 1))
-    nat.call("gb_box_sym_drop", n, 1, wR, dv.ptr(raw), dv.ptr(Aq), ctx.dm(i), ctx.sp(i), s)
+    with dv.phase("sym_drop"):
+        nat.call("gb_box_diag_min", N, 1, wR, dv.ptr(raw), ctx.dm(i), s)
+        nat.call("gb_box_sym_drop", n, 1, wR, dv.ptr(raw), dv.ptr(Aq), ctx.dm(i),
+                 ctx.sp(i), s)
     # flop model: patch Cholesky + two triangular solves; box products
     counter.add("line2a", _patch_flops(n, rho, 1))
     counter.add("line3", N * wd * wd)
@@ -526,7 +538,7 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
     counter = counter if counter is not None else FlopCounter()
     ctx = _Ctx()
     n = 1 << q
-    Mb, _ = dv.csr_to_box(M if is_canonical_csr(M) else as_csr(M), n)
+    Mb, _ = dv.csr_to_box(_canon(M), n)
     sM = dv.empty(N)
     nat.call("gb_box_scale", N, 1, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM),
              ctx.st(ctx.slot("scale", "mass")), ctx.s)
@@ -571,23 +583,26 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         # K3: B (sym + dead-tail drop fused), G, P A P^T
         ib = ctx.slot("sym", f"B^({k}),loc")
         bdiag = dv.empty(J)
-        nat.call("gb_level_diag", Lk, wA, dv.ptr(Ab.vals), w12, dv.ptr(bdiag), ctx.dm(ib), s)
         Bv = dv.empty(J * dv.box_slots(wB, 3))
         Gv = dv.empty(J * dv.box_slots(wB, 1))
         PAPt = dv.empty(P * dv.box_slots(wB, 1))
-        nat.call("gb_level_blocks", Lk, wA, dv.ptr(Ab.vals), w12, wB, dv.ptr(bdiag),
-                 ctx.dm(ib), dv.ptr(Bv), dv.ptr(Gv), dv.ptr(PAPt), ctx.sp(ib), s)
+        sB = dv.empty(J)
+        with dv.phase("level_blocks"):
+            nat.call("gb_level_diag", Lk, wA, dv.ptr(Ab.vals), w12, dv.ptr(bdiag),
+                     ctx.dm(ib), s)
+            nat.call("gb_level_blocks", Lk, wA, dv.ptr(Ab.vals), w12, wB, dv.ptr(bdiag),
+                     ctx.dm(ib), dv.ptr(Bv), dv.ptr(Gv), dv.ptr(PAPt), ctx.sp(ib), s)
+            nat.call("gb_box_scale", J, 3, wB, dv.ptr(Bv), dv.ptr(sB),
+                     ctx.st(ctx.slot("scale", f"B^({k}),loc")), s)
         del bdiag
         B = BoxMatrix(Bv, Lp, 3, wB, 3)
-        sB = dv.empty(J)
-        nat.call("gb_box_scale", J, 3, wB, dv.ptr(Bv), dv.ptr(sB),
-                 ctx.st(ctx.slot("scale", f"B^({k}),loc")), s)
         counter.add("line7", 2 * J * dv.box_slots(wB, 3) * 16)
         counter.add("scaling", 2 * J * dv.box_slots(wB, 3) + J)
 
         # K7: spectral extremes of S B S (gamblet_fast.py:531-534)
         if SPECTRAL:
-            lam_min, lam_max, calls = _eig_extremes(B, sB)
+            with dv.phase("spectral"):
+                lam_min, lam_max, calls = _eig_extremes(B, sB)
         else:
             lam_min = lam_max = None
             calls = 0
@@ -599,33 +614,38 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         blocks = _blocks_for(nmax, P)
         wsb = nat.query("gb_correction_workspace", rho, blocks)
         ws = dv.empty(wsb // 8) if wsb else None
-        nat.call("gb_correction_patches", Lp, wB, dv.ptr(Bv), dv.ptr(sB), wB, dv.ptr(Gv), rho,
-                 dv.ptr(Dt), ctx.st(ctx.slot("corr", f"level {k}", detail=k)), dv.ptr(ws),
-                 blocks, s)
+        with dv.phase("correction_patches"):
+            nat.call("gb_correction_patches", Lp, wB, dv.ptr(Bv), dv.ptr(sB), wB, dv.ptr(Gv),
+                     rho, dv.ptr(Dt), ctx.st(ctx.slot("corr", f"level {k}", detail=k)),
+                     dv.ptr(ws), blocks, s)
+        dv.Prof.add_work("correction_patches", flops=_patch_flops(Lp, rho, 3))
         del ws
         counter.add("line11", _patch_flops(Lp, rho, 3))
         counter.record_solve(f"line11 level {k}", 1, 0.0, stages=1)
 
         # K6: R, split triple product
         Rv = dv.empty(P * dv.box_slots(rho, 4))
-        nat.call("gb_restriction", Lp, rho, dv.ptr(Dt), w12, dv.ptr(Rv), s)
+        with dv.phase("restriction"):
+            nat.call("gb_restriction", Lp, rho, dv.ptr(Dt), w12, dv.ptr(Rv), s)
         counter.add("line12", 2 * P * dv.box_slots(rho, 4) * 3)
         wBD = min(wB + rho, Lp - 1)
         BD = dv.empty(J * dv.box_slots(wBD, 1))
-        nat.call("gb_bd", Lp, wB, dv.ptr(Bv), rho, dv.ptr(Dt), wBD, dv.ptr(BD), s)
         wGD = min(wB + rho, Lp - 1)
         GtD = dv.empty(P * dv.box_slots(wGD, 1))
-        nat.call("gb_gtd", Lp, wB, dv.ptr(Gv), rho, dv.ptr(Dt), wGD, dv.ptr(GtD), s)
         wA2 = min(2 * rho + wB, Lp - 1)
         raw = dv.empty(P * dv.box_slots(wA2, 1))
-        nat.call("gb_coarse_raw", Lp, wB, dv.ptr(PAPt), wGD, dv.ptr(GtD), rho, dv.ptr(Dt),
-                 wBD, dv.ptr(BD), wA2, dv.ptr(raw), s)
+        with dv.phase("triple_product"):
+            nat.call("gb_bd", Lp, wB, dv.ptr(Bv), rho, dv.ptr(Dt), wBD, dv.ptr(BD), s)
+            nat.call("gb_gtd", Lp, wB, dv.ptr(Gv), rho, dv.ptr(Dt), wGD, dv.ptr(GtD), s)
+            nat.call("gb_coarse_raw", Lp, wB, dv.ptr(PAPt), wGD, dv.ptr(GtD), rho,
+                     dv.ptr(Dt), wBD, dv.ptr(BD), wA2, dv.ptr(raw), s)
         del BD, GtD, PAPt, Gv
         ia = ctx.slot("sym", f"A^({k - 1}),loc")
-        nat.call("gb_box_diag_min", P, 1, wA2, dv.ptr(raw), ctx.dm(ia), s)
         An = dv.empty(P * dv.box_slots(wA2, 1))
-        nat.call("gb_box_sym_drop", Lp, 1, wA2, dv.ptr(raw), dv.ptr(An), ctx.dm(ia),
-                 ctx.sp(ia), s)
+        with dv.phase("sym_drop"):
+            nat.call("gb_box_diag_min", P, 1, wA2, dv.ptr(raw), ctx.dm(ia), s)
+            nat.call("gb_box_sym_drop", Lp, 1, wA2, dv.ptr(raw), dv.ptr(An), ctx.dm(ia),
+                     ctx.sp(ia), s)
         del raw
         nb = 3 * (2 * min(rho, wB) + 1) ** 2
         counter.add("line13", 2 * J * dv.box_slots(wBD, 1) * nb
@@ -638,14 +658,16 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
             lo, hi, wd = psiw.lo, psiw.hi, psiw.wd
             wdw = min(hi - lo + 1 + h, n)
             Wpsi = dv.empty(J * wdw * wdw)
-            nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw, dv.ptr(Wpsi), s)
             lo2, hi2 = -2 * rho * h + lo, (2 * rho + 1) * h + hi
             wd2 = PsiWindows.window(n, lo2, hi2)
             pv = dv.empty(P * wd2 * wd2)
-            nat.call("gb_psi_next", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw, dv.ptr(Wpsi),
-                     rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), s)
+            with dv.phase("psi_next"):
+                nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
+                         dv.ptr(Wpsi), s)
+                nat.call("gb_psi_next", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
+                         dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), s)
+                nat.call("gb_row_tail_drop", P, wd2 * wd2, dv.ptr(pv), s)
             del Wpsi
-            nat.call("gb_row_tail_drop", P, wd2 * wd2, dv.ptr(pv), s)
             psin = PsiWindows(pv, n, Lp, lo2, hi2)
             counter.add("line14", 2 * P * wd2 * wd2 * 3 * (2 * rho + 1) ** 2 // 4
                         + 2 * J * wdw * wdw * 4)
@@ -712,8 +734,9 @@ def solve_with_transform(levels, load, tree, schedule, g_mode="nodal", counter=N
     if isinstance(load, LoadVector):
         b, g_nodal = load.b, load.g_nodal
     else:
-        b, g_nodal = np.asarray(load, dtype=float), None
-    if b.shape != (N,):
+        b, g_nodal = (load if isinstance(load, torch.Tensor)
+                      else np.asarray(load, dtype=float)), None
+    if tuple(b.shape) != (N,):
         raise InvalidArgumentError(f"load shape {b.shape} does not match N={N}")
     s = dv.stream()
 
@@ -723,7 +746,8 @@ def solve_with_transform(levels, load, tree, schedule, g_mode="nodal", counter=N
                 raise InvalidArgumentError(
                     "nodal moment shortcut needs a LoadVector with g_nodal; "
                     "pass g_mode='measured' for a bare right-hand side")
-            g = dv.to_dev(np.asarray(g_nodal, dtype=float))
+            g = dv.to_dev(g_nodal if isinstance(g_nodal, torch.Tensor)
+                          else np.asarray(g_nodal, dtype=float))
             counter.add("line4", 0)
         elif g_mode == "measured":
             psiq = levels[q].raw("psi")
@@ -739,8 +763,8 @@ def solve_with_transform(levels, load, tree, schedule, g_mode="nodal", counter=N
         g = _solve_levels(levels, g, tree, schedule, tol, counter, records)
 
     sol_parts, U1 = g
-    u = sol_parts["partials"].device(q).cpu().numpy()
-    solution = MultiresSolution(u=u, u1_coarse=U1.cpu().numpy(),
+    u = dv.to_host(sol_parts["partials"].device(q))
+    solution = MultiresSolution(u=u, u1_coarse=dv.to_host(U1),
                                 subband_coeffs=sol_parts["coeffs"],
                                 increments=sol_parts["increments"],
                                 partials=sol_parts["partials"], records=records)
@@ -774,7 +798,9 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
         rhs = dv.empty(J)
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
         counter.add("line8", 8 * J + J)
-        z, its, rel, conv, brk, _ = _cg(B, sB, 1, rhs, tol)
+        with dv.phase("subband_cg"):
+            z, its, rel, conv, brk, _ = _cg(B, sB, 1, rhs, tol)
+        dv.Prof.add_work("subband_cg", nbytes=its * (8 * J * B.slots + 6 * 8 * J))
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")
