@@ -294,6 +294,8 @@ def run_ours(args, rank, world, local_rank):
         "phase_launch_groups": phase_counts,
         "fp64_peak_tflops": {k: round(v, 2) for k, v in fp64.items()},
         "subband_iterations": iters.get("line8"),
+        "spectral_iterations": [{"n": d["n"], "power": d["power"], "inner_cg": d["inner"]}
+                                for d in gf._SPECTRAL_LOG[-(q - 1):]],
     }
     return out
 

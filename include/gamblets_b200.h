@@ -79,6 +79,11 @@ int gb_mass_patches(int n, int wM, const double* M, const double* s, int rho, in
                     double* psi, int64_t* status, double* workspace, int blocks,
                     void* stream);
 
+/* v2: tiled DMMA Cholesky in shared memory on the pre-scaled S M S box
+ * (gb_scale_box); GB_ERR_INVALID when the patch does not fit (use v1) */
+int gb_mass_patches_v2(int n, int wM, const double* Ms, const double* s, int rho, int wd,
+                       double* psi, int64_t* status, void* stream);
+
 /* ---- K2 A^(q) = psi A psi^T (gamblet_fast.py:658-665) -------------------- */
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                    const double* A, int wX, double* X, void* stream);
@@ -98,6 +103,11 @@ size_t gb_correction_workspace(int rho, int blocks);
 int gb_correction_patches(int Lp, int wB, const double* B, const double* sB, int wG,
                           const double* G, int rho, double* Dt, int64_t* status,
                           double* workspace, int blocks, void* stream);
+
+/* v2: tiled DMMA Cholesky on the pre-scaled S B S box */
+int gb_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
+                             const double* G, int rho, double* Dt, int64_t* status,
+                             void* stream);
 
 /* ---- K6 R, split triple product, psi^(k-1) (gamblet_fast.py:587-624) ----- */
 int gb_restriction(int Lp, int rho, const double* Dt, const double* host_w12,
@@ -129,6 +139,32 @@ int gb_cg_iterations(int L, int nr, int w, const double* B, const double* s, int
 int gb_pow_iterations(int L, int nr, int w, const double* B, const double* s, int mode,
                       double* x, double* y, double tol, int iters, void* state,
                       double* partials, void* stream);
+/* v2 operator: pre-scaled Bs = S B S on zero-halo padded vectors */
+int gb_scale_box(int L, int nr, int w, const double* B, const double* s, double* Bs,
+                 void* stream);
+int gb_pad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+           void* stream);
+int gb_unpad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+             void* stream);
+int gb_pcg_iterations(int L, int nr, int w, const double* Bs, double* x, double* r,
+                      double* p, double* Ap, int iters, void* state, double* partials,
+                      void* stream);
+int gb_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, double* y,
+                       double tol, int iters, void* state, double* partials, void* stream);
+int gb_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
+                  void* stream);
+/* v3 operator: blocked slot-major S B S (BsT[(r/32)*S*32 + j*32 + r%32]),
+ * one thread per row; gb_boxT_elems gives the allocation size in doubles */
+size_t gb_boxT_elems(int L, int nr, int w);
+int gb_scale_box_T(int L, int nr, int w, const double* B, const double* s, double* BsT,
+                   void* stream);
+int gb_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
+                      double* p, double* Ap, int iters, void* state, double* partials,
+                      void* stream);
+int gb_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
+                       double tol, int iters, void* state, double* partials, void* stream);
+int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
+                  void* stream);
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream);
 int gb_scale_by_norm(int64_t n, const double* a, const double* norm2, int which,

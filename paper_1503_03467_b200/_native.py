@@ -36,6 +36,8 @@ _SIGS = {
     "gb_row_tail_drop": ([_L, _L, _P, _P], _I),
     "gb_mass_patch_workspace": ([_I, _I], _Z),
     "gb_mass_patches": ([_I, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P], _I),
+    "gb_mass_patches_v2": ([_I, _I, _P, _P, _I, _I, _P, _P, _P], _I),
+    "gb_correction_patches_v2": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _P], _I),
     "gb_psi_stencil": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_psi_galerkin": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_level_diag": ([_I, _I, _P, _P, _P, _P, _P], _I),
@@ -54,6 +56,17 @@ _SIGS = {
     "gb_cg_init": ([_L, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
     "gb_cg_iterations": ([_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P], _I),
     "gb_pow_iterations": ([_I, _I, _I, _P, _P, _I, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_scale_box": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_pad": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_unpad": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_pcg_iterations": ([_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
+    "gb_ppow_iterations": ([_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_pbox_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_boxT_elems": ([_I, _I, _I], _Z),
+    "gb_scale_box_T": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_tcg_iterations": ([_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
+    "gb_tpow_iterations": ([_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_tbox_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
     "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),
     "gb_box_apply": ([_I, _I, _I, _P, _P, _I, _P, _P, _P], _I),

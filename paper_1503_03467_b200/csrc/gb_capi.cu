@@ -99,6 +99,22 @@ int gb_mass_patches(int n, int wM, const double* M, const double* s, int rho, in
                                ST(stream)),
               "mass_patches");
 }
+int gb_mass_patches_v2(int n, int wM, const double* Ms, const double* s, int rho, int wd,
+                       double* psi, int64_t* status, void* stream) {
+  COUNT(1);
+  const int rc = gbk_mass_patches_v2(n, wM, Ms, s, rho, wd, psi, LL(status), ST(stream));
+  if (rc == 1) return invalid("mass_patches_v2: patch exceeds shared memory");
+  return wrap(rc, "mass_patches_v2");
+}
+int gb_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
+                             const double* G, int rho, double* Dt, int64_t* status,
+                             void* stream) {
+  COUNT(1);
+  const int rc = gbk_correction_patches_v2(Lp, wB, Bs, sB, wG, G, rho, Dt, LL(status),
+                                           ST(stream));
+  if (rc == 1) return invalid("correction_patches_v2: patch exceeds shared memory");
+  return wrap(rc, "correction_patches_v2");
+}
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                    const double* A, int wX, double* X, void* stream) {
   COUNT(1);
@@ -204,6 +220,67 @@ int gb_pow_iterations(int L, int nr, int w, const double* B, const double* s, in
   return wrap(gbk_pow_iterations(L, nr, w, B, s, mode, x, y, tol, iters, state,
                                  partials, ST(stream)),
               "pow_iterations");
+}
+int gb_scale_box(int L, int nr, int w, const double* B, const double* s, double* Bs,
+                 void* stream) {
+  COUNT(1);
+  return wrap(gbk_scale_box(L, nr, w, B, s, Bs, ST(stream)), "scale_box");
+}
+int gb_pad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+           void* stream) {
+  COUNT(1);
+  return wrap(gbk_pad(L, nr, w, src, scale, dst, ST(stream)), "pad");
+}
+int gb_unpad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+             void* stream) {
+  COUNT(1);
+  return wrap(gbk_unpad(L, nr, w, src, scale, dst, ST(stream)), "unpad");
+}
+int gb_pcg_iterations(int L, int nr, int w, const double* Bs, double* x, double* r,
+                      double* p, double* Ap, int iters, void* state, double* partials,
+                      void* stream) {
+  COUNT(3 * (unsigned long long)iters);
+  return wrap(gbk_pcg_iterations(L, nr, w, Bs, x, r, p, Ap, iters, state, partials,
+                                 ST(stream)),
+              "pcg_iterations");
+}
+int gb_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, double* y,
+                       double tol, int iters, void* state, double* partials, void* stream) {
+  COUNT(3 * (unsigned long long)iters);
+  return wrap(gbk_ppow_iterations(L, nr, w, Bs, x, y, tol, iters, state, partials,
+                                  ST(stream)),
+              "ppow_iterations");
+}
+int gb_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
+                  void* stream) {
+  COUNT(1);
+  return wrap(gbk_pbox_apply(L, nr, w, Bs, x, y, ST(stream)), "pbox_apply");
+}
+size_t gb_boxT_elems(int L, int nr, int w) { return gbk_boxT_elems(L, nr, w); }
+int gb_scale_box_T(int L, int nr, int w, const double* B, const double* s, double* BsT,
+                   void* stream) {
+  COUNT(1);
+  return wrap(gbk_scale_box_T(L, nr, w, B, s, BsT, ST(stream)), "scale_box_T");
+}
+int gb_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
+                      double* p, double* Ap, int iters, void* state, double* partials,
+                      void* stream) {
+  COUNT(3 * (unsigned long long)iters);
+  return wrap(gbk_tcg_iterations(L, nr, w, BsT, x, r, p, Ap, iters, state, partials,
+                                 ST(stream)),
+              "tcg_iterations");
+}
+int gb_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
+                       double tol, int iters, void* state, double* partials, void* stream) {
+  COUNT(3 * (unsigned long long)iters);
+  return wrap(gbk_tpow_iterations(L, nr, w, BsT, x, y, tol, iters, state, partials,
+                                  ST(stream)),
+              "tpow_iterations");
+}
+int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
+                  void* stream) {
+  COUNT(1);
+  return wrap(gbk_tbox_apply(L, nr, w, BsT, x, y, ST(stream)), "tbox_apply");
 }
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {

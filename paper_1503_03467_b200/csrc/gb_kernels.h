@@ -96,3 +96,31 @@ int gbk_vmul(long long n, const double* a, const double* b, double* out, cudaStr
 int gbk_vadd(long long n, const double* a, const double* b, double* out, cudaStream_t s);
 int gbk_psi_apply(int n, int L, int lo, int wd, const double* psi, const double* b,
                   double* out, cudaStream_t s);
+int gbk_scale_box(int L, int nr, int w, const double* B, const double* sv, double* Bs,
+                  cudaStream_t s);
+int gbk_pad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+            cudaStream_t s);
+int gbk_unpad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+              cudaStream_t s);
+int gbk_pcg_iterations(int L, int nr, int w, const double* Bs, double* x, double* r,
+                       double* p, double* Ap, int iters, void* st, double* part,
+                       cudaStream_t s);
+int gbk_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, double* y,
+                        double tol, int iters, void* st, double* part, cudaStream_t s);
+int gbk_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
+                   cudaStream_t s);
+int gbk_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
+                              const double* G, int rho, double* Dt, long long* status,
+                              cudaStream_t st);
+int gbk_mass_patches_v2(int n, int wM, const double* Ms, const double* s, int rho, int wd,
+                        double* psi, long long* status, cudaStream_t st);
+int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, double* BsT,
+                    cudaStream_t s);
+int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
+                       double* p, double* Ap, int iters, void* st, double* part,
+                       cudaStream_t s);
+int gbk_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
+                        double tol, int iters, void* st, double* part, cudaStream_t s);
+int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
+                   cudaStream_t s);
+size_t gbk_boxT_elems(int L, int nr, int w);

@@ -376,6 +376,341 @@ __global__ void k_box_apply(int L, int nr, int w, const double* __restrict__ B,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// v2 Krylov operator: pre-scaled box Bs = S B S (the reference materializes
+// exactly this for its spectral estimates, gamblet_fast.py:123-139) applied
+// to vectors in a zero-halo padded layout, so the gather needs no bounds
+// checks: grid point (s,t) with components c lives at
+// ((s + w) * Lpad + (t + w)) * nr + c, Lpad = L + 2w.  One warp per grid
+// point computes its nr rows together, loading each x value once; the slot ->
+// relative x offset table sits in shared memory.
+// ---------------------------------------------------------------------------
+__global__ void k_scale_box(int L, int nr, int w, const double* __restrict__ B,
+                            const double* __restrict__ s, double* __restrict__ Bs) {
+  const int W2 = 2 * w + 1, S = W2 * W2 * nr;
+  const long long total = (long long)L * L * nr * S;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / S;
+    const int sl = (int)(e - r * S);
+    const int cp = sl % nr, bs = sl / nr;
+    const long long p = r / nr;
+    const int qs = (int)(p / L) + bs / W2 - w, qt = (int)(p % L) + bs % W2 - w;
+    double v = 0.0;
+    if (qs >= 0 && qs < L && qt >= 0 && qt < L)
+      v = B[e] * s[r] * s[((long long)qs * L + qt) * nr + cp];
+    Bs[e] = v;
+  }
+}
+
+__global__ void k_pad(int L, int nr, int w, const double* __restrict__ src,
+                      const double* __restrict__ scale, double* __restrict__ dst) {
+  const long long n = (long long)L * L * nr;
+  const int Lpad = L + 2 * w;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long p = r / nr;
+    const int c = (int)(r - p * nr);
+    const long long pr = (((long long)(p / L) + w) * Lpad + (p % L) + w) * nr + c;
+    dst[pr] = scale ? scale[r] * src[r] : src[r];
+  }
+}
+
+__global__ void k_unpad(int L, int nr, int w, const double* __restrict__ src,
+                        const double* __restrict__ scale, double* __restrict__ dst) {
+  const long long n = (long long)L * L * nr;
+  const int Lpad = L + 2 * w;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long p = r / nr;
+    const int c = (int)(r - p * nr);
+    const long long pr = (((long long)(p / L) + w) * Lpad + (p % L) + w) * nr + c;
+    dst[r] = scale ? scale[r] * src[pr] : src[pr];
+  }
+}
+
+__device__ __forceinline__ void build_offsets(int nr, int w, int Lpad, int* off) {
+  const int W2 = 2 * w + 1, S = W2 * W2 * nr;
+  for (int j = threadIdx.x; j < S; j += blockDim.x) {
+    const int c = j % nr, bs = j / nr;
+    off[j] = ((bs / W2) * Lpad + (bs % W2)) * nr + c;
+  }
+  __syncthreads();
+}
+
+template <int NR>
+__device__ __forceinline__ void point_apply(const double* __restrict__ blk, int S,
+                                            const int* __restrict__ off,
+                                            const double* __restrict__ x, long long xb,
+                                            int lane, double* y) {
+  double a[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) a[c] = 0.0;
+#pragma unroll 4
+  for (int j = lane; j < S; j += 32) {
+    const double xv = x[xb + off[j]];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) a[c] = fma(__ldg(blk + c * S + j), xv, a[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < NR; ++c) y[c] = warp_sum(a[c]);
+}
+
+// y = Bs x over padded vectors; optional fused dot x.y into the state
+template <int NR>
+__device__ __forceinline__ double pbox_pass(int L, int w, const double* __restrict__ Bs,
+                                            const double* __restrict__ x,
+                                            double* __restrict__ y, const int* off,
+                                            double* yy_out) {
+  const int W2 = 2 * w + 1, S = W2 * W2 * NR, Lpad = L + 2 * w;
+  const long long P = (long long)L * L;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  double dot = 0.0, yy = 0.0;
+  for (long long p = wid; p < P; p += nwarps) {
+    const int ps = (int)(p / L), pt = (int)(p % L);
+    const long long xb = ((long long)ps * Lpad + pt) * NR;
+    double v[NR];
+    point_apply<NR>(Bs + p * NR * S, S, off, x, xb, lane, v);
+    if (lane == 0) {
+      const long long yr = ((long long)(ps + w) * Lpad + pt + w) * NR;
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        y[yr + c] = v[c];
+        dot += x[yr + c] * v[c];
+        yy += v[c] * v[c];
+      }
+    }
+  }
+  *yy_out = yy;
+  return dot;
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_pcg_spmv(int L, int w, const double* __restrict__ Bs,
+                                                  const double* __restrict__ p,
+                                                  double* __restrict__ Ap, KState* st,
+                                                  double* part) {
+  extern __shared__ int off[];
+  __shared__ double sh[32];
+  if (st->done) return;
+  build_offsets(NR, w, L + 2 * w, off);
+  double yy;
+  double dot = pbox_pass<NR>(L, w, Bs, p, Ap, off, &yy);
+  dot = block_sum(dot, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = dot;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->pAp = a;
+      if (!(a > 0.0)) {
+        st->breakdown = st->it + 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rs / a;
+      }
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_ppow_apply(int L, int w, const double* __restrict__ Bs,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y, KState* st,
+                                                    double* part) {
+  extern __shared__ int off[];
+  __shared__ double sh[32];
+  if (st->done) return;
+  build_offsets(NR, w, L + 2 * w, off);
+  double yy;
+  double xy = pbox_pass<NR>(L, w, Bs, x, y, off, &yy);
+  xy = block_sum(xy, sh);
+  yy = block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = xy;
+    part[2 * blockIdx.x + 1] = yy;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->lam = a;
+      st->ynorm = sqrt(b);
+      if (st->ynorm == 0.0) {
+        st->lam = 0.0;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_pbox_apply(int L, int w, const double* __restrict__ Bs,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+  extern __shared__ int off[];
+  build_offsets(NR, w, L + 2 * w, off);
+  double yy;
+  pbox_pass<NR>(L, w, Bs, x, y, off, &yy);
+}
+
+
+// ---------------------------------------------------------------------------
+// v3 Krylov operator: slot-major ("transposed box") copy of S B S,
+// BsT[j * R + r] for slot j, row r (R rows).  One thread per row streams its
+// slots: at every slot a warp reads 32 consecutive rows (256 B, coalesced)
+// and gathers x from 32 consecutive padded positions; no shuffles, long
+// unrollable loops.  The slot -> relative x offset table is in shared memory
+// (every thread reads the same entry: broadcast).
+// ---------------------------------------------------------------------------
+__global__ void k_scale_box_T(int L, int nr, int w, const double* __restrict__ B,
+                              const double* __restrict__ s, double* __restrict__ BsT) {
+  // blocked slot-major: BsT[(r / 32) * S * 32 + j * 32 + (r % 32)]
+  const int W2 = 2 * w + 1, S = W2 * W2 * nr;
+  const long long R = (long long)L * L * nr;
+  const long long nblk = (R + 31) / 32;
+  const long long total = nblk * S * 32;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long blk = e / (32LL * S);
+    const int rem = (int)(e - blk * 32LL * S);
+    const int j = rem >> 5;
+    const long long r = blk * 32 + (rem & 31);
+    double v = 0.0;
+    if (r < R) {
+      const int cp = j % nr, bs = j / nr;
+      const long long p = r / nr;
+      const int qs = (int)(p / L) + bs / W2 - w, qt = (int)(p % L) + bs % W2 - w;
+      if (qs >= 0 && qs < L && qt >= 0 && qt < L)
+        v = B[r * S + j] * s[r] * s[((long long)qs * L + qt) * nr + cp];
+    }
+    BsT[e] = v;
+  }
+}
+
+template <int NR>
+__device__ __forceinline__ double trow_apply(const double* __restrict__ BsT, long long R, int S,
+                                             const int* __restrict__ off,
+                                             const double* __restrict__ x, long long xb,
+                                             long long r) {
+  const double* a = BsT + (r >> 5) * (32LL * S) + (r & 31);
+  double acc0 = 0.0, acc1 = 0.0;
+  int j = 0;
+#pragma unroll 4
+  for (; j + 1 < S; j += 2) {
+    acc0 = fma(__ldg(a + 32 * j), __ldg(x + xb + off[j]), acc0);
+    acc1 = fma(__ldg(a + 32 * (j + 1)), __ldg(x + xb + off[j + 1]), acc1);
+  }
+  if (j < S) acc0 = fma(__ldg(a + 32 * j), __ldg(x + xb + off[j]), acc0);
+  return acc0 + acc1;
+}
+
+// y = BsT x over padded vectors for rows [0, R); returns partial dots x.y, y.y
+template <int NR>
+__device__ __forceinline__ void tbox_pass(int L, int w, const double* __restrict__ BsT,
+                                          const double* __restrict__ x, double* __restrict__ y,
+                                          const int* off, double* xy, double* yy) {
+  const int W2 = 2 * w + 1, S = W2 * W2 * NR, Lpad = L + 2 * w;
+  const long long R = (long long)L * L * NR;
+  double d0 = 0.0, d1 = 0.0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long p = r / NR;
+    const int c = (int)(r - p * NR);
+    const int ps = (int)(p / L), pt = (int)(p % L);
+    const long long xb = ((long long)ps * Lpad + pt) * NR;
+    const double v = trow_apply<NR>(BsT, R, S, off, x, xb, r);
+    const long long yr = ((long long)(ps + w) * Lpad + pt + w) * NR + c;
+    y[yr] = v;
+    d0 += x[yr] * v;
+    d1 += v * v;
+  }
+  *xy = d0;
+  *yy = d1;
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_tcg_spmv(int L, int w, const double* __restrict__ BsT,
+                                                  const double* __restrict__ p,
+                                                  double* __restrict__ Ap, KState* st,
+                                                  double* part) {
+  extern __shared__ int off[];
+  __shared__ double sh[32];
+  if (st->done) return;
+  build_offsets(NR, w, L + 2 * w, off);
+  double dot, yy;
+  tbox_pass<NR>(L, w, BsT, p, Ap, off, &dot, &yy);
+  dot = block_sum(dot, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = dot;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->pAp = a;
+      if (!(a > 0.0)) {
+        st->breakdown = st->it + 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rs / a;
+      }
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_tpow_apply(int L, int w, const double* __restrict__ BsT,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y, KState* st,
+                                                    double* part) {
+  extern __shared__ int off[];
+  __shared__ double sh[32];
+  if (st->done) return;
+  build_offsets(NR, w, L + 2 * w, off);
+  double xy, yy;
+  tbox_pass<NR>(L, w, BsT, x, y, off, &xy, &yy);
+  xy = block_sum(xy, sh);
+  yy = block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = xy;
+    part[2 * blockIdx.x + 1] = yy;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->lam = a;
+      st->ynorm = sqrt(b);
+      if (st->ynorm == 0.0) {
+        st->lam = 0.0;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_tbox_apply(int L, int w, const double* __restrict__ BsT,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+  extern __shared__ int off[];
+  build_offsets(NR, w, L + 2 * w, off);
+  double xy, yy;
+  tbox_pass<NR>(L, w, BsT, x, y, off, &xy, &yy);
+}
+
 // ---------------------------------------------------------------------------
 // K9 transfers
 // ---------------------------------------------------------------------------
@@ -534,7 +869,7 @@ __global__ void k_vadd(long long n, const double* __restrict__ a, const double* 
 
 using namespace gb;
 
-static const int kRedBlocks = 592;  // 4 per SM on 148 SMs; partials sized by the caller
+static const int kRedBlocks = 148 * 8;  // 8 per SM on 148 SMs; partials sized by the caller
 
 static inline int grid_for(long long work, int block, int cap) {
   long long g = (work + block - 1) / block;
@@ -603,6 +938,127 @@ int gbk_pow_iterations(int L, int nr, int w, const double* B, const double* sv,
     k_pow_step<<<gv, 256, 0, s>>>(n, x, y, tol, k, part);
     k_pow_scale<<<gv, 256, 0, s>>>(n, x, y, k);
   }
+  return (int)cudaGetLastError();
+}
+
+
+// ---- v2 (pre-scaled, padded) launchers ----
+int gbk_scale_box(int L, int nr, int w, const double* B, const double* sv, double* Bs,
+                  cudaStream_t s) {
+  const long long total = (long long)L * L * nr * (2 * w + 1) * (2 * w + 1) * nr;
+  k_scale_box<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, nr, w, B, sv, Bs);
+  return (int)cudaGetLastError();
+}
+int gbk_pad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+            cudaStream_t s) {
+  k_pad<<<grid_for((long long)L * L * nr, 256, 148 * 16), 256, 0, s>>>(L, nr, w, src, scale, dst);
+  return (int)cudaGetLastError();
+}
+int gbk_unpad(int L, int nr, int w, const double* src, const double* scale, double* dst,
+              cudaStream_t s) {
+  k_unpad<<<grid_for((long long)L * L * nr, 256, 148 * 16), 256, 0, s>>>(L, nr, w, src, scale, dst);
+  return (int)cudaGetLastError();
+}
+static inline size_t off_smem(int nr, int w) {
+  return (size_t)(2 * w + 1) * (2 * w + 1) * nr * sizeof(int);
+}
+static inline int point_grid(int L) {
+  return grid_for((long long)L * L * 32, 256, kRedBlocks);
+}
+int gbk_pcg_iterations(int L, int nr, int w, const double* Bs, double* x, double* r,
+                       double* p, double* Ap, int iters, void* st, double* part,
+                       cudaStream_t s) {
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * nr;
+  const int gs = point_grid(L);
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  const size_t sm = off_smem(nr, w);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    if (nr == 3) k_pcg_spmv<3><<<gs, 256, sm, s>>>(L, w, Bs, p, Ap, k, part);
+    else k_pcg_spmv<1><<<gs, 256, sm, s>>>(L, w, Bs, p, Ap, k, part);
+    k_cg_update<<<gv, 256, 0, s>>>(npad, x, r, p, Ap, k, part);
+    k_cg_dir<<<gv, 256, 0, s>>>(npad, r, p, k);
+  }
+  return (int)cudaGetLastError();
+}
+int gbk_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, double* y,
+                        double tol, int iters, void* st, double* part, cudaStream_t s) {
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * nr;
+  const int gs = point_grid(L);
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  const size_t sm = off_smem(nr, w);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    if (nr == 3) k_ppow_apply<3><<<gs, 256, sm, s>>>(L, w, Bs, x, y, k, part);
+    else k_ppow_apply<1><<<gs, 256, sm, s>>>(L, w, Bs, x, y, k, part);
+    k_pow_step<<<gv, 256, 0, s>>>(npad, x, y, tol, k, part);
+    k_pow_scale<<<gv, 256, 0, s>>>(npad, x, y, k);
+  }
+  return (int)cudaGetLastError();
+}
+int gbk_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
+                   cudaStream_t s) {
+  const int gs = point_grid(L);
+  const size_t sm = off_smem(nr, w);
+  if (nr == 3) k_pbox_apply<3><<<gs, 256, sm, s>>>(L, w, Bs, x, y);
+  else k_pbox_apply<1><<<gs, 256, sm, s>>>(L, w, Bs, x, y);
+  return (int)cudaGetLastError();
+}
+
+
+// ---- v3 (slot-major) launchers ----
+static inline int row_grid(long long R) { return grid_for(R, 256, kRedBlocks); }
+size_t gbk_boxT_elems(int L, int nr, int w) {
+  const long long R = (long long)L * L * nr;
+  return (size_t)((R + 31) / 32) * 32 * (2 * w + 1) * (2 * w + 1) * nr;
+}
+int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, double* BsT,
+                    cudaStream_t s) {
+  const long long total = (long long)gbk_boxT_elems(L, nr, w);
+  k_scale_box_T<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, nr, w, B, sv, BsT);
+  return (int)cudaGetLastError();
+}
+int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
+                       double* p, double* Ap, int iters, void* st, double* part,
+                       cudaStream_t s) {
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * nr;
+  const int gs = row_grid((long long)L * L * nr);
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  const size_t sm = off_smem(nr, w);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    if (nr == 3) k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
+    else k_tcg_spmv<1><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
+    k_cg_update<<<gv, 256, 0, s>>>(npad, x, r, p, Ap, k, part);
+    k_cg_dir<<<gv, 256, 0, s>>>(npad, r, p, k);
+  }
+  return (int)cudaGetLastError();
+}
+int gbk_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
+                        double tol, int iters, void* st, double* part, cudaStream_t s) {
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * nr;
+  const int gs = row_grid((long long)L * L * nr);
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  const size_t sm = off_smem(nr, w);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    if (nr == 3) k_tpow_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
+    else k_tpow_apply<1><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
+    k_pow_step<<<gv, 256, 0, s>>>(npad, x, y, tol, k, part);
+    k_pow_scale<<<gv, 256, 0, s>>>(npad, x, y, k);
+  }
+  return (int)cudaGetLastError();
+}
+int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
+                   cudaStream_t s) {
+  const int gs = row_grid((long long)L * L * nr);
+  const size_t sm = off_smem(nr, w);
+  if (nr == 3) k_tbox_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
+  else k_tbox_apply<1><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
   return (int)cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@
 // global-memory workspace with the same code.
 #include "gb_common.cuh"
 #include "gb_kernels.h"
+#include "gb_tiled_chol.cuh"
 
 namespace gb {
 
@@ -221,6 +222,222 @@ __global__ void k_correction_patches(int Lp, int wB, const double* __restrict__ 
   }
 }
 
+
+// ===========================================================================
+// v2: tiled DMMA Cholesky in shared memory (gb_tiled_chol.cuh), one CTA per
+// patch.  The gather forms the reference's materialized congruence entry by
+// entry, (x * s_i) * s_j (gamblet_fast.py:136), from the unscaled box.
+// ===========================================================================
+struct TileSmem {
+  double* tl;
+  double* invd;
+  double* z;
+  double* part;
+  int* tij;    // packed (it << 8) | jt per lower tile
+  int* rowg;   // global row of local index l
+  int* ploc;   // packed (a << 8) | b local parent / node coordinates
+  int* flag;
+};
+
+__host__ __device__ __forceinline__ size_t tile_smem_bytes(int Tmax, int nwarps) {
+  const size_t ntile = (size_t)Tmax * (Tmax + 1) / 2 + Tmax;
+  return ntile * 64 * 8 + (size_t)16 * Tmax * 8 + (size_t)8 * nwarps * 8 +
+         (size_t)(Tmax * (Tmax + 1) / 2) * 4 + (size_t)16 * Tmax * 4 + 16;
+}
+
+__device__ __forceinline__ TileSmem carve(double* sm, int Tmax, int nwarps) {
+  TileSmem t;
+  const int ntile = Tmax * (Tmax + 1) / 2 + Tmax;
+  t.tl = sm;
+  t.invd = t.tl + ntile * 64;
+  t.z = t.invd + 8 * Tmax;
+  t.part = t.z + 8 * Tmax;
+  int* ip = reinterpret_cast<int*>(t.part + 8 * nwarps);
+  t.tij = ip;
+  t.rowg = t.tij + Tmax * (Tmax + 1) / 2;
+  t.ploc = t.rowg + 8 * Tmax;
+  t.flag = t.ploc + 8 * Tmax;
+  return t;
+}
+
+__global__ void __launch_bounds__(256) k_correction_patches_v2(
+    int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB, int wG,
+    const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status,
+    int Tmax) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const int nw = blockDim.x >> 5;
+  TileSmem S = carve(sm, Tmax, nw);
+  const int SB = box_slots(wB, 3), SG = box_slots(wG, 1), SD = box_slots(rho, 3);
+  const long long P = (long long)Lp * Lp;
+  for (long long i = blockIdx.x; i < P; i += gridDim.x) {
+    const int si = (int)(i / Lp), ti = (int)(i % Lp);
+    const int s0 = imax(0, si - rho), s1 = imin(Lp - 1, si + rho);
+    const int t0 = imax(0, ti - rho), t1 = imin(Lp - 1, ti + rho);
+    const int nbt = t1 - t0 + 1;
+    const int m = 3 * (s1 - s0 + 1) * nbt;
+    const int T = (m + 7) >> 3;
+    const int nlt = T * (T + 1) / 2;
+    // local tables and the right-hand side s * (-G[:, i])
+    double nrm = 0.0;
+    for (int l = threadIdx.x; l < 8 * T; l += blockDim.x) {
+      double v = 0.0;
+      if (l < m) {
+        const int pl = l / 3, c = l - 3 * pl;
+        const int a = pl / nbt, b = pl - a * nbt;
+        const int ps = s0 + a, pt = t0 + b;
+        const long long r = ((long long)ps * Lp + pt) * 3 + c;
+        S.rowg[l] = (int)r;
+        S.ploc[l] = (a << 8) | b;
+        const int ds = si - ps, dt = ti - pt;
+        double g = 0.0;
+        if (ds >= -wG && ds <= wG && dt >= -wG && dt <= wG)
+          g = G[r * SG + slot_of(wG, 1, ds, dt, 0)];
+        v = sB[r] * (-g);
+      }
+      S.z[l] = v;
+      nrm += v * v;
+    }
+    for (int t = threadIdx.x; t < nlt; t += blockDim.x) {
+      int it = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((it + 1) * (it + 2) / 2 <= t) ++it;
+      while (it * (it + 1) / 2 > t) --it;
+      S.tij[t] = (it << 8) | (t - it * (it + 1) / 2);
+    }
+    nrm = block_sum(nrm, red);  // also orders the table writes
+    double* drow = Dt + i * SD;
+    if (nrm == 0.0) {  // gamblet_fast.py:561-562: empty correction column
+      for (int e = threadIdx.x; e < SD; e += blockDim.x) drow[e] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    // gather (S B S)[chi, chi] lower tiles + RHS tile row
+    for (int e = threadIdx.x; e < nlt * 64; e += blockDim.x) {
+      const int t = e >> 6, w = e & 63;
+      const int ij = S.tij[t];
+      const int r = w >> 3, c = w & 7;
+      const int l1 = ((ij >> 8) << 3) + r, l2 = ((ij & 255) << 3) + c;
+      double v = 0.0;
+      if (l1 < m && l2 < m) {
+        const int p1 = S.ploc[l1 / 3 * 3], p2 = S.ploc[l2 / 3 * 3];
+        const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
+        if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
+          v = B[(long long)S.rowg[l1] * SB + slot_of(wB, 3, ds, dt, l2 % 3)] *
+              sB[S.rowg[l1]] * sB[S.rowg[l2]];
+      } else if (l1 == l2) {
+        v = 1.0;
+      }
+      S.tl[t * 64 + eidx(r, c)] = v;
+    }
+    for (int e = threadIdx.x; e < T * 64; e += blockDim.x) {
+      const int jt = e >> 6, w = e & 63;
+      const int r = w >> 3, c = w & 7;
+      S.tl[(nlt + jt) * 64 + eidx(r, c)] = (r == 0) ? S.z[jt * 8 + c] : 0.0;
+    }
+    __syncthreads();
+    if (!tiled_chol_fwd(S.tl, T, S.invd, S.flag)) {
+      if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
+      __syncthreads();
+      continue;
+    }
+    tiled_back_subst(S.tl, T, S.invd, S.z, S.part);
+    // D = s z and the row-tail trim of this column of D
+    double mx = 0.0;
+    for (int l = threadIdx.x; l < m; l += blockDim.x) {
+      const double v = sB[S.rowg[l]] * S.z[l];
+      S.z[l] = v;
+      mx = fmax(mx, fabs(v));
+    }
+    mx = block_max(mx, red);
+    const double thr = 1e-11 * mx;
+    for (int e = threadIdx.x; e < SD; e += blockDim.x) {
+      const int c = e % 3, bs = e / 3;
+      const int ps = si + bs / (2 * rho + 1) - rho, pt = ti + bs % (2 * rho + 1) - rho;
+      double v = 0.0;
+      if (ps >= s0 && ps <= s1 && pt >= t0 && pt <= t1) {
+        v = S.z[((ps - s0) * nbt + (pt - t0)) * 3 + c];
+        if (!(fabs(v) >= thr)) v = 0.0;
+      }
+      drow[e] = v;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) k_mass_patches_v2(
+    int n, int wM, const double* __restrict__ M, const double* __restrict__ s, int rho,
+    int wd, double* __restrict__ psi, long long* status, int Tmax) {
+  extern __shared__ double sm[];
+  const int nw = blockDim.x >> 5;
+  TileSmem S = carve(sm, Tmax, nw);
+  const int SM = box_slots(wM, 1);
+  const long long N = (long long)n * n;
+  for (long long i = blockIdx.x; i < N; i += gridDim.x) {
+    const int si = (int)(i / n), ti = (int)(i % n);
+    const int s0 = imax(0, si - rho), s1 = imin(n - 1, si + rho);
+    const int t0 = imax(0, ti - rho), t1 = imin(n - 1, ti + rho);
+    const int nt = t1 - t0 + 1, m = (s1 - s0 + 1) * nt;
+    const int T = (m + 7) >> 3;
+    const int nlt = T * (T + 1) / 2;
+    const int li = (si - s0) * nt + (ti - t0);
+    for (int l = threadIdx.x; l < 8 * T; l += blockDim.x) {
+      if (l < m) {
+        const int a = l / nt, b = l - a * nt;
+        S.rowg[l] = (s0 + a) * n + (t0 + b);
+        S.ploc[l] = (a << 8) | b;
+      }
+    }
+    for (int t = threadIdx.x; t < nlt; t += blockDim.x) {
+      int it = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((it + 1) * (it + 2) / 2 <= t) ++it;
+      while (it * (it + 1) / 2 > t) --it;
+      S.tij[t] = (it << 8) | (t - it * (it + 1) / 2);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nlt * 64; e += blockDim.x) {
+      const int t = e >> 6, w = e & 63;
+      const int ij = S.tij[t];
+      const int r = w >> 3, c = w & 7;
+      const int l1 = ((ij >> 8) << 3) + r, l2 = ((ij & 255) << 3) + c;
+      double v = 0.0;
+      if (l1 < m && l2 < m) {
+        const int p1 = S.ploc[l1], p2 = S.ploc[l2];
+        const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
+        if (ds >= -wM && ds <= wM && dt >= -wM && dt <= wM)
+          v = M[(long long)S.rowg[l1] * SM + slot_of(wM, 1, ds, dt, 0)] * s[S.rowg[l1]] *
+              s[S.rowg[l2]];
+      } else if (l1 == l2) {
+        v = 1.0;
+      }
+      S.tl[t * 64 + eidx(r, c)] = v;
+    }
+    for (int e = threadIdx.x; e < T * 64; e += blockDim.x) {
+      const int jt = e >> 6, w = e & 63;
+      const int r = w >> 3, c = w & 7;
+      S.tl[(nlt + jt) * 64 + eidx(r, c)] = (r == 0 && jt * 8 + c == li) ? s[i] : 0.0;
+    }
+    __syncthreads();
+    if (!tiled_chol_fwd(S.tl, T, S.invd, S.flag)) {
+      if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
+      __syncthreads();
+      continue;
+    }
+    tiled_back_subst(S.tl, T, S.invd, S.z, S.part);
+    const int os = clampi(si - rho, 0, n - wd), ot = clampi(ti - rho, 0, n - wd);
+    double* row = psi + i * (long long)wd * wd;
+    for (int e = threadIdx.x; e < wd * wd; e += blockDim.x) {
+      const int fs = os + e / wd, ft = ot + e % wd;
+      double v = 0.0;
+      if (fs >= s0 && fs <= s1 && ft >= t0 && ft <= t1) {
+        const int l = (fs - s0) * nt + (ft - t0);
+        v = s[(long long)fs * n + ft] * S.z[l];
+      }
+      row[e] = v;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace gb
 
 using namespace gb;
@@ -279,5 +496,38 @@ int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB,
   int g = blocks > 0 ? blocks : (int)(P < 148 * 8 ? P : 148 * 8);
   k_correction_patches<<<g, 256, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt, status,
                                              gws, use_gmem, nmax);
+  return (int)cudaGetLastError();
+}
+
+// v2 entry points: pre-scaled boxes, shared-memory tiled DMMA Cholesky.
+// Return 1 (caller falls back to v1) when the patch does not fit.
+int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB, int wG,
+                              const double* G, int rho, double* Dt, long long* status,
+                              cudaStream_t st) {
+  const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
+  const int Tmax = (nmax + 7) / 8;
+  const size_t smem = tile_smem_bytes(Tmax, 8);
+  if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
+  cudaFuncSetAttribute(k_correction_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const long long P = (long long)Lp * Lp;
+  int per_sm = (int)((228 * 1024) / (smem + 1024));
+  if (per_sm < 1) per_sm = 1;
+  int g = (int)(P < 148LL * per_sm * 4 ? P : 148LL * per_sm * 4);
+  k_correction_patches_v2<<<g, 256, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt, status, Tmax);
+  return (int)cudaGetLastError();
+}
+
+int gbk_mass_patches_v2(int n, int wM, const double* M, const double* s, int rho, int wd,
+                        double* psi, long long* status, cudaStream_t st) {
+  const int nmax = (2 * rho + 1) * (2 * rho + 1);
+  const int Tmax = (nmax + 7) / 8;
+  const size_t smem = tile_smem_bytes(Tmax, 4);
+  if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
+  cudaFuncSetAttribute(k_mass_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const long long N = (long long)n * n;
+  int g = (int)(N < 148LL * 64 ? N : 148LL * 64);
+  k_mass_patches_v2<<<g, 128, smem, st>>>(n, wM, M, s, rho, wd, psi, status, Tmax);
   return (int)cudaGetLastError();
 }

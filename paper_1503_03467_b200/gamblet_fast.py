@@ -344,89 +344,126 @@ class _Krylov:
         return dv.to_host(self.state).view(_KSTATE)[0]
 
 
-def _cg(box, s, mode, b, rel_tol, x0=None, max_iter=None, kr=None):
-    """sparse_core.py:126-165 on the device.  Returns
-    (x, iterations, rel_residual, converged, breakdown_iteration)."""
-    n = box.rows
+class _POp:
+    """S B S in slot-major layout (the reference's materialized congruence,
+    gamblet_fast.py:123-139) on zero-halo padded vectors: csrc v3 SpMV."""
+
+    def __init__(self, box, s):
+        self.L, self.nr, self.w = box.L, box.nr, box.w
+        self.n = box.rows
+        self.slots = box.slots
+        self.Lpad = self.L + 2 * self.w
+        self.npad = self.Lpad * self.Lpad * self.nr
+        self.BsT = dv.empty(nat.query("gb_boxT_elems", self.L, self.nr, self.w))
+        nat.call("gb_scale_box_T", self.L, self.nr, self.w, dv.ptr(box.vals), dv.ptr(s),
+                 dv.ptr(self.BsT), dv.stream())
+
+    @property
+    def spmv_bytes(self):
+        return 8 * self.n * self.slots + 3 * 8 * self.npad
+
+    def vec(self):
+        return dv.zeros(self.npad)
+
+    def pad(self, x, scale=None):
+        out = self.vec()
+        nat.call("gb_pad", self.L, self.nr, self.w, dv.ptr(x), dv.ptr(scale), dv.ptr(out),
+                 dv.stream())
+        return out
+
+    def unpad(self, xp, scale=None):
+        out = dv.empty(self.n)
+        nat.call("gb_unpad", self.L, self.nr, self.w, dv.ptr(xp), dv.ptr(scale), dv.ptr(out),
+                 dv.stream())
+        return out
+
+    def apply(self, xp, yp):
+        nat.call("gb_tbox_apply", self.L, self.nr, self.w, dv.ptr(self.BsT), dv.ptr(xp),
+                 dv.ptr(yp), dv.stream())
+
+
+def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
+    """sparse_core.py:126-165 on the device, padded vectors.  Returns
+    (x, iterations, rel_residual, converged, breakdown_iteration, state)."""
     if max_iter is None:
-        max_iter = max(200, 2 * n)
-    kr = kr or _Krylov(n)
+        max_iter = max(200, 2 * op.n)
+    kr = kr or _Krylov(op.npad)
     st = dv.stream()
-    x, r, p, Ap = (dv.empty(n) for _ in range(4))
+    x, r, p, Ap = op.vec(), op.vec(), op.vec(), op.vec()
     nat.call("gb_state_reset", dv.ptr(kr.state), max_iter, st)
     Ax0 = None
     if x0 is not None:
-        Ax0 = dv.empty(n)
-        nat.call("gb_box_apply", box.L, box.nr, box.w, dv.ptr(box.vals), dv.ptr(s), mode,
-                 dv.ptr(x0), dv.ptr(Ax0), st)
-    nat.call("gb_cg_init", n, dv.ptr(b), dv.ptr(x0), dv.ptr(Ax0), dv.ptr(x), dv.ptr(r),
-             dv.ptr(p), float(rel_tol), int(max_iter), dv.ptr(kr.state), dv.ptr(kr.part), st)
-    chunk = 4
+        Ax0 = op.vec()
+        op.apply(x0, Ax0)
+    nat.call("gb_cg_init", op.npad, dv.ptr(b), dv.ptr(x0), dv.ptr(Ax0), dv.ptr(x),
+             dv.ptr(r), dv.ptr(p), float(rel_tol), int(max_iter), dv.ptr(kr.state),
+             dv.ptr(kr.part), st)
+    chunk = 8
     while True:
-        nat.call("gb_cg_iterations", box.L, box.nr, box.w, dv.ptr(box.vals), dv.ptr(s),
-                 mode, dv.ptr(x), dv.ptr(r), dv.ptr(p), dv.ptr(Ap), chunk, dv.ptr(kr.state),
-                 dv.ptr(kr.part), st)
+        nat.call("gb_tcg_iterations", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(r),
+                 dv.ptr(p), dv.ptr(Ap), chunk, dv.ptr(kr.state), dv.ptr(kr.part), st)
         h = kr.read()
         if h["done"]:
             break
-        chunk = min(2 * chunk, 64)
+        chunk = min(2 * chunk, 128)
     rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
     return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
 
 
-def _eig_extremes(box, s, tol=0.1, max_iter=500, seed=24337):
-    """(lambda_min, lambda_max) of S B S (mode 0 operator) exactly as
-    sparse_core.py:232-278: power iteration, then inverse iteration with
-    warm-started inner CG; start vectors from numpy default_rng(seed).
-    Returns (lam_min, lam_max, operator applications)."""
-    n = box.rows
+def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
+    """(lambda_min, lambda_max) of S B S exactly as sparse_core.py:232-278:
+    power iteration, then inverse iteration with warm-started inner CG;
+    start vectors from numpy default_rng(seed).  Returns (lam_min, lam_max,
+    operator applications)."""
+    n = op.n
     st = dv.stream()
     rng = np.random.default_rng(seed)
     x1 = rng.standard_normal(n)
     x2 = rng.standard_normal(n)
-    kr = _Krylov(n)
+    kr = _Krylov(op.npad)
     calls = 0
-    x = dv.to_dev(x1)
-    y = dv.empty(n)
-    nat.call("gb_dot2", n, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots), dv.ptr(kr.state),
-             dv.ptr(kr.part), st)
-    nat.call("gb_scale_by_norm", n, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
+    x = op.pad(dv.to_dev(x1))
+    y = op.vec()
+    nat.call("gb_dot2", op.npad, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots),
+             dv.ptr(kr.state), dv.ptr(kr.part), st)
+    nat.call("gb_scale_by_norm", op.npad, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
     nat.call("gb_state_reset", dv.ptr(kr.state), max_iter, st)
-    chunk = 4
+    chunk = 8
     while True:
-        nat.call("gb_pow_iterations", box.L, box.nr, box.w, dv.ptr(box.vals), dv.ptr(s), 0,
-                 dv.ptr(x), dv.ptr(y), float(tol), chunk, dv.ptr(kr.state),
-                 dv.ptr(kr.part), st)
+        nat.call("gb_tpow_iterations", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(y),
+                 float(tol), chunk, dv.ptr(kr.state), dv.ptr(kr.part), st)
         h = kr.read()
         if h["done"]:
             break
-        chunk = min(2 * chunk, 64)
+        chunk = min(2 * chunk, 128)
     lam_max = float(h["lam"])
     calls += int(h["it"]) + (0 if h["ynorm"] != 0 else 1)
 
     inner = max(1e-12, 1e-3 * tol)
-    x = dv.to_dev(x2)
-    nat.call("gb_dot2", n, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots), dv.ptr(kr.state),
-             dv.ptr(kr.part), st)
-    nat.call("gb_scale_by_norm", n, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
+    x = op.pad(dv.to_dev(x2))
+    nat.call("gb_dot2", op.npad, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots),
+             dv.ptr(kr.state), dv.ptr(kr.part), st)
+    nat.call("gb_scale_by_norm", op.npad, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
     lam_min, lam_prev, y_prev = lam_max, np.inf, None
-    ykr = _Krylov(n)
+    ykr = _Krylov(op.npad)
     dots = dv.empty(4)
+    outer = []
     for _ in range(max_iter):
-        yv, its, _, _, brk, _ = _cg(box, s, 0, x, inner, x0=y_prev, kr=ykr)
+        yv, its, _, _, brk, _ = _cg(op, x, inner, x0=y_prev, kr=ykr)
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")
+        outer.append(its)
         calls += its + (1 if y_prev is not None else 0)
-        nat.call("gb_dot2", n, dv.ptr(yv), dv.ptr(yv), None, dv.ptr(dots),
+        nat.call("gb_dot2", op.npad, dv.ptr(yv), dv.ptr(yv), None, dv.ptr(dots),
                  dv.ptr(kr.state), dv.ptr(kr.part), st)
-        xn, yp = dv.empty(n), dv.empty(n)
-        nat.call("gb_scale_by_norm", n, dv.ptr(yv), dv.ptr(dots), 0, dv.ptr(xn), dv.ptr(yp), st)
-        Ax = dv.empty(n)
-        nat.call("gb_box_apply", box.L, box.nr, box.w, dv.ptr(box.vals), dv.ptr(s), 0,
-                 dv.ptr(xn), dv.ptr(Ax), st)
+        xn, yp = op.vec(), op.vec()
+        nat.call("gb_scale_by_norm", op.npad, dv.ptr(yv), dv.ptr(dots), 0, dv.ptr(xn),
+                 dv.ptr(yp), st)
+        Ax = op.vec()
+        op.apply(xn, Ax)
         calls += 1
-        nat.call("gb_dot2", n, dv.ptr(xn), dv.ptr(Ax), None, dv.ptr(dots[2:]),
+        nat.call("gb_dot2", op.npad, dv.ptr(xn), dv.ptr(Ax), None, dv.ptr(dots[2:]),
                  dv.ptr(kr.state), dv.ptr(kr.part), st)
         d = dv.to_host(dots)
         if d[0] == 0.0:
@@ -436,7 +473,11 @@ def _eig_extremes(box, s, tol=0.1, max_iter=500, seed=24337):
         if abs(lam_min - lam_prev) <= 0.5 * tol * abs(lam_min):
             break
         lam_prev = lam_min
+    _SPECTRAL_LOG.append({"n": n, "power": int(h["it"]), "inner": outer})
     return lam_min, lam_max, calls
+
+
+_SPECTRAL_LOG = []
 
 
 # ---------------------------------------------------------------------------
@@ -490,12 +531,8 @@ def _level_q(M, A, tree, rho, ctx, counter):
     wd = PsiWindows.window(n, lo, hi)
     psi = dv.empty(N * wd * wd)
     nmax = (2 * rho + 1) ** 2
-    blocks = _blocks_for(nmax, N)
-    wsb = nat.query("gb_mass_patch_workspace", rho, blocks)
-    ws = dv.empty(wsb // 8) if wsb else None
     with dv.phase("mass_patches"):
-        nat.call("gb_mass_patches", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd,
-                 dv.ptr(psi), ctx.st(ctx.slot("mass", "mass")), dv.ptr(ws), blocks, s)
+        _mass_patches(n, Mb, sM, rho, wd, psi, ctx.st(ctx.slot("mass", "mass")), s)
     dv.Prof.add_work("mass_patches", flops=_patch_flops(n, rho, 1))
     wX = min(rho + Ab.w, n - 1)
     X = dv.empty(N * dv.box_slots(wX, 1))
@@ -519,6 +556,40 @@ def _level_q(M, A, tree, rho, ctx, counter):
     counter.add("line5", 2 * N * dv.box_slots(wX, 1) * 9 + 2 * N * dv.box_slots(wR, 1) * nmax)
     counter.add("scaling", 2 * N * dv.box_slots(Mb.w, 1) + N + 3 * N * dv.box_slots(wR, 1))
     return (PsiWindows(psi, n, n, lo, hi), BoxMatrix(Aq, n, 1, wR, 1), i)
+
+
+def _mass_patches(n, Mb, sM, rho, wd, psi, status_ptr, s):
+    """K1 on the pre-scaled S M S box: the shared-memory tiled DMMA Cholesky
+    (v2); patches larger than shared memory use the global-workspace v1."""
+    try:
+        nat.call("gb_mass_patches_v2", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd,
+                 dv.ptr(psi), status_ptr, s)
+        return
+    except InvalidArgumentError:
+        pass
+    nmax = (2 * rho + 1) ** 2
+    blocks = _blocks_for(nmax, n * n)
+    wsb = nat.query("gb_mass_patch_workspace", rho, blocks)
+    ws = dv.empty(wsb // 8) if wsb else None
+    nat.call("gb_mass_patches", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd, dv.ptr(psi),
+             status_ptr, dv.ptr(ws), blocks, s)
+
+
+def _correction_patches(Lp, B, op, sB, Gv, rho, Dt, status_ptr, s):
+    """K4: v2 (tiled DMMA Cholesky in shared memory on S B S) when the patch
+    fits, else the global-workspace v1."""
+    try:
+        nat.call("gb_correction_patches_v2", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w,
+                 dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, s)
+        return
+    except InvalidArgumentError:
+        pass
+    nmax = 3 * (2 * rho + 1) ** 2
+    blocks = _blocks_for(nmax, Lp * Lp)
+    wsb = nat.query("gb_correction_workspace", rho, blocks)
+    ws = dv.empty(wsb // 8) if wsb else None
+    nat.call("gb_correction_patches", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w, dv.ptr(Gv),
+             rho, dv.ptr(Dt), status_ptr, dv.ptr(ws), blocks, s)
 
 
 def _patch_flops(L, rho, comps):
@@ -545,12 +616,7 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
     rho = int(min(int(np.floor(rho)), n - 1))
     wd = PsiWindows.window(n, -rho, rho)
     psi = dv.empty(N * wd * wd)
-    nmax = (2 * rho + 1) ** 2
-    blocks = _blocks_for(nmax, N)
-    wsb = nat.query("gb_mass_patch_workspace", rho, blocks)
-    ws = dv.empty(wsb // 8) if wsb else None
-    nat.call("gb_mass_patches", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd, dv.ptr(psi),
-             ctx.st(ctx.slot("mass", "mass")), dv.ptr(ws), blocks, ctx.s)
+    _mass_patches(n, Mb, sM, rho, wd, psi, ctx.st(ctx.slot("mass", "mass")), ctx.s)
     ctx.check()
     counter.add("line2a", _patch_flops(n, rho, 1))
     return PsiWindows(psi, n, n, -rho, rho).to_csr()
@@ -600,9 +666,12 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         counter.add("scaling", 2 * J * dv.box_slots(wB, 3) + J)
 
         # K7: spectral extremes of S B S (gamblet_fast.py:531-534)
+        with dv.phase("level_blocks"):
+            op = _POp(B, sB)
         if SPECTRAL:
             with dv.phase("spectral"):
-                lam_min, lam_max, calls = _eig_extremes(B, sB)
+                lam_min, lam_max, calls = _eig_extremes(op)
+            dv.Prof.add_work("spectral", nbytes=calls * op.spmv_bytes)
         else:
             lam_min = lam_max = None
             calls = 0
@@ -610,16 +679,10 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
 
         # K4: correction patches -> D^T with the row-tail trim fused
         Dt = dv.empty(P * dv.box_slots(rho, 3))
-        nmax = 3 * (2 * rho + 1) ** 2
-        blocks = _blocks_for(nmax, P)
-        wsb = nat.query("gb_correction_workspace", rho, blocks)
-        ws = dv.empty(wsb // 8) if wsb else None
         with dv.phase("correction_patches"):
-            nat.call("gb_correction_patches", Lp, wB, dv.ptr(Bv), dv.ptr(sB), wB, dv.ptr(Gv),
-                     rho, dv.ptr(Dt), ctx.st(ctx.slot("corr", f"level {k}", detail=k)),
-                     dv.ptr(ws), blocks, s)
+            _correction_patches(Lp, B, op, sB, Gv, rho, Dt,
+                                ctx.st(ctx.slot("corr", f"level {k}", detail=k)), s)
         dv.Prof.add_work("correction_patches", flops=_patch_flops(Lp, rho, 3))
-        del ws
         counter.add("line11", _patch_flops(Lp, rho, 3))
         counter.record_solve(f"line11 level {k}", 1, 0.0, stages=1)
 
@@ -676,6 +739,7 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
     level.w_variant = w_variant
     level.subband = B
     level.subband_scale = sB
+    level._op = op
     level.correction = BoxMatrix(Dt, Lp, 1, rho, 3, kind=EXP_TDT)
     level.restriction = BoxMatrix(Rv, Lp, 1, rho, 4, kind=EXP_CHILD)
     level.lambda_min_subband = lam_min
@@ -795,19 +859,19 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
         w12 = w_template(lvl.w_variant or "orthonormal").ctypes.data
         Lp = B.L
         J = B.rows
+        op = getattr(lvl, "_op", None) or _POp(B, sB)
         rhs = dv.empty(J)
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
         counter.add("line8", 8 * J + J)
         with dv.phase("subband_cg"):
-            z, its, rel, conv, brk, _ = _cg(B, sB, 1, rhs, tol)
-        dv.Prof.add_work("subband_cg", nbytes=its * (8 * J * B.slots + 6 * 8 * J))
+            zp, its, rel, conv, brk, _ = _cg(op, op.pad(rhs), tol)
+        dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 6 * 8 * op.npad))
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")
         if not conv:
             raise NumericalError(f"subband solve at level {k} did not converge")
-        w = dv.empty(J)
-        nat.call("gb_vmul", J, dv.ptr(sB), dv.ptr(z), dv.ptr(w), s)
+        w = op.unpad(zp, sB)
         counter.add("line8", cg_flops(J * B.slots, J, its) + 2 * J * its)
         counter.record_iters("line8", its)
         counter.record_solve(f"line8 level {k}", its, tol)
@@ -833,16 +897,14 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
     s1 = dv.empty(4)
     st = dv.zeros(2, torch.int64)
     nat.call("gb_box_scale", 4, 1, A1.w, dv.ptr(A1.vals), dv.ptr(s1), dv.ptr(st), s)
-    rhs = dv.empty(4)
-    nat.call("gb_vmul", 4, dv.ptr(s1), dv.ptr(g), dv.ptr(rhs), s)
-    z, its, rel, conv, brk, _ = _cg(A1, s1, 1, rhs, tol)
+    op1 = _POp(A1, s1)
+    zp, its, rel, conv, brk, _ = _cg(op1, op1.pad(g, s1), tol)
     if brk:
         raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                              "(matrix is not SPD)")
     if not conv:
         raise NumericalError("coarse solve did not converge")
-    U1 = dv.empty(4)
-    nat.call("gb_vmul", 4, dv.ptr(s1), dv.ptr(z), dv.ptr(U1), s)
+    U1 = op1.unpad(zp, s1)
     counter.add("line16", cg_flops(4 * A1.slots, 4, its))
     counter.record_iters("line16", its)
     counter.record_solve("line16", its, tol)

@@ -36,16 +36,14 @@ for k in range(q, 0, -1):
         cmp(f"R{k}", g.restriction, o["restriction"])
 # CG on our B^(q)
 B = levels[q].raw("subband"); sB = levels[q].raw("subband_scale")
+op = gf._POp(B, sB)
 n = B.rows
 x = np.random.default_rng(0).standard_normal(n)
-xd = dv.to_dev(x); y = dv.empty(n)
-nat.call("gb_box_apply", B.L, B.nr, B.w, dv.ptr(B.vals), dv.ptr(sB), 0, dv.ptr(xd), dv.ptr(y), dv.stream())
+xp = op.pad(dv.to_dev(x)); yp = op.vec()
+op.apply(xp, yp)
 _, Bs = O.diag_scale(lv[q]["subband"])
-print("box_apply mode0 err", np.abs(y.cpu().numpy() - Bs @ x).max() / np.abs(Bs @ x).max())
-nat.call("gb_box_apply", B.L, B.nr, B.w, dv.ptr(B.vals), dv.ptr(sB), 1, dv.ptr(xd), dv.ptr(y), dv.stream())
-print("box_apply mode1 err", np.abs(y.cpu().numpy() - Bs @ x).max() / np.abs(Bs @ x).max())
-z, its, rel, conv, brk, h = gf._cg(B, sB, 0, xd, 1e-10)
-print("cg", its, rel, conv, brk, "err", np.abs(Bs @ z.cpu().numpy() - x).max())
-z, its, rel, conv, brk, h = gf._cg(B, sB, 0, xd, 1e-10, x0=dv.to_dev(0.5 * x))
-print("cg warm", its, rel, conv, brk, "err", np.abs(Bs @ z.cpu().numpy() - x).max())
-print("eig", gf._eig_extremes(B, sB)[:2], O.eig_extremes(Bs))
+y = op.unpad(yp).cpu().numpy()
+print("pbox_apply err", np.abs(y - Bs @ x).max() / np.abs(Bs @ x).max())
+z, its, rel, conv, brk, h = gf._cg(op, xp, 1e-10)
+print("cg", its, rel, conv, brk, "err", np.abs(Bs @ op.unpad(z).cpu().numpy() - x).max())
+print("eig", gf._eig_extremes(op)[:2], O.eig_extremes(Bs))
