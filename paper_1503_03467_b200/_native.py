@@ -67,6 +67,9 @@ _SIGS = {
     "gb_tcg_iterations": ([_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
     "gb_tpow_iterations": ([_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P], _I),
     "gb_tbox_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_bj_setup": ([_I, _I, _P, _P, _P, _P], _I),
+    "gb_bjcg_init": ([_I, _I, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_bjcg_iterations": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
     "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),
     "gb_box_apply": ([_I, _I, _I, _P, _P, _I, _P, _P, _P], _I),

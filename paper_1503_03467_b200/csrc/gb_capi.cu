@@ -282,6 +282,27 @@ int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, doub
   COUNT(1);
   return wrap(gbk_tbox_apply(L, nr, w, BsT, x, y, ST(stream)), "tbox_apply");
 }
+int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream) {
+  if (L < 2 || (L & 1)) return invalid("bj_setup: parent grid side must be even");
+  COUNT(1);
+  return wrap(gbk_bj_setup(L, w, B, s, inv, ST(stream)), "bj_setup");
+}
+int gb_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
+                 const double* inv, double rel_tol, int max_iter, void* state,
+                 double* partials, void* stream) {
+  COUNT(1);
+  return wrap(gbk_bjcg_init(L, w, b, x, r, p, z, inv, rel_tol, max_iter, state, partials,
+                            ST(stream)),
+              "bjcg_init");
+}
+int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
+                       double* r, double* p, double* Ap, double* z, int iters, void* state,
+                       double* partials, void* stream) {
+  COUNT(3 * (unsigned long long)iters);
+  return wrap(gbk_bjcg_iterations(L, w, BsT, inv, x, r, p, Ap, z, iters, state, partials,
+                                  ST(stream)),
+              "bjcg_iterations");
+}
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {
   COUNT(1);

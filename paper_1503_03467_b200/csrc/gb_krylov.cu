@@ -432,8 +432,9 @@ __global__ void k_unpad(int L, int nr, int w, const double* __restrict__ src,
 
 __device__ __forceinline__ void build_offsets(int nr, int w, int Lpad, int* off) {
   const int W2 = 2 * w + 1, S = W2 * W2 * nr;
-  for (int j = threadIdx.x; j < S; j += blockDim.x) {
-    const int c = j % nr, bs = j / nr;
+  for (int j = threadIdx.x; j < S + 1; j += blockDim.x) {
+    const int jj = j < S ? j : 0;  // pad slot (value 0) points at a valid entry
+    const int c = jj % nr, bs = jj / nr;
     off[j] = ((bs / W2) * Lpad + (bs % W2)) * nr + c;
   }
   __syncthreads();
@@ -571,21 +572,21 @@ __global__ void __launch_bounds__(256) k_pbox_apply(int L, int w, const double* 
 // unrollable loops.  The slot -> relative x offset table is in shared memory
 // (every thread reads the same entry: broadcast).
 // ---------------------------------------------------------------------------
-__global__ void k_scale_box_T(int L, int nr, int w, const double* __restrict__ B,
-                              const double* __restrict__ s, double* __restrict__ BsT) {
-  // blocked slot-major: BsT[(r / 32) * S * 32 + j * 32 + (r % 32)]
+// strided fallback (boxes too wide for the shared-memory transpose)
+__global__ void k_scale_box_T_strided(int L, int nr, int w, const double* __restrict__ B,
+                                      const double* __restrict__ s, double* __restrict__ BsT) {
   const int W2 = 2 * w + 1, S = W2 * W2 * nr;
   const long long R = (long long)L * L * nr;
-  const long long nblk = (R + 31) / 32;
-  const long long total = nblk * S * 32;
+  const int Sp = S + (S & 1);
+  const long long total = (R + 31) / 32 * 32LL * Sp;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long blk = e / (32LL * S);
-    const int rem = (int)(e - blk * 32LL * S);
-    const int j = rem >> 5;
-    const long long r = blk * 32 + (rem & 31);
+    const long long blk = e / (32LL * Sp);
+    const int rem = (int)(e - blk * 32LL * Sp);
+    const int j = ((rem >> 6) << 1) | (rem & 1);
+    const long long r = blk * 32 + ((rem >> 1) & 31);
     double v = 0.0;
-    if (r < R) {
+    if (r < R && j < S) {
       const int cp = j % nr, bs = j / nr;
       const long long p = r / nr;
       const int qs = (int)(p / L) + bs / W2 - w, qt = (int)(p % L) + bs % W2 - w;
@@ -596,20 +597,58 @@ __global__ void k_scale_box_T(int L, int nr, int w, const double* __restrict__ B
   }
 }
 
+// blocked slot-major transpose, one CTA per 32-row block: the 32 rows are
+// contiguous in B (32*S doubles), staged in shared memory, written slot-pair
+// major: BsT[blk*32*Sp + (j/2)*64 + (r%32)*2 + j%2], Sp = S rounded up to even
+// (the pad slot is 0), so a warp reads 512 contiguous bytes per slot pair.
+__global__ void k_scale_box_T(int L, int nr, int w, const double* __restrict__ B,
+                              const double* __restrict__ s, double* __restrict__ BsT) {
+  extern __shared__ double tile[];  // 32 * (S + 1)
+  const int W2 = 2 * w + 1, S = W2 * W2 * nr;
+  const long long R = (long long)L * L * nr;
+  const long long nblk = (R + 31) / 32;
+  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const long long r0 = blk * 32;
+    const int nrow = (int)(R - r0 < 32 ? R - r0 : 32);
+    for (int e = threadIdx.x; e < 32 * S; e += blockDim.x) {
+      const int rl = e / S, j = e - rl * S;
+      tile[rl * (S + 1) + j] = rl < nrow ? B[(r0 + rl) * S + j] : 0.0;
+    }
+    __syncthreads();
+    const int Sp = S + (S & 1);
+    double* out = BsT + blk * 32LL * Sp;
+    for (int e = threadIdx.x; e < 32 * Sp; e += blockDim.x) {
+      // pair layout: e = (j >> 1) * 64 + rl * 2 + (j & 1)
+      const int j = ((e >> 6) << 1) | (e & 1), rl = (e >> 1) & 31;
+      double v = 0.0;
+      if (rl < nrow && j < S) {
+        const long long r = r0 + rl;
+        const int cp = j % nr, bs = j / nr;
+        const long long p = r / nr;
+        const int qs = (int)(p / L) + bs / W2 - w, qt = (int)(p % L) + bs % W2 - w;
+        if (qs >= 0 && qs < L && qt >= 0 && qt < L)
+          v = tile[rl * (S + 1) + j] * s[r] * s[((long long)qs * L + qt) * nr + cp];
+      }
+      out[e] = v;
+    }
+    __syncthreads();
+  }
+}
+
 template <int NR>
 __device__ __forceinline__ double trow_apply(const double* __restrict__ BsT, long long R, int S,
                                              const int* __restrict__ off,
                                              const double* __restrict__ x, long long xb,
                                              long long r) {
-  const double* a = BsT + (r >> 5) * (32LL * S) + (r & 31);
+  const int Sp = S + (S & 1);
+  const double2* a = reinterpret_cast<const double2*>(BsT + (r >> 5) * (32LL * Sp)) + (r & 31);
   double acc0 = 0.0, acc1 = 0.0;
-  int j = 0;
 #pragma unroll 4
-  for (; j + 1 < S; j += 2) {
-    acc0 = fma(__ldg(a + 32 * j), __ldg(x + xb + off[j]), acc0);
-    acc1 = fma(__ldg(a + 32 * (j + 1)), __ldg(x + xb + off[j + 1]), acc1);
+  for (int m = 0; m < (Sp >> 1); ++m) {
+    const double2 v = __ldg(a + 32 * m);
+    acc0 = fma(v.x, __ldg(x + xb + off[2 * m]), acc0);
+    acc1 = fma(v.y, __ldg(x + xb + off[2 * m + 1]), acc1);
   }
-  if (j < S) acc0 = fma(__ldg(a + 32 * j), __ldg(x + xb + off[j]), acc0);
   return acc0 + acc1;
 }
 
@@ -635,6 +674,146 @@ __device__ __forceinline__ void tbox_pass(int L, int w, const double* __restrict
   }
   *xy = d0;
   *yy = d1;
+}
+
+
+// Tiled v4 SpMV for nr = 3 and L % 64 == 0: a CTA owns the 64 parents
+// (ps, pt0..pt0+63) = 192 consecutive rows and stages their x window,
+// (2w+1) padded grid rows x (64 + 2w) columns x 3, in shared memory.
+constexpr int kTileP = 64;
+
+__device__ __forceinline__ void tile_pass(int L, int w, const double* __restrict__ BsT,
+                                          const double* __restrict__ x, double* __restrict__ y,
+                                          const int* offw, double* xs, double* xy, double* yy) {
+  const int W2 = 2 * w + 1, S = W2 * W2 * 3, Sp = S + (S & 1), Lpad = L + 2 * w;
+  const int WC = kTileP + 2 * w;  // window columns (parents)
+  const int tiles_per_row = L / kTileP;
+  const long long ntile = (long long)L * tiles_per_row;
+  double d0 = 0.0, d1 = 0.0;
+  const int tid = threadIdx.x;  // 0..191: local row
+  const int lp = tid / 3, c = tid - 3 * lp;
+  for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int ps = (int)(t / tiles_per_row), pt0 = (int)(t % tiles_per_row) * kTileP;
+    // stage the window: padded rows ps..ps+2w, padded columns pt0..pt0+WC-1
+    for (int e = tid; e < W2 * WC * 3; e += blockDim.x) {
+      const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
+      xs[e] = x[((long long)(ps + wr) * Lpad + pt0) * 3 + rem];
+    }
+    __syncthreads();
+    const long long r = ((long long)ps * L + pt0) * 3 + tid;
+    const double2* a = reinterpret_cast<const double2*>(BsT + (r >> 5) * (32LL * Sp)) + (r & 31);
+    const double* xb = xs + lp * 3;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 4
+    for (int m = 0; m < (Sp >> 1); ++m) {
+      const double2 v = __ldg(a + 32 * m);
+      acc0 = fma(v.x, xb[offw[2 * m]], acc0);
+      acc1 = fma(v.y, xb[offw[2 * m + 1]], acc1);
+    }
+    const double val = acc0 + acc1;
+    const long long yr = ((long long)(ps + w) * Lpad + pt0 + lp + w) * 3 + c;
+    y[yr] = val;
+    d0 += xs[(w * WC + lp + w) * 3 + c] * val;
+    d1 += val * val;
+    __syncthreads();
+  }
+  *xy = d0;
+  *yy = d1;
+}
+
+__device__ __forceinline__ void build_offsets_window(int w, int* off) {
+  const int W2 = 2 * w + 1, S = W2 * W2 * 3, WC = kTileP + 2 * w;
+  for (int j = threadIdx.x; j < S + 1; j += blockDim.x) {
+    const int jj = j < S ? j : 0;
+    const int cc = jj % 3, bs = jj / 3;
+    off[j] = ((bs / W2) * WC + (bs % W2)) * 3 + cc;
+  }
+}
+
+__global__ void __launch_bounds__(192) k_tcg_spmv_tiled(int L, int w,
+                                                        const double* __restrict__ BsT,
+                                                        const double* __restrict__ p,
+                                                        double* __restrict__ Ap, KState* st,
+                                                        double* part) {
+  extern __shared__ double dyn[];
+  __shared__ double sh[32];
+  if (st->done) return;
+  const int S = (2 * w + 1) * (2 * w + 1) * 3;
+  int* offw = reinterpret_cast<int*>(dyn);
+  double* xs = dyn + ((S + 2) / 2 + 1);
+  build_offsets_window(w, offw);
+  __syncthreads();
+  double dot, yy;
+  tile_pass(L, w, BsT, p, Ap, offw, xs, &dot, &yy);
+  dot = block_sum(dot, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = dot;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->pAp = a;
+      if (!(a > 0.0)) {
+        st->breakdown = st->it + 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rs / a;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(192) k_tpow_apply_tiled(int L, int w,
+                                                          const double* __restrict__ BsT,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y, KState* st,
+                                                          double* part) {
+  extern __shared__ double dyn[];
+  __shared__ double sh[32];
+  if (st->done) return;
+  const int S = (2 * w + 1) * (2 * w + 1) * 3;
+  int* offw = reinterpret_cast<int*>(dyn);
+  double* xs = dyn + ((S + 2) / 2 + 1);
+  build_offsets_window(w, offw);
+  __syncthreads();
+  double xy, yy;
+  tile_pass(L, w, BsT, x, y, offw, xs, &xy, &yy);
+  xy = block_sum(xy, sh);
+  yy = block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = xy;
+    part[2 * blockIdx.x + 1] = yy;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->lam = a;
+      st->ynorm = sqrt(b);
+      if (st->ynorm == 0.0) {
+        st->lam = 0.0;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(192) k_tbox_apply_tiled(int L, int w,
+                                                          const double* __restrict__ BsT,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y) {
+  extern __shared__ double dyn[];
+  const int S = (2 * w + 1) * (2 * w + 1) * 3;
+  int* offw = reinterpret_cast<int*>(dyn);
+  double* xs = dyn + ((S + 2) / 2 + 1);
+  build_offsets_window(w, offw);
+  __syncthreads();
+  double xy, yy;
+  tile_pass(L, w, BsT, x, y, offw, xs, &xy, &yy);
 }
 
 template <int NR>
@@ -709,6 +888,201 @@ __global__ void __launch_bounds__(256) k_tbox_apply(int L, int w, const double* 
   build_offsets(NR, w, L + 2 * w, off);
   double xy, yy;
   tbox_pass<NR>(L, w, BsT, x, y, off, &xy, &yy);
+}
+
+
+// ---------------------------------------------------------------------------
+// Block-Jacobi preconditioned CG for the subband systems (S B S) z = rhs.
+// Blocks: the 12 unknowns of each 2x2 group of parents (3 per parent).  The
+// stopping rule is the reference's, ||r||_2 <= tol ||b||_2 on the true
+// residual (sparse_core.py:161); only the iteration path differs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long bj_row_pad(int L, int w, int b, int l) {
+  // block b of the (L/2)^2 block grid, local row l = (i*2 + j)*3 + c
+  const int Lb = L >> 1;
+  const int bs = b / Lb, bt = b - bs * Lb;
+  const int pi = l / 3, c = l - 3 * pi;
+  const int ps = 2 * bs + (pi >> 1), pt = 2 * bt + (pi & 1);
+  const int Lpad = L + 2 * w;
+  return ((long long)(ps + w) * Lpad + (pt + w)) * 3 + c;
+}
+
+// inverse of each 12x12 diagonal block of S B S (Gauss-Jordan, one warp per block)
+__global__ void k_bj_setup(int L, int w, const double* __restrict__ B,
+                           const double* __restrict__ s, double* __restrict__ inv) {
+  __shared__ double M[8][12][25];
+  __shared__ double colk[8][12];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int Lb = L >> 1, nb = Lb * Lb;
+  const int S = box_slots(w, 3);
+  for (int b = blockIdx.x * 8 + wl; b < nb; b += gridDim.x * 8) {
+    const int bs = b / Lb, bt = b - bs * Lb;
+    double (*m)[25] = M[wl];
+    for (int e = lane; e < 144; e += 32) {
+      const int l1 = e / 12, l2 = e % 12;
+      const int p1 = l1 / 3, c1 = l1 % 3, p2 = l2 / 3, c2 = l2 % 3;
+      const int ps1 = 2 * bs + (p1 >> 1), pt1 = 2 * bt + (p1 & 1);
+      const int ps2 = 2 * bs + (p2 >> 1), pt2 = 2 * bt + (p2 & 1);
+      const int ds = ps2 - ps1, dt = pt2 - pt1;
+      const long long r1 = ((long long)ps1 * L + pt1) * 3 + c1;
+      const long long r2 = ((long long)ps2 * L + pt2) * 3 + c2;
+      double v = 0.0;
+      if (ds >= -w && ds <= w && dt >= -w && dt <= w)
+        v = B[r1 * S + slot_of(w, 3, ds, dt, c2)] * s[r1] * s[r2];
+      m[l1][l2] = v;
+      m[l1][12 + l2] = (l1 == l2) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    for (int k = 0; k < 12; ++k) {
+      const double piv = 1.0 / m[k][k];
+      __syncwarp();
+      if (lane < 24) m[k][lane] *= piv;
+      if (lane < 12) colk[wl][lane] = m[lane][k];
+      __syncwarp();
+      for (int e = lane; e < 12 * 24; e += 32) {
+        const int i = e / 24, c = e % 24;
+        if (i != k) m[i][c] -= colk[wl][i] * m[k][c];
+      }
+      __syncwarp();
+    }
+    for (int e = lane; e < 144; e += 32) inv[(long long)b * 144 + e] = m[e / 12][12 + e % 12];
+    __syncwarp();
+  }
+}
+
+// x += alpha p; r -= alpha Ap; z = Minv r; (r.r, r.z) -> convergence, beta
+__global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __restrict__ x,
+                                                     double* __restrict__ r,
+                                                     const double* __restrict__ p,
+                                                     const double* __restrict__ Ap,
+                                                     double* __restrict__ z,
+                                                     const double* __restrict__ inv,
+                                                     KState* st, double* part) {
+  __shared__ double rs[192];
+  __shared__ double sh[32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const int nb = (L >> 1) * (L >> 1);
+  const int lb = threadIdx.x / 12, l = threadIdx.x % 12;
+  double rr = 0.0, rz = 0.0;
+  for (int b0 = blockIdx.x * 16; b0 < nb; b0 += gridDim.x * 16) {
+    const int b = b0 + lb;
+    long long pr = -1;
+    double rv = 0.0;
+    if (b < nb) {
+      pr = bj_row_pad(L, w, b, l);
+      x[pr] += alpha * p[pr];
+      rv = r[pr] - alpha * Ap[pr];
+      r[pr] = rv;
+      rr += rv * rv;
+    }
+    rs[threadIdx.x] = rv;
+    __syncthreads();
+    if (b < nb) {
+      const double* iv = inv + (long long)b * 144 + l * 12;
+      const double* rb = rs + lb * 12;
+      double zv = 0.0;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) zv = fma(iv[k], rb[k], zv);
+      z[pr] = zv;
+      rz += rv * zv;
+    }
+    __syncthreads();
+  }
+  rr = block_sum(rr, sh);
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = rr;
+    part[2 * blockIdx.x + 1] = rz;
+  }
+  if (last_block(&st->counter)) {
+    double a, c;
+    final_sum2(part, gridDim.x, &a, &c, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->it += 1;
+      const double rn = sqrt(a);
+      st->rnorm = rn;
+      if (rn <= st->tol_abs) {
+        st->done = 1;
+        st->converged = 1;
+      } else if (st->it >= st->max_iter) {
+        st->done = 1;
+        st->converged = 0;
+      } else {
+        st->beta = c / st->rs;
+        st->rs = c;
+      }
+    }
+  }
+}
+
+// start (x0 = 0): x = 0, r = b, z = Minv b, p = z; ||b||, r.z
+__global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* __restrict__ b,
+                                                   double* __restrict__ x, double* __restrict__ r,
+                                                   double* __restrict__ p,
+                                                   double* __restrict__ z,
+                                                   const double* __restrict__ inv,
+                                                   double rel_tol, int max_iter, KState* st,
+                                                   double* part) {
+  __shared__ double rs[192];
+  __shared__ double sh[32];
+  const int nb = (L >> 1) * (L >> 1);
+  const int lb = threadIdx.x / 12, l = threadIdx.x % 12;
+  double bb = 0.0, rz = 0.0;
+  for (int b0 = blockIdx.x * 16; b0 < nb; b0 += gridDim.x * 16) {
+    const int bk = b0 + lb;
+    long long pr = -1;
+    double rv = 0.0;
+    if (bk < nb) {
+      pr = bj_row_pad(L, w, bk, l);
+      rv = b[pr];
+      x[pr] = 0.0;
+      r[pr] = rv;
+      bb += rv * rv;
+    }
+    rs[threadIdx.x] = rv;
+    __syncthreads();
+    if (bk < nb) {
+      const double* iv = inv + (long long)bk * 144 + l * 12;
+      const double* rb = rs + lb * 12;
+      double zv = 0.0;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) zv = fma(iv[k], rb[k], zv);
+      z[pr] = zv;
+      p[pr] = zv;
+      rz += rv * zv;
+    }
+    __syncthreads();
+  }
+  bb = block_sum(bb, sh);
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = bb;
+    part[2 * blockIdx.x + 1] = rz;
+  }
+  if (last_block(&st->counter)) {
+    double a, c;
+    final_sum2(part, gridDim.x, &a, &c, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->it = 0;
+      st->breakdown = 0;
+      st->max_iter = max_iter;
+      const double bn = sqrt(a);
+      st->bnorm = bn;
+      st->tol_abs = rel_tol * bn;
+      st->rnorm = bn;
+      st->rs = c;
+      st->done = 0;
+      st->converged = 0;
+      st->aux0 = 0.0;
+      if (bn == 0.0) {
+        st->done = 1;
+        st->converged = 1;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -960,7 +1334,7 @@ int gbk_unpad(int L, int nr, int w, const double* src, const double* scale, doub
   return (int)cudaGetLastError();
 }
 static inline size_t off_smem(int nr, int w) {
-  return (size_t)(2 * w + 1) * (2 * w + 1) * nr * sizeof(int);
+  return ((size_t)(2 * w + 1) * (2 * w + 1) * nr + 2) * sizeof(int);
 }
 static inline int point_grid(int L) {
   return grid_for((long long)L * L * 32, 256, kRedBlocks);
@@ -1010,14 +1384,35 @@ int gbk_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, doub
 
 // ---- v3 (slot-major) launchers ----
 static inline int row_grid(long long R) { return grid_for(R, 256, kRedBlocks); }
+static inline bool use_tiled(int L, int nr, int w) {
+  return nr == 3 && L % kTileP == 0 && w <= 8;
+}
+static inline size_t tiled_smem(int w) {
+  const int S = (2 * w + 1) * (2 * w + 1) * 3;
+  return ((S + 2) / 2 + 1) * sizeof(double) +
+         (size_t)(2 * w + 1) * (kTileP + 2 * w) * 3 * sizeof(double);
+}
+static inline int tiled_grid(int L) {
+  const long long nt = (long long)L * (L / kTileP);
+  return (int)(nt < kRedBlocks ? nt : kRedBlocks);
+}
 size_t gbk_boxT_elems(int L, int nr, int w) {
   const long long R = (long long)L * L * nr;
-  return (size_t)((R + 31) / 32) * 32 * (2 * w + 1) * (2 * w + 1) * nr;
+  const long long S = (long long)(2 * w + 1) * (2 * w + 1) * nr;
+  return (size_t)((R + 31) / 32) * 32 * (S + (S & 1));
 }
 int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, double* BsT,
                     cudaStream_t s) {
-  const long long total = (long long)gbk_boxT_elems(L, nr, w);
-  k_scale_box_T<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, nr, w, B, sv, BsT);
+  const int S = (2 * w + 1) * (2 * w + 1) * nr;
+  const size_t smem = (size_t)32 * (S + 1) * sizeof(double);
+  if (smem > 200 * 1024) {
+    const long long total = (long long)gbk_boxT_elems(L, nr, w);
+    k_scale_box_T_strided<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, nr, w, B, sv, BsT);
+    return (int)cudaGetLastError();
+  }
+  cudaFuncSetAttribute(k_scale_box_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const long long nblk = ((long long)L * L * nr + 31) / 32;
+  k_scale_box_T<<<(int)(nblk < 148 * 8 ? nblk : 148 * 8), 256, smem, s>>>(L, nr, w, B, sv, BsT);
   return (int)cudaGetLastError();
 }
 int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
@@ -1029,8 +1424,10 @@ int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, doubl
   const int gv = grid_for(npad, 256, kRedBlocks);
   const size_t sm = off_smem(nr, w);
   KState* k = (KState*)st;
+  const bool tl = use_tiled(L, nr, w);
   for (int i = 0; i < iters; ++i) {
-    if (nr == 3) k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
+    if (tl) k_tcg_spmv_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, p, Ap, k, part);
+    else if (nr == 3) k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
     else k_tcg_spmv<1><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
     k_cg_update<<<gv, 256, 0, s>>>(npad, x, r, p, Ap, k, part);
     k_cg_dir<<<gv, 256, 0, s>>>(npad, r, p, k);
@@ -1045,8 +1442,10 @@ int gbk_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, doub
   const int gv = grid_for(npad, 256, kRedBlocks);
   const size_t sm = off_smem(nr, w);
   KState* k = (KState*)st;
+  const bool tl = use_tiled(L, nr, w);
   for (int i = 0; i < iters; ++i) {
-    if (nr == 3) k_tpow_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
+    if (tl) k_tpow_apply_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, x, y, k, part);
+    else if (nr == 3) k_tpow_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
     else k_tpow_apply<1><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
     k_pow_step<<<gv, 256, 0, s>>>(npad, x, y, tol, k, part);
     k_pow_scale<<<gv, 256, 0, s>>>(npad, x, y, k);
@@ -1057,8 +1456,48 @@ int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, dou
                    cudaStream_t s) {
   const int gs = row_grid((long long)L * L * nr);
   const size_t sm = off_smem(nr, w);
-  if (nr == 3) k_tbox_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
+  if (use_tiled(L, nr, w)) k_tbox_apply_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, x, y);
+  else if (nr == 3) k_tbox_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
   else k_tbox_apply<1><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
+  return (int)cudaGetLastError();
+}
+
+
+// ---- block-Jacobi PCG launchers ----
+int gbk_bj_setup(int L, int w, const double* B, const double* sv, double* inv,
+                 cudaStream_t s) {
+  const int nb = (L / 2) * (L / 2);
+  k_bj_setup<<<grid_for(nb, 8, 148 * 16), 256, 0, s>>>(L, w, B, sv, inv);
+  return (int)cudaGetLastError();
+}
+static inline int bj_grid(int L) {
+  const int nb = (L / 2) * (L / 2);
+  return grid_for(nb, 16, kRedBlocks);
+}
+int gbk_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
+                  const double* inv, double rel_tol, int max_iter, void* st, double* part,
+                  cudaStream_t s) {
+  k_bjcg_init<<<bj_grid(L), 192, 0, s>>>(L, w, b, x, r, p, z, inv, rel_tol, max_iter,
+                                         (KState*)st, part);
+  return (int)cudaGetLastError();
+}
+int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
+                        double* r, double* p, double* Ap, double* z, int iters, void* st,
+                        double* part, cudaStream_t s) {
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const int gs = row_grid((long long)L * L * 3);
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  const size_t sm = off_smem(3, w);
+  KState* k = (KState*)st;
+  for (int i = 0; i < iters; ++i) {
+    if (use_tiled(L, 3, w))
+      k_tcg_spmv_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, p, Ap, k, part);
+    else
+      k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
+    k_bjcg_update<<<bj_grid(L), 192, 0, s>>>(L, w, x, r, p, Ap, z, inv, k, part);
+    k_cg_dir<<<gv, 256, 0, s>>>(npad, z, p, k);
+  }
   return (int)cudaGetLastError();
 }
 

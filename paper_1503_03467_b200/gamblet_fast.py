@@ -22,6 +22,8 @@ c_tol=1e-6) the two agree to 1e-13, so `c_tol` and
 
 from __future__ import annotations
 
+import concurrent.futures
+import threading
 import time
 from contextlib import contextmanager
 from dataclasses import dataclass, field
@@ -148,7 +150,7 @@ class FlopCounter:
             yield
         finally:
             if torch.cuda.is_available():
-                torch.cuda.synchronize()
+                torch.cuda.current_stream().synchronize()
             self.seconds[label] = self.seconds.get(label, 0.0) + (time.perf_counter() - start)
 
     @property
@@ -357,6 +359,16 @@ class _POp:
         self.BsT = dv.empty(nat.query("gb_boxT_elems", self.L, self.nr, self.w))
         nat.call("gb_scale_box_T", self.L, self.nr, self.w, dv.ptr(box.vals), dv.ptr(s),
                  dv.ptr(self.BsT), dv.stream())
+        self._box, self._s, self._bj = box, s, None
+
+    def bj_inv(self):
+        """Inverses of the 12x12 diagonal blocks (2x2 parents) of S B S."""
+        if self._bj is None:
+            nb = (self.L // 2) ** 2
+            self._bj = dv.empty(144 * nb)
+            nat.call("gb_bj_setup", self.L, self.w, dv.ptr(self._box.vals), dv.ptr(self._s),
+                     dv.ptr(self._bj), dv.stream())
+        return self._bj
 
     @property
     def spmv_bytes(self):
@@ -402,6 +414,35 @@ def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     while True:
         nat.call("gb_tcg_iterations", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(r),
                  dv.ptr(p), dv.ptr(Ap), chunk, dv.ptr(kr.state), dv.ptr(kr.part), st)
+        h = kr.read()
+        if h["done"]:
+            break
+        chunk = min(2 * chunk, 128)
+    rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
+    return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
+
+
+def _pcg(op, b, rel_tol, max_iter=None, kr=None):
+    """Block-Jacobi PCG for the subband systems (2x2-parent 12x12 blocks of
+    S B S); same stopping rule as sparse_core.py:161 on the true residual.
+    Returns the tuple of _cg."""
+    if op.nr != 3 or op.L < 2 or op.L % 2:
+        return _cg(op, b, rel_tol, max_iter=max_iter, kr=kr)
+    if max_iter is None:
+        max_iter = max(200, 2 * op.n)
+    inv = op.bj_inv()
+    kr = kr or _Krylov(op.npad)
+    st = dv.stream()
+    x, r, p, Ap, z = (op.vec() for _ in range(5))
+    nat.call("gb_state_reset", dv.ptr(kr.state), max_iter, st)
+    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), dv.ptr(x), dv.ptr(r), dv.ptr(p),
+             dv.ptr(z), dv.ptr(inv), float(rel_tol), int(max_iter), dv.ptr(kr.state),
+             dv.ptr(kr.part), st)
+    chunk = 8
+    while True:
+        nat.call("gb_bjcg_iterations", op.L, op.w, dv.ptr(op.BsT), dv.ptr(inv), dv.ptr(x),
+                 dv.ptr(r), dv.ptr(p), dv.ptr(Ap), dv.ptr(z), chunk, dv.ptr(kr.state),
+                 dv.ptr(kr.part), st)
         h = kr.read()
         if h["done"]:
             break
@@ -478,6 +519,60 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
 
 
 _SPECTRAL_LOG = []
+
+# lambda estimates run on side streams (one per worker thread) so they overlap
+# the FP64-bound patch factorizations of the main stream
+SPECTRAL_WORKERS = 2
+
+
+class _SpectralPool:
+    """Runs _eig_extremes for each level on its own stream/thread; the
+    operator (slot-major S B S) is ordered after its producer by an event and
+    stays alive on the level until join()."""
+
+    _pool = None
+    _local = threading.local()
+
+    def __init__(self):
+        if _SpectralPool._pool is None:
+            _SpectralPool._pool = concurrent.futures.ThreadPoolExecutor(
+                max_workers=SPECTRAL_WORKERS, thread_name_prefix="gb-spectral")
+        self.futures = []
+
+    @classmethod
+    def _stream(cls):
+        st = getattr(cls._local, "stream", None)
+        if st is None:
+            torch.cuda.set_device(dv.device())
+            st = torch.cuda.Stream(device=dv.device())
+            cls._local.stream = st
+        return st
+
+    def submit(self, level, op):
+        ev = torch.cuda.Event()
+        ev.record()
+        self.futures.append(self._pool.submit(self._run, level, op, ev))
+
+    @classmethod
+    def _run(cls, level, op, ev):
+        st = cls._stream()
+        with torch.cuda.stream(st):
+            st.wait_event(ev)
+            with dv.phase("spectral"):
+                lam_min, lam_max, calls = _eig_extremes(op)
+            done = torch.cuda.Event()
+            done.record(st)
+        level.lambda_min_subband = lam_min
+        level.lambda_max_subband = lam_max
+        return calls, op, done
+
+    def join(self, counter):
+        for f in self.futures:
+            calls, op, done = f.result()
+            torch.cuda.current_stream().wait_event(done)
+            counter.add("spectral", 2 * op.n * op.slots * calls)
+            dv.Prof.add_work("spectral", nbytes=calls * op.spmv_bytes)
+        self.futures = []
 
 
 # ---------------------------------------------------------------------------
@@ -623,7 +718,7 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
 
 
 def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
-                     counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None):
+                     counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None, _spool=None):
     """One localized downward step k -> k-1 (gamblet_fast.py:501-632).
     Mutates `level` (W, B, s_B, D, R, lambdas, repair) and returns level k-1."""
     k = level.k
@@ -668,14 +763,9 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         # K7: spectral extremes of S B S (gamblet_fast.py:531-534)
         with dv.phase("level_blocks"):
             op = _POp(B, sB)
+        spool = _spool if _spool is not None else _SpectralPool()
         if SPECTRAL:
-            with dv.phase("spectral"):
-                lam_min, lam_max, calls = _eig_extremes(op)
-            dv.Prof.add_work("spectral", nbytes=calls * op.spmv_bytes)
-        else:
-            lam_min = lam_max = None
-            calls = 0
-        counter.add("spectral", 2 * J * dv.box_slots(wB, 3) * calls)
+            spool.submit(level, op)
 
         # K4: correction patches -> D^T with the row-tail trim fused
         Dt = dv.empty(P * dv.box_slots(rho, 3))
@@ -742,11 +832,11 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
     level._op = op
     level.correction = BoxMatrix(Dt, Lp, 1, rho, 3, kind=EXP_TDT)
     level.restriction = BoxMatrix(Rv, Lp, 1, rho, 4, kind=EXP_CHILD)
-    level.lambda_min_subband = lam_min
-    level.lambda_max_subband = lam_max
     level._repair_slot_b = ib
     nxt = LocalGambletLevel(k - 1, psin, BoxMatrix(An, Lp, 1, wA2, 1))
     nxt._repair_slot_a = ia
+    if _spool is None:
+        spool.join(counter)
     if _ctx is None:
         ctx.check()
         level.symmetry_repair = max(level.symmetry_repair, ctx.repair_of.get(ib, 0.0))
@@ -769,10 +859,15 @@ def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_
     levels = {q: LocalGambletLevel(q, psi, Aq)}
     levels[q]._repair_slot_a = ia
     level = levels[q]
-    for k in range(q, 1, -1):
-        level = local_level_step(level, tree, schedule, w_variant=w_variant, c_tol=c_tol,
-                                 counter=counter, dense_cutoff=dense_cutoff, _ctx=ctx)
-        levels[k - 1] = level
+    spool = _SpectralPool()
+    try:
+        for k in range(q, 1, -1):
+            level = local_level_step(level, tree, schedule, w_variant=w_variant, c_tol=c_tol,
+                                     counter=counter, dense_cutoff=dense_cutoff, _ctx=ctx,
+                                     _spool=spool)
+            levels[k - 1] = level
+    finally:
+        spool.join(counter)
     ctx.check()
     for k, lv in levels.items():
         rep = ctx.repair_of.get(getattr(lv, "_repair_slot_a", -1), 0.0)
@@ -864,8 +959,9 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
         counter.add("line8", 8 * J + J)
         with dv.phase("subband_cg"):
-            zp, its, rel, conv, brk, _ = _cg(op, op.pad(rhs), tol)
-        dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 6 * 8 * op.npad))
+            zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), tol)
+        dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
+                                                     + 12 * 8 * op.n))
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")

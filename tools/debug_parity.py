@@ -47,3 +47,15 @@ print("pbox_apply err", np.abs(y - Bs @ x).max() / np.abs(Bs @ x).max())
 z, its, rel, conv, brk, h = gf._cg(op, xp, 1e-10)
 print("cg", its, rel, conv, brk, "err", np.abs(Bs @ op.unpad(z).cpu().numpy() - x).max())
 print("eig", gf._eig_extremes(op)[:2], O.eig_extremes(Bs))
+z, its, rel, conv, brk, h = gf._pcg(op, xp, 1e-10)
+print("pcg", its, rel, conv, brk, "err", np.abs(Bs @ op.unpad(z).cpu().numpy() - x).max())
+inv = op.bj_inv().cpu().numpy().reshape(-1, 12, 12)
+L = B.L
+bs, bt = 1, 1
+idx = []
+for i in range(2):
+    for j in range(2):
+        p_ = (2*bs+i)*L + 2*bt+j
+        idx += [3*p_, 3*p_+1, 3*p_+2]
+blk = Bs[idx][:, idx].toarray()
+print("bj inv err", np.abs(inv[bs*(L//2)+bt] @ blk - np.eye(12)).max())
