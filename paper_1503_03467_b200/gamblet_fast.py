@@ -522,7 +522,8 @@ _SPECTRAL_LOG = []
 
 # lambda estimates run on side streams (one per worker thread) so they overlap
 # the FP64-bound patch factorizations of the main stream
-SPECTRAL_WORKERS = 2
+SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
+PIPELINE_SOLVE = __import__("os").environ.get("GB_PIPELINE", "1") == "1"
 
 
 class _SpectralPool:
@@ -718,7 +719,8 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
 
 
 def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
-                     counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None, _spool=None):
+                     counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None, _spool=None,
+                     _pipe=None):
     """One localized downward step k -> k-1 (gamblet_fast.py:501-632).
     Mutates `level` (W, B, s_B, D, R, lambdas, repair) and returns level k-1."""
     k = level.k
@@ -766,6 +768,12 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         spool = _spool if _spool is not None else _SpectralPool()
         if SPECTRAL:
             spool.submit(level, op)
+        level._op = op
+        level.subband = B
+        level.subband_scale = sB
+        level.w_variant = w_variant
+        if _pipe is not None:
+            _pipe.notify("op", k)
 
         # K4: correction patches -> D^T with the row-tail trim fused
         Dt = dv.empty(P * dv.box_slots(rho, 3))
@@ -826,15 +834,14 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
                         + 2 * J * wdw * wdw * 4)
 
     level.null_w = (lambda tree=tree, k=k, v=w_variant: tree.null_basis(k, v))
-    level.w_variant = w_variant
-    level.subband = B
-    level.subband_scale = sB
-    level._op = op
     level.correction = BoxMatrix(Dt, Lp, 1, rho, 3, kind=EXP_TDT)
     level.restriction = BoxMatrix(Rv, Lp, 1, rho, 4, kind=EXP_CHILD)
     level._repair_slot_b = ib
     nxt = LocalGambletLevel(k - 1, psin, BoxMatrix(An, Lp, 1, wA2, 1))
     nxt._repair_slot_a = ia
+    if _pipe is not None:
+        _pipe.levels_ref[k - 1] = nxt
+        _pipe.notify("step", k)
     if _spool is None:
         spool.join(counter)
     if _ctx is None:
@@ -845,7 +852,7 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
 
 
 def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
-                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF):
+                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None):
     """Load-independent phase, levels q..1 (gamblet_fast.py:635-674).
     Returns (levels, counter); all operators stay on the device."""
     counter = counter if counter is not None else FlopCounter()
@@ -860,15 +867,31 @@ def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_
     levels[q]._repair_slot_a = ia
     level = levels[q]
     spool = _SpectralPool()
+    pipe = None
+    if _load is not None and PIPELINE_SOLVE:  # pipelined solve: _load = (g_device, records)
+        pipe = _SolvePipeline(levels, _load[0], tree, schedule.subband_tol(), counter,
+                              _load[1])
+        pipe.levels_ref = levels
+    ok = False
     try:
         for k in range(q, 1, -1):
             level = local_level_step(level, tree, schedule, w_variant=w_variant, c_tol=c_tol,
                                      counter=counter, dense_cutoff=dense_cutoff, _ctx=ctx,
-                                     _spool=spool)
+                                     _spool=spool, _pipe=pipe)
             levels[k - 1] = level
+        if pipe is not None:
+            pipe.notify("step", 1)
+        ok = True
     finally:
+        if pipe is not None and not ok:
+            pipe.abort()
         spool.join(counter)
     ctx.check()
+    if pipe is not None:
+        fast_transform.last_solve = pipe.join()
+    elif _load is not None:
+        fast_transform.last_solve = _solve_levels(levels, _load[0], tree, schedule,
+                                                  schedule.subband_tol(), counter, _load[1])
     for k, lv in levels.items():
         rep = ctx.repair_of.get(getattr(lv, "_repair_slot_a", -1), 0.0)
         rep_b = ctx.repair_of.get(getattr(lv, "_repair_slot_b", -1), 0.0)
@@ -930,36 +953,48 @@ def solve_with_transform(levels, load, tree, schedule, g_mode="nodal", counter=N
     return solution, counter
 
 
-def _solve_levels(levels, g, tree, schedule, tol, counter, records):
-    q = tree.q
-    n = 1 << q
-    N = n * n
-    s = dv.stream()
-    coeffs, incs = HostDict(), HostDict()
-    for k in range(q, 1, -1):
-        lvl = levels[k]
+class _LevelSolver:
+    """Load-dependent work of one level at a time (gamblet_fast.py:717-765):
+    rhs = s (W g), block-Jacobi PCG on S B S, w = s z, increment psi^T W^T w,
+    g <- R g; then the coarse solve and the partial sums.  Used sequentially
+    by solve_with_transform and as the body of the pipelined fast_solve."""
+
+    def __init__(self, levels, tree, tol, counter, records):
+        self.levels, self.tree, self.tol = levels, tree, tol
+        self.counter, self.records = counter, records
+        self.n = 1 << tree.q
+        self.N = self.n * self.n
+        self.coeffs, self.incs = HostDict(), HostDict()
+
+    def _check(self, k, need_r=True):
+        lvl = self.levels[k]
         R = lvl.raw("restriction")
         B = lvl.raw("subband")
-        if R is None or B is None:
+        if B is None or (need_r and R is None):
             raise InvalidArgumentError(
                 f"level {k} is missing transform data; run fast_transform first")
-        if not isinstance(R, BoxMatrix) or not isinstance(B, BoxMatrix):
+        if not isinstance(B, BoxMatrix) or (need_r and not isinstance(R, BoxMatrix)):
             raise InvalidArgumentError(
                 f"level {k} was not produced by this package's fast_transform")
+        return lvl, B, R
+
+    def subband(self, k, g, pipelined=False):
+        lvl, B, _ = self._check(k, need_r=not pipelined)
+        s = dv.stream()
+        counter = self.counter
         sB = lvl.raw("subband_scale")
         if not isinstance(sB, torch.Tensor):
             sB = dv.empty(B.rows)
             st = dv.zeros(2, torch.int64)
             nat.call("gb_box_scale", B.rows, 3, B.w, dv.ptr(B.vals), dv.ptr(sB), dv.ptr(st), s)
         w12 = w_template(lvl.w_variant or "orthonormal").ctypes.data
-        Lp = B.L
-        J = B.rows
+        Lp, J = B.L, B.rows
         op = getattr(lvl, "_op", None) or _POp(B, sB)
         rhs = dv.empty(J)
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
         counter.add("line8", 8 * J + J)
         with dv.phase("subband_cg"):
-            zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), tol)
+            zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), self.tol)
         dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
                                                      + 12 * 8 * op.n))
         if brk:
@@ -970,58 +1005,142 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
         w = op.unpad(zp, sB)
         counter.add("line8", cg_flops(J * B.slots, J, its) + 2 * J * its)
         counter.record_iters("line8", its)
-        counter.record_solve(f"line8 level {k}", its, tol)
-        records.append(SolveRecord(k, "subband", J, 1, tol, np.array([its]), np.array([rel])))
+        counter.record_solve(f"line8 level {k}", its, self.tol)
+        self.records.append(SolveRecord(k, "subband", J, 1, self.tol, np.array([its]),
+                                        np.array([rel])))
         v = dv.empty(4 * Lp * Lp)
         nat.call("gb_apply_wt", Lp, w12, dv.ptr(w), dv.ptr(v), s)
         psi = lvl.raw("psi")
         if not isinstance(psi, PsiWindows):
-            psi = _psi_dev(lvl, n, 2 * Lp)
-        inc = dv.empty(N)
-        nat.call("gb_psi_t_apply", n, 2 * Lp, psi.lo, psi.wd, dv.ptr(psi.vals), dv.ptr(v),
-                 dv.ptr(inc), s)
+            psi = _psi_dev(lvl, self.n, 2 * Lp)
+        inc = dv.empty(self.N)
+        nat.call("gb_psi_t_apply", self.n, 2 * Lp, psi.lo, psi.wd, dv.ptr(psi.vals),
+                 dv.ptr(v), dv.ptr(inc), s)
         counter.add("line10", 8 * J + 2 * (4 * Lp * Lp) * psi.wd * psi.wd)
-        incs[k] = inc
-        coeffs[k] = w
-        gn = dv.empty(Lp * Lp)
-        nat.call("gb_apply_r", Lp, R.w, dv.ptr(R.vals), dv.ptr(g), dv.ptr(gn), s)
-        counter.add("line15", 2 * Lp * Lp * R.slots)
-        g = gn
+        self.incs[k] = inc
+        self.coeffs[k] = w
 
-    coarse = levels[1]
-    A1 = _box_dev(coarse, "stiffness", 2, None)
-    s1 = dv.empty(4)
-    st = dv.zeros(2, torch.int64)
-    nat.call("gb_box_scale", 4, 1, A1.w, dv.ptr(A1.vals), dv.ptr(s1), dv.ptr(st), s)
-    op1 = _POp(A1, s1)
-    zp, its, rel, conv, brk, _ = _cg(op1, op1.pad(g, s1), tol)
-    if brk:
-        raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
-                             "(matrix is not SPD)")
-    if not conv:
-        raise NumericalError("coarse solve did not converge")
-    U1 = op1.unpad(zp, s1)
-    counter.add("line16", cg_flops(4 * A1.slots, 4, its))
-    counter.record_iters("line16", its)
-    counter.record_solve("line16", its, tol)
-    records.append(SolveRecord(1, "coarse", 4, 1, tol, np.array([its]), np.array([rel])))
-    psi1 = coarse.raw("psi")
-    if not isinstance(psi1, PsiWindows):
-        psi1 = _psi_dev(coarse, n, 2)
-    inc1 = dv.empty(N)
-    nat.call("gb_psi_t_apply", n, 2, psi1.lo, psi1.wd, dv.ptr(psi1.vals), dv.ptr(U1),
-             dv.ptr(inc1), s)
-    counter.add("line17", 2 * 4 * psi1.wd * psi1.wd)
-    incs[1] = inc1
-    partials = HostDict({1: inc1})
-    prev = inc1
-    for k in range(2, q + 1):
-        out = dv.empty(N)
-        nat.call("gb_vadd", N, dv.ptr(prev), dv.ptr(incs.device(k)), dv.ptr(out), s)
-        partials[k] = out
-        prev = out
-    counter.add("line18", (q - 1) * N)
-    return {"coeffs": coeffs, "increments": incs, "partials": partials}, U1
+    def restrict(self, k, g):
+        _, B, R = self._check(k)
+        Lp = B.L
+        gn = dv.empty(Lp * Lp)
+        nat.call("gb_apply_r", Lp, R.w, dv.ptr(R.vals), dv.ptr(g), dv.ptr(gn), dv.stream())
+        self.counter.add("line15", 2 * Lp * Lp * R.slots)
+        return gn
+
+    def coarse(self, g):
+        s = dv.stream()
+        counter = self.counter
+        coarse = self.levels[1]
+        A1 = _box_dev(coarse, "stiffness", 2, None)
+        s1 = dv.empty(4)
+        st = dv.zeros(2, torch.int64)
+        nat.call("gb_box_scale", 4, 1, A1.w, dv.ptr(A1.vals), dv.ptr(s1), dv.ptr(st), s)
+        op1 = _POp(A1, s1)
+        zp, its, rel, conv, brk, _ = _cg(op1, op1.pad(g, s1), self.tol)
+        if brk:
+            raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
+                                 "(matrix is not SPD)")
+        if not conv:
+            raise NumericalError("coarse solve did not converge")
+        U1 = op1.unpad(zp, s1)
+        counter.add("line16", cg_flops(4 * A1.slots, 4, its))
+        counter.record_iters("line16", its)
+        counter.record_solve("line16", its, self.tol)
+        self.records.append(SolveRecord(1, "coarse", 4, 1, self.tol, np.array([its]),
+                                        np.array([rel])))
+        psi1 = coarse.raw("psi")
+        if not isinstance(psi1, PsiWindows):
+            psi1 = _psi_dev(coarse, self.n, 2)
+        inc1 = dv.empty(self.N)
+        nat.call("gb_psi_t_apply", self.n, 2, psi1.lo, psi1.wd, dv.ptr(psi1.vals), dv.ptr(U1),
+                 dv.ptr(inc1), s)
+        counter.add("line17", 2 * 4 * psi1.wd * psi1.wd)
+        self.incs[1] = inc1
+        self.U1 = U1
+
+    def finish(self):
+        q = self.tree.q
+        s = dv.stream()
+        prev = self.incs.device(1)
+        partials = HostDict({1: prev})
+        for k in range(2, q + 1):
+            out = dv.empty(self.N)
+            nat.call("gb_vadd", self.N, dv.ptr(prev), dv.ptr(self.incs.device(k)),
+                     dv.ptr(out), s)
+            partials[k] = out
+            prev = out
+        self.counter.add("line18", (q - 1) * self.N)
+        return {"coeffs": self.coeffs, "increments": self.incs, "partials": partials}, self.U1
+
+
+def _solve_levels(levels, g, tree, schedule, tol, counter, records):
+    """Sequential solve phase on the current stream."""
+    sv = _LevelSolver(levels, tree, tol, counter, records)
+    for k in range(tree.q, 1, -1):
+        sv.subband(k, g)
+        g = sv.restrict(k, g)
+    sv.coarse(g)
+    return sv.finish()
+
+
+class _SolvePipeline:
+    """Runs the solve phase on its own stream/thread, level by level, as the
+    transform produces the operators: level k's subband solve starts once
+    its S B S is built (event "op"), the restriction of the load once level
+    k's step has finished (event "step").  Same kernels and inputs as
+    _solve_levels, so results are identical."""
+
+    _pool = None
+
+    def __init__(self, levels, g, tree, tol, counter, records):
+        import queue
+        if _SolvePipeline._pool is None:
+            _SolvePipeline._pool = concurrent.futures.ThreadPoolExecutor(
+                max_workers=1, thread_name_prefix="gb-solve")
+        self.q = queue.Queue()
+        self.sv = _LevelSolver(levels, tree, tol, counter, records)
+        self.tree = tree
+        ev = torch.cuda.Event()
+        ev.record()
+        self.fut = self._pool.submit(self._run, g, ev)
+
+    def notify(self, kind, k):
+        ev = torch.cuda.Event()
+        ev.record()
+        self.q.put((kind, k, ev))
+
+    def _wait(self, want):
+        kind, k, ev = self.q.get()
+        if kind == "abort":
+            raise RuntimeError("solve pipeline aborted")
+        assert (kind, k) == want, ((kind, k), want)
+        torch.cuda.current_stream().wait_event(ev)
+
+    def _run(self, g, ev0):
+        torch.cuda.set_device(dv.device())
+        st = torch.cuda.Stream(device=dv.device())
+        with torch.cuda.stream(st):
+            st.wait_event(ev0)
+            for k in range(self.tree.q, 1, -1):
+                self._wait(("op", k))
+                self.sv.subband(k, g, pipelined=True)
+                self._wait(("step", k))
+                g = self.sv.restrict(k, g)
+            self._wait(("step", 1))
+            self.sv.coarse(g)
+            out = self.sv.finish()
+            done = torch.cuda.Event()
+            done.record(st)
+        return out, done
+
+    def abort(self):
+        self.q.put(("abort", 0, None))
+
+    def join(self):
+        out, done = self.fut.result()
+        torch.cuda.current_stream().wait_event(done)
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -1091,14 +1210,51 @@ def complexity_report(schedule, counter, levels):
 def fast_solve(M, A, load, tree, epsilon, c_rho=None, uniform_rho=None, schedule=None,
                w_variant="orthonormal", g_mode="nodal", c_tol=DEFAULT_C_TOL,
                dense_cutoff=DENSE_PATCH_CUTOFF):
-    """Localized transform plus solve in one call (gamblet_fast.py:815-837)."""
+    """Localized transform plus solve in one call (gamblet_fast.py:815-837).
+
+    With the nodal moment shortcut the solve phase is pipelined into the
+    transform (level k's subband solve runs on a second stream as soon as
+    S B^(k) S exists); the arithmetic is that of fast_transform followed by
+    solve_with_transform."""
     if schedule is None:
         schedule = make_schedule(epsilon, tree.q, c_rho=c_rho, uniform_rho=uniform_rho)
     counter = FlopCounter()
+    q = tree.q
+    N = 4 ** q
     with counter.timer("total"):
-        levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
-                                         c_tol=c_tol, counter=counter,
-                                         dense_cutoff=dense_cutoff)
-        solution, counter = solve_with_transform(levels, load, tree, schedule,
-                                                 g_mode=g_mode, counter=counter)
+        if g_mode == "nodal" and isinstance(load, LoadVector):
+            if tuple(np.shape(load.b)) != (N,):
+                raise InvalidArgumentError(f"load shape {np.shape(load.b)} does not match N={N}")
+            records = []
+            g = dv.to_dev(load.g_nodal if isinstance(load.g_nodal, torch.Tensor)
+                          else np.asarray(load.g_nodal, dtype=float))
+            counter.add("line4", 0)
+            levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
+                                             c_tol=c_tol, counter=counter,
+                                             dense_cutoff=dense_cutoff, _load=(g, records))
+            parts, U1 = fast_transform.last_solve
+            fast_transform.last_solve = None
+            solution = MultiresSolution(u=dv.to_host(parts["partials"].device(q)),
+                                        u1_coarse=dv.to_host(U1),
+                                        subband_coeffs=parts["coeffs"],
+                                        increments=parts["increments"],
+                                        partials=parts["partials"], records=records)
+        else:
+            levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
+                                             c_tol=c_tol, counter=counter,
+                                             dense_cutoff=dense_cutoff)
+            solution, counter = solve_with_transform(levels, load, tree, schedule,
+                                                     g_mode=g_mode, counter=counter)
     return FastResult(solution, levels, schedule, counter)
+
+
+def _fast_solve_device(M, A, g, tree, schedule, w_variant="orthonormal"):
+    """fast_solve with device-resident inputs (DeviceCSR M, A; device g);
+    returns (levels, parts, U1, counter) with everything left in HBM."""
+    counter = FlopCounter()
+    records = []
+    levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
+                                     counter=counter, _load=(g, records))
+    parts, U1 = fast_transform.last_solve
+    fast_transform.last_solve = None
+    return levels, parts, U1, counter

@@ -18,7 +18,6 @@ sched = gb.make_schedule(EPS, a.q, uniform_rho=RHO)
 Md, Ad = dv.DeviceCSR.from_scipy(M), dv.DeviceCSR.from_scipy(A)
 gd = dv.to_dev(load.g_nodal)
 for _ in range(a.steps):
-    levels, counter = gf.fast_transform(Md, Ad, tree, sched)
-    gf._solve_levels(levels, gd, tree, sched, sched.subband_tol(), counter, [])
+    gf._fast_solve_device(Md, Ad, gd, tree, sched)
 torch.cuda.synchronize()
 print("ok")
