@@ -230,7 +230,7 @@ __global__ void k_correction_patches(int Lp, int wB, const double* __restrict__ 
 // ===========================================================================
 struct TileSmem {
   double* tl;
-  double* invd;
+  double* sl;  // scale factor of local row l (and 8 scratch doubles after it)
   double* z;
   double* part;
   int* tij;    // packed (it << 8) | jt per lower tile
@@ -241,7 +241,7 @@ struct TileSmem {
 
 __host__ __device__ __forceinline__ size_t tile_smem_bytes(int Tmax, int nwarps) {
   const size_t ntile = (size_t)Tmax * (Tmax + 1) / 2 + Tmax;
-  return ntile * 64 * 8 + (size_t)16 * Tmax * 8 + (size_t)8 * nwarps * 8 +
+  return ntile * 64 * 8 + (size_t)(16 * Tmax + 8) * 8 + (size_t)8 * nwarps * 8 +
          (size_t)(Tmax * (Tmax + 1) / 2) * 4 + (size_t)16 * Tmax * 4 + 16;
 }
 
@@ -249,8 +249,8 @@ __device__ __forceinline__ TileSmem carve(double* sm, int Tmax, int nwarps) {
   TileSmem t;
   const int ntile = Tmax * (Tmax + 1) / 2 + Tmax;
   t.tl = sm;
-  t.invd = t.tl + ntile * 64;
-  t.z = t.invd + 8 * Tmax;
+  t.sl = t.tl + ntile * 64;
+  t.z = t.sl + 8 * Tmax + 8;
   t.part = t.z + 8 * Tmax;
   int* ip = reinterpret_cast<int*>(t.part + 8 * nwarps);
   t.tij = ip;
@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
         const long long r = ((long long)ps * Lp + pt) * 3 + c;
         S.rowg[l] = (int)r;
         S.ploc[l] = (a << 8) | b;
+        S.sl[l] = sB[r];
         const int ds = si - ps, dt = ti - pt;
         double g = 0.0;
         if (ds >= -wG && ds <= wG && dt >= -wG && dt <= wG)
@@ -322,8 +323,8 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
         const int p1 = S.ploc[l1 / 3 * 3], p2 = S.ploc[l2 / 3 * 3];
         const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
         if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
-          v = B[(long long)S.rowg[l1] * SB + slot_of(wB, 3, ds, dt, l2 % 3)] *
-              sB[S.rowg[l1]] * sB[S.rowg[l2]];
+          v = B[(long long)S.rowg[l1] * SB + slot_of(wB, 3, ds, dt, l2 % 3)] * S.sl[l1] *
+              S.sl[l2];
       } else if (l1 == l2) {
         v = 1.0;
       }
@@ -335,16 +336,16 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
       S.tl[(nlt + jt) * 64 + eidx(r, c)] = (r == 0) ? S.z[jt * 8 + c] : 0.0;
     }
     __syncthreads();
-    if (!tiled_chol_fwd(S.tl, T, S.invd, S.flag)) {
+    if (!tiled_chol_fwd(S.tl, T, S.sl + 8 * Tmax, S.flag)) {
       if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
       __syncthreads();
       continue;
     }
-    tiled_back_subst(S.tl, T, S.invd, S.z, S.part);
+    tiled_back_subst(S.tl, T, S.z, S.part);
     // D = s z and the row-tail trim of this column of D
     double mx = 0.0;
     for (int l = threadIdx.x; l < m; l += blockDim.x) {
-      const double v = sB[S.rowg[l]] * S.z[l];
+      const double v = S.sl[l] * S.z[l];
       S.z[l] = v;
       mx = fmax(mx, fabs(v));
     }
@@ -385,6 +386,7 @@ __global__ void __launch_bounds__(128) k_mass_patches_v2(
         const int a = l / nt, b = l - a * nt;
         S.rowg[l] = (s0 + a) * n + (t0 + b);
         S.ploc[l] = (a << 8) | b;
+        S.sl[l] = s[S.rowg[l]];
       }
     }
     for (int t = threadIdx.x; t < nlt; t += blockDim.x) {
@@ -404,8 +406,7 @@ __global__ void __launch_bounds__(128) k_mass_patches_v2(
         const int p1 = S.ploc[l1], p2 = S.ploc[l2];
         const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
         if (ds >= -wM && ds <= wM && dt >= -wM && dt <= wM)
-          v = M[(long long)S.rowg[l1] * SM + slot_of(wM, 1, ds, dt, 0)] * s[S.rowg[l1]] *
-              s[S.rowg[l2]];
+          v = M[(long long)S.rowg[l1] * SM + slot_of(wM, 1, ds, dt, 0)] * S.sl[l1] * S.sl[l2];
       } else if (l1 == l2) {
         v = 1.0;
       }
@@ -417,12 +418,12 @@ __global__ void __launch_bounds__(128) k_mass_patches_v2(
       S.tl[(nlt + jt) * 64 + eidx(r, c)] = (r == 0 && jt * 8 + c == li) ? s[i] : 0.0;
     }
     __syncthreads();
-    if (!tiled_chol_fwd(S.tl, T, S.invd, S.flag)) {
+    if (!tiled_chol_fwd(S.tl, T, S.sl + 8 * Tmax, S.flag)) {
       if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
       __syncthreads();
       continue;
     }
-    tiled_back_subst(S.tl, T, S.invd, S.z, S.part);
+    tiled_back_subst(S.tl, T, S.z, S.part);
     const int os = clampi(si - rho, 0, n - wd), ot = clampi(ti - rho, 0, n - wd);
     double* row = psi + i * (long long)wd * wd;
     for (int e = threadIdx.x; e < wd * wd; e += blockDim.x) {

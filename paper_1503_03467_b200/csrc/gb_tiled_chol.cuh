@@ -23,88 +23,118 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
       : "d"(a), "d"(b));
 }
 
-// Factor the 8x8 diagonal tile in place (one warp).  Returns false if a
-// pivot is not positive.  invd[j] = 1 / L_jj.
-__device__ __forceinline__ bool warp_chol8(double* t, double* invd) {
+// Factor the 8x8 diagonal tile (one warp, rows in lanes 0..7, registers and
+// shuffles), form L^-1 and store it OVER the tile: diagonal L tiles are never
+// DMMA operands, every later use (TRSM, back substitution) needs L_kk^-1.
+// `scratch` holds 8 doubles.  Returns false if a pivot is not positive.
+__device__ __forceinline__ bool warp_chol8_inv(double* t, double* scratch) {
   const int lane = threadIdx.x & 31;
+  const int r = lane & 7;
+  double v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = (c <= r) ? t[eidx(r, c)] : 0.0;
+  double il_r = 0.0;  // 1 / L_rr, kept by lane r
   bool ok = true;
+#pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const double d = t[eidx(j, j)];
-    if (!(d > 0.0)) {
-      ok = false;
-      break;
+    const double d = __shfl_sync(0xffffffffu, v[j], j);
+    ok = ok && (d > 0.0);
+    const double il = rsqrt(d);
+    if (r > j) v[j] *= il;
+    if (r == j) {
+      v[j] = d * il;
+      il_r = il;
     }
-    const double l = sqrt(d);
-    const double il = 1.0 / l;
-    __syncwarp();
-    if (lane > j && lane < 8) t[eidx(lane, j)] *= il;
-    __syncwarp();
-    for (int e = lane; e < 64; e += 32) {
-      const int r = e >> 3, c = e & 7;
-      if (c > j && c <= r) t[eidx(r, c)] -= t[eidx(r, j)] * t[eidx(c, j)];
+#pragma unroll
+    for (int c = j + 1; c < 8; ++c) {
+      const double lcj = __shfl_sync(0xffffffffu, v[j], c);
+      if (r > j && c <= r) v[c] = fma(-v[j], lcj, v[c]);
     }
-    __syncwarp();
-    if (lane == 0) {
-      t[eidx(j, j)] = l;
-      invd[j] = il;
-    }
-    __syncwarp();
   }
-  return ok;
+  if (!ok) return false;
+  if (lane < 8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c <= r) t[eidx(r, c)] = v[c];
+    scratch[r] = il_r;  // diagonal of L^-1, read back below
+  }
+  __syncwarp();
+  // L^-1, column r by lane r: x_i = -(sum_{r<=k<i} L_ik x_k) / L_ii, x_r = 1/L_rr
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) acc = fma(t[eidx(i, k)], x[k], acc);
+    const double ii = scratch[i];
+    x[i] = (i > r) ? -acc * ii : ((i == r) ? ii : 0.0);
+  }
+  __syncwarp();
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[eidx(i, r)] = x[i];  // column r of L^-1 (upper = 0)
+  }
+  __syncwarp();
+  return true;
 }
 
 // Left-looking tiled Cholesky + forward substitution of the RHS row.
-// tl: tile storage, T: tiles per dimension, invd: 8*T scratch (1/L_ii),
-// flag: shared int.  All threads of the CTA must call it.  Returns false
+// tl: tile storage (diagonal tiles end up holding L_kk^-1), T: tiles per
+// dimension, scratch: 8 doubles, flag: shared int.  Warp 0 owns the diagonal tile of every step;
+// warps 1.. own the off-diagonal tiles (round robin), keep them in registers
+// across the update and the TRSM (two DMMAs with L_kk^-T).  Returns false
 // (CTA-uniform) when the matrix is not SPD.
-__device__ bool tiled_chol_fwd(double* tl, int T, double* invd, int* flag) {
+__device__ bool tiled_chol_fwd(double* tl, int T, double* scratch, int* flag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
+  const int e0 = eidx(fr, 2 * fk), e1 = eidx(fr, 2 * fk + 1);
   if (threadIdx.x == 0) *flag = 0;
   __syncthreads();
   for (int kt = 0; kt < T; ++kt) {
-    // (1) column kt: C(it,kt) -= sum_{jt<kt} L(it,jt) L(kt,jt)^T, it = kt..T
-    for (int it = kt + warp; it <= T; it += nw) {
-      double* ct = tl + tidx(it, kt) * 64;
-      const int e0 = eidx(fr, 2 * fk), e1 = eidx(fr, 2 * fk + 1);
+    const double* bk = tl + tidx(kt, 0) * 64;
+    // (1) updates: C(it,kt) -= sum_{jt<kt} L(it,jt) L(kt,jt)^T
+    if (warp == 0) {
+      double* ct = tl + tidx(kt, kt) * 64;
       double c0 = ct[e0], c1 = ct[e1];
-      const double* ai = tl + tidx(it, 0) * 64;
-      const double* bk = tl + tidx(kt, 0) * 64;
       for (int jt = 0; jt < kt; ++jt) {
-        const double* a = ai + jt * 64;
         const double* b = bk + jt * 64;
-        dmma_884(c0, c1, -a[eidx(fr, fk)], b[eidx(fr, fk)]);
-        dmma_884(c0, c1, -a[eidx(fr, 4 + fk)], b[eidx(fr, 4 + fk)]);
+        dmma_884(c0, c1, -b[eidx(fr, fk)], b[eidx(fr, fk)]);
+        dmma_884(c0, c1, -b[eidx(fr, 4 + fk)], b[eidx(fr, 4 + fk)]);
       }
       ct[e0] = c0;
       ct[e1] = c1;
-      if (it == kt) {
-        __syncwarp();
-        if (!warp_chol8(ct, invd + 8 * kt) && lane == 0) *flag = 1;
+      __syncwarp();
+      if (!warp_chol8_inv(ct, scratch) && lane == 0) *flag = 1;
+    } else {
+      for (int it = kt + warp; it <= T; it += nw - 1) {
+        double* ct = tl + tidx(it, kt) * 64;
+        double c0 = ct[e0], c1 = ct[e1];
+        const double* ai = tl + tidx(it, 0) * 64;
+        for (int jt = 0; jt < kt; ++jt) {
+          const double* a = ai + jt * 64;
+          const double* b = bk + jt * 64;
+          dmma_884(c0, c1, -a[eidx(fr, fk)], b[eidx(fr, fk)]);
+          dmma_884(c0, c1, -a[eidx(fr, 4 + fk)], b[eidx(fr, 4 + fk)]);
+        }
+        ct[e0] = c0;
+        ct[e1] = c1;
       }
     }
     __syncthreads();
     if (*flag) return false;
-    // (2) TRSM: L(it,kt) = C(it,kt) L(kt,kt)^-T for it = kt+1..T; 4 tiles per
-    // warp pass, one row per lane
-    const double* lk = tl + tidx(kt, kt) * 64;
-    const double* iv = invd + 8 * kt;
-    const int ntile = T - kt;
-    for (int base = warp * 4; base < ntile; base += nw * 4) {
-      const int g = base + (lane >> 3);
-      const int r = lane & 7;
-      if (g < ntile) {
-        double* ct = tl + tidx(kt + 1 + g, kt) * 64;
-        double x[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          double v = ct[eidx(r, c)];
-#pragma unroll
-          for (int cc = 0; cc < c; ++cc) v -= x[cc] * lk[eidx(c, cc)];
-          x[c] = v * iv[c];
-        }
-#pragma unroll
-        for (int c = 0; c < 8; ++c) ct[eidx(r, c)] = x[c];
+    // (2) TRSM: L(it,kt) = C(it,kt) L_kk^-T as a product with Linv^T (DMMA)
+    if (warp != 0) {
+      const double* li = tl + tidx(kt, kt) * 64;  // L_kk^-1
+      const double bl0 = li[eidx(fr, fk)], bl1 = li[eidx(fr, 4 + fk)];
+      for (int it = kt + warp; it <= T; it += nw - 1) {
+        double* ct = tl + tidx(it, kt) * 64;
+        const double a0 = ct[eidx(fr, fk)], a1 = ct[eidx(fr, 4 + fk)];
+        double d0 = 0.0, d1 = 0.0;
+        dmma_884(d0, d1, a0, bl0);
+        dmma_884(d0, d1, a1, bl1);
+        __syncwarp();
+        ct[e0] = d0;
+        ct[e1] = d1;
       }
     }
     __syncthreads();
@@ -112,17 +142,15 @@ __device__ bool tiled_chol_fwd(double* tl, int T, double* invd, int* flag) {
   return true;
 }
 
-// Back substitution L^T z = y; y is row 0 of the RHS tiles, z (8T) written
-// to `z`.  part: 8 * nwarps scratch.
-__device__ void tiled_back_subst(const double* tl, int T, const double* invd, double* z,
-                                 double* part) {
+// Back substitution L^T z = y with the L_kk^-1 held in the diagonal tiles;
+// y is row 0 of the RHS tiles, z (8T) written to `z`.  part: 8 * nwarps.
+__device__ void tiled_back_subst(const double* tl, int T, double* z, double* part) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = threadIdx.x; i < 8 * T; i += blockDim.x)
     z[i] = tl[tidx(T, i >> 3) * 64 + eidx(0, i & 7)];
   __syncthreads();
   const int r = lane & 7, cg = lane >> 3;
   for (int it = T - 1; it >= 0; --it) {
-    // partial sums of L(jt,it)^T z_jt over jt > it
     double acc = 0.0;
     for (int jt = it + 1 + warp; jt < T; jt += nw) {
       const double* t = tl + tidx(jt, it) * 64;
@@ -139,15 +167,15 @@ __device__ void tiled_back_subst(const double* tl, int T, const double* invd, do
         v = z[8 * it + lane];
         for (int w = 0; w < nw; ++w) v -= part[w * 8 + lane];
       }
-      const double* t = tl + tidx(it, it) * 64;
-      const double* iv = invd + 8 * it;
-      // upper-triangular solve with L(it,it)^T, rows 7..0
-      for (int rr = 7; rr >= 0; --rr) {
-        const double xr = __shfl_sync(0xffffffffu, v, rr) * iv[rr];
-        if (lane == rr) v = xr;
-        if (lane < rr) v -= t[eidx(rr, lane)] * xr;
+      // z_it = L_kk^-T v: z[r] = sum_{c >= r} Linv[c][r] v[c]
+      const double* li = tl + tidx(it, it) * 64;
+      double zr = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double vc = __shfl_sync(0xffffffffu, v, c);
+        if (c >= r) zr += li[eidx(c, r)] * vc;
       }
-      if (lane < 8) z[8 * it + lane] = v;
+      if (lane < 8) z[8 * it + lane] = zr;
     }
     __syncthreads();
   }

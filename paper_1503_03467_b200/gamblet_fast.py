@@ -399,6 +399,7 @@ def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     (x, iterations, rel_residual, converged, breakdown_iteration, state)."""
     if max_iter is None:
         max_iter = max(200, 2 * op.n)
+    max_iter = min(max_iter, MAX_ITER_CAP)
     kr = kr or _Krylov(op.npad)
     st = dv.stream()
     x, r, p, Ap = op.vec(), op.vec(), op.vec(), op.vec()
@@ -430,6 +431,7 @@ def _pcg(op, b, rel_tol, max_iter=None, kr=None):
         return _cg(op, b, rel_tol, max_iter=max_iter, kr=kr)
     if max_iter is None:
         max_iter = max(200, 2 * op.n)
+    max_iter = min(max_iter, MAX_ITER_CAP)
     inv = op.bj_inv()
     kr = kr or _Krylov(op.npad)
     st = dv.stream()
@@ -524,6 +526,9 @@ _SPECTRAL_LOG = []
 # the FP64-bound patch factorizations of the main stream
 SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
 PIPELINE_SOLVE = __import__("os").environ.get("GB_PIPELINE", "1") == "1"
+# safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
+# it; converging solves here need < 2000)
+MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
 
 
 class _SpectralPool:
