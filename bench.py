@@ -164,10 +164,9 @@ def kernel_timings(levels, q):
     b.record()
     torch.cuda.synchronize()
     spmv_ms = a.elapsed_time(b) / reps
-    S = op.slots
     W2 = 2 * op.w + 1
     window = W2 * (64 + 2 * op.w) * 3 * 8 * ((op.L // 64) * op.L)
-    spmv_bytes = 8 * op.n * (S + (S & 1)) + window + 8 * op.n
+    spmv_bytes = 8 * op.n * op.stored_slots + window + 8 * op.n
     its = sum(d["power"] + sum(d["inner"]) + len(d["inner"]) for d in gf._SPECTRAL_LOG[-(q - 1):]
               if d["n"] == op.n)
     B = lv.raw("subband")
@@ -184,7 +183,8 @@ def kernel_timings(levels, q):
     b.record()
     torch.cuda.synchronize()
     corr_ms = a.elapsed_time(b)
-    return {"spmv": {"ms": spmv_ms, "bytes": spmv_bytes, "launches_per_step": its},
+    return {"layout": op.layout,
+            "spmv": {"ms": spmv_ms, "bytes": spmv_bytes, "launches_per_step": its},
             "corr": {"ms": corr_ms, "flops": gf._patch_flops(B.L, rho, 3)}}
 
 
@@ -236,6 +236,12 @@ def run_ours(args, rank, world, local_rank):
     phase_flops = {k: v / args.steps for k, v in dv.Prof.flops.items()}
     phase_bytes = {k: v / args.steps for k, v in dv.Prof.bytes.items()}
     phase_counts = {k: v // args.steps for k, v in dv.Prof.counts().items()}
+    # timeline of the last step: (start, end) ms of every phase instance,
+    # relative to the first event recorded in that step
+    evs = dv.Prof.events[-(len(dv.Prof.events) // args.steps):]
+    t0 = evs[0][1]
+    timeline = [(lbl, round(t0.elapsed_time(a), 2), round(t0.elapsed_time(b_), 2))
+                for lbl, a, b_ in evs]
     dv.Prof.reset(enabled=False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -282,12 +288,15 @@ def run_ours(args, rank, world, local_rank):
     # subband iterations are ~all SpMV time); algorithmic bytes = the box
     # values the format must stream (rows x slots x 8) + x window + y
     sp = kern["spmv"]
+    op_layout = kern["layout"]
     achieved = sp["bytes"] / (sp["ms"] * 1e-3) / 1e9
     prof_file = ROOT / "profiles" / "ncu_traffic.json"
     traffic = None
     if prof_file.exists():
         traffic = json.loads(prof_file.read_text()).get("k_tcg_spmv_tiled")
-    roof = {"kernel": "k_tcg_spmv_tiled / k_tpow_apply_tiled (finest-level S B S SpMV)",
+    roof = {"kernel": ("k_sym_apply (finest-level S B S SpMV, symmetric upper-half storage)"
+                       if op_layout == 1 else
+                       "k_tcg_spmv_tiled / k_tpow_apply_tiled (finest-level S B S SpMV)"),
             "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
             "peak_source": hbm_src,
@@ -342,6 +351,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks,
         "phases_ms": {k: round(v, 3) for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
         "phase_launch_groups": phase_counts,
+        "timeline_last_step_ms": timeline if args.timeline else None,
         "fp64_peak_tflops": {k: round(v, 2) for k, v in fp64.items()},
         "subband_iterations": iters.get("line8"),
         "spectral_iterations": [{"n": d["n"], "power": d["power"], "inner_cg": d["inner"]}
@@ -389,6 +399,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--q", type=int, default=None, help="override the config's q")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--timeline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

@@ -153,6 +153,13 @@ int gb_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, double
                        double tol, int iters, void* state, double* partials, void* stream);
 int gb_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
                   void* stream);
+/* layout argument of the Krylov entries: 0 = full blocked slot-major box
+ * (gb_scale_box_T), 1 = symmetric upper half (gb_scale_box_symT; tiled
+ * levels only, gb_sym_supported) */
+size_t gb_boxsym_elems(int L, int w);
+int gb_sym_supported(int L, int nr, int w);
+int gb_scale_box_symT(int L, int w, const double* B, const double* s, double* UsT,
+                      void* stream);
 /* v3 operator: blocked slot-major S B S (BsT[(r/32)*S*32 + j*32 + r%32]),
  * one thread per row; gb_boxT_elems gives the allocation size in doubles */
 size_t gb_boxT_elems(int L, int nr, int w);
@@ -160,11 +167,11 @@ int gb_scale_box_T(int L, int nr, int w, const double* B, const double* s, doubl
                    void* stream);
 int gb_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
                       double* p, double* Ap, int iters, void* state, double* partials,
-                      void* stream);
+                      void* stream, int layout);
 int gb_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
-                       double tol, int iters, void* state, double* partials, void* stream);
+                       double tol, int iters, void* state, double* partials, void* stream, int layout);
 int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
-                  void* stream);
+                  void* stream, int layout);
 /* block-Jacobi (2x2 parents = 12x12 blocks) PCG for the subband systems */
 int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream);
 int gb_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
@@ -172,7 +179,19 @@ int gb_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p,
                  double* partials, void* stream);
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
-                       double* partials, void* stream);
+                       double* partials, void* stream, int layout);
+/* whole Krylov loops driven from C (chunked launches, pinned state reads);
+ * host_state: pinned host buffer of gb_kstate_bytes() bytes */
+int gb_sync_read(const void* dev, void* host, size_t bytes, void* stream);
+int gb_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, double* p,
+                 double* Ap, void* state, double* partials, void* host_state, int max_chunk,
+                 void* stream, int layout);
+int gb_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+                  double* p, double* Ap, double* z, void* state, double* partials,
+                  void* host_state, int max_chunk, void* stream, int layout);
+int gb_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,
+                  void* state, double* partials, void* host_state, int max_chunk,
+                  void* stream, int layout);
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream);
 int gb_scale_by_norm(int64_t n, const double* a, const double* norm2, int which,

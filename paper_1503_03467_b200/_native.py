@@ -64,12 +64,19 @@ _SIGS = {
     "gb_pbox_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
     "gb_boxT_elems": ([_I, _I, _I], _Z),
     "gb_scale_box_T": ([_I, _I, _I, _P, _P, _P, _P], _I),
-    "gb_tcg_iterations": ([_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
-    "gb_tpow_iterations": ([_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P], _I),
-    "gb_tbox_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb_tcg_iterations": ([_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I], _I),
+    "gb_tpow_iterations": ([_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _I], _I),
+    "gb_tbox_apply": ([_I, _I, _I, _P, _P, _P, _P, _I], _I),
+    "gb_boxsym_elems": ([_I, _I], _Z),
+    "gb_sym_supported": ([_I, _I, _I], _I),
+    "gb_scale_box_symT": ([_I, _I, _P, _P, _P, _P], _I),
     "gb_bj_setup": ([_I, _I, _P, _P, _P, _P], _I),
     "gb_bjcg_init": ([_I, _I, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
-    "gb_bjcg_iterations": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
+    "gb_bjcg_iterations": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I], _I),
+    "gb_sync_read": ([_P, _P, _Z, _P], _I),
+    "gb_tcg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
+    "gb_bjcg_solve": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
+    "gb_tpow_solve": ([_I, _I, _I, _P, _P, _P, _D, _P, _P, _P, _I, _P, _I], _I),
     "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),
     "gb_box_apply": ([_I, _I, _I, _P, _P, _I, _P, _P, _P], _I),

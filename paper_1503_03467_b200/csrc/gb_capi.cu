@@ -23,7 +23,8 @@ int gbk_csr_to_dense(int nrows, int ncols, const int32_t* indptr, const int32_t*
 int gbk_eye(int n, double* out, cudaStream_t s);
 
 static thread_local char g_err[512];
-static unsigned long long g_launches = 0;  // kernels launched through this ABI
+#include <atomic>
+static std::atomic<unsigned long long> g_launches{0};  // kernels launched through this ABI
 #define COUNT(n) (g_launches += (unsigned long long)(n))
 
 static int wrap(int e, const char* what) {
@@ -43,8 +44,8 @@ static int invalid(const char* msg) {
 
 extern "C" {
 
-int gb_abi_version(void) { return 1; }
-unsigned long long gb_launch_count(void) { return g_launches; }
+int gb_abi_version(void) { return 2; }
+unsigned long long gb_launch_count(void) { return g_launches.load(); }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
   int n = 0;
@@ -264,23 +265,24 @@ int gb_scale_box_T(int L, int nr, int w, const double* B, const double* s, doubl
 }
 int gb_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
                       double* p, double* Ap, int iters, void* state, double* partials,
-                      void* stream) {
+                      void* stream, int layout) {
   COUNT(3 * (unsigned long long)iters);
   return wrap(gbk_tcg_iterations(L, nr, w, BsT, x, r, p, Ap, iters, state, partials,
-                                 ST(stream)),
+                                 ST(stream), layout),
               "tcg_iterations");
 }
 int gb_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
-                       double tol, int iters, void* state, double* partials, void* stream) {
+                       double tol, int iters, void* state, double* partials, void* stream,
+                       int layout) {
   COUNT(3 * (unsigned long long)iters);
   return wrap(gbk_tpow_iterations(L, nr, w, BsT, x, y, tol, iters, state, partials,
-                                  ST(stream)),
+                                  ST(stream), layout),
               "tpow_iterations");
 }
 int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
-                  void* stream) {
+                  void* stream, int layout) {
   COUNT(1);
-  return wrap(gbk_tbox_apply(L, nr, w, BsT, x, y, ST(stream)), "tbox_apply");
+  return wrap(gbk_tbox_apply(L, nr, w, BsT, x, y, ST(stream), layout), "tbox_apply");
 }
 int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream) {
   if (L < 2 || (L & 1)) return invalid("bj_setup: parent grid side must be even");
@@ -297,11 +299,48 @@ int gb_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p,
 }
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
-                       double* partials, void* stream) {
+                       double* partials, void* stream, int layout) {
   COUNT(3 * (unsigned long long)iters);
   return wrap(gbk_bjcg_iterations(L, w, BsT, inv, x, r, p, Ap, z, iters, state, partials,
-                                  ST(stream)),
+                                  ST(stream), layout),
               "bjcg_iterations");
+}
+int gb_sync_read(const void* dev, void* host, size_t bytes, void* stream) {
+  return wrap(gbk_sync_read(dev, host, bytes, ST(stream)), "sync_read");
+}
+int gb_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, double* p,
+                 double* Ap, void* state, double* partials, void* host_state, int max_chunk,
+                 void* stream, int layout) {
+  long long n = 0;
+  const int e = gbk_tcg_solve(L, nr, w, BsT, x, r, p, Ap, state, partials, host_state,
+                              max_chunk, ST(stream), &n, layout);
+  COUNT(n);
+  return wrap(e, "tcg_solve");
+}
+int gb_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+                  double* p, double* Ap, double* z, void* state, double* partials,
+                  void* host_state, int max_chunk, void* stream, int layout) {
+  long long n = 0;
+  const int e = gbk_bjcg_solve(L, w, BsT, inv, x, r, p, Ap, z, state, partials, host_state,
+                               max_chunk, ST(stream), &n, layout);
+  COUNT(n);
+  return wrap(e, "bjcg_solve");
+}
+int gb_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,
+                  void* state, double* partials, void* host_state, int max_chunk,
+                  void* stream, int layout) {
+  long long n = 0;
+  const int e = gbk_tpow_solve(L, nr, w, BsT, x, y, tol, state, partials, host_state,
+                               max_chunk, ST(stream), &n, layout);
+  COUNT(n);
+  return wrap(e, "tpow_solve");
+}
+size_t gb_boxsym_elems(int L, int w) { return gbk_boxsym_elems(L, w); }
+int gb_sym_supported(int L, int nr, int w) { return gbk_sym_supported(L, nr, w); }
+int gb_scale_box_symT(int L, int w, const double* B, const double* s, double* UsT,
+                      void* stream) {
+  COUNT(1);
+  return wrap(gbk_scale_box_symT(L, w, B, s, UsT, ST(stream)), "scale_box_symT");
 }
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {

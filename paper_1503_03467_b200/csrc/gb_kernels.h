@@ -118,11 +118,12 @@ int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, dou
                     cudaStream_t s);
 int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
                        double* p, double* Ap, int iters, void* st, double* part,
-                       cudaStream_t s);
+                       cudaStream_t s, int layout);
 int gbk_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
-                        double tol, int iters, void* st, double* part, cudaStream_t s);
+                        double tol, int iters, void* st, double* part, cudaStream_t s,
+                        int layout);
 int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
-                   cudaStream_t s);
+                   cudaStream_t s, int layout);
 size_t gbk_boxT_elems(int L, int nr, int w);
 int gbk_bj_setup(int L, int w, const double* B, const double* sv, double* inv,
                  cudaStream_t s);
@@ -131,4 +132,18 @@ int gbk_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p
                   cudaStream_t s);
 int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                         double* r, double* p, double* Ap, double* z, int iters, void* st,
-                        double* part, cudaStream_t s);
+                        double* part, cudaStream_t s, int layout);
+int gbk_sync_read(const void* dev, void* host, size_t bytes, cudaStream_t s);
+int gbk_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, double* p,
+                  double* Ap, void* st, double* part, void* host_state, int max_chunk,
+                  cudaStream_t s, long long* launches, int layout);
+int gbk_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+                   double* p, double* Ap, double* z, void* st, double* part, void* host_state,
+                   int max_chunk, cudaStream_t s, long long* launches, int layout);
+int gbk_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,
+                   void* st, double* part, void* host_state, int max_chunk, cudaStream_t s,
+                   long long* launches, int layout);
+size_t gbk_boxsym_elems(int L, int w);
+int gbk_sym_supported(int L, int nr, int w);
+int gbk_scale_box_symT(int L, int w, const double* B, const double* sv, double* UsT,
+                       cudaStream_t s);

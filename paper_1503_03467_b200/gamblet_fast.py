@@ -335,15 +335,30 @@ def _blocks_for(nmax, count):
 # ---------------------------------------------------------------------------
 
 class _Krylov:
+    """Device iteration state + pinned host mirror (reads go through C with
+    the GIL released, so side-stream solves never starve the main thread)."""
+
     def __init__(self, n):
         self.n = n
-        self.state = dv.empty(nat.query("gb_kstate_bytes"), torch.uint8)
+        nb = nat.query("gb_kstate_bytes")
+        self.state = dv.empty(nb, torch.uint8)
+        self.host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
         self.part = dv.empty(2 * nat.query("gb_red_blocks"))
         self.dots = dv.empty(4)
+        self.hdots = torch.empty(4, dtype=torch.float64, pin_memory=True)
         nat.call("gb_state_reset", dv.ptr(self.state), 0, dv.stream())
 
     def read(self):
-        return dv.to_host(self.state).view(_KSTATE)[0]
+        nat.call("gb_sync_read", dv.ptr(self.state), self.host.data_ptr(),
+                 self.host.numel(), dv.stream())
+        return self.host.numpy().view(_KSTATE)[0]
+
+    def host_view(self):
+        return self.host.numpy().view(_KSTATE)[0]
+
+    def read_dots(self, dots):
+        nat.call("gb_sync_read", dv.ptr(dots), self.hdots.data_ptr(), 32, dv.stream())
+        return self.hdots.numpy()
 
 
 class _POp:
@@ -356,9 +371,16 @@ class _POp:
         self.slots = box.slots
         self.Lpad = self.L + 2 * self.w
         self.npad = self.Lpad * self.Lpad * self.nr
-        self.BsT = dv.empty(nat.query("gb_boxT_elems", self.L, self.nr, self.w))
-        nat.call("gb_scale_box_T", self.L, self.nr, self.w, dv.ptr(box.vals), dv.ptr(s),
-                 dv.ptr(self.BsT), dv.stream())
+        self.layout = 1 if (SYMMETRIC_SPMV and
+                            nat.query("gb_sym_supported", self.L, self.nr, self.w)) else 0
+        if self.layout == 1:
+            self.BsT = dv.empty(nat.query("gb_boxsym_elems", self.L, self.w))
+            nat.call("gb_scale_box_symT", self.L, self.w, dv.ptr(box.vals), dv.ptr(s),
+                     dv.ptr(self.BsT), dv.stream())
+        else:
+            self.BsT = dv.empty(nat.query("gb_boxT_elems", self.L, self.nr, self.w))
+            nat.call("gb_scale_box_T", self.L, self.nr, self.w, dv.ptr(box.vals), dv.ptr(s),
+                     dv.ptr(self.BsT), dv.stream())
         self._box, self._s, self._bj = box, s, None
 
     def bj_inv(self):
@@ -371,8 +393,17 @@ class _POp:
         return self._bj
 
     @property
+    def stored_slots(self):
+        """Matrix slots per row the SpMV streams from HBM (upper half only in
+        the symmetric layout)."""
+        if self.layout == 1:
+            su = 3 * (2 * self.w * self.w + 2 * self.w) + 3
+            return su + (su & 1)
+        return self.slots + (self.slots & 1)
+
+    @property
     def spmv_bytes(self):
-        return 8 * self.n * self.slots + 3 * 8 * self.npad
+        return 8 * self.n * self.stored_slots + 3 * 8 * self.npad
 
     def vec(self):
         return dv.zeros(self.npad)
@@ -391,7 +422,7 @@ class _POp:
 
     def apply(self, xp, yp):
         nat.call("gb_tbox_apply", self.L, self.nr, self.w, dv.ptr(self.BsT), dv.ptr(xp),
-                 dv.ptr(yp), dv.stream())
+                 dv.ptr(yp), dv.stream(), self.layout)
 
 
 def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
@@ -411,14 +442,10 @@ def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     nat.call("gb_cg_init", op.npad, dv.ptr(b), dv.ptr(x0), dv.ptr(Ax0), dv.ptr(x),
              dv.ptr(r), dv.ptr(p), float(rel_tol), int(max_iter), dv.ptr(kr.state),
              dv.ptr(kr.part), st)
-    chunk = 8
-    while True:
-        nat.call("gb_tcg_iterations", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(r),
-                 dv.ptr(p), dv.ptr(Ap), chunk, dv.ptr(kr.state), dv.ptr(kr.part), st)
-        h = kr.read()
-        if h["done"]:
-            break
-        chunk = min(2 * chunk, 128)
+    nat.call("gb_tcg_solve", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(r),
+             dv.ptr(p), dv.ptr(Ap), dv.ptr(kr.state), dv.ptr(kr.part), kr.host.data_ptr(),
+             128, st, op.layout)
+    h = kr.host_view()
     rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
     return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
 
@@ -440,15 +467,10 @@ def _pcg(op, b, rel_tol, max_iter=None, kr=None):
     nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), dv.ptr(x), dv.ptr(r), dv.ptr(p),
              dv.ptr(z), dv.ptr(inv), float(rel_tol), int(max_iter), dv.ptr(kr.state),
              dv.ptr(kr.part), st)
-    chunk = 8
-    while True:
-        nat.call("gb_bjcg_iterations", op.L, op.w, dv.ptr(op.BsT), dv.ptr(inv), dv.ptr(x),
-                 dv.ptr(r), dv.ptr(p), dv.ptr(Ap), dv.ptr(z), chunk, dv.ptr(kr.state),
-                 dv.ptr(kr.part), st)
-        h = kr.read()
-        if h["done"]:
-            break
-        chunk = min(2 * chunk, 128)
+    nat.call("gb_bjcg_solve", op.L, op.w, dv.ptr(op.BsT), dv.ptr(inv), dv.ptr(x),
+             dv.ptr(r), dv.ptr(p), dv.ptr(Ap), dv.ptr(z), dv.ptr(kr.state), dv.ptr(kr.part),
+             kr.host.data_ptr(), 128, st, op.layout)
+    h = kr.host_view()
     rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
     return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
 
@@ -471,14 +493,10 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
              dv.ptr(kr.state), dv.ptr(kr.part), st)
     nat.call("gb_scale_by_norm", op.npad, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
     nat.call("gb_state_reset", dv.ptr(kr.state), max_iter, st)
-    chunk = 8
-    while True:
-        nat.call("gb_tpow_iterations", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(y),
-                 float(tol), chunk, dv.ptr(kr.state), dv.ptr(kr.part), st)
-        h = kr.read()
-        if h["done"]:
-            break
-        chunk = min(2 * chunk, 128)
+    nat.call("gb_tpow_solve", op.L, op.nr, op.w, dv.ptr(op.BsT), dv.ptr(x), dv.ptr(y),
+             float(tol), dv.ptr(kr.state), dv.ptr(kr.part), kr.host.data_ptr(), 128, st,
+             op.layout)
+    h = kr.host_view()
     lam_max = float(h["lam"])
     calls += int(h["it"]) + (0 if h["ynorm"] != 0 else 1)
 
@@ -508,7 +526,7 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
         calls += 1
         nat.call("gb_dot2", op.npad, dv.ptr(xn), dv.ptr(Ax), None, dv.ptr(dots[2:]),
                  dv.ptr(kr.state), dv.ptr(kr.part), st)
-        d = dv.to_host(dots)
+        d = kr.read_dots(dots)
         if d[0] == 0.0:
             raise NumericalError("inverse iteration broke down: A^{-1} x = 0")
         lam_min = float(d[2])
@@ -525,60 +543,80 @@ _SPECTRAL_LOG = []
 # lambda estimates run on side streams (one per worker thread) so they overlap
 # the FP64-bound patch factorizations of the main stream
 SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
-PIPELINE_SOLVE = __import__("os").environ.get("GB_PIPELINE", "1") == "1"
 # safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
 # it; converging solves here need < 2000)
+SPECTRAL_PRIORITY = int(__import__("os").environ.get("GB_SPECTRAL_PRIORITY", "-1"))
+# symmetric upper-half Krylov copy (opt-in): halves HBM bytes but the lower
+# half is re-read through L2 with too many misses -- measured 0.32-0.39 ms vs
+# 0.24 ms for the full box at q=10, so the full layout is the default
+SYMMETRIC_SPMV = __import__("os").environ.get("GB_SYM_SPMV", "0") == "1"
 MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
 
 
-class _SpectralPool:
-    """Runs _eig_extremes for each level on its own stream/thread; the
-    operator (slot-major S B S) is ordered after its producer by an event and
-    stays alive on the level until join()."""
+class _LevelTasks:
+    """Per-level device work that depends only on that level's operator: the
+    lambda estimates of S B^(k) S (sparse_core.eig_extremes) and, inside
+    fast_solve, the subband solve and increment of level k.  Each task runs
+    on a worker thread with its own high-priority stream (ordered after the
+    operator by an event) so the HBM-bound Krylov work of level k overlaps
+    the FP64-bound setup of the coarser levels on the main stream."""
 
     _pool = None
     _local = threading.local()
 
-    def __init__(self):
-        if _SpectralPool._pool is None:
-            _SpectralPool._pool = concurrent.futures.ThreadPoolExecutor(
-                max_workers=SPECTRAL_WORKERS, thread_name_prefix="gb-spectral")
+    def __init__(self, solver=None):
+        if _LevelTasks._pool is None:
+            _LevelTasks._pool = concurrent.futures.ThreadPoolExecutor(
+                max_workers=SPECTRAL_WORKERS, thread_name_prefix="gb-level")
         self.futures = []
+        self.solver = solver
 
     @classmethod
     def _stream(cls):
         st = getattr(cls._local, "stream", None)
         if st is None:
             torch.cuda.set_device(dv.device())
-            st = torch.cuda.Stream(device=dv.device())
+            st = torch.cuda.Stream(device=dv.device(), priority=SPECTRAL_PRIORITY)
             cls._local.stream = st
         return st
 
-    def submit(self, level, op):
+    def submit(self, level, op, k, g=None):
         ev = torch.cuda.Event()
         ev.record()
-        self.futures.append(self._pool.submit(self._run, level, op, ev))
+        self.futures.append(self._pool.submit(self._run, level, op, k, g, ev))
 
-    @classmethod
-    def _run(cls, level, op, ev):
-        st = cls._stream()
+    def _run(self, level, op, k, g, ev):
+        st = self._stream()
+        calls = 0
         with torch.cuda.stream(st):
             st.wait_event(ev)
-            with dv.phase("spectral"):
-                lam_min, lam_max, calls = _eig_extremes(op)
+            if g is not None:
+                g.record_stream(st)  # main-stream tensor read on this stream
+            if SPECTRAL:
+                with dv.phase("spectral"):
+                    lam_min, lam_max, calls = _eig_extremes(op)
+                level.lambda_min_subband = lam_min
+                level.lambda_max_subband = lam_max
+            if self.solver is not None and g is not None:
+                self.solver.subband(k, g, pipelined=True)
             done = torch.cuda.Event()
             done.record(st)
-        level.lambda_min_subband = lam_min
-        level.lambda_max_subband = lam_max
         return calls, op, done
 
     def join(self, counter):
-        for f in self.futures:
-            calls, op, done = f.result()
+        futs, self.futures = self.futures, []
+        err = None
+        for f in futs:
+            try:
+                calls, op, done = f.result()
+            except Exception as e:  # keep joining, re-raise the first error
+                err = err or e
+                continue
             torch.cuda.current_stream().wait_event(done)
             counter.add("spectral", 2 * op.n * op.slots * calls)
             dv.Prof.add_work("spectral", nbytes=calls * op.spmv_bytes)
-        self.futures = []
+        if err is not None:
+            raise err
 
 
 # ---------------------------------------------------------------------------
@@ -725,7 +763,7 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
 
 def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
                      counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None, _spool=None,
-                     _pipe=None):
+                     _g=None):
     """One localized downward step k -> k-1 (gamblet_fast.py:501-632).
     Mutates `level` (W, B, s_B, D, R, lambdas, repair) and returns level k-1."""
     k = level.k
@@ -770,15 +808,12 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         # K7: spectral extremes of S B S (gamblet_fast.py:531-534)
         with dv.phase("level_blocks"):
             op = _POp(B, sB)
-        spool = _spool if _spool is not None else _SpectralPool()
-        if SPECTRAL:
-            spool.submit(level, op)
         level._op = op
         level.subband = B
         level.subband_scale = sB
         level.w_variant = w_variant
-        if _pipe is not None:
-            _pipe.notify("op", k)
+        spool = _spool if _spool is not None else _LevelTasks()
+        spool.submit(level, op, k, _g)
 
         # K4: correction patches -> D^T with the row-tail trim fused
         Dt = dv.empty(P * dv.box_slots(rho, 3))
@@ -844,9 +879,6 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
     level._repair_slot_b = ib
     nxt = LocalGambletLevel(k - 1, psin, BoxMatrix(An, Lp, 1, wA2, 1))
     nxt._repair_slot_a = ia
-    if _pipe is not None:
-        _pipe.levels_ref[k - 1] = nxt
-        _pipe.notify("step", k)
     if _spool is None:
         spool.join(counter)
     if _ctx is None:
@@ -871,36 +903,30 @@ def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_
     levels = {q: LocalGambletLevel(q, psi, Aq)}
     levels[q]._repair_slot_a = ia
     level = levels[q]
-    spool = _SpectralPool()
-    pipe = None
-    if _load is not None and PIPELINE_SOLVE:  # pipelined solve: _load = (g_device, records)
-        pipe = _SolvePipeline(levels, _load[0], tree, schedule.subband_tol(), counter,
-                              _load[1])
-        pipe.levels_ref = levels
-    ok = False
+    solver = None
+    gk = None
+    if _load is not None:  # fast_solve: (g_device, records) -- solve pipelined per level
+        solver = _LevelSolver(levels, tree, schedule.subband_tol(), counter, _load[1])
+        gk = _load[0]
+    spool = _LevelTasks(solver)
     try:
         for k in range(q, 1, -1):
             level = local_level_step(level, tree, schedule, w_variant=w_variant, c_tol=c_tol,
                                      counter=counter, dense_cutoff=dense_cutoff, _ctx=ctx,
-                                     _spool=spool, _pipe=pipe)
+                                     _spool=spool, _g=gk)
             levels[k - 1] = level
-        if pipe is not None:
-            pipe.notify("step", 1)
-        ok = True
+            if solver is not None:
+                gk = solver.restrict(k, gk)     # g^(k-1) = R^(k) g^(k), main stream
     finally:
-        if pipe is not None and not ok:
-            pipe.abort()
         spool.join(counter)
     ctx.check()
-    if pipe is not None:
-        fast_transform.last_solve = pipe.join()
-    elif _load is not None:
-        fast_transform.last_solve = _solve_levels(levels, _load[0], tree, schedule,
-                                                  schedule.subband_tol(), counter, _load[1])
     for k, lv in levels.items():
         rep = ctx.repair_of.get(getattr(lv, "_repair_slot_a", -1), 0.0)
         rep_b = ctx.repair_of.get(getattr(lv, "_repair_slot_b", -1), 0.0)
         lv.symmetry_repair = max(rep, rep_b)
+    if solver is not None:
+        solver.coarse(gk)
+        fast_transform.last_solve = solver.finish()
     return levels, counter
 
 
@@ -1087,65 +1113,6 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
         g = sv.restrict(k, g)
     sv.coarse(g)
     return sv.finish()
-
-
-class _SolvePipeline:
-    """Runs the solve phase on its own stream/thread, level by level, as the
-    transform produces the operators: level k's subband solve starts once
-    its S B S is built (event "op"), the restriction of the load once level
-    k's step has finished (event "step").  Same kernels and inputs as
-    _solve_levels, so results are identical."""
-
-    _pool = None
-
-    def __init__(self, levels, g, tree, tol, counter, records):
-        import queue
-        if _SolvePipeline._pool is None:
-            _SolvePipeline._pool = concurrent.futures.ThreadPoolExecutor(
-                max_workers=1, thread_name_prefix="gb-solve")
-        self.q = queue.Queue()
-        self.sv = _LevelSolver(levels, tree, tol, counter, records)
-        self.tree = tree
-        ev = torch.cuda.Event()
-        ev.record()
-        self.fut = self._pool.submit(self._run, g, ev)
-
-    def notify(self, kind, k):
-        ev = torch.cuda.Event()
-        ev.record()
-        self.q.put((kind, k, ev))
-
-    def _wait(self, want):
-        kind, k, ev = self.q.get()
-        if kind == "abort":
-            raise RuntimeError("solve pipeline aborted")
-        assert (kind, k) == want, ((kind, k), want)
-        torch.cuda.current_stream().wait_event(ev)
-
-    def _run(self, g, ev0):
-        torch.cuda.set_device(dv.device())
-        st = torch.cuda.Stream(device=dv.device())
-        with torch.cuda.stream(st):
-            st.wait_event(ev0)
-            for k in range(self.tree.q, 1, -1):
-                self._wait(("op", k))
-                self.sv.subband(k, g, pipelined=True)
-                self._wait(("step", k))
-                g = self.sv.restrict(k, g)
-            self._wait(("step", 1))
-            self.sv.coarse(g)
-            out = self.sv.finish()
-            done = torch.cuda.Event()
-            done.record(st)
-        return out, done
-
-    def abort(self):
-        self.q.put(("abort", 0, None))
-
-    def join(self):
-        out, done = self.fut.result()
-        torch.cuda.current_stream().wait_event(done)
-        return out
 
 
 # ---------------------------------------------------------------------------
