@@ -199,6 +199,18 @@ int gb_scale_by_norm(int64_t n, const double* a, const double* norm2, int which,
 int gb_box_apply(int L, int nr, int w, const double* B, const double* s, int mode,
                  const double* x, double* y, void* stream);
 
+/* general CSR operator: sparse_core.cg_solve / eig_extremes (sparse_core.py:
+ * 126-165, 232-278) on any SPD canonical CSR matrix in device memory */
+int gb_csr_apply(int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
+                 const double* x, double* y, void* stream);
+int gb_csr_cg_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
+                    const double* data, double* x, double* r, double* p, double* Ap,
+                    void* state, double* partials, void* host_state, int max_chunk,
+                    void* stream);
+int gb_csr_pow_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
+                     const double* data, double* x, double* y, double tol, void* state,
+                     double* partials, void* host_state, int max_chunk, void* stream);
+
 /* ---- K9 load-dependent transfers (gamblet_fast.py:726-765) --------------- */
 int gb_apply_w(int Lp, const double* host_w12, const double* g, const double* s,
                double* out, void* stream);

@@ -77,6 +77,9 @@ _SIGS = {
     "gb_tcg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
     "gb_bjcg_solve": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
     "gb_tpow_solve": ([_I, _I, _I, _P, _P, _P, _D, _P, _P, _P, _I, _P, _I], _I),
+    "gb_csr_apply": ([_L, _P, _P, _P, _P, _P, _P], _I),
+    "gb_csr_cg_solve": ([_L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
+    "gb_csr_pow_solve": ([_L, _P, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
     "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),
     "gb_box_apply": ([_I, _I, _I, _P, _P, _I, _P, _P, _P], _I),

@@ -342,6 +342,30 @@ int gb_scale_box_symT(int L, int w, const double* B, const double* s, double* Us
   COUNT(1);
   return wrap(gbk_scale_box_symT(L, w, B, s, UsT, ST(stream)), "scale_box_symT");
 }
+int gb_csr_apply(int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
+                 const double* x, double* y, void* stream) {
+  COUNT(1);
+  return wrap(gbk_csr_apply(n, indptr, indices, data, x, y, ST(stream)), "csr_apply");
+}
+int gb_csr_cg_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
+                    const double* data, double* x, double* r, double* p, double* Ap,
+                    void* state, double* partials, void* host_state, int max_chunk,
+                    void* stream) {
+  long long k = 0;
+  const int e = gbk_csr_cg_solve(n, indptr, indices, data, x, r, p, Ap, state, partials,
+                                 host_state, max_chunk, ST(stream), &k);
+  COUNT(k);
+  return wrap(e, "csr_cg_solve");
+}
+int gb_csr_pow_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
+                     const double* data, double* x, double* y, double tol, void* state,
+                     double* partials, void* host_state, int max_chunk, void* stream) {
+  long long k = 0;
+  const int e = gbk_csr_pow_solve(n, indptr, indices, data, x, y, tol, state, partials,
+                                  host_state, max_chunk, ST(stream), &k);
+  COUNT(k);
+  return wrap(e, "csr_pow_solve");
+}
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {
   COUNT(1);

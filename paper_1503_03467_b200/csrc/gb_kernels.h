@@ -147,3 +147,13 @@ size_t gbk_boxsym_elems(int L, int w);
 int gbk_sym_supported(int L, int nr, int w);
 int gbk_scale_box_symT(int L, int w, const double* B, const double* sv, double* UsT,
                        cudaStream_t s);
+int gbk_csr_apply(long long n, const int32_t* indptr, const int32_t* indices,
+                  const double* data, const double* x, double* y, cudaStream_t s);
+int gbk_csr_cg_solve(long long n, const int32_t* indptr, const int32_t* indices,
+                     const double* data, double* x, double* r, double* p, double* Ap,
+                     void* st, double* part, void* host_state, int max_chunk, cudaStream_t s,
+                     long long* launches);
+int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices,
+                      const double* data, double* x, double* y, double tol, void* st,
+                      double* part, void* host_state, int max_chunk, cudaStream_t s,
+                      long long* launches);

@@ -1793,6 +1793,66 @@ int gbk_vadd(long long n, const double* a, const double* b, double* out, cudaStr
   return (int)cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// General CSR operator (sparse_core.cg_solve / eig_extremes on any SPD CSR):
+// one warp per row, the row's stored entries in column order; mode 0 = CG
+// (p.Ap -> alpha), 1 = power (x.y, y.y -> lam, ynorm), 2 = plain y = A x.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_csr_apply(long long n, const int32_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices,
+                                                   const double* __restrict__ data,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y, KState* st,
+                                                   double* part, int mode) {
+  __shared__ double sh[32];
+  if (mode != 2 && st->done) return;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  double xy = 0.0, yy = 0.0;
+  for (long long r = wid; r < n; r += nwarps) {
+    double acc = 0.0;
+    for (int e = indptr[r] + lane; e < indptr[r + 1]; e += 32) acc += data[e] * x[indices[e]];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      y[r] = acc;
+      xy += x[r] * acc;
+      yy += acc * acc;
+    }
+  }
+  if (mode == 2) return;
+  xy = block_sum(xy, sh);
+  yy = block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = xy;
+    part[2 * blockIdx.x + 1] = yy;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      if (mode == 0) {
+        st->pAp = a;
+        if (!(a > 0.0)) {
+          st->breakdown = st->it + 1;
+          st->done = 1;
+        } else {
+          st->alpha = st->rs / a;
+        }
+      } else {
+        st->lam = a;
+        st->ynorm = sqrt(b);
+        if (st->ynorm == 0.0) {
+          st->lam = 0.0;
+          st->done = 1;
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Host-side drivers: the whole iteration loop in C (one ctypes call, GIL
 // released): launch a chunk of iterations, copy the state to pinned host
@@ -1868,4 +1928,60 @@ int gbk_scale_box_symT(int L, int w, const double* B, const double* sv, double* 
   const long long total = (long long)gbk_boxsym_elems(L, w);
   k_scale_box_symT<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, w, B, sv, UsT);
   return (int)cudaGetLastError();
+}
+
+static inline int csr_grid(long long n) { return grid_for(n * 32, 256, kRedBlocks); }
+
+int gbk_csr_apply(long long n, const int32_t* indptr, const int32_t* indices,
+                  const double* data, const double* x, double* y, cudaStream_t s) {
+  k_csr_apply<<<csr_grid(n), 256, 0, s>>>(n, indptr, indices, data, x, y, nullptr, nullptr, 2);
+  return (int)cudaGetLastError();
+}
+
+int gbk_csr_cg_solve(long long n, const int32_t* indptr, const int32_t* indices,
+                     const double* data, double* x, double* r, double* p, double* Ap,
+                     void* st, double* part, void* host_state, int max_chunk, cudaStream_t s,
+                     long long* launches) {
+  KState* h = (KState*)host_state;
+  KState* k = (KState*)st;
+  const int gv = grid_for(n, 256, kRedBlocks);
+  int chunk = 8;
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      k_csr_apply<<<csr_grid(n), 256, 0, s>>>(n, indptr, indices, data, p, Ap, k, part, 0);
+      k_cg_update<<<gv, 256, 0, s>>>(n, x, r, p, Ap, k, part);
+      k_cg_dir<<<gv, 256, 0, s>>>(n, r, p, k);
+    }
+    *launches += 3LL * chunk;
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    e = read_state(st, h, s);
+    if (e) return e;
+    if (h->done) return 0;
+    chunk = chunk * 2 < max_chunk ? chunk * 2 : max_chunk;
+  }
+}
+
+int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices,
+                      const double* data, double* x, double* y, double tol, void* st,
+                      double* part, void* host_state, int max_chunk, cudaStream_t s,
+                      long long* launches) {
+  KState* h = (KState*)host_state;
+  KState* k = (KState*)st;
+  const int gv = grid_for(n, 256, kRedBlocks);
+  int chunk = 8;
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      k_csr_apply<<<csr_grid(n), 256, 0, s>>>(n, indptr, indices, data, x, y, k, part, 1);
+      k_pow_step<<<gv, 256, 0, s>>>(n, x, y, tol, k, part);
+      k_pow_scale<<<gv, 256, 0, s>>>(n, x, y, k);
+    }
+    *launches += 3LL * chunk;
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    e = read_state(st, h, s);
+    if (e) return e;
+    if (h->done) return 0;
+    chunk = chunk * 2 < max_chunk ? chunk * 2 : max_chunk;
+  }
 }
