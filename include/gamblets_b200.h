@@ -211,6 +211,12 @@ int gb_csr_pow_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
                      const double* data, double* x, double* y, double tol, void* state,
                      double* partials, void* host_state, int max_chunk, void* stream);
 
+/* level engine: lambda estimates of S B S (power + inverse iteration, the
+ * reference algorithm) paired with the subband PCG, one S B S pass per pair
+ * of iterations (argument block: paper_1503_03467_b200/csrc/gb_engine.h) */
+struct gb_level_engine_args;
+int gb_level_engine(struct gb_level_engine_args* args, void* stream);
+
 /* ---- K9 load-dependent transfers (gamblet_fast.py:726-765) --------------- */
 int gb_apply_w(int Lp, const double* host_w12, const double* g, const double* s,
                double* out, void* stream);

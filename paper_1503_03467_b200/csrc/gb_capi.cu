@@ -366,6 +366,12 @@ int gb_csr_pow_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
   COUNT(k);
   return wrap(e, "csr_pow_solve");
 }
+int gb_level_engine(gb_level_engine_args* args, void* stream) {
+  long long n = 0;
+  const int e = gbk_level_engine(args, ST(stream), &n);
+  COUNT(n);
+  return wrap(e, "level_engine");
+}
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {
   COUNT(1);

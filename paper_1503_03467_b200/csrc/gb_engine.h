@@ -1,0 +1,31 @@
+// Argument block of the level engine (C ABI, mirrored by ctypes in
+// paper_1503_03467_b200/engine.py).  All pointers are device pointers except
+// hsta/hstb/hdots (pinned host).  Vectors are zero-halo padded.
+#pragma once
+#include <stdint.h>
+
+typedef struct gb_level_engine_args {
+  int L, w, max_chunk, max_outer;
+  const double* BsT;       /* full blocked slot-major S B S (tiled level) */
+  /* A: subband block-Jacobi PCG, already initialised (gb_bjcg_init) */
+  const double* inv;
+  double *xa, *ra, *pa, *apa, *za;
+  void* sta;
+  double* parta;
+  void* hsta;
+  /* B: lambda estimates; xb = normalized start 1 (power), x2 = normalized
+   * start 2 (inverse iteration); state reset with max_iter for the power loop */
+  double *xb, *yb, *x2, *xn, *ax, *cx, *cr, *cp, *cap;
+  void* stb;
+  double* partb;
+  void* hstb;
+  double* dots;            /* 4 device doubles */
+  double* hdots;           /* 4 pinned doubles */
+  double tol, inner_tol;
+  int64_t inner_max_iter;
+  /* outputs */
+  double lam_min, lam_max;
+  int64_t calls;
+  int power_its, n_outer, breakdown, pad;
+  int inner_its[64];
+} gb_level_engine_args;

@@ -157,3 +157,5 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
                       const double* data, double* x, double* y, double tol, void* st,
                       double* part, void* host_state, int max_chunk, cudaStream_t s,
                       long long* launches);
+#include "gb_engine.h"
+int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches);

@@ -1023,6 +1023,143 @@ __global__ void __launch_bounds__(192) k_sym_apply(int L, int w, const double* _
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Dual tiled SpMV: one pass over S B S serves two independent iterations
+// (the subband PCG "A" and the lambda-estimate iteration "B" of the same
+// level).  Each half has its own state, partials and reduction mode
+// (0 = CG p.Ap -> alpha, 1 = power x.y, y.y -> lam, ynorm); a half whose
+// state is done is skipped.  Block arrival is counted on A's state.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void finish_reduction(KState* st, int mode, double a, double b) {
+  if (mode == 0) {
+    st->pAp = a;
+    if (!(a > 0.0)) {
+      st->breakdown = st->it + 1;
+      st->done = 1;
+    } else {
+      st->alpha = st->rs / a;
+    }
+  } else {
+    st->lam = a;
+    st->ynorm = sqrt(b);
+    if (st->ynorm == 0.0) {
+      st->lam = 0.0;
+      st->done = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(192) k_dual_apply(int L, int w, const double* __restrict__ BsT,
+                                                    const double* __restrict__ xa,
+                                                    double* __restrict__ ya, KState* sa,
+                                                    double* pa, int ma,
+                                                    const double* __restrict__ xb,
+                                                    double* __restrict__ yb, KState* sb,
+                                                    double* pb, int mb) {
+  extern __shared__ double dyn[];
+  __shared__ double sh[32];
+  const bool act_a = !sa->done, act_b = !sb->done;
+  if (!act_a && !act_b) return;
+  if (!act_a || !act_b) {
+    // one live half: plain single pass
+    const double* x = act_a ? xa : xb;
+    double* y = act_a ? ya : yb;
+    KState* st = act_a ? sa : sb;
+    double* part = act_a ? pa : pb;
+    const int mode = act_a ? ma : mb;
+    const int S = (2 * w + 1) * (2 * w + 1) * 3;
+    int* offw = reinterpret_cast<int*>(dyn);
+    double* xs = dyn + ((S + 2) / 2 + 1);
+    build_offsets_window(w, offw);
+    __syncthreads();
+    double xy, yy;
+    tile_pass(L, w, BsT, x, y, offw, xs, &xy, &yy);
+    xy = block_sum(xy, sh);
+    yy = block_sum(yy, sh);
+    if (threadIdx.x == 0) {
+      part[2 * blockIdx.x] = xy;
+      part[2 * blockIdx.x + 1] = yy;
+    }
+    if (last_block(&st->counter)) {
+      double a, b;
+      final_sum2(part, gridDim.x, &a, &b, sh);
+      if (threadIdx.x == 0) {
+        st->counter = 0;
+        finish_reduction(st, mode, a, b);
+      }
+    }
+    return;
+  }
+  const int W2 = 2 * w + 1, S = W2 * W2 * 3, Sp = S + (S & 1), Lpad = L + 2 * w;
+  const int WC = kTileP + 2 * w;
+  int* offw = reinterpret_cast<int*>(dyn);
+  double* xsa = dyn + ((S + 2) / 2 + 1);
+  double* xsb = xsa + W2 * WC * 3;
+  build_offsets_window(w, offw);
+  __syncthreads();
+  const int tiles_per_row = L / kTileP;
+  const long long ntile = (long long)L * tiles_per_row;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  const int tid = threadIdx.x;
+  const int lp = tid / 3, c = tid - 3 * lp;
+  for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int ps = (int)(t / tiles_per_row), pt0 = (int)(t % tiles_per_row) * kTileP;
+    for (int e = tid; e < W2 * WC * 3; e += blockDim.x) {
+      const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
+      const long long gi = ((long long)(ps + wr) * Lpad + pt0) * 3 + rem;
+      xsa[e] = xa[gi];
+      xsb[e] = xb[gi];
+    }
+    __syncthreads();
+    const long long r = ((long long)ps * L + pt0) * 3 + tid;
+    const double2* m = reinterpret_cast<const double2*>(BsT + (r >> 5) * (32LL * Sp)) + (r & 31);
+    const double* xpa = xsa + lp * 3;
+    const double* xpb = xsb + lp * 3;
+    double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < (Sp >> 1); ++k) {
+      const double2 v = __ldg(m + 32 * k);
+      const int o0 = offw[2 * k], o1 = offw[2 * k + 1];
+      u0 = fma(v.x, xpa[o0], u0);
+      u1 = fma(v.y, xpa[o1], u1);
+      v0 = fma(v.x, xpb[o0], v0);
+      v1 = fma(v.y, xpb[o1], v1);
+    }
+    const double ua = u0 + u1, vb = v0 + v1;
+    const long long yr = ((long long)(ps + w) * Lpad + pt0 + lp + w) * 3 + c;
+    ya[yr] = ua;
+    yb[yr] = vb;
+    const int own = (w * WC + lp + w) * 3 + c;
+    a0 += xsa[own] * ua;
+    a1 += ua * ua;
+    b0 += xsb[own] * vb;
+    b1 += vb * vb;
+    __syncthreads();
+  }
+  a0 = block_sum(a0, sh);
+  a1 = block_sum(a1, sh);
+  b0 = block_sum(b0, sh);
+  b1 = block_sum(b1, sh);
+  if (threadIdx.x == 0) {
+    pa[2 * blockIdx.x] = a0;
+    pa[2 * blockIdx.x + 1] = a1;
+    pb[2 * blockIdx.x] = b0;
+    pb[2 * blockIdx.x + 1] = b1;
+  }
+  if (last_block(&sa->counter)) {
+    double a, b;
+    final_sum2(pa, gridDim.x, &a, &b, sh);
+    double cc, d;
+    final_sum2(pb, gridDim.x, &cc, &d, sh);
+    if (threadIdx.x == 0) {
+      sa->counter = 0;
+      finish_reduction(sa, ma, a, b);
+      finish_reduction(sb, mb, cc, d);
+    }
+  }
+}
+
 template <int NR>
 __global__ void __launch_bounds__(256) k_tcg_spmv(int L, int w, const double* __restrict__ BsT,
                                                   const double* __restrict__ p,
@@ -1984,4 +2121,141 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
     if (h->done) return 0;
     chunk = chunk * 2 < max_chunk ? chunk * 2 : max_chunk;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Level engine: the lambda estimates of S B S (sparse_core.eig_extremes,
+// power iteration then inverse iteration with warm-started inner CG) paired
+// with the subband PCG of the same level, every operator pass shared by both
+// through k_dual_apply.  Host control flow mirrors sparse_core.py:232-278.
+// ---------------------------------------------------------------------------
+#include "gb_engine.h"
+
+static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, int mb,
+                       cudaStream_t s) {
+  const int W2 = 2 * e->w + 1;
+  const size_t smem = ((size_t)(W2 * W2 * 3 + 2) / 2 + 1) * sizeof(double) +
+                      2 * (size_t)W2 * (kTileP + 2 * e->w) * 3 * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_dual_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  k_dual_apply<<<tiled_grid(e->L), 192, smem, s>>>(
+      e->L, e->w, e->BsT, e->pa, e->apa, (KState*)e->sta, e->parta, 0, xb, yb,
+      (KState*)e->stb, e->partb, mb);
+  return (int)cudaGetLastError();
+}
+
+static void post_a(const gb_level_engine_args* e, cudaStream_t s) {
+  const int Lpad = e->L + 2 * e->w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  KState* k = (KState*)e->sta;
+  k_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, e->xa, e->ra, e->pa, e->apa, e->za,
+                                              e->inv, k, e->parta);
+  k_cg_dir<<<grid_for(npad, 256, kRedBlocks), 256, 0, s>>>(npad, e->za, e->pa, k);
+}
+
+int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches) {
+  const int Lpad = e->L + 2 * e->w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  KState* ka = (KState*)e->sta;
+  KState* kb = (KState*)e->stb;
+  KState* ha = (KState*)e->hsta;
+  KState* hb = (KState*)e->hstb;
+  int err;
+  int chunk = 8;
+  // --- power iteration (B) paired with the PCG (A) -----------------------
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      if ((err = launch_dual(e, e->xb, e->yb, 1, s))) return err;
+      post_a(e, s);
+      k_pow_step<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, e->tol, kb, e->partb);
+      k_pow_scale<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, kb);
+    }
+    *launches += 5LL * chunk;
+    if ((err = (int)cudaGetLastError())) return err;
+    if ((err = read_state(e->sta, ha, s))) return err;
+    if ((err = read_state(e->stb, hb, s))) return err;
+    if (hb->done) break;
+    chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;
+  }
+  e->lam_max = hb->lam;
+  e->power_its = hb->it;
+  e->calls = hb->it + (hb->ynorm != 0.0 ? 0 : 1);
+  // --- inverse iteration -------------------------------------------------
+  double* cur = e->x2;     // right-hand side of the inner solve (unit vector)
+  double* nxt = e->xn;     // next iterate
+  double lam_prev = 1.0 / 0.0;
+  int have_prev = 0;       // warm start x0 = previous normalized iterate (= cur)
+  e->lam_min = e->lam_max;
+  e->n_outer = 0;
+  for (int outer = 0; outer < e->max_outer; ++outer) {
+    // inner CG: A_op y = cur, x0 = cur when warm (its A x0 is e->ax from the
+    // previous Rayleigh quotient)
+    k_state_reset<<<1, 1, 0, s>>>(kb, (int)e->inner_max_iter);
+    k_cg_init<<<gv, 256, 0, s>>>(npad, cur, have_prev ? cur : nullptr,
+                                 have_prev ? e->ax : nullptr, e->cx, e->cr, e->cp,
+                                 e->inner_tol, (int)e->inner_max_iter, kb, e->partb);
+    k_cg_zero_if<<<gv, 256, 0, s>>>(npad, e->cx, kb);
+    *launches += 3;
+    chunk = 8;
+    for (;;) {
+      for (int i = 0; i < chunk; ++i) {
+        if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;
+        post_a(e, s);
+        k_cg_update<<<gv, 256, 0, s>>>(npad, e->cx, e->cr, e->cp, e->cap, kb, e->partb);
+        k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cr, e->cp, kb);
+      }
+      *launches += 5LL * chunk;
+      if ((err = (int)cudaGetLastError())) return err;
+      if ((err = read_state(e->sta, ha, s))) return err;
+      if ((err = read_state(e->stb, hb, s))) return err;
+      if (hb->done) break;
+      chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;
+    }
+    if (hb->breakdown) {
+      e->breakdown = hb->breakdown;
+      return 0;
+    }
+    if (outer < 64) e->inner_its[outer] = hb->it;
+    e->calls += hb->it + (have_prev ? 1 : 0);
+    // y -> unit vector, Rayleigh quotient x.(A x)
+    k_dot2<<<gv, 256, 0, s>>>(npad, e->cx, e->cx, nullptr, e->dots, kb, e->partb);
+    k_scale_by_norm<<<grid_for(npad, 256, 148 * 16), 256, 0, s>>>(npad, e->cx, e->dots, 0, nxt,
+                                                                  nullptr);
+    k_tbox_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, nxt,
+                                                                      e->ax);
+    k_dot2<<<gv, 256, 0, s>>>(npad, nxt, e->ax, nullptr, e->dots + 2, kb, e->partb);
+    *launches += 4;
+    e->calls += 1;
+    if ((err = gbk_sync_read(e->dots, e->hdots, 4 * sizeof(double), s))) return err;
+    e->n_outer = outer + 1;
+    if (e->hdots[0] == 0.0) {
+      e->breakdown = -1;  // A^-1 x = 0
+      return 0;
+    }
+    const double lam = e->hdots[2];
+    e->lam_min = lam;
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
+    have_prev = 1;
+    if (fabs(lam - lam_prev) <= 0.5 * e->tol * fabs(lam)) break;
+    lam_prev = lam;
+  }
+  // --- the PCG alone until it converges ---------------------------------
+  chunk = 8;
+  while (!ha->done) {
+    for (int i = 0; i < chunk; ++i) {
+      if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;  // B done: single pass
+      post_a(e, s);
+    }
+    *launches += 3LL * chunk;
+    if ((err = (int)cudaGetLastError())) return err;
+    if ((err = read_state(e->sta, ha, s))) return err;
+    chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;
+  }
+  return 0;
 }

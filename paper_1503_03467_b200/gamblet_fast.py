@@ -540,6 +540,70 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
 
 _SPECTRAL_LOG = []
 
+# pair the lambda estimate and the subband PCG of a level in one engine
+# (shared S B S passes); levels the tiled kernels do not cover run them apart
+PAIRED_ENGINE = __import__("os").environ.get("GB_PAIRED", "1") == "1"
+
+
+def _engine_ok(op):
+    return (op.nr == 3 and op.layout == 0 and op.L % 64 == 0 and op.w <= 8)
+
+
+def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
+    """Run csrc gb_level_engine: block-Jacobi PCG for (S B S) z = rhs and the
+    reference's lambda estimates of S B S (same start vectors as
+    sparse_core.eig_extremes), sharing every operator pass."""
+    from .engine import LevelEngineArgs
+    n = op.n
+    st = dv.stream()
+    # A: initialised PCG
+    inv = op.bj_inv()
+    ka = _Krylov(op.npad)
+    xa, ra, pa, apa, za = (op.vec() for _ in range(5))
+    max_a = min(max(200, 2 * n), MAX_ITER_CAP)
+    nat.call("gb_state_reset", dv.ptr(ka.state), max_a, st)
+    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(rhs_pad), dv.ptr(xa), dv.ptr(ra), dv.ptr(pa),
+             dv.ptr(za), dv.ptr(inv), float(tol_a), int(max_a), dv.ptr(ka.state),
+             dv.ptr(ka.part), st)
+    # B: start vectors drawn exactly as eig_extremes draws them
+    rng = np.random.default_rng(seed)
+    x1 = rng.standard_normal(n)
+    x2 = rng.standard_normal(n)
+    kb = _Krylov(op.npad)
+    xb = op.pad(dv.to_dev(x1))
+    nat.call("gb_dot2", op.npad, dv.ptr(xb), dv.ptr(xb), None, dv.ptr(kb.dots),
+             dv.ptr(kb.state), dv.ptr(kb.part), st)
+    nat.call("gb_scale_by_norm", op.npad, dv.ptr(xb), dv.ptr(kb.dots), 0, dv.ptr(xb), None, st)
+    xs = op.pad(dv.to_dev(x2))
+    nat.call("gb_dot2", op.npad, dv.ptr(xs), dv.ptr(xs), None, dv.ptr(kb.dots),
+             dv.ptr(kb.state), dv.ptr(kb.part), st)
+    nat.call("gb_scale_by_norm", op.npad, dv.ptr(xs), dv.ptr(kb.dots), 0, dv.ptr(xs), None, st)
+    nat.call("gb_state_reset", dv.ptr(kb.state), max_iter, st)
+    yb, xn, ax, cx, cr, cp, cap = (op.vec() for _ in range(7))
+    dots = dv.empty(4)
+    args = LevelEngineArgs(
+        L=op.L, w=op.w, max_chunk=128, max_outer=max_iter, BsT=dv.ptr(op.BsT),
+        inv=dv.ptr(inv), xa=dv.ptr(xa), ra=dv.ptr(ra), pa=dv.ptr(pa), apa=dv.ptr(apa),
+        za=dv.ptr(za), sta=dv.ptr(ka.state), parta=dv.ptr(ka.part), hsta=ka.host.data_ptr(),
+        xb=dv.ptr(xb), yb=dv.ptr(yb), x2=dv.ptr(xs), xn=dv.ptr(xn), ax=dv.ptr(ax),
+        cx=dv.ptr(cx), cr=dv.ptr(cr), cp=dv.ptr(cp), cap=dv.ptr(cap), stb=dv.ptr(kb.state),
+        partb=dv.ptr(kb.part), hstb=kb.host.data_ptr(), dots=dv.ptr(dots),
+        hdots=kb.hdots.data_ptr(), tol=tol, inner_tol=max(1e-12, 1e-3 * tol),
+        inner_max_iter=min(max(200, 2 * n), MAX_ITER_CAP))
+    nat.call("gb_level_engine", nat.ctypes.byref(args), st)
+    if args.breakdown > 0:
+        raise NumericalError(f"CG breakdown at iteration {args.breakdown}: p^T A p <= 0 "
+                             "(matrix is not SPD)")
+    if args.breakdown < 0:
+        raise NumericalError("inverse iteration broke down: A^{-1} x = 0")
+    h = ka.host_view()
+    _SPECTRAL_LOG.append({"n": n, "power": int(args.power_its),
+                          "inner": [int(args.inner_its[i]) for i in range(min(args.n_outer, 64))]})
+    rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
+    return {"x": xa, "its": int(h["it"]), "rel": rel, "conv": bool(h["converged"]),
+            "brk": int(h["breakdown"]), "lam_min": float(args.lam_min),
+            "lam_max": float(args.lam_max), "calls": int(args.calls)}
+
 # lambda estimates run on side streams (one per worker thread) so they overlap
 # the FP64-bound patch factorizations of the main stream
 SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
@@ -592,6 +656,22 @@ class _LevelTasks:
             st.wait_event(ev)
             if g is not None:
                 g.record_stream(st)  # main-stream tensor read on this stream
+            if (SPECTRAL and PAIRED_ENGINE and self.solver is not None and g is not None
+                    and _engine_ok(op)):
+                box = {}
+
+                def run_engine(op_, rhs_pad, tol):
+                    with dv.phase("level_engine"):
+                        out = _paired_level(op_, rhs_pad, tol)
+                    box.update(out)
+                    return out["x"], out["its"], out["rel"], out["conv"], out["brk"]
+
+                self.solver.subband(k, g, pipelined=True, engine=run_engine)
+                level.lambda_min_subband = box["lam_min"]
+                level.lambda_max_subband = box["lam_max"]
+                done = torch.cuda.Event()
+                done.record(st)
+                return box["calls"], op, done
             if SPECTRAL:
                 with dv.phase("spectral"):
                     lam_min, lam_max, calls = _eig_extremes(op)
@@ -661,7 +741,6 @@ def _level_q(M, A, tree, rho, ctx, counter):
         raise InvalidArgumentError(f"stiffness shape {A.shape} does not match q={q}")
     with dv.phase("input_to_box"):
         Mb, _ = dv.csr_to_box(_canon(M), n)
-        Ab, _ = dv.csr_to_box(_canon(A), n)
     sM = dv.empty(N)
     nat.call("gb_box_scale", N, 1, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM),
              ctx.st(ctx.slot("scale", "mass")), s)
@@ -673,6 +752,19 @@ def _level_q(M, A, tree, rho, ctx, counter):
     with dv.phase("mass_patches"):
         _mass_patches(n, Mb, sM, rho, wd, psi, ctx.st(ctx.slot("mass", "mass")), s)
     dv.Prof.add_work("mass_patches", flops=_patch_flops(n, rho, 1))
+    # the stiffness is needed only after the mass patches: a host-resident A
+    # is uploaded on a copy stream while they run
+    A = _canon(A)
+    if not isinstance(A, dv.DeviceCSR):
+        cs = _copy_stream()
+        with torch.cuda.stream(cs):
+            A = dv.DeviceCSR.from_scipy(A)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        torch.cuda.current_stream().wait_event(ev)
+        for t in (A.indptr, A.indices, A.data):
+            t.record_stream(torch.cuda.current_stream())
+    Ab, _ = dv.csr_to_box(A, n)
     wX = min(rho + Ab.w, n - 1)
     X = dv.empty(N * dv.box_slots(wX, 1))
     wR = min(wX + rho, n - 1)
@@ -729,6 +821,16 @@ def _correction_patches(Lp, B, op, sB, Gv, rho, Dt, status_ptr, s):
     ws = dv.empty(wsb // 8) if wsb else None
     nat.call("gb_correction_patches", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w, dv.ptr(Gv),
              rho, dv.ptr(Dt), status_ptr, dv.ptr(ws), blocks, s)
+
+
+_COPY_STREAM = {}
+
+
+def _copy_stream():
+    dev = dv.device()
+    if dev not in _COPY_STREAM:
+        _COPY_STREAM[dev] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAM[dev]
 
 
 def _patch_flops(L, rho, comps):
@@ -1009,7 +1111,7 @@ class _LevelSolver:
                 f"level {k} was not produced by this package's fast_transform")
         return lvl, B, R
 
-    def subband(self, k, g, pipelined=False):
+    def subband(self, k, g, pipelined=False, engine=None):
         lvl, B, _ = self._check(k, need_r=not pipelined)
         s = dv.stream()
         counter = self.counter
@@ -1024,8 +1126,11 @@ class _LevelSolver:
         rhs = dv.empty(J)
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
         counter.add("line8", 8 * J + J)
-        with dv.phase("subband_cg"):
-            zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), self.tol)
+        if engine is not None:
+            zp, its, rel, conv, brk = engine(op, op.pad(rhs), self.tol)
+        else:
+            with dv.phase("subband_cg"):
+                zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), self.tol)
         dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
                                                      + 12 * 8 * op.n))
         if brk:

@@ -17,7 +17,8 @@ import scipy.sparse as sp
 
 from .errors import InvalidArgumentError
 
-__all__ = ["CgReport", "as_csr", "spmv_flops", "matmul_flops", "cg_flops"]
+__all__ = ["CgReport", "as_csr", "spmv_flops", "matmul_flops", "cg_flops", "cg_solve",
+           "cg_solve_block", "eig_extremes"]
 
 
 def _require(cond, msg):
@@ -71,3 +72,20 @@ def matmul_flops(A, B):
 
 def cg_flops(nnz, n, iterations, ncols=1):
     return int(iterations) * (2 * int(nnz) + 12 * int(n)) * ncols
+
+
+# GPU Krylov solvers with the reference's signatures (sparse_core.py:126-278);
+# imported lazily so the host-side helpers above stay importable without CUDA.
+def cg_solve(A, b, rel_tol=1e-10, max_iter=None, x0=None):
+    from .krylov import cg_solve as _f
+    return _f(A, b, rel_tol=rel_tol, max_iter=max_iter, x0=x0)
+
+
+def cg_solve_block(A, B, rel_tol=1e-10, max_iter=None):
+    from .krylov import cg_solve_block as _f
+    return _f(A, B, rel_tol=rel_tol, max_iter=max_iter)
+
+
+def eig_extremes(A, tol=1e-2, max_iter=500, seed=24337):
+    from .krylov import eig_extremes as _f
+    return _f(A, tol=tol, max_iter=max_iter, seed=seed)
