@@ -121,9 +121,14 @@ int gb_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD
                   double* raw, void* stream);
 int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double* psi,
             int wdw, double* Wpsi, void* stream);
+/* psi^(k-1) = drop_row(0.25 P psi + Dt (W psi)) (gamblet_fast.py:615-622),
+ * row-tail drop included; rowmax: (Lk/2)^2 doubles of workspace.
+ * gb_psi_next_mode: 1 (default) tensor-core block GEMM, 0 per-entry gather in
+ * the reference's summation order, -1 queries; returns the previous mode. */
+int gb_psi_next_mode(int mma);
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
-                double* psi_next, void* stream);
+                double* psi_next, double* rowmax, void* stream);
 
 /* ---- K7/K8 Krylov (sparse_core.py:126-165, 232-278;
  *      gamblet_fast.py:380-387, 717-760) ---------------------------------- */

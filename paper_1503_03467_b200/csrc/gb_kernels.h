@@ -62,7 +62,7 @@ int gbk_wpsi(int n, int Lk, int lo, int wd, const double* w12, const double* psi
              int wdw, double* Wpsi, cudaStream_t s);
 int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                  const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
-                 double* psi_next, cudaStream_t s);
+                 double* psi_next, double* rowmax, cudaStream_t s);
 
 // gb_krylov.cu
 size_t gbk_kstate_bytes();
@@ -159,3 +159,4 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
                       long long* launches);
 #include "gb_engine.h"
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches);
+int gbk_psi_next_mode(int mma);

@@ -967,10 +967,10 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
             with dv.phase("psi_next"):
                 nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
                          dv.ptr(Wpsi), s)
+                rmax = dv.empty(P)
                 nat.call("gb_psi_next", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
-                         dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), s)
-                nat.call("gb_row_tail_drop", P, wd2 * wd2, dv.ptr(pv), s)
-            del Wpsi
+                         dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax), s)
+            del Wpsi, rmax
             psin = PsiWindows(pv, n, Lp, lo2, hi2)
             counter.add("line14", 2 * P * wd2 * wd2 * 3 * (2 * rho + 1) ** 2 // 4
                         + 2 * J * wdw * wdw * 4)
