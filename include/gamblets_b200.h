@@ -123,9 +123,11 @@ int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double*
             int wdw, double* Wpsi, void* stream);
 /* psi^(k-1) = drop_row(0.25 P psi + Dt (W psi)) (gamblet_fast.py:615-622),
  * row-tail drop included; rowmax: (Lk/2)^2 doubles of workspace.
- * gb_psi_next_mode: 1 (default) tensor-core block GEMM, 0 per-entry gather in
- * the reference's summation order, -1 queries; returns the previous mode. */
-int gb_psi_next_mode(int mma);
+ * gb_products_mode selects the kernels of psi_next, gb_bd, gb_gtd and
+ * gb_coarse_raw: 1 (default) tensor-core block GEMMs, 0 per-entry gathers;
+ * both accumulate in the reference's order (ascending CSR column), -1
+ * queries; returns the previous mode. */
+int gb_products_mode(int mma);
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
                 double* psi_next, double* rowmax, void* stream);

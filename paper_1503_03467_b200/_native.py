@@ -50,7 +50,7 @@ _SIGS = {
     "gb_coarse_raw": ([_I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_wpsi": ([_I, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "gb_psi_next": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P, _P, _P], _I),
-    "gb_psi_next_mode": ([_I], _I),
+    "gb_products_mode": ([_I], _I),
     "gb_kstate_bytes": ([], _Z),
     "gb_red_blocks": ([], _I),
     "gb_state_reset": ([_P, _I, _P], _I),

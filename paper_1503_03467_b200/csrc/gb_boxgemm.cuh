@@ -1,0 +1,135 @@
+// Box-stencil block GEMM on the FP64 tensor cores (DMMA m8n8k4) for the
+// split triple product A^(k-1) = 0.0625 P A P^T + G^T D + D^T G + D^T B D
+// (gamblet_fast.py:590-612).  One CTA computes an output tile of TB x TB row
+// parents (x MC components) by TB x TB column parents; K runs over the
+// parents (x 3 components) both operands can touch, in ascending
+// (q_s, q_t, c) order -- the CSR column order the reference's SpGEMM
+// accumulates in -- so every output is the same sequential FMA chain as the
+// per-entry gather (zero products are skipped or added as +0, which does not
+// change a nonzero sum).  Operand/epilogue access is supplied by functors:
+//   a(i_s, i_t, m_comp, q_s, q_t, k_comp)  (0 outside the operand's box)
+//   b(q_s, q_t, k_comp, j_s, j_t)
+//   out.store(i_s, i_t, m_comp, j_s, j_t, acc)   called for |j - i| <= wOut
+#pragma once
+#include "gb_common.cuh"
+
+namespace gb {
+
+__device__ __forceinline__ void dmma_884b(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+constexpr int BG_KC = 32, BG_LDA = 36, BG_LDB = 20;
+
+// MC: row components (1 or 3) -> M = 16 MC rows, N = 16 columns, 4 warps;
+// warp w: n-tile w & 1, m-tiles (w >> 1) + 2 j, j < MC.
+template <int MC, class AOp, class BOp, class OutOp>
+__global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb, int wOut,
+                                                  AOp aop, BOp bop, OutOp out) {
+  __shared__ double As[16 * MC * BG_LDA];
+  __shared__ double Bs[BG_KC * BG_LDB];
+  __shared__ int kq[BG_KC];  // (q_s << 16 | q_t) * 4 + comp, -1 = padding
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (Lp + TB - 1) / TB;
+  const int nbo = (wOut + TB - 1) / TB;
+  const int side = 2 * nbo + 1;
+  const long long ntiles = (long long)nb * nb * side * side;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long mb = t / (side * side);
+    const int ob = (int)(t - mb * side * side);
+    const int mbs = (int)(mb / nb), mbt = (int)(mb % nb);
+    const int nbs = mbs + ob / side - nbo, nbt = mbt + ob % side - nbo;
+    if (nbs < 0 || nbs >= nb || nbt < 0 || nbt >= nb) continue;  // CTA-uniform
+    const int i0s = mbs * TB, i0t = mbt * TB, j0s = nbs * TB, j0t = nbt * TB;
+    const int nis = imin(TB, Lp - i0s), nit = imin(TB, Lp - i0t);
+    const int njs = imin(TB, Lp - j0s), njt = imin(TB, Lp - j0t);
+    // skip tiles with no (i, j) pair inside the output box
+    if (j0s - (i0s + nis - 1) > wOut || i0s - (j0s + njs - 1) > wOut ||
+        j0t - (i0t + nit - 1) > wOut || i0t - (j0t + njt - 1) > wOut)
+      continue;
+    const int qs0 = imax(imax(i0s - wa, j0s - wb), 0);
+    const int qs1 = imin(imin(i0s + nis - 1 + wa, j0s + njs - 1 + wb), Lp - 1);
+    const int qt0 = imax(imax(i0t - wa, j0t - wb), 0);
+    const int qt1 = imin(imin(i0t + nit - 1 + wa, j0t + njt - 1 + wb), Lp - 1);
+    const int nqs = qs1 - qs0 + 1, nqt = qt1 - qt0 + 1;
+    const int K = (nqs > 0 && nqt > 0) ? nqs * nqt * 3 : 0;
+    double c[MC][2];
+#pragma unroll
+    for (int j = 0; j < MC; ++j) c[j][0] = c[j][1] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += BG_KC) {
+      if (threadIdx.x < BG_KC) {
+        const int kk = k0 + threadIdx.x;
+        int code = -1;
+        if (kk < K) {
+          const int pl = kk / 3, cc = kk - 3 * pl;
+          code = (((qs0 + pl / nqt) << 16) | (qt0 + pl % nqt)) * 4 + cc;
+        }
+        kq[threadIdx.x] = code;
+      }
+      __syncthreads();
+      // A: (16 MC) x 32
+      for (int e = threadIdx.x; e < 16 * MC * BG_KC; e += 128) {
+        const int m = e >> 5, kk = e & 31;
+        const int code = kq[kk];
+        double v = 0.0;
+        const int lm = m / MC, mc = m - lm * MC;
+        const int ls = lm / TB, lt = lm - ls * TB;
+        if (code >= 0 && lm < TB * TB && ls < nis && lt < nit) {
+          const int q = code >> 2;
+          v = aop(i0s + ls, i0t + lt, mc, q >> 16, q & 0xffff, code & 3);
+        }
+        As[m * BG_LDA + kk] = v;
+      }
+      // B: 32 x 16
+      for (int e = threadIdx.x; e < BG_KC * 16; e += 128) {
+        const int kk = e >> 4, nn = e & 15;
+        const int code = kq[kk];
+        double v = 0.0;
+        const int ls = nn / TB, lt = nn - ls * TB;
+        if (code >= 0 && nn < TB * TB && ls < njs && lt < njt) {
+          const int q = code >> 2;
+          v = bop(q >> 16, q & 0xffff, code & 3, j0s + ls, j0t + lt);
+        }
+        Bs[kk * BG_LDB + nn] = v;
+      }
+      __syncthreads();
+      const int nt = warp & 1;
+#pragma unroll
+      for (int ks = 0; ks < BG_KC / 4; ++ks) {
+        const double b = Bs[(ks * 4 + (lane & 3)) * BG_LDB + nt * 8 + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < MC; ++j) {
+          const int mt = (warp >> 1) + 2 * j;
+          const double a = As[(mt * 8 + (lane >> 2)) * BG_LDA + ks * 4 + (lane & 3)];
+          dmma_884b(c[j][0], c[j][1], a, b);
+        }
+      }
+      __syncthreads();
+    }
+    // epilogue
+    const int nt = warp & 1;
+#pragma unroll
+    for (int j = 0; j < MC; ++j) {
+      const int mt = (warp >> 1) + 2 * j;
+      const int m = mt * 8 + (lane >> 2);
+      const int lm = m / MC, mc = m - lm * MC;
+      const int ls = lm / TB, lt = lm - ls * TB;
+      if (lm >= TB * TB || ls >= nis || lt >= nit) continue;
+      const int is = i0s + ls, it = i0t + lt;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int nn = nt * 8 + 2 * (lane & 3) + h;
+        const int ns = nn / TB, ntt = nn - ns * TB;
+        if (nn >= TB * TB || ns >= njs || ntt >= njt) continue;
+        const int js = j0s + ns, jt = j0t + ntt;
+        if (js - is > wOut || is - js > wOut || jt - it > wOut || it - jt > wOut) continue;
+        out.store(is, it, mc, js, jt, c[j][h]);
+      }
+    }
+  }
+}
+
+}  // namespace gb

@@ -186,13 +186,13 @@ int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double*
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
                 double* psi_next, double* rowmax, void* stream) {
-  COUNT(3);
+  COUNT(2);
   return wrap(gbk_psi_next(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2, psi_next,
                            rowmax, ST(stream)),
               "psi_next");
 }
 
-int gb_psi_next_mode(int mma) { return gbk_psi_next_mode(mma); }
+int gb_products_mode(int mma) { return gbk_products_mode(mma); }
 size_t gb_kstate_bytes(void) { return gbk_kstate_bytes(); }
 int gb_red_blocks(void) { return gbk_red_blocks(); }
 int gb_state_reset(void* state, int max_iter, void* stream) {

@@ -159,4 +159,4 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
                       long long* launches);
 #include "gb_engine.h"
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches);
-int gbk_psi_next_mode(int mma);
+int gbk_products_mode(int mma);

@@ -12,6 +12,7 @@
 //       BD = B D, GtD = G^T D, DtBD, raw A^(k-1) gamblet_fast.py:602-611
 //       psi^(k-1) = 0.25 P psi + Dt (W psi)   gamblet_fast.py:615-622
 #include "gb_common.cuh"
+#include "gb_boxgemm.cuh"
 #include "gb_kernels.h"
 
 namespace gb {
@@ -726,6 +727,80 @@ __global__ void k_drop_by_rowmax(long long rows, long long S, double* __restrict
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// operand / epilogue functors of the triple-product block GEMMs (gb_boxgemm.cuh)
+// ---------------------------------------------------------------------------
+struct OpBrows {  // A operand: B[(i,mc)][(q,c)]
+  const double* B;
+  int Lp, w, S;
+  __device__ double operator()(int is, int it, int mc, int qs, int qt, int kc) const {
+    const int ds = qs - is, dt = qt - it;
+    if (ds < -w || ds > w || dt < -w || dt > w) return 0.0;
+    return B[(((long long)is * Lp + it) * 3 + mc) * S + slot_of(w, 3, ds, dt, kc)];
+  }
+};
+struct OpDtRowsA {  // A operand: Dt[i][(q,c)]
+  const double* Dt;
+  int Lp, rho, S;
+  __device__ double operator()(int is, int it, int, int qs, int qt, int kc) const {
+    const int ds = qs - is, dt = qt - it;
+    if (ds < -rho || ds > rho || dt < -rho || dt > rho) return 0.0;
+    return Dt[((long long)is * Lp + it) * S + slot_of(rho, 3, ds, dt, kc)];
+  }
+};
+struct OpDtRowsB {  // B operand: Dt[j][(q,c)]  (i.e. D)
+  const double* Dt;
+  int Lp, rho, S;
+  __device__ double operator()(int qs, int qt, int kc, int js, int jt) const {
+    const int ds = qs - js, dt = qt - jt;
+    if (ds < -rho || ds > rho || dt < -rho || dt > rho) return 0.0;
+    return Dt[((long long)js * Lp + jt) * S + slot_of(rho, 3, ds, dt, kc)];
+  }
+};
+struct OpGcols {  // A operand: G^T, G[(q,c)][i]
+  const double* G;
+  int Lp, w, S;
+  __device__ double operator()(int is, int it, int, int qs, int qt, int kc) const {
+    const int ds = is - qs, dt = it - qt;
+    if (ds < -w || ds > w || dt < -w || dt > w) return 0.0;
+    return G[(((long long)qs * Lp + qt) * 3 + kc) * S + slot_of(w, 1, ds, dt, 0)];
+  }
+};
+struct OpBDrows {  // B operand: BD[(q,c)][j]
+  const double* BD;
+  int Lp, w, S;
+  __device__ double operator()(int qs, int qt, int kc, int js, int jt) const {
+    const int ds = js - qs, dt = jt - qt;
+    if (ds < -w || ds > w || dt < -w || dt > w) return 0.0;
+    return BD[(((long long)qs * Lp + qt) * 3 + kc) * S + slot_of(w, 1, ds, dt, 0)];
+  }
+};
+struct StoreBox {
+  double* out;
+  int Lp, MC, w, S;
+  __device__ void store(int is, int it, int mc, int js, int jt, double v) const {
+    out[(((long long)is * Lp + it) * MC + mc) * S + slot_of(w, 1, js - is, jt - it, 0)] = v;
+  }
+};
+struct StoreRaw {  // ((0.0625 PAPt + GtD_ij) + GtD_ji) + DtBD_ij
+  double* raw;
+  const double *PAPt, *GtD;
+  int Lp, wB, wGD, wA2;
+  __device__ void store(int is, int it, int, int js, int jt, double acc) const {
+    const int ds = js - is, dt = jt - it;
+    const long long i = (long long)is * Lp + it, j = (long long)js * Lp + jt;
+    double pap = 0.0, gij = 0.0, gji = 0.0;
+    if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
+      pap = PAPt[i * box_slots(wB, 1) + slot_of(wB, 1, ds, dt, 0)];
+    if (ds >= -wGD && ds <= wGD && dt >= -wGD && dt <= wGD) {
+      gij = GtD[i * box_slots(wGD, 1) + slot_of(wGD, 1, ds, dt, 0)];
+      gji = GtD[j * box_slots(wGD, 1) + slot_of(wGD, 1, -ds, -dt, 0)];
+    }
+    raw[i * box_slots(wA2, 1) + slot_of(wA2, 1, ds, dt, 0)] = ((0.0625 * pap + gij) + gji) + acc;
+  }
+};
+
 }  // namespace gb
 
 using namespace gb;
@@ -737,10 +812,10 @@ static inline int grid_for(long long work, int block, int cap = 148 * 32) {
   return (int)g;
 }
 
-static int psi_next_use_mma = 1;
-int gbk_psi_next_mode(int mma) {
-  const int old = psi_next_use_mma;
-  if (mma >= 0) psi_next_use_mma = mma;
+static int products_use_mma = 1;
+int gbk_products_mode(int mma) {
+  const int old = products_use_mma;
+  if (mma >= 0) products_use_mma = mma;
   return old;
 }
 
@@ -790,8 +865,24 @@ int gbk_restriction(int Lp, int rho, const double* Dt, const double* w12, double
   return (int)cudaGetLastError();
 }
 
+static int box_gemm_grid(int Lp, int TB, int wOut) {
+  const long long nb = (Lp + TB - 1) / TB, side = 2 * ((wOut + TB - 1) / TB) + 1;
+  const long long nt = nb * nb * side * side;
+  return (int)(nt < 148LL * 48 ? nt : 148LL * 48);
+}
+
 int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
            double* BD, cudaStream_t s) {
+  if (products_use_mma) {
+    const int TB = Lp < 4 ? Lp : 4;
+    const size_t bytes = (size_t)Lp * Lp * 3 * box_slots(wBD, 1) * sizeof(double);
+    cudaError_t e = cudaMemsetAsync(BD, 0, bytes, s);
+    if (e != cudaSuccess) return (int)e;
+    k_box_gemm<3><<<box_gemm_grid(Lp, TB, wBD), 128, 0, s>>>(
+        Lp, TB, wB, rho, wBD, OpBrows{B, Lp, wB, box_slots(wB, 3)},
+        OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{BD, Lp, 3, wBD, box_slots(wBD, 1)});
+    return (int)cudaGetLastError();
+  }
   const long long total = (long long)Lp * Lp * 3 * box_slots(wBD, 1);
   k_bd<<<grid_for(total, 256), 256, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD);
   return (int)cudaGetLastError();
@@ -799,6 +890,16 @@ int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
 
 int gbk_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
             double* GtD, cudaStream_t s) {
+  if (products_use_mma) {
+    const int TB = Lp < 4 ? Lp : 4;
+    const size_t bytes = (size_t)Lp * Lp * box_slots(wGD, 1) * sizeof(double);
+    cudaError_t e = cudaMemsetAsync(GtD, 0, bytes, s);
+    if (e != cudaSuccess) return (int)e;
+    k_box_gemm<1><<<box_gemm_grid(Lp, TB, wGD), 128, 0, s>>>(
+        Lp, TB, wG, rho, wGD, OpGcols{G, Lp, wG, box_slots(wG, 1)},
+        OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{GtD, Lp, 1, wGD, box_slots(wGD, 1)});
+    return (int)cudaGetLastError();
+  }
   const long long total = (long long)Lp * Lp * box_slots(wGD, 1);
   k_gtd<<<grid_for(total, 256), 256, 0, s>>>(Lp, wG, G, rho, Dt, wGD, GtD);
   return (int)cudaGetLastError();
@@ -807,6 +908,16 @@ int gbk_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
 int gbk_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
                    int rho, const double* Dt, int wBD, const double* BD, int wA2,
                    double* raw, cudaStream_t s) {
+  if (products_use_mma) {
+    const int TB = Lp < 4 ? Lp : 4;
+    const size_t bytes = (size_t)Lp * Lp * box_slots(wA2, 1) * sizeof(double);
+    cudaError_t e = cudaMemsetAsync(raw, 0, bytes, s);
+    if (e != cudaSuccess) return (int)e;
+    k_box_gemm<1><<<box_gemm_grid(Lp, TB, wA2), 128, 0, s>>>(
+        Lp, TB, rho, wBD, wA2, OpDtRowsA{Dt, Lp, rho, box_slots(rho, 3)},
+        OpBDrows{BD, Lp, wBD, box_slots(wBD, 1)}, StoreRaw{raw, PAPt, GtD, Lp, wB, wGD, wA2});
+    return (int)cudaGetLastError();
+  }
   const long long total = (long long)Lp * Lp * box_slots(wA2, 1);
   k_coarse_raw<<<grid_for(total, 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt,
                                                     wBD, BD, wA2, raw);
@@ -829,7 +940,7 @@ int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int w
   const long long rows = (long long)Lp * Lp, S = (long long)wd2 * wd2;
   cudaError_t e = cudaMemsetAsync(rowmax, 0, rows * sizeof(double), s);
   if (e != cudaSuccess) return (int)e;
-  if (psi_next_use_mma) {
+  if (products_use_mma) {
     const int TB = Lp < 4 ? Lp : 4;
     const int hp = n / Lp;  // output row spacing (fine units)
     const int span = imin(wd2 + (TB - 1) * hp, n);

@@ -17,17 +17,18 @@ for q, coeff in [(int(a.split(":")[0]), a.split(":")[1]) for a in (sys.argv[1:] 
     sched = gb.make_schedule(1e-13, q, uniform_rho=3)
     out = {}
     for mode in (0, 1):
-        nat.load().gb_psi_next_mode(mode)
+        nat.load().gb_products_mode(mode)
         gb.fast_transform(p.M, p.A, p.tree, sched)  # warm
         torch.cuda.synchronize()
         t = time.perf_counter()
         lv, _ = gb.fast_transform(p.M, p.A, p.tree, sched)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
-        out[mode] = {k: lv[k].psi.tocsr() if hasattr(lv[k].psi, "tocsr") else lv[k].psi
-                     for k in range(1, q + 1) if lv[k].psi is not None}
+        out[mode] = {(k, f): getattr(lv[k], f) for k in range(1, q + 1)
+                     for f in ("psi", "stiffness", "subband", "correction")
+                     if getattr(lv[k], f, None) is not None}
         print(f"q={q} {coeff} mode={mode} transform {dt * 1e3:.1f} ms", flush=True)
     for k in sorted(out[0]):
         a, b = out[0][k], out[1][k]
-        print(f"  level {k}: nnz {a.nnz} vs {b.nnz} same_pattern={O.same_pattern(a, b)} "
+        print(f"  {k}: nnz {a.nnz} vs {b.nnz} same_pattern={O.same_pattern(a, b)} "
               f"rel={O.rel_fro(b, a):.2e}", flush=True)
