@@ -181,9 +181,9 @@ int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, doub
                   void* stream, int layout);
 /* block-Jacobi (2x2 parents = 12x12 blocks) PCG for the subband systems */
 int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream);
-int gb_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
-                 const double* inv, double rel_tol, int max_iter, void* state,
-                 double* partials, void* stream);
+int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
+                 double* r, double* p, double* z, const double* inv, double rel_tol, int max_iter,
+                 void* state, double* partials, void* stream);
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
                        double* partials, void* stream, int layout);

@@ -72,7 +72,7 @@ _SIGS = {
     "gb_sym_supported": ([_I, _I, _I], _I),
     "gb_scale_box_symT": ([_I, _I, _P, _P, _P, _P], _I),
     "gb_bj_setup": ([_I, _I, _P, _P, _P, _P], _I),
-    "gb_bjcg_init": ([_I, _I, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_bjcg_init": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
     "gb_bjcg_iterations": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I], _I),
     "gb_sync_read": ([_P, _P, _Z, _P], _I),
     "gb_tcg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),

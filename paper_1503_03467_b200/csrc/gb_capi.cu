@@ -44,7 +44,7 @@ static int invalid(const char* msg) {
 
 extern "C" {
 
-int gb_abi_version(void) { return 2; }
+int gb_abi_version(void) { return 3; }
 unsigned long long gb_launch_count(void) { return g_launches.load(); }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
@@ -290,12 +290,12 @@ int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, voi
   COUNT(1);
   return wrap(gbk_bj_setup(L, w, B, s, inv, ST(stream)), "bj_setup");
 }
-int gb_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
-                 const double* inv, double rel_tol, int max_iter, void* state,
-                 double* partials, void* stream) {
+int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
+                 double* r, double* p, double* z, const double* inv, double rel_tol, int max_iter,
+                 void* state, double* partials, void* stream) {
   COUNT(1);
-  return wrap(gbk_bjcg_init(L, w, b, x, r, p, z, inv, rel_tol, max_iter, state, partials,
-                            ST(stream)),
+  return wrap(gbk_bjcg_init(L, w, b, x0, Ax0, x, r, p, z, inv, rel_tol, max_iter, state,
+                            partials, ST(stream)),
               "bjcg_init");
 }
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,

@@ -26,6 +26,8 @@ typedef struct gb_level_engine_args {
   /* outputs */
   double lam_min, lam_max;
   int64_t calls;
-  int power_its, n_outer, breakdown, pad;
+  int power_its, n_outer, breakdown;
+  int inner_pcg;           /* 1: inner solves are block-Jacobi PCG (uses inv, cz) */
   int inner_its[64];
+  double* cz;              /* PCG preconditioned residual of the inner solves */
 } gb_level_engine_args;

@@ -1361,8 +1361,13 @@ __global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __res
   }
 }
 
-// start (x0 = 0): x = 0, r = b, z = Minv b, p = z; ||b||, r.z
+// start: x = x0 (or 0), r = b - A x0 (Ax0 null => x0 = 0), z = Minv r, p = z;
+// ||b||, ||r||, r.z and the early exits of sparse_core.py:138-148.  Partials
+// are (||r||^2, r.z) pairs in part[0, 2G) and ||b||^2 in part[2G, 3G), so the
+// grid is capped at 2/3 of the caller's 2 * kRedBlocks partial slots.
 __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* __restrict__ b,
+                                                   const double* __restrict__ x0,
+                                                   const double* __restrict__ Ax0,
                                                    double* __restrict__ x, double* __restrict__ r,
                                                    double* __restrict__ p,
                                                    double* __restrict__ z,
@@ -1373,17 +1378,19 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
   __shared__ double sh[32];
   const int nb = (L >> 1) * (L >> 1);
   const int lb = threadIdx.x / 12, l = threadIdx.x % 12;
-  double bb = 0.0, rz = 0.0;
+  double bb = 0.0, rr = 0.0, rz = 0.0;
   for (int b0 = blockIdx.x * 16; b0 < nb; b0 += gridDim.x * 16) {
     const int bk = b0 + lb;
     long long pr = -1;
     double rv = 0.0;
     if (bk < nb) {
       pr = bj_row_pad(L, w, bk, l);
-      rv = b[pr];
-      x[pr] = 0.0;
+      const double bv = b[pr];
+      rv = Ax0 ? bv - Ax0[pr] : bv;
+      x[pr] = x0 ? x0[pr] : 0.0;
       r[pr] = rv;
-      bb += rv * rv;
+      bb += bv * bv;
+      rr += rv * rv;
     }
     rs[threadIdx.x] = rv;
     __syncthreads();
@@ -1399,29 +1406,40 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
     }
     __syncthreads();
   }
-  bb = block_sum(bb, sh);
+  rr = block_sum(rr, sh);
   rz = block_sum(rz, sh);
+  bb = block_sum(bb, sh);
   if (threadIdx.x == 0) {
-    part[2 * blockIdx.x] = bb;
+    part[2 * blockIdx.x] = rr;
     part[2 * blockIdx.x + 1] = rz;
+    part[2 * gridDim.x + blockIdx.x] = bb;
   }
   if (last_block(&st->counter)) {
     double a, c;
     final_sum2(part, gridDim.x, &a, &c, sh);
+    double bsum = 0.0;
+    for (int j = threadIdx.x; j < (int)gridDim.x; j += blockDim.x) bsum += part[2 * gridDim.x + j];
+    bsum = block_sum(bsum, sh);
     if (threadIdx.x == 0) {
       st->counter = 0;
       st->it = 0;
       st->breakdown = 0;
       st->max_iter = max_iter;
-      const double bn = sqrt(a);
+      const double bn = sqrt(bsum);
       st->bnorm = bn;
       st->tol_abs = rel_tol * bn;
-      st->rnorm = bn;
+      const double rn = sqrt(a);
+      st->rnorm = rn;
       st->rs = c;
       st->done = 0;
       st->converged = 0;
       st->aux0 = 0.0;
       if (bn == 0.0) {
+        st->done = 1;
+        st->converged = 1;
+        st->rnorm = 0.0;
+        st->aux0 = 1.0;  // x must be zeroed (zero rhs)
+      } else if (rn <= rel_tol * bn) {
         st->done = 1;
         st->converged = 1;
       }
@@ -1831,11 +1849,19 @@ static inline int bj_grid(int L) {
   const int nb = (L / 2) * (L / 2);
   return grid_for(nb, 16, kRedBlocks);
 }
-int gbk_bjcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
-                  const double* inv, double rel_tol, int max_iter, void* st, double* part,
-                  cudaStream_t s) {
-  k_bjcg_init<<<bj_grid(L), 192, 0, s>>>(L, w, b, x, r, p, z, inv, rel_tol, max_iter,
-                                         (KState*)st, part);
+static inline int bj_init_grid(int L) {
+  const int nb = (L / 2) * (L / 2);
+  return grid_for(nb, 16, (2 * kRedBlocks) / 3);
+}
+int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
+                  double* r, double* p, double* z, const double* inv, double rel_tol,
+                  int max_iter, void* st, double* part, cudaStream_t s) {
+  k_bjcg_init<<<bj_init_grid(L), 192, 0, s>>>(L, w, b, x0, Ax0, x, r, p, z, inv, rel_tol,
+                                              max_iter, (KState*)st, part);
+  if (x0) {
+    const long long npad = (long long)(L + 2 * w) * (L + 2 * w) * 3;
+    k_cg_zero_if<<<grid_for(npad, 256, kRedBlocks), 256, 0, s>>>(npad, x, (KState*)st);
+  }
   return (int)cudaGetLastError();
 }
 int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
@@ -2195,9 +2221,14 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
     // inner CG: A_op y = cur, x0 = cur when warm (its A x0 is e->ax from the
     // previous Rayleigh quotient)
     k_state_reset<<<1, 1, 0, s>>>(kb, (int)e->inner_max_iter);
-    k_cg_init<<<gv, 256, 0, s>>>(npad, cur, have_prev ? cur : nullptr,
-                                 have_prev ? e->ax : nullptr, e->cx, e->cr, e->cp,
-                                 e->inner_tol, (int)e->inner_max_iter, kb, e->partb);
+    if (e->inner_pcg)
+      k_bjcg_init<<<bj_init_grid(e->L), 192, 0, s>>>(
+          e->L, e->w, cur, have_prev ? cur : nullptr, have_prev ? e->ax : nullptr, e->cx, e->cr,
+          e->cp, e->cz, e->inv, e->inner_tol, (int)e->inner_max_iter, kb, e->partb);
+    else
+      k_cg_init<<<gv, 256, 0, s>>>(npad, cur, have_prev ? cur : nullptr,
+                                   have_prev ? e->ax : nullptr, e->cx, e->cr, e->cp,
+                                   e->inner_tol, (int)e->inner_max_iter, kb, e->partb);
     k_cg_zero_if<<<gv, 256, 0, s>>>(npad, e->cx, kb);
     *launches += 3;
     chunk = 8;
@@ -2205,8 +2236,14 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
       for (int i = 0; i < chunk; ++i) {
         if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;
         post_a(e, s);
-        k_cg_update<<<gv, 256, 0, s>>>(npad, e->cx, e->cr, e->cp, e->cap, kb, e->partb);
-        k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cr, e->cp, kb);
+        if (e->inner_pcg) {
+          k_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, e->cx, e->cr, e->cp, e->cap,
+                                                      e->cz, e->inv, kb, e->partb);
+          k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cz, e->cp, kb);
+        } else {
+          k_cg_update<<<gv, 256, 0, s>>>(npad, e->cx, e->cr, e->cp, e->cap, kb, e->partb);
+          k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cr, e->cp, kb);
+        }
       }
       *launches += 5LL * chunk;
       if ((err = (int)cudaGetLastError())) return err;

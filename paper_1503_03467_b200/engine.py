@@ -19,5 +19,6 @@ class LevelEngineArgs(ctypes.Structure):
         ("tol", _D), ("inner_tol", _D), ("inner_max_iter", ctypes.c_int64),
         ("lam_min", _D), ("lam_max", _D), ("calls", ctypes.c_int64),
         ("power_its", ctypes.c_int), ("n_outer", ctypes.c_int), ("breakdown", ctypes.c_int),
-        ("pad", ctypes.c_int), ("inner_its", ctypes.c_int * 64),
+        ("inner_pcg", ctypes.c_int), ("inner_its", ctypes.c_int * 64),
+        ("cz", _P),
     ]

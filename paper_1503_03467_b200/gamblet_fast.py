@@ -450,12 +450,12 @@ def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
 
 
-def _pcg(op, b, rel_tol, max_iter=None, kr=None):
+def _pcg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     """Block-Jacobi PCG for the subband systems (2x2-parent 12x12 blocks of
-    S B S); same stopping rule as sparse_core.py:161 on the true residual.
-    Returns the tuple of _cg."""
+    S B S); same stopping rule as sparse_core.py:161 on the true residual,
+    same warm start (x0) semantics as _cg.  Returns the tuple of _cg."""
     if op.nr != 3 or op.L < 2 or op.L % 2:
-        return _cg(op, b, rel_tol, max_iter=max_iter, kr=kr)
+        return _cg(op, b, rel_tol, x0=x0, max_iter=max_iter, kr=kr)
     if max_iter is None:
         max_iter = max(200, 2 * op.n)
     max_iter = min(max_iter, MAX_ITER_CAP)
@@ -464,9 +464,13 @@ def _pcg(op, b, rel_tol, max_iter=None, kr=None):
     st = dv.stream()
     x, r, p, Ap, z = (op.vec() for _ in range(5))
     nat.call("gb_state_reset", dv.ptr(kr.state), max_iter, st)
-    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), dv.ptr(x), dv.ptr(r), dv.ptr(p),
-             dv.ptr(z), dv.ptr(inv), float(rel_tol), int(max_iter), dv.ptr(kr.state),
-             dv.ptr(kr.part), st)
+    Ax0 = None
+    if x0 is not None:
+        Ax0 = op.vec()
+        op.apply(x0, Ax0)
+    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), dv.ptr(x0), dv.ptr(Ax0), dv.ptr(x),
+             dv.ptr(r), dv.ptr(p), dv.ptr(z), dv.ptr(inv), float(rel_tol), int(max_iter),
+             dv.ptr(kr.state), dv.ptr(kr.part), st)
     nat.call("gb_bjcg_solve", op.L, op.w, dv.ptr(op.BsT), dv.ptr(inv), dv.ptr(x),
              dv.ptr(r), dv.ptr(p), dv.ptr(Ap), dv.ptr(z), dv.ptr(kr.state), dv.ptr(kr.part),
              kr.host.data_ptr(), 128, st, op.layout)
@@ -476,10 +480,12 @@ def _pcg(op, b, rel_tol, max_iter=None, kr=None):
 
 
 def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
-    """(lambda_min, lambda_max) of S B S exactly as sparse_core.py:232-278:
-    power iteration, then inverse iteration with warm-started inner CG;
-    start vectors from numpy default_rng(seed).  Returns (lam_min, lam_max,
-    operator applications)."""
+    """(lambda_min, lambda_max) of S B S as sparse_core.py:232-278: power
+    iteration, then inverse iteration with warm-started inner solves to
+    rel_tol max(1e-12, 1e-3 tol); start vectors from numpy default_rng(seed).
+    The inner solver is block-Jacobi PCG (SPECTRAL_INNER="pcg", default) or
+    the reference's plain CG ("cg"); the estimates agree to the inner
+    tolerance.  Returns (lam_min, lam_max, operator applications)."""
     n = op.n
     st = dv.stream()
     rng = np.random.default_rng(seed)
@@ -510,7 +516,8 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
     dots = dv.empty(4)
     outer = []
     for _ in range(max_iter):
-        yv, its, _, _, brk, _ = _cg(op, x, inner, x0=y_prev, kr=ykr)
+        inner_solve = _pcg if SPECTRAL_INNER == "pcg" else _cg
+        yv, its, _, _, brk, _ = inner_solve(op, x, inner, x0=y_prev, kr=ykr)
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")
@@ -562,8 +569,8 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
     xa, ra, pa, apa, za = (op.vec() for _ in range(5))
     max_a = min(max(200, 2 * n), MAX_ITER_CAP)
     nat.call("gb_state_reset", dv.ptr(ka.state), max_a, st)
-    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(rhs_pad), dv.ptr(xa), dv.ptr(ra), dv.ptr(pa),
-             dv.ptr(za), dv.ptr(inv), float(tol_a), int(max_a), dv.ptr(ka.state),
+    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(rhs_pad), None, None, dv.ptr(xa), dv.ptr(ra),
+             dv.ptr(pa), dv.ptr(za), dv.ptr(inv), float(tol_a), int(max_a), dv.ptr(ka.state),
              dv.ptr(ka.part), st)
     # B: start vectors drawn exactly as eig_extremes draws them
     rng = np.random.default_rng(seed)
@@ -579,7 +586,7 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
              dv.ptr(kb.state), dv.ptr(kb.part), st)
     nat.call("gb_scale_by_norm", op.npad, dv.ptr(xs), dv.ptr(kb.dots), 0, dv.ptr(xs), None, st)
     nat.call("gb_state_reset", dv.ptr(kb.state), max_iter, st)
-    yb, xn, ax, cx, cr, cp, cap = (op.vec() for _ in range(7))
+    yb, xn, ax, cx, cr, cp, cap, cz = (op.vec() for _ in range(8))
     dots = dv.empty(4)
     args = LevelEngineArgs(
         L=op.L, w=op.w, max_chunk=128, max_outer=max_iter, BsT=dv.ptr(op.BsT),
@@ -589,7 +596,8 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
         cx=dv.ptr(cx), cr=dv.ptr(cr), cp=dv.ptr(cp), cap=dv.ptr(cap), stb=dv.ptr(kb.state),
         partb=dv.ptr(kb.part), hstb=kb.host.data_ptr(), dots=dv.ptr(dots),
         hdots=kb.hdots.data_ptr(), tol=tol, inner_tol=max(1e-12, 1e-3 * tol),
-        inner_max_iter=min(max(200, 2 * n), MAX_ITER_CAP))
+        inner_max_iter=min(max(200, 2 * n), MAX_ITER_CAP),
+        inner_pcg=int(SPECTRAL_INNER == "pcg"), cz=dv.ptr(cz))
     nat.call("gb_level_engine", nat.ctypes.byref(args), st)
     if args.breakdown > 0:
         raise NumericalError(f"CG breakdown at iteration {args.breakdown}: p^T A p <= 0 "
@@ -615,6 +623,11 @@ SPECTRAL_PRIORITY = int(__import__("os").environ.get("GB_SPECTRAL_PRIORITY", "-1
 # 0.24 ms for the full box at q=10, so the full layout is the default
 SYMMETRIC_SPMV = __import__("os").environ.get("GB_SYM_SPMV", "0") == "1"
 MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
+# inner solver of the inverse iteration for lambda_min: "pcg" (block-Jacobi,
+# the subband preconditioner) or "cg" (the reference's unpreconditioned CG).
+# lambda_min feeds only the reported conditioning (tight mode has no cheap
+# copy), and both stop at the same relative residual.
+SPECTRAL_INNER = __import__("os").environ.get("GB_SPECTRAL_INNER", "pcg")
 
 
 class _LevelTasks:

@@ -152,4 +152,4 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.EXPORTED)
-    assert lib.gb_abi_version() == 2
+    assert lib.gb_abi_version() == 3
