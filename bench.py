@@ -251,14 +251,19 @@ def run_ours(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         ev0.record()
+        marks = []
         for _ in range(args.steps):
             levels, parts, counter = step_device()
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record()
         ev1.record()
         torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     launches = nat.query("gb_launch_count") - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
+    step_ms = [round(ev0.elapsed_time(marks[0]), 1)] + [
+        round(a.elapsed_time(b_), 1) for a, b_ in zip(marks, marks[1:])]
     phase_ms = {k: v / args.steps for k, v in dv.Prof.times_ms().items()}
     phase_flops = {k: v / args.steps for k, v in dv.Prof.flops.items()}
     phase_bytes = {k: v / args.steps for k, v in dv.Prof.bytes.items()}
@@ -371,6 +376,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline_fp64": fp,
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "step_ms": step_ms,
         "phases_ms": {k: round(v, 3) for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
         "phase_launch_groups": phase_counts,
         "timeline_last_step_ms": timeline if args.timeline else None,

@@ -128,6 +128,9 @@ int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double*
  * both accumulate in the reference's order (ascending CSR column), -1
  * queries; returns the previous mode. */
 int gb_products_mode(int mma);
+/* launch tuning: what = 0 -> total CTAs of the correction-patch grid (0 =
+ * auto); value < 0 queries.  Returns the previous value (-1: unknown key). */
+int gb_tune(int what, int value);
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
                 double* psi_next, double* rowmax, void* stream);
@@ -181,9 +184,10 @@ int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, doub
                   void* stream, int layout);
 /* block-Jacobi (2x2 parents = 12x12 blocks) PCG for the subband systems */
 int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream);
-int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
-                 double* r, double* p, double* z, const double* inv, double rel_tol, int max_iter,
-                 void* state, double* partials, void* stream);
+/* x = x0_scale * x0 (x0, Ax0 = A x0 nullable: zero start) */
+int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
+                 double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                 double rel_tol, int max_iter, void* state, double* partials, void* stream);
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
                        double* partials, void* stream, int layout);

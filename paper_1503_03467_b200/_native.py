@@ -51,6 +51,7 @@ _SIGS = {
     "gb_wpsi": ([_I, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "gb_psi_next": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P, _P, _P], _I),
     "gb_products_mode": ([_I], _I),
+    "gb_tune": ([_I, _I], _I),
     "gb_kstate_bytes": ([], _Z),
     "gb_red_blocks": ([], _I),
     "gb_state_reset": ([_P, _I, _P], _I),
@@ -72,7 +73,7 @@ _SIGS = {
     "gb_sym_supported": ([_I, _I, _I], _I),
     "gb_scale_box_symT": ([_I, _I, _P, _P, _P, _P], _I),
     "gb_bj_setup": ([_I, _I, _P, _P, _P, _P], _I),
-    "gb_bjcg_init": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
+    "gb_bjcg_init": ([_I, _I, _P, _P, _P, _D, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P], _I),
     "gb_bjcg_iterations": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I], _I),
     "gb_sync_read": ([_P, _P, _Z, _P], _I),
     "gb_tcg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
@@ -127,6 +128,12 @@ def load(path=None):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    # launch tuning from the environment (see gb_tune in include/gamblets_b200.h)
+    import os
+    if os.environ.get("GB_PATCH_GRID"):
+        lib.gb_tune(0, int(os.environ["GB_PATCH_GRID"]))
+    if os.environ.get("GB_PRODUCTS_MODE"):
+        lib.gb_products_mode(int(os.environ["GB_PRODUCTS_MODE"]))
     _lib = lib
     return lib
 

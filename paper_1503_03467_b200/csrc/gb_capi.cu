@@ -193,6 +193,7 @@ int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wd
 }
 
 int gb_products_mode(int mma) { return gbk_products_mode(mma); }
+int gb_tune(int what, int value) { return gbk_tune(what, value); }
 size_t gb_kstate_bytes(void) { return gbk_kstate_bytes(); }
 int gb_red_blocks(void) { return gbk_red_blocks(); }
 int gb_state_reset(void* state, int max_iter, void* stream) {
@@ -290,12 +291,12 @@ int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, voi
   COUNT(1);
   return wrap(gbk_bj_setup(L, w, B, s, inv, ST(stream)), "bj_setup");
 }
-int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
-                 double* r, double* p, double* z, const double* inv, double rel_tol, int max_iter,
-                 void* state, double* partials, void* stream) {
+int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
+                 double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                 double rel_tol, int max_iter, void* state, double* partials, void* stream) {
   COUNT(1);
-  return wrap(gbk_bjcg_init(L, w, b, x0, Ax0, x, r, p, z, inv, rel_tol, max_iter, state,
-                            partials, ST(stream)),
+  return wrap(gbk_bjcg_init(L, w, b, x0, Ax0, x0_scale, x, r, p, z, inv, rel_tol, max_iter,
+                            state, partials, ST(stream)),
               "bjcg_init");
 }
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,

@@ -127,9 +127,9 @@ int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, dou
 size_t gbk_boxT_elems(int L, int nr, int w);
 int gbk_bj_setup(int L, int w, const double* B, const double* sv, double* inv,
                  cudaStream_t s);
-int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
-                  double* r, double* p, double* z, const double* inv, double rel_tol,
-                  int max_iter, void* st, double* part, cudaStream_t s);
+int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
+                  double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                  double rel_tol, int max_iter, void* st, double* part, cudaStream_t s);
 int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                         double* r, double* p, double* Ap, double* z, int iters, void* st,
                         double* part, cudaStream_t s, int layout);
@@ -160,3 +160,4 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
 #include "gb_engine.h"
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches);
 int gbk_products_mode(int mma);
+int gbk_tune(int what, int value);

@@ -1361,13 +1361,14 @@ __global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __res
   }
 }
 
-// start: x = x0 (or 0), r = b - A x0 (Ax0 null => x0 = 0), z = Minv r, p = z;
+// start: x = s x0 (or 0), r = b - s A x0 (Ax0 null => x0 = 0), z = Minv r, p = z;
 // ||b||, ||r||, r.z and the early exits of sparse_core.py:138-148.  Partials
 // are (||r||^2, r.z) pairs in part[0, 2G) and ||b||^2 in part[2G, 3G), so the
 // grid is capped at 2/3 of the caller's 2 * kRedBlocks partial slots.
 __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* __restrict__ b,
                                                    const double* __restrict__ x0,
                                                    const double* __restrict__ Ax0,
+                                                   double x0_scale,
                                                    double* __restrict__ x, double* __restrict__ r,
                                                    double* __restrict__ p,
                                                    double* __restrict__ z,
@@ -1386,8 +1387,8 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
     if (bk < nb) {
       pr = bj_row_pad(L, w, bk, l);
       const double bv = b[pr];
-      rv = Ax0 ? bv - Ax0[pr] : bv;
-      x[pr] = x0 ? x0[pr] : 0.0;
+      rv = Ax0 ? bv - x0_scale * Ax0[pr] : bv;
+      x[pr] = x0 ? x0_scale * x0[pr] : 0.0;
       r[pr] = rv;
       bb += bv * bv;
       rr += rv * rv;
@@ -1853,11 +1854,11 @@ static inline int bj_init_grid(int L) {
   const int nb = (L / 2) * (L / 2);
   return grid_for(nb, 16, (2 * kRedBlocks) / 3);
 }
-int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0, double* x,
-                  double* r, double* p, double* z, const double* inv, double rel_tol,
-                  int max_iter, void* st, double* part, cudaStream_t s) {
-  k_bjcg_init<<<bj_init_grid(L), 192, 0, s>>>(L, w, b, x0, Ax0, x, r, p, z, inv, rel_tol,
-                                              max_iter, (KState*)st, part);
+int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
+                  double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                  double rel_tol, int max_iter, void* st, double* part, cudaStream_t s) {
+  k_bjcg_init<<<bj_init_grid(L), 192, 0, s>>>(L, w, b, x0, Ax0, x0_scale, x, r, p, z, inv,
+                                              rel_tol, max_iter, (KState*)st, part);
   if (x0) {
     const long long npad = (long long)(L + 2 * w) * (L + 2 * w) * 3;
     k_cg_zero_if<<<grid_for(npad, 256, kRedBlocks), 256, 0, s>>>(npad, x, (KState*)st);
@@ -2173,6 +2174,19 @@ static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, in
   return (int)cudaGetLastError();
 }
 
+// one live Krylov half: the dedicated single-vector tiled pass (smaller
+// shared-memory footprint than the dual kernel, same arithmetic)
+static int launch_single(const gb_level_engine_args* e, const double* x, double* y, void* st,
+                         double* part, int mode, cudaStream_t s) {
+  if (mode == 0)
+    k_tcg_spmv_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y,
+                                                                      (KState*)st, part);
+  else
+    k_tpow_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x,
+                                                                        y, (KState*)st, part);
+  return (int)cudaGetLastError();
+}
+
 static void post_a(const gb_level_engine_args* e, cudaStream_t s) {
   const int Lpad = e->L + 2 * e->w;
   const long long npad = (long long)Lpad * Lpad * 3;
@@ -2194,9 +2208,14 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
   int chunk = 8;
   // --- power iteration (B) paired with the PCG (A) -----------------------
   for (;;) {
+    const bool a_live = !ha->done;
     for (int i = 0; i < chunk; ++i) {
-      if ((err = launch_dual(e, e->xb, e->yb, 1, s))) return err;
-      post_a(e, s);
+      if (a_live) {
+        if ((err = launch_dual(e, e->xb, e->yb, 1, s))) return err;
+        post_a(e, s);
+      } else if ((err = launch_single(e, e->xb, e->yb, e->stb, e->partb, 1, s))) {
+        return err;
+      }
       k_pow_step<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, e->tol, kb, e->partb);
       k_pow_scale<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, kb);
     }
@@ -2221,10 +2240,13 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
     // inner CG: A_op y = cur, x0 = cur when warm (its A x0 is e->ax from the
     // previous Rayleigh quotient)
     k_state_reset<<<1, 1, 0, s>>>(kb, (int)e->inner_max_iter);
+    // PCG mode warm-starts from cur / lambda (the current Rayleigh quotient),
+    // the reference's CG mode from cur itself (sparse_core.py:266)
     if (e->inner_pcg)
       k_bjcg_init<<<bj_init_grid(e->L), 192, 0, s>>>(
-          e->L, e->w, cur, have_prev ? cur : nullptr, have_prev ? e->ax : nullptr, e->cx, e->cr,
-          e->cp, e->cz, e->inv, e->inner_tol, (int)e->inner_max_iter, kb, e->partb);
+          e->L, e->w, cur, have_prev ? cur : nullptr, have_prev ? e->ax : nullptr,
+          have_prev ? 1.0 / e->lam_min : 1.0, e->cx, e->cr, e->cp, e->cz, e->inv, e->inner_tol,
+          (int)e->inner_max_iter, kb, e->partb);
     else
       k_cg_init<<<gv, 256, 0, s>>>(npad, cur, have_prev ? cur : nullptr,
                                    have_prev ? e->ax : nullptr, e->cx, e->cr, e->cp,
@@ -2233,9 +2255,14 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
     *launches += 3;
     chunk = 8;
     for (;;) {
+      const bool a_live = !ha->done;
       for (int i = 0; i < chunk; ++i) {
-        if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;
-        post_a(e, s);
+        if (a_live) {
+          if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;
+          post_a(e, s);
+        } else if ((err = launch_single(e, e->cp, e->cap, e->stb, e->partb, 0, s))) {
+          return err;
+        }
         if (e->inner_pcg) {
           k_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, e->cx, e->cr, e->cp, e->cap,
                                                       e->cz, e->inv, kb, e->partb);
@@ -2286,7 +2313,7 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
   chunk = 8;
   while (!ha->done) {
     for (int i = 0; i < chunk; ++i) {
-      if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;  // B done: single pass
+      if ((err = launch_single(e, e->pa, e->apa, e->sta, e->parta, 0, s))) return err;
       post_a(e, s);
     }
     *launches += 3LL * chunk;

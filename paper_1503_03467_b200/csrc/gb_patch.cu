@@ -502,6 +502,19 @@ int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB,
 
 // v2 entry points: pre-scaled boxes, shared-memory tiled DMMA Cholesky.
 // Return 1 (caller falls back to v1) when the patch does not fit.
+// launch tuning (gb_tune): total CTAs of the correction-patch grid, 0 = auto
+// (4 waves of the resident CTAs).  Fewer CTAs leave SMs (shared memory) free
+// for the HBM-bound Krylov kernels running concurrently on the level streams.
+static int g_patch_grid = 0;
+int gbk_tune(int what, int value) {
+  if (what == 0) {
+    const int old = g_patch_grid;
+    if (value >= 0) g_patch_grid = value;
+    return old;
+  }
+  return -1;
+}
+
 int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB, int wG,
                               const double* G, int rho, double* Dt, long long* status,
                               cudaStream_t st) {
@@ -514,7 +527,8 @@ int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB,
   const long long P = (long long)Lp * Lp;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
-  int g = (int)(P < 148LL * per_sm * 4 ? P : 148LL * per_sm * 4);
+  long long gmax = g_patch_grid > 0 ? g_patch_grid : 148LL * per_sm * 4;
+  int g = (int)(P < gmax ? P : gmax);
   k_correction_patches_v2<<<g, 256, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt, status, Tmax);
   return (int)cudaGetLastError();
 }

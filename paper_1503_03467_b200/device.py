@@ -44,6 +44,16 @@ def ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def reserve(nbytes):
+    """Grow the caching allocator by one segment of `nbytes` (released back to
+    the cache immediately).  Later work tensors are carved out of it, so a
+    steady-state solve makes no cudaMalloc calls -- those stall every stream."""
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    blk = torch.empty(int(nbytes), dtype=torch.uint8, device=device())
+    del blk
+
+
 def empty(n, dtype=torch.float64):
     return torch.empty(int(n), dtype=dtype, device=device())
 

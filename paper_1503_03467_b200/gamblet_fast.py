@@ -450,7 +450,7 @@ def _cg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
 
 
-def _pcg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
+def _pcg(op, b, rel_tol, x0=None, max_iter=None, kr=None, x0_scale=1.0):
     """Block-Jacobi PCG for the subband systems (2x2-parent 12x12 blocks of
     S B S); same stopping rule as sparse_core.py:161 on the true residual,
     same warm start (x0) semantics as _cg.  Returns the tuple of _cg."""
@@ -468,7 +468,8 @@ def _pcg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     if x0 is not None:
         Ax0 = op.vec()
         op.apply(x0, Ax0)
-    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), dv.ptr(x0), dv.ptr(Ax0), dv.ptr(x),
+    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), dv.ptr(x0), dv.ptr(Ax0), float(x0_scale),
+             dv.ptr(x),
              dv.ptr(r), dv.ptr(p), dv.ptr(z), dv.ptr(inv), float(rel_tol), int(max_iter),
              dv.ptr(kr.state), dv.ptr(kr.part), st)
     nat.call("gb_bjcg_solve", op.L, op.w, dv.ptr(op.BsT), dv.ptr(inv), dv.ptr(x),
@@ -477,6 +478,27 @@ def _pcg(op, b, rel_tol, x0=None, max_iter=None, kr=None):
     h = kr.host_view()
     rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
     return x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h
+
+
+_START_VECTORS = {}
+_START_LOCK = threading.Lock()
+
+
+def _start_vectors(n, seed):
+    """The two standard-normal start vectors eig_extremes draws from
+    default_rng(seed) (sparse_core.py:244, 262), as device arrays.  They are
+    a pure function of (n, seed), so they are drawn and uploaded once."""
+    key = (n, seed)
+    with _START_LOCK:
+        v = _START_VECTORS.get(key)
+        if v is None:
+            rng = np.random.default_rng(seed)
+            x1 = rng.standard_normal(n)
+            x2 = rng.standard_normal(n)
+            v = (dv.to_dev(x1), dv.to_dev(x2))
+            torch.cuda.current_stream().synchronize()
+            _START_VECTORS[key] = v
+    return v
 
 
 def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
@@ -488,12 +510,10 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
     tolerance.  Returns (lam_min, lam_max, operator applications)."""
     n = op.n
     st = dv.stream()
-    rng = np.random.default_rng(seed)
-    x1 = rng.standard_normal(n)
-    x2 = rng.standard_normal(n)
+    x1, x2 = _start_vectors(n, seed)
     kr = _Krylov(op.npad)
     calls = 0
-    x = op.pad(dv.to_dev(x1))
+    x = op.pad(x1)
     y = op.vec()
     nat.call("gb_dot2", op.npad, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots),
              dv.ptr(kr.state), dv.ptr(kr.part), st)
@@ -507,7 +527,7 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
     calls += int(h["it"]) + (0 if h["ynorm"] != 0 else 1)
 
     inner = max(1e-12, 1e-3 * tol)
-    x = op.pad(dv.to_dev(x2))
+    x = op.pad(x2)
     nat.call("gb_dot2", op.npad, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots),
              dv.ptr(kr.state), dv.ptr(kr.part), st)
     nat.call("gb_scale_by_norm", op.npad, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
@@ -516,8 +536,11 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
     dots = dv.empty(4)
     outer = []
     for _ in range(max_iter):
-        inner_solve = _pcg if SPECTRAL_INNER == "pcg" else _cg
-        yv, its, _, _, brk, _ = inner_solve(op, x, inner, x0=y_prev, kr=ykr)
+        if SPECTRAL_INNER == "pcg":  # warm start y_prev / lambda (see gb_level_engine)
+            yv, its, _, _, brk, _ = _pcg(op, x, inner, x0=y_prev, kr=ykr,
+                                         x0_scale=1.0 / lam_min if y_prev is not None else 1.0)
+        else:
+            yv, its, _, _, brk, _ = _cg(op, x, inner, x0=y_prev, kr=ykr)
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")
@@ -569,19 +592,17 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
     xa, ra, pa, apa, za = (op.vec() for _ in range(5))
     max_a = min(max(200, 2 * n), MAX_ITER_CAP)
     nat.call("gb_state_reset", dv.ptr(ka.state), max_a, st)
-    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(rhs_pad), None, None, dv.ptr(xa), dv.ptr(ra),
+    nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(rhs_pad), None, None, 1.0, dv.ptr(xa), dv.ptr(ra),
              dv.ptr(pa), dv.ptr(za), dv.ptr(inv), float(tol_a), int(max_a), dv.ptr(ka.state),
              dv.ptr(ka.part), st)
     # B: start vectors drawn exactly as eig_extremes draws them
-    rng = np.random.default_rng(seed)
-    x1 = rng.standard_normal(n)
-    x2 = rng.standard_normal(n)
+    x1, x2 = _start_vectors(n, seed)
     kb = _Krylov(op.npad)
-    xb = op.pad(dv.to_dev(x1))
+    xb = op.pad(x1)
     nat.call("gb_dot2", op.npad, dv.ptr(xb), dv.ptr(xb), None, dv.ptr(kb.dots),
              dv.ptr(kb.state), dv.ptr(kb.part), st)
     nat.call("gb_scale_by_norm", op.npad, dv.ptr(xb), dv.ptr(kb.dots), 0, dv.ptr(xb), None, st)
-    xs = op.pad(dv.to_dev(x2))
+    xs = op.pad(x2)
     nat.call("gb_dot2", op.npad, dv.ptr(xs), dv.ptr(xs), None, dv.ptr(kb.dots),
              dv.ptr(kb.state), dv.ptr(kb.part), st)
     nat.call("gb_scale_by_norm", op.npad, dv.ptr(xs), dv.ptr(kb.dots), 0, dv.ptr(xs), None, st)
