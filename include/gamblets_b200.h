@@ -164,9 +164,13 @@ int gb_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, double
 int gb_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
                   void* stream);
 /* layout argument of the Krylov entries: 0 = full blocked slot-major box
- * (gb_scale_box_T), 1 = symmetric upper half (gb_scale_box_symT; tiled
- * levels only, gb_sym_supported) */
+ * (gb_scale_box_T), 1 = symmetric band: upper 3x3 blocks per parent
+ * (gb_scale_box_symT; tiled levels only, gb_sym_supported).  In layout 1
+ * every OUTPUT vector of an S B S application (Ap, y) must have
+ * (L+2w)^2*3 + gb_sym_overflow_elems(L, w) doubles: the tail holds the
+ * tiles' spill-over between the two passes of one application. */
 size_t gb_boxsym_elems(int L, int w);
+size_t gb_sym_overflow_elems(int L, int w);
 int gb_sym_supported(int L, int nr, int w);
 int gb_scale_box_symT(int L, int w, const double* B, const double* s, double* UsT,
                       void* stream);

@@ -70,6 +70,7 @@ _SIGS = {
     "gb_tpow_iterations": ([_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _I], _I),
     "gb_tbox_apply": ([_I, _I, _I, _P, _P, _P, _P, _I], _I),
     "gb_boxsym_elems": ([_I, _I], _Z),
+    "gb_sym_overflow_elems": ([_I, _I], _Z),
     "gb_sym_supported": ([_I, _I, _I], _I),
     "gb_scale_box_symT": ([_I, _I, _P, _P, _P, _P], _I),
     "gb_bj_setup": ([_I, _I, _P, _P, _P, _P], _I),

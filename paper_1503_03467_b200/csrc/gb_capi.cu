@@ -260,6 +260,10 @@ int gb_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, doubl
   return wrap(gbk_pbox_apply(L, nr, w, Bs, x, y, ST(stream)), "pbox_apply");
 }
 size_t gb_boxT_elems(int L, int nr, int w) { return gbk_boxT_elems(L, nr, w); }
+// launches of one Krylov iteration: S B S application (2 kernels in the
+// symmetric band layout) + update + direction
+#define SPL(layout, L, nr, w) \
+  (((layout) == 1 && gbk_sym_supported((L), (nr), (w))) ? 4ULL : 3ULL)
 int gb_scale_box_T(int L, int nr, int w, const double* B, const double* s, double* BsT,
                    void* stream) {
   COUNT(1);
@@ -268,7 +272,7 @@ int gb_scale_box_T(int L, int nr, int w, const double* B, const double* s, doubl
 int gb_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
                       double* p, double* Ap, int iters, void* state, double* partials,
                       void* stream, int layout) {
-  COUNT(3 * (unsigned long long)iters);
+  COUNT(SPL(layout, L, nr, w) * (unsigned long long)iters);
   return wrap(gbk_tcg_iterations(L, nr, w, BsT, x, r, p, Ap, iters, state, partials,
                                  ST(stream), layout),
               "tcg_iterations");
@@ -276,14 +280,14 @@ int gb_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double
 int gb_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, double* y,
                        double tol, int iters, void* state, double* partials, void* stream,
                        int layout) {
-  COUNT(3 * (unsigned long long)iters);
+  COUNT(SPL(layout, L, nr, w) * (unsigned long long)iters);
   return wrap(gbk_tpow_iterations(L, nr, w, BsT, x, y, tol, iters, state, partials,
                                   ST(stream), layout),
               "tpow_iterations");
 }
 int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
                   void* stream, int layout) {
-  COUNT(1);
+  COUNT(SPL(layout, L, nr, w) - 2);
   return wrap(gbk_tbox_apply(L, nr, w, BsT, x, y, ST(stream), layout), "tbox_apply");
 }
 int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream) {
@@ -302,7 +306,7 @@ int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* 
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
                        double* partials, void* stream, int layout) {
-  COUNT(3 * (unsigned long long)iters);
+  COUNT(SPL(layout, L, 3, w) * (unsigned long long)iters);
   return wrap(gbk_bjcg_iterations(L, w, BsT, inv, x, r, p, Ap, z, iters, state, partials,
                                   ST(stream), layout),
               "bjcg_iterations");
@@ -338,6 +342,7 @@ int gb_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y,
   return wrap(e, "tpow_solve");
 }
 size_t gb_boxsym_elems(int L, int w) { return gbk_boxsym_elems(L, w); }
+size_t gb_sym_overflow_elems(int L, int w) { return gbk_sym_overflow_elems(L, w); }
 int gb_sym_supported(int L, int nr, int w) { return gbk_sym_supported(L, nr, w); }
 int gb_scale_box_symT(int L, int w, const double* B, const double* s, double* UsT,
                       void* stream) {

@@ -30,4 +30,6 @@ typedef struct gb_level_engine_args {
   int inner_pcg;           /* 1: inner solves are block-Jacobi PCG (uses inv, cz) */
   int inner_its[64];
   double* cz;              /* PCG preconditioned residual of the inner solves */
+  int layout;              /* 0: full box BsT, 1: symmetric band (gb_scale_box_symT);
+                            * output vectors then carry gb_sym_overflow_elems tail */
 } gb_level_engine_args;

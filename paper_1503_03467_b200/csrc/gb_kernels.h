@@ -144,6 +144,7 @@ int gbk_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y
                    void* st, double* part, void* host_state, int max_chunk, cudaStream_t s,
                    long long* launches, int layout);
 size_t gbk_boxsym_elems(int L, int w);
+size_t gbk_sym_overflow_elems(int L, int w);
 int gbk_sym_supported(int L, int nr, int w);
 int gbk_scale_box_symT(int L, int w, const double* B, const double* sv, double* UsT,
                        cudaStream_t s);

@@ -818,213 +818,6 @@ __global__ void __launch_bounds__(192) k_tbox_apply_tiled(int L, int w,
 
 
 // ---------------------------------------------------------------------------
-// Symmetric v5 SpMV (nr = 3, tiled): only the upper half of S B S is stored.
-// Upper slots of row r = (p, c): the 2w^2 + 2w positive offsets d > 0
-// (lexicographic in (ds, dt)) x 3 components, then the 3 slots of d = 0 (the
-// entries with c' < c stored as 0).  Su = 3 (2w^2 + 2w) + 3 slots, padded to
-// even; same blocked slot-pair layout as v3.  The lower half of row r is read
-// from the upper halves of the rows q = (p - d, c') of the w grid rows above,
-// which neighbouring CTAs stream at the same time (L2 hits), so DRAM moves
-// half the bytes of the full box.
-// ---------------------------------------------------------------------------
-__host__ __device__ __forceinline__ int sym_slots(int w) { return 3 * (2 * w * w + 2 * w) + 3; }
-__host__ __device__ __forceinline__ int sym_pad(int w) {
-  const int su = sym_slots(w);
-  return su + (su & 1);
-}
-
-__global__ void k_scale_box_symT(int L, int w, const double* __restrict__ B,
-                                 const double* __restrict__ s, double* __restrict__ UsT) {
-  const int W2 = 2 * w + 1, S = W2 * W2 * 3, Sp = sym_pad(w), npos = 2 * w * w + 2 * w;
-  const int bsc = w * W2 + w;  // centre offset index
-  const long long R = (long long)L * L * 3;
-  const long long total = (R + 31) / 32 * 32LL * Sp;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long blk = e / (32LL * Sp);
-    const int rem = (int)(e - blk * 32LL * Sp);
-    const int j = ((rem >> 6) << 1) | (rem & 1);
-    const long long r = blk * 32 + ((rem >> 1) & 31);
-    double v = 0.0;
-    if (r < R && j < 3 * npos + 3) {
-      const int c = (int)(r % 3);
-      int bs, cp;
-      bool keep = true;
-      if (j < 3 * npos) {
-        bs = bsc + 1 + j / 3;
-        cp = j % 3;
-      } else {
-        bs = bsc;
-        cp = j - 3 * npos;
-        keep = cp >= c;
-      }
-      const long long p = r / 3;
-      const int qs = (int)(p / L) + bs / W2 - w, qt = (int)(p % L) + bs % W2 - w;
-      if (keep && qs >= 0 && qs < L && qt >= 0 && qt < L)
-        v = B[r * S + bs * 3 + cp] * s[r] * s[((long long)qs * L + qt) * 3 + cp];
-    }
-    UsT[e] = v;
-  }
-}
-
-__device__ __forceinline__ void build_offsets_sym(int w, int* offu, int* offl, int* dsl,
-                                                  int* dtl) {
-  // offu[j]: window offset of upper slot j relative to the row's own parent
-  // offl[e]: window offset of the negative offset -d_e (e-th positive offset)
-  const int W2 = 2 * w + 1, WC = kTileP + 2 * w, npos = 2 * w * w + 2 * w;
-  const int bsc = w * W2 + w;
-  for (int j = threadIdx.x; j < 3 * npos + 4; j += blockDim.x) {
-    int bs, cp;
-    if (j < 3 * npos) {
-      bs = bsc + 1 + j / 3;
-      cp = j % 3;
-    } else {
-      bs = bsc;
-      cp = j < 3 * npos + 3 ? j - 3 * npos : 0;
-    }
-    offu[j] = ((bs / W2) * WC + (bs % W2)) * 3 + cp;
-  }
-  for (int e = threadIdx.x; e < npos; e += blockDim.x) {
-    const int bs = bsc - 1 - e;  // mirror of bsc + 1 + e
-    offl[e] = ((bs / W2) * WC + (bs % W2)) * 3;
-    dsl[e] = bs / W2 - w;
-    dtl[e] = bs % W2 - w;
-  }
-}
-
-__device__ __forceinline__ void tile_pass_sym(int L, int w, const double* __restrict__ UsT,
-                                              const double* __restrict__ x,
-                                              double* __restrict__ y, const int* offu,
-                                              const int* offl, const int* dsl, const int* dtl,
-                                              double* xs, double* lpart, double* xy,
-                                              double* yy) {
-  const int W2 = 2 * w + 1, Sp = sym_pad(w), Lpad = L + 2 * w, npos = 2 * w * w + 2 * w;
-  const int WC = kTileP + 2 * w;
-  const int tiles_per_row = L / kTileP;
-  const long long ntile = (long long)L * tiles_per_row;
-  double d0 = 0.0, d1 = 0.0;
-  const int tid = threadIdx.x;
-  const int lp = tid / 3, c = tid - 3 * lp;
-  for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
-    const int ps = (int)(t / tiles_per_row), pt0 = (int)(t % tiles_per_row) * kTileP;
-    for (int e = tid; e < W2 * WC * 3; e += blockDim.x) {
-      const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
-      xs[e] = x[((long long)(ps + wr) * Lpad + pt0) * 3 + rem];
-    }
-    __syncthreads();
-    const int pt = pt0 + lp;
-    const long long r = ((long long)ps * L + pt) * 3 + c;
-    const double* xb = xs + lp * 3;
-    // upper half: own row, contiguous slot pairs
-    const double2* a = reinterpret_cast<const double2*>(UsT + (r >> 5) * (32LL * Sp)) + (r & 31);
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 4
-    for (int m = 0; m < (Sp >> 1); ++m) {
-      const double2 v = __ldg(a + 32 * m);
-      acc0 = fma(v.x, xb[offu[2 * m]], acc0);
-      acc1 = fma(v.y, xb[offu[2 * m + 1]], acc1);
-    }
-    // lower half, source-major: this thread reads row q = (p - d_e, cs) of the
-    // upper storage (cs = its component), slots 3e..3e+2 (32 consecutive
-    // source rows per warp: coalesced) and accumulates the contributions to
-    // the 3 target rows (p, c); partials of the 3 threads of a parent are
-    // combined through shared memory below.
-    const int cs = c;
-    double l0 = 0.0, l1 = 0.0, l2 = 0.0;
-#pragma unroll 2
-    for (int e = 0; e < npos; ++e) {
-      const int qs = ps + dsl[e], qt = pt + dtl[e];
-      if (qs < 0 || qs >= L || qt < 0 || qt >= L) continue;
-      const long long q = ((long long)qs * L + qt) * 3 + cs;
-      const double* base = UsT + (q >> 5) * (32LL * Sp) + (q & 31) * 2;
-      const int j0 = 3 * e;
-      const double u0 = __ldg(base + (long long)(j0 >> 1) * 64 + (j0 & 1));
-      const double u1 = __ldg(base + (long long)((j0 + 1) >> 1) * 64 + ((j0 + 1) & 1));
-      const double u2 = __ldg(base + (long long)((j0 + 2) >> 1) * 64 + ((j0 + 2) & 1));
-      const double xq = xb[offl[e] + cs];
-      l0 = fma(u0, xq, l0);
-      l1 = fma(u1, xq, l1);
-      l2 = fma(u2, xq, l2);
-    }
-    {  // d = 0, c > cs: stored in row (p, cs) at slot 3 npos + c
-      const long long q = ((long long)ps * L + pt) * 3 + cs;
-      const double* base = UsT + (q >> 5) * (32LL * Sp) + (q & 31) * 2;
-      const double xq = xb[(w * WC + w) * 3 + cs];
-      const int j1 = 3 * npos + 1, j2 = 3 * npos + 2;
-      if (cs < 1) l1 = fma(__ldg(base + (long long)(j1 >> 1) * 64 + (j1 & 1)), xq, l1);
-      if (cs < 2) l2 = fma(__ldg(base + (long long)(j2 >> 1) * 64 + (j2 & 1)), xq, l2);
-    }
-    lpart[tid * 3 + 0] = l0;
-    lpart[tid * 3 + 1] = l1;
-    lpart[tid * 3 + 2] = l2;
-    __syncthreads();
-    const double acc2 = lpart[(3 * lp + 0) * 3 + c] + lpart[(3 * lp + 1) * 3 + c] +
-                        lpart[(3 * lp + 2) * 3 + c];
-    const double acc3 = 0.0;
-    const double val = (acc0 + acc1) + (acc2 + acc3);
-    const long long yr = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
-    y[yr] = val;
-    d0 += xs[(w * WC + lp + w) * 3 + c] * val;
-    d1 += val * val;
-    __syncthreads();
-  }
-  *xy = d0;
-  *yy = d1;
-}
-
-// mode: 0 = CG (dot x.y -> alpha), 1 = power (x.y, y.y -> lam, ynorm), 2 = plain
-__global__ void __launch_bounds__(192) k_sym_apply(int L, int w, const double* __restrict__ UsT,
-                                                   const double* __restrict__ x,
-                                                   double* __restrict__ y, KState* st,
-                                                   double* part, int mode) {
-  extern __shared__ double dyn[];
-  __shared__ double sh[32];
-  __shared__ int tabs[4 * 512];
-  if (mode != 2 && st->done) return;
-  const int npos = 2 * w * w + 2 * w;
-  int* offu = tabs;
-  int* offl = tabs + 3 * npos + 4;
-  int* dsl = offl + npos;
-  int* dtl = dsl + npos;
-  build_offsets_sym(w, offu, offl, dsl, dtl);
-  __syncthreads();
-  double xy, yy;
-  tile_pass_sym(L, w, UsT, x, y, offu, offl, dsl, dtl, dyn,
-                dyn + (2 * w + 1) * (kTileP + 2 * w) * 3, &xy, &yy);
-  if (mode == 2) return;
-  xy = block_sum(xy, sh);
-  yy = block_sum(yy, sh);
-  if (threadIdx.x == 0) {
-    part[2 * blockIdx.x] = xy;
-    part[2 * blockIdx.x + 1] = yy;
-  }
-  if (last_block(&st->counter)) {
-    double a, b;
-    final_sum2(part, gridDim.x, &a, &b, sh);
-    if (threadIdx.x == 0) {
-      st->counter = 0;
-      if (mode == 0) {
-        st->pAp = a;
-        if (!(a > 0.0)) {
-          st->breakdown = st->it + 1;
-          st->done = 1;
-        } else {
-          st->alpha = st->rs / a;
-        }
-      } else {
-        st->lam = a;
-        st->ynorm = sqrt(b);
-        if (st->ynorm == 0.0) {
-          st->lam = 0.0;
-          st->done = 1;
-        }
-      }
-    }
-  }
-}
-
-
-// ---------------------------------------------------------------------------
 // Dual tiled SpMV: one pass over S B S serves two independent iterations
 // (the subband PCG "A" and the lambda-estimate iteration "B" of the same
 // level).  Each half has its own state, partials and reduction mode
@@ -1049,6 +842,8 @@ __device__ __forceinline__ void finish_reduction(KState* st, int mode, double a,
     }
   }
 }
+
+#include "gb_symspmv.cuh"
 
 __global__ void __launch_bounds__(192) k_dual_apply(int L, int w, const double* __restrict__ BsT,
                                                     const double* __restrict__ xa,
@@ -1778,11 +1573,40 @@ int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, dou
   k_scale_box_T<<<(int)(nblk < 148 * 8 ? nblk : 148 * 8), 256, smem, s>>>(L, nr, w, B, sv, BsT);
   return (int)cudaGetLastError();
 }
-static inline size_t sym_smem(int w) {
-  return ((size_t)(2 * w + 1) * (kTileP + 2 * w) * 3 + 192 * 3) * sizeof(double);
-}
 static inline bool use_sym(int layout, int L, int nr, int w) {
-  return layout == 1 && use_tiled(L, nr, w);
+  return layout == 1 && use_tiled(L, nr, w) && L % kSymTH == 0 &&
+         symb_smem(w, 2) <= 227 * 1024;
+}
+// one symmetric-band application y_v = (S B S) x_v for nv = 1 or 2 vectors
+// (phase 1 + phase 2; mode_v as finish_reduction, 2 = no reduction)
+static int sym_apply(int L, int w, const double* U, int nv, const double* x0, double* y0,
+                     KState* s0, double* p0, int m0, const double* x1, double* y1, KState* s1,
+                     double* p1, int m1, cudaStream_t s) {
+  const int nt = (int)symb_ntile(L);
+  const size_t sm = symb_smem(w, nv);
+  const long long R = (long long)L * L * 3;
+  const int gf = grid_for(R, 256, kRedBlocks);
+  if (nv == 2) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_symb_apply<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+      attr2 = true;
+    }
+    k_symb_apply<2><<<nt, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, x1, y1, s1);
+    k_symb_fix<2><<<gf, 256, 0, s>>>(L, w, x0, y0, s0, p0, m0, x1, y1, s1, p1, m1);
+  } else {
+    static bool attr1 = false;
+    if (!attr1) {
+      cudaFuncSetAttribute(k_symb_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+      attr1 = true;
+    }
+    k_symb_apply<1><<<nt, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, nullptr, nullptr, nullptr);
+    k_symb_fix<1><<<gf, 256, 0, s>>>(L, w, x0, y0, s0, p0, m0, nullptr, nullptr, nullptr,
+                                     nullptr, 2);
+  }
+  return (int)cudaGetLastError();
 }
 int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
                        double* p, double* Ap, int iters, void* st, double* part,
@@ -1796,7 +1620,7 @@ int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, doubl
   const bool tl = use_tiled(L, nr, w);
   const bool sy = use_sym(layout, L, nr, w);
   for (int i = 0; i < iters; ++i) {
-    if (sy) k_sym_apply<<<tiled_grid(L), 192, sym_smem(w), s>>>(L, w, BsT, p, Ap, k, part, 0);
+    if (sy) sym_apply(L, w, BsT, 1, p, Ap, k, part, 0, nullptr, nullptr, nullptr, nullptr, 2, s);
     else if (tl) k_tcg_spmv_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, p, Ap, k, part);
     else if (nr == 3) k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
     else k_tcg_spmv<1><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
@@ -1817,7 +1641,7 @@ int gbk_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, doub
   const bool tl = use_tiled(L, nr, w);
   const bool sy = use_sym(layout, L, nr, w);
   for (int i = 0; i < iters; ++i) {
-    if (sy) k_sym_apply<<<tiled_grid(L), 192, sym_smem(w), s>>>(L, w, BsT, x, y, k, part, 1);
+    if (sy) sym_apply(L, w, BsT, 1, x, y, k, part, 1, nullptr, nullptr, nullptr, nullptr, 2, s);
     else if (tl) k_tpow_apply_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, x, y, k, part);
     else if (nr == 3) k_tpow_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
     else k_tpow_apply<1><<<gs, 256, sm, s>>>(L, w, BsT, x, y, k, part);
@@ -1831,7 +1655,7 @@ int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, dou
   const int gs = row_grid((long long)L * L * nr);
   const size_t sm = off_smem(nr, w);
   if (use_sym(layout, L, nr, w))
-    k_sym_apply<<<tiled_grid(L), 192, sym_smem(w), s>>>(L, w, BsT, x, y, nullptr, nullptr, 2);
+    sym_apply(L, w, BsT, 1, x, y, nullptr, nullptr, 2, nullptr, nullptr, nullptr, nullptr, 2, s);
   else if (use_tiled(L, nr, w)) k_tbox_apply_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, x, y);
   else if (nr == 3) k_tbox_apply<3><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
   else k_tbox_apply<1><<<gs, 256, sm, s>>>(L, w, BsT, x, y);
@@ -1877,7 +1701,7 @@ int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, doub
   const bool sy = use_sym(layout, L, 3, w);
   for (int i = 0; i < iters; ++i) {
     if (sy)
-      k_sym_apply<<<tiled_grid(L), 192, sym_smem(w), s>>>(L, w, BsT, p, Ap, k, part, 0);
+      sym_apply(L, w, BsT, 1, p, Ap, k, part, 0, nullptr, nullptr, nullptr, nullptr, 2, s);
     else if (use_tiled(L, 3, w))
       k_tcg_spmv_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, p, Ap, k, part);
     else
@@ -2041,7 +1865,7 @@ int gbk_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r,
   int chunk = 8;
   for (;;) {
     int e = gbk_tcg_iterations(L, nr, w, BsT, x, r, p, Ap, chunk, st, part, s, layout);
-    *launches += 3LL * chunk;
+    *launches += (use_sym(layout, L, nr, w) ? 4LL : 3LL) * chunk;
     if (e) return e;
     e = read_state(st, h, s);
     if (e) return e;
@@ -2057,7 +1881,7 @@ int gbk_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x
   int chunk = 8;
   for (;;) {
     int e = gbk_bjcg_iterations(L, w, BsT, inv, x, r, p, Ap, z, chunk, st, part, s, layout);
-    *launches += 3LL * chunk;
+    *launches += (use_sym(layout, L, 3, w) ? 4LL : 3LL) * chunk;
     if (e) return e;
     e = read_state(st, h, s);
     if (e) return e;
@@ -2073,7 +1897,7 @@ int gbk_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y
   int chunk = 8;
   for (;;) {
     int e = gbk_tpow_iterations(L, nr, w, BsT, x, y, tol, chunk, st, part, s, layout);
-    *launches += 3LL * chunk;
+    *launches += (use_sym(layout, L, nr, w) ? 4LL : 3LL) * chunk;
     if (e) return e;
     e = read_state(st, h, s);
     if (e) return e;
@@ -2082,15 +1906,15 @@ int gbk_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y
   }
 }
 
-size_t gbk_boxsym_elems(int L, int w) {
-  const long long R = (long long)L * L * 3;
-  return (size_t)((R + 31) / 32) * 32 * sym_pad(w);
+size_t gbk_boxsym_elems(int L, int w) { return (size_t)L * L * symb_ns(w); }
+size_t gbk_sym_overflow_elems(int L, int w) {
+  return L % kSymTW == 0 && L % kSymTH == 0 ? (size_t)symb_ntile(L) * symb_region(w) : 0;
 }
-int gbk_sym_supported(int L, int nr, int w) { return use_tiled(L, nr, w) ? 1 : 0; }
+int gbk_sym_supported(int L, int nr, int w) { return use_sym(1, L, nr, w) ? 1 : 0; }
 int gbk_scale_box_symT(int L, int w, const double* B, const double* sv, double* UsT,
                        cudaStream_t s) {
   const long long total = (long long)gbk_boxsym_elems(L, w);
-  k_scale_box_symT<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, w, B, sv, UsT);
+  k_scale_box_symb<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, w, B, sv, UsT);
   return (int)cudaGetLastError();
 }
 
@@ -2160,6 +1984,9 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
 
 static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, int mb,
                        cudaStream_t s) {
+  if (e->layout == 1)
+    return sym_apply(e->L, e->w, e->BsT, 2, e->pa, e->apa, (KState*)e->sta, e->parta, 0, xb, yb,
+                     (KState*)e->stb, e->partb, mb, s);
   const int W2 = 2 * e->w + 1;
   const size_t smem = ((size_t)(W2 * W2 * 3 + 2) / 2 + 1) * sizeof(double) +
                       2 * (size_t)W2 * (kTileP + 2 * e->w) * 3 * sizeof(double);
@@ -2178,12 +2005,24 @@ static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, in
 // shared-memory footprint than the dual kernel, same arithmetic)
 static int launch_single(const gb_level_engine_args* e, const double* x, double* y, void* st,
                          double* part, int mode, cudaStream_t s) {
+  if (e->layout == 1)
+    return sym_apply(e->L, e->w, e->BsT, 1, x, y, (KState*)st, part, mode, nullptr, nullptr,
+                     nullptr, nullptr, 2, s);
   if (mode == 0)
     k_tcg_spmv_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y,
                                                                       (KState*)st, part);
   else
     k_tpow_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x,
                                                                         y, (KState*)st, part);
+  return (int)cudaGetLastError();
+}
+
+static int launch_plain(const gb_level_engine_args* e, const double* x, double* y,
+                        cudaStream_t s) {
+  if (e->layout == 1)
+    return sym_apply(e->L, e->w, e->BsT, 1, x, y, nullptr, nullptr, 2, nullptr, nullptr, nullptr,
+                     nullptr, 2, s);
+  k_tbox_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y);
   return (int)cudaGetLastError();
 }
 
@@ -2206,6 +2045,7 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
   KState* hb = (KState*)e->hstb;
   int err;
   int chunk = 8;
+  const long long spl = e->layout == 1 ? 2 : 1;  // launches per S B S pass
   // --- power iteration (B) paired with the PCG (A) -----------------------
   for (;;) {
     const bool a_live = !ha->done;
@@ -2219,7 +2059,7 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
       k_pow_step<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, e->tol, kb, e->partb);
       k_pow_scale<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, kb);
     }
-    *launches += 5LL * chunk;
+    *launches += (spl + 2 + (a_live ? 2 : 0)) * chunk;
     if ((err = (int)cudaGetLastError())) return err;
     if ((err = read_state(e->sta, ha, s))) return err;
     if ((err = read_state(e->stb, hb, s))) return err;
@@ -2272,7 +2112,7 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
           k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cr, e->cp, kb);
         }
       }
-      *launches += 5LL * chunk;
+      *launches += (spl + 2 + (a_live ? 2 : 0)) * chunk;
       if ((err = (int)cudaGetLastError())) return err;
       if ((err = read_state(e->sta, ha, s))) return err;
       if ((err = read_state(e->stb, hb, s))) return err;
@@ -2289,10 +2129,9 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
     k_dot2<<<gv, 256, 0, s>>>(npad, e->cx, e->cx, nullptr, e->dots, kb, e->partb);
     k_scale_by_norm<<<grid_for(npad, 256, 148 * 16), 256, 0, s>>>(npad, e->cx, e->dots, 0, nxt,
                                                                   nullptr);
-    k_tbox_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, nxt,
-                                                                      e->ax);
+    if ((err = launch_plain(e, nxt, e->ax, s))) return err;
     k_dot2<<<gv, 256, 0, s>>>(npad, nxt, e->ax, nullptr, e->dots + 2, kb, e->partb);
-    *launches += 4;
+    *launches += 3 + spl;
     e->calls += 1;
     if ((err = gbk_sync_read(e->dots, e->hdots, 4 * sizeof(double), s))) return err;
     e->n_outer = outer + 1;
@@ -2316,7 +2155,7 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
       if ((err = launch_single(e, e->pa, e->apa, e->sta, e->parta, 0, s))) return err;
       post_a(e, s);
     }
-    *launches += 3LL * chunk;
+    *launches += (spl + 2) * chunk;
     if ((err = (int)cudaGetLastError())) return err;
     if ((err = read_state(e->sta, ha, s))) return err;
     chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;

@@ -1,0 +1,295 @@
+// Symmetric band SpMV (v6) for the tiled Krylov levels (nr = 3, L % 64 == 0).
+//
+// S B S is symmetric, so only its upper half is streamed from HBM: for every
+// parent p the 3x3 blocks U_e[c][c'] = (S B S)[(p,c), (p+d_e,c')] of the
+// npos = 2w^2 + 2w positive offsets d_e (lexicographic: (0,1..w), then
+// ds = 1..w, dt = -w..w) plus the full 3x3 diagonal block.  Layout: 32
+// consecutive parents per block, slot pairs innermost across the 32 lanes
+// (double2 per lane), NS = 9 npos + 10 slots per parent (diagonal block
+// padded to 10):
+//
+//     U[((p >> 5) * NS/2 + m/2) * 64 + (p & 31) * 2 + (m & 1)],  m = 9e + 3c + c'.
+//
+// One thread per parent reads its own slots once and applies them twice:
+// gather  y(p,c)      += U_e[c][c'] x(p+d_e, c')      (upper half)
+// scatter y(p+d_e,c') += U_e[c][c'] x(p, c)           (lower half = U^T)
+// The scatter goes to per-warp private accumulators in shared memory (for a
+// fixed e the targets of a warp are distinct, e advances in program order with
+// a __syncwarp: deterministic); a CTA owns a tile of kSymTH grid rows x 64
+// parent columns.  Phase 1 combines the warps' accumulators in a fixed order,
+// writes the tile's own rows of y (partial) and the spill-over region (rows
+// below, columns left/right) to an overflow area at the tail of y.  Phase 2
+// adds the neighbours' spill-over in a fixed order and does the CG / power
+// reductions.  DRAM moves half the matrix bytes of the full box, every run is
+// bitwise reproducible.
+#pragma once
+
+constexpr int kSymTH = 4;    // grid rows per tile
+constexpr int kSymTW = 64;   // parent columns per tile (two warps)
+constexpr int kSymThreads = 2 * kSymTH * 32;
+
+__host__ __device__ __forceinline__ int symb_npos(int w) { return 2 * w * w + 2 * w; }
+__host__ __device__ __forceinline__ int symb_ns(int w) { return 9 * symb_npos(w) + 10; }
+// spill region of a tile: rows [0, TH + w) x columns [-w, 64 + w) x 3
+__host__ __device__ __forceinline__ int symb_region(int w) {
+  return (kSymTH + w) * (kSymTW + 2 * w) * 3;
+}
+__host__ __device__ __forceinline__ long long symb_ntile(int L) {
+  return (long long)(L / kSymTH) * (L / kSymTW);
+}
+__host__ __device__ __forceinline__ void symb_offset(int w, int e, int* ds, int* dt) {
+  if (e < w) {
+    *ds = 0;
+    *dt = e + 1;
+  } else {
+    const int f = e - w;
+    *ds = 1 + f / (2 * w + 1);
+    *dt = f % (2 * w + 1) - w;
+  }
+}
+
+// (S B S) upper blocks from the unscaled box, entry by entry the reference's
+// materialized congruence (x * s_i) * s_j (gamblet_fast.py:136)
+__global__ void k_scale_box_symb(int L, int w, const double* __restrict__ B,
+                                 const double* __restrict__ s, double* __restrict__ U) {
+  const int S = (2 * w + 1) * (2 * w + 1) * 3, NS = symb_ns(w), npos = symb_npos(w);
+  const long long total = (long long)L * L * NS;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long blk = e / (32LL * NS);
+    const int rem = (int)(e - blk * 32LL * NS);
+    const int m = ((rem >> 6) << 1) | (rem & 1);
+    const long long p = blk * 32 + ((rem >> 1) & 31);
+    const int ps = (int)(p / L), pt = (int)(p % L);
+    double v = 0.0;
+    if (m < 9 * npos) {
+      const int eo = m / 9, c = (m % 9) / 3, cp = m % 3;
+      int ds, dt;
+      symb_offset(w, eo, &ds, &dt);
+      const int qs = ps + ds, qt = pt + dt;
+      if (qs < L && qt >= 0 && qt < L) {
+        const long long r = p * 3 + c;
+        v = B[r * S + slot_of(w, 3, ds, dt, cp)] * s[r] * s[((long long)qs * L + qt) * 3 + cp];
+      }
+    } else if (m < 9 * npos + 9) {
+      const int c = (m - 9 * npos) / 3, cp = (m - 9 * npos) % 3;
+      const long long r = p * 3 + c;
+      v = B[r * S + slot_of(w, 3, 0, 0, cp)] * s[r] * s[p * 3 + cp];
+    }
+    U[e] = v;
+  }
+}
+
+// Phase 1: y_own (partial) and the tile's spill-over, for NV vectors sharing
+// one pass over U.  Vectors are zero-halo padded ((L+2w)^2 x 3); the spill
+// area of y_v starts at y_v + (L+2w)^2 * 3.
+template <int NV>
+__global__ void __launch_bounds__(kSymThreads) k_symb_apply(
+    int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
+    double* __restrict__ y0, const KState* s0, const double* __restrict__ x1,
+    double* __restrict__ y1, const KState* s1) {
+  extern __shared__ double dyn[];
+  const bool live0 = !(s0 && s0->done);
+  const bool live1 = NV == 2 && !(s1 && s1->done);
+  if (!live0 && !live1) return;
+  const int npos = symb_npos(w), NS2 = symb_ns(w) >> 1;
+  const int WC = kSymTW + 2 * w, Lpad = L + 2 * w;
+  const int XW = (kSymTH + w) * WC * 3;            // x window doubles
+  const int AC = 32 + 2 * w, AREG = (w + 1) * AC * 3;  // per-warp accumulator
+  int* xoff = reinterpret_cast<int*>(dyn);
+  int* aoff = xoff + npos;
+  double* xs = dyn + ((2 * npos + 1) >> 1) + 1;
+  double* acc = xs + NV * XW;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tpr = L / kSymTW;
+  const long long t = blockIdx.x;
+  const int I = (int)(t / tpr), J = (int)(t % tpr);
+  const int ps0 = I * kSymTH, pt0 = J * kSymTW;
+  for (int e = tid; e < npos; e += blockDim.x) {
+    int ds, dt;
+    symb_offset(w, e, &ds, &dt);
+    xoff[e] = (ds * WC + dt) * 3;
+    aoff[e] = (ds * AC + dt) * 3;
+  }
+  // stage x windows: the tile's own rows and the w rows below (padded rows
+  // ps0 + w .. ps0 + TH + 2w - 1), padded columns pt0 .. pt0 + 64 + 2w - 1
+  for (int e = tid; e < XW; e += blockDim.x) {
+    const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
+    const long long gi = ((long long)(ps0 + w + wr) * Lpad + pt0) * 3 + rem;
+    xs[e] = x0[gi];
+    if (NV == 2) xs[XW + e] = x1[gi];
+  }
+  for (int e = tid; e < NV * 2 * kSymTH * AREG; e += blockDim.x) acc[e] = 0.0;
+  __syncthreads();
+  const int h = warp >> 1, j = (warp & 1) * 32 + lane;
+  const long long p = (long long)(ps0 + h) * L + pt0 + j;
+  const double2* up = reinterpret_cast<const double2*>(U) + (p >> 5) * (32LL * NS2) + lane;
+  const int xo = (h * WC + (j + w)) * 3;        // own position in the window
+  const int ao = (lane + w) * 3;                // own position in the warp accumulator
+  double xa[NV][3], g[NV][3];
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      xa[v][c] = xs[v * XW + xo + c];
+      g[v][c] = 0.0;
+    }
+  double* aw = acc + warp * AREG;
+  for (int e = 0; e < npos; e += 2) {
+    double u[18];
+    const double2* q = up + (long long)(9 * e / 2) * 32;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const double2 d = __ldg(q + 32 * k);
+      u[2 * k] = d.x;
+      u[2 * k + 1] = d.y;
+    }
+#pragma unroll
+    for (int ee = 0; ee < 2; ++ee) {
+      const double* ub = u + 9 * ee;
+      const int xe = xo + xoff[e + ee], ae = ao + aoff[e + ee];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double* xw = xs + v * XW + xe;
+        const double n0 = xw[0], n1 = xw[1], n2 = xw[2];
+        g[v][0] = fma(ub[0], n0, fma(ub[1], n1, fma(ub[2], n2, g[v][0])));
+        g[v][1] = fma(ub[3], n0, fma(ub[4], n1, fma(ub[5], n2, g[v][1])));
+        g[v][2] = fma(ub[6], n0, fma(ub[7], n1, fma(ub[8], n2, g[v][2])));
+        double* a = aw + v * 2 * kSymTH * AREG + ae;
+        a[0] += fma(ub[0], xa[v][0], fma(ub[3], xa[v][1], ub[6] * xa[v][2]));
+        a[1] += fma(ub[1], xa[v][0], fma(ub[4], xa[v][1], ub[7] * xa[v][2]));
+        a[2] += fma(ub[2], xa[v][0], fma(ub[5], xa[v][1], ub[8] * xa[v][2]));
+      }
+      __syncwarp();
+    }
+  }
+  {  // diagonal block
+    double u[10];
+    const double2* q = up + (long long)(9 * npos / 2) * 32;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double2 d = __ldg(q + 32 * k);
+      u[2 * k] = d.x;
+      u[2 * k + 1] = d.y;
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double* a = aw + v * 2 * kSymTH * AREG + ao;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        a[c] += fma(u[3 * c], xa[v][0], fma(u[3 * c + 1], xa[v][1],
+                                           fma(u[3 * c + 2], xa[v][2], g[v][c])));
+    }
+  }
+  __syncthreads();
+  // combine the warps' accumulators over the tile region in a fixed order
+  const int RW = WC * 3, RG = symb_region(w);
+  const long long npad = (long long)Lpad * Lpad * 3;
+  for (int idx = tid; idx < RG; idx += blockDim.x) {
+    const int rr = idx / RW, rem = idx - rr * RW;
+    const int cc = rem / 3 - w, c = rem % 3;
+    const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (v == 0 ? !live0 : !live1) continue;
+      const double* av = acc + v * 2 * kSymTH * AREG;
+      double s = 0.0;
+      for (int hh = h0; hh <= h1; ++hh) {
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int lc = cc - half * 32 + w;
+          if (lc >= 0 && lc < AC) s += av[(2 * hh + half) * AREG + ((rr - hh) * AC + lc) * 3 + c];
+        }
+      }
+      double* y = v == 0 ? y0 : y1;
+      if (rr < kSymTH && cc >= 0 && cc < kSymTW)
+        y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = s;
+      else
+        y[npad + t * RG + idx] = s;
+    }
+  }
+}
+
+// Phase 2: y_own += the neighbours' spill-over (fixed order: tile rows above
+// by distance, then columns left, same, right), then the reductions of
+// finish_reduction (mode 0: x.y -> alpha, 1: x.y, y.y -> lam, ynorm, 2: none).
+template <int NV>
+__global__ void __launch_bounds__(256) k_symb_fix(int L, int w, const double* __restrict__ x0,
+                                                  double* __restrict__ y0, KState* s0,
+                                                  double* part0, int mode0,
+                                                  const double* __restrict__ x1,
+                                                  double* __restrict__ y1, KState* s1,
+                                                  double* part1, int mode1) {
+  __shared__ double sh[32];
+  const bool live0 = !(s0 && s0->done);
+  const bool live1 = NV == 2 && !(s1 && s1->done);
+  if (!live0 && !live1) return;
+  const int Lpad = L + 2 * w, WC = kSymTW + 2 * w, RG = symb_region(w), tpr = L / kSymTW;
+  const int KI = (w + kSymTH - 1) / kSymTH;
+  const long long npad = (long long)Lpad * Lpad * 3, R = (long long)L * L * 3;
+  double d[NV][2];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) d[v][0] = d[v][1] = 0.0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long pp = r / 3;
+    const int c = (int)(r - pp * 3);
+    const int ps = (int)(pp / L), pt = (int)(pp % L);
+    const int I = ps / kSymTH, h = ps - I * kSymTH, J = pt / kSymTW, j = pt - J * kSymTW;
+    const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (v == 0 ? !live0 : !live1) continue;
+      double* y = v == 0 ? y0 : y1;
+      const double* ov = y + npad;
+      double s = y[yi];
+      for (int dI = 0; dI <= KI; ++dI) {
+        const int Ip = I - dI, rr = h + dI * kSymTH;
+        if (Ip < 0 || rr >= kSymTH + w) break;
+        for (int dJ = -1; dJ <= 1; ++dJ) {
+          if (dI == 0 && dJ == 0) continue;
+          const int Jp = J + dJ, cc = j - dJ * kSymTW;
+          if (Jp < 0 || Jp >= tpr || cc < -w || cc >= kSymTW + w) continue;
+          s += ov[((long long)Ip * tpr + Jp) * RG + (rr * WC + cc + w) * 3 + c];
+        }
+      }
+      y[yi] = s;
+      const double* x = v == 0 ? x0 : x1;
+      d[v][0] = fma(x[yi], s, d[v][0]);
+      d[v][1] = fma(s, s, d[v][1]);
+    }
+  }
+  const bool red0 = live0 && mode0 != 2, red1 = NV == 2 && live1 && mode1 != 2;
+  if (!red0 && !red1) return;
+  KState* cs = red0 ? s0 : s1;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const bool rv = v == 0 ? red0 : red1;
+    if (!rv) continue;
+    const double a = block_sum(d[v][0], sh);
+    const double b = block_sum(d[v][1], sh);
+    double* part = v == 0 ? part0 : part1;
+    if (threadIdx.x == 0) {
+      part[2 * blockIdx.x] = a;
+      part[2 * blockIdx.x + 1] = b;
+    }
+  }
+  if (last_block(&cs->counter)) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const bool rv = v == 0 ? red0 : red1;
+      if (!rv) continue;
+      double a, b;
+      final_sum2(v == 0 ? part0 : part1, gridDim.x, &a, &b, sh);
+      if (threadIdx.x == 0) finish_reduction(v == 0 ? s0 : s1, v == 0 ? mode0 : mode1, a, b);
+    }
+    if (threadIdx.x == 0) cs->counter = 0;
+  }
+}
+
+static inline size_t symb_smem(int w, int nv) {
+  const int npos = symb_npos(w), WC = kSymTW + 2 * w;
+  return (size_t)(((2 * npos + 1) >> 1) + 1) * 8 +
+         (size_t)nv * (kSymTH + w) * WC * 3 * 8 +
+         (size_t)nv * 2 * kSymTH * (w + 1) * (32 + 2 * w) * 3 * 8;
+}

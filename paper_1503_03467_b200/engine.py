@@ -20,5 +20,5 @@ class LevelEngineArgs(ctypes.Structure):
         ("lam_min", _D), ("lam_max", _D), ("calls", ctypes.c_int64),
         ("power_its", ctypes.c_int), ("n_outer", ctypes.c_int), ("breakdown", ctypes.c_int),
         ("inner_pcg", ctypes.c_int), ("inner_its", ctypes.c_int * 64),
-        ("cz", _P),
+        ("cz", _P), ("layout", ctypes.c_int),
     ]

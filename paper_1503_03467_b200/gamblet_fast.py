@@ -373,6 +373,10 @@ class _POp:
         self.npad = self.Lpad * self.Lpad * self.nr
         self.layout = 1 if (SYMMETRIC_SPMV and
                             nat.query("gb_sym_supported", self.L, self.nr, self.w)) else 0
+        # output vectors of the symmetric band SpMV carry the tiles' spill-over
+        # area after the padded vector (gamblets_b200.h, gb_sym_overflow_elems)
+        self.vtail = (nat.query("gb_sym_overflow_elems", self.L, self.w)
+                      if self.layout == 1 else 0)
         if self.layout == 1:
             self.BsT = dv.empty(nat.query("gb_boxsym_elems", self.L, self.w))
             nat.call("gb_scale_box_symT", self.L, self.w, dv.ptr(box.vals), dv.ptr(s),
@@ -396,9 +400,8 @@ class _POp:
     def stored_slots(self):
         """Matrix slots per row the SpMV streams from HBM (upper half only in
         the symmetric layout)."""
-        if self.layout == 1:
-            su = 3 * (2 * self.w * self.w + 2 * self.w) + 3
-            return su + (su & 1)
+        if self.layout == 1:  # 9 npos + 10 slots per parent of 3 rows
+            return (9 * (2 * self.w * self.w + 2 * self.w) + 10) / 3
         return self.slots + (self.slots & 1)
 
     @property
@@ -406,7 +409,9 @@ class _POp:
         return 8 * self.n * self.stored_slots + 3 * 8 * self.npad
 
     def vec(self):
-        return dv.zeros(self.npad)
+        """A zero padded vector (plus the spill-over tail in the symmetric
+        layout, so any vector can be an SpMV output)."""
+        return dv.zeros(self.npad + self.vtail)
 
     def pad(self, x, scale=None):
         out = self.vec()
@@ -576,7 +581,7 @@ PAIRED_ENGINE = __import__("os").environ.get("GB_PAIRED", "1") == "1"
 
 
 def _engine_ok(op):
-    return (op.nr == 3 and op.layout == 0 and op.L % 64 == 0 and op.w <= 8)
+    return (op.nr == 3 and op.L % 64 == 0 and op.w <= 8)
 
 
 def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
@@ -618,7 +623,7 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
         partb=dv.ptr(kb.part), hstb=kb.host.data_ptr(), dots=dv.ptr(dots),
         hdots=kb.hdots.data_ptr(), tol=tol, inner_tol=max(1e-12, 1e-3 * tol),
         inner_max_iter=min(max(200, 2 * n), MAX_ITER_CAP),
-        inner_pcg=int(SPECTRAL_INNER == "pcg"), cz=dv.ptr(cz))
+        inner_pcg=int(SPECTRAL_INNER == "pcg"), cz=dv.ptr(cz), layout=op.layout)
     nat.call("gb_level_engine", nat.ctypes.byref(args), st)
     if args.breakdown > 0:
         raise NumericalError(f"CG breakdown at iteration {args.breakdown}: p^T A p <= 0 "
@@ -639,10 +644,10 @@ SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
 # safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
 # it; converging solves here need < 2000)
 SPECTRAL_PRIORITY = int(__import__("os").environ.get("GB_SPECTRAL_PRIORITY", "-1"))
-# symmetric upper-half Krylov copy (opt-in): halves HBM bytes but the lower
-# half is re-read through L2 with too many misses -- measured 0.32-0.39 ms vs
-# 0.24 ms for the full box at q=10, so the full layout is the default
-SYMMETRIC_SPMV = __import__("os").environ.get("GB_SYM_SPMV", "0") == "1"
+# symmetric band Krylov copy (csrc/gb_symspmv.cuh): only the upper 3x3 blocks
+# of S B S are streamed, the lower half is applied from the same registers
+# (scatter through shared memory) -- half the HBM bytes of the full box
+SYMMETRIC_SPMV = __import__("os").environ.get("GB_SYM_SPMV", "1") == "1"
 MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
 # inner solver of the inverse iteration for lambda_min: "pcg" (block-Jacobi,
 # the subband preconditioner) or "cg" (the reference's unpreconditioned CG).
