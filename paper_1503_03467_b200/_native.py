@@ -119,7 +119,9 @@ def load(path=None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    import os
+    # GB_LIB: an alternative build of the same library (tools/build_variant.sh)
+    p = Path(path) if path else Path(os.environ.get("GB_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"{p} is missing: build the CUDA library first "

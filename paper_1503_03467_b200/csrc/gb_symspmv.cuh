@@ -24,7 +24,10 @@
 // bitwise reproducible.
 #pragma once
 
-constexpr int kSymTH = 4;    // grid rows per tile
+#ifndef GB_SYM_TH
+#define GB_SYM_TH 4
+#endif
+constexpr int kSymTH = GB_SYM_TH;  // grid rows per tile
 constexpr int kSymTW = 64;   // parent columns per tile (two warps)
 constexpr int kSymThreads = 2 * kSymTH * 32;
 
@@ -84,7 +87,7 @@ __global__ void k_scale_box_symb(int L, int w, const double* __restrict__ B,
 // one pass over U.  Vectors are zero-halo padded ((L+2w)^2 x 3); the spill
 // area of y_v starts at y_v + (L+2w)^2 * 3.
 template <int NV>
-__global__ void __launch_bounds__(kSymThreads) k_symb_apply(
+__global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
     int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
     double* __restrict__ y0, const KState* s0, const double* __restrict__ x1,
     double* __restrict__ y1, const KState* s1) {
@@ -135,18 +138,27 @@ __global__ void __launch_bounds__(kSymThreads) k_symb_apply(
       g[v][c] = 0.0;
     }
   double* aw = acc + warp * AREG;
-  for (int e = 0; e < npos; e += 2) {
-    double u[18];
-    const double2* q = up + (long long)(9 * e / 2) * 32;
+  // software pipeline: the slots of offset pair e + 2 are in flight while
+  // pair e is applied; the diagonal block is loaded up front
+  double2 cur[9], nxt[9], dg[5];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      const double2 d = __ldg(q + 32 * k);
-      u[2 * k] = d.x;
-      u[2 * k + 1] = d.y;
+  for (int k = 0; k < 5; ++k) dg[k] = __ldg(up + (long long)(9 * npos / 2 + k) * 32);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) cur[k] = __ldg(up + 32 * k);
+  for (int e = 0; e < npos; e += 2) {
+    if (e + 2 < npos) {
+      const double2* q = up + (long long)(9 * (e + 2) / 2) * 32;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) nxt[k] = __ldg(q + 32 * k);
     }
 #pragma unroll
     for (int ee = 0; ee < 2; ++ee) {
-      const double* ub = u + 9 * ee;
+      double ub[9];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        const int m = 9 * ee + i;
+        ub[i] = (m & 1) ? cur[m >> 1].y : cur[m >> 1].x;
+      }
       const int xe = xo + xoff[e + ee], ae = ao + aoff[e + ee];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -162,23 +174,21 @@ __global__ void __launch_bounds__(kSymThreads) k_symb_apply(
       }
       __syncwarp();
     }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cur[k] = nxt[k];
   }
   {  // diagonal block
-    double u[10];
-    const double2* q = up + (long long)(9 * npos / 2) * 32;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const double2 d = __ldg(q + 32 * k);
-      u[2 * k] = d.x;
-      u[2 * k + 1] = d.y;
-    }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double* a = aw + v * 2 * kSymTH * AREG + ao;
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        a[c] += fma(u[3 * c], xa[v][0], fma(u[3 * c + 1], xa[v][1],
-                                           fma(u[3 * c + 2], xa[v][2], g[v][c])));
+      for (int c = 0; c < 3; ++c) {
+        const int m0 = 3 * c;
+        const double d0 = (m0 & 1) ? dg[m0 >> 1].y : dg[m0 >> 1].x;
+        const double d1 = ((m0 + 1) & 1) ? dg[(m0 + 1) >> 1].y : dg[(m0 + 1) >> 1].x;
+        const double d2 = ((m0 + 2) & 1) ? dg[(m0 + 2) >> 1].y : dg[(m0 + 2) >> 1].x;
+        a[c] += fma(d0, xa[v][0], fma(d1, xa[v][1], fma(d2, xa[v][2], g[v][c])));
+      }
     }
   }
   __syncthreads();
