@@ -261,6 +261,9 @@ def run_ours(args, rank, world, local_rank):
             levels, parts, counter = step_device()
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()
+            # a step is one complete solve: the host waits for it (as a caller
+            # reading its results would) before the next one is enqueued
+            torch.cuda.synchronize()
         ev1.record()
         torch.cuda.synchronize()
     barrier()

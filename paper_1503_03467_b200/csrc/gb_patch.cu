@@ -15,6 +15,9 @@
 #include "gb_common.cuh"
 #include "gb_kernels.h"
 #include "gb_tiled_chol.cuh"
+#ifdef GB_PATCH_PROF
+#include <cstdio>
+#endif
 
 namespace gb {
 
@@ -270,6 +273,12 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
   TileSmem S = carve(sm, Tmax, nw);
   const int SB = box_slots(wB, 3), SG = box_slots(wG, 1), SD = box_slots(rho, 3);
   const long long P = (long long)Lp * Lp;
+#ifdef GB_PATCH_PROF
+  long long tp[5] = {0, 0, 0, 0, 0}, tc = clock64(), tn;
+#define GB_TICK(k) do { __syncthreads(); tn = clock64(); tp[k] += tn - tc; tc = tn; } while (0)
+#else
+#define GB_TICK(k) do {} while (0)
+#endif
   for (long long i = blockIdx.x; i < P; i += gridDim.x) {
     const int si = (int)(i / Lp), ti = (int)(i % Lp);
     const int s0 = imax(0, si - rho), s1 = imin(Lp - 1, si + rho);
@@ -312,23 +321,50 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
       __syncthreads();
       continue;
     }
-    // gather (S B S)[chi, chi] lower tiles + RHS tile row
-    for (int e = threadIdx.x; e < nlt * 64; e += blockDim.x) {
-      const int t = e >> 6, w = e & 63;
-      const int ij = S.tij[t];
-      const int r = w >> 3, c = w & 7;
-      const int l1 = ((ij >> 8) << 3) + r, l2 = ((ij & 255) << 3) + c;
-      double v = 0.0;
-      if (l1 < m && l2 < m) {
-        const int p1 = S.ploc[l1 / 3 * 3], p2 = S.ploc[l2 / 3 * 3];
-        const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
-        if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
-          v = B[(long long)S.rowg[l1] * SB + slot_of(wB, 3, ds, dt, l2 % 3)] * S.sl[l1] *
-              S.sl[l2];
-      } else if (l1 == l2) {
-        v = 1.0;
+    GB_TICK(0);
+    // gather (S B S)[chi, chi] lower tiles + RHS tile row, 8 independent
+    // loads in flight per thread (the B rows are L2 hits shared by the
+    // neighbouring patches; the gather is latency-bound without the batching)
+    {
+      const int nel = nlt * 64, stride = blockDim.x;
+      for (int e0 = threadIdx.x; e0 < nel; e0 += 8 * stride) {
+        long long addr[8];
+        double sc1[8], sc2[8], v[8];
+        int dst[8], kind[8];  // kind: 0 zero, 1 load, 2 unit diagonal pad
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * stride;
+          kind[u] = 0;
+          dst[u] = -1;
+          addr[u] = 0;
+          sc1[u] = sc2[u] = 0.0;
+          if (e < nel) {
+            const int t = e >> 6, w = e & 63;
+            const int ij = S.tij[t];
+            const int r = w >> 3, c = w & 7;
+            const int l1 = ((ij >> 8) << 3) + r, l2 = ((ij & 255) << 3) + c;
+            dst[u] = t * 64 + eidx(r, c);
+            if (l1 < m && l2 < m) {
+              const int p1 = S.ploc[l1 / 3 * 3], p2 = S.ploc[l2 / 3 * 3];
+              const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
+              if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB) {
+                kind[u] = 1;
+                addr[u] = (long long)S.rowg[l1] * SB + slot_of(wB, 3, ds, dt, l2 % 3);
+                sc1[u] = S.sl[l1];
+                sc2[u] = S.sl[l2];
+              }
+            } else if (l1 == l2) {
+              kind[u] = 2;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = kind[u] == 1 ? __ldg(B + addr[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (dst[u] >= 0)
+            S.tl[dst[u]] = kind[u] == 1 ? v[u] * sc1[u] * sc2[u] : (kind[u] == 2 ? 1.0 : 0.0);
       }
-      S.tl[t * 64 + eidx(r, c)] = v;
     }
     for (int e = threadIdx.x; e < T * 64; e += blockDim.x) {
       const int jt = e >> 6, w = e & 63;
@@ -336,12 +372,15 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
       S.tl[(nlt + jt) * 64 + eidx(r, c)] = (r == 0) ? S.z[jt * 8 + c] : 0.0;
     }
     __syncthreads();
+    GB_TICK(1);
     if (!tiled_chol_fwd(S.tl, T, S.sl + 8 * Tmax, S.flag)) {
       if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
       __syncthreads();
       continue;
     }
+    GB_TICK(2);
     tiled_back_subst(S.tl, T, S.z, S.part);
+    GB_TICK(3);
     // D = s z and the row-tail trim of this column of D
     double mx = 0.0;
     for (int l = threadIdx.x; l < m; l += blockDim.x) {
@@ -362,7 +401,16 @@ __global__ void __launch_bounds__(256) k_correction_patches_v2(
       drow[e] = v;
     }
     __syncthreads();
+    GB_TICK(4);
   }
+#ifdef GB_PATCH_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 4)
+    printf("patch prof blk %d: tables %lld gather %lld factor %lld backsubst %lld out %lld"
+           " | blk0 factor: w0A %llu w1A %llu w2A %llu A+sync %llu trsm %llu\n",
+           blockIdx.x, tp[0], tp[1], tp[2], tp[3], tp[4], g_fprof[0], g_fprof[1], g_fprof[2],
+           g_fprof[3], g_fprof[4]);
+#endif
+#undef GB_TICK
 }
 
 __global__ void __launch_bounds__(128) k_mass_patches_v2(

@@ -23,112 +23,154 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
       : "d"(a), "d"(b));
 }
 
-// Factor the 8x8 diagonal tile (one warp, rows in lanes 0..7, registers and
-// shuffles), form L^-1 and store it OVER the tile: diagonal L tiles are never
-// DMMA operands, every later use (TRSM, back substitution) needs L_kk^-1.
-// `scratch` holds 8 doubles.  Returns false if a pivot is not positive.
-__device__ __forceinline__ bool warp_chol8_inv(double* t, double* scratch) {
+// Factor the 8x8 diagonal tile and form L^-1 over it, in registers: every
+// lane of the warp runs the same fully unrolled Cholesky-Crout and in-place
+// inversion (no shuffles on the serial pivot chain), lanes 0..7 write one row
+// each.  Diagonal L tiles are never DMMA operands; every later use (TRSM, back
+// substitution) needs L_kk^-1.  Returns false if a pivot is not positive.
+__device__ __forceinline__ bool warp_chol8_inv(double* t) {
   const int lane = threadIdx.x & 31;
-  const int r = lane & 7;
-  double v[8];
+  double a[8][8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) v[c] = (c <= r) ? t[eidx(r, c)] : 0.0;
-  double il_r = 0.0;  // 1 / L_rr, kept by lane r
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) a[r][c] = t[eidx(r, c)];
+  __syncwarp();
   bool ok = true;
+  double il[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const double d = __shfl_sync(0xffffffffu, v[j], j);
+    double d = a[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = fma(-a[j][k], a[j][k], d);
     ok = ok && (d > 0.0);
-    const double il = rsqrt(d);
-    if (r > j) v[j] *= il;
-    if (r == j) {
-      v[j] = d * il;
-      il_r = il;
+    const double inv = rsqrt(d);
+    il[j] = inv;
+    a[j][j] = d * inv;
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i) {
+      double v = a[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v = fma(-a[i][k], a[j][k], v);
+      a[i][j] = v * inv;
     }
+  }
+  // L^-1 in place, column by column left to right:
+  // X_jj = 1/L_jj, X_ij = -(sum_{j<=k<i} L_ik X_kj) / L_ii
 #pragma unroll
-    for (int c = j + 1; c < 8; ++c) {
-      const double lcj = __shfl_sync(0xffffffffu, v[j], c);
-      if (r > j && c <= r) v[c] = fma(-v[j], lcj, v[c]);
+  for (int j = 0; j < 8; ++j) {
+    a[j][j] = il[j];
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i) {
+      double acc = a[i][j] * a[j][j];
+#pragma unroll
+      for (int k = j + 1; k < i; ++k) acc = fma(a[i][k], a[k][j], acc);
+      a[i][j] = -acc * il[i];
     }
   }
-  if (!ok) return false;
-  if (lane < 8) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c <= r) t[eidx(r, c)] = v[c];
-    scratch[r] = il_r;  // diagonal of L^-1, read back below
-  }
+  for (int r = 0; r < 8; ++r)
+    if (lane == r) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) t[eidx(r, c)] = c <= r ? a[r][c] : 0.0;
+    }
   __syncwarp();
-  // L^-1, column r by lane r: x_i = -(sum_{r<=k<i} L_ik x_k) / L_ii, x_r = 1/L_rr
-  double x[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) acc = fma(t[eidx(i, k)], x[k], acc);
-    const double ii = scratch[i];
-    x[i] = (i > r) ? -acc * ii : ((i == r) ? ii : 0.0);
-  }
-  __syncwarp();
-  if (lane < 8) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) t[eidx(i, r)] = x[i];  // column r of L^-1 (upper = 0)
-  }
-  __syncwarp();
-  return true;
+  return ok;
 }
 
-// Left-looking tiled Cholesky + forward substitution of the RHS row.
-// tl: tile storage (diagonal tiles end up holding L_kk^-1), T: tiles per
-// dimension, scratch: 8 doubles, flag: shared int.  Warp 0 owns the diagonal tile of every step;
-// warps 1.. own the off-diagonal tiles (round robin), keep them in registers
-// across the update and the TRSM (two DMMAs with L_kk^-T).  Returns false
+// Left-looking tiled Cholesky + forward substitution of the RHS row, with a
+// one-column lookahead.  Invariant at the start of step kt: every tile
+// (it, kt), it >= kt, already holds the contributions of columns < kt-1.
+// Step kt: warp 0 adds column kt-1 to the diagonal tile and factors it
+// (L_kk^-1 in registers); meanwhile warps 1.. finish the rest of column kt
+// (one DMMA pair per tile) and pre-accumulate column kt+1 from columns
+// 0..kt-1 (the bulk of the flops, two independent accumulator chains per
+// tile).  Then all warps apply the TRSM L(it,kt) = C(it,kt) L_kk^-T (two
+// DMMAs with L_kk^-1).  The serial chain per step is one DMMA pair, the
+// register 8x8 factor and the TRSM.  tl: tile storage (diagonal tiles end up
+// holding L_kk^-1), T: tiles per dimension, flag: shared int.  Returns false
 // (CTA-uniform) when the matrix is not SPD.
-__device__ bool tiled_chol_fwd(double* tl, int T, double* scratch, int* flag) {
+#ifdef GB_PATCH_PROF
+__device__ unsigned long long g_fprof[8];
+#endif
+__device__ bool tiled_chol_fwd(double* tl, int T, double* /*scratch*/, int* flag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const int e0 = eidx(fr, 2 * fk), e1 = eidx(fr, 2 * fk + 1);
+  const int ea = eidx(fr, fk), eb = eidx(fr, 4 + fk);
   if (threadIdx.x == 0) *flag = 0;
   __syncthreads();
   for (int kt = 0; kt < T; ++kt) {
-    const double* bk = tl + tidx(kt, 0) * 64;
-    // (1) updates: C(it,kt) -= sum_{jt<kt} L(it,jt) L(kt,jt)^T
+#ifdef GB_PATCH_PROF
+    long long q0 = clock64();
+#endif
+    const double* lk1 = tl + tidx(kt, 0) * 64 + (kt - 1) * 64;  // L(kt, kt-1)
     if (warp == 0) {
       double* ct = tl + tidx(kt, kt) * 64;
-      double c0 = ct[e0], c1 = ct[e1];
-      for (int jt = 0; jt < kt; ++jt) {
-        const double* b = bk + jt * 64;
-        dmma_884(c0, c1, -b[eidx(fr, fk)], b[eidx(fr, fk)]);
-        dmma_884(c0, c1, -b[eidx(fr, 4 + fk)], b[eidx(fr, 4 + fk)]);
-      }
-      ct[e0] = c0;
-      ct[e1] = c1;
-      __syncwarp();
-      if (!warp_chol8_inv(ct, scratch) && lane == 0) *flag = 1;
-    } else {
-      for (int it = kt + warp; it <= T; it += nw - 1) {
-        double* ct = tl + tidx(it, kt) * 64;
+      if (kt > 0) {
         double c0 = ct[e0], c1 = ct[e1];
-        const double* ai = tl + tidx(it, 0) * 64;
-        for (int jt = 0; jt < kt; ++jt) {
-          const double* a = ai + jt * 64;
-          const double* b = bk + jt * 64;
-          dmma_884(c0, c1, -a[eidx(fr, fk)], b[eidx(fr, fk)]);
-          dmma_884(c0, c1, -a[eidx(fr, 4 + fk)], b[eidx(fr, 4 + fk)]);
-        }
+        dmma_884(c0, c1, -lk1[ea], lk1[ea]);
+        dmma_884(c0, c1, -lk1[eb], lk1[eb]);
         ct[e0] = c0;
         ct[e1] = c1;
+        __syncwarp();
+      }
+      if (!warp_chol8_inv(ct) && lane == 0) *flag = 1;
+    } else {
+      if (kt > 0) {  // finish column kt: C(it,kt) -= L(it,kt-1) L(kt,kt-1)^T
+        const double b0 = lk1[ea], b1 = lk1[eb];
+        for (int it = kt + warp; it <= T; it += nw - 1) {
+          double* ct = tl + tidx(it, kt) * 64;
+          const double* a = tl + tidx(it, kt - 1) * 64;
+          double c0 = ct[e0], c1 = ct[e1];
+          dmma_884(c0, c1, -a[ea], b0);
+          dmma_884(c0, c1, -a[eb], b1);
+          ct[e0] = c0;
+          ct[e1] = c1;
+        }
+      }
+      if (kt + 1 < T) {  // pre-accumulate column kt+1 from columns 0..kt-1
+        const double* bk = tl + tidx(kt + 1, 0) * 64;
+        for (int it = kt + warp; it <= T; it += nw - 1) {
+          double* ct = tl + tidx(it, kt + 1) * 64;
+          const double* ai = tl + tidx(it, 0) * 64;
+          double c0 = ct[e0], c1 = ct[e1], d0 = 0.0, d1 = 0.0;
+          int jt = 0;
+          for (; jt + 1 < kt; jt += 2) {
+            const double* a = ai + jt * 64;
+            const double* b = bk + jt * 64;
+            dmma_884(c0, c1, -a[ea], b[ea]);
+            dmma_884(d0, d1, -a[64 + ea], b[64 + ea]);
+            dmma_884(c0, c1, -a[eb], b[eb]);
+            dmma_884(d0, d1, -a[64 + eb], b[64 + eb]);
+          }
+          if (jt < kt) {
+            const double* a = ai + jt * 64;
+            const double* b = bk + jt * 64;
+            dmma_884(c0, c1, -a[ea], b[ea]);
+            dmma_884(c0, c1, -a[eb], b[eb]);
+          }
+          ct[e0] = c0 + d0;
+          ct[e1] = c1 + d1;
+        }
       }
     }
+#ifdef GB_PATCH_PROF
+    if (blockIdx.x == 0 && lane == 0 && warp < 3) atomicAdd(&g_fprof[warp], clock64() - q0);
+#endif
     __syncthreads();
+#ifdef GB_PATCH_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_fprof[3], clock64() - q0);
+    long long q1 = clock64();
+#endif
     if (*flag) return false;
-    // (2) TRSM: L(it,kt) = C(it,kt) L_kk^-T as a product with Linv^T (DMMA)
-    if (warp != 0) {
+    // TRSM: L(it,kt) = C(it,kt) L_kk^-T as a product with Linv^T (DMMA)
+    {
       const double* li = tl + tidx(kt, kt) * 64;  // L_kk^-1
-      const double bl0 = li[eidx(fr, fk)], bl1 = li[eidx(fr, 4 + fk)];
-      for (int it = kt + warp; it <= T; it += nw - 1) {
+      const double bl0 = li[ea], bl1 = li[eb];
+      for (int it = kt + 1 + warp; it <= T; it += nw) {
         double* ct = tl + tidx(it, kt) * 64;
-        const double a0 = ct[eidx(fr, fk)], a1 = ct[eidx(fr, 4 + fk)];
+        const double a0 = ct[ea], a1 = ct[eb];
         double d0 = 0.0, d1 = 0.0;
         dmma_884(d0, d1, a0, bl0);
         dmma_884(d0, d1, a1, bl1);
@@ -138,47 +180,49 @@ __device__ bool tiled_chol_fwd(double* tl, int T, double* scratch, int* flag) {
       }
     }
     __syncthreads();
+#ifdef GB_PATCH_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_fprof[4], clock64() - q1);
+#endif
   }
   return true;
 }
 
 // Back substitution L^T z = y with the L_kk^-1 held in the diagonal tiles;
-// y is row 0 of the RHS tiles, z (8T) written to `z`.  part: 8 * nwarps.
-__device__ void tiled_back_subst(const double* tl, int T, double* z, double* part) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < 8 * T; i += blockDim.x)
-    z[i] = tl[tidx(T, i >> 3) * 64 + eidx(0, i & 7)];
-  __syncthreads();
-  const int r = lane & 7, cg = lane >> 3;
-  for (int it = T - 1; it >= 0; --it) {
-    double acc = 0.0;
-    for (int jt = it + 1 + warp; jt < T; jt += nw) {
-      const double* t = tl + tidx(jt, it) * 64;
-      const double* zj = z + 8 * jt;
-      acc += t[eidx(2 * cg, r)] * zj[2 * cg] + t[eidx(2 * cg + 1, r)] * zj[2 * cg + 1];
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-    if (lane < 8) part[warp * 8 + lane] = acc;
-    __syncthreads();
-    if (warp == 0) {
-      double v = 0.0;
-      if (lane < 8) {
-        v = z[8 * it + lane];
-        for (int w = 0; w < nw; ++w) v -= part[w * 8 + lane];
+// y is row 0 of the RHS tiles, z (8T) written to `z`.  One warp, no CTA
+// barriers: step it, the 4 lane groups of 8 split the tiles jt > it and
+// accumulate column r of L(jt,it) . z_jt, then z_it = L_kk^-T (y_it - acc).
+// Called by all threads; returns after a __syncthreads with z complete.
+__device__ void tiled_back_subst(const double* tl, int T, double* z, double* /*part*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    for (int i = lane; i < 8 * T; i += 32) z[i] = tl[tidx(T, i >> 3) * 64 + eidx(0, i & 7)];
+    __syncwarp();
+    const int r = lane & 7, cg = lane >> 3;
+    for (int it = T - 1; it >= 0; --it) {
+      double acc = 0.0;
+      for (int jt = it + 1 + cg; jt < T; jt += 4) {
+        const double* t = tl + tidx(jt, it) * 64;
+        const double* zj = z + 8 * jt;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = fma(t[eidx(k, r)], zj[k], acc);
       }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+      const double v = z[8 * it + r] - acc;
       // z_it = L_kk^-T v: z[r] = sum_{c >= r} Linv[c][r] v[c]
       const double* li = tl + tidx(it, it) * 64;
       double zr = 0.0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const double vc = __shfl_sync(0xffffffffu, v, c);
-        if (c >= r) zr += li[eidx(c, r)] * vc;
+        if (c >= r) zr = fma(li[eidx(c, r)], vc, zr);
       }
+      __syncwarp();
       if (lane < 8) z[8 * it + lane] = zr;
+      __syncwarp();
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 }  // namespace gb

@@ -8,8 +8,16 @@ import paper_1503_03467_b200 as gb
 from paper_1503_03467_b200 import device as dv, gamblet_fast as gf
 from bench import build_inputs, EPS, RHO
 
+import os
+import subprocess
 q = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+smi = None
+if os.environ.get("SV_SMI"):
+    smi = subprocess.Popen(["nvidia-smi", "--id=0", "--query-gpu=clocks.sm", "--format=csv",
+                            "-lms", os.environ["SV_SMI"]], stdout=subprocess.DEVNULL)
+if os.environ.get("SV_PROF"):
+    dv.Prof.reset(enabled=True)
 grid, M, A, load, tree = build_inputs(q, "checker")
 sched = gb.make_schedule(EPS, q, uniform_rho=RHO)
 Md, Ad = dv.DeviceCSR.from_scipy(M), dv.DeviceCSR.from_scipy(A)
@@ -33,3 +41,5 @@ for i in range(n):
           f"retries +{s1['num_alloc_retries'] - s0['num_alloc_retries']} "
           f"peak {s1['allocated_bytes.all.peak'] / 2**30:.1f} GiB "
           f"reserved {s1['reserved_bytes.all.current'] / 2**30:.1f} GiB", flush=True)
+if smi is not None:
+    smi.terminate()
