@@ -306,7 +306,7 @@ int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* 
 int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
                        double* partials, void* stream, int layout) {
-  COUNT(SPL(layout, L, 3, w) * (unsigned long long)iters);
+  COUNT(3ULL * (unsigned long long)iters);  // sym layout: fused phase 2 + update
   return wrap(gbk_bjcg_iterations(L, w, BsT, inv, x, r, p, Ap, z, iters, state, partials,
                                   ST(stream), layout),
               "bjcg_iterations");

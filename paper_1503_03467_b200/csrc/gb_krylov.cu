@@ -1156,6 +1156,80 @@ __global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __res
   }
 }
 
+// k_bjcg_update for the symmetric band layout: Ap of each row is the phase-1
+// partial plus the neighbour tiles' spill-over (symb_fix_value, the value
+// k_symb_fix would store), alpha was set by k_symb_apply (red = 1).
+__global__ void __launch_bounds__(192) k_symb_bjcg_update(int L, int w, double* __restrict__ x,
+                                                          double* __restrict__ r,
+                                                          const double* __restrict__ p,
+                                                          const double* __restrict__ Ap,
+                                                          double* __restrict__ z,
+                                                          const double* __restrict__ inv,
+                                                          KState* st, double* part) {
+  __shared__ double rs[192];
+  __shared__ double sh[32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const int nb = (L >> 1) * (L >> 1), Lb = L >> 1, Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const int lb = threadIdx.x / 12, l = threadIdx.x % 12;
+  const int pi = l / 3, c = l - 3 * pi;
+  double rr = 0.0, rz = 0.0;
+  for (int b0 = blockIdx.x * 16; b0 < nb; b0 += gridDim.x * 16) {
+    const int b = b0 + lb;
+    long long pr = -1;
+    double rv = 0.0;
+    if (b < nb) {
+      const int bs = b / Lb, bt = b - bs * Lb;
+      const int ps = 2 * bs + (pi >> 1), pt = 2 * bt + (pi & 1);
+      pr = ((long long)(ps + w) * Lpad + (pt + w)) * 3 + c;
+      const double ap = symb_fix_value(Ap[pr], Ap + npad, L, w, ps, pt, c);
+      x[pr] += alpha * p[pr];
+      rv = r[pr] - alpha * ap;
+      r[pr] = rv;
+      rr += rv * rv;
+    }
+    rs[threadIdx.x] = rv;
+    __syncthreads();
+    if (b < nb) {
+      const double* iv = inv + (long long)b * 144 + l * 12;
+      const double* rb = rs + lb * 12;
+      double zv = 0.0;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) zv = fma(iv[k], rb[k], zv);
+      z[pr] = zv;
+      rz += rv * zv;
+    }
+    __syncthreads();
+  }
+  rr = block_sum(rr, sh);
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = rr;
+    part[2 * blockIdx.x + 1] = rz;
+  }
+  if (last_block(&st->counter)) {
+    double a, cc;
+    final_sum2(part, gridDim.x, &a, &cc, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      st->it += 1;
+      const double rn = sqrt(a);
+      st->rnorm = rn;
+      if (rn <= st->tol_abs) {
+        st->done = 1;
+        st->converged = 1;
+      } else if (st->it >= st->max_iter) {
+        st->done = 1;
+        st->converged = 0;
+      } else {
+        st->beta = cc / st->rs;
+        st->rs = cc;
+      }
+    }
+  }
+}
+
 // start: x = s x0 (or 0), r = b - s A x0 (Ax0 null => x0 = 0), z = Minv r, p = z;
 // ||b||, ||r||, r.z and the early exits of sparse_core.py:138-148.  Partials
 // are (||r||^2, r.z) pairs in part[0, 2G) and ||b||^2 in part[2G, 3G), so the
@@ -1575,37 +1649,50 @@ int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, dou
 }
 static inline bool use_sym(int layout, int L, int nr, int w) {
   return layout == 1 && use_tiled(L, nr, w) && L % kSymTH == 0 &&
-         symb_smem(w, 2) <= 227 * 1024;
+         symb_smem(w, 2) <= 226 * 1024;
 }
-// one symmetric-band application y_v = (S B S) x_v for nv = 1 or 2 vectors
-// (phase 1 + phase 2; mode_v as finish_reduction, 2 = no reduction)
+// phase 1 of the symmetric band SpMV for nv = 1 or 2 vectors; red_v = 1 forms
+// the CG reduction x_v.(A x_v) -> alpha in the same pass (the consumer is then
+// k_symb_bjcg_update, which adds the spill-over itself)
+static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, double* y0,
+                       KState* s0, double* p0, int r0, const double* x1, double* y1,
+                       KState* s1, double* p1, int r1, cudaStream_t s) {
+  const int nt = (int)symb_ntile(L);
+  const int gp = nt < kRedBlocks ? nt : kRedBlocks;
+  const size_t sm = symb_smem(w, nv);
+  // dynamic shared memory attribute raised to what this launch needs (the
+  // kernel also has static shared memory, so the 227 KB cap is not usable)
+  static size_t attr[3] = {0, 0, 0};
+  if (sm > attr[nv]) {
+    if (nv == 2)
+      cudaFuncSetAttribute(k_symb_apply<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    else
+      cudaFuncSetAttribute(k_symb_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr[nv] = sm;
+  }
+  if (nv == 2)
+    k_symb_apply<2><<<gp, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1, s1, p1, r1);
+  else
+    k_symb_apply<1><<<gp, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr, nullptr,
+                                                 nullptr, nullptr, 0);
+}
+// phase 2 alone (spill-over + reductions of mode m_v) for nv vectors
+static void sym_phase2(int L, int w, int nv, const double* x0, double* y0, KState* s0,
+                       double* p0, int m0, const double* x1, double* y1, KState* s1, double* p1,
+                       int m1, cudaStream_t s) {
+  const int gf = grid_for((long long)L * L * 3, 256, kRedBlocks);
+  if (nv == 2)
+    k_symb_fix<2><<<gf, 256, 0, s>>>(L, w, x0, y0, s0, p0, m0, x1, y1, s1, p1, m1);
+  else
+    k_symb_fix<1><<<gf, 256, 0, s>>>(L, w, x0, y0, s0, p0, m0, nullptr, nullptr, nullptr,
+                                     nullptr, 2);
+}
+// one complete symmetric-band application y_v = (S B S) x_v (phase 1 + 2)
 static int sym_apply(int L, int w, const double* U, int nv, const double* x0, double* y0,
                      KState* s0, double* p0, int m0, const double* x1, double* y1, KState* s1,
                      double* p1, int m1, cudaStream_t s) {
-  const int nt = (int)symb_ntile(L);
-  const size_t sm = symb_smem(w, nv);
-  const long long R = (long long)L * L * 3;
-  const int gf = grid_for(R, 256, kRedBlocks);
-  if (nv == 2) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(k_symb_apply<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
-      attr2 = true;
-    }
-    k_symb_apply<2><<<nt, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, x1, y1, s1);
-    k_symb_fix<2><<<gf, 256, 0, s>>>(L, w, x0, y0, s0, p0, m0, x1, y1, s1, p1, m1);
-  } else {
-    static bool attr1 = false;
-    if (!attr1) {
-      cudaFuncSetAttribute(k_symb_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
-      attr1 = true;
-    }
-    k_symb_apply<1><<<nt, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, nullptr, nullptr, nullptr);
-    k_symb_fix<1><<<gf, 256, 0, s>>>(L, w, x0, y0, s0, p0, m0, nullptr, nullptr, nullptr,
-                                     nullptr, 2);
-  }
+  sym_phase1(L, w, U, nv, x0, y0, s0, p0, 0, x1, y1, s1, p1, 0, s);
+  sym_phase2(L, w, nv, x0, y0, s0, p0, m0, x1, y1, s1, p1, m1, s);
   return (int)cudaGetLastError();
 }
 int gbk_tcg_iterations(int L, int nr, int w, const double* BsT, double* x, double* r,
@@ -1700,13 +1787,16 @@ int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, doub
   KState* k = (KState*)st;
   const bool sy = use_sym(layout, L, 3, w);
   for (int i = 0; i < iters; ++i) {
-    if (sy)
-      sym_apply(L, w, BsT, 1, p, Ap, k, part, 0, nullptr, nullptr, nullptr, nullptr, 2, s);
-    else if (use_tiled(L, 3, w))
-      k_tcg_spmv_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, p, Ap, k, part);
-    else
-      k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
-    k_bjcg_update<<<bj_grid(L), 192, 0, s>>>(L, w, x, r, p, Ap, z, inv, k, part);
+    if (sy) {  // alpha from phase 1, spill-over added by the fused update
+      sym_phase1(L, w, BsT, 1, p, Ap, k, part, 1, nullptr, nullptr, nullptr, nullptr, 0, s);
+      k_symb_bjcg_update<<<bj_grid(L), 192, 0, s>>>(L, w, x, r, p, Ap, z, inv, k, part);
+    } else {
+      if (use_tiled(L, 3, w))
+        k_tcg_spmv_tiled<<<tiled_grid(L), 192, tiled_smem(w), s>>>(L, w, BsT, p, Ap, k, part);
+      else
+        k_tcg_spmv<3><<<gs, 256, sm, s>>>(L, w, BsT, p, Ap, k, part);
+      k_bjcg_update<<<bj_grid(L), 192, 0, s>>>(L, w, x, r, p, Ap, z, inv, k, part);
+    }
     k_cg_dir<<<gv, 256, 0, s>>>(npad, z, p, k);
   }
   return (int)cudaGetLastError();
@@ -1881,7 +1971,7 @@ int gbk_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x
   int chunk = 8;
   for (;;) {
     int e = gbk_bjcg_iterations(L, w, BsT, inv, x, r, p, Ap, z, chunk, st, part, s, layout);
-    *launches += (use_sym(layout, L, 3, w) ? 4LL : 3LL) * chunk;
+    *launches += 3LL * chunk;
     if (e) return e;
     e = read_state(st, h, s);
     if (e) return e;
@@ -1982,11 +2072,22 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
 // ---------------------------------------------------------------------------
 #include "gb_engine.h"
 
+// ---- engine building blocks (count their launches into *nl) ----
+// dual pass: A (subband PCG, mode 0) and B (mode mb) on one sweep of S B S;
+// b_fused: B is a block-Jacobi PCG step whose update adds the spill-over
 static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, int mb,
-                       cudaStream_t s) {
-  if (e->layout == 1)
-    return sym_apply(e->L, e->w, e->BsT, 2, e->pa, e->apa, (KState*)e->sta, e->parta, 0, xb, yb,
-                     (KState*)e->stb, e->partb, mb, s);
+                       int b_fused, cudaStream_t s, long long* nl) {
+  if (e->layout == 1) {
+    sym_phase1(e->L, e->w, e->BsT, 2, e->pa, e->apa, (KState*)e->sta, e->parta, 1, xb, yb,
+               (KState*)e->stb, e->partb, b_fused, s);
+    *nl += 1;
+    if (!b_fused) {
+      sym_phase2(e->L, e->w, 1, xb, yb, (KState*)e->stb, e->partb, mb, nullptr, nullptr,
+                 nullptr, nullptr, 2, s);
+      *nl += 1;
+    }
+    return (int)cudaGetLastError();
+  }
   const int W2 = 2 * e->w + 1;
   const size_t smem = ((size_t)(W2 * W2 * 3 + 2) / 2 + 1) * sizeof(double) +
                       2 * (size_t)W2 * (kTileP + 2 * e->w) * 3 * sizeof(double);
@@ -1998,44 +2099,71 @@ static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, in
   k_dual_apply<<<tiled_grid(e->L), 192, smem, s>>>(
       e->L, e->w, e->BsT, e->pa, e->apa, (KState*)e->sta, e->parta, 0, xb, yb,
       (KState*)e->stb, e->partb, mb);
+  *nl += 1;
   return (int)cudaGetLastError();
 }
 
-// one live Krylov half: the dedicated single-vector tiled pass (smaller
-// shared-memory footprint than the dual kernel, same arithmetic)
+// one live Krylov half; fused: a block-Jacobi PCG step (see launch_dual)
 static int launch_single(const gb_level_engine_args* e, const double* x, double* y, void* st,
-                         double* part, int mode, cudaStream_t s) {
-  if (e->layout == 1)
-    return sym_apply(e->L, e->w, e->BsT, 1, x, y, (KState*)st, part, mode, nullptr, nullptr,
-                     nullptr, nullptr, 2, s);
+                         double* part, int mode, int fused, cudaStream_t s, long long* nl) {
+  if (e->layout == 1) {
+    sym_phase1(e->L, e->w, e->BsT, 1, x, y, (KState*)st, part, fused, nullptr, nullptr,
+               nullptr, nullptr, 0, s);
+    *nl += 1;
+    if (!fused) {
+      sym_phase2(e->L, e->w, 1, x, y, (KState*)st, part, mode, nullptr, nullptr, nullptr,
+                 nullptr, 2, s);
+      *nl += 1;
+    }
+    return (int)cudaGetLastError();
+  }
   if (mode == 0)
     k_tcg_spmv_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y,
                                                                       (KState*)st, part);
   else
     k_tpow_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x,
                                                                         y, (KState*)st, part);
+  *nl += 1;
   return (int)cudaGetLastError();
 }
 
 static int launch_plain(const gb_level_engine_args* e, const double* x, double* y,
-                        cudaStream_t s) {
-  if (e->layout == 1)
+                        cudaStream_t s, long long* nl) {
+  if (e->layout == 1) {
+    *nl += 2;
     return sym_apply(e->L, e->w, e->BsT, 1, x, y, nullptr, nullptr, 2, nullptr, nullptr, nullptr,
                      nullptr, 2, s);
+  }
   k_tbox_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y);
+  *nl += 1;
   return (int)cudaGetLastError();
 }
 
-static void post_a(const gb_level_engine_args* e, cudaStream_t s) {
+// block-Jacobi PCG update + direction of one half
+static void pcg_post(const gb_level_engine_args* e, double* x, double* r, double* p, double* Ap,
+                     double* z, KState* k, double* part, cudaStream_t s, long long* nl) {
   const int Lpad = e->L + 2 * e->w;
   const long long npad = (long long)Lpad * Lpad * 3;
-  KState* k = (KState*)e->sta;
-  k_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, e->xa, e->ra, e->pa, e->apa, e->za,
-                                              e->inv, k, e->parta);
-  k_cg_dir<<<grid_for(npad, 256, kRedBlocks), 256, 0, s>>>(npad, e->za, e->pa, k);
+  if (e->layout == 1)
+    k_symb_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, x, r, p, Ap, z, e->inv, k, part);
+  else
+    k_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, x, r, p, Ap, z, e->inv, k, part);
+  k_cg_dir<<<grid_for(npad, 256, kRedBlocks), 256, 0, s>>>(npad, z, p, k);
+  *nl += 2;
 }
 
+static void post_a(const gb_level_engine_args* e, cudaStream_t s, long long* nl) {
+  pcg_post(e, e->xa, e->ra, e->pa, e->apa, e->za, (KState*)e->sta, e->parta, s, nl);
+}
+
+static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl);
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches) {
+  long long nl = 0;
+  const int rc = level_engine(e, s, nl);
+  *launches += nl;
+  return rc;
+}
+static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
   const int Lpad = e->L + 2 * e->w;
   const long long npad = (long long)Lpad * Lpad * 3;
   const int gv = grid_for(npad, 256, kRedBlocks);
@@ -2045,21 +2173,20 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
   KState* hb = (KState*)e->hstb;
   int err;
   int chunk = 8;
-  const long long spl = e->layout == 1 ? 2 : 1;  // launches per S B S pass
   // --- power iteration (B) paired with the PCG (A) -----------------------
   for (;;) {
     const bool a_live = !ha->done;
     for (int i = 0; i < chunk; ++i) {
       if (a_live) {
-        if ((err = launch_dual(e, e->xb, e->yb, 1, s))) return err;
-        post_a(e, s);
-      } else if ((err = launch_single(e, e->xb, e->yb, e->stb, e->partb, 1, s))) {
+        if ((err = launch_dual(e, e->xb, e->yb, 1, 0, s, &nl))) return err;
+        post_a(e, s, &nl);
+      } else if ((err = launch_single(e, e->xb, e->yb, e->stb, e->partb, 1, 0, s, &nl))) {
         return err;
       }
       k_pow_step<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, e->tol, kb, e->partb);
       k_pow_scale<<<gv, 256, 0, s>>>(npad, e->xb, e->yb, kb);
+      nl += 2;
     }
-    *launches += (spl + 2 + (a_live ? 2 : 0)) * chunk;
     if ((err = (int)cudaGetLastError())) return err;
     if ((err = read_state(e->sta, ha, s))) return err;
     if ((err = read_state(e->stb, hb, s))) return err;
@@ -2092,27 +2219,26 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
                                    have_prev ? e->ax : nullptr, e->cx, e->cr, e->cp,
                                    e->inner_tol, (int)e->inner_max_iter, kb, e->partb);
     k_cg_zero_if<<<gv, 256, 0, s>>>(npad, e->cx, kb);
-    *launches += 3;
+    nl += 3;
     chunk = 8;
     for (;;) {
       const bool a_live = !ha->done;
       for (int i = 0; i < chunk; ++i) {
         if (a_live) {
-          if ((err = launch_dual(e, e->cp, e->cap, 0, s))) return err;
-          post_a(e, s);
-        } else if ((err = launch_single(e, e->cp, e->cap, e->stb, e->partb, 0, s))) {
+          if ((err = launch_dual(e, e->cp, e->cap, 0, e->inner_pcg, s, &nl))) return err;
+          post_a(e, s, &nl);
+        } else if ((err = launch_single(e, e->cp, e->cap, e->stb, e->partb, 0, e->inner_pcg, s,
+                                        &nl))) {
           return err;
         }
         if (e->inner_pcg) {
-          k_bjcg_update<<<bj_grid(e->L), 192, 0, s>>>(e->L, e->w, e->cx, e->cr, e->cp, e->cap,
-                                                      e->cz, e->inv, kb, e->partb);
-          k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cz, e->cp, kb);
+          pcg_post(e, e->cx, e->cr, e->cp, e->cap, e->cz, kb, e->partb, s, &nl);
         } else {
           k_cg_update<<<gv, 256, 0, s>>>(npad, e->cx, e->cr, e->cp, e->cap, kb, e->partb);
           k_cg_dir<<<gv, 256, 0, s>>>(npad, e->cr, e->cp, kb);
+          nl += 2;
         }
       }
-      *launches += (spl + 2 + (a_live ? 2 : 0)) * chunk;
       if ((err = (int)cudaGetLastError())) return err;
       if ((err = read_state(e->sta, ha, s))) return err;
       if ((err = read_state(e->stb, hb, s))) return err;
@@ -2129,9 +2255,9 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
     k_dot2<<<gv, 256, 0, s>>>(npad, e->cx, e->cx, nullptr, e->dots, kb, e->partb);
     k_scale_by_norm<<<grid_for(npad, 256, 148 * 16), 256, 0, s>>>(npad, e->cx, e->dots, 0, nxt,
                                                                   nullptr);
-    if ((err = launch_plain(e, nxt, e->ax, s))) return err;
+    if ((err = launch_plain(e, nxt, e->ax, s, &nl))) return err;
     k_dot2<<<gv, 256, 0, s>>>(npad, nxt, e->ax, nullptr, e->dots + 2, kb, e->partb);
-    *launches += 3 + spl;
+    nl += 3;
     e->calls += 1;
     if ((err = gbk_sync_read(e->dots, e->hdots, 4 * sizeof(double), s))) return err;
     e->n_outer = outer + 1;
@@ -2152,10 +2278,9 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
   chunk = 8;
   while (!ha->done) {
     for (int i = 0; i < chunk; ++i) {
-      if ((err = launch_single(e, e->pa, e->apa, e->sta, e->parta, 0, s))) return err;
-      post_a(e, s);
+      if ((err = launch_single(e, e->pa, e->apa, e->sta, e->parta, 0, 1, s, &nl))) return err;
+      post_a(e, s, &nl);
     }
-    *launches += (spl + 2) * chunk;
     if ((err = (int)cudaGetLastError())) return err;
     if ((err = read_state(e->sta, ha, s))) return err;
     chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;

@@ -83,145 +83,200 @@ __global__ void k_scale_box_symb(int L, int w, const double* __restrict__ B,
   }
 }
 
-// Phase 1: y_own (partial) and the tile's spill-over, for NV vectors sharing
+// spill-over sum of the neighbour tiles into own row (ps, pt, c), added to
+// `own` in a fixed order (tile rows above by distance, columns left, same,
+// right): the value phase 2 produces and the fused CG update consumes
+__device__ __forceinline__ double symb_fix_value(double own, const double* __restrict__ ov,
+                                                 int L, int w, int ps, int pt, int c) {
+  const int WC = kSymTW + 2 * w, RG = symb_region(w), tpr = L / kSymTW;
+  const int KI = (w + kSymTH - 1) / kSymTH;
+  const int I = ps / kSymTH, h = ps - I * kSymTH, J = pt / kSymTW, j = pt - J * kSymTW;
+  double s = own;
+  for (int dI = 0; dI <= KI; ++dI) {
+    const int Ip = I - dI, rr = h + dI * kSymTH;
+    if (Ip < 0 || rr >= kSymTH + w) break;
+    for (int dJ = -1; dJ <= 1; ++dJ) {
+      if (dI == 0 && dJ == 0) continue;
+      const int Jp = J + dJ, cc = j - dJ * kSymTW;
+      if (Jp < 0 || Jp >= tpr || cc < -w || cc >= kSymTW + w) continue;
+      s += ov[((long long)Ip * tpr + Jp) * RG + (rr * WC + cc + w) * 3 + c];
+    }
+  }
+  return s;
+}
+
+// Phase 1: y_own (partial) and the tiles' spill-over, for NV vectors sharing
 // one pass over U.  Vectors are zero-halo padded ((L+2w)^2 x 3); the spill
-// area of y_v starts at y_v + (L+2w)^2 * 3.
+// area of y_v starts at y_v + (L+2w)^2 * 3.  red_v = 1: the CG reduction
+// x_v . (A x_v) is formed here by linearity (every tile's partial sums over
+// its whole region against the staged x window, out-of-domain x is the zero
+// halo) and finish_reduction(mode 0) sets alpha -- the fused CG update
+// (k_symb_bjcg_update) then adds the spill-over itself and no phase 2 runs.
 template <int NV>
 __global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
     int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
-    double* __restrict__ y0, const KState* s0, const double* __restrict__ x1,
-    double* __restrict__ y1, const KState* s1) {
+    double* __restrict__ y0, KState* s0, double* part0, int red0,
+    const double* __restrict__ x1, double* __restrict__ y1, KState* s1, double* part1,
+    int red1) {
   extern __shared__ double dyn[];
+  __shared__ double sh[32];
   const bool live0 = !(s0 && s0->done);
   const bool live1 = NV == 2 && !(s1 && s1->done);
   if (!live0 && !live1) return;
+  const bool rd0 = live0 && red0, rd1 = NV == 2 && live1 && red1;
   const int npos = symb_npos(w), NS2 = symb_ns(w) >> 1;
   const int WC = kSymTW + 2 * w, Lpad = L + 2 * w;
-  const int XW = (kSymTH + w) * WC * 3;            // x window doubles
+  const int XW = (kSymTH + w) * WC * 3;                 // x window doubles
   const int AC = 32 + 2 * w, AREG = (w + 1) * AC * 3;  // per-warp accumulator
+  const int RW = WC * 3, RG = symb_region(w);
+  const long long npad = (long long)Lpad * Lpad * 3, ntile = symb_ntile(L);
   int* xoff = reinterpret_cast<int*>(dyn);
   int* aoff = xoff + npos;
   double* xs = dyn + ((2 * npos + 1) >> 1) + 1;
   double* acc = xs + NV * XW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tpr = L / kSymTW;
-  const long long t = blockIdx.x;
-  const int I = (int)(t / tpr), J = (int)(t % tpr);
-  const int ps0 = I * kSymTH, pt0 = J * kSymTW;
   for (int e = tid; e < npos; e += blockDim.x) {
     int ds, dt;
     symb_offset(w, e, &ds, &dt);
     xoff[e] = (ds * WC + dt) * 3;
     aoff[e] = (ds * AC + dt) * 3;
   }
-  // stage x windows: the tile's own rows and the w rows below (padded rows
-  // ps0 + w .. ps0 + TH + 2w - 1), padded columns pt0 .. pt0 + 64 + 2w - 1
-  for (int e = tid; e < XW; e += blockDim.x) {
-    const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
-    const long long gi = ((long long)(ps0 + w + wr) * Lpad + pt0) * 3 + rem;
-    xs[e] = x0[gi];
-    if (NV == 2) xs[XW + e] = x1[gi];
-  }
-  for (int e = tid; e < NV * 2 * kSymTH * AREG; e += blockDim.x) acc[e] = 0.0;
-  __syncthreads();
-  const int h = warp >> 1, j = (warp & 1) * 32 + lane;
-  const long long p = (long long)(ps0 + h) * L + pt0 + j;
-  const double2* up = reinterpret_cast<const double2*>(U) + (p >> 5) * (32LL * NS2) + lane;
-  const int xo = (h * WC + (j + w)) * 3;        // own position in the window
-  const int ao = (lane + w) * 3;                // own position in the warp accumulator
-  double xa[NV][3], g[NV][3];
+  double dot[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      xa[v][c] = xs[v * XW + xo + c];
-      g[v][c] = 0.0;
+  for (int v = 0; v < NV; ++v) dot[v] = 0.0;
+  for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int I = (int)(t / tpr), J = (int)(t % tpr);
+    const int ps0 = I * kSymTH, pt0 = J * kSymTW;
+    // stage x windows: the tile's own rows and the w rows below (padded rows
+    // ps0 + w .. ps0 + TH + 2w - 1), padded columns pt0 .. pt0 + 64 + 2w - 1
+    for (int e = tid; e < XW; e += blockDim.x) {
+      const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
+      const long long gi = ((long long)(ps0 + w + wr) * Lpad + pt0) * 3 + rem;
+      xs[e] = x0[gi];
+      if (NV == 2) xs[XW + e] = x1[gi];
     }
-  double* aw = acc + warp * AREG;
-  // software pipeline: the slots of offset pair e + 2 are in flight while
-  // pair e is applied; the diagonal block is loaded up front
-  double2 cur[9], nxt[9], dg[5];
+    for (int e = tid; e < NV * 2 * kSymTH * AREG; e += blockDim.x) acc[e] = 0.0;
+    __syncthreads();
+    const int h = warp >> 1, j = (warp & 1) * 32 + lane;
+    const long long p = (long long)(ps0 + h) * L + pt0 + j;
+    const double2* up = reinterpret_cast<const double2*>(U) + (p >> 5) * (32LL * NS2) + lane;
+    const int xo = (h * WC + (j + w)) * 3;  // own position in the window
+    const int ao = (lane + w) * 3;          // own position in the warp accumulator
+    double xa[NV][3], g[NV][3];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) dg[k] = __ldg(up + (long long)(9 * npos / 2 + k) * 32);
-#pragma unroll
-  for (int k = 0; k < 9; ++k) cur[k] = __ldg(up + 32 * k);
-  for (int e = 0; e < npos; e += 2) {
-    if (e + 2 < npos) {
-      const double2* q = up + (long long)(9 * (e + 2) / 2) * 32;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) nxt[k] = __ldg(q + 32 * k);
-    }
-#pragma unroll
-    for (int ee = 0; ee < 2; ++ee) {
-      double ub[9];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) {
-        const int m = 9 * ee + i;
-        ub[i] = (m & 1) ? cur[m >> 1].y : cur[m >> 1].x;
-      }
-      const int xe = xo + xoff[e + ee], ae = ao + aoff[e + ee];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double* xw = xs + v * XW + xe;
-        const double n0 = xw[0], n1 = xw[1], n2 = xw[2];
-        g[v][0] = fma(ub[0], n0, fma(ub[1], n1, fma(ub[2], n2, g[v][0])));
-        g[v][1] = fma(ub[3], n0, fma(ub[4], n1, fma(ub[5], n2, g[v][1])));
-        g[v][2] = fma(ub[6], n0, fma(ub[7], n1, fma(ub[8], n2, g[v][2])));
-        double* a = aw + v * 2 * kSymTH * AREG + ae;
-        a[0] += fma(ub[0], xa[v][0], fma(ub[3], xa[v][1], ub[6] * xa[v][2]));
-        a[1] += fma(ub[1], xa[v][0], fma(ub[4], xa[v][1], ub[7] * xa[v][2]));
-        a[2] += fma(ub[2], xa[v][0], fma(ub[5], xa[v][1], ub[8] * xa[v][2]));
-      }
-      __syncwarp();
-    }
-#pragma unroll
-    for (int k = 0; k < 9; ++k) cur[k] = nxt[k];
-  }
-  {  // diagonal block
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      double* a = aw + v * 2 * kSymTH * AREG + ao;
+    for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const int m0 = 3 * c;
-        const double d0 = (m0 & 1) ? dg[m0 >> 1].y : dg[m0 >> 1].x;
-        const double d1 = ((m0 + 1) & 1) ? dg[(m0 + 1) >> 1].y : dg[(m0 + 1) >> 1].x;
-        const double d2 = ((m0 + 2) & 1) ? dg[(m0 + 2) >> 1].y : dg[(m0 + 2) >> 1].x;
-        a[c] += fma(d0, xa[v][0], fma(d1, xa[v][1], fma(d2, xa[v][2], g[v][c])));
+        xa[v][c] = xs[v * XW + xo + c];
+        g[v][c] = 0.0;
       }
+    double* aw = acc + warp * AREG;
+    // software pipeline: the slots of offset pair e + 2 are in flight while
+    // pair e is applied; the diagonal block is loaded up front
+    double2 cur[9], nxt[9], dg[5];
+  #pragma unroll
+    for (int k = 0; k < 5; ++k) dg[k] = __ldg(up + (long long)(9 * npos / 2 + k) * 32);
+  #pragma unroll
+    for (int k = 0; k < 9; ++k) cur[k] = __ldg(up + 32 * k);
+    for (int e = 0; e < npos; e += 2) {
+      if (e + 2 < npos) {
+        const double2* q = up + (long long)(9 * (e + 2) / 2) * 32;
+  #pragma unroll
+        for (int k = 0; k < 9; ++k) nxt[k] = __ldg(q + 32 * k);
+      }
+  #pragma unroll
+      for (int ee = 0; ee < 2; ++ee) {
+        double ub[9];
+  #pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const int m = 9 * ee + i;
+          ub[i] = (m & 1) ? cur[m >> 1].y : cur[m >> 1].x;
+        }
+        const int xe = xo + xoff[e + ee], ae = ao + aoff[e + ee];
+  #pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double* xw = xs + v * XW + xe;
+          const double n0 = xw[0], n1 = xw[1], n2 = xw[2];
+          g[v][0] = fma(ub[0], n0, fma(ub[1], n1, fma(ub[2], n2, g[v][0])));
+          g[v][1] = fma(ub[3], n0, fma(ub[4], n1, fma(ub[5], n2, g[v][1])));
+          g[v][2] = fma(ub[6], n0, fma(ub[7], n1, fma(ub[8], n2, g[v][2])));
+          double* a = aw + v * 2 * kSymTH * AREG + ae;
+          a[0] += fma(ub[0], xa[v][0], fma(ub[3], xa[v][1], ub[6] * xa[v][2]));
+          a[1] += fma(ub[1], xa[v][0], fma(ub[4], xa[v][1], ub[7] * xa[v][2]));
+          a[2] += fma(ub[2], xa[v][0], fma(ub[5], xa[v][1], ub[8] * xa[v][2]));
+        }
+        __syncwarp();
+      }
+  #pragma unroll
+      for (int k = 0; k < 9; ++k) cur[k] = nxt[k];
     }
-  }
-  __syncthreads();
-  // combine the warps' accumulators over the tile region in a fixed order
-  const int RW = WC * 3, RG = symb_region(w);
-  const long long npad = (long long)Lpad * Lpad * 3;
-  for (int idx = tid; idx < RG; idx += blockDim.x) {
-    const int rr = idx / RW, rem = idx - rr * RW;
-    const int cc = rem / 3 - w, c = rem % 3;
-    const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      if (v == 0 ? !live0 : !live1) continue;
-      const double* av = acc + v * 2 * kSymTH * AREG;
-      double s = 0.0;
-      for (int hh = h0; hh <= h1; ++hh) {
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int lc = cc - half * 32 + w;
-          if (lc >= 0 && lc < AC) s += av[(2 * hh + half) * AREG + ((rr - hh) * AC + lc) * 3 + c];
+    {  // diagonal block
+  #pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double* a = aw + v * 2 * kSymTH * AREG + ao;
+  #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int m0 = 3 * c;
+          const double d0 = (m0 & 1) ? dg[m0 >> 1].y : dg[m0 >> 1].x;
+          const double d1 = ((m0 + 1) & 1) ? dg[(m0 + 1) >> 1].y : dg[(m0 + 1) >> 1].x;
+          const double d2 = ((m0 + 2) & 1) ? dg[(m0 + 2) >> 1].y : dg[(m0 + 2) >> 1].x;
+          a[c] += fma(d0, xa[v][0], fma(d1, xa[v][1], fma(d2, xa[v][2], g[v][c])));
         }
       }
-      double* y = v == 0 ? y0 : y1;
-      if (rr < kSymTH && cc >= 0 && cc < kSymTW)
-        y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = s;
-      else
-        y[npad + t * RG + idx] = s;
     }
+    __syncthreads();
+    // combine the warps' accumulators over the tile region in a fixed order
+    for (int idx = tid; idx < RG; idx += blockDim.x) {
+      const int rr = idx / RW, rem = idx - rr * RW;
+      const int cc = rem / 3 - w, c = rem % 3;
+      const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (v == 0 ? !live0 : !live1) continue;
+        const double* av = acc + v * 2 * kSymTH * AREG;
+        double sm = 0.0;
+        for (int hh = h0; hh <= h1; ++hh) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int lc = cc - half * 32 + w;
+            if (lc >= 0 && lc < AC)
+              sm += av[(2 * hh + half) * AREG + ((rr - hh) * AC + lc) * 3 + c];
+          }
+        }
+        double* y = v == 0 ? y0 : y1;
+        if (rr < kSymTH && cc >= 0 && cc < kSymTW)
+          y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = sm;
+        else
+          y[npad + t * RG + idx] = sm;
+        if (v == 0 ? rd0 : rd1) dot[v] = fma(xs[v * XW + idx], sm, dot[v]);
+      }
+    }
+    __syncthreads();
+  }
+  if (!rd0 && !rd1) return;
+  KState* cs = rd0 ? s0 : s1;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (!(v == 0 ? rd0 : rd1)) continue;
+    const double a = block_sum(dot[v], sh);
+    if (threadIdx.x == 0) (v == 0 ? part0 : part1)[2 * blockIdx.x] = a;
+  }
+  if (last_block(&cs->counter)) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!(v == 0 ? rd0 : rd1)) continue;
+      const double* part = v == 0 ? part0 : part1;
+      double a = 0.0;
+      for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) a += part[2 * k];
+      a = block_sum(a, sh);
+      if (threadIdx.x == 0) finish_reduction(v == 0 ? s0 : s1, 0, a, 0.0);
+    }
+    if (threadIdx.x == 0) cs->counter = 0;
   }
 }
 
-// Phase 2: y_own += the neighbours' spill-over (fixed order: tile rows above
-// by distance, then columns left, same, right), then the reductions of
+// Phase 2: y_own += the neighbours' spill-over, then the reductions of
 // finish_reduction (mode 0: x.y -> alpha, 1: x.y, y.y -> lam, ynorm, 2: none).
 template <int NV>
 __global__ void __launch_bounds__(256) k_symb_fix(int L, int w, const double* __restrict__ x0,
@@ -234,8 +289,7 @@ __global__ void __launch_bounds__(256) k_symb_fix(int L, int w, const double* __
   const bool live0 = !(s0 && s0->done);
   const bool live1 = NV == 2 && !(s1 && s1->done);
   if (!live0 && !live1) return;
-  const int Lpad = L + 2 * w, WC = kSymTW + 2 * w, RG = symb_region(w), tpr = L / kSymTW;
-  const int KI = (w + kSymTH - 1) / kSymTH;
+  const int Lpad = L + 2 * w;
   const long long npad = (long long)Lpad * Lpad * 3, R = (long long)L * L * 3;
   double d[NV][2];
 #pragma unroll
@@ -245,24 +299,12 @@ __global__ void __launch_bounds__(256) k_symb_fix(int L, int w, const double* __
     const long long pp = r / 3;
     const int c = (int)(r - pp * 3);
     const int ps = (int)(pp / L), pt = (int)(pp % L);
-    const int I = ps / kSymTH, h = ps - I * kSymTH, J = pt / kSymTW, j = pt - J * kSymTW;
     const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       if (v == 0 ? !live0 : !live1) continue;
       double* y = v == 0 ? y0 : y1;
-      const double* ov = y + npad;
-      double s = y[yi];
-      for (int dI = 0; dI <= KI; ++dI) {
-        const int Ip = I - dI, rr = h + dI * kSymTH;
-        if (Ip < 0 || rr >= kSymTH + w) break;
-        for (int dJ = -1; dJ <= 1; ++dJ) {
-          if (dI == 0 && dJ == 0) continue;
-          const int Jp = J + dJ, cc = j - dJ * kSymTW;
-          if (Jp < 0 || Jp >= tpr || cc < -w || cc >= kSymTW + w) continue;
-          s += ov[((long long)Ip * tpr + Jp) * RG + (rr * WC + cc + w) * 3 + c];
-        }
-      }
+      const double s = symb_fix_value(y[yi], y + npad, L, w, ps, pt, c);
       y[yi] = s;
       const double* x = v == 0 ? x0 : x1;
       d[v][0] = fma(x[yi], s, d[v][0]);

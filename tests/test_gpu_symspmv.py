@@ -137,3 +137,38 @@ def test_sym_band_cg_and_power_match_full_box(L, w):
         out[layout] = (_unpad(L, w, dv.to_host(x)), _unpad(L, w, dv.to_host(xp)))
     for a, b_ in zip(out[0], out[1]):
         assert np.abs(a - b_).max() <= 1e-12 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("L,w", [(128, 4), (128, 6)])
+def test_sym_band_block_jacobi_pcg_matches_full_box(L, w):
+    """Block-Jacobi PCG steps: the symmetric layout's fused update (alpha from
+    phase 1 by linearity, spill-over added in the update) follows the full-box
+    iteration to rounding."""
+    vals, A, s = _sym_box(L, w, seed=5)
+    R = L * L * 3
+    B, sd = dv.to_dev(vals.reshape(-1)), dv.to_dev(s)
+    st = dv.stream()
+    ops = {0: dv.empty(nat.query("gb_boxT_elems", L, 3, w)),
+           1: dv.empty(nat.query("gb_boxsym_elems", L, w))}
+    nat.call("gb_scale_box_T", L, 3, w, dv.ptr(B), dv.ptr(sd), dv.ptr(ops[0]), st)
+    nat.call("gb_scale_box_symT", L, w, dv.ptr(B), dv.ptr(sd), dv.ptr(ops[1]), st)
+    inv = dv.empty(144 * (L // 2) ** 2)
+    nat.call("gb_bj_setup", L, w, dv.ptr(B), dv.ptr(sd), dv.ptr(inv), st)
+    npad = (L + 2 * w) ** 2 * 3
+    tail = nat.query("gb_sym_overflow_elems", L, w)
+    b = dv.to_dev(_pad(L, w, np.random.default_rng(4).standard_normal(R)))
+    red = nat.query("gb_red_blocks")
+    out = {}
+    for layout in (0, 1):
+        x, r, p, Ap, z = (dv.zeros(npad + tail) for _ in range(5))
+        state = dv.zeros(32)
+        part = dv.empty(2 * red)
+        nat.call("gb_state_reset", dv.ptr(state), 1000, st)
+        nat.call("gb_bjcg_init", L, w, dv.ptr(b), None, None, 1.0, dv.ptr(x), dv.ptr(r),
+                 dv.ptr(p), dv.ptr(z), dv.ptr(inv), 1e-30, 1000, dv.ptr(state), dv.ptr(part), st)
+        nat.call("gb_bjcg_iterations", L, w, dv.ptr(ops[layout]), dv.ptr(inv), dv.ptr(x),
+                 dv.ptr(r), dv.ptr(p), dv.ptr(Ap), dv.ptr(z), 10, dv.ptr(state), dv.ptr(part),
+                 st, layout)
+        torch.cuda.synchronize()
+        out[layout] = _unpad(L, w, dv.to_host(x))
+    assert np.abs(out[0] - out[1]).max() <= 1e-12 * np.abs(out[0]).max()
