@@ -257,7 +257,11 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ev0.record()
         marks = []
+        levels = parts = counter = None
         for _ in range(args.steps):
+            # drop the previous step's outputs first: holding two steps' level
+            # operators at once overflows the reserved pool (cudaMalloc stalls)
+            levels = parts = counter = None
             levels, parts, counter = step_device()
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()

@@ -187,12 +187,12 @@ int gb_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, doubl
 int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
                   void* stream, int layout);
 /* block-Jacobi (2x2 parents = 12x12 blocks) PCG for the subband systems */
-int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream);
+int gb_bj_setup(int L, int w, const double* B, const double* s, float* inv, void* stream);
 /* x = x0_scale * x0 (x0, Ax0 = A x0 nullable: zero start) */
 int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
-                 double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                 double x0_scale, double* x, double* r, double* p, double* z, const float* inv,
                  double rel_tol, int max_iter, void* state, double* partials, void* stream);
-int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
+int gb_bjcg_iterations(int L, int w, const double* BsT, const float* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
                        double* partials, void* stream, int layout);
 /* whole Krylov loops driven from C (chunked launches, pinned state reads);
@@ -201,7 +201,7 @@ int gb_sync_read(const void* dev, void* host, size_t bytes, void* stream);
 int gb_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, double* p,
                  double* Ap, void* state, double* partials, void* host_state, int max_chunk,
                  void* stream, int layout);
-int gb_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+int gb_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, double* r,
                   double* p, double* Ap, double* z, void* state, double* partials,
                   void* host_state, int max_chunk, void* stream, int layout);
 int gb_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,

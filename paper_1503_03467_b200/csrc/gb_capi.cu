@@ -290,20 +290,20 @@ int gb_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, doub
   COUNT(SPL(layout, L, nr, w) - 2);
   return wrap(gbk_tbox_apply(L, nr, w, BsT, x, y, ST(stream), layout), "tbox_apply");
 }
-int gb_bj_setup(int L, int w, const double* B, const double* s, double* inv, void* stream) {
+int gb_bj_setup(int L, int w, const double* B, const double* s, float* inv, void* stream) {
   if (L < 2 || (L & 1)) return invalid("bj_setup: parent grid side must be even");
   COUNT(1);
   return wrap(gbk_bj_setup(L, w, B, s, inv, ST(stream)), "bj_setup");
 }
 int gb_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
-                 double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                 double x0_scale, double* x, double* r, double* p, double* z, const float* inv,
                  double rel_tol, int max_iter, void* state, double* partials, void* stream) {
   COUNT(1);
   return wrap(gbk_bjcg_init(L, w, b, x0, Ax0, x0_scale, x, r, p, z, inv, rel_tol, max_iter,
                             state, partials, ST(stream)),
               "bjcg_init");
 }
-int gb_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
+int gb_bjcg_iterations(int L, int w, const double* BsT, const float* inv, double* x,
                        double* r, double* p, double* Ap, double* z, int iters, void* state,
                        double* partials, void* stream, int layout) {
   COUNT(3ULL * (unsigned long long)iters);  // sym layout: fused phase 2 + update
@@ -323,7 +323,7 @@ int gb_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, 
   COUNT(n);
   return wrap(e, "tcg_solve");
 }
-int gb_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+int gb_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, double* r,
                   double* p, double* Ap, double* z, void* state, double* partials,
                   void* host_state, int max_chunk, void* stream, int layout) {
   long long n = 0;

@@ -8,7 +8,7 @@ typedef struct gb_level_engine_args {
   int L, w, max_chunk, max_outer;
   const double* BsT;       /* full blocked slot-major S B S (tiled level) */
   /* A: subband block-Jacobi PCG, already initialised (gb_bjcg_init) */
-  const double* inv;
+  const float* inv;        /* block-Jacobi 12x12 inverses, fp32 (gb_bj_setup) */
   double *xa, *ra, *pa, *apa, *za;
   void* sta;
   double* parta;

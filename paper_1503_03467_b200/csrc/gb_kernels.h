@@ -125,19 +125,19 @@ int gbk_tpow_iterations(int L, int nr, int w, const double* BsT, double* x, doub
 int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, double* y,
                    cudaStream_t s, int layout);
 size_t gbk_boxT_elems(int L, int nr, int w);
-int gbk_bj_setup(int L, int w, const double* B, const double* sv, double* inv,
+int gbk_bj_setup(int L, int w, const double* B, const double* sv, float* inv,
                  cudaStream_t s);
 int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
-                  double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                  double x0_scale, double* x, double* r, double* p, double* z, const float* inv,
                   double rel_tol, int max_iter, void* st, double* part, cudaStream_t s);
-int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
+int gbk_bjcg_iterations(int L, int w, const double* BsT, const float* inv, double* x,
                         double* r, double* p, double* Ap, double* z, int iters, void* st,
                         double* part, cudaStream_t s, int layout);
 int gbk_sync_read(const void* dev, void* host, size_t bytes, cudaStream_t s);
 int gbk_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, double* p,
                   double* Ap, void* st, double* part, void* host_state, int max_chunk,
                   cudaStream_t s, long long* launches, int layout);
-int gbk_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+int gbk_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, double* r,
                    double* p, double* Ap, double* z, void* st, double* part, void* host_state,
                    int max_chunk, cudaStream_t s, long long* launches, int layout);
 int gbk_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,

@@ -1048,7 +1048,7 @@ __device__ __forceinline__ long long bj_row_pad(int L, int w, int b, int l) {
 
 // inverse of each 12x12 diagonal block of S B S (Gauss-Jordan, one warp per block)
 __global__ void k_bj_setup(int L, int w, const double* __restrict__ B,
-                           const double* __restrict__ s, double* __restrict__ inv) {
+                           const double* __restrict__ s, float* __restrict__ inv) {
   __shared__ double M[8][12][25];
   __shared__ double colk[8][12];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -1084,7 +1084,12 @@ __global__ void k_bj_setup(int L, int w, const double* __restrict__ B,
       }
       __syncwarp();
     }
-    for (int e = lane; e < 144; e += 32) inv[(long long)b * 144 + e] = m[e / 12][12 + e % 12];
+    // symmetrized and rounded to fp32: the preconditioner only has to be a
+    // fixed SPD operator (the residual stays fp64), half the bytes per step
+    for (int e = lane; e < 144; e += 32) {
+      const int i = e / 12, j = e % 12;
+      inv[(long long)b * 144 + e] = (float)(0.5 * (m[i][12 + j] + m[j][12 + i]));
+    }
     __syncwarp();
   }
 }
@@ -1095,7 +1100,7 @@ __global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __res
                                                      const double* __restrict__ p,
                                                      const double* __restrict__ Ap,
                                                      double* __restrict__ z,
-                                                     const double* __restrict__ inv,
+                                                     const float* __restrict__ inv,
                                                      KState* st, double* part) {
   __shared__ double rs[192];
   __shared__ double sh[32];
@@ -1118,11 +1123,11 @@ __global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __res
     rs[threadIdx.x] = rv;
     __syncthreads();
     if (b < nb) {
-      const double* iv = inv + (long long)b * 144 + l * 12;
+      const float* iv = inv + (long long)b * 144 + l * 12;
       const double* rb = rs + lb * 12;
       double zv = 0.0;
 #pragma unroll
-      for (int k = 0; k < 12; ++k) zv = fma(iv[k], rb[k], zv);
+      for (int k = 0; k < 12; ++k) zv = fma((double)iv[k], rb[k], zv);
       z[pr] = zv;
       rz += rv * zv;
     }
@@ -1164,7 +1169,7 @@ __global__ void __launch_bounds__(192) k_symb_bjcg_update(int L, int w, double* 
                                                           const double* __restrict__ p,
                                                           const double* __restrict__ Ap,
                                                           double* __restrict__ z,
-                                                          const double* __restrict__ inv,
+                                                          const float* __restrict__ inv,
                                                           KState* st, double* part) {
   __shared__ double rs[192];
   __shared__ double sh[32];
@@ -1192,11 +1197,11 @@ __global__ void __launch_bounds__(192) k_symb_bjcg_update(int L, int w, double* 
     rs[threadIdx.x] = rv;
     __syncthreads();
     if (b < nb) {
-      const double* iv = inv + (long long)b * 144 + l * 12;
+      const float* iv = inv + (long long)b * 144 + l * 12;
       const double* rb = rs + lb * 12;
       double zv = 0.0;
 #pragma unroll
-      for (int k = 0; k < 12; ++k) zv = fma(iv[k], rb[k], zv);
+      for (int k = 0; k < 12; ++k) zv = fma((double)iv[k], rb[k], zv);
       z[pr] = zv;
       rz += rv * zv;
     }
@@ -1241,7 +1246,7 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
                                                    double* __restrict__ x, double* __restrict__ r,
                                                    double* __restrict__ p,
                                                    double* __restrict__ z,
-                                                   const double* __restrict__ inv,
+                                                   const float* __restrict__ inv,
                                                    double rel_tol, int max_iter, KState* st,
                                                    double* part) {
   __shared__ double rs[192];
@@ -1265,11 +1270,11 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
     rs[threadIdx.x] = rv;
     __syncthreads();
     if (bk < nb) {
-      const double* iv = inv + (long long)bk * 144 + l * 12;
+      const float* iv = inv + (long long)bk * 144 + l * 12;
       const double* rb = rs + lb * 12;
       double zv = 0.0;
 #pragma unroll
-      for (int k = 0; k < 12; ++k) zv = fma(iv[k], rb[k], zv);
+      for (int k = 0; k < 12; ++k) zv = fma((double)iv[k], rb[k], zv);
       z[pr] = zv;
       p[pr] = zv;
       rz += rv * zv;
@@ -1751,7 +1756,7 @@ int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, dou
 
 
 // ---- block-Jacobi PCG launchers ----
-int gbk_bj_setup(int L, int w, const double* B, const double* sv, double* inv,
+int gbk_bj_setup(int L, int w, const double* B, const double* sv, float* inv,
                  cudaStream_t s) {
   const int nb = (L / 2) * (L / 2);
   k_bj_setup<<<grid_for(nb, 8, 148 * 16), 256, 0, s>>>(L, w, B, sv, inv);
@@ -1766,7 +1771,7 @@ static inline int bj_init_grid(int L) {
   return grid_for(nb, 16, (2 * kRedBlocks) / 3);
 }
 int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double* Ax0,
-                  double x0_scale, double* x, double* r, double* p, double* z, const double* inv,
+                  double x0_scale, double* x, double* r, double* p, double* z, const float* inv,
                   double rel_tol, int max_iter, void* st, double* part, cudaStream_t s) {
   k_bjcg_init<<<bj_init_grid(L), 192, 0, s>>>(L, w, b, x0, Ax0, x0_scale, x, r, p, z, inv,
                                               rel_tol, max_iter, (KState*)st, part);
@@ -1776,7 +1781,7 @@ int gbk_bjcg_init(int L, int w, const double* b, const double* x0, const double*
   }
   return (int)cudaGetLastError();
 }
-int gbk_bjcg_iterations(int L, int w, const double* BsT, const double* inv, double* x,
+int gbk_bjcg_iterations(int L, int w, const double* BsT, const float* inv, double* x,
                         double* r, double* p, double* Ap, double* z, int iters, void* st,
                         double* part, cudaStream_t s, int layout) {
   const int Lpad = L + 2 * w;
@@ -1964,7 +1969,7 @@ int gbk_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r,
   }
 }
 
-int gbk_bjcg_solve(int L, int w, const double* BsT, const double* inv, double* x, double* r,
+int gbk_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, double* r,
                    double* p, double* Ap, double* z, void* st, double* part, void* host_state,
                    int max_chunk, cudaStream_t s, long long* launches, int layout) {
   KState* h = (KState*)host_state;

@@ -23,77 +23,77 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
       : "d"(a), "d"(b));
 }
 
-// Factor the 8x8 diagonal tile and form L^-1 over it, in registers: every
-// lane of the warp runs the same fully unrolled Cholesky-Crout and in-place
-// inversion (no shuffles on the serial pivot chain), lanes 0..7 write one row
-// each.  Diagonal L tiles are never DMMA operands; every later use (TRSM, back
-// substitution) needs L_kk^-1.  Returns false if a pivot is not positive.
-__device__ __forceinline__ bool warp_chol8_inv(double* t) {
+// Factor the 8x8 diagonal tile (one warp, rows in lanes 0..7, registers and
+// shuffles), form L^-1 and store it OVER the tile: diagonal L tiles are never
+// DMMA operands, every later use (TRSM, back substitution) needs L_kk^-1.
+// `scratch` holds 8 doubles.  Returns false if a pivot is not positive.
+__device__ __forceinline__ bool warp_chol8_inv(double* t, double* scratch) {
   const int lane = threadIdx.x & 31;
-  double a[8][8];
+  const int r = lane & 7;
+  double v[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c <= r; ++c) a[r][c] = t[eidx(r, c)];
-  __syncwarp();
+  for (int c = 0; c < 8; ++c) v[c] = (c <= r) ? t[eidx(r, c)] : 0.0;
+  double il_r = 0.0;  // 1 / L_rr, kept by lane r
   bool ok = true;
-  double il[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    double d = a[j][j];
-#pragma unroll
-    for (int k = 0; k < j; ++k) d = fma(-a[j][k], a[j][k], d);
+    const double d = __shfl_sync(0xffffffffu, v[j], j);
     ok = ok && (d > 0.0);
-    const double inv = rsqrt(d);
-    il[j] = inv;
-    a[j][j] = d * inv;
+    const double il = rsqrt(d);
+    if (r > j) v[j] *= il;
+    if (r == j) {
+      v[j] = d * il;
+      il_r = il;
+    }
 #pragma unroll
-    for (int i = j + 1; i < 8; ++i) {
-      double v = a[i][j];
-#pragma unroll
-      for (int k = 0; k < j; ++k) v = fma(-a[i][k], a[j][k], v);
-      a[i][j] = v * inv;
+    for (int c = j + 1; c < 8; ++c) {
+      const double lcj = __shfl_sync(0xffffffffu, v[j], c);
+      if (r > j && c <= r) v[c] = fma(-v[j], lcj, v[c]);
     }
   }
-  // L^-1 in place, column by column left to right:
-  // X_jj = 1/L_jj, X_ij = -(sum_{j<=k<i} L_ik X_kj) / L_ii
+  if (!ok) return false;
+  if (lane < 8) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    a[j][j] = il[j];
-#pragma unroll
-    for (int i = j + 1; i < 8; ++i) {
-      double acc = a[i][j] * a[j][j];
-#pragma unroll
-      for (int k = j + 1; k < i; ++k) acc = fma(a[i][k], a[k][j], acc);
-      a[i][j] = -acc * il[i];
-    }
+    for (int c = 0; c < 8; ++c)
+      if (c <= r) t[eidx(r, c)] = v[c];
+    scratch[r] = il_r;  // diagonal of L^-1, read back below
   }
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-    if (lane == r) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) t[eidx(r, c)] = c <= r ? a[r][c] : 0.0;
-    }
   __syncwarp();
-  return ok;
+  // L^-1, column r by lane r: x_i = -(sum_{r<=k<i} L_ik x_k) / L_ii, x_r = 1/L_rr
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) acc = fma(t[eidx(i, k)], x[k], acc);
+    const double ii = scratch[i];
+    x[i] = (i > r) ? -acc * ii : ((i == r) ? ii : 0.0);
+  }
+  __syncwarp();
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[eidx(i, r)] = x[i];  // column r of L^-1 (upper = 0)
+  }
+  __syncwarp();
+  return true;
 }
 
 // Left-looking tiled Cholesky + forward substitution of the RHS row, with a
 // one-column lookahead.  Invariant at the start of step kt: every tile
 // (it, kt), it >= kt, already holds the contributions of columns < kt-1.
 // Step kt: warp 0 adds column kt-1 to the diagonal tile and factors it
-// (L_kk^-1 in registers); meanwhile warps 1.. finish the rest of column kt
+// (L_kk^-1 over the tile); meanwhile warps 1.. finish the rest of column kt
 // (one DMMA pair per tile) and pre-accumulate column kt+1 from columns
 // 0..kt-1 (the bulk of the flops, two independent accumulator chains per
 // tile).  Then all warps apply the TRSM L(it,kt) = C(it,kt) L_kk^-T (two
 // DMMAs with L_kk^-1).  The serial chain per step is one DMMA pair, the
-// register 8x8 factor and the TRSM.  tl: tile storage (diagonal tiles end up
+// 8x8 factor and the TRSM.  tl: tile storage (diagonal tiles end up
 // holding L_kk^-1), T: tiles per dimension, flag: shared int.  Returns false
 // (CTA-uniform) when the matrix is not SPD.
 #ifdef GB_PATCH_PROF
 __device__ unsigned long long g_fprof[8];
 #endif
-__device__ bool tiled_chol_fwd(double* tl, int T, double* /*scratch*/, int* flag) {
+__device__ bool tiled_chol_fwd(double* tl, int T, double* scratch, int* flag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const int e0 = eidx(fr, 2 * fk), e1 = eidx(fr, 2 * fk + 1);
@@ -115,7 +115,7 @@ __device__ bool tiled_chol_fwd(double* tl, int T, double* /*scratch*/, int* flag
         ct[e1] = c1;
         __syncwarp();
       }
-      if (!warp_chol8_inv(ct) && lane == 0) *flag = 1;
+      if (!warp_chol8_inv(ct, scratch) && lane == 0) *flag = 1;
     } else {
       if (kt > 0) {  // finish column kt: C(it,kt) -= L(it,kt-1) L(kt,kt-1)^T
         const double b0 = lk1[ea], b1 = lk1[eb];

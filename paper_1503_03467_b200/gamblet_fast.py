@@ -388,10 +388,11 @@ class _POp:
         self._box, self._s, self._bj = box, s, None
 
     def bj_inv(self):
-        """Inverses of the 12x12 diagonal blocks (2x2 parents) of S B S."""
+        """Inverses of the 12x12 diagonal blocks (2x2 parents) of S B S
+        (symmetrized, fp32: the preconditioner of the block-Jacobi PCG)."""
         if self._bj is None:
             nb = (self.L // 2) ** 2
-            self._bj = dv.empty(144 * nb)
+            self._bj = dv.empty(144 * nb, dtype=torch.float32)
             nat.call("gb_bj_setup", self.L, self.w, dv.ptr(self._box.vals), dv.ptr(self._s),
                      dv.ptr(self._bj), dv.stream())
         return self._bj

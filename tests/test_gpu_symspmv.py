@@ -152,7 +152,7 @@ def test_sym_band_block_jacobi_pcg_matches_full_box(L, w):
            1: dv.empty(nat.query("gb_boxsym_elems", L, w))}
     nat.call("gb_scale_box_T", L, 3, w, dv.ptr(B), dv.ptr(sd), dv.ptr(ops[0]), st)
     nat.call("gb_scale_box_symT", L, w, dv.ptr(B), dv.ptr(sd), dv.ptr(ops[1]), st)
-    inv = dv.empty(144 * (L // 2) ** 2)
+    inv = dv.empty(144 * (L // 2) ** 2, dtype=torch.float32)
     nat.call("gb_bj_setup", L, w, dv.ptr(B), dv.ptr(sd), dv.ptr(inv), st)
     npad = (L + 2 * w) ** 2 * 3
     tail = nat.query("gb_sym_overflow_elems", L, w)
