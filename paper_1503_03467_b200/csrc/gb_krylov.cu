@@ -1659,21 +1659,45 @@ static inline bool use_sym(int layout, int L, int nr, int w) {
 // phase 1 of the symmetric band SpMV for nv = 1 or 2 vectors; red_v = 1 forms
 // the CG reduction x_v.(A x_v) -> alpha in the same pass (the consumer is then
 // k_symb_bjcg_update, which adds the spill-over itself)
+#ifndef GB_SYM_WS
+#define GB_SYM_WS 1  // warp-specialized bulk-copy phase 1 (0: register-pipelined)
+#endif
 static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, double* y0,
                        KState* s0, double* p0, int r0, const double* x1, double* y1,
                        KState* s1, double* p1, int r1, cudaStream_t s) {
   const int nt = (int)symb_ntile(L);
+  // dynamic shared memory attribute raised to what a launch needs (the
+  // kernels also have static shared memory, so the 227 KB cap is not usable)
+  static size_t attr[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  const bool ws = GB_SYM_WS && symb_ws_smem(w, nv) <= 226 * 1024;
+  if (ws) {
+    const int gp = nt < 148 ? nt : 148;  // persistent: one CTA per SM
+    const size_t sm = symb_ws_smem(w, nv);
+    if (sm > attr[1][nv]) {
+      if (nv == 2)
+        cudaFuncSetAttribute(k_symb_apply_ws<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+      else
+        cudaFuncSetAttribute(k_symb_apply_ws<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+      attr[1][nv] = sm;
+    }
+    if (nv == 2)
+      k_symb_apply_ws<2><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1,
+                                                          s1, p1, r1);
+    else
+      k_symb_apply_ws<1><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr,
+                                                          nullptr, nullptr, nullptr, 0);
+    return;
+  }
   const int gp = nt < kRedBlocks ? nt : kRedBlocks;
   const size_t sm = symb_smem(w, nv);
-  // dynamic shared memory attribute raised to what this launch needs (the
-  // kernel also has static shared memory, so the 227 KB cap is not usable)
-  static size_t attr[3] = {0, 0, 0};
-  if (sm > attr[nv]) {
+  if (sm > attr[0][nv]) {
     if (nv == 2)
       cudaFuncSetAttribute(k_symb_apply<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     else
       cudaFuncSetAttribute(k_symb_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr[nv] = sm;
+    attr[0][nv] = sm;
   }
   if (nv == 2)
     k_symb_apply<2><<<gp, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1, s1, p1, r1);

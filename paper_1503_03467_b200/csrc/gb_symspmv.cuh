@@ -276,6 +276,279 @@ __global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phase 1, warp-specialized (default): a persistent CTA per SM, 8 consumer
+// warps as above plus one producer warp that streams the consumers' U blocks
+// into a kSymWsStages-deep shared-memory ring with 1-D bulk copies
+// (cp.async.bulk, TMA engine; full/empty mbarriers per stage).  The producer
+// runs ahead across tile boundaries, so the x staging and the combine of a
+// tile overlap the HBM stream of the next; bytes in flight cost no registers.
+// Same arithmetic and summation order as k_symb_apply.
+// ---------------------------------------------------------------------------
+constexpr int kSymWsPairs = 9;  // slot pairs of one chunk (two offsets)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {  // the 8 consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"r"(kSymThreads) : "memory");
+}
+
+template <int NV>
+__host__ __device__ constexpr int symb_ws_stages() { return NV == 1 ? 4 : 3; }
+
+static inline size_t symb_ws_smem(int w, int nv) {
+  const int npos = symb_npos(w), WC = kSymTW + 2 * w, nwarp = 2 * kSymTH;
+  const int st = nv == 1 ? symb_ws_stages<1>() : symb_ws_stages<2>();
+  return (size_t)2 * st * 8 +                                        // full/empty barriers
+         (size_t)st * nwarp * kSymWsPairs * 32 * 16 +                 // U ring
+         (size_t)nv * (kSymTH + w) * WC * 3 * 8 +                     // x windows
+         (size_t)nv * nwarp * (w + 1) * (32 + 2 * w) * 3 * 8 +        // accumulators
+         (size_t)2 * npos * 4;                                        // offset tables
+}
+
+template <int NV>
+__global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
+    int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
+    double* __restrict__ y0, KState* s0, double* part0, int red0,
+    const double* __restrict__ x1, double* __restrict__ y1, KState* s1, double* part1,
+    int red1) {
+  constexpr int NS = symb_ws_stages<NV>();
+  constexpr int NW = 2 * kSymTH;  // consumer warps
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ double sh[32];
+  const bool live0 = !(s0 && s0->done);
+  const bool live1 = NV == 2 && !(s1 && s1->done);
+  if (!live0 && !live1) return;
+  const bool rd0 = live0 && red0, rd1 = NV == 2 && live1 && red1;
+  const int npos = symb_npos(w), NS2 = symb_ns(w) >> 1, nch = npos / 2 + 1;
+  const int WC = kSymTW + 2 * w, Lpad = L + 2 * w;
+  const int XW = (kSymTH + w) * WC * 3;
+  const int AC = 32 + 2 * w, AREG = (w + 1) * AC * 3;
+  const int RW = WC * 3, RG = symb_region(w);
+  const long long npad = (long long)Lpad * Lpad * 3, ntile = symb_ntile(L);
+  const int tpr = L / kSymTW;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(dsm);
+  unsigned long long* empty = full + NS;
+  double2* ring = reinterpret_cast<double2*>(dsm + 2 * NS * 8);
+  double* xs = reinterpret_cast<double*>(ring + NS * NW * kSymWsPairs * 32);
+  double* acc = xs + NV * XW;
+  int* xoff = reinterpret_cast<int*>(acc + NV * NW * AREG);
+  int* aoff = xoff + npos;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int st = 0; st < NS; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = tid; e < npos; e += blockDim.x) {
+    int ds, dt;
+    symb_offset(w, e, &ds, &dt);
+    xoff[e] = (ds * WC + dt) * 3;
+    aoff[e] = (ds * AC + dt) * 3;
+  }
+  __syncthreads();
+  double dot[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) dot[v] = 0.0;
+  if (warp == NW) {
+    // ---- producer: chunk g = (tile iteration, k) -> stage g % NS ----
+    if (lane == 0) {
+      long long g = 0;
+      for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const int I = (int)(t / tpr), J = (int)(t % tpr);
+        for (int k = 0; k < nch; ++k, ++g) {
+          const int st = (int)(g % NS);
+          const long long r = g / NS;
+          if (r > 0) mbar_wait(empty + st, (unsigned)((r - 1) & 1));
+          const int pairs = k < nch - 1 ? kSymWsPairs : 5;
+          const unsigned bytes = (unsigned)pairs * 32 * 16;
+          mbar_expect_tx(full + st, bytes * NW);
+          double2* dst = ring + (long long)st * NW * kSymWsPairs * 32;
+          for (int cw = 0; cw < NW; ++cw) {
+            const long long p =
+                (long long)(I * kSymTH + (cw >> 1)) * L + J * kSymTW + (cw & 1) * 32;
+            const double2* src = reinterpret_cast<const double2*>(U) + (p >> 5) * (32LL * NS2) +
+                                  (long long)k * kSymWsPairs * 32;
+            bulk_g2s(dst + cw * kSymWsPairs * 32, src, bytes, full + st);
+          }
+        }
+      }
+    }
+  } else {
+    // ---- consumers ----
+    long long g = 0;
+    for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+      const int I = (int)(t / tpr), J = (int)(t % tpr);
+      const int ps0 = I * kSymTH, pt0 = J * kSymTW;
+      // x windows, 8 independent loads in flight per thread (L2 latency)
+      for (int e0 = tid; e0 < XW; e0 += 8 * kSymThreads) {
+        double va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * kSymThreads;
+          va[u] = vb[u] = 0.0;
+          if (e < XW) {
+            const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
+            const long long gi = ((long long)(ps0 + w + wr) * Lpad + pt0) * 3 + rem;
+            va[u] = x0[gi];
+            if (NV == 2) vb[u] = x1[gi];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * kSymThreads;
+          if (e < XW) {
+            xs[e] = va[u];
+            if (NV == 2) xs[XW + e] = vb[u];
+          }
+        }
+      }
+      for (int e = tid; e < NV * NW * AREG; e += kSymThreads) acc[e] = 0.0;
+      consumer_sync();
+      const int h = warp >> 1, j = (warp & 1) * 32 + lane;
+      const int xo = (h * WC + (j + w)) * 3;
+      const int ao = (lane + w) * 3;
+      double xa[NV][3], gg[NV][3];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xa[v][c] = xs[v * XW + xo + c];
+          gg[v][c] = 0.0;
+        }
+      double* aw = acc + warp * AREG;
+      for (int k = 0; k < nch; ++k, ++g) {
+        const int st = (int)(g % NS);
+        mbar_wait(full + st, (unsigned)((g / NS) & 1));
+        const double2* sb = ring + ((long long)st * NW + warp) * kSymWsPairs * 32 + lane;
+        if (k < nch - 1) {
+#pragma unroll
+          for (int ee = 0; ee < 2; ++ee) {
+            double ub[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+              const int m = 9 * ee + i;
+              const double2 d = sb[(m >> 1) * 32];
+              ub[i] = (m & 1) ? d.y : d.x;
+            }
+            const int e = 2 * k + ee;
+            const int xe = xo + xoff[e], ae = ao + aoff[e];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const double* xw = xs + v * XW + xe;
+              const double n0 = xw[0], n1 = xw[1], n2 = xw[2];
+              gg[v][0] = fma(ub[0], n0, fma(ub[1], n1, fma(ub[2], n2, gg[v][0])));
+              gg[v][1] = fma(ub[3], n0, fma(ub[4], n1, fma(ub[5], n2, gg[v][1])));
+              gg[v][2] = fma(ub[6], n0, fma(ub[7], n1, fma(ub[8], n2, gg[v][2])));
+              double* a = aw + v * NW * AREG + ae;
+              a[0] += fma(ub[0], xa[v][0], fma(ub[3], xa[v][1], ub[6] * xa[v][2]));
+              a[1] += fma(ub[1], xa[v][0], fma(ub[4], xa[v][1], ub[7] * xa[v][2]));
+              a[2] += fma(ub[2], xa[v][0], fma(ub[5], xa[v][1], ub[8] * xa[v][2]));
+            }
+            __syncwarp();
+          }
+        } else {  // diagonal block
+          double u[10];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            const double2 d = sb[i * 32];
+            u[2 * i] = d.x;
+            u[2 * i + 1] = d.y;
+          }
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double* a = aw + v * NW * AREG + ao;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              a[c] += fma(u[3 * c], xa[v][0], fma(u[3 * c + 1], xa[v][1],
+                                                 fma(u[3 * c + 2], xa[v][2], gg[v][c])));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+      }
+      consumer_sync();
+      for (int idx = tid; idx < RG; idx += kSymThreads) {
+        const int rr = idx / RW, rem = idx - rr * RW;
+        const int cc = rem / 3 - w, c = rem % 3;
+        const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          if (v == 0 ? !live0 : !live1) continue;
+          const double* av = acc + v * NW * AREG;
+          double sm = 0.0;
+          for (int hh = h0; hh <= h1; ++hh) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              const int lc = cc - half * 32 + w;
+              if (lc >= 0 && lc < AC)
+                sm += av[(2 * hh + half) * AREG + ((rr - hh) * AC + lc) * 3 + c];
+            }
+          }
+          double* y = v == 0 ? y0 : y1;
+          if (rr < kSymTH && cc >= 0 && cc < kSymTW)
+            y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = sm;
+          else
+            y[npad + t * RG + idx] = sm;
+          if (v == 0 ? rd0 : rd1) dot[v] = fma(xs[v * XW + idx], sm, dot[v]);
+        }
+      }
+      consumer_sync();
+    }
+  }
+  __syncthreads();
+  if (!rd0 && !rd1) return;
+  KState* cs = rd0 ? s0 : s1;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (!(v == 0 ? rd0 : rd1)) continue;
+    const double a = block_sum(dot[v], sh);
+    if (threadIdx.x == 0) (v == 0 ? part0 : part1)[2 * blockIdx.x] = a;
+  }
+  if (last_block(&cs->counter)) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!(v == 0 ? rd0 : rd1)) continue;
+      const double* part = v == 0 ? part0 : part1;
+      double a = 0.0;
+      for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) a += part[2 * k];
+      a = block_sum(a, sh);
+      if (threadIdx.x == 0) finish_reduction(v == 0 ? s0 : s1, 0, a, 0.0);
+    }
+    if (threadIdx.x == 0) cs->counter = 0;
+  }
+}
+
 // Phase 2: y_own += the neighbours' spill-over, then the reductions of
 // finish_reduction (mode 0: x.y -> alpha, 1: x.y, y.y -> lam, ynorm, 2: none).
 template <int NV>
