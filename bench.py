@@ -158,6 +158,8 @@ def kernel_timings(levels, q):
     from paper_1503_03467_b200 import _native as nat, device as dv, gamblet_fast as gf
     lv = levels[q]
     op = lv._op
+    if op is None:
+        return None
     x = op.vec()
     y = op.vec()
     s = dv.stream()
@@ -178,6 +180,10 @@ def kernel_timings(levels, q):
     its = sum(d["power"] + sum(d["inner"]) + len(d["inner"]) for d in gf._SPECTRAL_LOG[-(q - 1):]
               if d["n"] == op.n)
     B = lv.raw("subband")
+    if B is None:  # lean transform (q >= 12): the subband box is not retained
+        return {"layout": op.layout,
+                "spmv": {"ms": spmv_ms, "bytes": spmv_bytes, "launches_per_step": its},
+                "corr": None}
     rho = min(3, B.L - 1)
     Dt = dv.empty(B.L * B.L * dv.box_slots(rho, 3))
     st = dv.zeros(2, torch.int64)
@@ -233,8 +239,12 @@ def run_ours(args, rank, world, local_rank):
     Ad = dv.DeviceCSR.from_scipy(A)
     gd = dv.to_dev(load.g_nodal)
 
+    # q >= 12: the memory-bounded transform (same arithmetic; level operators
+    # released once consumed) -- 16.8 M DOFs do not fit otherwise
+    lean = q >= 12
+
     def step_device():
-        levels, parts, U1, counter = gf._fast_solve_device(Md, Ad, gd, tree, sched)
+        levels, parts, U1, counter = gf._fast_solve_device(Md, Ad, gd, tree, sched, lean=lean)
         return levels, parts, counter
 
     def barrier():
@@ -302,7 +312,7 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         dv.Traffic.reset()
         t0 = time.perf_counter()
-        res = gb.fast_solve(M, A, load, tree, EPS, uniform_rho=RHO, c_tol=CTOL)
+        res = gb.fast_solve(M, A, load, tree, EPS, uniform_rho=RHO, c_tol=CTOL, lean=lean)
         u = res.solution.u  # host copy made inside the call
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
@@ -347,7 +357,7 @@ def run_ours(args, rank, world, local_rank):
             "launches_per_step": sp["launches_per_step"],
             "share_of_step_serialized": round(sp["ms"] * sp["launches_per_step"] / ms, 3)}
     cp = kern["corr"]
-    fp = {"kernel": "k_correction_patches_v2 (finest level, tiled DMMA Cholesky)",
+    fp = None if cp is None else {"kernel": "k_correction_patches_v2 (finest level, tiled DMMA Cholesky)",
           "bound": "fp64", "achieved": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12, 3),
           "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
           "frac": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12 / fp64_peak, 4),
@@ -384,7 +394,8 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": (f"{world} independent seeded instances, one per GPU "
                                    "(weak scaling, no data-path collective)")
                                   if world > 1 else "single GPU",
-                   "l2": "working set > 126 MB L2 (operators ~GBs), no flush needed"},
+                   "l2": "working set > 126 MB L2 (operators ~GBs), no flush needed",
+                   "lean": bool(q >= 12)},
         "e2e": {"value": round(whole_job_rate(N, world, e2e), 1), "unit": "fine-DOF/s",
                 "ms_per_step": round(e2e, 3), "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
@@ -452,6 +463,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if (args.q or CONFIGS[args.config]["q"]) >= 12:
+        # 16.8 M DOFs on one GPU: expandable allocator segments, and a third
+        # Krylov worker so queued levels release their psi^(k) sooner
+        os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+        os.environ.setdefault("GB_SPECTRAL_WORKERS", "3")
     if args.impl == "reference":
         out = run_reference(args, rank)
     else:

@@ -687,9 +687,13 @@ class _LevelTasks:
     def submit(self, level, op, k, g=None):
         ev = torch.cuda.Event()
         ev.record()
-        self.futures.append(self._pool.submit(self._run, level, op, k, g, ev))
+        # the increment psi^(k)T W^T w^(k) holds its own reference to psi^(k),
+        # so a lean transform may drop it from the level meanwhile
+        psi = level.raw("psi") if self.solver is not None else None
+        level._krylov_op = op  # the task's operator (a lean level drops B meanwhile)
+        self.futures.append(self._pool.submit(self._run, level, op, k, g, ev, psi))
 
-    def _run(self, level, op, k, g, ev):
+    def _run(self, level, op, k, g, ev, psi=None):
         st = self._stream()
         calls = 0
         with torch.cuda.stream(st):
@@ -706,35 +710,45 @@ class _LevelTasks:
                     box.update(out)
                     return out["x"], out["its"], out["rel"], out["conv"], out["brk"]
 
-                self.solver.subband(k, g, pipelined=True, engine=run_engine)
+                self.solver.subband(k, g, pipelined=True, engine=run_engine, psi=psi)
+                del psi
                 level.lambda_min_subband = box["lam_min"]
                 level.lambda_max_subband = box["lam_max"]
                 done = torch.cuda.Event()
                 done.record(st)
-                return box["calls"], op, done
+                info = (op.n, op.slots, op.spmv_bytes)
+                level._krylov_op = None
+                if getattr(level, "_lean", False) and not getattr(level, "_keep_op", False):
+                    level._op = None  # the operator copy is not retained
+                return box["calls"], info, done
             if SPECTRAL:
                 with dv.phase("spectral"):
                     lam_min, lam_max, calls = _eig_extremes(op)
                 level.lambda_min_subband = lam_min
                 level.lambda_max_subband = lam_max
             if self.solver is not None and g is not None:
-                self.solver.subband(k, g, pipelined=True)
+                self.solver.subband(k, g, pipelined=True, psi=psi)
+            del psi
             done = torch.cuda.Event()
             done.record(st)
-        return calls, op, done
+        info = (op.n, op.slots, op.spmv_bytes)
+        level._krylov_op = None
+        if getattr(level, "_lean", False):
+            level._op = None
+        return calls, info, done
 
     def join(self, counter):
         futs, self.futures = self.futures, []
         err = None
         for f in futs:
             try:
-                calls, op, done = f.result()
+                calls, (op_n, op_slots, op_bytes), done = f.result()
             except Exception as e:  # keep joining, re-raise the first error
                 err = err or e
                 continue
             torch.cuda.current_stream().wait_event(done)
-            counter.add("spectral", 2 * op.n * op.slots * calls)
-            dv.Prof.add_work("spectral", nbytes=calls * op.spmv_bytes)
+            counter.add("spectral", 2 * op_n * op_slots * calls)
+            dv.Prof.add_work("spectral", nbytes=calls * op_bytes)
         if err is not None:
             raise err
 
@@ -905,7 +919,7 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
 
 def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
                      counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None, _spool=None,
-                     _g=None):
+                     _g=None, _lean=False):
     """One localized downward step k -> k-1 (gamblet_fast.py:501-632).
     Mutates `level` (W, B, s_B, D, R, lambdas, repair) and returns level k-1."""
     k = level.k
@@ -943,6 +957,9 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
             nat.call("gb_box_scale", J, 3, wB, dv.ptr(Bv), dv.ptr(sB),
                      ctx.st(ctx.slot("scale", f"B^({k}),loc")), s)
         del bdiag
+        if _lean:  # A^(k) is consumed: the lean transform does not retain it
+            Ab = None
+            level.stiffness = None
         B = BoxMatrix(Bv, Lp, 3, wB, 3)
         counter.add("line7", 2 * J * dv.box_slots(wB, 3) * 16)
         counter.add("scaling", 2 * J * dv.box_slots(wB, 3) + J)
@@ -950,7 +967,12 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         # K7: spectral extremes of S B S (gamblet_fast.py:531-534)
         with dv.phase("level_blocks"):
             op = _POp(B, sB)
+            if _lean:  # preconditioner now, so the Krylov copy does not need B
+                op.bj_inv()
+                op._box = None
         level._op = op
+        level._lean = _lean
+        level._keep_op = k == q  # the finest operator stays for instrumentation
         level.subband = B
         level.subband_scale = sB
         level.w_variant = w_variant
@@ -1012,11 +1034,18 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
                          dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax), s)
             del Wpsi, rmax
             psin = PsiWindows(pv, n, Lp, lo2, hi2)
+            if _lean:  # psi^(k) lives on only in the level-k increment task
+                psiw = None
+                level.psi = None
             counter.add("line14", 2 * P * wd2 * wd2 * 3 * (2 * rho + 1) ** 2 // 4
                         + 2 * J * wdw * wdw * 4)
 
     level.null_w = (lambda tree=tree, k=k, v=w_variant: tree.null_basis(k, v))
-    level.correction = BoxMatrix(Dt, Lp, 1, rho, 3, kind=EXP_TDT)
+    if _lean:  # B^(k), D^(k,k-1) consumed; R kept until g^(k-1) = R g^(k)
+        level.subband = None
+        del Dt, B, Bv
+    else:
+        level.correction = BoxMatrix(Dt, Lp, 1, rho, 3, kind=EXP_TDT)
     level.restriction = BoxMatrix(Rv, Lp, 1, rho, 4, kind=EXP_CHILD)
     level._repair_slot_b = ib
     nxt = LocalGambletLevel(k - 1, psin, BoxMatrix(An, Lp, 1, wA2, 1))
@@ -1031,7 +1060,7 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
 
 
 def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
-                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None):
+                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None, _lean=False):
     """Load-independent phase, levels q..1 (gamblet_fast.py:635-674).
     Returns (levels, counter); all operators stay on the device."""
     counter = counter if counter is not None else FlopCounter()
@@ -1055,10 +1084,12 @@ def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_
         for k in range(q, 1, -1):
             level = local_level_step(level, tree, schedule, w_variant=w_variant, c_tol=c_tol,
                                      counter=counter, dense_cutoff=dense_cutoff, _ctx=ctx,
-                                     _spool=spool, _g=gk)
+                                     _spool=spool, _g=gk, _lean=_lean and _load is not None)
             levels[k - 1] = level
             if solver is not None:
                 gk = solver.restrict(k, gk)     # g^(k-1) = R^(k) g^(k), main stream
+                if _lean:
+                    levels[k].restriction = None
     finally:
         spool.join(counter)
     ctx.check()
@@ -1151,8 +1182,11 @@ class _LevelSolver:
                 f"level {k} was not produced by this package's fast_transform")
         return lvl, B, R
 
-    def subband(self, k, g, pipelined=False, engine=None):
-        lvl, B, _ = self._check(k, need_r=not pipelined)
+    def subband(self, k, g, pipelined=False, engine=None, psi=None):
+        lvl = self.levels[k]
+        op = getattr(lvl, "_krylov_op", None) if pipelined else None
+        if op is None:  # B^(k) must be on the level (a lean level hands its operator over)
+            lvl, B, _ = self._check(k, need_r=not pipelined)
         s = dv.stream()
         counter = self.counter
         sB = lvl.raw("subband_scale")
@@ -1161,8 +1195,9 @@ class _LevelSolver:
             st = dv.zeros(2, torch.int64)
             nat.call("gb_box_scale", B.rows, 3, B.w, dv.ptr(B.vals), dv.ptr(sB), dv.ptr(st), s)
         w12 = w_template(lvl.w_variant or "orthonormal").ctypes.data
-        Lp, J = B.L, B.rows
-        op = getattr(lvl, "_op", None) or _POp(B, sB)
+        if op is None:
+            op = getattr(lvl, "_op", None) or _POp(B, sB)
+        Lp, J = op.L, op.n
         rhs = dv.empty(J)
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
         counter.add("line8", 8 * J + J)
@@ -1179,26 +1214,30 @@ class _LevelSolver:
         if not conv:
             raise NumericalError(f"subband solve at level {k} did not converge")
         w = op.unpad(zp, sB)
-        counter.add("line8", cg_flops(J * B.slots, J, its) + 2 * J * its)
+        counter.add("line8", cg_flops(J * op.slots, J, its) + 2 * J * its)
         counter.record_iters("line8", its)
         counter.record_solve(f"line8 level {k}", its, self.tol)
         self.records.append(SolveRecord(k, "subband", J, 1, self.tol, np.array([its]),
                                         np.array([rel])))
         v = dv.empty(4 * Lp * Lp)
         nat.call("gb_apply_wt", Lp, w12, dv.ptr(w), dv.ptr(v), s)
-        psi = lvl.raw("psi")
+        if psi is None:
+            psi = lvl.raw("psi")
         if not isinstance(psi, PsiWindows):
             psi = _psi_dev(lvl, self.n, 2 * Lp)
         inc = dv.empty(self.N)
         nat.call("gb_psi_t_apply", self.n, 2 * Lp, psi.lo, psi.wd, dv.ptr(psi.vals),
                  dv.ptr(v), dv.ptr(inc), s)
+        psi.vals.record_stream(torch.cuda.current_stream())
         counter.add("line10", 8 * J + 2 * (4 * Lp * Lp) * psi.wd * psi.wd)
         self.incs[k] = inc
         self.coeffs[k] = w
 
     def restrict(self, k, g):
-        _, B, R = self._check(k)
-        Lp = B.L
+        R = self.levels[k].raw("restriction")
+        if not isinstance(R, BoxMatrix):
+            self._check(k)
+        Lp = R.L
         gn = dv.empty(Lp * Lp)
         nat.call("gb_apply_r", Lp, R.w, dv.ptr(R.vals), dv.ptr(g), dv.ptr(gn), dv.stream())
         self.counter.add("line15", 2 * Lp * Lp * R.slots)
@@ -1326,8 +1365,13 @@ def complexity_report(schedule, counter, levels):
 
 def fast_solve(M, A, load, tree, epsilon, c_rho=None, uniform_rho=None, schedule=None,
                w_variant="orthonormal", g_mode="nodal", c_tol=DEFAULT_C_TOL,
-               dense_cutoff=DENSE_PATCH_CUTOFF):
+               dense_cutoff=DENSE_PATCH_CUTOFF, lean=False):
     """Localized transform plus solve in one call (gamblet_fast.py:815-837).
+
+    lean (extension, default off): bound device memory for the largest grids
+    (q=12 on one GPU) -- identical arithmetic and solution, but the level
+    operators of k >= 2 are released once consumed and not returned (see
+    _fast_solve_device).
 
     With the nodal moment shortcut the solve phase is pipelined into the
     transform (level k's subband solve runs on a second stream as soon as
@@ -1348,7 +1392,8 @@ def fast_solve(M, A, load, tree, epsilon, c_rho=None, uniform_rho=None, schedule
             counter.add("line4", 0)
             levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
                                              c_tol=c_tol, counter=counter,
-                                             dense_cutoff=dense_cutoff, _load=(g, records))
+                                             dense_cutoff=dense_cutoff, _load=(g, records),
+                                             _lean=lean)
             parts, U1 = fast_transform.last_solve
             fast_transform.last_solve = None
             solution = MultiresSolution(u=dv.to_host(parts["partials"].device(q)),
@@ -1365,13 +1410,18 @@ def fast_solve(M, A, load, tree, epsilon, c_rho=None, uniform_rho=None, schedule
     return FastResult(solution, levels, schedule, counter)
 
 
-def _fast_solve_device(M, A, g, tree, schedule, w_variant="orthonormal"):
+def _fast_solve_device(M, A, g, tree, schedule, w_variant="orthonormal", lean=False):
     """fast_solve with device-resident inputs (DeviceCSR M, A; device g);
-    returns (levels, parts, U1, counter) with everything left in HBM."""
+    returns (levels, parts, U1, counter) with everything left in HBM.
+
+    lean=True bounds device memory for the largest grids (q=12 on one GPU):
+    the same arithmetic, but psi^(k) and A^(k) (k >= 2) are released once
+    consumed (psi^(k) after psi^(k-1) and the level-k increment, A^(k) after
+    B^(k), G, P A P^T), so the returned levels do not carry them."""
     counter = FlopCounter()
     records = []
     levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
-                                     counter=counter, _load=(g, records))
+                                     counter=counter, _load=(g, records), _lean=lean)
     parts, U1 = fast_transform.last_solve
     fast_transform.last_solve = None
     return levels, parts, U1, counter
