@@ -253,10 +253,11 @@ def run_ours(args, rank, world, local_rank):
 
     for i in range(args.warmup):
         step_device()
-        if i == 0:
+        if i == 0 and not lean:
             # grow the caching allocator once to the step's high-water mark
             # (+25% against fragmentation): later steps make no cudaMalloc,
-            # which would stall every stream of the level engine
+            # which would stall every stream of the level engine (the lean
+            # q >= 12 runs use expandable segments instead)
             dv.reserve(1.25 * torch.cuda.max_memory_allocated())
     torch.cuda.synchronize()
     barrier()
