@@ -1060,7 +1060,8 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
 
 
 def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
-                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None, _lean=False):
+                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None, _lean=False,
+                   _keep_below=0):
     """Load-independent phase, levels q..1 (gamblet_fast.py:635-674).
     Returns (levels, counter); all operators stay on the device."""
     counter = counter if counter is not None else FlopCounter()
@@ -1084,11 +1085,12 @@ def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_
         for k in range(q, 1, -1):
             level = local_level_step(level, tree, schedule, w_variant=w_variant, c_tol=c_tol,
                                      counter=counter, dense_cutoff=dense_cutoff, _ctx=ctx,
-                                     _spool=spool, _g=gk, _lean=_lean and _load is not None)
+                                     _spool=spool, _g=gk,
+                                     _lean=_lean and _load is not None and k > _keep_below)
             levels[k - 1] = level
             if solver is not None:
                 gk = solver.restrict(k, gk)     # g^(k-1) = R^(k) g^(k), main stream
-                if _lean:
+                if _lean and k > _keep_below:
                     levels[k].restriction = None
     finally:
         spool.join(counter)
@@ -1410,18 +1412,21 @@ def fast_solve(M, A, load, tree, epsilon, c_rho=None, uniform_rho=None, schedule
     return FastResult(solution, levels, schedule, counter)
 
 
-def _fast_solve_device(M, A, g, tree, schedule, w_variant="orthonormal", lean=False):
+def _fast_solve_device(M, A, g, tree, schedule, w_variant="orthonormal", lean=False,
+                       keep_below=0):
     """fast_solve with device-resident inputs (DeviceCSR M, A; device g);
     returns (levels, parts, U1, counter) with everything left in HBM.
 
     lean=True bounds device memory for the largest grids (q=12 on one GPU):
     the same arithmetic, but psi^(k) and A^(k) (k >= 2) are released once
     consumed (psi^(k) after psi^(k-1) and the level-k increment, A^(k) after
-    B^(k), G, P A P^T), so the returned levels do not carry them."""
+    B^(k), G, P A P^T), so the returned levels do not carry them; levels
+    k <= keep_below keep everything (per-level parity checks at q=12)."""
     counter = FlopCounter()
     records = []
     levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
-                                     counter=counter, _load=(g, records), _lean=lean)
+                                     counter=counter, _load=(g, records), _lean=lean,
+                                     _keep_below=keep_below)
     parts, U1 = fast_transform.last_solve
     fast_transform.last_solve = None
     return levels, parts, U1, counter

@@ -2,6 +2,7 @@
 oracle/make_goldens.py), cached problems built with the package's host-side
 input builders, and the CPU oracle."""
 
+import os
 import sys
 from pathlib import Path
 
@@ -10,6 +11,11 @@ import pytest
 import scipy.sparse as sp
 
 ROOT = Path(__file__).resolve().parents[1]
+
+# the q=12 test (tests/test_gpu_q12.py) needs the settings bench.py uses for
+# q >= 12; both must be in place before CUDA and the package initialize
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+os.environ.setdefault("GB_SPECTRAL_WORKERS", "3")
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
