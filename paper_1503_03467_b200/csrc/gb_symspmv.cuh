@@ -498,29 +498,33 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
         if (lane == 0) mbar_arrive(empty + st);
       }
       consumer_sync();
-      for (int idx = tid; idx < RG; idx += kSymThreads) {
-        const int rr = idx / RW, rem = idx - rr * RW;
-        const int cc = rem / 3 - w, c = rem % 3;
-        const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
+      // combine: region row rr outer (uniform warp-row range), the thread's
+      // column/component fixed, so no index division in the loop
+      if (tid < RW) {
+        const int cc = tid / 3 - w, c = tid - 3 * (tid / 3);
+        const int lc0 = cc + w, lc1 = cc - 32 + w;
+        const bool in0 = lc0 < AC, in1 = lc1 >= 0;
+        const bool own_col = cc >= 0 && cc < kSymTW;
+        for (int rr = 0; rr < kSymTH + w; ++rr) {
+          const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
+          const int idx = rr * RW + tid;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          if (v == 0 ? !live0 : !live1) continue;
-          const double* av = acc + v * NW * AREG;
-          double sm = 0.0;
-          for (int hh = h0; hh <= h1; ++hh) {
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              const int lc = cc - half * 32 + w;
-              if (lc >= 0 && lc < AC)
-                sm += av[(2 * hh + half) * AREG + ((rr - hh) * AC + lc) * 3 + c];
+          for (int v = 0; v < NV; ++v) {
+            if (v == 0 ? !live0 : !live1) continue;
+            const double* av = acc + v * NW * AREG;
+            double sm = 0.0;
+            for (int hh = h0; hh <= h1; ++hh) {
+              const int ro = ((rr - hh) * AC) * 3 + c;
+              if (in0) sm += av[(2 * hh) * AREG + ro + lc0 * 3];
+              if (in1) sm += av[(2 * hh + 1) * AREG + ro + lc1 * 3];
             }
+            double* y = v == 0 ? y0 : y1;
+            if (rr < kSymTH && own_col)
+              y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = sm;
+            else
+              y[npad + t * RG + idx] = sm;
+            if (v == 0 ? rd0 : rd1) dot[v] = fma(xs[v * XW + idx], sm, dot[v]);
           }
-          double* y = v == 0 ? y0 : y1;
-          if (rr < kSymTH && cc >= 0 && cc < kSymTW)
-            y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = sm;
-          else
-            y[npad + t * RG + idx] = sm;
-          if (v == 0 ? rd0 : rd1) dot[v] = fma(xs[v * XW + idx], sm, dot[v]);
         }
       }
       consumer_sync();
