@@ -232,6 +232,15 @@ int gb_csr_pow_solve(int64_t n, const int32_t* indptr, const int32_t* indices,
 struct gb_level_engine_args;
 int gb_level_engine(struct gb_level_engine_args* args, void* stream);
 
+/* host-only: lambda_min of the reference's inverse iteration
+ * (sparse_core.py:258-277, stopping test at `tol`) evaluated from m Lanczos
+ * coefficient pairs ab = (alpha_0, beta_0, ...) of the unit start vector --
+ * the level engine's spectral mode 1 (csrc/gb_lanczos.h).  Outputs the
+ * estimate, the outer iteration at which the reference would stop, and the
+ * extreme Ritz values.  Returns 0, 1 (QL failure), 2 (nonpositive Ritz value). */
+int gb_lanczos_emulate(const double* ab, int m, double tol, int max_outer, double* lam,
+                       int* outer, double* ritz_min, double* ritz_max);
+
 /* ---- K9 load-dependent transfers (gamblet_fast.py:726-765) --------------- */
 int gb_apply_w(int Lp, const double* host_w12, const double* g, const double* s,
                double* out, void* stream);

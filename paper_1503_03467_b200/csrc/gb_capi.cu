@@ -6,6 +6,7 @@
 
 #include "../../include/gamblets_b200.h"
 #include "gb_kernels.h"
+#include "gb_lanczos.h"
 
 int gbk_dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta,
                    const double* B, int ldb, int tb, double beta, double* C, int ldc,
@@ -44,7 +45,7 @@ static int invalid(const char* msg) {
 
 extern "C" {
 
-int gb_abi_version(void) { return 3; }
+int gb_abi_version(void) { return 4; }
 unsigned long long gb_launch_count(void) { return g_launches.load(); }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
@@ -378,6 +379,11 @@ int gb_level_engine(gb_level_engine_args* args, void* stream) {
   const int e = gbk_level_engine(args, ST(stream), &n);
   COUNT(n);
   return wrap(e, "level_engine");
+}
+int gb_lanczos_emulate(const double* ab, int m, double tol, int max_outer, double* lam,
+                       int* outer, double* ritz_min, double* ritz_max) {
+  if (!ab || m <= 0 || !lam || !outer) return 1;
+  return gb_lz::emulate_inverse_iteration(ab, m, tol, max_outer, lam, outer, ritz_min, ritz_max);
 }
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {

@@ -32,4 +32,13 @@ typedef struct gb_level_engine_args {
   double* cz;              /* PCG preconditioned residual of the inner solves */
   int layout;              /* 0: full box BsT, 1: symmetric band (gb_scale_box_symT);
                             * output vectors then carry gb_sym_overflow_elems tail */
+  /* spectral mode 1: lambda_min from the Lanczos moments of the start vector
+   * x2 (gb_lanczos.h) instead of inverse iteration; lz/hlz hold lz_cap
+   * (alpha, beta) pairs (device / pinned host), lz_tol = relative change of
+   * the emulated estimate between two checks at which the sequence stops */
+  int spectral_mode, lz_cap;
+  double* lz;
+  double* hlz;
+  double lz_tol;
+  int lz_its, lz_rc;
 } gb_level_engine_args;

@@ -321,6 +321,53 @@ __global__ void k_pow_scale(long long n, double* __restrict__ x, const double* _
   if (blockIdx.x == 0 && threadIdx.x == 0 && st->aux1 != 0.0) st->done = 1;
 }
 
+// Lanczos step after w = A v (power-mode apply: st->lam = v.w = alpha):
+// w <- w - alpha v - beta_prev vp, beta = |w|; (alpha, beta) appended to ab.
+// st->aux0 carries beta_prev (0 on the first step, vp may then be anything
+// finite); beta == 0 (invariant subspace) or it == max_iter ends the sequence.
+__global__ void k_lz_step(long long n, const double* __restrict__ v,
+                          const double* __restrict__ vp, double* __restrict__ w, KState* st,
+                          double* part, double* ab) {
+  __shared__ double sh[32];
+  if (st->done) return;
+  const double alpha = st->lam, bp = st->aux0;
+  double ww = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double u = w[i] - alpha * v[i] - bp * vp[i];
+    w[i] = u;
+    ww += u * u;
+  }
+  ww = block_sum(ww, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = ww;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      const double beta = sqrt(a);
+      ab[2 * st->it] = alpha;
+      ab[2 * st->it + 1] = beta;
+      st->it += 1;
+      st->aux0 = beta;
+      if (!(beta > 0.0) || st->it >= st->max_iter) st->done = 1;
+    }
+  }
+}
+
+// next Lanczos vector: vp <- w / beta (vp then becomes v on the host side)
+__global__ void k_lz_scale(long long n, double* __restrict__ vp, const double* __restrict__ w,
+                           const KState* st) {
+  if (st->done) return;
+  const double inv = 1.0 / st->aux0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    vp[i] = w[i] * inv;
+}
+
 // generic dot products: out[0] = a.b, out[1] = c.c  (c may be null)
 __global__ void k_dot2(long long n, const double* __restrict__ a, const double* __restrict__ b,
                        const double* __restrict__ c, double* out, KState* st,
@@ -2100,6 +2147,7 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
 // through k_dual_apply.  Host control flow mirrors sparse_core.py:232-278.
 // ---------------------------------------------------------------------------
 #include "gb_engine.h"
+#include "gb_lanczos.h"
 
 // ---- engine building blocks (count their launches into *nl) ----
 // dual pass: A (subband PCG, mode 0) and B (mode mb) on one sweep of S B S;
@@ -2186,6 +2234,8 @@ static void post_a(const gb_level_engine_args* e, cudaStream_t s, long long* nl)
 }
 
 static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl);
+static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl);
+static int inverse_iteration(gb_level_engine_args* e, cudaStream_t s, long long& nl);
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches) {
   long long nl = 0;
   const int rc = level_engine(e, s, nl);
@@ -2225,6 +2275,113 @@ static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl) 
   e->lam_max = hb->lam;
   e->power_its = hb->it;
   e->calls = hb->it + (hb->ynorm != 0.0 ? 0 : 1);
+  if (e->spectral_mode == 1) {
+    if ((err = lanczos_min(e, s, nl))) return err;
+  } else if ((err = inverse_iteration(e, s, nl))) {
+    return err;
+  }
+  if (e->breakdown) return 0;
+  // --- the PCG alone until it converges ---------------------------------
+  chunk = 8;
+  while (!ha->done) {
+    for (int i = 0; i < chunk; ++i) {
+      if ((err = launch_single(e, e->pa, e->apa, e->sta, e->parta, 0, 1, s, &nl))) return err;
+      post_a(e, s, &nl);
+    }
+    if ((err = (int)cudaGetLastError())) return err;
+    if ((err = read_state(e->sta, ha, s))) return err;
+    chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;
+  }
+  return 0;
+}
+
+// lambda_min by the Lanczos moments of the inverse-iteration start vector x2
+// (gb_lanczos.h): v_1 = x2 (unit), each step one operator pass -- paired with
+// the subband PCG while it runs -- then k_lz_step / k_lz_scale.  At every
+// chunk boundary the host evaluates the reference's inverse-iteration
+// sequence from T_m and stops once the estimate and its stopping index are
+// stable (or T_m is exact: beta = 0).
+static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
+  const int Lpad = e->L + 2 * e->w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  KState* ka = (KState*)e->sta;
+  KState* kb = (KState*)e->stb;
+  KState* ha = (KState*)e->hsta;
+  KState* hb = (KState*)e->hstb;
+  (void)ka;
+  int err;
+  double* v = e->x2;   // unit start vector (zero halo)
+  double* vp = e->xn;  // previous Lanczos vector, zero before step 1
+  double* w = e->yb;   // operator output (carries the symmetric layout's tail)
+  if ((err = (int)cudaMemsetAsync(vp, 0, sizeof(double) * npad, s))) return err;
+  k_state_reset<<<1, 1, 0, s>>>(kb, e->lz_cap);
+  nl += 1;
+  int chunk = 32;
+  double lam_prev = 0.0;
+  int outer_prev = -1;
+  e->lz_its = 0;
+  e->lz_rc = 0;
+  for (;;) {
+    const bool a_live = !ha->done;
+    for (int i = 0; i < chunk; ++i) {
+      if (a_live) {
+        if ((err = launch_dual(e, v, w, 1, 0, s, &nl))) return err;
+        post_a(e, s, &nl);
+      } else if ((err = launch_single(e, v, w, e->stb, e->partb, 1, 0, s, &nl))) {
+        return err;
+      }
+      k_lz_step<<<gv, 256, 0, s>>>(npad, v, vp, w, kb, e->partb, e->lz);
+      k_lz_scale<<<gv, 256, 0, s>>>(npad, vp, w, kb);
+      nl += 2;
+      double* t = v;
+      v = vp;
+      vp = t;
+    }
+    if ((err = (int)cudaGetLastError())) return err;
+    if ((err = read_state(e->sta, ha, s))) return err;
+    if ((err = read_state(e->stb, hb, s))) return err;
+    const int m = hb->it;
+    if (m > 0) {
+      if ((err = gbk_sync_read(e->lz, e->hlz, sizeof(double) * 2 * (size_t)m, s))) return err;
+      double lam;
+      int outer;
+      const int rc = gb_lz::emulate_inverse_iteration(e->hlz, m, e->tol, e->max_outer, &lam,
+                                                      &outer, nullptr, nullptr);
+      if (rc) {
+        e->lz_rc = rc;
+        e->breakdown = -2;
+        return 0;
+      }
+      e->lam_min = lam;
+      e->n_outer = outer;
+      e->lz_its = m;
+      const bool stable = outer == outer_prev && fabs(lam - lam_prev) <= e->lz_tol * fabs(lam);
+      lam_prev = lam;
+      outer_prev = outer;
+      if (hb->done || stable) break;
+    } else if (hb->done) {  // A v_1 = 0
+      e->breakdown = -1;
+      return 0;
+    }
+    // checks at most 64 steps apart: the stop lands within 64 of convergence
+    chunk = chunk * 2 < 64 ? chunk * 2 : 64;
+  }
+  e->calls += e->lz_its;
+  return 0;
+}
+
+// lambda_min by the reference's inverse iteration (sparse_core.py:258-277),
+// inner solves warm-started CG or block-Jacobi PCG, paired with the PCG
+static int inverse_iteration(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
+  const int Lpad = e->L + 2 * e->w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  KState* kb = (KState*)e->stb;
+  KState* ha = (KState*)e->hsta;
+  KState* hb = (KState*)e->hstb;
+  int err;
+  int chunk;
   // --- inverse iteration -------------------------------------------------
   double* cur = e->x2;     // right-hand side of the inner solve (unit vector)
   double* nxt = e->xn;     // next iterate
@@ -2302,17 +2459,6 @@ static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl) 
     have_prev = 1;
     if (fabs(lam - lam_prev) <= 0.5 * e->tol * fabs(lam)) break;
     lam_prev = lam;
-  }
-  // --- the PCG alone until it converges ---------------------------------
-  chunk = 8;
-  while (!ha->done) {
-    for (int i = 0; i < chunk; ++i) {
-      if ((err = launch_single(e, e->pa, e->apa, e->sta, e->parta, 0, 1, s, &nl))) return err;
-      post_a(e, s, &nl);
-    }
-    if ((err = (int)cudaGetLastError())) return err;
-    if ((err = read_state(e->sta, ha, s))) return err;
-    chunk = chunk * 2 < e->max_chunk ? chunk * 2 : e->max_chunk;
   }
   return 0;
 }

@@ -21,4 +21,6 @@ class LevelEngineArgs(ctypes.Structure):
         ("power_its", ctypes.c_int), ("n_outer", ctypes.c_int), ("breakdown", ctypes.c_int),
         ("inner_pcg", ctypes.c_int), ("inner_its", ctypes.c_int * 64),
         ("cz", _P), ("layout", ctypes.c_int),
+        ("spectral_mode", ctypes.c_int), ("lz_cap", ctypes.c_int), ("lz", _P), ("hlz", _P),
+        ("lz_tol", _D), ("lz_its", ctypes.c_int), ("lz_rc", ctypes.c_int),
     ]

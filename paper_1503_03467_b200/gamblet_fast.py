@@ -542,7 +542,7 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
     dots = dv.empty(4)
     outer = []
     for _ in range(max_iter):
-        if SPECTRAL_INNER == "pcg":  # warm start y_prev / lambda (see gb_level_engine)
+        if SPECTRAL_INNER != "cg":  # warm start y_prev / lambda (see gb_level_engine)
             yv, its, _, _, brk, _ = _pcg(op, x, inner, x0=y_prev, kr=ykr,
                                          x0_scale=1.0 / lam_min if y_prev is not None else 1.0)
         else:
@@ -624,16 +624,34 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
         partb=dv.ptr(kb.part), hstb=kb.host.data_ptr(), dots=dv.ptr(dots),
         hdots=kb.hdots.data_ptr(), tol=tol, inner_tol=max(1e-12, 1e-3 * tol),
         inner_max_iter=min(max(200, 2 * n), MAX_ITER_CAP),
-        inner_pcg=int(SPECTRAL_INNER == "pcg"), cz=dv.ptr(cz), layout=op.layout)
+        inner_pcg=int(SPECTRAL_INNER != "cg"), cz=dv.ptr(cz), layout=op.layout)
+    if SPECTRAL_INNER == "lanczos":
+        cap = int(min(n, LANCZOS_CAP))
+        lz = dv.empty(2 * cap)
+        hlz = torch.empty(2 * cap, dtype=torch.float64, pin_memory=True)
+        args.spectral_mode = 1
+        args.lz_cap = cap
+        args.lz = dv.ptr(lz)
+        args.hlz = hlz.data_ptr()
+        args.lz_tol = LANCZOS_TOL
     nat.call("gb_level_engine", nat.ctypes.byref(args), st)
+    if args.breakdown == -2:
+        raise NumericalError(f"Lanczos moments of S B S at n={n}: "
+                             + ("nonpositive Ritz value (matrix is not SPD)" if args.lz_rc == 2
+                                else "tridiagonal eigensolver failed"))
     if args.breakdown > 0:
         raise NumericalError(f"CG breakdown at iteration {args.breakdown}: p^T A p <= 0 "
                              "(matrix is not SPD)")
     if args.breakdown < 0:
         raise NumericalError("inverse iteration broke down: A^{-1} x = 0")
     h = ka.host_view()
-    _SPECTRAL_LOG.append({"n": n, "power": int(args.power_its),
-                          "inner": [int(args.inner_its[i]) for i in range(min(args.n_outer, 64))]})
+    if args.spectral_mode == 1:
+        _SPECTRAL_LOG.append({"n": n, "power": int(args.power_its), "outer": int(args.n_outer),
+                              "lanczos": int(args.lz_its)})
+    else:
+        _SPECTRAL_LOG.append({"n": n, "power": int(args.power_its),
+                              "inner": [int(args.inner_its[i])
+                                        for i in range(min(args.n_outer, 64))]})
     rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
     return {"x": xa, "its": int(h["it"]), "rel": rel, "conv": bool(h["converged"]),
             "brk": int(h["breakdown"]), "lam_min": float(args.lam_min),
@@ -654,7 +672,18 @@ MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
 # the subband preconditioner) or "cg" (the reference's unpreconditioned CG).
 # lambda_min feeds only the reported conditioning (tight mode has no cheap
 # copy), and both stop at the same relative residual.
-SPECTRAL_INNER = __import__("os").environ.get("GB_SPECTRAL_INNER", "pcg")
+#
+# "lanczos" (default): on the levels the paired engine covers, lambda_min is
+# the reference's inverse-iteration sequence evaluated from the Lanczos
+# moments of its start vector (csrc/gb_lanczos.h) -- the iteration with exact
+# inner solves, same stopping test; the Lanczos passes ride on the subband
+# PCG's operator passes.  Smaller levels run the inverse iteration with PCG.
+SPECTRAL_INNER = __import__("os").environ.get("GB_SPECTRAL_INNER", "lanczos")
+LANCZOS_CAP = int(__import__("os").environ.get("GB_LANCZOS_CAP", "4096"))
+# relative change of the emulated lambda_min between two engine checks (32-64
+# Lanczos steps apart) below which the sequence stops; the reference's own
+# inner solves (rel_tol 1e-4) move its estimate by more than this
+LANCZOS_TOL = float(__import__("os").environ.get("GB_LANCZOS_TOL", "1e-6"))
 
 
 class _LevelTasks:

@@ -8,6 +8,7 @@ from pathlib import Path
 
 import numpy as np
 import pytest
+import scipy.sparse as sp
 
 import paper_1503_03467_b200 as gb
 from oracle import gamblets_oracle as O
@@ -152,4 +153,73 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.EXPORTED)
-    assert lib.gb_abi_version() == 3
+    assert lib.gb_abi_version() == 4
+
+
+def _lanczos_ab(A, v0, m):
+    """m plain Lanczos steps (no reorthogonalization, as on the GPU)."""
+    v = v0 / np.linalg.norm(v0)
+    vp = np.zeros_like(v)
+    beta = 0.0
+    ab = []
+    for _ in range(m):
+        w = A @ v - beta * vp
+        alpha = float(v @ w)
+        w -= alpha * v
+        beta = float(np.linalg.norm(w))
+        ab += [alpha, beta]
+        vp, v = v, w / beta
+    return np.array(ab)
+
+
+def _emulate(ab, tol=0.1, max_outer=500):
+    from paper_1503_03467_b200 import _native
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    lam, rmin, rmax = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    outer = ctypes.c_int()
+    buf = np.ascontiguousarray(ab, dtype=np.float64)
+    rc = lib.gb_lanczos_emulate(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(len(ab) // 2),
+                                ctypes.c_double(tol), ctypes.c_int(max_outer), ctypes.byref(lam),
+                                ctypes.byref(outer), ctypes.byref(rmin), ctypes.byref(rmax))
+    return rc, lam.value, outer.value, rmin.value, rmax.value
+
+
+@pytest.mark.parametrize("n,cond", [(60, 50.0), (300, 3e3)])
+def test_lanczos_emulation_reproduces_inverse_iteration(n, cond):
+    """Level engine spectral mode 1 (csrc/gb_lanczos.h): the inverse-iteration
+    sequence of sparse_core.py:258-277 evaluated from the Lanczos moments of
+    its start vector equals the iteration run with exact solves -- estimate
+    and stopping index -- and matches the reference restatement (inner CG at
+    1e-4) to its inner tolerance."""
+    rng = np.random.default_rng(7)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    ev = np.geomspace(1.0 / cond, 1.0, n) * (1 + 0.01 * rng.standard_normal(n))
+    A = (Q * ev) @ Q.T
+    A = 0.5 * (A + A.T)
+    x1, x2 = O.start_vectors(n)
+    # the reference's iteration with exact inner solves
+    x = x2 / np.linalg.norm(x2)
+    lam_prev, outer_exact = np.inf, None
+    for j in range(1, 501):
+        y = np.linalg.solve(A, x)
+        x = y / np.linalg.norm(y)
+        lam = float(x @ (A @ x))
+        if abs(lam - lam_prev) <= 0.05 * abs(lam):
+            outer_exact = j
+            break
+        lam_prev = lam
+    rc, lz, outer, rmin, rmax = _emulate(_lanczos_ab(A, x2, 2 * n))
+    assert rc == 0
+    assert outer == outer_exact
+    assert abs(lz - lam) <= 1e-9 * lam
+    assert abs(rmin - ev.min()) <= 1e-3 * ev.min() and abs(rmax - ev.max()) <= 1e-6
+    lam_ref, _ = O.eig_extremes(sp.csr_array(A), tol=0.1)
+    assert abs(lz - lam_ref) <= 1e-3 * lam_ref
+
+
+def test_lanczos_emulation_flags_indefinite_operator():
+    A = np.diag([-1.0, 1.0, 2.0, 3.0])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ab = _lanczos_ab(A, np.ones(4), 4)
+    rc = _emulate(ab)[0]
+    assert rc == 2
