@@ -60,6 +60,19 @@ int gb_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,
 int gb_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
                   const double* data, double* box, int64_t* status, void* stream);
 
+/* ---- on-device Q1 assembly (replaces grid_fem.py:189-227 _assemble /
+ * assemble_mass / assemble_stiffness and the b = M g of assemble_load,
+ * grid_fem.py:238-245) ---------------------------------------------------
+ * box: n*n rows x 9 slots (half-width-1 box, slot (ds+1)*3 + (dt+1)); entry =
+ * sum over the adjacent cells in increasing flat cell order of
+ * scale[cell] * E[r][c] (cell_scale == NULL: const_scale for every cell),
+ * host_e16 = the 4x4 element matrix (corners SW, SE, NE, NW), row major.
+ * Bitwise equal to the reference's canonical CSR values. */
+int gb_assemble_q1(int n, const double* cell_scale, double const_scale, const double* host_e16,
+                   double* box, void* stream);
+/* b = M g for a half-width-1 box in scipy csr_matvec order (bitwise) */
+int gb_box1_matvec(int n, const double* box, const double* g, double* b, void* stream);
+
 /* ---- unit-diagonal congruence s = diag^-1/2 (gamblet_fast.py:123-139) ---- */
 int gb_box_scale(int64_t rows, int nr, int w, const double* box, double* s,
                  int64_t* status, void* stream);

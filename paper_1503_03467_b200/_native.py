@@ -84,6 +84,8 @@ _SIGS = {
     "gb_csr_cg_solve": ([_L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
     "gb_csr_pow_solve": ([_L, _P, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
     "gb_level_engine": ([_P, _P], _I),
+    "gb_assemble_q1": ([_I, _P, _D, _P, _P, _P], _I),
+    "gb_box1_matvec": ([_I, _P, _P, _P, _P], _I),
     "gb_lanczos_emulate": ([_P, _I, _D, _I, _P, _P, _P, _P], _I),
     "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),

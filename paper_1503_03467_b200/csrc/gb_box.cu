@@ -8,6 +8,79 @@
 namespace gb {
 
 // ---------------------------------------------------------------------------
+// On-device Q1 assembly (grid_fem.py:189-227) straight into the box layout
+// (half-width 1, slot (ds+1)*3 + (dt+1)).  The reference scatters the
+// element matrices cell by cell into COO and canonicalizes; each entry is the
+// sum of its cells' scale*E[r][c] in increasing flat cell order (checked
+// bitwise against scipy's canonical CSR).  Products and sums are explicitly
+// rounded (no FMA contraction) to reproduce the host arithmetic.
+// ---------------------------------------------------------------------------
+struct Elem16 {
+  double e[16];
+};
+
+__global__ void k_assemble_q1(int n, const double* __restrict__ cell_scale, double const_scale,
+                              Elem16 E, double* __restrict__ box) {
+  const long long N = (long long)n * n;
+  const int m = n + 1;
+  // corner k of cell (ci, cj) is node (ci + di[k], cj + dj[k]): SW, SE, NE, NW
+  const int di[4] = {0, 1, 1, 0}, dj[4] = {0, 0, 1, 1};
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < N;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int I = (int)(r / n) + 1, J = (int)(r % n) + 1;
+    double acc[9];
+    bool any[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      acc[k] = 0.0;
+      any[k] = false;
+    }
+    // the four cells around node (I, J) in increasing flat order
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const int ci = I - 1 + (cc >> 1), cj = J - 1 + (cc & 1);
+      const double sc = cell_scale ? cell_scale[(long long)ci * m + cj] : const_scale;
+      int rl = 0;  // local corner of (I, J)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ci + di[k] == I && cj + dj[k] == J) rl = k;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int I2 = ci + di[k], J2 = cj + dj[k];
+        if (I2 < 1 || I2 > n || J2 < 1 || J2 > n) continue;  // boundary elimination
+        const int slot = (I2 - I + 1) * 3 + (J2 - J + 1);
+        const double v = __dmul_rn(sc, E.e[rl * 4 + k]);
+        acc[slot] = any[slot] ? __dadd_rn(acc[slot], v) : v;
+        any[slot] = true;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) box[r * 9 + k] = acc[k];
+  }
+}
+
+// b = M g on the half-width-1 box in scipy's csr_matvec order (sorted
+// columns = slot order, sum from 0, no FMA)
+__global__ void k_box1_matvec(int n, const double* __restrict__ box,
+                              const double* __restrict__ g, double* __restrict__ b) {
+  const long long N = (long long)n * n;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < N;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int s0 = (int)(r / n), t0 = (int)(r % n);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int s1 = s0 + k / 3 - 1, t1 = t0 + k % 3 - 1;
+      if (s1 < 0 || s1 >= n || t1 < 0 || t1 >= n) continue;
+      const double v = box[r * 9 + k];
+      if (v == 0.0) continue;  // not stored in the canonical CSR
+      acc = __dadd_rn(acc, __dmul_rn(v, g[(long long)s1 * n + t1]));
+    }
+    b[r] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CSR (fine grid, side n) -> box of half-width w
 // ---------------------------------------------------------------------------
 __global__ void k_csr_halfwidth(int n, const int32_t* __restrict__ indptr,
@@ -284,6 +357,21 @@ static inline int grid_for(long long work, int block, int cap = 148 * 64) {
   if (g < 1) g = 1;
   if (g > cap) g = cap;
   return (int)g;
+}
+
+int gbk_assemble_q1(int n, const double* cell_scale, double const_scale, const double* host_e16,
+                    double* box, cudaStream_t s) {
+  Elem16 E;
+  for (int i = 0; i < 16; ++i) E.e[i] = host_e16[i];
+  const long long N = (long long)n * n;
+  k_assemble_q1<<<grid_for(N, 256), 256, 0, s>>>(n, cell_scale, const_scale, E, box);
+  return (int)cudaGetLastError();
+}
+
+int gbk_box1_matvec(int n, const double* box, const double* g, double* b, cudaStream_t s) {
+  const long long N = (long long)n * n;
+  k_box1_matvec<<<grid_for(N, 256), 256, 0, s>>>(n, box, g, b);
+  return (int)cudaGetLastError();
 }
 
 int gbk_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,

@@ -60,6 +60,18 @@ int gb_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,
   COUNT(1);
   return wrap(gbk_csr_halfwidth(n, indptr, indices, out_w, ST(stream)), "csr_halfwidth");
 }
+int gb_assemble_q1(int n, const double* cell_scale, double const_scale, const double* host_e16,
+                   double* box, void* stream) {
+  if (n <= 0 || !host_e16 || !box) return invalid("assemble_q1: bad arguments");
+  COUNT(1);
+  return wrap(gbk_assemble_q1(n, cell_scale, const_scale, host_e16, box, ST(stream)),
+              "assemble_q1");
+}
+int gb_box1_matvec(int n, const double* box, const double* g, double* b, void* stream) {
+  if (n <= 0) return invalid("box1_matvec: n <= 0");
+  COUNT(1);
+  return wrap(gbk_box1_matvec(n, box, g, b, ST(stream)), "box1_matvec");
+}
 int gb_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
                   const double* data, double* box, int64_t* status, void* stream) {
   if (n <= 0 || w < 0) return invalid("csr_to_box: bad geometry");

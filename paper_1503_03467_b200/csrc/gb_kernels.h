@@ -8,6 +8,9 @@
 enum { EXP_SQUARE = 0, EXP_CHILD = 1, EXP_PSI = 2, EXP_TDT = 3 };
 
 // gb_box.cu
+int gbk_assemble_q1(int n, const double* cell_scale, double const_scale, const double* host_e16,
+                    double* box, cudaStream_t s);
+int gbk_box1_matvec(int n, const double* box, const double* g, double* b, cudaStream_t s);
 int gbk_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices, int* out,
                       cudaStream_t s);
 int gbk_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,

@@ -221,6 +221,10 @@ class BoxMatrix(_Exportable):
         return self.L * self.L * self.nr
 
     @property
+    def shape(self):
+        return self._export_args()[-1]
+
+    @property
     def slots(self):
         return box_slots(self.w, self.nc)
 
@@ -295,3 +299,33 @@ def csr_to_psi(mat, n, L):
     buf = np.zeros((L * L, wd, wd))
     buf[rows, fs - os_, ft - ot_] = mat.data
     return PsiWindows(to_dev(buf.ravel()), n, L, lo, hi)
+
+
+def assemble_q1(n, cell_scale, const_scale, element):
+    """On-device Q1 assembly (grid_fem.py:205-214) into the half-width-1 box:
+    bitwise the reference's canonical CSR values (csrc gb_assemble_q1).
+    cell_scale: (n+1)^2 per-cell factors (host array or device tensor) or
+    None for const_scale everywhere."""
+    s = stream()
+    e16 = np.ascontiguousarray(np.asarray(element, dtype=np.float64).reshape(16))
+    cs = None
+    if cell_scale is not None:
+        cs = cell_scale if isinstance(cell_scale, torch.Tensor) else to_dev(
+            np.ascontiguousarray(cell_scale, dtype=np.float64))
+        if cs.numel() != (n + 1) * (n + 1):
+            raise InvalidArgumentError(f"expected {(n + 1) ** 2} cell values, got {cs.numel()}")
+    box = empty(n * n * 9)
+    nat.call("gb_assemble_q1", n, None if cs is None else ptr(cs), float(const_scale),
+             e16.ctypes.data, ptr(box), s)
+    if cs is not None:
+        cs.record_stream(torch.cuda.current_stream())
+    return BoxMatrix(box, n, 1, 1, 1)
+
+
+def box1_matvec(M, g):
+    """b = M g for a half-width-1 BoxMatrix, scipy csr_matvec order (bitwise)."""
+    s = stream()
+    gd = g if isinstance(g, torch.Tensor) else to_dev(np.ascontiguousarray(g, dtype=np.float64))
+    b = empty(M.L * M.L)
+    nat.call("gb_box1_matvec", M.L, ptr(M.vals), ptr(gd), ptr(b), s)
+    return b, gd

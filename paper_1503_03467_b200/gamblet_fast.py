@@ -787,7 +787,7 @@ class _LevelTasks:
 # ---------------------------------------------------------------------------
 
 def _canon(mat):
-    if isinstance(mat, dv.DeviceCSR) or is_canonical_csr(mat):
+    if isinstance(mat, (dv.DeviceCSR, BoxMatrix)) or is_canonical_csr(mat):
         return mat
     return as_csr(mat)
 
@@ -823,7 +823,8 @@ def _level_q(M, A, tree, rho, ctx, counter):
     if A.shape != (N, N):
         raise InvalidArgumentError(f"stiffness shape {A.shape} does not match q={q}")
     with dv.phase("input_to_box"):
-        Mb, _ = dv.csr_to_box(_canon(M), n)
+        # device-assembled inputs (grid_fem.assemble_*(device=True)) are boxes
+        Mb = M if isinstance(M, BoxMatrix) else dv.csr_to_box(_canon(M), n)[0]
     sM = dv.empty(N)
     nat.call("gb_box_scale", N, 1, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM),
              ctx.st(ctx.slot("scale", "mass")), s)
@@ -838,7 +839,7 @@ def _level_q(M, A, tree, rho, ctx, counter):
     # the stiffness is needed only after the mass patches: a host-resident A
     # is uploaded on a copy stream while they run
     A = _canon(A)
-    if not isinstance(A, dv.DeviceCSR):
+    if not isinstance(A, (dv.DeviceCSR, BoxMatrix)):
         cs = _copy_stream()
         with torch.cuda.stream(cs):
             A = dv.DeviceCSR.from_scipy(A)
@@ -847,7 +848,7 @@ def _level_q(M, A, tree, rho, ctx, counter):
         torch.cuda.current_stream().wait_event(ev)
         for t in (A.indptr, A.indices, A.data):
             t.record_stream(torch.cuda.current_stream())
-    Ab, _ = dv.csr_to_box(A, n)
+    Ab = A if isinstance(A, BoxMatrix) else dv.csr_to_box(A, n)[0]
     wX = min(rho + Ab.w, n - 1)
     X = dv.empty(N * dv.box_slots(wX, 1))
     wR = min(wX + rho, n - 1)
