@@ -321,26 +321,31 @@ __global__ void k_pow_scale(long long n, double* __restrict__ x, const double* _
   if (blockIdx.x == 0 && threadIdx.x == 0 && st->aux1 != 0.0) st->done = 1;
 }
 
-// Lanczos step after w = A v (power-mode apply: st->lam = v.w = alpha):
-// w <- w - alpha v - beta_prev vp, beta = |w|; (alpha, beta) appended to ab.
-// st->aux0 carries beta_prev (0 on the first step, vp may then be anything
-// finite); beta == 0 (invariant subspace) or it == max_iter ends the sequence.
-__global__ void k_lz_step(long long n, const double* __restrict__ v,
-                          const double* __restrict__ vp, double* __restrict__ w, KState* st,
-                          double* part, double* ab) {
+// Lanczos step on an unnormalized iterate (one launch per step): x = u_j
+// with |u_j| = beta_{j-1} = st->aux0 (x = v_1, aux0 = 1 on the first step),
+// y = A x from a power-mode apply (st->lam = x.y).  With v_j = x / beta_{j-1}:
+// alpha_j = x.y / beta_{j-1}^2, u_{j+1} = (y - alpha_j x) / beta_{j-1} -
+// beta_{j-1} v_{j-1}; vp <- v_j, y <- u_{j+1} (the next operator input),
+// beta_j = |u_{j+1}|; (alpha_j, beta_j) appended to ab.  beta_j == 0
+// (invariant subspace) or it == max_iter ends the sequence.
+__global__ void k_lz_step(long long n, const double* __restrict__ x, double* __restrict__ vp,
+                          double* __restrict__ y, KState* st, double* part, double* ab) {
   __shared__ double sh[32];
   if (st->done) return;
-  const double alpha = st->lam, bp = st->aux0;
-  double ww = 0.0;
+  const double bp = st->aux0, ibp = 1.0 / bp;
+  const double alpha = st->lam * ibp * ibp;
+  double uu = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const double u = w[i] - alpha * v[i] - bp * vp[i];
-    w[i] = u;
-    ww += u * u;
+    const double v = x[i] * ibp;
+    const double u = (y[i] - alpha * x[i]) * ibp - bp * vp[i];
+    vp[i] = v;
+    y[i] = u;
+    uu += u * u;
   }
-  ww = block_sum(ww, sh);
+  uu = block_sum(uu, sh);
   if (threadIdx.x == 0) {
-    part[2 * blockIdx.x] = ww;
+    part[2 * blockIdx.x] = uu;
     part[2 * blockIdx.x + 1] = 0.0;
   }
   if (last_block(&st->counter)) {
@@ -358,15 +363,7 @@ __global__ void k_lz_step(long long n, const double* __restrict__ v,
   }
 }
 
-// next Lanczos vector: vp <- w / beta (vp then becomes v on the host side)
-__global__ void k_lz_scale(long long n, double* __restrict__ vp, const double* __restrict__ w,
-                           const KState* st) {
-  if (st->done) return;
-  const double inv = 1.0 / st->aux0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    vp[i] = w[i] * inv;
-}
+__global__ void k_lz_init(KState* st) { st->aux0 = 1.0; }
 
 // generic dot products: out[0] = a.b, out[1] = c.c  (c may be null)
 __global__ void k_dot2(long long n, const double* __restrict__ a, const double* __restrict__ b,
@@ -2297,7 +2294,7 @@ static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl) 
 
 // lambda_min by the Lanczos moments of the inverse-iteration start vector x2
 // (gb_lanczos.h): v_1 = x2 (unit), each step one operator pass -- paired with
-// the subband PCG while it runs -- then k_lz_step / k_lz_scale.  At every
+// the subband PCG while it runs -- then k_lz_step.  At every
 // chunk boundary the host evaluates the reference's inverse-iteration
 // sequence from T_m and stops once the estimate and its stopping index are
 // stable (or T_m is exact: beta = 0).
@@ -2311,12 +2308,19 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
   KState* hb = (KState*)e->hstb;
   (void)ka;
   int err;
-  double* v = e->x2;   // unit start vector (zero halo)
-  double* vp = e->xn;  // previous Lanczos vector, zero before step 1
-  double* w = e->yb;   // operator output (carries the symmetric layout's tail)
+  // x: operator input u_j (unnormalized), w: operator output, vp: v_{j-1}.
+  // x starts as the unit start vector; after each step the new u_{j+1} sits
+  // in w and the two swap.  Both carry the symmetric layout's output tail.
+  if ((err = (int)cudaMemcpyAsync(e->cx, e->x2, sizeof(double) * npad,
+                                  cudaMemcpyDeviceToDevice, s)))
+    return err;
+  double* v = e->cx;
+  double* vp = e->xn;  // zero before step 1
+  double* w = e->yb;
   if ((err = (int)cudaMemsetAsync(vp, 0, sizeof(double) * npad, s))) return err;
   k_state_reset<<<1, 1, 0, s>>>(kb, e->lz_cap);
-  nl += 1;
+  k_lz_init<<<1, 1, 0, s>>>(kb);
+  nl += 2;
   int chunk = 32;
   double lam_prev = 0.0;
   int outer_prev = -1;
@@ -2332,11 +2336,10 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
         return err;
       }
       k_lz_step<<<gv, 256, 0, s>>>(npad, v, vp, w, kb, e->partb, e->lz);
-      k_lz_scale<<<gv, 256, 0, s>>>(npad, vp, w, kb);
-      nl += 2;
+      nl += 1;
       double* t = v;
-      v = vp;
-      vp = t;
+      v = w;
+      w = t;
     }
     if ((err = (int)cudaGetLastError())) return err;
     if ((err = read_state(e->sta, ha, s))) return err;

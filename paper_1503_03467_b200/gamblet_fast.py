@@ -683,7 +683,7 @@ LANCZOS_CAP = int(__import__("os").environ.get("GB_LANCZOS_CAP", "4096"))
 # relative change of the emulated lambda_min between two engine checks (32-64
 # Lanczos steps apart) below which the sequence stops; the reference's own
 # inner solves (rel_tol 1e-4) move its estimate by more than this
-LANCZOS_TOL = float(__import__("os").environ.get("GB_LANCZOS_TOL", "1e-6"))
+LANCZOS_TOL = float(__import__("os").environ.get("GB_LANCZOS_TOL", "1e-5"))
 
 
 class _LevelTasks:
