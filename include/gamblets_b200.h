@@ -254,6 +254,30 @@ int gb_level_engine(struct gb_level_engine_args* args, void* stream);
 int gb_lanczos_emulate(const double* ab, int m, double tol, int max_outer, double* lam,
                        int* outer, double* ritz_min, double* ritz_max);
 
+/* ---- diagnostics on the device (replaces diagnostics.py:40-155) --------
+ * cell energies a_c * v_c^T E v_c of a fine vector (diagnostics.py:40-49);
+ * decay sums: out[j] = sum of energies of the cells whose centre lies at
+ * distance >= radii[j] from (cx, cy), out[nr] = total (diagnostics.py:58-74),
+ * part = gb_decay_part_elems(nr) doubles; |coef_r| sqrt(diag_r) of a square
+ * box (coefficient_spectrum, diagnostics.py:97-107); stable top-n_keep mask
+ * of mags (compress, diagnostics.py:110-142; work NULL = size query);
+ * x^T A x on a square half-width-w box (energy_norm, grid_fem.py:248-257),
+ * part = gb_quad_part_elems() doubles. */
+int gb_cell_energies(int n, const double* v, const double* coef, const double* host_e16,
+                     double* out, void* stream);
+size_t gb_decay_part_elems(int nr);
+int gb_decay_sums(int n, double h, const double* energies, double cx, double cy,
+                  const double* radii, int nr, double* part, double* out, void* stream);
+int gb_box_diag_spectrum(int64_t rows, int nr, int w, const double* box, const double* coef,
+                         double* out, void* stream);
+int gb_topk_mask(int64_t n, const double* mags, int64_t n_keep, double* mask, void* work,
+                 size_t* work_bytes, void* stream);
+size_t gb_quad_part_elems(void);
+int gb_box_quadform(int L, int w, const double* box, const double* x, double* part, double* out,
+                    void* stream);
+/* max_i |x_i| (part = gb_quad_part_elems() doubles) */
+int gb_max_abs(int64_t n, const double* x, double* part, double* out, void* stream);
+
 /* ---- K9 load-dependent transfers (gamblet_fast.py:726-765) --------------- */
 int gb_apply_w(int Lp, const double* host_w12, const double* g, const double* s,
                double* out, void* stream);

@@ -84,6 +84,14 @@ _SIGS = {
     "gb_csr_cg_solve": ([_L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
     "gb_csr_pow_solve": ([_L, _P, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
     "gb_level_engine": ([_P, _P], _I),
+    "gb_cell_energies": ([_I, _P, _P, _P, _P, _P], _I),
+    "gb_decay_part_elems": ([_I], _Z),
+    "gb_decay_sums": ([_I, _D, _P, _D, _D, _P, _I, _P, _P, _P], _I),
+    "gb_box_diag_spectrum": ([_L, _I, _I, _P, _P, _P, _P], _I),
+    "gb_topk_mask": ([_L, _P, _L, _P, _P, _P, _P], _I),
+    "gb_quad_part_elems": ([], _Z),
+    "gb_box_quadform": ([_I, _I, _P, _P, _P, _P, _P], _I),
+    "gb_max_abs": ([_L, _P, _P, _P, _P], _I),
     "gb_assemble_q1": ([_I, _P, _D, _P, _P, _P], _I),
     "gb_box1_matvec": ([_I, _P, _P, _P, _P], _I),
     "gb_lanczos_emulate": ([_P, _I, _D, _I, _P, _P, _P, _P], _I),

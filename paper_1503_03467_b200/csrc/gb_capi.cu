@@ -397,6 +397,45 @@ int gb_lanczos_emulate(const double* ab, int m, double tol, int max_outer, doubl
   if (!ab || m <= 0 || !lam || !outer) return 1;
   return gb_lz::emulate_inverse_iteration(ab, m, tol, max_outer, lam, outer, ritz_min, ritz_max);
 }
+int gb_cell_energies(int n, const double* v, const double* coef, const double* host_e16,
+                     double* out, void* stream) {
+  if (n <= 0 || !host_e16) return invalid("cell_energies: bad arguments");
+  COUNT(1);
+  return wrap(gbk_cell_energies(n, v, coef, host_e16, out, ST(stream)), "cell_energies");
+}
+size_t gb_decay_part_elems(int nr) { return gbk_decay_part_elems(nr); }
+int gb_decay_sums(int n, double h, const double* energies, double cx, double cy,
+                  const double* radii, int nr, double* part, double* out, void* stream) {
+  if (n <= 0 || nr < 0) return invalid("decay_sums: bad arguments");
+  COUNT(2);
+  return wrap(gbk_decay_sums(n, h, energies, cx, cy, radii, nr, part, out, ST(stream)),
+              "decay_sums");
+}
+int gb_box_diag_spectrum(int64_t rows, int nr, int w, const double* box, const double* coef,
+                         double* out, void* stream) {
+  if (rows < 0 || nr <= 0 || w < 0) return invalid("box_diag_spectrum: bad geometry");
+  COUNT(1);
+  return wrap(gbk_box_diag_spectrum(rows, nr, w, box, coef, out, ST(stream)),
+              "box_diag_spectrum");
+}
+int gb_topk_mask(int64_t n, const double* mags, int64_t n_keep, double* mask, void* work,
+                 size_t* work_bytes, void* stream) {
+  if (n <= 0 || n_keep < 0 || !work_bytes) return invalid("topk_mask: bad arguments");
+  if (work) COUNT(3);
+  return wrap(gbk_topk_mask(n, mags, n_keep, mask, work, work_bytes, ST(stream)), "topk_mask");
+}
+size_t gb_quad_part_elems(void) { return gbk_quad_part_elems(); }
+int gb_box_quadform(int L, int w, const double* box, const double* x, double* part, double* out,
+                    void* stream) {
+  if (L <= 0 || w < 0) return invalid("box_quadform: bad geometry");
+  COUNT(2);
+  return wrap(gbk_box_quadform(L, w, box, x, part, out, ST(stream)), "box_quadform");
+}
+int gb_max_abs(int64_t n, const double* x, double* part, double* out, void* stream) {
+  if (n < 0) return invalid("max_abs: n < 0");
+  COUNT(2);
+  return wrap(gbk_max_abs(n, x, part, out, ST(stream)), "max_abs");
+}
 int gb_dot2(int64_t n, const double* a, const double* b, const double* c, double* out,
             void* state, double* partials, void* stream) {
   COUNT(1);

@@ -165,3 +165,18 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches);
 int gbk_products_mode(int mma);
 int gbk_tune(int what, int value);
+
+// gb_diag.cu
+int gbk_cell_energies(int n, const double* v, const double* coef, const double* host_e16,
+                      double* out, cudaStream_t s);
+size_t gbk_decay_part_elems(int nr);
+int gbk_decay_sums(int n, double h, const double* en, double cx, double cy, const double* radii,
+                   int nr, double* part, double* out, cudaStream_t s);
+int gbk_box_diag_spectrum(long long rows, int nr, int w, const double* box, const double* coef,
+                          double* out, cudaStream_t s);
+int gbk_topk_mask(long long n, const double* mags, long long n_keep, double* mask, void* work,
+                  size_t* work_bytes, cudaStream_t s);
+size_t gbk_quad_part_elems();
+int gbk_box_quadform(int L, int w, const double* box, const double* x, double* part, double* out,
+                     cudaStream_t s);
+int gbk_max_abs(long long n, const double* x, double* part, double* out, cudaStream_t s);
