@@ -223,3 +223,15 @@ def test_lanczos_emulation_flags_indefinite_operator():
         ab = _lanczos_ab(A, np.ones(4), 4)
     rc = _emulate(ab)[0]
     assert rc == 2
+
+
+def test_matrix_market_roundtrip_and_bad_transform_file(tmp_path):
+    from paper_1503_03467_b200.persistence import load_transform, mm_read, mm_write
+    rng = np.random.default_rng(3)
+    m = sp.random_array((40, 30), density=0.2, random_state=rng, format="csr")
+    mm_write(tmp_path / "m.mtx", m)
+    back = mm_read(tmp_path / "m.mtx")
+    assert np.array_equal(back.toarray(), m.toarray())
+    np.savez(tmp_path / "bad.npz", x=np.zeros(3))
+    with pytest.raises(gb.InvalidArgumentError):
+        load_transform(tmp_path / "bad.npz")
