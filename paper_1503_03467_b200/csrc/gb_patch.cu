@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Batched SPD patch solves (Algorithm 2 lines 2a/3 and 11).
 //
 // K1 mass patches  (gamblet_fast.py:464-498): per fine node i,
@@ -487,6 +488,141 @@ __global__ void __launch_bounds__(128) k_mass_patches_v2(
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Mass patches as banded solves (gamblet_fast.py:464-498, line 2a/3).  With
+// the local nodes of the clipped (2 rho + 1)^2 box numbered row-major (nt per
+// row), the 9-point mass stencil couples l only to l +- {0, 1, nt - 1, nt,
+// nt + 1}: (S M S)[i^rho, i^rho] is banded with half-bandwidth b = nt + 1 and
+// its Cholesky factor has the same band (no fill outside it).  One warp per
+// patch: the band (m x (b+1), <= 49 x 9 at rho = 3) in shared memory,
+// right-looking column steps (<= 36 independent updates per step across the
+// lanes), then the forward (RHS s_i e_i) and backward band substitutions
+// with shuffle dot products.  ~b^2 m instead of m^3/3 flops; the serial
+// chain is m short steps instead of 7 dense 8x8 tile factorizations.
+// ---------------------------------------------------------------------------
+constexpr int kBandMaxM = 49, kBandMaxB = 8, kBandW = kBandMaxB + 1, kBandWarps = 4;
+
+__global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
+    int n, const double* __restrict__ M, const double* __restrict__ s, int rho, int wd,
+    double* __restrict__ psi, long long* status) {
+  __shared__ double sLb[kBandWarps][kBandMaxM * kBandW];
+  __shared__ double sSl[kBandWarps][kBandMaxM];
+  __shared__ double sX[kBandWarps][kBandMaxM];
+  __shared__ double sId[kBandWarps][kBandMaxM];  // 1 / L[r][r]
+  __shared__ int sRC[kBandWarps][kBandMaxM];     // (r / nt) << 8 | (r % nt)
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  double* Lb = sLb[wi];
+  double* sl = sSl[wi];
+  double* x = sX[wi];
+  double* id = sId[wi];
+  int* rc = sRC[wi];
+  // this lane's two trailing-update pairs p = lane, lane + 32 of the full
+  // b = 8 triangle, enumerated by rows: p = rr (rr + 1) / 2 + cc, cc <= rr;
+  // offsets from the pivot column: ro = rr + 1, co = cc + 1 (pairs 36.. unused)
+  int ro[2], co[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int p = lane + 32 * u;
+    int rr = 0;
+    while ((rr + 1) * (rr + 2) / 2 <= p) ++rr;
+    ro[u] = rr + 1;
+    co[u] = p - rr * (rr + 1) / 2 + 1;
+    if (p >= kBandMaxB * (kBandMaxB + 1) / 2) ro[u] = 99;
+  }
+  const long long N = (long long)n * n;
+  const long long nwarps = (long long)gridDim.x * kBandWarps;
+  for (long long i = (long long)blockIdx.x * kBandWarps + wi; i < N; i += nwarps) {
+    const int si = (int)(i / n), ti = (int)(i % n);
+    const int s0 = imax(0, si - rho), s1 = imin(n - 1, si + rho);
+    const int t0 = imax(0, ti - rho), t1 = imin(n - 1, ti + rho);
+    const int nt = t1 - t0 + 1, m = (s1 - s0 + 1) * nt;
+    const int b = imin(nt + 1, m - 1);  // half-bandwidth
+    const int li = (si - s0) * nt + (ti - t0);
+    for (int l = lane; l < m; l += 32) {
+      const int a = l / nt, c = l - a * nt;
+      rc[l] = (a << 8) | c;
+      sl[l] = s[(long long)(s0 + a) * n + (t0 + c)];
+    }
+    __syncwarp();
+    // band gather: Lb[r * kBandW + d] = (S M S)[r][r - d], d = 0..b
+    for (int e = lane; e < m * kBandW; e += 32) {
+      const int r = e / kBandW, d = e - r * kBandW;
+      const int c = r - d;
+      double v = 0.0;
+      if (d <= b && c >= 0) {
+        const int pr = rc[r], pc = rc[c];
+        const int ds = (pc >> 8) - (pr >> 8), dt = (pc & 255) - (pr & 255);
+        if (ds >= -1 && ds <= 1 && dt >= -1 && dt <= 1) {
+          const long long gr = (long long)(s0 + (pr >> 8)) * n + (t0 + (pr & 255));
+          v = M[gr * 9 + (ds + 1) * 3 + (dt + 1)] * sl[r] * sl[c];
+        }
+      }
+      Lb[e] = v;
+    }
+    __syncwarp();
+    // right-hand side s_i e_li, forward-substituted inside the factorization
+    for (int l = lane; l < m; l += 32) x[l] = (l == li) ? sl[li] : 0.0;
+    __syncwarp();
+    bool ok = true;
+    // right-looking band Cholesky: column j, y_j = x_j / L_jj, then the <= 36
+    // trailing updates and x_{j+k} -= L[j+k][j] y_j
+    for (int j = 0; j < m; ++j) {
+      const double piv = Lb[j * kBandW];
+      ok = ok && (piv > 0.0);
+      const double il = rsqrt(piv);
+      const double yj = x[j] * il;
+      const int kmax = imin(b, m - 1 - j);
+      double lc = 0.0;  // L[j + lane][j], lanes 1..kmax
+      if (lane >= 1 && lane <= kmax) lc = Lb[(j + lane) * kBandW + lane] * il;
+      __syncwarp();
+      if (lane == 0) {
+        Lb[j * kBandW] = piv * il;
+        id[j] = il;
+        x[j] = yj;
+      }
+      if (lane >= 1 && lane <= kmax) {
+        Lb[(j + lane) * kBandW + lane] = lc;
+        x[j + lane] = fma(-lc, yj, x[j + lane]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double vr = __shfl_sync(0xffffffffu, lc, ro[u] & 31);
+        const double vc = __shfl_sync(0xffffffffu, lc, co[u] & 31);
+        if (ro[u] <= kmax) {
+          double* a = Lb + (j + ro[u]) * kBandW + (ro[u] - co[u]);
+          *a = fma(-vr, vc, *a);
+        }
+      }
+      __syncwarp();
+    }
+    if (!__all_sync(0xffffffffu, ok)) {
+      if (lane == 0) raise_status(status, ST_NOT_SPD, i);
+      continue;
+    }
+    // backward, column oriented: z_r = y_r / L_rr, then y_{r-k} -= L[r][r-k] z_r
+    for (int r = m - 1; r >= 0; --r) {
+      const double z = x[r] * id[r];
+      if (lane >= 1 && lane <= b && r - lane >= 0)
+        x[r - lane] = fma(-Lb[r * kBandW + lane], z, x[r - lane]);
+      __syncwarp();
+      if (lane == 0) x[r] = z;
+      __syncwarp();
+    }
+    const int os = clampi(si - rho, 0, n - wd), ot = clampi(ti - rho, 0, n - wd);
+    double* row = psi + i * (long long)wd * wd;
+    for (int e = lane; e < wd * wd; e += 32) {
+      const int fs = os + e / wd, ft = ot + e % wd;
+      double v = 0.0;
+      if (fs >= s0 && fs <= s1 && ft >= t0 && ft <= t1) {
+        const int l = (fs - s0) * nt + (ft - t0);
+        v = sl[l] * x[l];
+      }
+      row[e] = v;
+    }
+    __syncwarp();
+  }
+}
 }  // namespace gb
 
 using namespace gb;
@@ -581,10 +717,20 @@ int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB,
   return (int)cudaGetLastError();
 }
 
+static int g_mass_mode = -1;  // -1: unset (env GB_MASS_DENSE)
 int gbk_mass_patches_v2(int n, int wM, const double* M, const double* s, int rho, int wd,
                         double* psi, long long* status, cudaStream_t st) {
   const int nmax = (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
+  const long long NN = (long long)n * n;
+  if (g_mass_mode < 0) g_mass_mode = getenv("GB_MASS_DENSE") ? 1 : 0;
+  if (wM == 1 && rho <= 3 && g_mass_mode == 0) {  // banded warp solver (rho = 3: b <= 8)
+    const long long warps = 148LL * 16 * 4;
+    const long long g = (NN + kBandWarps - 1) / kBandWarps;
+    k_mass_patches_band<<<(int)(g < warps / kBandWarps ? g : warps / kBandWarps),
+                          32 * kBandWarps, 0, st>>>(n, M, s, rho, wd, psi, status);
+    return (int)cudaGetLastError();
+  }
   const size_t smem = tile_smem_bytes(Tmax, 4);
   if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
   cudaFuncSetAttribute(k_mass_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
