@@ -60,6 +60,16 @@ int gb_csr_halfwidth(int n, const int32_t* indptr, const int32_t* indices,
 int gb_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
                   const double* data, double* box, int64_t* status, void* stream);
 
+/* ---- host input upload -------------------------------------------------
+ * bytes of pageable host memory -> device, staged through a pinned ring by
+ * nthreads host threads, DMA asynchronous on `stream` (ordered before later
+ * work on that stream). */
+int gb_h2d_staged(void* dst, const void* src, int64_t bytes, int nthreads, void* stream);
+/* the same for count int64 host indices narrowed to int32 on the way (scipy
+ * int64 CSR indices; 1 = a value outside int32) */
+int gb_h2d_staged_i64_i32(int32_t* dst, const int64_t* src, int64_t count, int nthreads,
+                          void* stream);
+
 /* ---- on-device Q1 assembly (replaces grid_fem.py:189-227 _assemble /
  * assemble_mass / assemble_stiffness and the b = M g of assemble_load,
  * grid_fem.py:238-245) ---------------------------------------------------

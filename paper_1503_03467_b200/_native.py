@@ -92,6 +92,8 @@ _SIGS = {
     "gb_quad_part_elems": ([], _Z),
     "gb_box_quadform": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "gb_max_abs": ([_L, _P, _P, _P, _P], _I),
+    "gb_h2d_staged": ([_P, _P, _L, _I, _P], _I),
+    "gb_h2d_staged_i64_i32": ([_P, _P, _L, _I, _P], _I),
     "gb_assemble_q1": ([_I, _P, _D, _P, _P, _P], _I),
     "gb_box1_matvec": ([_I, _P, _P, _P, _P], _I),
     "gb_lanczos_emulate": ([_P, _I, _D, _I, _P, _P, _P, _P], _I),

@@ -561,3 +561,112 @@ int gb_fp64_peak_probe(int kind, int iters, double* sink, void* stream) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host -> device upload of pageable host memory (the API's scipy inputs):
+// chunks are copied into a process-wide pinned staging ring by several host
+// threads and DMA'd asynchronously on `stream`, the next chunk's host copy
+// overlapping the previous chunk's DMA.  A pageable cudaMemcpy is bounded by
+// one driver memcpy thread.
+// ---------------------------------------------------------------------------
+#include <stdint.h>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace {
+constexpr size_t kStageChunk = 16u << 20;
+constexpr int kStageSlots = 3;
+std::mutex g_stage_mu;
+char* g_stage = nullptr;
+cudaEvent_t g_stage_ev[kStageSlots];
+
+void par_memcpy(char* dst, const char* src, size_t bytes, int nthreads) {
+  if (nthreads <= 1 || bytes < (1u << 20)) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t step = ((bytes + nthreads - 1) / nthreads + 4095) & ~(size_t)4095;
+  for (size_t off = 0; off < bytes; off += step) {
+    const size_t len = off + step <= bytes ? step : bytes - off;
+    th.emplace_back([=] { memcpy(dst + off, src + off, len); });
+  }
+  for (auto& t : th) t.join();
+}
+}  // namespace
+
+// narrowing copy int64 -> int32 by several threads; false if a value does not fit
+bool par_narrow(int32_t* dst, const int64_t* src, size_t count, int nthreads) {
+  std::vector<std::thread> th;
+  std::vector<char> okv((size_t)(nthreads > 0 ? nthreads : 1), 1);
+  const size_t step = (count + (size_t)nthreads - 1) / (size_t)nthreads;
+  int w = 0;
+  for (size_t off = 0; off < count; off += step, ++w) {
+    const size_t len = off + step <= count ? step : count - off;
+    char* ok = &okv[(size_t)w];
+    th.emplace_back([=] {
+      bool good = true;
+      for (size_t i = 0; i < len; ++i) {
+        const int64_t v = src[off + i];
+        good = good && v >= INT32_MIN && v <= INT32_MAX;
+        dst[off + i] = (int32_t)v;
+      }
+      *ok = good;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (char c : okv)
+    if (!c) return false;
+  return true;
+}
+
+static int h2d_staged(void* dst, const void* src, int64_t count, int elem_in, int elem_out,
+                      int nthreads, void* stream);
+
+int gb_h2d_staged(void* dst, const void* src, int64_t bytes, int nthreads, void* stream) {
+  return h2d_staged(dst, src, bytes, 1, 1, nthreads, stream);
+}
+
+int gb_h2d_staged_i64_i32(int32_t* dst, const int64_t* src, int64_t count, int nthreads,
+                          void* stream) {
+  return h2d_staged(dst, src, count, 8, 4, nthreads, stream);
+}
+
+// count elements of elem_in bytes -> elem_out bytes (1/1: raw bytes, 8/4: int64 -> int32)
+static int h2d_staged(void* dst, const void* src, int64_t count, int elem_in, int elem_out,
+                      int nthreads, void* stream) {
+  if (count < 0 || (count > 0 && (!dst || !src))) return invalid("h2d_staged: bad arguments");
+  if (nthreads < 1) nthreads = 1;
+  std::lock_guard<std::mutex> lock(g_stage_mu);
+  cudaError_t e;
+  if (!g_stage) {
+    e = cudaHostAlloc((void**)&g_stage, kStageChunk * kStageSlots, cudaHostAllocDefault);
+    if (e != cudaSuccess) return wrap((int)e, "h2d_staged: cudaHostAlloc");
+    for (int i = 0; i < kStageSlots; ++i) {
+      e = cudaEventCreateWithFlags(&g_stage_ev[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return wrap((int)e, "h2d_staged: event");
+      cudaEventRecord(g_stage_ev[i], 0);
+    }
+  }
+  int slot = 0;
+  const int64_t chunk = (int64_t)(kStageChunk / (size_t)elem_out);  // elements per chunk
+  for (int64_t off = 0; off < count; off += chunk, slot = (slot + 1) % kStageSlots) {
+    const int64_t cnt = count - off < chunk ? count - off : chunk;
+    const size_t len = (size_t)cnt * (size_t)elem_out;
+    char* buf = g_stage + (size_t)slot * kStageChunk;
+    e = cudaEventSynchronize(g_stage_ev[slot]);  // the slot's previous DMA is done
+    if (e != cudaSuccess) return wrap((int)e, "h2d_staged: sync");
+    if (elem_in == elem_out) {
+      par_memcpy(buf, (const char*)src + off * elem_in, len, nthreads);
+    } else if (!par_narrow((int32_t*)buf, (const int64_t*)src + off, (size_t)cnt, nthreads)) {
+      return invalid("h2d_staged: index does not fit in int32");
+    }
+    e = cudaMemcpyAsync((char*)dst + off * elem_out, buf, len, cudaMemcpyHostToDevice,
+                        ST(stream));
+    if (e != cudaSuccess) return wrap((int)e, "h2d_staged: copy");
+    e = cudaEventRecord(g_stage_ev[slot], ST(stream));
+    if (e != cudaSuccess) return wrap((int)e, "h2d_staged: record");
+  }
+  return 0;
+}

@@ -73,6 +73,33 @@ class Traffic:
         cls.h2d = cls.d2h = 0
 
 
+# host->device: arrays above this size go through the library's pinned
+# staging ring (gb_h2d_staged: multi-threaded host copy overlapped with the
+# DMA) -- a pageable copy is bounded by one driver memcpy thread
+_STAGE_MIN_BYTES = 4 << 20
+_STAGE_THREADS = 8
+
+
+def _staged_copy(t):
+    out = torch.empty(t.shape, dtype=t.dtype, device=device())
+    nat.call("gb_h2d_staged", out.data_ptr(), t.data_ptr(), t.numel() * t.element_size(),
+             _STAGE_THREADS, stream())
+    return out
+
+
+def _index_to_dev(idx):
+    """Host CSR index array (int32 or int64) -> device int32; int64 input is
+    narrowed by the staging threads instead of a host astype pass."""
+    idx = np.ascontiguousarray(idx)
+    if idx.dtype == np.int64 and idx.nbytes >= _STAGE_MIN_BYTES and torch.cuda.is_available():
+        out = torch.empty(idx.shape, dtype=torch.int32, device=device())
+        Traffic.h2d += idx.size * 4
+        nat.call("gb_h2d_staged_i64_i32", out.data_ptr(), idx.ctypes.data, idx.size,
+                 _STAGE_THREADS, stream())
+        return out
+    return to_dev(idx.astype(np.int32, copy=False))
+
+
 def to_dev(arr, dtype=None):
     """Host array -> new device tensor (counted in Traffic.h2d).  A torch
     tensor already on the device is returned as is."""
@@ -85,6 +112,8 @@ def to_dev(arr, dtype=None):
     if dtype is not None:
         t = t.to(dtype)
     Traffic.h2d += t.numel() * t.element_size()
+    if t.numel() * t.element_size() >= _STAGE_MIN_BYTES and torch.cuda.is_available():
+        return _staged_copy(t)
     return t.to(device(), non_blocking=False)
 
 
@@ -103,8 +132,7 @@ class DeviceCSR:
 
     @classmethod
     def from_scipy(cls, mat):
-        return cls(to_dev(mat.indptr.astype(np.int32, copy=False)),
-                   to_dev(mat.indices.astype(np.int32, copy=False)),
+        return cls(_index_to_dev(mat.indptr), _index_to_dev(mat.indices),
                    to_dev(mat.data.astype(np.float64, copy=False)), mat.shape)
 
 
