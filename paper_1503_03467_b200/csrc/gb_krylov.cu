@@ -1279,6 +1279,55 @@ __global__ void __launch_bounds__(192) k_symb_bjcg_update(int L, int w, double* 
   }
 }
 
+// Lanczos step fused with phase 2 of the symmetric SpMV (layout 1): y's own
+// partial plus the neighbours' spill-over is completed in registers, alpha
+// comes from the phase-1 reduction by linearity (st->pAp = x.y, run with
+// red = 1), then the recurrence of k_lz_step.  Interior rows only: the
+// zero halo of every vector is never written.
+__global__ void __launch_bounds__(256) k_symb_lz_update(int L, int w, const double* __restrict__ x,
+                                                        double* __restrict__ y,
+                                                        double* __restrict__ vp, KState* st,
+                                                        double* part, double* ab) {
+  __shared__ double sh[32];
+  if (st->done) return;
+  const double bp = st->aux0, ibp = 1.0 / bp;
+  const double alpha = st->pAp * ibp * ibp;
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * 3, R = (long long)L * L * 3;
+  double uu = 0.0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long pp = r / 3;
+    const int c = (int)(r - pp * 3);
+    const int ps = (int)(pp / L), pt = (int)(pp % L);
+    const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
+    const double yv = symb_fix_value(y[yi], y + npad, L, w, ps, pt, c);
+    const double xv = x[yi];
+    const double u = (yv - alpha * xv) * ibp - bp * vp[yi];
+    vp[yi] = xv * ibp;
+    y[yi] = u;
+    uu += u * u;
+  }
+  uu = block_sum(uu, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = uu;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      const double beta = sqrt(a);
+      ab[2 * st->it] = alpha;
+      ab[2 * st->it + 1] = beta;
+      st->it += 1;
+      st->aux0 = beta;
+      if (!(beta > 0.0) || st->it >= st->max_iter) st->done = 1;
+    }
+  }
+}
+
 // start: x = s x0 (or 0), r = b - s A x0 (Ax0 null => x0 = 0), z = Minv r, p = z;
 // ||b||, ||r||, r.z and the early exits of sparse_core.py:138-148.  Partials
 // are (||r||^2, r.z) pairs in part[0, 2G) and ||b||^2 in part[2G, 3G), so the
@@ -2329,13 +2378,21 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
   for (;;) {
     const bool a_live = !ha->done;
     for (int i = 0; i < chunk; ++i) {
+      // symmetric layout: the B-half's reduction x.y by linearity in phase 1
+      // and phase 2 fused into the Lanczos update (no k_symb_fix launch)
+      const int fused = e->layout == 1;
       if (a_live) {
-        if ((err = launch_dual(e, v, w, 1, 0, s, &nl))) return err;
+        if ((err = launch_dual(e, v, w, fused ? 0 : 1, fused, s, &nl))) return err;
         post_a(e, s, &nl);
-      } else if ((err = launch_single(e, v, w, e->stb, e->partb, 1, 0, s, &nl))) {
+      } else if ((err = launch_single(e, v, w, e->stb, e->partb, fused ? 0 : 1, fused, s,
+                                      &nl))) {
         return err;
       }
-      k_lz_step<<<gv, 256, 0, s>>>(npad, v, vp, w, kb, e->partb, e->lz);
+      if (fused)
+        k_symb_lz_update<<<grid_for((long long)e->L * e->L * 3, 256, kRedBlocks), 256, 0, s>>>(
+            e->L, e->w, v, w, vp, kb, e->partb, e->lz);
+      else
+        k_lz_step<<<gv, 256, 0, s>>>(npad, v, vp, w, kb, e->partb, e->lz);
       nl += 1;
       double* t = v;
       v = w;
