@@ -363,7 +363,7 @@ def run_ours(args, rank, world, local_rank):
             "launches_per_step": passes,
             "share_of_step_serialized": round(sp["ms"] * passes / ms, 3)}
     cp = kern["corr"]
-    fp = None if cp is None else {"kernel": "k_correction_patches_v2 (finest level, tiled DMMA Cholesky)",
+    fp = None if cp is None else {"kernel": "k_correction_patches_v3 (finest level, left-looking tiled DMMA Cholesky, L streamed through L2 scratch)",
           "bound": "fp64", "achieved": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12, 3),
           "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
           "frac": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12 / fp64_peak, 4),

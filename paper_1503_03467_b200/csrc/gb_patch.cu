@@ -625,6 +625,8 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
 }
 }  // namespace gb
 
+#include "gb_patch_l2.cuh"
+
 using namespace gb;
 
 static const int kMaxSmem = 227 * 1024;
@@ -699,11 +701,41 @@ int gbk_tune(int what, int value) {
   return -1;
 }
 
+static int g_patch_v3 = -1;  // -1: unset (env GB_PATCH_V2 selects the smem-resident v2)
+static double* g_v3_scratch = nullptr;
+static size_t g_v3_scratch_bytes = 0;
+
 int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB, int wG,
                               const double* G, int rho, double* Dt, long long* status,
                               cudaStream_t st) {
   const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
+  if (g_patch_v3 < 0) g_patch_v3 = getenv("GB_PATCH_V2") ? 0 : 1;
+  if (g_patch_v3 && Tmax <= 255) {
+    const size_t smem = v3_smem_bytes(Tmax);
+    int per_sm = 6;
+    if (const char* e = getenv("GB_PATCH_V3_PER_SM")) per_sm = atoi(e) > 0 ? atoi(e) : 6;
+    const long long P = (long long)Lp * Lp;
+    const long long gmax = 148LL * per_sm;
+    const int g = (int)(P < gmax ? P : gmax);
+    const size_t need = (size_t)g * ((size_t)Tmax * (Tmax + 1) / 2 + Tmax) * 64 * sizeof(double);
+    if (need > g_v3_scratch_bytes) {
+      if (g_v3_scratch) {
+        cudaDeviceSynchronize();
+        cudaFree(g_v3_scratch);
+      }
+      g_v3_scratch = nullptr;
+      g_v3_scratch_bytes = 0;
+      cudaError_t e = cudaMalloc((void**)&g_v3_scratch, need);
+      if (e != cudaSuccess) return (int)e;
+      g_v3_scratch_bytes = need;
+    }
+    cudaFuncSetAttribute(k_correction_patches_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_correction_patches_v3<<<g, 32 * kV3Warps, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt,
+                                                            status, Tmax, g_v3_scratch);
+    return (int)cudaGetLastError();
+  }
   const size_t smem = tile_smem_bytes(Tmax, 8);
   if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
   cudaFuncSetAttribute(k_correction_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,304 @@
+// Correction patches, v3: left-looking tiled Cholesky with the finished L
+// columns streamed through an L2-resident global scratch instead of held in
+// shared memory (gamblet_fast.py:546-580; same arithmetic family as v2:
+// 8x8 FP64 tiles, DMMA m8n8k4 updates, L_kk^-1 on the diagonal, the RHS
+// folded in as tile row T).
+//
+// Why: v2 keeps the whole packed lower factor (~107 KB at m = 147) in shared
+// memory, so only 2 patches fit per SM and the per-step serial chain (8x8
+// diagonal factor + TRSM + barriers) leaves the SM idle most of the time
+// (ncu: IPC 1.4, 13 % of the FP64 peak).  Here a CTA holds only the current
+// tile column and the L row it needs (~24 KB): 6+ patches per SM overlap
+// their serial chains.  Step kt gathers column kt of (S B S)[chi, chi] from
+// the box, subtracts sum_jt L(it, jt) L(kt, jt)^T (A fragments streamed from
+// the scratch, B fragments from the staged L row), factors the diagonal tile
+// and writes L(it, kt) = C(it, kt) L_kk^-T back.  The scratch of a CTA is
+// ~107 KB; all CTAs together stay inside the 126 MB L2.
+//
+// Scratch tile layout ("fragment order"): element (r, c) of an 8x8 tile at
+// (c >> 2) * 32 + r * 4 + (c & 3), so the DMMA A / B fragment of k-chunk ch
+// (row lane >> 2, column 4 ch + (lane & 3)) is the contiguous 256 B run
+// ch * 32 + lane.  Diagonal tiles hold L_kk^-1.  Tile (it, jt) of the packed
+// lower factor (RHS row it = T included) is at index it (it + 1) / 2 + jt.
+#pragma once
+
+namespace gb {
+
+__device__ __forceinline__ int fpos(int r, int c) { return ((c >> 2) << 5) + (r << 2) + (c & 3); }
+
+constexpr int kV3Warps = 4;
+
+struct V3Smem {
+  double* col;   // 2 x (Tmax + 1) tiles, row-major 8x8: C(it, kt), it = kt..T
+  double* lrow;  // Tmax tiles, fragment order: L(kt, jt), jt < kt
+  double* dg;    // 64: diagonal tile, swizzled (warp_chol8_inv layout)
+  double* sl;    // 8 Tmax + 8 (scale; 8 scratch doubles after it)
+  double* z;     // 8 Tmax
+  long long* rowb;  // 8 Tmax: B offset of local row l minus its key (separable gather)
+  int* colk;     // 8 Tmax: key of local column l
+  int* ploc;     // 8 Tmax
+  int* flag;
+};
+
+__host__ __device__ __forceinline__ size_t v3_smem_bytes(int Tmax) {
+  return ((size_t)2 * (Tmax + 1) * 64 + (size_t)Tmax * 64 + 64 + (8 * Tmax + 8) + 8 * Tmax +
+          8 * Tmax) * 8 + (size_t)16 * Tmax * 4 + 16;
+}
+
+__device__ __forceinline__ V3Smem v3_carve(double* sm, int Tmax) {
+  V3Smem s;
+  s.col = sm;  // two column buffers (ping-pong)
+  s.lrow = s.col + 2 * (Tmax + 1) * 64;
+  s.dg = s.lrow + Tmax * 64;
+  s.sl = s.dg + 64;
+  s.z = s.sl + 8 * Tmax + 8;
+  s.rowb = reinterpret_cast<long long*>(s.z + 8 * Tmax);
+  int* ip = reinterpret_cast<int*>(s.rowb + 8 * Tmax);
+  s.colk = ip;
+  s.ploc = s.colk + 8 * Tmax;
+  s.flag = s.ploc + 8 * Tmax;
+  return s;
+}
+
+// gather column kt of (S B S)[chi, chi] (tiles (it, kt), it = kt..T-1, rows
+// l1 = 8 kt .. 8 T - 1, row-major) and the RHS tile (T, kt) into `col`, by
+// threads tl = 0..nt-1 (nt a multiple of 8): thread tl owns column c = tl & 7
+// and rows l1 = 8 kt + (tl >> 3) + (nt / 8) j; entries are the reference's
+// congruence (B s_i) s_j (gamblet_fast.py:136)
+__device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, int T, int m,
+                                          int wB, const double* __restrict__ B, int tl, int nt) {
+  const int c = tl & 7;
+  const int l2 = 8 * kt + c;
+  const bool cval = l2 < m;
+  const long long ck = cval ? S.colk[l2] : 0;
+  const int p2 = cval ? S.ploc[l2] : 0;
+  const double s2 = cval ? S.sl[l2] : 0.0;
+  const int step = nt >> 3;
+#pragma unroll 4
+  for (int l1 = 8 * kt + (tl >> 3); l1 < 8 * T; l1 += step) {
+    double v = 0.0;
+    if (l1 < m && cval) {
+      const int p1 = S.ploc[l1];
+      const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
+      if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
+        v = __ldg(B + S.rowb[l1] + ck) * S.sl[l1] * s2;
+    } else if (l1 == l2) {
+      v = 1.0;  // padding rows: unit diagonal
+    }
+    col[(l1 - 8 * kt) * 8 + c] = v;
+  }
+  for (int r = tl >> 3; r < 8; r += step) col[(T - kt) * 64 + r * 8 + c] = (r == 0) ? S.z[l2] : 0.0;
+}
+
+__global__ void __launch_bounds__(32 * kV3Warps, 6) k_correction_patches_v3(
+    int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB, int wG,
+    const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status, int Tmax,
+    double* __restrict__ scratch) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  V3Smem S = v3_carve(sm, Tmax);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int SB = box_slots(wB, 3), SG = box_slots(wG, 1), SD = box_slots(rho, 3);
+  const long long P = (long long)Lp * Lp;
+  double* L = scratch + (long long)blockIdx.x * ((Tmax * (Tmax + 1)) / 2 + Tmax) * 64;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (long long i = blockIdx.x; i < P; i += gridDim.x) {
+    const int si = (int)(i / Lp), ti = (int)(i % Lp);
+    const int s0 = imax(0, si - rho), s1 = imin(Lp - 1, si + rho);
+    const int t0 = imax(0, ti - rho), t1 = imin(Lp - 1, ti + rho);
+    const int nbt = t1 - t0 + 1;
+    const int m = 3 * (s1 - s0 + 1) * nbt;
+    const int T = (m + 7) >> 3;
+    // local tables and the right-hand side s * (-G[:, i])
+    double nrm = 0.0;
+    for (int l = threadIdx.x; l < 8 * T; l += blockDim.x) {
+      double v = 0.0;
+      if (l < m) {
+        const int pl = l / 3, c = l - 3 * pl;
+        const int a = pl / nbt, b = pl - a * nbt;
+        const long long r = ((long long)(s0 + a) * Lp + (t0 + b)) * 3 + c;
+        // slot_of(wB, 3, a2 - a1, b2 - b1, c2) = key(l2) - 3 (a1 W2 + b1) + K
+        const int key = (a * (2 * wB + 1) + b) * 3;
+        S.rowb[l] = r * SB - key + (wB * (2 * wB + 1) + wB) * 3;
+        S.colk[l] = key + c;
+        S.ploc[l] = (a << 8) | b;
+        S.sl[l] = sB[r];
+        const int ds = si - (s0 + a), dt = ti - (t0 + b);
+        double g = 0.0;
+        if (ds >= -wG && ds <= wG && dt >= -wG && dt <= wG)
+          g = G[r * SG + slot_of(wG, 1, ds, dt, 0)];
+        v = sB[r] * (-g);
+      }
+      S.z[l] = v;
+      nrm += v * v;
+    }
+    nrm = block_sum(nrm, red);  // also orders the table writes
+    double* drow = Dt + i * SD;
+    if (nrm == 0.0) {  // gamblet_fast.py:561-562: empty correction column
+      for (int e = threadIdx.x; e < SD; e += blockDim.x) drow[e] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    if (threadIdx.x == 0) *S.flag = 0;
+    bool ok = true;
+    const int colstride = (Tmax + 1) * 64;
+    v3_gather(S, S.col, 0, T, m, wB, B, threadIdx.x, blockDim.x);
+    __syncthreads();
+    // step kt: [update column kt] | [warp 0: factor the diagonal tile;
+    // warps 1..: gather column kt + 1, stage L(kt + 1, 0..kt-1)] | [TRSM]
+    for (int kt = 0; kt < T; ++kt) {
+      double* cur = S.col + (kt & 1) * colstride;
+      double* nxt = S.col + ((kt + 1) & 1) * colstride;
+      // (3) C(it, kt) -= sum_jt L(it, jt) L(kt, jt)^T, a warp per tile row
+      if (kt > 0) {
+        // two tile rows per warp iteration: 4 independent accumulator chains
+        for (int it = kt + warp; it <= T; it += 2 * kV3Warps) {
+          const int it2 = it + kV3Warps;
+          const bool two = it2 <= T;
+          double* ct = cur + (it - kt) * 64;
+          double* ct2 = cur + ((two ? it2 : it) - kt) * 64;
+          double c0 = ct[2 * lane], c1 = ct[2 * lane + 1];
+          double g0 = two ? ct2[2 * lane] : 0.0, g1 = two ? ct2[2 * lane + 1] : 0.0;
+          double d0 = 0.0, d1 = 0.0, h0 = 0.0, h1 = 0.0;
+          const double* ai = L + (long long)((it * (it + 1)) >> 1) * 64;
+          const double* ai2 = L + (long long)(((two ? it2 : it) * ((two ? it2 : it) + 1)) >> 1) * 64;
+          int jt = 0;
+          for (; jt + 1 < kt; jt += 2) {
+            double a[4], q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = __ldcg(ai + jt * 64 + 32 * u + lane);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = two ? __ldcg(ai2 + jt * 64 + 32 * u + lane) : 0.0;
+            const double* bj = S.lrow + jt * 64;
+            const double b0 = bj[lane], b1 = bj[32 + lane], b2 = bj[64 + lane], b3 = bj[96 + lane];
+            dmma_884(c0, c1, -a[0], b0);
+            dmma_884(g0, g1, -q[0], b0);
+            dmma_884(d0, d1, -a[2], b2);
+            dmma_884(h0, h1, -q[2], b2);
+            dmma_884(c0, c1, -a[1], b1);
+            dmma_884(g0, g1, -q[1], b1);
+            dmma_884(d0, d1, -a[3], b3);
+            dmma_884(h0, h1, -q[3], b3);
+          }
+          if (jt < kt) {
+            const double* bj = S.lrow + jt * 64;
+            const double b0 = bj[lane], b1 = bj[32 + lane];
+            const double a0 = __ldcg(ai + jt * 64 + lane), a1 = __ldcg(ai + jt * 64 + 32 + lane);
+            const double q0 = two ? __ldcg(ai2 + jt * 64 + lane) : 0.0;
+            const double q1 = two ? __ldcg(ai2 + jt * 64 + 32 + lane) : 0.0;
+            dmma_884(c0, c1, -a0, b0);
+            dmma_884(g0, g1, -q0, b0);
+            dmma_884(c0, c1, -a1, b1);
+            dmma_884(g0, g1, -q1, b1);
+          }
+          ct[2 * lane] = c0 + d0;
+          ct[2 * lane + 1] = c1 + d1;
+          if (two) {
+            ct2[2 * lane] = g0 + h0;
+            ct2[2 * lane + 1] = g1 + h1;
+          }
+        }
+        __syncthreads();
+      }
+      if (warp == 0) {
+        // (4) factor the diagonal tile -> L_kk^-1 (swizzled in S.dg, and the
+        // scratch diagonal tile for the back substitution)
+        for (int e = lane; e < 64; e += 32) S.dg[eidx(e >> 3, e & 7)] = cur[e];
+        __syncwarp();
+        if (!warp_chol8_inv(S.dg, S.sl + 8 * Tmax) && lane == 0) *S.flag = 1;
+        __syncwarp();
+        double* dt_ = L + (long long)(((kt * (kt + 1)) >> 1) + kt) * 64;
+        for (int e = lane; e < 64; e += 32) dt_[fpos(e >> 3, e & 7)] = S.dg[eidx(e >> 3, e & 7)];
+      } else if (kt + 1 < T) {
+        // meanwhile: column kt + 1 and the finished part of L row kt + 1
+        v3_gather(S, nxt, kt + 1, T, m, wB, B, threadIdx.x - 32, blockDim.x - 32);
+        const double* src = L + (long long)(((kt + 1) * (kt + 2)) >> 1) * 64;
+        for (int e = threadIdx.x - 32; e < kt * 64; e += blockDim.x - 32)
+          S.lrow[e] = __ldcg(src + e);
+      }
+      __syncthreads();
+      if (*S.flag) {
+        ok = false;
+        break;
+      }
+      // (5) TRSM: L(it, kt) = C(it, kt) L_kk^-T (it = kt+1..T) -> scratch;
+      // L(kt + 1, kt) also completes the staged L row
+      {
+        const double bl0 = S.dg[eidx(fr, fk)], bl1 = S.dg[eidx(fr, 4 + fk)];
+        for (int it = kt + 1 + warp; it <= T; it += kV3Warps) {
+          const double* ct = cur + (it - kt) * 64;
+          const double a0 = ct[fr * 8 + fk], a1 = ct[fr * 8 + 4 + fk];
+          double e0 = 0.0, e1 = 0.0;
+          dmma_884(e0, e1, a0, bl0);
+          dmma_884(e0, e1, a1, bl1);
+          double* out = L + (long long)(((it * (it + 1)) >> 1) + kt) * 64;
+          out[fpos(fr, 2 * fk)] = e0;
+          out[fpos(fr, 2 * fk + 1)] = e1;
+          if (it == kt + 1 && it < T) {
+            S.lrow[kt * 64 + fpos(fr, 2 * fk)] = e0;
+            S.lrow[kt * 64 + fpos(fr, 2 * fk + 1)] = e1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (!ok) {
+      if (threadIdx.x == 0) raise_status(status, ST_NOT_SPD, i);
+      __syncthreads();
+      continue;
+    }
+    // back substitution L^T z = y (y = row 0 of the RHS tiles (T, jt)), one
+    // warp: step it, the 4 lane groups split the tiles jt > it
+    if (warp == 0) {
+      const double* yrow = L + (long long)((T * (T + 1)) >> 1) * 64;
+      for (int e = lane; e < 8 * T; e += 32) S.z[e] = __ldcg(yrow + (e >> 3) * 64 + fpos(0, e & 7));
+      __syncwarp();
+      const int r = lane & 7, cg = lane >> 3;
+      for (int it = T - 1; it >= 0; --it) {
+        double acc = 0.0;
+        for (int jt = it + 1 + cg; jt < T; jt += 4) {
+          const double* t = L + (long long)(((jt * (jt + 1)) >> 1) + it) * 64;
+          const double* zj = S.z + 8 * jt;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = fma(__ldcg(t + fpos(k, r)), zj[k], acc);
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+        const double v = S.z[8 * it + r] - acc;
+        const double* li = L + (long long)(((it * (it + 1)) >> 1) + it) * 64;
+        double zr = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double vc = __shfl_sync(0xffffffffu, v, c);
+          if (c >= r) zr = fma(__ldcg(li + fpos(c, r)), vc, zr);
+        }
+        __syncwarp();
+        if (lane < 8) S.z[8 * it + lane] = zr;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // D = s z and the row-tail trim of this column of D (as v2)
+    double mx = 0.0;
+    for (int l = threadIdx.x; l < m; l += blockDim.x) {
+      const double v = S.sl[l] * S.z[l];
+      S.z[l] = v;
+      mx = fmax(mx, fabs(v));
+    }
+    mx = block_max(mx, red);
+    const double thr = 1e-11 * mx;
+    for (int e = threadIdx.x; e < SD; e += blockDim.x) {
+      const int c = e % 3, bs = e / 3;
+      const int ps = si + bs / (2 * rho + 1) - rho, pt = ti + bs % (2 * rho + 1) - rho;
+      double v = 0.0;
+      if (ps >= s0 && ps <= s1 && pt >= t0 && pt <= t1) {
+        v = S.z[((ps - s0) * nbt + (pt - t0)) * 3 + c];
+        if (!(fabs(v) >= thr)) v = 0.0;
+      }
+      drow[e] = v;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace gb
