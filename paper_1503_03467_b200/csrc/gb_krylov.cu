@@ -1283,30 +1283,53 @@ __global__ void __launch_bounds__(192) k_symb_bjcg_update(int L, int w, double* 
 // partial plus the neighbours' spill-over is completed in registers, alpha
 // comes from the phase-1 reduction by linearity (st->pAp = x.y, run with
 // red = 1), then the recurrence of k_lz_step.  Interior rows only: the
-// zero halo of every vector is never written.
-__global__ void __launch_bounds__(256) k_symb_lz_update(int L, int w, const double* __restrict__ x,
-                                                        double* __restrict__ y,
-                                                        double* __restrict__ vp, KState* st,
-                                                        double* part, double* ab) {
+// zero halo of every vector is never written.  Tile-aligned: a CTA walks
+// whole tiles (kSymTH grid rows x 64 parents), so the neighbour spill
+// regions are CTA-uniform and added in symb_fix_value's order without any
+// per-element division.
+constexpr int kLzThreads = 256;
+__global__ void __launch_bounds__(kLzThreads) k_symb_lz_update(int L, int w,
+                                                               const double* __restrict__ x,
+                                                               double* __restrict__ y,
+                                                               double* __restrict__ vp,
+                                                               KState* st, double* part,
+                                                               double* ab) {
   __shared__ double sh[32];
   if (st->done) return;
   const double bp = st->aux0, ibp = 1.0 / bp;
   const double alpha = st->pAp * ibp * ibp;
   const int Lpad = L + 2 * w;
-  const long long npad = (long long)Lpad * Lpad * 3, R = (long long)L * L * 3;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const double* ov = y + npad;
+  const int WC = kSymTW + 2 * w, RG = symb_region(w), tpr = L / kSymTW;
+  const int KI = (w + kSymTH - 1) / kSymTH;
+  const long long ntile = symb_ntile(L);
+  constexpr int TE = kSymTH * kSymTW * 3;  // elements per tile
   double uu = 0.0;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
-       r += (long long)gridDim.x * blockDim.x) {
-    const long long pp = r / 3;
-    const int c = (int)(r - pp * 3);
-    const int ps = (int)(pp / L), pt = (int)(pp % L);
-    const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
-    const double yv = symb_fix_value(y[yi], y + npad, L, w, ps, pt, c);
-    const double xv = x[yi];
-    const double u = (yv - alpha * xv) * ibp - bp * vp[yi];
-    vp[yi] = xv * ibp;
-    y[yi] = u;
-    uu += u * u;
+  for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int I = (int)(tile / tpr), J = (int)(tile - (long long)I * tpr);
+    for (int e = threadIdx.x; e < TE; e += kLzThreads) {
+      const int h = e / (kSymTW * 3), rem = e - h * (kSymTW * 3);
+      const int j = rem / 3, c = rem - 3 * j;
+      const int ps = I * kSymTH + h, pt = J * kSymTW + j;
+      const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
+      double yv = y[yi];
+      for (int dI = 0; dI <= KI; ++dI) {
+        const int Ip = I - dI, rr = h + dI * kSymTH;
+        if (Ip < 0 || rr >= kSymTH + w) break;
+        for (int dJ = -1; dJ <= 1; ++dJ) {
+          if (dI == 0 && dJ == 0) continue;
+          const int Jp = J + dJ, cc = j - dJ * kSymTW;
+          if (Jp < 0 || Jp >= tpr || cc < -w || cc >= kSymTW + w) continue;
+          yv += ov[((long long)Ip * tpr + Jp) * RG + (rr * WC + cc + w) * 3 + c];
+        }
+      }
+      const double xv = x[yi];
+      const double u = (yv - alpha * xv) * ibp - bp * vp[yi];
+      vp[yi] = xv * ibp;
+      y[yi] = u;
+      uu += u * u;
+    }
   }
   uu = block_sum(uu, sh);
   if (threadIdx.x == 0) {
@@ -2389,8 +2412,8 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
         return err;
       }
       if (fused)
-        k_symb_lz_update<<<grid_for((long long)e->L * e->L * 3, 256, kRedBlocks), 256, 0, s>>>(
-            e->L, e->w, v, w, vp, kb, e->partb, e->lz);
+        k_symb_lz_update<<<(int)(symb_ntile(e->L) < kRedBlocks ? symb_ntile(e->L) : kRedBlocks),
+                           kLzThreads, 0, s>>>(e->L, e->w, v, w, vp, kb, e->partb, e->lz);
       else
         k_lz_step<<<gv, 256, 0, s>>>(npad, v, vp, w, kb, e->partb, e->lz);
       nl += 1;
