@@ -31,12 +31,16 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
                                                   AOp aop, BOp bop, OutOp out) {
   __shared__ double As[16 * MC * BG_LDA];
   __shared__ double Bs[BG_KC * BG_LDB];
-  __shared__ int kq[BG_KC];  // (q_s << 16 | q_t) * 4 + comp, -1 = padding
+  __shared__ long long aro[16 * MC], bco[16], akq[BG_KC], bkq[BG_KC];  // separable offsets
+  __shared__ int arp[16 * MC], bcp[16], kq[BG_KC];  // packed (s << 16 | t), -1 = none
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = (Lp + TB - 1) / TB;
   const int nbo = (wOut + TB - 1) / TB;
   const int side = 2 * nbo + 1;
   const long long ntiles = (long long)nb * nb * side * side;
+  const double* Ab = aop.base();
+  const double* Bb = bop.base();
+  const int wA = aop.hw(), wB_ = bop.hw();
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const long long mb = t / (side * side);
     const int ob = (int)(t - mb * side * side);
@@ -56,6 +60,21 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
     const int qt1 = imin(imin(i0t + nit - 1 + wa, j0t + njt - 1 + wb), Lp - 1);
     const int nqs = qs1 - qs0 + 1, nqt = qt1 - qt0 + 1;
     const int K = (nqs > 0 && nqt > 0) ? nqs * nqt * 3 : 0;
+    // per-tile row / column tables
+    if (threadIdx.x < 16 * MC) {
+      const int m = threadIdx.x;
+      const int lm = m / MC, mc = m - lm * MC;
+      const int ls = lm / TB, lt = lm - ls * TB;
+      const bool ok = lm < TB * TB && ls < nis && lt < nit;
+      arp[m] = ok ? (((i0s + ls) << 16) | (i0t + lt)) : -1;
+      aro[m] = ok ? aop.ipart(i0s + ls, i0t + lt, mc) : 0;
+    } else if (threadIdx.x >= 64 && threadIdx.x < 80) {
+      const int nn = threadIdx.x - 64;
+      const int ls = nn / TB, lt = nn - ls * TB;
+      const bool ok = nn < TB * TB && ls < njs && lt < njt;
+      bcp[nn] = ok ? (((j0s + ls) << 16) | (j0t + lt)) : -1;
+      bco[nn] = ok ? bop.ipart(j0s + ls, j0t + lt, 0) : 0;
+    }
     double c[MC][2];
 #pragma unroll
     for (int j = 0; j < MC; ++j) c[j][0] = c[j][1] = 0.0;
@@ -63,37 +82,53 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
       if (threadIdx.x < BG_KC) {
         const int kk = k0 + threadIdx.x;
         int code = -1;
+        long long ao = 0, bo = 0;
         if (kk < K) {
           const int pl = kk / 3, cc = kk - 3 * pl;
-          code = (((qs0 + pl / nqt) << 16) | (qt0 + pl % nqt)) * 4 + cc;
+          const int qs = qs0 + pl / nqt, qt = qt0 + pl % nqt;
+          code = (qs << 16) | qt;
+          ao = aop.qpart(qs, qt, cc);
+          bo = bop.qpart(qs, qt, cc);
         }
         kq[threadIdx.x] = code;
+        akq[threadIdx.x] = ao;
+        bkq[threadIdx.x] = bo;
       }
       __syncthreads();
-      // A: (16 MC) x 32
-      for (int e = threadIdx.x; e < 16 * MC * BG_KC; e += 128) {
-        const int m = e >> 5, kk = e & 31;
+      // A: (16 MC) x 32; thread: fixed k column, rows warp + 4 r
+      {
+        const int kk = threadIdx.x & 31;
         const int code = kq[kk];
-        double v = 0.0;
-        const int lm = m / MC, mc = m - lm * MC;
-        const int ls = lm / TB, lt = lm - ls * TB;
-        if (code >= 0 && lm < TB * TB && ls < nis && lt < nit) {
-          const int q = code >> 2;
-          v = aop(i0s + ls, i0t + lt, mc, q >> 16, q & 0xffff, code & 3);
+        const int qs = code >> 16, qt = code & 0xffff;
+        const long long ko = akq[kk];
+#pragma unroll
+        for (int r = 0; r < 4 * MC; ++r) {
+          const int m = warp + 4 * r;
+          const int rp = arp[m];
+          double v = 0.0;
+          if (code >= 0 && rp >= 0) {
+            const int ds = qs - (rp >> 16), dt = qt - (rp & 0xffff);
+            if (ds >= -wA && ds <= wA && dt >= -wA && dt <= wA) v = Ab[aro[m] + ko];
+          }
+          As[m * BG_LDA + kk] = v;
         }
-        As[m * BG_LDA + kk] = v;
       }
-      // B: 32 x 16
-      for (int e = threadIdx.x; e < BG_KC * 16; e += 128) {
-        const int kk = e >> 4, nn = e & 15;
-        const int code = kq[kk];
-        double v = 0.0;
-        const int ls = nn / TB, lt = nn - ls * TB;
-        if (code >= 0 && nn < TB * TB && ls < njs && lt < njt) {
-          const int q = code >> 2;
-          v = bop(q >> 16, q & 0xffff, code & 3, j0s + ls, j0t + lt);
+      // B: 32 x 16; thread: fixed column nn = t & 15, rows (t >> 4) + 8 r
+      {
+        const int nn = threadIdx.x & 15;
+        const int cp = bcp[nn];
+        const long long co = bco[nn];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int kk = (threadIdx.x >> 4) + 8 * r;
+          const int code = kq[kk];
+          double v = 0.0;
+          if (code >= 0 && cp >= 0) {
+            const int ds = (code >> 16) - (cp >> 16), dt = (code & 0xffff) - (cp & 0xffff);
+            if (ds >= -wB_ && ds <= wB_ && dt >= -wB_ && dt <= wB_) v = Bb[bkq[kk] + co];
+          }
+          Bs[kk * BG_LDB + nn] = v;
         }
-        Bs[kk * BG_LDB + nn] = v;
       }
       __syncthreads();
       const int nt = warp & 1;

@@ -731,9 +731,22 @@ __global__ void k_drop_by_rowmax(long long rows, long long S, double* __restrict
 // ---------------------------------------------------------------------------
 // operand / epilogue functors of the triple-product block GEMMs (gb_boxgemm.cuh)
 // ---------------------------------------------------------------------------
+// Every operand address is separable: addr = ipart(i) + qpart(q), valid for
+// |q - i| <= hw (slot_of is linear in the offset) -- the GEMM gathers with
+// two table lookups per element instead of the per-element index chain.
 struct OpBrows {  // A operand: B[(i,mc)][(q,c)]
   const double* B;
   int Lp, w, S;
+  __device__ const double* base() const { return B; }
+  __device__ int hw() const { return w; }
+  __device__ long long ipart(int is, int it, int mc) const {
+    const int W2 = 2 * w + 1;
+    return (((long long)is * Lp + it) * 3 + mc) * S - (long long)(is * W2 + it) * 3 +
+           (w * W2 + w) * 3;
+  }
+  __device__ long long qpart(int qs, int qt, int kc) const {
+    return (long long)(qs * (2 * w + 1) + qt) * 3 + kc;
+  }
   __device__ double operator()(int is, int it, int mc, int qs, int qt, int kc) const {
     const int ds = qs - is, dt = qt - it;
     if (ds < -w || ds > w || dt < -w || dt > w) return 0.0;
@@ -743,6 +756,15 @@ struct OpBrows {  // A operand: B[(i,mc)][(q,c)]
 struct OpDtRowsA {  // A operand: Dt[i][(q,c)]
   const double* Dt;
   int Lp, rho, S;
+  __device__ const double* base() const { return Dt; }
+  __device__ int hw() const { return rho; }
+  __device__ long long ipart(int is, int it, int) const {
+    const int W2 = 2 * rho + 1;
+    return ((long long)is * Lp + it) * S - (long long)(is * W2 + it) * 3 + (rho * W2 + rho) * 3;
+  }
+  __device__ long long qpart(int qs, int qt, int kc) const {
+    return (long long)(qs * (2 * rho + 1) + qt) * 3 + kc;
+  }
   __device__ double operator()(int is, int it, int, int qs, int qt, int kc) const {
     const int ds = qs - is, dt = qt - it;
     if (ds < -rho || ds > rho || dt < -rho || dt > rho) return 0.0;
@@ -752,6 +774,15 @@ struct OpDtRowsA {  // A operand: Dt[i][(q,c)]
 struct OpDtRowsB {  // B operand: Dt[j][(q,c)]  (i.e. D)
   const double* Dt;
   int Lp, rho, S;
+  __device__ const double* base() const { return Dt; }
+  __device__ int hw() const { return rho; }
+  __device__ long long ipart(int js, int jt, int) const {
+    const int W2 = 2 * rho + 1;
+    return ((long long)js * Lp + jt) * S - (long long)(js * W2 + jt) * 3 + (rho * W2 + rho) * 3;
+  }
+  __device__ long long qpart(int qs, int qt, int kc) const {
+    return (long long)(qs * (2 * rho + 1) + qt) * 3 + kc;
+  }
   __device__ double operator()(int qs, int qt, int kc, int js, int jt) const {
     const int ds = qs - js, dt = qt - jt;
     if (ds < -rho || ds > rho || dt < -rho || dt > rho) return 0.0;
@@ -761,6 +792,15 @@ struct OpDtRowsB {  // B operand: Dt[j][(q,c)]  (i.e. D)
 struct OpGcols {  // A operand: G^T, G[(q,c)][i]
   const double* G;
   int Lp, w, S;
+  __device__ const double* base() const { return G; }
+  __device__ int hw() const { return w; }
+  __device__ long long ipart(int is, int it, int) const {
+    return (long long)is * (2 * w + 1) + it;
+  }
+  __device__ long long qpart(int qs, int qt, int kc) const {
+    const int W2 = 2 * w + 1;
+    return (((long long)qs * Lp + qt) * 3 + kc) * S - (long long)(qs * W2 + qt) + (w * W2 + w);
+  }
   __device__ double operator()(int is, int it, int, int qs, int qt, int kc) const {
     const int ds = is - qs, dt = it - qt;
     if (ds < -w || ds > w || dt < -w || dt > w) return 0.0;
@@ -770,6 +810,15 @@ struct OpGcols {  // A operand: G^T, G[(q,c)][i]
 struct OpBDrows {  // B operand: BD[(q,c)][j]
   const double* BD;
   int Lp, w, S;
+  __device__ const double* base() const { return BD; }
+  __device__ int hw() const { return w; }
+  __device__ long long ipart(int js, int jt, int) const {
+    return (long long)js * (2 * w + 1) + jt;
+  }
+  __device__ long long qpart(int qs, int qt, int kc) const {
+    const int W2 = 2 * w + 1;
+    return (((long long)qs * Lp + qt) * 3 + kc) * S - (long long)(qs * W2 + qt) + (w * W2 + w);
+  }
   __device__ double operator()(int qs, int qt, int kc, int js, int jt) const {
     const int ds = js - qs, dt = jt - qt;
     if (ds < -w || ds > w || dt < -w || dt > w) return 0.0;
