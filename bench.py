@@ -33,6 +33,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
+    "c0": dict(q=5, coeff="example1", exact=True),
     "c1": dict(q=7, coeff="example1"),
     "c2": dict(q=10, coeff="checker"),
     "c3": dict(q=12, coeff="checker"),
@@ -222,6 +223,59 @@ def whole_job_rate(dofs_per_rank, world, ms):
     """Weak scaling over independent instances: every rank solves N fine DOFs;
     the job rate is world * N per (max-over-ranks) step time."""
     return world * dofs_per_rank / (ms * 1e-3)
+
+
+def run_exact(args, rank, world, local_rank):
+    """BASELINE configs[0]: exact (global) gamblets, q=5, through the public
+    exact_solve with host inputs in tight mode (tol 1e-14); each step is one
+    complete call (uploads, dense sweep, reassembly, u download)."""
+    import torch
+    import paper_1503_03467_b200 as gb
+    from paper_1503_03467_b200 import _native as nat, device as dv
+    torch.cuda.set_device(local_rank)
+    cfg = CONFIGS[args.config]
+    q = args.q or cfg["q"]
+    N = 4 ** q
+    grid, M, A, load, tree = build_inputs(q, cfg["coeff"], rank)
+
+    def step():
+        sol, _ = gb.exact_solve(M, A, load, tree, tol_mass=1e-14, tol_subband=1e-14)
+        return sol.u
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = nat.query("gb_launch_count")
+    dv.Traffic.reset()
+    with ClockSampler(local_rank) as clk:
+        ts = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            step()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+    launches = nat.query("gb_launch_count") - launches0
+    ms = reduce_max(float(np.median(ts)), world, "cuda")
+    if rank != 0:
+        return None
+    value = whole_job_rate(N, world, ms)
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": "fine-DOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators: example1 coefficient and load)",
+        "config": {"workload": f"c0: q={q}, N={N} fine DOFs, exact (global) gamblets, "
+                               "tight mode tol 1e-14", "q": q, "fine_dofs": N,
+                   "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
+        "e2e": {"value": round(value, 1), "unit": "fine-DOF/s", "ms_per_step": round(ms, 3),
+                "h2d_bytes_per_step": int(dv.Traffic.h2d / max(1, args.steps)),
+                "d2h_bytes_per_step": int(dv.Traffic.d2h / max(1, args.steps))},
+        "gpu_launches": int(launches), "roofline": None,
+        "note": "launch/latency-bound dense path (SURVEY 8(d): ~6.4 GFlop total); "
+                "value is measured through the public call with host inputs",
+        "clocks": clk.summary(), "step_ms": [round(t, 2) for t in ts],
+    }
 
 
 def run_ours(args, rank, world, local_rank):
@@ -432,6 +486,33 @@ def run_reference(args, rank):
         return None
     cfg = CONFIGS[args.config]
     threads = os.cpu_count() or 1
+    if cfg.get("exact"):  # config 0: the whole q=5 exact sweep fits a CPU step
+        from threadpoolctl import threadpool_limits
+        from oracle import gamblets_oracle as O
+        q = cfg["q"]
+        grid, M, A, load, tree = build_inputs(q, cfg["coeff"])
+        times = []
+        with threadpool_limits(threads):
+            for i in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                O.exact_solve(M, A, load.b, q)
+                if i >= args.warmup:
+                    times.append(time.perf_counter() - t0)
+        dt = float(np.median(times))
+        value = 4 ** q / dt
+        sample = (f"oracle/gamblets_oracle.exact_solve (dense direct restatement of the "
+                  f"reference's exact sweep), the full q={q} config per step")
+        return {
+            "impl": "reference", "metric": METRIC, "value": round(value, 2),
+            "unit": "fine-DOF/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} (q={q}, exact)"},
+            "cpu_baseline": {"value": round(value, 2), "unit": "fine-DOF/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 2), "unit": "fine-DOF/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
     times = []
     for i in range(args.warmup + args.steps):
         v, dt = cpu_oracle_sample(cfg["coeff"], threads)
@@ -483,7 +564,8 @@ def main():
             import torch
             torch.cuda.set_device(local_rank)
             torch.distributed.init_process_group("nccl")
-        out = run_ours(args, rank, world, local_rank)
+        runner = run_exact if CONFIGS[args.config].get("exact") else run_ours
+        out = runner(args, rank, world, local_rank)
         if world > 1:
             import torch
             torch.distributed.destroy_process_group()
