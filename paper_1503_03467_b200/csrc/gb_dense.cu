@@ -10,6 +10,9 @@
 //
 // config 0 is launch/latency bound (6.4 GFlop total); these
 // kernels aim for correctness and reasonable DFMA use, not peak.
+#include <cublas_v2.h>
+#include <stdlib.h>
+
 #include "gb_common.cuh"
 
 namespace gb {
@@ -105,6 +108,115 @@ __global__ void k_potrf_panel(int n, int j0, int nb, double* __restrict__ A, int
       for (int kk = 0; kk < j; ++kk) v -= ai[kk] * a[(long long)j * lda + kk];
       ai[j] = v / a[(long long)j * lda + j];
     }
+  }
+}
+
+// Cholesky of the nb x nb (nb <= 64) diagonal block at (j0, j0) in shared
+// memory by one CTA (right-looking); L11 written back (lower part).
+constexpr int kDnb = 64;
+__global__ void __launch_bounds__(256) k_potrf_diag(int j0, int nb, double* __restrict__ A,
+                                                    int lda, long long* status) {
+  __shared__ double t[kDnb * (kDnb + 1)];
+  __shared__ int bad;
+  const int tid = threadIdx.x, LD = kDnb + 1;
+  double* a = A + (long long)j0 * lda + j0;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, k = e - i * nb;
+    t[i * LD + k] = (k <= i) ? a[(long long)i * lda + k] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double d = t[j * LD + j];
+    if (!(d > 0.0)) {
+      if (tid == 0) {
+        bad = 1;
+        raise_status(status, ST_NOT_SPD, j0 + j);
+      }
+      return;
+    }
+    const double l = sqrt(d);
+    __syncthreads();
+    for (int i = j + 1 + tid; i < nb; i += blockDim.x) t[i * LD + j] /= l;
+    if (tid == 0) t[j * LD + j] = l;
+    __syncthreads();
+    for (int e = tid; e < (nb - j - 1) * (nb - j - 1); e += blockDim.x) {
+      const int i = j + 1 + e / (nb - j - 1), k = j + 1 + e % (nb - j - 1);
+      if (k <= i) t[i * LD + k] -= t[i * LD + j] * t[k * LD + j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, k = e - i * nb;
+    if (k <= i) a[(long long)i * lda + k] = t[i * LD + k];
+  }
+}
+
+// panel below the diagonal block: rows i >= j0 + nb solve x L11^T = a_i, a
+// warp per row (column-oriented: x_j /= L_jj, then x_k -= x_j L_kj, k > j),
+// L11 staged in shared memory
+__global__ void __launch_bounds__(256) k_potrf_trsm(int n, int j0, int nb, double* __restrict__ A,
+                                                    int lda) {
+  __shared__ double l11[kDnb * (kDnb + 1)];
+  const int LD = kDnb + 1, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double* a = A + (long long)j0 * lda + j0;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, k = e - i * nb;
+    l11[i * LD + k] = (k <= i) ? a[(long long)i * lda + k] : 0.0;
+  }
+  __syncthreads();
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int i = j0 + nb + blockIdx.x * (blockDim.x >> 5) + w; i < n; i += nwarps) {
+    double* ai = A + (long long)i * lda + j0;
+    double x0 = lane < nb ? ai[lane] : 0.0, x1 = lane + 32 < nb ? ai[lane + 32] : 0.0;
+    for (int j = 0; j < nb; ++j) {
+      const double xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31) / l11[j * LD + j];
+      if (lane == (j & 31)) {
+        if (j < 32) x0 = xj;
+        else x1 = xj;
+      }
+      if (lane > j) x0 = fma(-xj, l11[lane * LD + j], x0);
+      if (lane + 32 > j && lane + 32 < nb) x1 = fma(-xj, l11[(lane + 32) * LD + j], x1);
+    }
+    if (lane < nb) ai[lane] = x0;
+    if (lane + 32 < nb) ai[lane + 32] = x1;
+  }
+}
+
+// diagonal-block triangular solves for many right-hand sides with the block
+// staged in shared memory: thread per column, column-oriented updates
+__global__ void __launch_bounds__(128) k_trsv_smem(int j0, int nb, int nrhs,
+                                                   const double* __restrict__ L, int lda,
+                                                   double* __restrict__ X, int ldx, int fwd) {
+  extern __shared__ double dsm[];
+  double* lb = dsm;                      // kDnb x (kDnb + 1)
+  double* xs = dsm + kDnb * (kDnb + 1);  // kDnb x 128
+  const int LD = kDnb + 1;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, k = e - i * nb;
+    lb[i * LD + k] = (k <= i) ? L[(long long)(j0 + i) * lda + j0 + k] : 0.0;
+  }
+  for (int c0 = blockIdx.x * 128; c0 < nrhs; c0 += gridDim.x * 128) {
+    const int c = c0 + threadIdx.x;
+    __syncthreads();
+    for (int i = 0; i < nb; ++i)
+      xs[i * 128 + threadIdx.x] = c < nrhs ? X[(long long)(j0 + i) * ldx + c] : 0.0;
+    __syncthreads();
+    if (fwd) {
+      for (int i = 0; i < nb; ++i) {
+        const double v = xs[i * 128 + threadIdx.x] / lb[i * LD + i];
+        xs[i * 128 + threadIdx.x] = v;
+        for (int k = i + 1; k < nb; ++k) xs[k * 128 + threadIdx.x] -= lb[k * LD + i] * v;
+      }
+    } else {
+      for (int i = nb - 1; i >= 0; --i) {
+        const double v = xs[i * 128 + threadIdx.x] / lb[i * LD + i];
+        xs[i * 128 + threadIdx.x] = v;
+        for (int k = 0; k < i; ++k) xs[k * 128 + threadIdx.x] -= lb[i * LD + k] * v;
+      }
+    }
+    if (c < nrhs)
+      for (int i = 0; i < nb; ++i) X[(long long)(j0 + i) * ldx + c] = xs[i * 128 + threadIdx.x];
   }
 }
 
@@ -252,10 +364,26 @@ __global__ void k_dmma_probe(int iters, double* sink) {
 
 using namespace gb;
 
+// plain dense GEMMs go to cuBLAS (row-major C = op(A) op(B) is the
+// column-major C^T = op(B)^T op(A)^T); GB_DENSE_GEMM=own selects k_dgemm
+static cublasHandle_t g_cublas = nullptr;
+static int g_own_gemm = -1;
 int gbk_dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta,
                    const double* B, int ldb, int tb, double beta, double* C, int ldc,
                    cudaStream_t s) {
   if (m <= 0 || n <= 0) return 0;
+  if (g_own_gemm < 0) {
+    const char* e = getenv("GB_DENSE_GEMM");
+    g_own_gemm = (e && e[0] == 'o') ? 1 : 0;
+  }
+  if (!g_own_gemm) {
+    if (!g_cublas && cublasCreate(&g_cublas) != CUBLAS_STATUS_SUCCESS) return 999;
+    if (cublasSetStream(g_cublas, s) != CUBLAS_STATUS_SUCCESS) return 999;
+    const cublasStatus_t st =
+        cublasDgemm(g_cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n,
+                    m, k, &alpha, B, ldb, A, lda, &beta, C, ldc);
+    return st == CUBLAS_STATUS_SUCCESS ? 0 : 999;
+  }
   dim3 grid((n + TN - 1) / TN, (m + TM - 1) / TM);
   k_dgemm<<<grid, 256, 0, s>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
   return (int)cudaGetLastError();
@@ -265,9 +393,11 @@ int gbk_dense_potrf(int n, double* A, int lda, long long* status, cudaStream_t s
   const int nb = 64;
   for (int j0 = 0; j0 < n; j0 += nb) {
     const int b = (n - j0) < nb ? (n - j0) : nb;
-    k_potrf_panel<<<1, 256, 0, s>>>(n, j0, b, A, lda, status);
+    k_potrf_diag<<<1, 256, 0, s>>>(j0, b, A, lda, status);
     const int r0 = j0 + b, m = n - r0;
     if (m > 0) {
+      const int g = (m + 7) / 8 < 148 ? (m + 7) / 8 : 148;
+      k_potrf_trsm<<<g, 256, 0, s>>>(n, j0, b, A, lda);
       // A22 -= L21 L21^T  (full trailing block; upper part is ignored)
       int e = gbk_dense_gemm(m, m, b, -1.0, A + (long long)r0 * lda + j0, lda, 0,
                              A + (long long)r0 * lda + j0, lda, 1, 1.0,
@@ -283,10 +413,12 @@ int gbk_dense_potrs(int n, int nrhs, const double* L, int lda, double* X, int ld
                     cudaStream_t s) {
   const int nb = 64;
   const int g = (nrhs + 127) / 128;
+  const size_t trsv_smem = (size_t)(kDnb * (kDnb + 1) + kDnb * 128) * sizeof(double);
+  cudaFuncSetAttribute(k_trsv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsv_smem);
   // forward: L Y = B
   for (int j0 = 0; j0 < n; j0 += nb) {
     const int b = (n - j0) < nb ? (n - j0) : nb;
-    k_trsv_block<<<g, 128, 0, s>>>(j0, b, nrhs, L, lda, X, ldx, 1);
+    k_trsv_smem<<<g, 128, trsv_smem, s>>>(j0, b, nrhs, L, lda, X, ldx, 1);
     const int r0 = j0 + b, m = n - r0;
     if (m > 0) {
       int e = gbk_dense_gemm(m, nrhs, b, -1.0, L + (long long)r0 * lda + j0, lda, 0,
@@ -300,7 +432,7 @@ int gbk_dense_potrs(int n, int nrhs, const double* L, int lda, double* X, int ld
   for (int bi = nblk - 1; bi >= 0; --bi) {
     const int j0 = bi * nb;
     const int b = (n - j0) < nb ? (n - j0) : nb;
-    k_trsv_block<<<g, 128, 0, s>>>(j0, b, nrhs, L, lda, X, ldx, 0);
+    k_trsv_smem<<<g, 128, trsv_smem, s>>>(j0, b, nrhs, L, lda, X, ldx, 0);
     if (j0 > 0) {
       // X[0:j0] -= L[j0:j0+b, 0:j0]^T X[j0:j0+b]
       int e = gbk_dense_gemm(j0, nrhs, b, -1.0, L + (long long)j0 * lda, lda, 1,
