@@ -363,6 +363,10 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = []
     h2d = d2h = 0
     levels = parts = None  # the device leg's last outputs are not needed any more
+    Md = Ad = gd = None    # nor its device-resident inputs (3.9 GB at q=12)
+    res = None
+    # one untimed call first: the allocator adapts to the host-input pattern
+    res = gb.fast_solve(M, A, load, tree, EPS, uniform_rho=RHO, c_tol=CTOL, lean=lean)
     res = None
     for i in range(max(1, args.steps)):
         res = None  # as in the device leg: one solve's operators live at a time
