@@ -26,6 +26,9 @@ namespace gb {
 
 __device__ __forceinline__ int fpos(int r, int c) { return ((c >> 2) << 5) + (r << 2) + (c & 3); }
 
+#ifndef GB_V3_MINB
+#define GB_V3_MINB 6
+#endif
 constexpr int kV3Warps = 4;
 
 struct V3Smem {
@@ -90,7 +93,7 @@ __device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, 
   for (int r = tl >> 3; r < 8; r += step) col[(T - kt) * 64 + r * 8 + c] = (r == 0) ? S.z[l2] : 0.0;
 }
 
-__global__ void __launch_bounds__(32 * kV3Warps, 6) k_correction_patches_v3(
+__global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patches_v3(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB, int wG,
     const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status, int Tmax,
     double* __restrict__ scratch) {
