@@ -77,21 +77,39 @@ __device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, 
   const int p2 = cval ? S.ploc[l2] : 0;
   const double s2 = cval ? S.sl[l2] : 0.0;
   const int step = nt >> 3;
-#pragma unroll 4
-  for (int l1 = 8 * kt + (tl >> 3); l1 < 8 * T; l1 += step) {
-    double v = 0.0;
-    if (l1 < m && cval) {
-      const int p1 = S.ploc[l1];
-      const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
-      if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
-        v = __ldg(B + S.rowb[l1] + ck) * S.sl[l1] * s2;
-    } else if (l1 == l2) {
-      v = 1.0;  // padding rows: unit diagonal
+  // kGU independent loads in flight per thread (the box reads are L2 latency
+  // bound); values are written in a second pass
+  constexpr int kGU = 8;
+  for (int l1b = 8 * kt + (tl >> 3); l1b < 8 * T; l1b += kGU * step) {
+    double v[kGU];
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const int l1 = l1b + u * step;
+      v[u] = 0.0;
+      if (l1 < m && cval) {
+        const int p1 = S.ploc[l1];
+        const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
+        if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
+          v[u] = __ldg(B + S.rowb[l1] + ck) * S.sl[l1] * s2;
+      } else if (l1 == l2) {
+        v[u] = 1.0;  // padding rows: unit diagonal
+      }
     }
-    col[(l1 - 8 * kt) * 8 + c] = v;
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const int l1 = l1b + u * step;
+      if (l1 < 8 * T) col[(l1 - 8 * kt) * 8 + c] = v[u];
+    }
   }
   for (int r = tl >> 3; r < 8; r += step) col[(T - kt) * 64 + r * 8 + c] = (r == 0) ? S.z[l2] : 0.0;
 }
+
+// 16-byte global -> shared copies (LDGSTS, L2 only); completion via v3_cp_wait
+__device__ __forceinline__ void v3_cp16(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void v3_cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patches_v3(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB, int wG,
@@ -214,10 +232,11 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
         for (int e = lane; e < 64; e += 32) dt_[fpos(e >> 3, e & 7)] = S.dg[eidx(e >> 3, e & 7)];
       } else if (kt + 1 < T) {
         // meanwhile: column kt + 1 and the finished part of L row kt + 1
-        v3_gather(S, nxt, kt + 1, T, m, wB, B, threadIdx.x - 32, blockDim.x - 32);
         const double* src = L + (long long)(((kt + 1) * (kt + 2)) >> 1) * 64;
-        for (int e = threadIdx.x - 32; e < kt * 64; e += blockDim.x - 32)
-          S.lrow[e] = __ldcg(src + e);
+        for (int e = 2 * (threadIdx.x - 32); e < kt * 64; e += 2 * (blockDim.x - 32))
+          v3_cp16(S.lrow + e, src + e);
+        v3_gather(S, nxt, kt + 1, T, m, wB, B, threadIdx.x - 32, blockDim.x - 32);
+        v3_cp_wait();
       }
       __syncthreads();
       if (*S.flag) {
@@ -250,37 +269,53 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
       __syncthreads();
       continue;
     }
-    // back substitution L^T z = y (y = row 0 of the RHS tiles (T, jt)), one
-    // warp: step it, the 4 lane groups split the tiles jt > it
-    if (warp == 0) {
+    // back substitution L^T z = y (y = row 0 of the RHS tiles (T, jt)),
+    // column oriented over all warps: step it finishes z_it = L_ii^-T y_it
+    // (8 threads) and then subtracts L(it, jt)^T z_it from every y_jt, jt <
+    // it (one thread per (jt, column)).  Row it of the packed factor (tiles
+    // jt = 0..it, the diagonal one holding L_ii^-1) is staged into the idle
+    // column buffers by cp.async one step ahead.
+    {
       const double* yrow = L + (long long)((T * (T + 1)) >> 1) * 64;
-      for (int e = lane; e < 8 * T; e += 32) S.z[e] = __ldcg(yrow + (e >> 3) * 64 + fpos(0, e & 7));
-      __syncwarp();
-      const int r = lane & 7, cg = lane >> 3;
-      for (int it = T - 1; it >= 0; --it) {
-        double acc = 0.0;
-        for (int jt = it + 1 + cg; jt < T; jt += 4) {
-          const double* t = L + (long long)(((jt * (jt + 1)) >> 1) + it) * 64;
-          const double* zj = S.z + 8 * jt;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc = fma(__ldcg(t + fpos(k, r)), zj[k], acc);
-        }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-        const double v = S.z[8 * it + r] - acc;
-        const double* li = L + (long long)(((it * (it + 1)) >> 1) + it) * 64;
-        double zr = 0.0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double vc = __shfl_sync(0xffffffffu, v, c);
-          if (c >= r) zr = fma(__ldcg(li + fpos(c, r)), vc, zr);
-        }
-        __syncwarp();
-        if (lane < 8) S.z[8 * it + lane] = zr;
-        __syncwarp();
+      for (int e = threadIdx.x; e < 8 * T; e += blockDim.x)
+        S.z[e] = __ldcg(yrow + (e >> 3) * 64 + fpos(0, e & 7));
+      {
+        const int it = T - 1;
+        const double* src = L + (long long)((it * (it + 1)) >> 1) * 64;
+        for (int e = 2 * threadIdx.x; e < (it + 1) * 64; e += 2 * blockDim.x)
+          v3_cp16(S.col + (it & 1) * colstride + e, src + e);
       }
+      for (int it = T - 1; it >= 0; --it) {
+        v3_cp_wait();
+        __syncthreads();  // row it staged, y_it final, buffer (it - 1) & 1 free
+        if (it > 0) {
+          const double* src = L + (long long)(((it - 1) * it) >> 1) * 64;
+          for (int e = 2 * threadIdx.x; e < it * 64; e += 2 * blockDim.x)
+            v3_cp16(S.col + ((it - 1) & 1) * colstride + e, src + e);
+        }
+        const double* row = S.col + (it & 1) * colstride;
+        if (threadIdx.x < 8) {
+          const int r = threadIdx.x;
+          const double* li = row + it * 64;
+          double zr = 0.0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c >= r) zr = fma(li[fpos(c, r)], S.z[8 * it + c], zr);
+          S.sl[8 * Tmax + r] = zr;
+        }
+        __syncthreads();
+        if (threadIdx.x < 8) S.z[8 * it + threadIdx.x] = S.sl[8 * Tmax + threadIdx.x];
+        for (int o = threadIdx.x; o < 8 * it; o += blockDim.x) {
+          const int jt = o >> 3, c = o & 7;
+          const double* t = row + jt * 64;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = fma(t[fpos(k, c)], S.sl[8 * Tmax + k], acc);
+          S.z[o] -= acc;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
     // D = s z and the row-tail trim of this column of D (as v2)
     double mx = 0.0;
     for (int l = threadIdx.x; l < m; l += blockDim.x) {
