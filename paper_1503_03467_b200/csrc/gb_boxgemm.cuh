@@ -29,10 +29,12 @@ constexpr int BG_KC = 32, BG_LDA = 36, BG_LDB = 20;
 template <int MC, class AOp, class BOp, class OutOp>
 __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb, int wOut,
                                                   AOp aop, BOp bop, OutOp out) {
-  __shared__ double As[16 * MC * BG_LDA];
-  __shared__ double Bs[BG_KC * BG_LDB];
-  __shared__ long long aro[16 * MC], bco[16], akq[BG_KC], bkq[BG_KC];  // separable offsets
-  __shared__ int arp[16 * MC], bcp[16], kq[BG_KC];  // packed (s << 16 | t), -1 = none
+  // double-buffered: chunk c + 1 is gathered into registers while chunk c is
+  // multiplied (the operand gathers are L2-latency bound)
+  __shared__ double As[2][16 * MC * BG_LDA];
+  __shared__ double Bs[2][BG_KC * BG_LDB];
+  __shared__ long long aro[16 * MC], bco[16], akq[2][BG_KC], bkq[2][BG_KC];  // separable offsets
+  __shared__ int arp[16 * MC], bcp[16], kq[2][BG_KC];  // packed (s << 16 | t), -1 = none
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = (Lp + TB - 1) / TB;
   const int nbo = (wOut + TB - 1) / TB;
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
     double c[MC][2];
 #pragma unroll
     for (int j = 0; j < MC; ++j) c[j][0] = c[j][1] = 0.0;
-    for (int k0 = 0; k0 < K; k0 += BG_KC) {
+    auto meta = [&](int k0, int u) {
       if (threadIdx.x < BG_KC) {
         const int kk = k0 + threadIdx.x;
         int code = -1;
@@ -90,17 +92,20 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
           ao = aop.qpart(qs, qt, cc);
           bo = bop.qpart(qs, qt, cc);
         }
-        kq[threadIdx.x] = code;
-        akq[threadIdx.x] = ao;
-        bkq[threadIdx.x] = bo;
+        kq[u][threadIdx.x] = code;
+        akq[u][threadIdx.x] = ao;
+        bkq[u][threadIdx.x] = bo;
       }
-      __syncthreads();
-      // A: (16 MC) x 32; thread: fixed k column, rows warp + 4 r
+    };
+    double ra[4 * MC], rb[4];
+    // A: (16 MC) x 32; thread: fixed k column, rows warp + 4 r.
+    // B: 32 x 16; thread: fixed column nn = t & 15, rows (t >> 4) + 8 r
+    auto gather = [&](int u) {
       {
         const int kk = threadIdx.x & 31;
-        const int code = kq[kk];
+        const int code = kq[u][kk];
         const int qs = code >> 16, qt = code & 0xffff;
-        const long long ko = akq[kk];
+        const long long ko = akq[u][kk];
 #pragma unroll
         for (int r = 0; r < 4 * MC; ++r) {
           const int m = warp + 4 * r;
@@ -110,10 +115,9 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
             const int ds = qs - (rp >> 16), dt = qt - (rp & 0xffff);
             if (ds >= -wA && ds <= wA && dt >= -wA && dt <= wA) v = Ab[aro[m] + ko];
           }
-          As[m * BG_LDA + kk] = v;
+          ra[r] = v;
         }
       }
-      // B: 32 x 16; thread: fixed column nn = t & 15, rows (t >> 4) + 8 r
       {
         const int nn = threadIdx.x & 15;
         const int cp = bcp[nn];
@@ -121,29 +125,43 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int kk = (threadIdx.x >> 4) + 8 * r;
-          const int code = kq[kk];
+          const int code = kq[u][kk];
           double v = 0.0;
           if (code >= 0 && cp >= 0) {
             const int ds = (code >> 16) - (cp >> 16), dt = (code & 0xffff) - (cp & 0xffff);
-            if (ds >= -wB_ && ds <= wB_ && dt >= -wB_ && dt <= wB_) v = Bb[bkq[kk] + co];
+            if (ds >= -wB_ && ds <= wB_ && dt >= -wB_ && dt <= wB_) v = Bb[bkq[u][kk] + co];
           }
-          Bs[kk * BG_LDB + nn] = v;
+          rb[r] = v;
         }
       }
+    };
+    if (K > 0) {
+      meta(0, 0);
+      __syncthreads();  // also publishes the row / column tables
+      gather(0);
+    }
+    for (int k0 = 0, cb = 0; k0 < K; k0 += BG_KC, cb ^= 1) {
+#pragma unroll
+      for (int r = 0; r < 4 * MC; ++r) As[cb][(warp + 4 * r) * BG_LDA + (threadIdx.x & 31)] = ra[r];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) Bs[cb][((threadIdx.x >> 4) + 8 * r) * BG_LDB + (threadIdx.x & 15)] = rb[r];
+      const bool more = k0 + BG_KC < K;
+      if (more) meta(k0 + BG_KC, cb ^ 1);
       __syncthreads();
+      if (more) gather(cb ^ 1);
       const int nt = warp & 1;
 #pragma unroll
       for (int ks = 0; ks < BG_KC / 4; ++ks) {
-        const double b = Bs[(ks * 4 + (lane & 3)) * BG_LDB + nt * 8 + (lane >> 2)];
+        const double b = Bs[cb][(ks * 4 + (lane & 3)) * BG_LDB + nt * 8 + (lane >> 2)];
 #pragma unroll
         for (int j = 0; j < MC; ++j) {
           const int mt = (warp >> 1) + 2 * j;
-          const double a = As[(mt * 8 + (lane >> 2)) * BG_LDA + ks * 4 + (lane & 3)];
+          const double a = As[cb][(mt * 8 + (lane >> 2)) * BG_LDA + ks * 4 + (lane & 3)];
           dmma_884b(c[j][0], c[j][1], a, b);
         }
       }
-      __syncthreads();
     }
+    __syncthreads();  // tables and buffers are rewritten by the next tile
     // epilogue
     const int nt = warp & 1;
 #pragma unroll

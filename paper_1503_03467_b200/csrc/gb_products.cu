@@ -553,10 +553,12 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
                                                       PsiWin out, double* __restrict__ psi_next,
                                                       double* __restrict__ rowmax, int TB, int nfs,
                                                       int nft) {
-  __shared__ double As[16 * PN_LDA];
-  __shared__ double Bs[PN_KC * PN_LDB];
-  __shared__ long long kbase[PN_KC];  // Wpsi row offset of k column, -1 = padding
-  __shared__ int kps[PN_KC], kpt[PN_KC], kc[PN_KC], kos[PN_KC], kot[PN_KC];
+  // double-buffered: chunk c + 1 is gathered into registers while chunk c
+  // is multiplied (the gathers are L2-latency bound)
+  __shared__ double As[2][16 * PN_LDA];
+  __shared__ double Bs[2][PN_KC * PN_LDB];
+  __shared__ long long kbase[2][PN_KC];  // Wpsi row offset of k column, -1 = padding
+  __shared__ int kps[2][PN_KC], kpt[2][PN_KC], kc[2][PN_KC], kos[2][PN_KC], kot[2][PN_KC];
   const int Lp = out.L;
   const int nbs = (Lp + TB - 1) / TB;
   const long long nblk = (long long)nbs * nbs;
@@ -596,7 +598,10 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     const bool arow = am < TB * TB && ams < nrs && amt < nrt;
     const int ais = bi_s + ams, ait = bi_t + amt;
     const double* drow = Dt + ((long long)ais * Lp + ait) * SD;
-    for (int k0 = 0; k0 < K; k0 += PN_KC) {
+    const int n_ = threadIdx.x & 31;
+    const int bfs = F0s + (n_ >> 2), bft = F0t + (n_ & 3);
+    // chunk metadata (threads < PN_KC) into buffer u
+    auto meta = [&](int k0, int u) {
       if (threadIdx.x < PN_KC) {
         const int kk = k0 + threadIdx.x;
         long long base = -1;
@@ -610,55 +615,67 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
           os = par.origin(ps);
           ot = par.origin(pt);
         }
-        kbase[threadIdx.x] = base;
-        kps[threadIdx.x] = ps;
-        kpt[threadIdx.x] = pt;
-        kc[threadIdx.x] = cc;
-        kos[threadIdx.x] = os;
-        kot[threadIdx.x] = ot;
+        kbase[u][threadIdx.x] = base;
+        kps[u][threadIdx.x] = ps;
+        kpt[u][threadIdx.x] = pt;
+        kc[u][threadIdx.x] = cc;
+        kos[u][threadIdx.x] = os;
+        kot[u][threadIdx.x] = ot;
       }
-      __syncthreads();
-      // A: 16 rows x 32 k (Dt values; 0 outside the row's ball / padding rows)
+    };
+    double ra[4], rb[8];
+    // gather A (16 rows x 32 k: Dt, 0 outside the row's ball / padding rows)
+    // and B (32 k x 32 fine points: Wpsi, 0 outside the parent's window)
+    auto gather = [&](int u) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int kk = (threadIdx.x & 7) + 8 * j;
         double v = 0.0;
-        if (arow && kbase[kk] >= 0) {
-          const int ds = kps[kk] - ais, dt = kpt[kk] - ait;
+        if (arow && kbase[u][kk] >= 0) {
+          const int ds = kps[u][kk] - ais, dt = kpt[u][kk] - ait;
           if (ds >= -rho && ds <= rho && dt >= -rho && dt <= rho)
-            v = drow[((ds + rho) * side + (dt + rho)) * 3 + kc[kk]];
+            v = drow[((ds + rho) * side + (dt + rho)) * 3 + kc[u][kk]];
         }
-        As[am * PN_LDA + kk] = v;
+        ra[j] = v;
       }
-      // B: 32 k x 32 fine points (Wpsi, 0 outside the parent's window)
-      {
-        const int n = threadIdx.x & 31;
-        const int fs = F0s + (n >> 2), ft = F0t + (n & 3);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int kk = (threadIdx.x >> 5) + 4 * j;
-          double v = 0.0;
-          const long long base = kbase[kk];
-          if (base >= 0) {
-            const int ls = fs - kos[kk], lt = ft - kot[kk];
-            if (ls >= 0 && ls < par.wd && lt >= 0 && lt < par.wd)
-              v = __ldg(Wpsi + base + ls * par.wd + lt);
-          }
-          Bs[kk * PN_LDB + n] = v;
+      for (int j = 0; j < 8; ++j) {
+        const int kk = (threadIdx.x >> 5) + 4 * j;
+        double v = 0.0;
+        const long long base = kbase[u][kk];
+        if (base >= 0) {
+          const int ls = bfs - kos[u][kk], lt = bft - kot[u][kk];
+          if (ls >= 0 && ls < par.wd && lt >= 0 && lt < par.wd)
+            v = __ldg(Wpsi + base + ls * par.wd + lt);
         }
+        rb[j] = v;
       }
+    };
+    if (K > 0) {
+      meta(0, 0);
       __syncthreads();
+      gather(0);
+    }
+    for (int k0 = 0, cb = 0; k0 < K; k0 += PN_KC, cb ^= 1) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) As[cb][am * PN_LDA + (threadIdx.x & 7) + 8 * j] = ra[j];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) Bs[cb][((threadIdx.x >> 5) + 4 * j) * PN_LDB + n_] = rb[j];
+      const bool more = k0 + PN_KC < K;
+      if (more) meta(k0 + PN_KC, cb ^ 1);
+      __syncthreads();
+      if (more) gather(cb ^ 1);
 #pragma unroll
       for (int ks = 0; ks < PN_KC / 4; ++ks) {
-        const double b = Bs[(ks * 4 + (lane & 3)) * PN_LDB + warp * 8 + (lane >> 2)];
+        const double b = Bs[cb][(ks * 4 + (lane & 3)) * PN_LDB + warp * 8 + (lane >> 2)];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-          const double a = As[(mt * 8 + (lane >> 2)) * PN_LDA + ks * 4 + (lane & 3)];
+          const double a = As[cb][(mt * 8 + (lane >> 2)) * PN_LDA + ks * 4 + (lane & 3)];
           dmma_acc(c[mt][0], c[mt][1], a, b);
         }
       }
-      __syncthreads();
     }
+    __syncthreads();  // buffers are reused by the next tile
     // epilogue: + 0.25 P psi, store inside each row's window, row max
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
