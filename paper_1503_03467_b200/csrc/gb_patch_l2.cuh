@@ -68,6 +68,27 @@ __device__ __forceinline__ V3Smem v3_carve(double* sm, int Tmax) {
 // threads tl = 0..nt-1 (nt a multiple of 8): thread tl owns column c = tl & 7
 // and rows l1 = 8 kt + (tl >> 3) + (nt / 8) j; entries are the reference's
 // congruence (B s_i) s_j (gamblet_fast.py:136)
+// 16-byte global -> shared copies (LDGSTS, L2 only); completion via v3_cp_wait
+__device__ __forceinline__ void v3_cp16(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void v3_cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// 8-byte global -> shared copy (LDGSTS through L1); completion via v3_cp_wait
+__device__ __forceinline__ void v3_cp8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+// gather column kt of B[chi, chi] (tiles (it, kt), it = kt..T-1, rows
+// l1 = 8 kt .. 8 T - 1, row-major) and the RHS tile (T, kt) into `col`, by
+// threads tl = 0..nt-1 (nt a multiple of 8): thread tl owns column c = tl & 7
+// and rows l1 = 8 kt + (tl >> 3) + (nt / 8) j.  Box entries are copied raw
+// and asynchronously (cp.async; the caller waits before its barrier); the
+// reference's congruence (B s_i) s_j (gamblet_fast.py:136) is applied when
+// the update phase first reads the column (v3 step (3)); padding rows hold
+// the unit diagonal and S.sl = 1 there.
 __device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, int T, int m,
                                           int wB, const double* __restrict__ B, int tl, int nt) {
   const int c = tl & 7;
@@ -75,41 +96,26 @@ __device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, 
   const bool cval = l2 < m;
   const long long ck = cval ? S.colk[l2] : 0;
   const int p2 = cval ? S.ploc[l2] : 0;
-  const double s2 = cval ? S.sl[l2] : 0.0;
   const int step = nt >> 3;
-  // kGU independent loads in flight per thread (the box reads are L2 latency
-  // bound); values are written in a second pass
-  constexpr int kGU = 8;
-  for (int l1b = 8 * kt + (tl >> 3); l1b < 8 * T; l1b += kGU * step) {
-    double v[kGU];
-#pragma unroll
-    for (int u = 0; u < kGU; ++u) {
-      const int l1 = l1b + u * step;
-      v[u] = 0.0;
-      if (l1 < m && cval) {
-        const int p1 = S.ploc[l1];
-        const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
-        if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB)
-          v[u] = __ldg(B + S.rowb[l1] + ck) * S.sl[l1] * s2;
-      } else if (l1 == l2) {
-        v[u] = 1.0;  // padding rows: unit diagonal
+#pragma unroll 4
+  for (int l1 = 8 * kt + (tl >> 3); l1 < 8 * T; l1 += step) {
+    double* dst = col + (l1 - 8 * kt) * 8 + c;
+    bool zero = true;
+    if (l1 < m && cval) {
+      const int p1 = S.ploc[l1];
+      const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
+      if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB) {
+        v3_cp8(dst, B + S.rowb[l1] + ck);
+        zero = false;
       }
+    } else if (l1 == l2) {
+      *dst = 1.0;  // padding rows: unit diagonal
+      zero = false;
     }
-#pragma unroll
-    for (int u = 0; u < kGU; ++u) {
-      const int l1 = l1b + u * step;
-      if (l1 < 8 * T) col[(l1 - 8 * kt) * 8 + c] = v[u];
-    }
+    if (zero) *dst = 0.0;
   }
   for (int r = tl >> 3; r < 8; r += step) col[(T - kt) * 64 + r * 8 + c] = (r == 0) ? S.z[l2] : 0.0;
 }
-
-// 16-byte global -> shared copies (LDGSTS, L2 only); completion via v3_cp_wait
-__device__ __forceinline__ void v3_cp16(double* dst, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void v3_cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patches_v3(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB, int wG,
@@ -150,6 +156,9 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
           g = G[r * SG + slot_of(wG, 1, ds, dt, 0)];
         v = sB[r] * (-g);
       }
+      else {
+        S.sl[l] = 1.0;  // padding rows: the deferred scaling leaves them as gathered
+      }
       S.z[l] = v;
       nrm += v * v;
     }
@@ -164,6 +173,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
     bool ok = true;
     const int colstride = (Tmax + 1) * 64;
     v3_gather(S, S.col, 0, T, m, wB, B, threadIdx.x, blockDim.x);
+    v3_cp_wait();
     __syncthreads();
     // step kt: [update column kt] | [warp 0: factor the diagonal tile;
     // warps 1..: gather column kt + 1, stage L(kt + 1, 0..kt-1)] | [TRSM]
@@ -171,7 +181,9 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
       double* cur = S.col + (kt & 1) * colstride;
       double* nxt = S.col + ((kt + 1) & 1) * colstride;
       // (3) C(it, kt) -= sum_jt L(it, jt) L(kt, jt)^T, a warp per tile row
-      if (kt > 0) {
+      // (the gathered column is scaled here: C = (B s_l1) s_l2, RHS row unscaled)
+      {
+        const double sc0 = S.sl[8 * kt + ((2 * lane) & 7)], sc1 = S.sl[8 * kt + ((2 * lane) & 7) + 1];
         // two tile rows per warp iteration: 4 independent accumulator chains
         for (int it = kt + warp; it <= T; it += 2 * kV3Warps) {
           const int it2 = it + kV3Warps;
@@ -180,6 +192,16 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
           double* ct2 = cur + ((two ? it2 : it) - kt) * 64;
           double c0 = ct[2 * lane], c1 = ct[2 * lane + 1];
           double g0 = two ? ct2[2 * lane] : 0.0, g1 = two ? ct2[2 * lane + 1] : 0.0;
+          if (it < T) {
+            const double sr = S.sl[8 * it + (lane >> 2)];
+            c0 = c0 * sr * sc0;
+            c1 = c1 * sr * sc1;
+          }
+          if (two && it2 < T) {
+            const double sr = S.sl[8 * it2 + (lane >> 2)];
+            g0 = g0 * sr * sc0;
+            g1 = g1 * sr * sc1;
+          }
           double d0 = 0.0, d1 = 0.0, h0 = 0.0, h1 = 0.0;
           const double* ai = L + (long long)((it * (it + 1)) >> 1) * 64;
           const double* ai2 = L + (long long)(((two ? it2 : it) * ((two ? it2 : it) + 1)) >> 1) * 64;
