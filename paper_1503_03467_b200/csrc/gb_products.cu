@@ -557,8 +557,11 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
   // is multiplied (the gathers are L2-latency bound)
   __shared__ double As[2][16 * PN_LDA];
   __shared__ double Bs[2][PN_KC * PN_LDB];
-  __shared__ long long kbase[2][PN_KC];  // Wpsi row offset of k column, -1 = padding
-  __shared__ int kps[2][PN_KC], kpt[2][PN_KC], kc[2][PN_KC], kos[2][PN_KC], kot[2][PN_KC];
+  // separable per-k tables: B address = kbB + (fs wd + ft), A slot = kakey -
+  // (row offset); window / ball tests on the packed (s << 16 | t) positions
+  // (-1 = padding column)
+  __shared__ long long kbB[2][PN_KC];
+  __shared__ int kbpos[2][PN_KC], kakey[2][PN_KC], kapos[2][PN_KC];
   const int Lp = out.L;
   const int nbs = (Lp + TB - 1) / TB;
   const long long nblk = (long long)nbs * nbs;
@@ -601,26 +604,28 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     const int n_ = threadIdx.x & 31;
     const int bfs = F0s + (n_ >> 2), bft = F0t + (n_ & 3);
     // chunk metadata (threads < PN_KC) into buffer u
+    const int arowoff = ((ais - rho) * side + (ait - rho)) * 3;
+    const long long bfsw = (long long)bfs * par.wd + bft;
     auto meta = [&](int k0, int u) {
       if (threadIdx.x < PN_KC) {
         const int kk = k0 + threadIdx.x;
-        long long base = -1;
-        int ps = 0, pt = 0, cc = 0, os = 0, ot = 0;
+        long long bb = 0;
+        int bpos = -1, akey = 0, apos = -1;
         if (kk < K) {
           const int pl = kk / 3;
-          cc = kk - 3 * pl;
-          ps = ps0 + pl / npt;
-          pt = pt0 + pl % npt;
-          base = ((long long)(ps * Lp + pt) * 3 + cc) * wper;
-          os = par.origin(ps);
-          ot = par.origin(pt);
+          const int cc = kk - 3 * pl;
+          const int ps = ps0 + pl / npt;
+          const int pt = pt0 + pl % npt;
+          const int os = par.origin(ps), ot = par.origin(pt);
+          bb = ((long long)(ps * Lp + pt) * 3 + cc) * wper - (long long)os * par.wd - ot;
+          bpos = (os << 16) | ot;
+          akey = (ps * side + pt) * 3 + cc;
+          apos = (ps << 16) | pt;
         }
-        kbase[u][threadIdx.x] = base;
-        kps[u][threadIdx.x] = ps;
-        kpt[u][threadIdx.x] = pt;
-        kc[u][threadIdx.x] = cc;
-        kos[u][threadIdx.x] = os;
-        kot[u][threadIdx.x] = ot;
+        kbB[u][threadIdx.x] = bb;
+        kbpos[u][threadIdx.x] = bpos;
+        kakey[u][threadIdx.x] = akey;
+        kapos[u][threadIdx.x] = apos;
       }
     };
     double ra[4], rb[8];
@@ -630,23 +635,24 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int kk = (threadIdx.x & 7) + 8 * j;
+        const int ap = kapos[u][kk];
         double v = 0.0;
-        if (arow && kbase[u][kk] >= 0) {
-          const int ds = kps[u][kk] - ais, dt = kpt[u][kk] - ait;
-          if (ds >= -rho && ds <= rho && dt >= -rho && dt <= rho)
-            v = drow[((ds + rho) * side + (dt + rho)) * 3 + kc[u][kk]];
+        if (arow && ap >= 0) {
+          const unsigned ds = (unsigned)((ap >> 16) - ais + rho);
+          const unsigned dt = (unsigned)((ap & 0xffff) - ait + rho);
+          if (ds <= (unsigned)(2 * rho) && dt <= (unsigned)(2 * rho))
+            v = drow[kakey[u][kk] - arowoff];
         }
         ra[j] = v;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int kk = (threadIdx.x >> 5) + 4 * j;
+        const int bp = kbpos[u][kk];
         double v = 0.0;
-        const long long base = kbase[u][kk];
-        if (base >= 0) {
-          const int ls = bfs - kos[u][kk], lt = bft - kot[u][kk];
-          if (ls >= 0 && ls < par.wd && lt >= 0 && lt < par.wd)
-            v = __ldg(Wpsi + base + ls * par.wd + lt);
+        if (bp >= 0) {
+          const unsigned ls = (unsigned)(bfs - (bp >> 16)), lt = (unsigned)(bft - (bp & 0xffff));
+          if (ls < (unsigned)par.wd && lt < (unsigned)par.wd) v = __ldg(Wpsi + kbB[u][kk] + bfsw);
         }
         rb[j] = v;
       }
