@@ -1170,8 +1170,17 @@ __global__ void __launch_bounds__(192) k_bjcg_update(int L, int w, double* __res
       const float* iv = inv + (long long)b * 144 + l * 12;
       const double* rb = rs + lb * 12;
       double zv = 0.0;
+      float iw[12];  // 48-byte rows of a 576-byte block: three 16-byte loads
 #pragma unroll
-      for (int k = 0; k < 12; ++k) zv = fma((double)iv[k], rb[k], zv);
+      for (int q4 = 0; q4 < 3; ++q4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(iv) + q4);
+        iw[4 * q4] = f.x;
+        iw[4 * q4 + 1] = f.y;
+        iw[4 * q4 + 2] = f.z;
+        iw[4 * q4 + 3] = f.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 12; ++k) zv = fma((double)iw[k], rb[k], zv);
       z[pr] = zv;
       rz += rv * zv;
     }
@@ -1244,8 +1253,17 @@ __global__ void __launch_bounds__(192) k_symb_bjcg_update(int L, int w, double* 
       const float* iv = inv + (long long)b * 144 + l * 12;
       const double* rb = rs + lb * 12;
       double zv = 0.0;
+      float iw[12];  // 48-byte rows of a 576-byte block: three 16-byte loads
 #pragma unroll
-      for (int k = 0; k < 12; ++k) zv = fma((double)iv[k], rb[k], zv);
+      for (int q4 = 0; q4 < 3; ++q4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(iv) + q4);
+        iw[4 * q4] = f.x;
+        iw[4 * q4 + 1] = f.y;
+        iw[4 * q4 + 2] = f.z;
+        iw[4 * q4 + 3] = f.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 12; ++k) zv = fma((double)iw[k], rb[k], zv);
       z[pr] = zv;
       rz += rv * zv;
     }
@@ -1314,15 +1332,15 @@ __global__ void __launch_bounds__(kLzThreads) k_symb_lz_update(int L, int w,
       const int ps = I * kSymTH + h, pt = J * kSymTW + j;
       const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
       double yv = y[yi];
+      // neighbour spill-over in symb_fix_value's order
+      const bool left = j < w && J > 0, right = j >= kSymTW - w && J + 1 < tpr;
       for (int dI = 0; dI <= KI; ++dI) {
         const int Ip = I - dI, rr = h + dI * kSymTH;
         if (Ip < 0 || rr >= kSymTH + w) break;
-        for (int dJ = -1; dJ <= 1; ++dJ) {
-          if (dI == 0 && dJ == 0) continue;
-          const int Jp = J + dJ, cc = j - dJ * kSymTW;
-          if (Jp < 0 || Jp >= tpr || cc < -w || cc >= kSymTW + w) continue;
-          yv += ov[((long long)Ip * tpr + Jp) * RG + (rr * WC + cc + w) * 3 + c];
-        }
+        const double* base = ov + ((long long)Ip * tpr + J) * RG + (rr * WC + w) * 3 + c;
+        if (left) yv += base[-RG + (j + kSymTW) * 3];
+        if (dI > 0) yv += base[j * 3];
+        if (right) yv += base[RG + (j - kSymTW) * 3];
       }
       const double xv = x[yi];
       const double u = (yv - alpha * xv) * ibp - bp * vp[yi];
@@ -1389,8 +1407,17 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
       const float* iv = inv + (long long)bk * 144 + l * 12;
       const double* rb = rs + lb * 12;
       double zv = 0.0;
+      float iw[12];  // 48-byte rows of a 576-byte block: three 16-byte loads
 #pragma unroll
-      for (int k = 0; k < 12; ++k) zv = fma((double)iv[k], rb[k], zv);
+      for (int q4 = 0; q4 < 3; ++q4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(iv) + q4);
+        iw[4 * q4] = f.x;
+        iw[4 * q4 + 1] = f.y;
+        iw[4 * q4 + 2] = f.z;
+        iw[4 * q4 + 3] = f.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 12; ++k) zv = fma((double)iw[k], rb[k], zv);
       z[pr] = zv;
       p[pr] = zv;
       rz += rv * zv;

@@ -91,16 +91,17 @@ __device__ __forceinline__ double symb_fix_value(double own, const double* __res
   const int WC = kSymTW + 2 * w, RG = symb_region(w), tpr = L / kSymTW;
   const int KI = (w + kSymTH - 1) / kSymTH;
   const int I = ps / kSymTH, h = ps - I * kSymTH, J = pt / kSymTW, j = pt - J * kSymTW;
+  // the left tile's spill covers j < w, the right tile's j >= kSymTW - w
+  const bool left = j < w && J > 0, right = j >= kSymTW - w && J + 1 < tpr;
   double s = own;
   for (int dI = 0; dI <= KI; ++dI) {
     const int Ip = I - dI, rr = h + dI * kSymTH;
     if (Ip < 0 || rr >= kSymTH + w) break;
-    for (int dJ = -1; dJ <= 1; ++dJ) {
-      if (dI == 0 && dJ == 0) continue;
-      const int Jp = J + dJ, cc = j - dJ * kSymTW;
-      if (Jp < 0 || Jp >= tpr || cc < -w || cc >= kSymTW + w) continue;
-      s += ov[((long long)Ip * tpr + Jp) * RG + (rr * WC + cc + w) * 3 + c];
-    }
+    // region entry (rr, cc) of tile (Ip, Jp): (rr WC + cc + w) 3 + c
+    const double* base = ov + ((long long)Ip * tpr + J) * RG + (rr * WC + w) * 3 + c;
+    if (left) s += base[-RG + (j + kSymTW) * 3];
+    if (dI > 0) s += base[j * 3];
+    if (right) s += base[RG + (j - kSymTW) * 3];
   }
   return s;
 }
