@@ -112,6 +112,12 @@ int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                    const double* A, int wX, double* X, void* stream);
 int gb_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
                     const double* X, int wR, double* raw, void* stream);
+/* coalesced form of gb_psi_galerkin (same sums): psi and X transposed to
+ * plane-major into `work` (gb_psi_galerkin_workspace bytes), a CTA per
+ * 32 fine nodes of a grid row, outputs staged in shared memory */
+size_t gb_psi_galerkin_workspace(int n, int wd, int wX);
+int gb_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,
+                      const double* X, int wR, double* raw, double* work, void* stream);
 
 /* ---- K3 B = W A W^T, G = W A pibar^T, P A P^T (gamblet_fast.py:520-544,
  *      597-601); w12 = the 3x4 null-basis template (hierarchy.py:31-42) ----- */

@@ -40,6 +40,8 @@ _SIGS = {
     "gb_correction_patches_v2": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _P], _I),
     "gb_psi_stencil": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_psi_galerkin": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb_psi_galerkin_workspace": ([_I, _I, _I], _Z),
+    "gb_psi_galerkin_t": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _P], _I),
     "gb_level_diag": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "gb_level_blocks": ([_I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_correction_workspace": ([_I, _I], _Z),

@@ -135,6 +135,16 @@ int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
   return wrap(gbk_psi_stencil(n, lo, wd, rho, psi, wA, A, wX, X, ST(stream)),
               "psi_stencil");
 }
+size_t gb_psi_galerkin_workspace(int n, int wd, int wX) {
+  return gbk_psi_galerkin_workspace(n, wd, wX);
+}
+int gb_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,
+                      const double* X, int wR, double* raw, double* work, void* stream) {
+  COUNT(3);
+  const int rc = gbk_psi_galerkin_t(n, lo, wd, rho, psi, wX, X, wR, raw, work, ST(stream));
+  if (rc == 1) return invalid("psi_galerkin_t: output block exceeds shared memory");
+  return wrap(rc, "psi_galerkin_t");
+}
 int gb_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
                     const double* X, int wR, double* raw, void* stream) {
   COUNT(1);

@@ -99,6 +99,79 @@ __global__ void k_psi_galerkin(PsiWin pw, int rho, const double* __restrict__ ps
 }
 
 // ---------------------------------------------------------------------------
+// K2b, coalesced form: the same sums over transposed operands.  psi^(q)
+// (N x wd^2 windows) and X (N x SX box slots) are transposed to plane-major
+// (psiT[w][i], XT[slot][i]); a CTA owns one fine row si and 32 consecutive
+// nodes ti (lane = ti offset) for all SR output slots, so every operand load
+// of a warp is one contiguous 256-byte run.  Each output is the gather
+// kernel's FMA chain (ms, then mt ascending) without the zero-skip (adding a
+// +-0 product leaves a sum unchanged up to the sign of a zero); the 32 x SR
+// output block is staged in shared memory and written contiguously.
+// ---------------------------------------------------------------------------
+__global__ void k_transpose_f64(long long R, int C, const double* __restrict__ in,
+                                double* __restrict__ out) {
+  __shared__ double t[32][33];
+  const long long r0 = (long long)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const long long r = r0 + k;
+    const int c = c0 + threadIdx.x;
+    if (r < R && c < C) t[k][threadIdx.x] = in[r * C + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k;
+    const long long r = r0 + threadIdx.x;
+    if (r < R && c < C) out[(long long)c * R + r] = t[threadIdx.x][k];
+  }
+}
+
+constexpr int GT_THREADS = 256;
+
+__global__ void __launch_bounds__(GT_THREADS) k_psi_galerkin_t(PsiWin pw, int rho,
+                                                               const double* __restrict__ psiT,
+                                                               int wX, const double* __restrict__ XT,
+                                                               int wR, double* __restrict__ raw) {
+  extern __shared__ double ob[];  // 32 x SR
+  const int n = pw.n;
+  const long long N = (long long)n * n;
+  const int SR = box_slots(wR, 1), WR = 2 * wR + 1, WX = 2 * wX + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ncb = (n + 31) / 32;
+  for (long long cta = blockIdx.x; cta < (long long)n * ncb; cta += gridDim.x) {
+    const int si = (int)(cta / ncb), ti0 = (int)(cta - (long long)si * ncb) * 32;
+    const int ti = ti0 + lane;
+    const bool live = ti < n;
+    const long long i = (long long)si * n + ti;
+    for (int sl = warp; sl < SR; sl += GT_THREADS / 32) {
+      const int ds = sl / WR - wR, dt = sl - (sl / WR) * WR - wR;
+      const int js = si + ds, jt = ti + dt;
+      double acc = 0.0;
+      if (live && js >= 0 && js < n && jt >= 0 && jt < n) {
+        const int os = pw.origin(js), ot = pw.origin(jt);
+        const long long j = (long long)js * n + jt;
+        const int ms0 = imax(imax(si - wX, 0), imax(os, js - rho));
+        const int ms1 = imin(imin(si + wX, n - 1), imin(os + pw.wd - 1, js + rho));
+        const int mt0 = imax(imax(ti - wX, 0), imax(ot, jt - rho));
+        const int mt1 = imin(imin(ti + wX, n - 1), imin(ot + pw.wd - 1, jt + rho));
+        for (int ms = ms0; ms <= ms1; ++ms) {
+          const double* xp = XT + ((long long)(ms - si + wX) * WX - ti + wX) * N + i;
+          const double* pp = psiT + ((long long)(ms - os) * pw.wd - ot) * N + j;
+          for (int mt = mt0; mt <= mt1; ++mt)
+            acc = fma(__ldg(xp + (long long)mt * N), __ldg(pp + (long long)mt * N), acc);
+        }
+      }
+      ob[lane * SR + sl] = acc;
+    }
+    __syncthreads();
+    const int nl = imin(32, n - ti0);
+    double* dst = raw + ((long long)si * n + ti0) * SR;
+    for (int e = threadIdx.x; e < nl * SR; e += GT_THREADS) dst[e] = ob[e];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3: level blocks.  A: box on Lk x Lk (wA).  Parent grid Lp = Lk/2.
 // ---------------------------------------------------------------------------
 struct Blk {
@@ -903,6 +976,30 @@ int gbk_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
   PsiWin pw{n, n, lo, wd, -lo};
   const long long total = (long long)n * n * box_slots(wX, 1);
   k_psi_stencil<<<grid_for(total, 256), 256, 0, s>>>(pw, rho, psi, wA, A, wX, X);
+  return (int)cudaGetLastError();
+}
+
+size_t gbk_psi_galerkin_workspace(int n, int wd, int wX) {
+  return (size_t)n * n * ((size_t)wd * wd + (size_t)box_slots(wX, 1)) * sizeof(double);
+}
+
+int gbk_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,
+                       const double* X, int wR, double* raw, double* work, cudaStream_t s) {
+  PsiWin pw{n, n, lo, wd, -lo};
+  const long long N = (long long)n * n;
+  const int SX = box_slots(wX, 1), SR = box_slots(wR, 1);
+  double* psiT = work;
+  double* XT = work + N * wd * wd;
+  const dim3 tb(32, 8);
+  k_transpose_f64<<<dim3((unsigned)((N + 31) / 32), (wd * wd + 31) / 32), tb, 0, s>>>(
+      N, wd * wd, psi, psiT);
+  k_transpose_f64<<<dim3((unsigned)((N + 31) / 32), (SX + 31) / 32), tb, 0, s>>>(N, SX, X, XT);
+  const size_t smem = (size_t)32 * SR * sizeof(double);
+  if (smem > 200 * 1024) return 1;
+  cudaFuncSetAttribute(k_psi_galerkin_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const long long nct = (long long)n * ((n + 31) / 32);
+  const int g = (int)(nct < 148LL * 8 ? nct : 148LL * 8);
+  k_psi_galerkin_t<<<g, GT_THREADS, smem, s>>>(pw, rho, psiT, wX, XT, wR, raw);
   return (int)cudaGetLastError();
 }
 

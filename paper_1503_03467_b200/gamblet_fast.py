@@ -22,6 +22,8 @@ c_tol=1e-6) the two agree to 1e-13, so `c_tol` and
 
 from __future__ import annotations
 
+import os
+
 import concurrent.futures
 import threading
 import time
@@ -814,6 +816,10 @@ def _psi_dev(level, n, L):
     return dv.csr_to_psi(v, n, L)
 
 
+# GB_GALERKIN_GATHER=1 selects the per-entry gather kernel for A^(q) = psi A psi^T
+_GALERKIN_GATHER = bool(os.environ.get("GB_GALERKIN_GATHER"))
+
+
 def _level_q(M, A, tree, rho, ctx, counter):
     """Alg. 2 lines 2a/3/5: psi^(q) and A^(q) (gamblet_fast.py:464-498, 650-665)."""
     q = tree.q
@@ -855,14 +861,23 @@ def _level_q(M, A, tree, rho, ctx, counter):
     X = dv.empty(N * dv.box_slots(wX, 1))
     wR = min(wX + rho, n - 1)
     raw = dv.empty(N * dv.box_slots(wR, 1))
+    # A^(q)'s own buffer doubles as the transposes' workspace (N (wd^2 + SX)
+    # <= N SR doubles): no extra allocation inside the step
+    Aq = dv.empty(N * dv.box_slots(wR, 1))
     with dv.phase("psi_A_psiT"):
         nat.call("gb_psi_stencil", n, lo, wd, rho, dv.ptr(psi), Ab.w, dv.ptr(Ab.vals), wX,
                  dv.ptr(X), s)
-        nat.call("gb_psi_galerkin", n, lo, wd, rho, dv.ptr(psi), wX, dv.ptr(X), wR,
-                 dv.ptr(raw), s)
+        if _GALERKIN_GATHER:  # the per-entry gather form (same sums)
+            nat.call("gb_psi_galerkin", n, lo, wd, rho, dv.ptr(psi), wX, dv.ptr(X), wR,
+                     dv.ptr(raw), s)
+        else:  # coalesced form over plane-major copies of psi and X
+            need = nat.query("gb_psi_galerkin_workspace", n, wd, wX)
+            work = Aq if Aq.numel() * 8 >= need else dv.empty(need // 8)
+            nat.call("gb_psi_galerkin_t", n, lo, wd, rho, dv.ptr(psi), wX, dv.ptr(X), wR,
+                     dv.ptr(raw), dv.ptr(work), s)
+            del work
     del X
     i = ctx.slot("sym", "A^(q),loc")
-    Aq = dv.empty(N * dv.box_slots(wR, 1))
     with dv.phase("sym_drop"):
         nat.call("gb_box_diag_min", N, 1, wR, dv.ptr(raw), ctx.dm(i), s)
         nat.call("gb_box_sym_drop", n, 1, wR, dv.ptr(raw), dv.ptr(Aq), ctx.dm(i),
