@@ -1326,26 +1326,40 @@ __global__ void __launch_bounds__(kLzThreads) k_symb_lz_update(int L, int w,
   double uu = 0.0;
   for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
     const int I = (int)(tile / tpr), J = (int)(tile - (long long)I * tpr);
-    for (int e = threadIdx.x; e < TE; e += kLzThreads) {
+    // all loads of the thread's NE elements first (stores to y / vp would
+    // otherwise order them), then the recurrence in element order
+    constexpr int NE = TE / kLzThreads;
+    static_assert(TE % kLzThreads == 0, "tile must split evenly over the CTA");
+    double yv[NE], xv[NE], vv[NE];
+    long long yis[NE];
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      const int e = threadIdx.x + q * kLzThreads;
       const int h = e / (kSymTW * 3), rem = e - h * (kSymTW * 3);
       const int j = rem / 3, c = rem - 3 * j;
       const int ps = I * kSymTH + h, pt = J * kSymTW + j;
       const long long yi = ((long long)(ps + w) * Lpad + pt + w) * 3 + c;
-      double yv = y[yi];
+      yis[q] = yi;
+      double v = y[yi];
       // neighbour spill-over in symb_fix_value's order
       const bool left = j < w && J > 0, right = j >= kSymTW - w && J + 1 < tpr;
       for (int dI = 0; dI <= KI; ++dI) {
         const int Ip = I - dI, rr = h + dI * kSymTH;
         if (Ip < 0 || rr >= kSymTH + w) break;
         const double* base = ov + ((long long)Ip * tpr + J) * RG + (rr * WC + w) * 3 + c;
-        if (left) yv += base[-RG + (j + kSymTW) * 3];
-        if (dI > 0) yv += base[j * 3];
-        if (right) yv += base[RG + (j - kSymTW) * 3];
+        if (left) v += base[-RG + (j + kSymTW) * 3];
+        if (dI > 0) v += base[j * 3];
+        if (right) v += base[RG + (j - kSymTW) * 3];
       }
-      const double xv = x[yi];
-      const double u = (yv - alpha * xv) * ibp - bp * vp[yi];
-      vp[yi] = xv * ibp;
-      y[yi] = u;
+      yv[q] = v;
+      xv[q] = x[yis[q]];
+      vv[q] = vp[yis[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      const double u = (yv[q] - alpha * xv[q]) * ibp - bp * vv[q];
+      vp[yis[q]] = xv[q] * ibp;
+      y[yis[q]] = u;
       uu += u * u;
     }
   }
