@@ -256,6 +256,8 @@ def run_exact(args, rank, world, local_rank):
             torch.cuda.synchronize()
             ts.append((time.perf_counter() - t0) * 1e3)
     launches = nat.query("gb_launch_count") - launches0
+    # cudaMalloc calls inside the timed region (each stalls every stream)
+    new_segments = torch.cuda.memory_stats().get("segment.all.allocated", 0) - seg0
     ms = reduce_max(float(np.median(ts)), world, "cuda")
     if rank != 0:
         return None
@@ -312,15 +314,16 @@ def run_ours(args, rank, world, local_rank):
         step_device()
         if i == 0 and not lean:
             # grow the caching allocator once to the step's high-water mark
-            # (+25% against fragmentation): later steps make no cudaMalloc,
+            # (+50% against fragmentation): later steps make no cudaMalloc,
             # which would stall every stream of the level engine (the lean
             # q >= 12 runs use expandable segments instead)
-            dv.reserve(1.25 * torch.cuda.max_memory_allocated())
+            dv.reserve(1.5 * torch.cuda.max_memory_allocated())
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     dv.Prof.reset(enabled=True)
     launches0 = nat.query("gb_launch_count")
+    seg0 = torch.cuda.memory_stats().get("segment.all.allocated", 0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         ev0.record()
@@ -341,6 +344,8 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     launches = nat.query("gb_launch_count") - launches0
+    # cudaMalloc calls inside the timed region (each stalls every stream)
+    new_segments = torch.cuda.memory_stats().get("segment.all.allocated", 0) - seg0
     ms = ev0.elapsed_time(ev1) / args.steps
     step_ms = [round(ev0.elapsed_time(marks[0]), 1)] + [
         round(a.elapsed_time(b_), 1) for a, b_ in zip(marks, marks[1:])]
@@ -465,6 +470,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": int(launches // max(1, args.steps)),
+        "allocator_segments_timed": int(new_segments),
         "roofline": roof,
         "roofline_fp64": fp,
         "cpu_baseline": cpu,

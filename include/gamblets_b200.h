@@ -107,6 +107,17 @@ int gb_mass_patches(int n, int wM, const double* M, const double* s, int rho, in
 int gb_mass_patches_v2(int n, int wM, const double* Ms, const double* s, int rho, int wd,
                        double* psi, int64_t* status, void* stream);
 
+/* spatial strips (multi-GPU row partition): the same
+ * patch solves restricted to grid rows [r0, r1) of the patch centres
+ * (fine rows for the mass patches, parent rows for the correction
+ * patches); output rows outside the strip are not written.  The union of
+ * the strips of a partition equals the whole-level call bitwise. */
+int gb_mass_patches_rows(int n, int wM, const double* Ms, const double* s, int rho, int wd,
+                         double* psi, int64_t* status, int r0, int r1, void* stream);
+int gb_correction_patches_rows(int Lp, int wB, const double* Bs, const double* sB, int wG,
+                               const double* G, int rho, double* Dt, int64_t* status, int r0,
+                               int r1, void* stream);
+
 /* ---- K2 A^(q) = psi A psi^T (gamblet_fast.py:658-665) -------------------- */
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                    const double* A, int wX, double* X, void* stream);

@@ -38,6 +38,8 @@ _SIGS = {
     "gb_mass_patches": ([_I, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P], _I),
     "gb_mass_patches_v2": ([_I, _I, _P, _P, _I, _I, _P, _P, _P], _I),
     "gb_correction_patches_v2": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _P], _I),
+    "gb_mass_patches_rows": ([_I, _I, _P, _P, _I, _I, _P, _P, _I, _I, _P], _I),
+    "gb_correction_patches_rows": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _I, _P], _I),
     "gb_psi_stencil": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_psi_galerkin": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_psi_galerkin_workspace": ([_I, _I, _I], _Z),

@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
           const int rp = arp[m];
           double v = 0.0;
           if (code >= 0 && rp >= 0) {
-            const int ds = qs - (rp >> 16), dt = qt - (rp & 0xffff);
-            if (ds >= -wA && ds <= wA && dt >= -wA && dt <= wA) v = Ab[aro[m] + ko];
+            const unsigned ds = (unsigned)(qs - (rp >> 16) + wA), dt = (unsigned)(qt - (rp & 0xffff) + wA);
+            if (ds <= (unsigned)(2 * wA) && dt <= (unsigned)(2 * wA)) v = Ab[aro[m] + ko];
           }
           ra[r] = v;
         }
@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
           const int code = kq[u][kk];
           double v = 0.0;
           if (code >= 0 && cp >= 0) {
-            const int ds = (code >> 16) - (cp >> 16), dt = (code & 0xffff) - (cp & 0xffff);
-            if (ds >= -wB_ && ds <= wB_ && dt >= -wB_ && dt <= wB_) v = Bb[bkq[u][kk] + co];
+            const unsigned ds = (unsigned)((code >> 16) - (cp >> 16) + wB_);
+            const unsigned dt = (unsigned)((code & 0xffff) - (cp & 0xffff) + wB_);
+            if (ds <= (unsigned)(2 * wB_) && dt <= (unsigned)(2 * wB_)) v = Bb[bkq[u][kk] + co];
           }
           rb[r] = v;
         }

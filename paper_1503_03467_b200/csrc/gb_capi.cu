@@ -129,6 +129,22 @@ int gb_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB,
   if (rc == 1) return invalid("correction_patches_v2: patch exceeds shared memory");
   return wrap(rc, "correction_patches_v2");
 }
+int gb_mass_patches_rows(int n, int wM, const double* Ms, const double* s, int rho, int wd,
+                         double* psi, int64_t* status, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_mass_patches_rows(n, wM, Ms, s, rho, wd, psi, LL(status), r0, r1, ST(stream));
+  if (rc == 1) return invalid("mass_patches_rows: bad row range or no strip kernel for this patch");
+  return wrap(rc, "mass_patches_rows");
+}
+int gb_correction_patches_rows(int Lp, int wB, const double* Bs, const double* sB, int wG,
+                               const double* G, int rho, double* Dt, int64_t* status, int r0,
+                               int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_correction_patches_rows(Lp, wB, Bs, sB, wG, G, rho, Dt, LL(status), r0, r1,
+                                             ST(stream));
+  if (rc == 1) return invalid("correction_patches_rows: bad row range or no strip kernel");
+  return wrap(rc, "correction_patches_rows");
+}
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                    const double* A, int wX, double* X, void* stream) {
   COUNT(1);

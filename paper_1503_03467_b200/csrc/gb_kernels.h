@@ -115,6 +115,11 @@ int gbk_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, doubl
                         double tol, int iters, void* st, double* part, cudaStream_t s);
 int gbk_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
                    cudaStream_t s);
+int gbk_correction_patches_rows(int Lp, int wB, const double* B, const double* sB, int wG,
+                                const double* G, int rho, double* Dt, long long* status, int r0,
+                                int r1, cudaStream_t st);
+int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int rho, int wd,
+                          double* psi, long long* status, int r0, int r1, cudaStream_t st);
 int gbk_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
                               const double* G, int rho, double* Dt, long long* status,
                               cudaStream_t st);

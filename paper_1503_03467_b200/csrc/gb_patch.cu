@@ -505,7 +505,7 @@ constexpr int kBandMaxM = 49, kBandMaxB = 8, kBandW = kBandMaxB + 1, kBandWarps 
 
 __global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
     int n, const double* __restrict__ M, const double* __restrict__ s, int rho, int wd,
-    double* __restrict__ psi, long long* status) {
+    double* __restrict__ psi, long long* status, long long p0, long long p1) {
   __shared__ double sLb[kBandWarps][kBandMaxM * kBandW];
   __shared__ double sSl[kBandWarps][kBandMaxM];
   __shared__ double sX[kBandWarps][kBandMaxM];
@@ -530,9 +530,9 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
     co[u] = p - rr * (rr + 1) / 2 + 1;
     if (p >= kBandMaxB * (kBandMaxB + 1) / 2) ro[u] = 99;
   }
-  const long long N = (long long)n * n;
+  // patches [p0, p1) (node order; a row strip of the fine grid)
   const long long nwarps = (long long)gridDim.x * kBandWarps;
-  for (long long i = (long long)blockIdx.x * kBandWarps + wi; i < N; i += nwarps) {
+  for (long long i = p0 + (long long)blockIdx.x * kBandWarps + wi; i < p1; i += nwarps) {
     const int si = (int)(i / n), ti = (int)(i % n);
     const int s0 = imax(0, si - rho), s1 = imin(n - 1, si + rho);
     const int t0 = imax(0, ti - rho), t1 = imin(n - 1, ti + rho);
@@ -705,9 +705,13 @@ static int g_patch_v3 = -1;  // -1: unset (env GB_PATCH_V2 selects the smem-resi
 static double* g_v3_scratch = nullptr;
 static size_t g_v3_scratch_bytes = 0;
 
-int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB, int wG,
-                              const double* G, int rho, double* Dt, long long* status,
-                              cudaStream_t st) {
+// parent grid rows [r0, r1) only (a spatial strip; the v3 kernel is required
+// for a proper strip, returns 1 otherwise); Dt rows outside are not touched
+int gbk_correction_patches_rows(int Lp, int wB, const double* B, const double* sB, int wG,
+                                const double* G, int rho, double* Dt, long long* status, int r0,
+                                int r1, cudaStream_t st) {
+  if (r0 < 0 || r1 > Lp || r0 > r1) return 1;
+  if (r0 == r1) return 0;
   const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
   if (g_patch_v3 < 0) g_patch_v3 = getenv("GB_PATCH_V2") ? 0 : 1;
@@ -715,7 +719,7 @@ int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB,
     const size_t smem = v3_smem_bytes(Tmax);
     int per_sm = 6;
     if (const char* e = getenv("GB_PATCH_V3_PER_SM")) per_sm = atoi(e) > 0 ? atoi(e) : 6;
-    const long long P = (long long)Lp * Lp;
+    const long long P = (long long)(r1 - r0) * Lp;
     const long long gmax = 148LL * per_sm;
     const int g = (int)(P < gmax ? P : gmax);
     const size_t need = (size_t)g * ((size_t)Tmax * (Tmax + 1) / 2 + Tmax) * 64 * sizeof(double);
@@ -733,9 +737,12 @@ int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB,
     cudaFuncSetAttribute(k_correction_patches_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     k_correction_patches_v3<<<g, 32 * kV3Warps, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt,
-                                                            status, Tmax, g_v3_scratch);
+                                                            status, Tmax, g_v3_scratch,
+                                                            (long long)r0 * Lp,
+                                                            (long long)r1 * Lp);
     return (int)cudaGetLastError();
   }
+  if (r0 != 0 || r1 != Lp) return 1;  // v2 runs whole levels only
   const size_t smem = tile_smem_bytes(Tmax, 8);
   if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
   cudaFuncSetAttribute(k_correction_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -749,20 +756,33 @@ int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB,
   return (int)cudaGetLastError();
 }
 
+int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB, int wG,
+                              const double* G, int rho, double* Dt, long long* status,
+                              cudaStream_t st) {
+  return gbk_correction_patches_rows(Lp, wB, B, sB, wG, G, rho, Dt, status, 0, Lp, st);
+}
+
 static int g_mass_mode = -1;  // -1: unset (env GB_MASS_DENSE)
-int gbk_mass_patches_v2(int n, int wM, const double* M, const double* s, int rho, int wd,
-                        double* psi, long long* status, cudaStream_t st) {
+// fine-grid rows [r0, r1) only (the banded kernel is required for a proper
+// strip, returns 1 otherwise)
+int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int rho, int wd,
+                          double* psi, long long* status, int r0, int r1, cudaStream_t st) {
+  if (r0 < 0 || r1 > n || r0 > r1) return 1;
+  if (r0 == r1) return 0;
   const int nmax = (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
   const long long NN = (long long)n * n;
   if (g_mass_mode < 0) g_mass_mode = getenv("GB_MASS_DENSE") ? 1 : 0;
   if (wM == 1 && rho <= 3 && g_mass_mode == 0) {  // banded warp solver (rho = 3: b <= 8)
     const long long warps = 148LL * 16 * 4;
-    const long long g = (NN + kBandWarps - 1) / kBandWarps;
+    const long long np = (long long)(r1 - r0) * n;
+    const long long g = (np + kBandWarps - 1) / kBandWarps;
     k_mass_patches_band<<<(int)(g < warps / kBandWarps ? g : warps / kBandWarps),
-                          32 * kBandWarps, 0, st>>>(n, M, s, rho, wd, psi, status);
+                          32 * kBandWarps, 0, st>>>(n, M, s, rho, wd, psi, status,
+                                                    (long long)r0 * n, (long long)r1 * n);
     return (int)cudaGetLastError();
   }
+  if (r0 != 0 || r1 != n) return 1;  // the dense tiled kernel runs whole grids only
   const size_t smem = tile_smem_bytes(Tmax, 4);
   if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
   cudaFuncSetAttribute(k_mass_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -771,4 +791,8 @@ int gbk_mass_patches_v2(int n, int wM, const double* M, const double* s, int rho
   int g = (int)(N < 148LL * 64 ? N : 148LL * 64);
   k_mass_patches_v2<<<g, 128, smem, st>>>(n, wM, M, s, rho, wd, psi, status, Tmax);
   return (int)cudaGetLastError();
+}
+int gbk_mass_patches_v2(int n, int wM, const double* M, const double* s, int rho, int wd,
+                        double* psi, long long* status, cudaStream_t st) {
+  return gbk_mass_patches_rows(n, wM, M, s, rho, wd, psi, status, 0, n, st);
 }

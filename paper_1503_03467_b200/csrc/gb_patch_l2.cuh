@@ -120,16 +120,16 @@ __device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, 
 __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patches_v3(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB, int wG,
     const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status, int Tmax,
-    double* __restrict__ scratch) {
+    double* __restrict__ scratch, long long p0, long long p1) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   V3Smem S = v3_carve(sm, Tmax);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int SB = box_slots(wB, 3), SG = box_slots(wG, 1), SD = box_slots(rho, 3);
-  const long long P = (long long)Lp * Lp;
   double* L = scratch + (long long)blockIdx.x * ((Tmax * (Tmax + 1)) / 2 + Tmax) * 64;
   const int fr = lane >> 2, fk = lane & 3;
-  for (long long i = blockIdx.x; i < P; i += gridDim.x) {
+  // patches [p0, p1) (parent order; a row strip of the parent grid)
+  for (long long i = p0 + blockIdx.x; i < p1; i += gridDim.x) {
     const int si = (int)(i / Lp), ti = (int)(i % Lp);
     const int s0 = imax(0, si - rho), s1 = imin(Lp - 1, si + rho);
     const int t0 = imax(0, ti - rho), t1 = imin(Lp - 1, ti + rho);

@@ -36,6 +36,7 @@ import torch
 
 from . import _native as nat
 from . import device as dv
+from . import partition as part
 from .device import EXP_CHILD, EXP_SQUARE, EXP_TDT, BoxMatrix, PsiWindows
 from .errors import InvalidArgumentError, NumericalError
 from .gamblet_exact import HostDict, MultiresSolution, SolveRecord
@@ -890,9 +891,22 @@ def _level_q(M, A, tree, rho, ctx, counter):
     return (PsiWindows(psi, n, n, lo, hi), BoxMatrix(Aq, n, 1, wR, 1), i)
 
 
+# row-strip partition of the patch solves (partition.Strips; None = whole
+# levels): the multi-GPU building block, DESIGN.md section 6
+_STRIPS = None
+
+
 def _mass_patches(n, Mb, sM, rho, wd, psi, status_ptr, s):
     """K1 on the pre-scaled S M S box: the shared-memory tiled DMMA Cholesky
     (v2); patches larger than shared memory use the global-workspace v1."""
+    if _STRIPS is not None:
+        try:
+            part.run_strips(_STRIPS, n, n * wd * wd, psi, lambda r0, r1: nat.call(
+                "gb_mass_patches_rows", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd,
+                dv.ptr(psi), status_ptr, r0, r1, s))
+            return
+        except InvalidArgumentError:  # no strip kernel for this patch: whole level
+            pass
     try:
         nat.call("gb_mass_patches_v2", n, Mb.w, dv.ptr(Mb.vals), dv.ptr(sM), rho, wd,
                  dv.ptr(psi), status_ptr, s)
@@ -910,6 +924,14 @@ def _mass_patches(n, Mb, sM, rho, wd, psi, status_ptr, s):
 def _correction_patches(Lp, B, op, sB, Gv, rho, Dt, status_ptr, s):
     """K4: v2 (tiled DMMA Cholesky in shared memory on S B S) when the patch
     fits, else the global-workspace v1."""
+    if _STRIPS is not None:
+        try:
+            part.run_strips(_STRIPS, Lp, Lp * dv.box_slots(rho, 3), Dt, lambda r0, r1: nat.call(
+                "gb_correction_patches_rows", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w,
+                dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, r0, r1, s))
+            return
+        except InvalidArgumentError:  # no strip kernel for this patch: whole level
+            pass
     try:
         nat.call("gb_correction_patches_v2", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w,
                  dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, s)
