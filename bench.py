@@ -246,6 +246,7 @@ def run_exact(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     launches0 = nat.query("gb_launch_count")
+    seg0 = torch.cuda.memory_stats().get("segment.all.allocated", 0)
     dv.Traffic.reset()
     with ClockSampler(local_rank) as clk:
         ts = []
