@@ -117,6 +117,10 @@ int gb_mass_patches_rows(int n, int wM, const double* Ms, const double* s, int r
 int gb_correction_patches_rows(int Lp, int wB, const double* Bs, const double* sB, int wG,
                                const double* G, int rho, double* Dt, int64_t* status, int r0,
                                int r1, void* stream);
+/* psi^(k-1) rows of the parents in rows [r0, r1) (gb_psi_next, strip form) */
+int gb_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                     const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                     double* psi_next, double* rowmax, int r0, int r1, void* stream);
 
 /* ---- K2 A^(q) = psi A psi^T (gamblet_fast.py:658-665) -------------------- */
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,

@@ -54,6 +54,8 @@ _SIGS = {
     "gb_coarse_raw": ([_I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_wpsi": ([_I, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "gb_psi_next": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P, _P, _P], _I),
+    "gb_psi_next_rows": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P, _P, _I, _I, _P],
+                         _I),
     "gb_products_mode": ([_I], _I),
     "gb_tune": ([_I, _I], _I),
     "gb_kstate_bytes": ([], _Z),

@@ -136,6 +136,15 @@ int gb_mass_patches_rows(int n, int wM, const double* Ms, const double* s, int r
   if (rc == 1) return invalid("mass_patches_rows: bad row range or no strip kernel for this patch");
   return wrap(rc, "mass_patches_rows");
 }
+int gb_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                     const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                     double* psi_next, double* rowmax, int r0, int r1, void* stream) {
+  COUNT(3);
+  const int rc = gbk_psi_next_rows(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2, psi_next,
+                                   rowmax, r0, r1, ST(stream));
+  if (rc == 1) return invalid("psi_next_rows: bad row range or per-entry products mode");
+  return wrap(rc, "psi_next_rows");
+}
 int gb_correction_patches_rows(int Lp, int wB, const double* Bs, const double* sB, int wG,
                                const double* G, int rho, double* Dt, int64_t* status, int r0,
                                int r1, void* stream) {

@@ -115,6 +115,9 @@ int gbk_ppow_iterations(int L, int nr, int w, const double* Bs, double* x, doubl
                         double tol, int iters, void* st, double* part, cudaStream_t s);
 int gbk_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, double* y,
                    cudaStream_t s);
+int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                      const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                      double* psi_next, double* rowmax, int r0, int r1, cudaStream_t s);
 int gbk_correction_patches_rows(int Lp, int wB, const double* B, const double* sB, int wG,
                                 const double* G, int rho, double* Dt, long long* status, int r0,
                                 int r1, cudaStream_t st);

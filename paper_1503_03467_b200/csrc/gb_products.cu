@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
                                                       int rho, const double* __restrict__ Dt,
                                                       PsiWin out, double* __restrict__ psi_next,
                                                       double* __restrict__ rowmax, int TB, int nfs,
-                                                      int nft) {
+                                                      int nft, int r0, int r1) {
   // double-buffered: chunk c + 1 is gathered into registers while chunk c
   // is multiplied (the gathers are L2-latency bound)
   __shared__ double As[2][16 * PN_LDA];
@@ -637,7 +637,9 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
   __shared__ int kbpos[2][PN_KC], kakey[2][PN_KC], kapos[2][PN_KC];
   const int Lp = out.L;
   const int nbs = (Lp + TB - 1) / TB;
-  const long long nblk = (long long)nbs * nbs;
+  // output parent rows [r0, r1) only: the row blocks meeting the strip
+  const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
+  const long long nblk = (long long)(rb1 - rb0) * nbs;
   const int tpb = nfs * nft;
   const long long ntiles = nblk * tpb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -651,7 +653,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const long long blk = t / tpb;
     const int tt = (int)(t - blk * tpb);
-    const int bi_s = (int)(blk / nbs) * TB, bi_t = (int)(blk % nbs) * TB;
+    const int bi_s = (rb0 + (int)(blk / nbs)) * TB, bi_t = (int)(blk % nbs) * TB;
     const int nrs = imin(TB, Lp - bi_s), nrt = imin(TB, Lp - bi_t);
     // union of the block rows' windows (origins are monotone in the row)
     const int us0 = out.origin(bi_s), us1 = out.origin(bi_s + nrs - 1) + out.wd - 1;
@@ -671,8 +673,8 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     // the A rows this thread gathers: m = threadIdx.x / 8 (+ fixed), kk strided
     const int am = threadIdx.x >> 3;  // 0..15
     const int ams = am / TB, amt = am - (am / TB) * TB;
-    const bool arow = am < TB * TB && ams < nrs && amt < nrt;
     const int ais = bi_s + ams, ait = bi_t + amt;
+    const bool arow = am < TB * TB && ams < nrs && amt < nrt && ais >= r0 && ais < r1;
     const double* drow = Dt + ((long long)ais * Lp + ait) * SD;
     const int n_ = threadIdx.x & 31;
     const int bfs = F0s + (n_ >> 2), bft = F0t + (n_ & 3);
@@ -760,8 +762,8 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     for (int mt = 0; mt < 2; ++mt) {
       const int m = mt * 8 + (lane >> 2);
       const int ms = m / TB, mtt = m - ms * TB;
-      const bool live = m < TB * TB && ms < nrs && mtt < nrt;
       const int is = bi_s + ms, it = bi_t + mtt;
+      const bool live = m < TB * TB && ms < nrs && mtt < nrt && is >= r0 && is < r1;
       double amax = 0.0;
       if (live) {
         const int os = out.origin(is), ot = out.origin(it);
@@ -1101,13 +1103,19 @@ int gbk_wpsi(int n, int Lk, int lo, int wd, const double* w12, const double* psi
   return (int)cudaGetLastError();
 }
 
-int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
-                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
-                 double* psi_next, double* rowmax, cudaStream_t s) {
+// output parent rows [r0, r1) only (tensor-core mode required for a proper
+// strip, returns 1 otherwise): rows outside are not written
+int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                      const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                      double* psi_next, double* rowmax, int r0, int r1, cudaStream_t s) {
   PsiWin child{n, Lk, lo, wd, hi}, par{n, Lk / 2, lo, wdw, 0}, out{n, Lk / 2, lo2, wd2, 0};
   const int Lp = Lk / 2;
-  const long long rows = (long long)Lp * Lp, S = (long long)wd2 * wd2;
-  cudaError_t e = cudaMemsetAsync(rowmax, 0, rows * sizeof(double), s);
+  if (r0 < 0 || r1 > Lp || r0 > r1) return 1;
+  if (r0 == r1) return 0;
+  if (!products_use_mma && (r0 != 0 || r1 != Lp)) return 1;
+  const long long S = (long long)wd2 * wd2;
+  const long long rows = (long long)(r1 - r0) * Lp, roff = (long long)r0 * Lp;
+  cudaError_t e = cudaMemsetAsync(rowmax + roff, 0, rows * sizeof(double), s);
   if (e != cudaSuccess) return (int)e;
   if (products_use_mma) {
     const int TB = Lp < 4 ? Lp : 4;
@@ -1115,10 +1123,11 @@ int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int w
     const int span = imin(wd2 + (TB - 1) * hp, n);
     const int nfs = (span + 7) / 8, nft = (span + 3) / 4;
     const long long nb = (Lp + TB - 1) / TB;
-    const long long nt = nb * nb * nfs * nft;
+    const long long nrb = (r1 + TB - 1) / TB - r0 / TB;
+    const long long nt = nrb * nb * nfs * nft;
     const int g = (int)(nt < 148LL * 64 ? nt : 148LL * 64);
     k_psi_next_mma<<<g, 128, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out, psi_next, rowmax, TB,
-                                     nfs, nft);
+                                     nfs, nft, r0, r1);
   } else {
     const long long total = rows * S;
     k_psi_next<<<grid_for(total, 256), 256, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out,
@@ -1128,7 +1137,13 @@ int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int w
                                                                               rowmax);
   }
   const long long nch = rows * ((S + RT_CHUNK - 1) / RT_CHUNK);
-  k_drop_by_rowmax<<<(int)(nch < 148LL * 32 ? nch : 148LL * 32), 256, 0, s>>>(rows, S, psi_next,
-                                                                             rowmax);
+  k_drop_by_rowmax<<<(int)(nch < 148LL * 32 ? nch : 148LL * 32), 256, 0, s>>>(
+      rows, S, psi_next + roff * S, rowmax + roff);
   return (int)cudaGetLastError();
+}
+int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                 double* psi_next, double* rowmax, cudaStream_t s) {
+  return gbk_psi_next_rows(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2, psi_next, rowmax,
+                           0, Lk / 2, s);
 }

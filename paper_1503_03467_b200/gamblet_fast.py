@@ -1099,8 +1099,15 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
                 nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
                          dv.ptr(Wpsi), s)
                 rmax = dv.empty(P)
-                nat.call("gb_psi_next", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
-                         dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax), s)
+                if _STRIPS is not None:  # row strips of the parent grid (multi-GPU block)
+                    part.run_strips(_STRIPS, Lp, Lp * wd2 * wd2, pv, lambda r0, r1: nat.call(
+                        "gb_psi_next_rows", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
+                        dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax),
+                        r0, r1, s))
+                else:
+                    nat.call("gb_psi_next", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
+                             dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv),
+                             dv.ptr(rmax), s)
             del Wpsi, rmax
             psin = PsiWindows(pv, n, Lp, lo2, hi2)
             if _lean:  # psi^(k) lives on only in the level-k increment task
