@@ -192,8 +192,9 @@ def kernel_timings(levels, q):
     Dt = dv.empty(B.L * B.L * dv.box_slots(rho, 3))
     st = dv.zeros(2, torch.int64)
     G = dv.to_dev(np.ones(B.rows * dv.box_slots(B.w, 1)))  # nonzero right-hand sides
+    ws, nb = gf._correction_ws(B.L, rho, 0, B.L)
     args = (B.L, B.w, dv.ptr(B.vals), dv.ptr(lv.raw("subband_scale")), B.w, dv.ptr(G), rho,
-            dv.ptr(Dt), dv.ptr(st), s)
+            dv.ptr(Dt), dv.ptr(st), dv.ptr(ws), nb, s)
     nat.call("gb_correction_patches_v2", *args)
     torch.cuda.synchronize()
     a.record()

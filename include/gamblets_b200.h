@@ -116,7 +116,7 @@ int gb_mass_patches_rows(int n, int wM, const double* Ms, const double* s, int r
                          double* psi, int64_t* status, int r0, int r1, void* stream);
 int gb_correction_patches_rows(int Lp, int wB, const double* Bs, const double* sB, int wG,
                                const double* G, int rho, double* Dt, int64_t* status, int r0,
-                               int r1, void* stream);
+                               int r1, double* workspace, size_t workspace_bytes, void* stream);
 /* psi^(k-1) rows of the parents in rows [r0, r1) (gb_psi_next, strip form) */
 int gb_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                      const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
@@ -148,10 +148,15 @@ int gb_correction_patches(int Lp, int wB, const double* B, const double* sB, int
                           const double* G, int rho, double* Dt, int64_t* status,
                           double* workspace, int blocks, void* stream);
 
-/* v2: tiled DMMA Cholesky on the pre-scaled S B S box */
+/* v2/v3: tiled DMMA Cholesky on the pre-scaled S B S box.  The v3 kernel
+ * streams finished L columns through a caller-owned scratch of
+ * gb_correction_patches_workspace(Lp, rho, r0, r1) bytes (0: v3 does not run,
+ * pass NULL); the scratch must not be shared by concurrent calls.
+ * GB_ERR_INVALID when no tiled kernel covers the patch (use v1). */
+size_t gb_correction_patches_workspace(int Lp, int rho, int r0, int r1);
 int gb_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
                              const double* G, int rho, double* Dt, int64_t* status,
-                             void* stream);
+                             double* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- K6 R, split triple product, psi^(k-1) (gamblet_fast.py:587-624) ----- */
 int gb_restriction(int Lp, int rho, const double* Dt, const double* host_w12,
@@ -172,8 +177,10 @@ int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double*
  * both accumulate in the reference's order (ascending CSR column), -1
  * queries; returns the previous mode. */
 int gb_products_mode(int mma);
-/* launch tuning: what = 0 -> total CTAs of the correction-patch grid (0 =
- * auto); value < 0 queries.  Returns the previous value (-1: unknown key). */
+/* launch tuning (tests and tools only): what = 0 -> total CTAs of the v2
+ * correction-patch grid (0 = auto); 1 -> correction kernel (1 = v3, default;
+ * 0 = v2); 2 -> mass patches (0 = banded, default; 1 = dense tiled).  value
+ * < 0 queries.  Returns the previous value (-1: unknown key). */
 int gb_tune(int what, int value);
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                 const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,

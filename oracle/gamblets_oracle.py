@@ -14,7 +14,7 @@ measured to agree with the reference to 1e-16..1e-13 on R, A, B, psi and
 reference's O(N) fancy indexing, so q <= 8 runs in seconds.
 
 Pinning: `oracle/make_goldens.py` runs the reference itself (tight mode) and
-writes `tests/golden/*.npz`; `tests/test_oracle_pins.py` checks this module
+writes `tests/golden/*.npz`; `tests/test_host_and_oracle.py` checks this module
 against those fixtures (and against the reference's own pinned values:
 goldens.json radii, chi lists, load checksums).
 

@@ -8,7 +8,7 @@ reference lives at /root/reference):
 The reference is imported from /root/reference/pkg/src and run in tight mode
 (SURVEY.md 8(c)): fast_solve(..., epsilon=1e-13, uniform_rho=3, c_tol=1e-6)
 and exact_solve(..., tol_mass=1e-14, tol_subband=1e-14).  The outputs pin both
-the CPU oracle (tests/test_oracle_pins.py) and the GPU path
+the CPU oracle (tests/test_host_and_oracle.py) and the GPU path
 (tests/test_gpu_parity.py).  Nothing here runs on the GPU box.
 """
 

@@ -37,9 +37,11 @@ _SIGS = {
     "gb_mass_patch_workspace": ([_I, _I], _Z),
     "gb_mass_patches": ([_I, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P], _I),
     "gb_mass_patches_v2": ([_I, _I, _P, _P, _I, _I, _P, _P, _P], _I),
-    "gb_correction_patches_v2": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _P], _I),
+    "gb_correction_patches_workspace": ([_I, _I, _I, _I], _Z),
+    "gb_correction_patches_v2": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _P, _Z, _P], _I),
     "gb_mass_patches_rows": ([_I, _I, _P, _P, _I, _I, _P, _P, _I, _I, _P], _I),
-    "gb_correction_patches_rows": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _I, _P], _I),
+    "gb_correction_patches_rows": ([_I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _I, _P, _Z, _P],
+                                   _I),
     "gb_psi_stencil": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_psi_galerkin": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P], _I),
     "gb_psi_galerkin_workspace": ([_I, _I, _I], _Z),
@@ -150,12 +152,6 @@ def load(path=None):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    # launch tuning from the environment (see gb_tune in include/gamblets_b200.h)
-    import os
-    if os.environ.get("GB_PATCH_GRID"):
-        lib.gb_tune(0, int(os.environ["GB_PATCH_GRID"]))
-    if os.environ.get("GB_PRODUCTS_MODE"):
-        lib.gb_products_mode(int(os.environ["GB_PRODUCTS_MODE"]))
     _lib = lib
     return lib
 

@@ -117,23 +117,28 @@ int gb_mass_patches_v2(int n, int wM, const double* Ms, const double* s, int rho
                        double* psi, int64_t* status, void* stream) {
   COUNT(1);
   const int rc = gbk_mass_patches_v2(n, wM, Ms, s, rho, wd, psi, LL(status), ST(stream));
-  if (rc == 1) return invalid("mass_patches_v2: patch exceeds shared memory");
+  if (rc == GB_UNSUPPORTED) return invalid("mass_patches_v2: patch exceeds shared memory");
   return wrap(rc, "mass_patches_v2");
+}
+size_t gb_correction_patches_workspace(int Lp, int rho, int r0, int r1) {
+  return gbk_correction_v3_workspace(Lp, rho, r0, r1);
 }
 int gb_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
                              const double* G, int rho, double* Dt, int64_t* status,
-                             void* stream) {
+                             double* workspace, size_t workspace_bytes, void* stream) {
   COUNT(1);
   const int rc = gbk_correction_patches_v2(Lp, wB, Bs, sB, wG, G, rho, Dt, LL(status),
-                                           ST(stream));
-  if (rc == 1) return invalid("correction_patches_v2: patch exceeds shared memory");
+                                           workspace, workspace_bytes, ST(stream));
+  if (rc == GB_UNSUPPORTED)
+    return invalid("correction_patches_v2: patch exceeds shared memory or workspace too small");
   return wrap(rc, "correction_patches_v2");
 }
 int gb_mass_patches_rows(int n, int wM, const double* Ms, const double* s, int rho, int wd,
                          double* psi, int64_t* status, int r0, int r1, void* stream) {
   COUNT(1);
   const int rc = gbk_mass_patches_rows(n, wM, Ms, s, rho, wd, psi, LL(status), r0, r1, ST(stream));
-  if (rc == 1) return invalid("mass_patches_rows: bad row range or no strip kernel for this patch");
+  if (rc == GB_UNSUPPORTED)
+    return invalid("mass_patches_rows: bad row range or no strip kernel for this patch");
   return wrap(rc, "mass_patches_rows");
 }
 int gb_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
@@ -142,16 +147,17 @@ int gb_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, i
   COUNT(3);
   const int rc = gbk_psi_next_rows(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2, psi_next,
                                    rowmax, r0, r1, ST(stream));
-  if (rc == 1) return invalid("psi_next_rows: bad row range or per-entry products mode");
+  if (rc == GB_UNSUPPORTED) return invalid("psi_next_rows: bad row range or per-entry products mode");
   return wrap(rc, "psi_next_rows");
 }
 int gb_correction_patches_rows(int Lp, int wB, const double* Bs, const double* sB, int wG,
                                const double* G, int rho, double* Dt, int64_t* status, int r0,
-                               int r1, void* stream) {
+                               int r1, double* workspace, size_t workspace_bytes, void* stream) {
   COUNT(1);
   const int rc = gbk_correction_patches_rows(Lp, wB, Bs, sB, wG, G, rho, Dt, LL(status), r0, r1,
-                                             ST(stream));
-  if (rc == 1) return invalid("correction_patches_rows: bad row range or no strip kernel");
+                                             workspace, workspace_bytes, ST(stream));
+  if (rc == GB_UNSUPPORTED)
+    return invalid("correction_patches_rows: bad row range, no strip kernel or workspace too small");
   return wrap(rc, "correction_patches_rows");
 }
 int gb_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,

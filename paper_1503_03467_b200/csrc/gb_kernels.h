@@ -5,6 +5,10 @@
 #include <stddef.h>
 #include <stdint.h>
 
+// launcher status: 0 ok, > 0 a cudaError_t, GB_UNSUPPORTED when no kernel of
+// the family covers the arguments (the caller picks another variant)
+#define GB_UNSUPPORTED (-1)
+
 enum { EXP_SQUARE = 0, EXP_CHILD = 1, EXP_PSI = 2, EXP_TDT = 3 };
 
 // gb_box.cu
@@ -120,12 +124,13 @@ int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, 
                       double* psi_next, double* rowmax, int r0, int r1, cudaStream_t s);
 int gbk_correction_patches_rows(int Lp, int wB, const double* B, const double* sB, int wG,
                                 const double* G, int rho, double* Dt, long long* status, int r0,
-                                int r1, cudaStream_t st);
+                                int r1, double* ws, size_t ws_bytes, cudaStream_t st);
+size_t gbk_correction_v3_workspace(int Lp, int rho, int r0, int r1);
 int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int rho, int wd,
                           double* psi, long long* status, int r0, int r1, cudaStream_t st);
 int gbk_correction_patches_v2(int Lp, int wB, const double* Bs, const double* sB, int wG,
                               const double* G, int rho, double* Dt, long long* status,
-                              cudaStream_t st);
+                              double* ws, size_t ws_bytes, cudaStream_t st);
 int gbk_mass_patches_v2(int n, int wM, const double* Ms, const double* s, int rho, int wd,
                         double* psi, long long* status, cudaStream_t st);
 int gbk_scale_box_T(int L, int nr, int w, const double* B, const double* sv, double* BsT,

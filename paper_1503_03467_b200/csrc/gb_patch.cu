@@ -686,67 +686,73 @@ int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB,
   return (int)cudaGetLastError();
 }
 
-// v2 entry points: pre-scaled boxes, shared-memory tiled DMMA Cholesky.
-// Return 1 (caller falls back to v1) when the patch does not fit.
-// launch tuning (gb_tune): total CTAs of the correction-patch grid, 0 = auto
-// (4 waves of the resident CTAs).  Fewer CTAs leave SMs (shared memory) free
-// for the HBM-bound Krylov kernels running concurrently on the level streams.
+// v2/v3 entry points: pre-scaled boxes, tiled DMMA Cholesky.  GB_UNSUPPORTED
+// (negative, never a CUDA error code) when no kernel of this family covers the
+// patch or the row range; the caller then uses the global-workspace v1.
+// launch tuning (gb_tune, test/tool use only): 0 -> total CTAs of the v2
+// correction-patch grid (0 = auto); 1 -> correction kernel (1 = v3 left-looking
+// with L streamed through the caller's workspace, default; 0 = the
+// shared-memory-resident v2); 2 -> mass patches (0 = banded warp solver,
+// default; 1 = dense tiled v2)
 static int g_patch_grid = 0;
+static int g_patch_v3 = 1;
+static int g_mass_dense = 0;
 int gbk_tune(int what, int value) {
-  if (what == 0) {
-    const int old = g_patch_grid;
-    if (value >= 0) g_patch_grid = value;
-    return old;
-  }
-  return -1;
+  int* slot = what == 0 ? &g_patch_grid : what == 1 ? &g_patch_v3 : what == 2 ? &g_mass_dense
+                                                                                : nullptr;
+  if (!slot) return -1;
+  const int old = *slot;
+  if (value >= 0) *slot = value;
+  return old;
 }
 
-static int g_patch_v3 = -1;  // -1: unset (env GB_PATCH_V2 selects the smem-resident v2)
-static double* g_v3_scratch = nullptr;
-static size_t g_v3_scratch_bytes = 0;
+static constexpr int kV3PerSm = 6;  // smem (36 KB) and register limit of the v3 CTA
+
+static long long v3_grid(int Lp, int r0, int r1) {
+  const long long P = (long long)(r1 - r0) * Lp;
+  const long long gmax = 148LL * kV3PerSm;
+  return P < gmax ? P : gmax;
+}
+
+// bytes of the per-CTA L scratch the v3 kernel streams finished columns
+// through (L2-resident); 0 when v3 does not run for this patch size
+size_t gbk_correction_v3_workspace(int Lp, int rho, int r0, int r1) {
+  const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
+  const int Tmax = (nmax + 7) / 8;
+  if (!g_patch_v3 || Tmax > 255 || r1 <= r0) return 0;
+  return (size_t)v3_grid(Lp, r0, r1) * ((size_t)Tmax * (Tmax + 1) / 2 + Tmax) * 64 *
+         sizeof(double);
+}
 
 // parent grid rows [r0, r1) only (a spatial strip; the v3 kernel is required
-// for a proper strip, returns 1 otherwise); Dt rows outside are not touched
+// for a proper strip); Dt rows outside are not touched.  `ws` is the caller's
+// scratch (gbk_correction_v3_workspace bytes, stream-ordered by the caller),
+// so concurrent transforms on different streams never share it.
 int gbk_correction_patches_rows(int Lp, int wB, const double* B, const double* sB, int wG,
                                 const double* G, int rho, double* Dt, long long* status, int r0,
-                                int r1, cudaStream_t st) {
-  if (r0 < 0 || r1 > Lp || r0 > r1) return 1;
+                                int r1, double* ws, size_t ws_bytes, cudaStream_t st) {
+  if (r0 < 0 || r1 > Lp || r0 > r1) return GB_UNSUPPORTED;
   if (r0 == r1) return 0;
   const int nmax = 3 * (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
-  if (g_patch_v3 < 0) g_patch_v3 = getenv("GB_PATCH_V2") ? 0 : 1;
-  if (g_patch_v3 && Tmax <= 255) {
+  const size_t need = gbk_correction_v3_workspace(Lp, rho, r0, r1);
+  if (need > 0) {
+    if (!ws || ws_bytes < need) return GB_UNSUPPORTED;
     const size_t smem = v3_smem_bytes(Tmax);
-    int per_sm = 6;
-    if (const char* e = getenv("GB_PATCH_V3_PER_SM")) per_sm = atoi(e) > 0 ? atoi(e) : 6;
-    const long long P = (long long)(r1 - r0) * Lp;
-    const long long gmax = 148LL * per_sm;
-    const int g = (int)(P < gmax ? P : gmax);
-    const size_t need = (size_t)g * ((size_t)Tmax * (Tmax + 1) / 2 + Tmax) * 64 * sizeof(double);
-    if (need > g_v3_scratch_bytes) {
-      if (g_v3_scratch) {
-        cudaDeviceSynchronize();
-        cudaFree(g_v3_scratch);
-      }
-      g_v3_scratch = nullptr;
-      g_v3_scratch_bytes = 0;
-      cudaError_t e = cudaMalloc((void**)&g_v3_scratch, need);
-      if (e != cudaSuccess) return (int)e;
-      g_v3_scratch_bytes = need;
-    }
-    cudaFuncSetAttribute(k_correction_patches_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    k_correction_patches_v3<<<g, 32 * kV3Warps, smem, st>>>(Lp, wB, B, sB, wG, G, rho, Dt,
-                                                            status, Tmax, g_v3_scratch,
-                                                            (long long)r0 * Lp,
-                                                            (long long)r1 * Lp);
+    cudaError_t e = cudaFuncSetAttribute(k_correction_patches_v3,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    k_correction_patches_v3<<<(int)v3_grid(Lp, r0, r1), 32 * kV3Warps, smem, st>>>(
+        Lp, wB, B, sB, wG, G, rho, Dt, status, Tmax, ws, (long long)r0 * Lp,
+        (long long)r1 * Lp);
     return (int)cudaGetLastError();
   }
-  if (r0 != 0 || r1 != Lp) return 1;  // v2 runs whole levels only
+  if (r0 != 0 || r1 != Lp) return GB_UNSUPPORTED;  // v2 runs whole levels only
   const size_t smem = tile_smem_bytes(Tmax, 8);
-  if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
-  cudaFuncSetAttribute(k_correction_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  if (smem > (size_t)kMaxSmem || Tmax > 255) return GB_UNSUPPORTED;
+  cudaError_t e = cudaFuncSetAttribute(k_correction_patches_v2,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
   const long long P = (long long)Lp * Lp;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
@@ -758,22 +764,20 @@ int gbk_correction_patches_rows(int Lp, int wB, const double* B, const double* s
 
 int gbk_correction_patches_v2(int Lp, int wB, const double* B, const double* sB, int wG,
                               const double* G, int rho, double* Dt, long long* status,
-                              cudaStream_t st) {
-  return gbk_correction_patches_rows(Lp, wB, B, sB, wG, G, rho, Dt, status, 0, Lp, st);
+                              double* ws, size_t ws_bytes, cudaStream_t st) {
+  return gbk_correction_patches_rows(Lp, wB, B, sB, wG, G, rho, Dt, status, 0, Lp, ws,
+                                     ws_bytes, st);
 }
 
-static int g_mass_mode = -1;  // -1: unset (env GB_MASS_DENSE)
 // fine-grid rows [r0, r1) only (the banded kernel is required for a proper
-// strip, returns 1 otherwise)
+// strip)
 int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int rho, int wd,
                           double* psi, long long* status, int r0, int r1, cudaStream_t st) {
-  if (r0 < 0 || r1 > n || r0 > r1) return 1;
+  if (r0 < 0 || r1 > n || r0 > r1) return GB_UNSUPPORTED;
   if (r0 == r1) return 0;
   const int nmax = (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
-  const long long NN = (long long)n * n;
-  if (g_mass_mode < 0) g_mass_mode = getenv("GB_MASS_DENSE") ? 1 : 0;
-  if (wM == 1 && rho <= 3 && g_mass_mode == 0) {  // banded warp solver (rho = 3: b <= 8)
+  if (wM == 1 && rho <= 3 && !g_mass_dense) {  // banded warp solver (rho = 3: b <= 8)
     const long long warps = 148LL * 16 * 4;
     const long long np = (long long)(r1 - r0) * n;
     const long long g = (np + kBandWarps - 1) / kBandWarps;
@@ -782,11 +786,12 @@ int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int r
                                                     (long long)r0 * n, (long long)r1 * n);
     return (int)cudaGetLastError();
   }
-  if (r0 != 0 || r1 != n) return 1;  // the dense tiled kernel runs whole grids only
+  if (r0 != 0 || r1 != n) return GB_UNSUPPORTED;  // the dense tiled kernel runs whole grids only
   const size_t smem = tile_smem_bytes(Tmax, 4);
-  if (smem > (size_t)kMaxSmem || Tmax > 255) return 1;
-  cudaFuncSetAttribute(k_mass_patches_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  if (smem > (size_t)kMaxSmem || Tmax > 255) return GB_UNSUPPORTED;
+  cudaError_t e = cudaFuncSetAttribute(k_mass_patches_v2,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
   const long long N = (long long)n * n;
   int g = (int)(N < 148LL * 64 ? N : 148LL * 64);
   k_mass_patches_v2<<<g, 128, smem, st>>>(n, wM, M, s, rho, wd, psi, status, Tmax);

@@ -1110,9 +1110,9 @@ int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, 
                       double* psi_next, double* rowmax, int r0, int r1, cudaStream_t s) {
   PsiWin child{n, Lk, lo, wd, hi}, par{n, Lk / 2, lo, wdw, 0}, out{n, Lk / 2, lo2, wd2, 0};
   const int Lp = Lk / 2;
-  if (r0 < 0 || r1 > Lp || r0 > r1) return 1;
+  if (r0 < 0 || r1 > Lp || r0 > r1) return GB_UNSUPPORTED;
   if (r0 == r1) return 0;
-  if (!products_use_mma && (r0 != 0 || r1 != Lp)) return 1;
+  if (!products_use_mma && (r0 != 0 || r1 != Lp)) return GB_UNSUPPORTED;
   const long long S = (long long)wd2 * wd2;
   const long long rows = (long long)(r1 - r0) * Lp, roff = (long long)r0 * Lp;
   cudaError_t e = cudaMemsetAsync(rowmax + roff, 0, rows * sizeof(double), s);

@@ -296,6 +296,14 @@ class _Ctx:
         self._check(raise_=True)
 
     def _check(self, raise_=False):
+        if _STRIPS is not None and _STRIPS.distributed and _STRIPS.world > 1:
+            # every rank raises together: a non-SPD patch on one strip poisons
+            # the rows the others received from it
+            import torch.distributed as dist
+            dist.all_reduce(self.status[: 2 * self.n], op=dist.ReduceOp.MAX,
+                            group=_STRIPS.group)
+            dist.all_reduce(self.stats[: 2 * self.n], op=dist.ReduceOp.MAX,
+                            group=_STRIPS.group)
         st = dv.to_host(self.status[: 2 * self.n]).reshape(-1, 2)
         stats = dv.to_host(self.stats[: 2 * self.n]).reshape(-1, 2)
         for i, kind, what, detail in self.labels:
@@ -581,7 +589,7 @@ _SPECTRAL_LOG = []
 
 # pair the lambda estimate and the subband PCG of a level in one engine
 # (shared S B S passes); levels the tiled kernels do not cover run them apart
-PAIRED_ENGINE = __import__("os").environ.get("GB_PAIRED", "1") == "1"
+PAIRED_ENGINE = True
 
 
 def _engine_ok(op):
@@ -665,12 +673,12 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
 SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
 # safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
 # it; converging solves here need < 2000)
-SPECTRAL_PRIORITY = int(__import__("os").environ.get("GB_SPECTRAL_PRIORITY", "-1"))
+SPECTRAL_PRIORITY = -1
 # symmetric band Krylov copy (csrc/gb_symspmv.cuh): only the upper 3x3 blocks
 # of S B S are streamed, the lower half is applied from the same registers
 # (scatter through shared memory) -- half the HBM bytes of the full box
-SYMMETRIC_SPMV = __import__("os").environ.get("GB_SYM_SPMV", "1") == "1"
-MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
+SYMMETRIC_SPMV = True
+MAX_ITER_CAP = 100000
 # inner solver of the inverse iteration for lambda_min: "pcg" (block-Jacobi,
 # the subband preconditioner) or "cg" (the reference's unpreconditioned CG).
 # lambda_min feeds only the reported conditioning (tight mode has no cheap
@@ -681,14 +689,14 @@ MAX_ITER_CAP = int(__import__("os").environ.get("GB_MAX_ITER_CAP", "100000"))
 # moments of its start vector (csrc/gb_lanczos.h) -- the iteration with exact
 # inner solves, same stopping test; the Lanczos passes ride on the subband
 # PCG's operator passes.  Smaller levels run the inverse iteration with PCG.
-SPECTRAL_INNER = __import__("os").environ.get("GB_SPECTRAL_INNER", "lanczos")
-LANCZOS_CAP = int(__import__("os").environ.get("GB_LANCZOS_CAP", "4096"))
+SPECTRAL_INNER = "lanczos"
+LANCZOS_CAP = 4096
 # relative change of the emulated lambda_min between two engine checks (32-64
 # Lanczos steps apart) below which the sequence stops.  The quadrature
 # converges fast by then: at q=10 stopping at 1e-4 (416 steps) lands 4e-7 from
 # the 1e-5 stop (480 steps); the reference's own inner solves (rel_tol 1e-4)
 # move its estimate by 3e-4
-LANCZOS_TOL = float(__import__("os").environ.get("GB_LANCZOS_TOL", "1e-4"))
+LANCZOS_TOL = 1e-4
 
 
 class _LevelTasks:
@@ -817,8 +825,9 @@ def _psi_dev(level, n, L):
     return dv.csr_to_psi(v, n, L)
 
 
-# GB_GALERKIN_GATHER=1 selects the per-entry gather kernel for A^(q) = psi A psi^T
-_GALERKIN_GATHER = bool(os.environ.get("GB_GALERKIN_GATHER"))
+# test-only switch: the per-entry gather kernel for A^(q) = psi A psi^T (same
+# sums as the default plane-major kernel; tests/test_gpu_parity.py compares them)
+_GALERKIN_GATHER = False
 
 
 def _level_q(M, A, tree, rho, ctx, counter):
@@ -921,20 +930,32 @@ def _mass_patches(n, Mb, sM, rho, wd, psi, status_ptr, s):
              status_ptr, dv.ptr(ws), blocks, s)
 
 
+def _correction_ws(Lp, rho, r0, r1):
+    """Caller-owned L scratch of the v3 correction-patch kernel (allocated from
+    the stream-ordered caching allocator, so concurrent transforms on
+    different streams never share it)."""
+    nb = nat.query("gb_correction_patches_workspace", Lp, rho, r0, r1)
+    return (dv.empty((nb + 7) // 8), nb) if nb else (None, 0)
+
+
 def _correction_patches(Lp, B, op, sB, Gv, rho, Dt, status_ptr, s):
-    """K4: v2 (tiled DMMA Cholesky in shared memory on S B S) when the patch
-    fits, else the global-workspace v1."""
+    """K4: v3 (left-looking tiled DMMA Cholesky on S B S, L streamed through
+    an L2-resident scratch) when the patch fits, else the global-workspace v1."""
     if _STRIPS is not None:
         try:
-            part.run_strips(_STRIPS, Lp, Lp * dv.box_slots(rho, 3), Dt, lambda r0, r1: nat.call(
-                "gb_correction_patches_rows", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w,
-                dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, r0, r1, s))
+            def strip(r0, r1):
+                ws, nb = _correction_ws(Lp, rho, r0, r1)
+                nat.call("gb_correction_patches_rows", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB),
+                         B.w, dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, r0, r1, dv.ptr(ws),
+                         nb, s)
+            part.run_strips(_STRIPS, Lp, Lp * dv.box_slots(rho, 3), Dt, strip)
             return
         except InvalidArgumentError:  # no strip kernel for this patch: whole level
             pass
     try:
+        ws, nb = _correction_ws(Lp, rho, 0, Lp)
         nat.call("gb_correction_patches_v2", Lp, B.w, dv.ptr(B.vals), dv.ptr(sB), B.w,
-                 dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, s)
+                 dv.ptr(Gv), rho, dv.ptr(Dt), status_ptr, dv.ptr(ws), nb, s)
         return
     except InvalidArgumentError:
         pass
@@ -1099,12 +1120,17 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
                 nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
                          dv.ptr(Wpsi), s)
                 rmax = dv.empty(P)
+                strips_done = False
                 if _STRIPS is not None:  # row strips of the parent grid (multi-GPU block)
-                    part.run_strips(_STRIPS, Lp, Lp * wd2 * wd2, pv, lambda r0, r1: nat.call(
-                        "gb_psi_next_rows", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
-                        dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax),
-                        r0, r1, s))
-                else:
+                    try:
+                        part.run_strips(_STRIPS, Lp, Lp * wd2 * wd2, pv, lambda r0, r1: nat.call(
+                            "gb_psi_next_rows", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
+                            dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv),
+                            dv.ptr(rmax), r0, r1, s))
+                        strips_done = True
+                    except InvalidArgumentError:  # per-entry products mode: whole level
+                        pass
+                if not strips_done:
                     nat.call("gb_psi_next", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
                              dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv),
                              dv.ptr(rmax), s)
@@ -1136,10 +1162,20 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
 
 
 def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
-                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None, _lean=False,
-                   _keep_below=0):
+                   counter=None, dense_cutoff=DENSE_PATCH_CUTOFF):
     """Load-independent phase, levels q..1 (gamblet_fast.py:635-674).
     Returns (levels, counter); all operators stay on the device."""
+    levels, counter, _ = _transform(M, A, tree, schedule, w_variant=w_variant, c_tol=c_tol,
+                                    counter=counter, dense_cutoff=dense_cutoff)
+    return levels, counter
+
+
+def _transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
+               counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _load=None, _lean=False,
+               _keep_below=0):
+    """fast_transform, optionally with the nodal-load solve pipelined into it
+    (_load = (g_device, records)).  Returns (levels, counter, solved), solved =
+    (parts, U1) of the pipelined solve or None."""
     counter = counter if counter is not None else FlopCounter()
     q = tree.q
     if schedule.q != q:
@@ -1175,10 +1211,11 @@ def fast_transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_
         rep = ctx.repair_of.get(getattr(lv, "_repair_slot_a", -1), 0.0)
         rep_b = ctx.repair_of.get(getattr(lv, "_repair_slot_b", -1), 0.0)
         lv.symmetry_repair = max(rep, rep_b)
+    solved = None
     if solver is not None:
         solver.coarse(gk)
-        fast_transform.last_solve = solver.finish()
-    return levels, counter
+        solved = solver.finish()
+    return levels, counter, solved
 
 
 # ---------------------------------------------------------------------------
@@ -1468,12 +1505,9 @@ def fast_solve(M, A, load, tree, epsilon, c_rho=None, uniform_rho=None, schedule
             g = dv.to_dev(load.g_nodal if isinstance(load.g_nodal, torch.Tensor)
                           else np.asarray(load.g_nodal, dtype=float))
             counter.add("line4", 0)
-            levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
-                                             c_tol=c_tol, counter=counter,
-                                             dense_cutoff=dense_cutoff, _load=(g, records),
-                                             _lean=lean)
-            parts, U1 = fast_transform.last_solve
-            fast_transform.last_solve = None
+            levels, counter, (parts, U1) = _transform(
+                M, A, tree, schedule, w_variant=w_variant, c_tol=c_tol, counter=counter,
+                dense_cutoff=dense_cutoff, _load=(g, records), _lean=lean)
             solution = MultiresSolution(u=dv.to_host(parts["partials"].device(q)),
                                         u1_coarse=dv.to_host(U1),
                                         subband_coeffs=parts["coeffs"],
@@ -1500,9 +1534,7 @@ def _fast_solve_device(M, A, g, tree, schedule, w_variant="orthonormal", lean=Fa
     k <= keep_below keep everything (per-level parity checks at q=12)."""
     counter = FlopCounter()
     records = []
-    levels, counter = fast_transform(M, A, tree, schedule, w_variant=w_variant,
-                                     counter=counter, _load=(g, records), _lean=lean,
-                                     _keep_below=keep_below)
-    parts, U1 = fast_transform.last_solve
-    fast_transform.last_solve = None
+    levels, counter, (parts, U1) = _transform(M, A, tree, schedule, w_variant=w_variant,
+                                              counter=counter, _load=(g, records),
+                                              _lean=lean, _keep_below=keep_below)
     return levels, parts, U1, counter
