@@ -40,7 +40,9 @@ CONFIGS = {
 }
 EPS, RHO, CTOL = 1e-13, 3, 1e-6
 METRIC = "fine-DOF/s for gamblet setup+solve (fp64)"
-CPU_SAMPLE_Q = 6
+# CPU sample of configs 1-3: the oracle's complete tight-mode pipeline on a
+# 2^CPU_WINDOW_Q x 2^CPU_WINDOW_Q block of the config's own instance
+CPU_WINDOW_Q = 7
 
 
 def instance_seeds(rank):
@@ -66,17 +68,51 @@ def build_inputs(q, coeff, rank=0):
     return grid, M, A, load, gb.build_hierarchy(grid)
 
 
-def cpu_oracle_sample(coeff, threads):
-    """The CPU oracle (numpy/scipy restatement of the reference, tight mode)
-    on the q=CPU_SAMPLE_Q instance of the same configuration family."""
+def window_inputs(q, coeff, m, index):
+    """Block `index` (row-major over the (2^q / 2^m)^2 disjoint blocks) of the
+    config's own q-instance: its coefficient cells and nodal load restricted
+    to a 2^m x 2^m node window with Dirichlet conditions on the window edge
+    (the same coefficient statistics, patch sizes and localization radii)."""
+    import paper_1503_03467_b200 as gb
+    grid = gb.build_grid(q)
+    if coeff == "example1":
+        c = gb.coefficient_example1(grid).as_cell_grid()
+        g = gb.example_load(grid).reshape(grid.n, grid.n)
+    else:
+        sa, sg = instance_seeds(0)
+        c = gb.coefficient_checkerboard(grid, 1e4, sa).as_cell_grid()
+        g = np.random.default_rng(sg).standard_normal(grid.num_nodes).reshape(grid.n, grid.n)
+    w = 1 << m
+    nb = grid.n // w
+    bi, bj = divmod(int(index) % (nb * nb), nb)
+    gw = gb.build_grid(m)
+    cw = gb.CoefficientField(gw, c[bi * w:bi * w + w + 1, bj * w:bj * w + w + 1].ravel().copy())
+    M = gb.assemble_mass(gw)
+    A = gb.assemble_stiffness(gw, cw)
+    load = gb.assemble_load(gw, g[bi * w:(bi + 1) * w, bj * w:(bj + 1) * w].ravel().copy(),
+                            mass=M)
+    return M, A, load, (bi, bj)
+
+
+def window_order(q, m):
+    """A fixed pseudo-random visiting order of the disjoint windows."""
+    nb = (1 << q) >> m
+    return np.random.default_rng(12345).permutation(nb * nb)
+
+
+def cpu_oracle_sample(q, coeff, threads, index=0):
+    """The CPU oracle (numpy/scipy restatement of the reference, tight mode,
+    direct patch solves) over one window of the config's own instance:
+    (fine-DOF/s, seconds, window)."""
     from threadpoolctl import threadpool_limits
     from oracle import gamblets_oracle as O
-    grid, M, A, load, tree = build_inputs(CPU_SAMPLE_Q, coeff)
+    m = min(q, CPU_WINDOW_Q)
+    M, A, load, win = window_inputs(q, coeff, m, index)
     with threadpool_limits(threads):
         t0 = time.perf_counter()
-        O.fast_solve(M, A, load.g_nodal, CPU_SAMPLE_Q, EPS, uniform_rho=RHO)
+        O.fast_solve(M, A, load.g_nodal, m, EPS, uniform_rho=RHO)
         dt = time.perf_counter() - t0
-    return 4 ** CPU_SAMPLE_Q / dt, dt
+    return 4 ** m / dt, dt, win
 
 
 class ClockSampler:
@@ -153,41 +189,17 @@ def fp64_peak_tflops():
 
 
 def kernel_timings(levels, q):
-    """Average device time of the dominant kernels, timed in isolation with
-    CUDA events on the launching stream (warm, 10 repeats for the SpMV)."""
+    """The finest level's Krylov operator, and the finest correction-patch
+    launch re-timed in isolation (CUDA events on the launching stream) on the
+    level's own B^(q) and a nonzero G block."""
     import torch
     from paper_1503_03467_b200 import _native as nat, device as dv, gamblet_fast as gf
     lv = levels[q]
     op = lv._op
-    if op is None:
-        return None
-    x = op.vec()
-    y = op.vec()
     s = dv.stream()
-    for _ in range(2):
-        op.apply(x, y)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    reps = 10
-    for _ in range(reps):
-        op.apply(x, y)
-    b.record()
-    torch.cuda.synchronize()
-    spmv_ms = a.elapsed_time(b) / reps
-    # algorithmic bytes: the stored operator values (full box, or the upper
-    # 3x3 blocks in the symmetric band layout) + x read once + y written once
-    spmv_bytes = int(8 * op.n * op.stored_slots) + 16 * op.n
-    # operator passes of the finest level's engine: the subband PCG's passes
-    # carry the power / Lanczos / inner-solve vectors as their second half
-    its = sum(max(d["power"] + (d["lanczos"] if "lanczos" in d
-                                else sum(d["inner"]) + len(d["inner"])), 0)
-              for d in gf._SPECTRAL_LOG[-(q - 1):] if d["n"] == op.n)
     B = lv.raw("subband")
     if B is None:  # lean transform (q >= 12): the subband box is not retained
-        return {"layout": op.layout,
-                "spmv": {"ms": spmv_ms, "bytes": spmv_bytes, "launches_per_step": its},
-                "corr": None}
+        return {"op": op, "corr": None}
     rho = min(3, B.L - 1)
     Dt = dv.empty(B.L * B.L * dv.box_slots(rho, 3))
     st = dv.zeros(2, torch.int64)
@@ -195,16 +207,42 @@ def kernel_timings(levels, q):
     ws, nb = gf._correction_ws(B.L, rho, 0, B.L)
     args = (B.L, B.w, dv.ptr(B.vals), dv.ptr(lv.raw("subband_scale")), B.w, dv.ptr(G), rho,
             dv.ptr(Dt), dv.ptr(st), dv.ptr(ws), nb, s)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nat.call("gb_correction_patches_v2", *args)
     torch.cuda.synchronize()
     a.record()
     nat.call("gb_correction_patches_v2", *args)
     b.record()
     torch.cuda.synchronize()
-    corr_ms = a.elapsed_time(b)
-    return {"layout": op.layout,
-            "spmv": {"ms": spmv_ms, "bytes": spmv_bytes, "launches_per_step": its},
-            "corr": {"ms": corr_ms, "flops": gf._patch_flops(B.L, rho, 3)}}
+    return {"op": op, "corr": {"ms": a.elapsed_time(b), "flops": gf._patch_flops(B.L, rho, 3)}}
+
+
+def ncu_traffic(config, q, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from this config's committed ncu --set full capture
+    (profiles/r02_ncu_traffic.json), or None when it was not captured."""
+    f = ROOT / "profiles" / "r02_ncu_traffic.json"
+    if not f.exists():
+        return None
+    return json.loads(f.read_text()).get(f"{config}:q{q}:{kernel}")
+
+
+def workload_config(name, q, world):
+    """The `config` object both arms print (identical for the same run)."""
+    cfg = CONFIGS[name]
+    N = 4 ** q
+    if cfg.get("exact"):
+        return {"workload": f"{name}: q={q}, N={N} fine DOFs, exact (global) gamblets, "
+                            "tight mode tol 1e-14", "q": q, "fine_dofs": N,
+                "parallelism": "single GPU" if world == 1 else f"{world} replicas"}
+    return {"workload": f"{name}: q={q}, N={N} fine DOFs, {cfg['coeff']}, "
+                        f"localized gamblets rho={RHO}, tight mode eps={EPS}",
+            "q": q, "fine_dofs": N, "rho": RHO, "epsilon": EPS,
+            "parallelism": (f"{world} independent seeded instances, one per GPU "
+                            "(weak scaling, no data-path collective)")
+                           if world > 1 else "single GPU",
+            "l2": "working set > 126 MB L2 (operators ~GBs), no flush needed",
+            "lean": bool(q >= 12)}
 
 
 def reduce_max(value, world, device=None):
@@ -269,9 +307,7 @@ def run_exact(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generators: example1 coefficient and load)",
-        "config": {"workload": f"c0: q={q}, N={N} fine DOFs, exact (global) gamblets, "
-                               "tight mode tol 1e-14", "q": q, "fine_dofs": N,
-                   "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
+        "config": workload_config(args.config, q, world),
         "e2e": {"value": round(value, 1), "unit": "fine-DOF/s", "ms_per_step": round(ms, 3),
                 "h2d_bytes_per_step": int(dv.Traffic.h2d / max(1, args.steps)),
                 "d2h_bytes_per_step": int(dv.Traffic.d2h / max(1, args.steps))},
@@ -324,6 +360,10 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     dv.Prof.reset(enabled=True)
+    # live timing of the dominant kernel inside the timed steps: the finest
+    # level's engine records CUDA events on its own stream around its first
+    # 64 dual-vector phase-1 launches (k_symb_apply_ws<2>) of every step
+    gf.ENGINE_TIMING = {"n": 3 * 4 ** (q - 1), "cap": 64, "ms": []}
     launches0 = nat.query("gb_launch_count")
     seg0 = torch.cuda.memory_stats().get("segment.all.allocated", 0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -351,6 +391,8 @@ def run_ours(args, rank, world, local_rank):
     ms = ev0.elapsed_time(ev1) / args.steps
     step_ms = [round(ev0.elapsed_time(marks[0]), 1)] + [
         round(a.elapsed_time(b_), 1) for a, b_ in zip(marks, marks[1:])]
+    engine_ms = list(gf.ENGINE_TIMING.get("ms", []))
+    gf.ENGINE_TIMING = None
     phase_ms = {k: v / args.steps for k, v in dv.Prof.times_ms().items()}
     phase_flops = {k: v / args.steps for k, v in dv.Prof.flops.items()}
     phase_bytes = {k: v / args.steps for k, v in dv.Prof.bytes.items()}
@@ -399,50 +441,77 @@ def run_ours(args, rank, world, local_rank):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs")
-    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if hbm_peak else "fallback B200_PROFILING.md"
+    hbm_src = ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if hbm_peak
+               else "fallback 6650 GB/s of B200_PROFILING.md")
     hbm_peak = hbm_peak or 6650.0
     fp64 = fp64_peak_tflops()
     fp64_peak = max(fp64.values())
 
-    # roofline of the dominant kernel: the finest-level S B S SpMV (spectral and
-    # subband iterations are ~all SpMV time); algorithmic bytes = the box
-    # values the format must stream (rows x slots x 8) + x window + y
-    sp = kern["spmv"]
-    op_layout = kern["layout"]
-    # finest-level passes: the subband PCG and the spectral sequence share them
-    passes = max(sp["launches_per_step"], max(iters.get("line8") or [0]))
-    achieved = sp["bytes"] / (sp["ms"] * 1e-3) / 1e9
-    prof_file = ROOT / "profiles" / "ncu_traffic.json"
-    traffic = None
-    if prof_file.exists():
-        traffic = json.loads(prof_file.read_text()).get(
-            "k_symb_apply+k_symb_fix" if op_layout == 1 else "k_tcg_spmv_tiled")
-    roof = {"kernel": ("k_symb_apply + k_symb_fix (finest-level S B S SpMV, symmetric band "
-                       "storage: upper 3x3 blocks, lower half applied by scatter)"
-                       if op_layout == 1 else
-                       "k_tcg_spmv_tiled / k_tpow_apply_tiled (finest-level S B S SpMV)"),
-            "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-            "peak_source": hbm_src,
-            "bytes_per_launch": sp["bytes"], "ms_per_launch": round(sp["ms"], 4),
-            "launches_per_step": passes,
-            "share_of_step_serialized": round(sp["ms"] * passes / ms, 3)}
+    # roofline of the dominant kernel: k_symb_apply_ws<2>, the finest level's
+    # dual-vector pass (subband PCG + Lanczos halves) of the symmetric band
+    # S B S SpMV, timed live inside the timed steps on the engine's stream.
+    # Algorithmic bytes per launch: the stored upper 3x3 blocks once, plus x
+    # read and y written for each of the two vectors
+    op = kern["op"]
+    dual_bytes = op.matrix_bytes + 4 * 8 * op.n
+    roof = None
+    if engine_ms:
+        dual_ms = float(np.mean(engine_ms))
+        achieved = dual_bytes / (dual_ms * 1e-3) / 1e9
+        roof = {"kernel": "k_symb_apply_ws<2> (finest-level S B S dual-vector pass: symmetric "
+                          "band, upper 3x3 blocks streamed once by bulk copies, lower half "
+                          "applied by scatter; PCG + Lanczos vectors)",
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "traffic": ncu_traffic(args.config, q, "k_symb_apply_ws<2>"),
+                "peak_source": hbm_src, "bytes_per_launch": int(dual_bytes),
+                "ms_per_launch": round(dual_ms, 4), "launches_timed": len(engine_ms),
+                "timing": "CUDA events on the level engine's stream around the first 64 "
+                          "dual launches of the finest level in every timed step"}
     cp = kern["corr"]
-    fp = None if cp is None else {"kernel": "k_correction_patches_v3 (finest level, left-looking tiled DMMA Cholesky, L streamed through L2 scratch)",
-          "bound": "fp64", "achieved": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12, 3),
-          "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
-          "frac": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12 / fp64_peak, 4),
-          "peak_source": "measured in-run (max of DFMA/DMMA probes; MEASURED_PEAKS.json "
-                         "has no fp64 figure)",
-          "ms_per_launch": round(cp["ms"], 3), "flops_per_launch": cp["flops"]}
+    fp = None if cp is None else {
+        "kernel": "k_correction_patches_v3 (finest level, left-looking tiled DMMA Cholesky, "
+                  "L streamed through an L2-resident scratch)",
+        "bound": "fp64", "achieved": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12, 3),
+        "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
+        "frac": round(cp["flops"] / (cp["ms"] * 1e-3) / 1e12 / fp64_peak, 4),
+        "peak_source": "measured in-run (max of DFMA/DMMA probes; MEASURED_PEAKS.json "
+                       "has no fp64 figure)",
+        "ms_per_launch": round(cp["ms"], 3), "flops_per_launch": cp["flops"],
+        "timing": "isolated re-launch after the timed region on the finest level's own B and "
+                  "its G block (CUDA events, same stream)"}
+
+    # aggregate step roofline: sum over phases of
+    # max(algorithmic flops / fp64 peak, algorithmic bytes / HBM peak), against
+    # the measured step time (phases on different streams overlap)
+    agg_phases = {}
+    roof_ms = 0.0
+    for lbl in sorted(set(phase_flops) | set(phase_bytes)):
+        f_ms = phase_flops.get(lbl, 0) / (fp64_peak * 1e12) * 1e3
+        b_ms = phase_bytes.get(lbl, 0) / (hbm_peak * 1e9) * 1e3
+        roof_ms += max(f_ms, b_ms)
+        agg_phases[lbl] = {"roof_ms": round(max(f_ms, b_ms), 3),
+                           "bound": "fp64" if f_ms > b_ms else "hbm",
+                           "measured_ms": round(phase_ms.get(lbl, 0.0), 3),
+                           "gflop": round(phase_flops.get(lbl, 0) / 1e9, 2),
+                           "gbytes": round(phase_bytes.get(lbl, 0) / 1e9, 3)}
+    aggregate = {"roofline_ms": round(roof_ms, 3), "step_ms": round(ms, 3),
+                 "frac": round(roof_ms / ms, 4),
+                 "dofs_per_s_at_roofline": round(N / (roof_ms * 1e-3), 1),
+                 "note": "per-phase measured_ms are CUDA-event spans per step on the "
+                         "launching stream; spans on the level-engine streams overlap the "
+                         "main stream",
+                 "phases": agg_phases}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, dt = cpu_oracle_sample(coeff, threads)
+        v, dt, win = cpu_oracle_sample(q, coeff, threads, index=int(window_order(q, min(q, CPU_WINDOW_Q))[0]))
+        m = min(q, CPU_WINDOW_Q)
         cpu = {"value": round(v, 2), "unit": "fine-DOF/s", "cores": threads, "kind": "port",
-               "sample": f"oracle/gamblets_oracle.fast_solve, q={CPU_SAMPLE_Q} instance of "
-                         f"the same config family ({4 ** CPU_SAMPLE_Q} DOFs), {dt:.1f} s"}
+               "sample": f"oracle/gamblets_oracle.fast_solve (tight mode) over window {win} "
+                         f"({1 << m}x{1 << m} nodes = {4 ** m} DOFs) of this config's own "
+                         f"q={q} instance, {dt:.1f} s"}
 
     clocks = clk.summary()
     out = {
@@ -459,14 +528,7 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "f64",
         "data": "synthetic (seeded reference generators: checkerboard contrast 1e4 seed 0, "
                 "Gaussian nodal load seed 1)",
-        "config": {"workload": f"{args.config}: q={q}, N={N} fine DOFs, {coeff}, "
-                               f"localized gamblets rho={RHO}, tight mode eps={EPS}",
-                   "q": q, "fine_dofs": N, "rho": RHO, "epsilon": EPS,
-                   "parallelism": (f"{world} independent seeded instances, one per GPU "
-                                   "(weak scaling, no data-path collective)")
-                                  if world > 1 else "single GPU",
-                   "l2": "working set > 126 MB L2 (operators ~GBs), no flush needed",
-                   "lean": bool(q >= 12)},
+        "config": workload_config(args.config, q, world),
         "e2e": {"value": round(whole_job_rate(N, world, e2e), 1), "unit": "fine-DOF/s",
                 "ms_per_step": round(e2e, 3), "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
@@ -475,6 +537,7 @@ def run_ours(args, rank, world, local_rank):
         "allocator_segments_timed": int(new_segments),
         "roofline": roof,
         "roofline_fp64": fp,
+        "roofline_aggregate": aggregate,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "step_ms": step_ms,
@@ -491,17 +554,27 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def run_reference(args, rank):
-    """Reference arm: the CPU oracle port (the reference is pure Python and
-    cannot travel to the GPU box), all host threads, bounded sample."""
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle port (numpy/scipy restatement of the
+    reference, tight mode, direct patch solves; the reference itself is pure
+    Python and cannot travel to the GPU box), all host threads.
+
+    Config 0: the complete q=5 exact sweep every step.  Configs 1-3: every
+    step is the oracle's complete pipeline (transform + subband solves) on one
+    2^7 x 2^7-node window of the config's OWN instance (its coefficient cells
+    and load; steps visit different windows in a fixed order), and the rate
+    is window DOFs / time.  The oracle's cost per DOF is level-size
+    independent (O(patch) gathers), so the window rate is the instance's
+    rate; the reference itself is super-linear (O(N) per patch extraction),
+    so this over-states the reference at q=10."""
     if rank != 0:
         return None
+    from threadpoolctl import threadpool_limits
+    from oracle import gamblets_oracle as O
     cfg = CONFIGS[args.config]
+    q = args.q or cfg["q"]
     threads = os.cpu_count() or 1
     if cfg.get("exact"):  # config 0: the whole q=5 exact sweep fits a CPU step
-        from threadpoolctl import threadpool_limits
-        from oracle import gamblets_oracle as O
-        q = cfg["q"]
         grid, M, A, load, tree = build_inputs(q, cfg["coeff"])
         times = []
         with threadpool_limits(threads):
@@ -510,37 +583,32 @@ def run_reference(args, rank):
                 O.exact_solve(M, A, load.b, q)
                 if i >= args.warmup:
                     times.append(time.perf_counter() - t0)
-        dt = float(np.median(times))
-        value = 4 ** q / dt
+        dofs = 4 ** q
         sample = (f"oracle/gamblets_oracle.exact_solve (dense direct restatement of the "
-                  f"reference's exact sweep), the full q={q} config per step")
-        return {
-            "impl": "reference", "metric": METRIC, "value": round(value, 2),
-            "unit": "fine-DOF/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} (q={q}, exact)"},
-            "cpu_baseline": {"value": round(value, 2), "unit": "fine-DOF/s", "cores": threads,
-                             "kind": "port", "sample": sample},
-            "e2e": {"value": round(value, 2), "unit": "fine-DOF/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-        }
-    times = []
-    for i in range(args.warmup + args.steps):
-        v, dt = cpu_oracle_sample(cfg["coeff"], threads)
-        if i >= args.warmup:
-            times.append(dt)
-    dt = float(np.median(times))
-    value = 4 ** CPU_SAMPLE_Q / dt
-    sample = (f"oracle/gamblets_oracle.fast_solve (numpy/scipy restatement of the "
-              f"reference, tight mode), q={CPU_SAMPLE_Q} instance of {args.config}'s "
-              f"config family ({4 ** CPU_SAMPLE_Q} DOFs) per step")
+                  f"reference's exact sweep), the full q={q} config every step")
+    else:
+        m = min(q, CPU_WINDOW_Q)
+        order = window_order(q, m)
+        times, wins = [], []
+        for i in range(args.warmup + args.steps):
+            _, dt, win = cpu_oracle_sample(q, cfg["coeff"], threads, index=int(order[i % len(order)]))
+            if i >= args.warmup:
+                times.append(dt)
+                wins.append(win)
+        dofs = 4 ** m
+        sample = (f"oracle/gamblets_oracle.fast_solve (tight mode, uniform rho={RHO}) on one "
+                  f"{1 << m}x{1 << m}-node window ({dofs} DOFs) of this config's own q={q} "
+                  f"instance per step (coefficient cells and load of the window, Dirichlet on "
+                  f"its edge); {len(set(wins))} distinct windows timed")
+    dt = float(np.mean(times))
+    value = dofs / dt
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 2),
-        "unit": "fine-DOF/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "unit": "fine-DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} (CPU sample q={CPU_SAMPLE_Q})"},
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded reference generators, same instance as the GPU arm)",
+        "config": workload_config(args.config, q, world),
         "cpu_baseline": {"value": round(value, 2), "unit": "fine-DOF/s", "cores": threads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 2), "unit": "fine-DOF/s", "h2d_bytes_per_step": 0,
@@ -570,7 +638,7 @@ def main():
         os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
         os.environ.setdefault("GB_SPECTRAL_WORKERS", "3")
     if args.impl == "reference":
-        out = run_reference(args, rank)
+        out = run_reference(args, rank, world)
     else:
         if world > 1:
             import torch

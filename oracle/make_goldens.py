@@ -96,6 +96,22 @@ def fast_case(gb, q, coeff, name):
     print("wrote", name)
 
 
+def sketch(X):
+    """X @ Omega with a fixed Gaussian Omega (ncols x 8, seeded by ncols):
+    ||(X - Y) Omega||_F / ||Y Omega||_F tracks the relative Frobenius error of
+    X against Y entry by entry (E||E Omega||^2 = 8 ||E||_F^2), so the dense
+    exact-path levels are pinned without storing them."""
+    X = np.asarray(X.toarray() if sp.issparse(X) else X, dtype=float)
+    om = np.random.default_rng(1000 + X.shape[1]).standard_normal((X.shape[1], 8))
+    return X @ om
+
+
+def sketch_err(X, sk):
+    """Relative error of X against a stored reference sketch X_ref @ Omega."""
+    mine = sketch(X)
+    return float(np.linalg.norm(mine - sk) / np.linalg.norm(sk))
+
+
 def exact_case(gb, q, coeff, name, full):
     grid, c, M, A, load, tree = problem(gb, q, coeff)
     sol, levels = gb.exact_solve(M, A, load, tree, tol_mass=1e-14, tol_subband=1e-14)
@@ -104,6 +120,12 @@ def exact_case(gb, q, coeff, name, full):
     for k, lv in levels.items():
         d[f"fro_A{k}"] = np.linalg.norm(lv.stiffness)
         d[f"fro_psi{k}"] = np.linalg.norm(lv.psi)
+        d[f"sk_A{k}"] = sketch(lv.stiffness)
+        d[f"sk_psi{k}"] = sketch(lv.psi)
+        if k >= 2:
+            d[f"sk_B{k}"] = sketch(lv.subband)
+            d[f"sk_R{k}"] = sketch(lv.restriction)
+            d[f"sk_D{k}"] = sketch(lv.correction)
         if full or k <= 2:
             d[f"A{k}"] = lv.stiffness
             d[f"psi{k}"] = lv.psi
@@ -153,6 +175,10 @@ def pins(gb):
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     gb = _ref()
+    if sys.argv[1:] == ["exact"]:  # regenerate only the exact-path fixtures
+        exact_case(gb, 3, "example1", "exact_q3_example1", full=True)
+        exact_case(gb, 5, "example1", "exact_q5_example1", full=False)
+        return
     pins(gb)
     fast_case(gb, 4, "example1", "fast_q4_example1")
     fast_case(gb, 5, "checker", "fast_q5_checker")

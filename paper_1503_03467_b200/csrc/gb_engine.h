@@ -41,4 +41,13 @@ typedef struct gb_level_engine_args {
   double* hlz;
   double lz_tol;
   int lz_its, lz_rc;
+  /* outputs: operator passes (phase-1 launches of the symmetric band SpMV)
+   * carrying two vectors (PCG + spectral) and one vector */
+  int64_t n_dual, n_single;
+  /* optional live timing: CUDA events on the engine's stream around the first
+   * ev_cap dual-vector phase-1 launches; durations (ms) into the pinned host
+   * array ev_ms, ev_n of them (ev_events: engine-internal, pass NULL) */
+  int ev_cap, ev_n;
+  float* ev_ms;
+  void* ev_events;
 } gb_level_engine_args;

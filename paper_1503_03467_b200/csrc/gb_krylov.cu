@@ -8,6 +8,8 @@
 // chunks of iterations without a round trip per step.  Reductions are two
 // level with a fixed order (per-block partials summed by the last block), so
 // every run is bitwise reproducible.
+#include <vector>
+
 #include "gb_common.cuh"
 #include "gb_kernels.h"
 
@@ -2262,11 +2264,17 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
 // ---- engine building blocks (count their launches into *nl) ----
 // dual pass: A (subband PCG, mode 0) and B (mode mb) on one sweep of S B S;
 // b_fused: B is a block-Jacobi PCG step whose update adds the spill-over
-static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, int mb,
+static int launch_dual(const gb_level_engine_args* ec, double* xb, double* yb, int mb,
                        int b_fused, cudaStream_t s, long long* nl) {
+  gb_level_engine_args* e = const_cast<gb_level_engine_args*>(ec);
+  e->n_dual += 1;
   if (e->layout == 1) {
+    cudaEvent_t* ev = (cudaEvent_t*)e->ev_events;
+    const bool timed = ev && e->ev_n < e->ev_cap;
+    if (timed) cudaEventRecord(ev[2 * e->ev_n], s);
     sym_phase1(e->L, e->w, e->BsT, 2, e->pa, e->apa, (KState*)e->sta, e->parta, 1, xb, yb,
                (KState*)e->stb, e->partb, b_fused, s);
+    if (timed) cudaEventRecord(ev[2 * e->ev_n++ + 1], s);
     *nl += 1;
     if (!b_fused) {
       sym_phase2(e->L, e->w, 1, xb, yb, (KState*)e->stb, e->partb, mb, nullptr, nullptr,
@@ -2293,6 +2301,7 @@ static int launch_dual(const gb_level_engine_args* e, double* xb, double* yb, in
 // one live Krylov half; fused: a block-Jacobi PCG step (see launch_dual)
 static int launch_single(const gb_level_engine_args* e, const double* x, double* y, void* st,
                          double* part, int mode, int fused, cudaStream_t s, long long* nl) {
+  const_cast<gb_level_engine_args*>(e)->n_single += 1;
   if (e->layout == 1) {
     sym_phase1(e->L, e->w, e->BsT, 1, x, y, (KState*)st, part, fused, nullptr, nullptr,
                nullptr, nullptr, 0, s);
@@ -2348,7 +2357,25 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl);
 static int inverse_iteration(gb_level_engine_args* e, cudaStream_t s, long long& nl);
 int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launches) {
   long long nl = 0;
-  const int rc = level_engine(e, s, nl);
+  e->n_dual = e->n_single = 0;
+  e->ev_n = 0;
+  std::vector<cudaEvent_t> ev;
+  if (e->ev_cap > 0 && e->ev_ms) {
+    ev.resize(2 * (size_t)e->ev_cap);
+    for (auto& x : ev) cudaEventCreate(&x);
+    e->ev_events = ev.data();
+  } else {
+    e->ev_events = nullptr;
+  }
+  int rc = level_engine(e, s, nl);
+  if (!ev.empty()) {
+    const cudaError_t se = e->ev_n > 0 ? cudaEventSynchronize(ev[2 * e->ev_n - 1]) : cudaSuccess;
+    for (int i = 0; i < e->ev_n && se == cudaSuccess; ++i)
+      cudaEventElapsedTime(&e->ev_ms[i], ev[2 * i], ev[2 * i + 1]);
+    for (auto& x : ev) cudaEventDestroy(x);
+    e->ev_events = nullptr;
+    if (!rc && se != cudaSuccess) rc = (int)se;
+  }
   *launches += nl;
   return rc;
 }

@@ -23,4 +23,6 @@ class LevelEngineArgs(ctypes.Structure):
         ("cz", _P), ("layout", ctypes.c_int),
         ("spectral_mode", ctypes.c_int), ("lz_cap", ctypes.c_int), ("lz", _P), ("hlz", _P),
         ("lz_tol", _D), ("lz_its", ctypes.c_int), ("lz_rc", ctypes.c_int),
+        ("n_dual", ctypes.c_int64), ("n_single", ctypes.c_int64),
+        ("ev_cap", ctypes.c_int), ("ev_n", ctypes.c_int), ("ev_ms", _P), ("ev_events", _P),
     ]

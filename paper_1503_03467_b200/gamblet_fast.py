@@ -417,6 +417,10 @@ class _POp:
         return self.slots + (self.slots & 1)
 
     @property
+    def matrix_bytes(self):
+        return int(8 * self.n * self.stored_slots)
+
+    @property
     def spmv_bytes(self):
         return 8 * self.n * self.stored_slots + 3 * 8 * self.npad
 
@@ -518,7 +522,14 @@ def _start_vectors(n, seed):
     return v
 
 
-def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
+def _eig_extremes_reference(op):
+    """The reference's eig_extremes verbatim on the device (power iteration,
+    inverse iteration with plain-CG inner solves to 1e-4): the cross-check of
+    the Lanczos-moment evaluation at sizes the host cannot run."""
+    return _eig_extremes(op, inner_solver="cg")
+
+
+def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337, inner_solver=None):
     """(lambda_min, lambda_max) of S B S as sparse_core.py:232-278: power
     iteration, then inverse iteration with warm-started inner solves to
     rel_tol max(1e-12, 1e-3 tol); start vectors from numpy default_rng(seed).
@@ -552,8 +563,9 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
     ykr = _Krylov(op.npad)
     dots = dv.empty(4)
     outer = []
+    inner_solver = inner_solver or SPECTRAL_INNER
     for _ in range(max_iter):
-        if SPECTRAL_INNER != "cg":  # warm start y_prev / lambda (see gb_level_engine)
+        if inner_solver != "cg":  # warm start y_prev / lambda (see gb_level_engine)
             yv, its, _, _, brk, _ = _pcg(op, x, inner, x0=y_prev, kr=ykr,
                                          x0_scale=1.0 / lam_min if y_prev is not None else 1.0)
         else:
@@ -586,6 +598,12 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337):
 
 
 _SPECTRAL_LOG = []
+
+# live timing of the level engine's dual-vector operator passes (bench.py):
+# {"n": rows of the level to time, "cap": launches per engine} -> the engine
+# records CUDA events on its own stream around its first `cap` dual phase-1
+# launches and appends their durations (ms) to ENGINE_TIMING["ms"]
+ENGINE_TIMING = None
 
 # pair the lambda estimate and the subband PCG of a level in one engine
 # (shared S B S passes); levels the tiled kernels do not cover run them apart
@@ -645,7 +663,15 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
         args.lz = dv.ptr(lz)
         args.hlz = hlz.data_ptr()
         args.lz_tol = LANCZOS_TOL
+    timing = ENGINE_TIMING
+    ev_ms = None
+    if timing is not None and timing.get("n") == n:
+        ev_ms = torch.zeros(int(timing["cap"]), dtype=torch.float32, pin_memory=True)
+        args.ev_cap = int(timing["cap"])
+        args.ev_ms = ev_ms.data_ptr()
     nat.call("gb_level_engine", nat.ctypes.byref(args), st)
+    if ev_ms is not None:
+        timing.setdefault("ms", []).extend(ev_ms[:args.ev_n].tolist())
     if args.breakdown == -2:
         raise NumericalError(f"Lanczos moments of S B S at n={n}: "
                              + ("nonpositive Ritz value (matrix is not SPD)" if args.lz_rc == 2
@@ -664,9 +690,15 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
                               "inner": [int(args.inner_its[i])
                                         for i in range(min(args.n_outer, 64))]})
     rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
+    # algorithmic HBM bytes of the engine's operator passes: the stored band
+    # once per phase-1 launch plus x/y of each vector it carries
+    vec = 2 * 8 * op.npad
+    dv.Prof.add_work("level_engine", nbytes=args.n_dual * (op.matrix_bytes + 2 * vec)
+                     + args.n_single * (op.matrix_bytes + vec))
     return {"x": xa, "its": int(h["it"]), "rel": rel, "conv": bool(h["converged"]),
             "brk": int(h["breakdown"]), "lam_min": float(args.lam_min),
-            "lam_max": float(args.lam_max), "calls": int(args.calls)}
+            "lam_max": float(args.lam_max), "calls": int(args.calls),
+            "passes": (int(args.n_dual), int(args.n_single))}
 
 # lambda estimates run on side streams (one per worker thread) so they overlap
 # the FP64-bound patch factorizations of the main stream
@@ -762,7 +794,7 @@ class _LevelTasks:
                 level._krylov_op = None
                 if getattr(level, "_lean", False) and not getattr(level, "_keep_op", False):
                     level._op = None  # the operator copy is not retained
-                return box["calls"], info, done
+                return box["calls"], info, done, True
             if SPECTRAL:
                 with dv.phase("spectral"):
                     lam_min, lam_max, calls = _eig_extremes(op)
@@ -777,20 +809,21 @@ class _LevelTasks:
         level._krylov_op = None
         if getattr(level, "_lean", False):
             level._op = None
-        return calls, info, done
+        return calls, info, done, False
 
     def join(self, counter):
         futs, self.futures = self.futures, []
         err = None
         for f in futs:
             try:
-                calls, (op_n, op_slots, op_bytes), done = f.result()
+                calls, (op_n, op_slots, op_bytes), done, engine = f.result()
             except Exception as e:  # keep joining, re-raise the first error
                 err = err or e
                 continue
             torch.cuda.current_stream().wait_event(done)
             counter.add("spectral", 2 * op_n * op_slots * calls)
-            dv.Prof.add_work("spectral", nbytes=calls * op_bytes)
+            if not engine:  # the engine books its own passes ("level_engine")
+                dv.Prof.add_work("spectral", nbytes=calls * op_bytes)
         if err is not None:
             raise err
 
@@ -853,7 +886,10 @@ def _level_q(M, A, tree, rho, ctx, counter):
     nmax = (2 * rho + 1) ** 2
     with dv.phase("mass_patches"):
         _mass_patches(n, Mb, sM, rho, wd, psi, ctx.st(ctx.slot("mass", "mass")), s)
-    dv.Prof.add_work("mass_patches", flops=_patch_flops(n, rho, 1))
+    # algorithmic work per phase (the aggregate roofline of bench.py): patch
+    # factor/solve flops, box values read once and written once
+    dv.Prof.add_work("mass_patches", flops=_patch_flops(n, rho, 1),
+                     nbytes=8 * N * (dv.box_slots(Mb.w, 1) + wd * wd))
     # the stiffness is needed only after the mass patches: a host-resident A
     # is uploaded on a copy stream while they run
     A = _canon(A)
@@ -892,6 +928,10 @@ def _level_q(M, A, tree, rho, ctx, counter):
         nat.call("gb_box_diag_min", N, 1, wR, dv.ptr(raw), ctx.dm(i), s)
         nat.call("gb_box_sym_drop", n, 1, wR, dv.ptr(raw), dv.ptr(Aq), ctx.dm(i),
                  ctx.sp(i), s)
+    dv.Prof.add_work("psi_A_psiT", flops=2 * N * dv.box_slots(wX, 1) * 9
+                     + 2 * N * dv.box_slots(wR, 1) * nmax,
+                     nbytes=8 * N * (wd * wd + dv.box_slots(Ab.w, 1) + dv.box_slots(wR, 1)))
+    dv.Prof.add_work("sym_drop", nbytes=16 * N * dv.box_slots(wR, 1))
     # flop model: patch Cholesky + two triangular solves; box products
     counter.add("line2a", _patch_flops(n, rho, 1))
     counter.add("line3", N * wd * wd)
@@ -1051,6 +1091,9 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
             Ab = None
             level.stiffness = None
         B = BoxMatrix(Bv, Lp, 3, wB, 3)
+        dv.Prof.add_work("level_blocks", flops=2 * J * dv.box_slots(wB, 3) * 16,
+                         nbytes=8 * (Lk * Lk * dv.box_slots(wA, 1) + J * dv.box_slots(wB, 3)
+                                     + J * dv.box_slots(wB, 1) + P * dv.box_slots(wB, 1)))
         counter.add("line7", 2 * J * dv.box_slots(wB, 3) * 16)
         counter.add("scaling", 2 * J * dv.box_slots(wB, 3) + J)
 
@@ -1061,6 +1104,7 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
                 op.bj_inv()
                 op._box = None
         level._op = op
+        dv.Prof.add_work("level_blocks", nbytes=8 * J * dv.box_slots(wB, 3) + op.matrix_bytes)
         level._lean = _lean
         level._keep_op = k == q  # the finest operator stays for instrumentation
         level.subband = B
@@ -1074,7 +1118,9 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         with dv.phase("correction_patches"):
             _correction_patches(Lp, B, op, sB, Gv, rho, Dt,
                                 ctx.st(ctx.slot("corr", f"level {k}", detail=k)), s)
-        dv.Prof.add_work("correction_patches", flops=_patch_flops(Lp, rho, 3))
+        dv.Prof.add_work("correction_patches", flops=_patch_flops(Lp, rho, 3),
+                         nbytes=8 * (J * dv.box_slots(wB, 3) + J * dv.box_slots(wB, 1)
+                                     + P * dv.box_slots(rho, 3)))
         counter.add("line11", _patch_flops(Lp, rho, 3))
         counter.record_solve(f"line11 level {k}", 1, 0.0, stages=1)
 
@@ -1083,6 +1129,8 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         with dv.phase("restriction"):
             nat.call("gb_restriction", Lp, rho, dv.ptr(Dt), w12, dv.ptr(Rv), s)
         counter.add("line12", 2 * P * dv.box_slots(rho, 4) * 3)
+        dv.Prof.add_work("restriction", nbytes=8 * P * (dv.box_slots(rho, 3)
+                                                        + dv.box_slots(rho, 4)))
         wBD = min(wB + rho, Lp - 1)
         BD = dv.empty(J * dv.box_slots(wBD, 1))
         wGD = min(wB + rho, Lp - 1)
@@ -1105,6 +1153,13 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
         nb = 3 * (2 * min(rho, wB) + 1) ** 2
         counter.add("line13", 2 * J * dv.box_slots(wBD, 1) * nb
                     + 2 * P * dv.box_slots(wA2, 1) * nb + 2 * P * dv.box_slots(wGD, 1) * nb)
+        dv.Prof.add_work("triple_product",
+                         flops=2 * J * dv.box_slots(wBD, 1) * nb
+                         + 2 * P * dv.box_slots(wA2, 1) * nb + 2 * P * dv.box_slots(wGD, 1) * nb,
+                         nbytes=8 * (J * dv.box_slots(wB, 3) + J * dv.box_slots(wB, 1)
+                                     + P * dv.box_slots(wB, 1) + P * dv.box_slots(rho, 3)
+                                     + P * dv.box_slots(wA2, 1)))
+        dv.Prof.add_work("sym_drop", nbytes=16 * P * dv.box_slots(wA2, 1))
 
         # psi^(k-1) = drop_row(0.25 P psi + D^T (W psi))
         psin = None
@@ -1141,6 +1196,9 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
                 level.psi = None
             counter.add("line14", 2 * P * wd2 * wd2 * 3 * (2 * rho + 1) ** 2 // 4
                         + 2 * J * wdw * wdw * 4)
+            dv.Prof.add_work("psi_next", flops=2 * P * wd2 * wd2 * 3 * (2 * rho + 1) ** 2 // 4,
+                             nbytes=8 * (Lk * Lk * wd * wd + P * dv.box_slots(rho, 3)
+                                         + P * wd2 * wd2))
 
     level.null_w = (lambda tree=tree, k=k, v=w_variant: tree.null_basis(k, v))
     if _lean:  # B^(k), D^(k,k-1) consumed; R kept until g^(k-1) = R g^(k)
@@ -1321,8 +1379,8 @@ class _LevelSolver:
         else:
             with dv.phase("subband_cg"):
                 zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), self.tol)
-        dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
-                                                     + 12 * 8 * op.n))
+            dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
+                                                         + 12 * 8 * op.n))
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")

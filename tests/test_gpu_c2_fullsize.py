@@ -141,3 +141,168 @@ def test_solve_is_linear_and_repeatable_at_full_size(c2):
     again, _ = gb.solve_with_transform(res.levels, gb.assemble_load(grid, g1, mass=M), tree,
                                        sched)
     assert np.array_equal(again.u, u1)
+
+
+# ---------------------------------------------------------------------------
+# the finest levels at full size: psi^(10), A^(10), psi^(9) windows, levels
+# 9 and 8 through the oracle's level step, the lambda estimates at k = 10
+# ---------------------------------------------------------------------------
+
+L10 = 2 ** Q
+NODES = [(0, 0), (0, 1023), (511, 512), (1023, 1023), (5, 700), (300, 2), (777, 1000)]
+
+
+def _psi_row(pw, i):
+    """Row i of a PsiWindows operator as {fine column: value} (nonzeros)."""
+    n, L = pw.n, pw.L
+    h = n // L
+    s, t = divmod(int(i), L)
+    os_ = min(max(s * h + pw.lo, 0), n - pw.wd)
+    ot_ = min(max(t * h + pw.lo, 0), n - pw.wd)
+    v = _vec(pw.vals, np.arange(i * pw.wd * pw.wd, (i + 1) * pw.wd * pw.wd)).reshape(pw.wd, pw.wd)
+    a, b = np.nonzero(v)
+    return dict(zip(((os_ + a) * n + ot_ + b).tolist(), v[a, b].tolist()))
+
+
+def _box_row(box, i):
+    """Row i of a 1-component box operator as {column: value} (nonzeros)."""
+    L, w = box.L, box.w
+    s, t = divmod(int(i), L)
+    v = _rows(box, [i])[0].reshape(2 * w + 1, 2 * w + 1)
+    a, b = np.nonzero(v)
+    return dict(zip(((s + a - w) * L + t + b - w).tolist(), v[a, b].tolist()))
+
+
+def _compare_rows(got, want, what, tol=1e-10):
+    cols = sorted(set(got) | set(want))
+    g = np.array([got.get(c, 0.0) for c in cols])
+    w = np.array([want.get(c, 0.0) for c in cols])
+    err = np.linalg.norm(g - w) / np.linalg.norm(w)
+    assert err <= tol, f"{what}: rel error {err:.3e}"
+    assert set(got) == set(want), f"{what}: support differs"
+
+
+@pytest.fixture(scope="module")
+def psi10(c2):
+    """psi^(10) exported once to canonical CSR (1 M rows, <= 49 per row)."""
+    return c2[5].levels[Q].psi
+
+
+@pytest.mark.parametrize("node", NODES)
+def test_finest_psi_windows(c2, node):
+    """psi^(10) row = s[i^rho] (S M S)[i^rho, i^rho]^{-1} s_i e_i
+    (gamblet_fast.py:464-498), recomputed on the host from M's rows."""
+    grid, M, A, load, tree, res = c2
+    pw = res.levels[Q].raw("psi")
+    i = node[0] * L10 + node[1]
+    s, Ms = O.diag_scale(M)
+    idx = O.box_indices(L10, i, RHO)
+    K = O.principal_dense(Ms, idx, np.full(M.shape[0], -1))
+    rhs = np.zeros(idx.size)
+    rhs[int(np.searchsorted(idx, i))] = s[i]
+    want = s[idx] * np.linalg.solve(K, rhs)
+    _compare_rows(_psi_row(pw, i), {int(c): v for c, v in zip(idx, want) if v != 0.0},
+                  f"psi^(10) row {node}")
+
+
+def test_finest_stiffness_rows(c2, psi10):
+    """A^(10) = drop_dead(sym(psi A psi^T)) (gamblet_fast.py:658-665) row by
+    row from the GPU's own psi^(10): row i of X = psi A psi^T, column i by
+    symmetry of A, the symmetrized entry, and the 1e-12 sqrt(d_i d_j) drop on
+    the diagonal d_j = psi_j A psi_j^T."""
+    import scipy.sparse as sp
+    grid, M, A, load, tree, res = c2
+    Ab = res.levels[Q].raw("stiffness")
+    Psi = sp.csr_array(psi10)
+    X = O.canon(Psi @ A)
+    d = np.asarray(X.multiply(Psi).sum(axis=1)).ravel()
+    PsiT = O.canon(Psi.T)
+    for node in NODES:
+        i = node[0] * L10 + node[1]
+        xi = X[[i], :]
+        row = (xi @ PsiT).toarray().ravel()
+        col = (Psi @ xi.T).toarray().ravel()
+        v = 0.5 * (row + col)
+        keep = np.abs(v) >= 1e-12 * np.sqrt(d[i] * d)
+        keep[i] = True
+        nz = np.nonzero(keep & (v != 0.0))[0]
+        want = dict(zip(nz.tolist(), v[nz].tolist()))
+        _compare_rows(_box_row(Ab, i), want, f"A^(10) row {node}")
+
+
+@pytest.mark.parametrize("node", [(0, 0), (255, 256), (511, 511), (3, 400), (137, 63)])
+def test_psi9_windows(c2, psi10, node):
+    """psi^(9) = drop_row(0.25 P psi^(10) + D^T (W psi^(10)))
+    (gamblet_fast.py:615-624) for one parent, from the GPU's psi^(10) and D."""
+    import scipy.sparse as sp
+    from paper_1503_03467_b200.hierarchy import w_template
+    grid, M, A, load, tree, res = c2
+    lv = res.levels[Q]
+    Psi = sp.csr_array(psi10)
+    Lp = L10 // 2
+    i = node[0] * Lp + node[1]
+    W = w_template("orthonormal")
+    Dtb = lv.raw("correction")
+    R1 = 2 * RHO + 1
+    dt = _rows(Dtb, [i])[0]
+
+    def kids(p):
+        a, b = divmod(p, Lp)
+        base = 2 * a * L10 + 2 * b
+        return [base, base + 1, base + L10, base + L10 + 1]
+
+    acc = 0.25 * Psi[kids(i), :].sum(axis=0)
+    for u in range(-RHO, RHO + 1):
+        for v in range(-RHO, RHO + 1):
+            a, b = node[0] + u, node[1] + v
+            if not (0 <= a < Lp and 0 <= b < Lp):
+                continue
+            p = a * Lp + b
+            rows = Psi[kids(p), :]
+            for c in range(3):
+                coef = dt[((u + RHO) * R1 + v + RHO) * 3 + c]
+                if coef != 0.0:
+                    acc = acc + coef * (sp.csr_array(W[c][None, :]) @ rows)
+    acc = sp.csr_array(acc)
+    vals = acc.toarray().ravel()
+    keep = np.abs(vals) >= 1e-11 * np.abs(vals).max()
+    nz = np.nonzero(keep & (vals != 0.0))[0]
+    want = dict(zip(nz.tolist(), vals[nz].tolist()))
+    _compare_rows(_psi_row(res.levels[Q - 1].raw("psi"), i), want, f"psi^(9) row {node}")
+
+
+@pytest.mark.parametrize("k", [9, 8])
+def test_fine_levels_match_oracle_level_step(c2, k):
+    """The oracle's level step (gamblet_fast.py:501-632, direct patch solves)
+    on the GPU's A^(k) at the two levels below the finest: B, R, D and
+    A^(k-1) within 1e-10 with identical patterns."""
+    test_coarse_levels_match_oracle_level_step(c2, k)
+
+
+def test_finest_lambda_estimates(c2):
+    """lambda_max of S B^(10) S: the reference's power iteration
+    (sparse_core.py:242-262) run on the host over the GPU's B^(10) rows
+    reproduces the engine's estimate; lambda_min: the engine's Lanczos-moment
+    evaluation of the inverse iteration against the reference's inverse
+    iteration itself (plain CG inner solves to 1e-4, run on the GPU, the
+    form checked against the reference goldens at q <= 5), within that inner
+    tolerance's effect."""
+    from paper_1503_03467_b200 import gamblet_fast as gf
+    grid, M, A, load, tree, res = c2
+    lv = res.levels[Q]
+    B = lv.subband
+    s, Bs = O.diag_scale(B)
+    x1, _ = O.start_vectors(Bs.shape[0])
+    x = x1 / np.linalg.norm(x1)
+    lam_max = 0.0
+    for _ in range(500):
+        y = Bs @ x
+        lam_max = float(x @ y)
+        res_ = float(np.linalg.norm(y - lam_max * x))
+        x = y / np.linalg.norm(y)
+        if res_ <= 0.05 * abs(lam_max):
+            break
+    np.testing.assert_allclose(lv.lambda_max_subband, lam_max, rtol=1e-6)
+    lam_min_ref, lam_max_gpu, _ = gf._eig_extremes_reference(lv._op)
+    np.testing.assert_allclose(lam_max_gpu, lam_max, rtol=1e-6)
+    np.testing.assert_allclose(lv.lambda_min_subband, lam_min_ref, rtol=5e-4)

@@ -52,6 +52,23 @@ def test_oracle_exact_matches_reference(golden, problem):
     assert O.rel_energy(p.A, sol["u"], G["u"]) <= 1e-12
 
 
+def test_oracle_exact_q5_matches_reference_every_level(golden, problem):
+    """Config 0 (q = 5): the oracle's exact sweep against the reference's
+    A, psi, B, R, D at every level (sketches) and u."""
+    from oracle.make_goldens import sketch_err
+    G = golden("exact_q5_example1")
+    p = problem(5)
+    sol, lv = O.exact_solve(p.M, p.A, p.load.b, 5)
+    for k in range(5, 0, -1):
+        assert sketch_err(lv[k]["stiffness"], G[f"sk_A{k}"]) <= 1e-12, k
+        assert sketch_err(lv[k]["psi"], G[f"sk_psi{k}"]) <= 1e-12, k
+        if k >= 2:
+            assert sketch_err(lv[k]["subband"], G[f"sk_B{k}"]) <= 1e-12, k
+            assert sketch_err(lv[k]["restriction"], G[f"sk_R{k}"]) <= 1e-12, k
+            assert sketch_err(lv[k]["correction"], G[f"sk_D{k}"]) <= 1e-12, k
+    assert O.rel_energy(p.A, sol["u"], G["u"]) <= 1e-12
+
+
 def test_oracle_reproduces_reference_goldens_json(problem):
     """The reference's own pinned values (pkg/tests/golden/goldens.json:
     fast/q4/relerr and fast/q4/biorth_defect, rtol 1e-3), reproduced by the
