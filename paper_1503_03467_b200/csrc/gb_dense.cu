@@ -1,7 +1,7 @@
 // K10: dense FP64 kernels for the exact (global-gamblet) path,
 // gamblet_exact.py:115-263 (config 0).  Row-major storage throughout.
 //
-//   - tiled DGEMM  C = alpha op(A) op(B) + beta C  (64x64 tiles, DFMA)
+//   - tiled DGEMM  C = alpha op(A) op(B) + beta C  (64x64 tiles, DMMA m8n8k4)
 //   - blocked right-looking Cholesky (panel in one CTA + DGEMM trailing update)
 //   - blocked triangular solves L L^T X = B (diagonal blocks by one CTA,
 //     off-diagonal updates by DGEMM)
@@ -10,66 +10,117 @@
 //
 // config 0 is launch/latency bound (6.4 GFlop total); these
 // kernels aim for correctness and reasonable DFMA use, not peak.
-#include <cublas_v2.h>
 #include <stdlib.h>
 
 #include "gb_common.cuh"
 
 namespace gb {
 
-constexpr int TM = 64, TN = 64, TK = 16;
+// Dense DGEMM on the FP64 tensor cores (DMMA m8n8k4 = mma.sync f64; tcgen05
+// has no f64 kind, so this is the FP64 tensor path on sm_100).  A CTA of 8
+// warps owns a 64 x 64 tile of C; warp (wm, wn) in a 2 x 4 grid owns 32 x 16
+// = 4 x 2 m8n8 accumulators.  K advances in chunks of 16 staged k-major in
+// shared memory (leading dimension 68 = 4 mod 16 doubles: the fragment loads
+// As[k0 + l%4][m0 + l/4] hit 16 distinct bank pairs per half warp); the next
+// chunk is fetched into registers while the current one is multiplied.
+// op(A) (m x k) and op(B) (k x n) are row-major with optional transposes.
+constexpr int TM = 64, TN = 64, TK = 16, TLD = 68;
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
 
 __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int k, double alpha,
                                                const double* __restrict__ A, int lda,
                                                int ta, const double* __restrict__ B,
                                                int ldb, int tb, double beta,
                                                double* __restrict__ C, int ldc) {
-  __shared__ double As[TK][TM + 1];
-  __shared__ double Bs[TK][TN + 1];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  __shared__ double As[2][TK * TLD];
+  __shared__ double Bs[2][TK * TLD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
   const int row0 = blockIdx.y * TM, col0 = blockIdx.x * TN;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < k; k0 += TK) {
-    for (int e = threadIdx.x; e < TM * TK; e += 256) {
-      const int r = e / TK, kk = e % TK;
+  // global -> register staging: 4 elements of A and 4 of B per thread
+  double ra[4], rb[4];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + 256 * u;
+      int r, kk;
+      if (ta) { kk = e >> 6; r = e & 63; } else { r = e >> 4; kk = e & 15; }
       const int gr = row0 + r, gk = k0 + kk;
       double v = 0.0;
       if (gr < m && gk < k) v = ta ? A[(long long)gk * lda + gr] : A[(long long)gr * lda + gk];
-      As[kk][r] = v;
+      ra[u] = v;
+      int c, kb;
+      if (tb) { c = e >> 4; kb = e & 15; } else { kb = e >> 6; c = e & 63; }
+      const int gc = col0 + c, gkb = k0 + kb;
+      double w = 0.0;
+      if (gc < n && gkb < k) w = tb ? B[(long long)gc * ldb + gkb] : B[(long long)gkb * ldb + gc];
+      rb[u] = w;
     }
-    for (int e = threadIdx.x; e < TK * TN; e += 256) {
-      const int kk = e / TN, c = e % TN;
-      const int gk = k0 + kk, gc = col0 + c;
-      double v = 0.0;
-      if (gk < k && gc < n) v = tb ? B[(long long)gc * ldb + gk] : B[(long long)gk * ldb + gc];
-      Bs[kk][c] = v;
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + 256 * u;
+      int r, kk;
+      if (ta) { kk = e >> 6; r = e & 63; } else { r = e >> 4; kk = e & 15; }
+      As[buf][kk * TLD + r] = ra[u];
+      int c, kb;
+      if (tb) { c = e >> 4; kb = e & 15; } else { kb = e >> 6; c = e & 63; }
+      Bs[buf][kb * TLD + c] = rb[u];
     }
-    __syncthreads();
+  };
+  double acc[4][2][2];
 #pragma unroll
-    for (int kk = 0; kk < TK; ++kk) {
-      double a[4], b[4];
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = (k + TK - 1) / TK;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int c = 0; c < nk; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nk) fetch((c + 1) * TK);
+    const double* as = As[buf];
+    const double* bs = Bs[buf];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+    for (int k4 = 0; k4 < TK; k4 += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(k4 + fk) * TLD + wm * 32 + i * 8 + fr];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = bs[(k4 + fk) * TLD + wn * 16 + j * 8 + fr];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 2; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
+    if (c + 1 < nk) {
+      stash(buf ^ 1);
+      __syncthreads();
+    }
   }
+  // epilogue: accumulator (i, j) element e at row fr, column 2 fk + e
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int gr = row0 + ty + 16 * i;
+    const int gr = row0 + wm * 32 + i * 8 + fr;
     if (gr >= m) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gc = col0 + tx + 16 * j;
-      if (gc >= n) continue;
-      double* c = C + (long long)gr * ldc + gc;
-      *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[i][j];
-    }
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gc = col0 + wn * 16 + j * 8 + 2 * fk + e;
+        if (gc >= n) continue;
+        double* cp = C + (long long)gr * ldc + gc;
+        *cp = (beta == 0.0 ? 0.0 : beta * *cp) + alpha * acc[i][j][e];
+      }
   }
 }
 
@@ -364,26 +415,10 @@ __global__ void k_dmma_probe(int iters, double* sink) {
 
 using namespace gb;
 
-// plain dense GEMMs go to cuBLAS (row-major C = op(A) op(B) is the
-// column-major C^T = op(B)^T op(A)^T); GB_DENSE_GEMM=own selects k_dgemm
-static cublasHandle_t g_cublas = nullptr;
-static int g_own_gemm = -1;
 int gbk_dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta,
                    const double* B, int ldb, int tb, double beta, double* C, int ldc,
                    cudaStream_t s) {
   if (m <= 0 || n <= 0) return 0;
-  if (g_own_gemm < 0) {
-    const char* e = getenv("GB_DENSE_GEMM");
-    g_own_gemm = (e && e[0] == 'o') ? 1 : 0;
-  }
-  if (!g_own_gemm) {
-    if (!g_cublas && cublasCreate(&g_cublas) != CUBLAS_STATUS_SUCCESS) return 999;
-    if (cublasSetStream(g_cublas, s) != CUBLAS_STATUS_SUCCESS) return 999;
-    const cublasStatus_t st =
-        cublasDgemm(g_cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n,
-                    m, k, &alpha, B, ldb, A, lda, &beta, C, ldc);
-    return st == CUBLAS_STATUS_SUCCESS ? 0 : 999;
-  }
   dim3 grid((n + TN - 1) / TN, (m + TM - 1) / TM);
   k_dgemm<<<grid, 256, 0, s>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
   return (int)cudaGetLastError();

@@ -13,5 +13,5 @@ for s in gb_box gb_patch gb_products gb_krylov gb_dense gb_diag gb_capi; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC $objs -o $out/libgamblets_b200.so \
-  -lcublas -Xlinker -rpath=/usr/local/cuda/lib64
+  -Xlinker -rpath=/usr/local/cuda/lib64
 echo built $out/libgamblets_b200.so
