@@ -438,6 +438,34 @@ def run_ours(args, rank, world, local_rank):
     # isolated timing of the dominant kernels on the last solve's finest level
     kern = kernel_timings(levels, q)
 
+    # repeat solves on the stored transform ("subsequent
+    # solves"): K loads one call at a time vs one batched call (subband PCGs
+    # two at a time through the dual-vector SpMV), host loads in, u out
+    rep = None
+    if args.repeat_solves > 0 and not lean:
+        sched = res_sched = gb.make_schedule(EPS, q, uniform_rho=RHO)
+        rng = np.random.default_rng(99)
+        loads = [gb.assemble_load(grid, rng.standard_normal(grid.num_nodes), mass=M)
+                 for _ in range(args.repeat_solves)]
+        gb.solve_with_transform(levels, loads[:2], tree, res_sched)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for ld in loads:
+            gb.solve_with_transform(levels, ld, tree, sched)
+        torch.cuda.synchronize()
+        t_single = (time.perf_counter() - t0) / len(loads)
+        t0 = time.perf_counter()
+        gb.solve_with_transform(levels, loads, tree, sched)
+        torch.cuda.synchronize()
+        t_batch = (time.perf_counter() - t0) / len(loads)
+        rep = {"loads": len(loads), "ms_per_load_single": round(t_single * 1e3, 3),
+               "ms_per_load_batched": round(t_batch * 1e3, 3),
+               "fine_dofs_per_s_batched": round(N / t_batch, 1),
+               "fine_dofs_per_s_single": round(N / t_single, 1),
+               "note": "solve_with_transform on the stored transform, host loads "
+                       "(g uploaded, u downloaded) inside the timing; wall clock with a "
+                       "device synchronize on both sides"}
+
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs")
@@ -538,6 +566,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof,
         "roofline_fp64": fp,
         "roofline_aggregate": aggregate,
+        "repeat_solves": rep,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "step_ms": step_ms,
@@ -626,6 +655,8 @@ def main():
     ap.add_argument("--q", type=int, default=None, help="override the config's q")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timeline", action="store_true")
+    ap.add_argument("--repeat-solves", type=int, default=4,
+                    help="loads of the repeat-solve leg (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

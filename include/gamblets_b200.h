@@ -255,6 +255,15 @@ int gb_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, 
 int gb_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, double* r,
                   double* p, double* Ap, double* z, void* state, double* partials,
                   void* host_state, int max_chunk, void* stream, int layout);
+/* two independent block-Jacobi PCG solves in lockstep sharing every operator
+ * pass (batched repeat solves of solve_with_transform, gamblet_fast.py:
+ * 717-760): each argument is a 2-array (vector 0, vector 1), both initialised
+ * by gb_bjcg_init; each result is bitwise the single solve's.  Symmetric band
+ * layout only (GB_ERR_INVALID otherwise). */
+int gb_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* const* x,
+                   double* const* r, double* const* p, double* const* Ap, double* const* z,
+                   void* const* state, double* const* partials, void* const* host_state,
+                   int max_chunk, void* stream);
 int gb_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,
                   void* state, double* partials, void* host_state, int max_chunk,
                   void* stream, int layout);

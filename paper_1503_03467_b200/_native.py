@@ -87,6 +87,7 @@ _SIGS = {
     "gb_sync_read": ([_P, _P, _Z, _P], _I),
     "gb_tcg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
     "gb_bjcg_solve": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I], _I),
+    "gb_bjcg_solve2": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
     "gb_tpow_solve": ([_I, _I, _I, _P, _P, _P, _D, _P, _P, _P, _I, _P, _I], _I),
     "gb_csr_apply": ([_L, _P, _P, _P, _P, _P, _P], _I),
     "gb_csr_cg_solve": ([_L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),

@@ -386,6 +386,19 @@ int gb_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, 
   COUNT(n);
   return wrap(e, "bjcg_solve");
 }
+int gb_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* const* x,
+                   double* const* r, double* const* p, double* const* Ap, double* const* z,
+                   void* const* state, double* const* partials, void* const* host_state,
+                   int max_chunk, void* stream) {
+  if (!x || !r || !p || !Ap || !z || !state || !partials || !host_state)
+    return invalid("bjcg_solve2: null pointer array");
+  long long n = 0;
+  const int e = gbk_bjcg_solve2(L, w, BsT, inv, x, r, p, Ap, z, state, partials, host_state,
+                                max_chunk, ST(stream), &n);
+  COUNT(n);
+  if (e == GB_UNSUPPORTED) return invalid("bjcg_solve2: level not in the symmetric band layout");
+  return wrap(e, "bjcg_solve2");
+}
 int gb_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,
                   void* state, double* partials, void* host_state, int max_chunk,
                   void* stream, int layout) {

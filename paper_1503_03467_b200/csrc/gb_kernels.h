@@ -156,6 +156,10 @@ int gbk_sync_read(const void* dev, void* host, size_t bytes, cudaStream_t s);
 int gbk_tcg_solve(int L, int nr, int w, const double* BsT, double* x, double* r, double* p,
                   double* Ap, void* st, double* part, void* host_state, int max_chunk,
                   cudaStream_t s, long long* launches, int layout);
+int gbk_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* const* x,
+                    double* const* r, double* const* p, double* const* Ap, double* const* z,
+                    void* const* st, double* const* part, void* const* host_state,
+                    int max_chunk, cudaStream_t s, long long* launches);
 int gbk_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, double* r,
                    double* p, double* Ap, double* z, void* st, double* part, void* host_state,
                    int max_chunk, cudaStream_t s, long long* launches, int layout);

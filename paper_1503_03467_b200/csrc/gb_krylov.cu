@@ -2168,6 +2168,46 @@ int gbk_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x,
   }
 }
 
+// Two independent block-Jacobi PCG solves on the same operator in lockstep
+// (batched repeat solves): one dual-vector phase-1 pass streams S B S once for
+// both search directions, then each vector's fused update and direction.
+// Every kernel computes a vector exactly as the single-vector solve does
+// (same per-vector summation order, same persistent grid), so each result is
+// bitwise the single solve's; a converged vector's kernels are no-ops
+// (KState.done) while the other one runs on.  Symmetric band layout only.
+int gbk_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* const* x,
+                    double* const* r, double* const* p, double* const* Ap, double* const* z,
+                    void* const* st, double* const* part, void* const* host_state,
+                    int max_chunk, cudaStream_t s, long long* launches) {
+  if (!use_sym(1, L, 3, w)) return GB_UNSUPPORTED;
+  const int Lpad = L + 2 * w;
+  const long long npad = (long long)Lpad * Lpad * 3;
+  const int gv = grid_for(npad, 256, kRedBlocks);
+  KState* k0 = (KState*)st[0];
+  KState* k1 = (KState*)st[1];
+  KState* h0 = (KState*)host_state[0];
+  KState* h1 = (KState*)host_state[1];
+  int chunk = 8;
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      sym_phase1(L, w, BsT, 2, p[0], Ap[0], k0, part[0], 1, p[1], Ap[1], k1, part[1], 1, s);
+      k_symb_bjcg_update<<<bj_grid(L), 192, 0, s>>>(L, w, x[0], r[0], p[0], Ap[0], z[0], inv,
+                                                     k0, part[0]);
+      k_cg_dir<<<gv, 256, 0, s>>>(npad, z[0], p[0], k0);
+      k_symb_bjcg_update<<<bj_grid(L), 192, 0, s>>>(L, w, x[1], r[1], p[1], Ap[1], z[1], inv,
+                                                     k1, part[1]);
+      k_cg_dir<<<gv, 256, 0, s>>>(npad, z[1], p[1], k1);
+    }
+    *launches += 5LL * chunk;
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    if ((e = read_state(st[0], h0, s))) return e;
+    if ((e = read_state(st[1], h1, s))) return e;
+    if (h0->done && h1->done) return 0;
+    chunk = chunk * 2 < max_chunk ? chunk * 2 : max_chunk;
+  }
+}
+
 int gbk_tpow_solve(int L, int nr, int w, const double* BsT, double* x, double* y, double tol,
                    void* st, double* part, void* host_state, int max_chunk, cudaStream_t s,
                    long long* launches, int layout) {

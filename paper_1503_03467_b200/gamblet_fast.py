@@ -1283,51 +1283,67 @@ def _transform(M, A, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TO
 def solve_with_transform(levels, load, tree, schedule, g_mode="nodal", counter=None):
     """Load-dependent phase (gamblet_fast.py:677-775): moments, subband CG per
     level, increments psi^(k)T W^T w^(k), restriction of the load, coarse
-    solve, reassembly.  Repeat solves reuse `levels` unchanged."""
+    solve, reassembly.  Repeat solves reuse `levels` unchanged.
+
+    Extension (batched repeat solves, "subsequent solves"):
+    `load` may be a list/tuple of loads; the subband PCGs of two loads then
+    share every operator pass (gb_bjcg_solve2) and the call returns
+    ([MultiresSolution, ...], counter), each solution bitwise the one a
+    single-load call returns."""
     counter = counter if counter is not None else FlopCounter()
     q = tree.q
     n = 1 << q
     N = n * n
     tol = schedule.subband_tol()
-    records = []
-    if isinstance(load, LoadVector):
-        b, g_nodal = load.b, load.g_nodal
-    else:
-        b, g_nodal = (load if isinstance(load, torch.Tensor)
-                      else np.asarray(load, dtype=float)), None
-    if tuple(b.shape) != (N,):
-        raise InvalidArgumentError(f"load shape {b.shape} does not match N={N}")
+    batch = isinstance(load, (list, tuple))
+    loads = list(load) if batch else [load]
+    if batch and not loads:
+        raise InvalidArgumentError("empty list of loads")
     s = dv.stream()
-
+    gs = []
     with counter.timer("solve phase"):
-        if g_mode == "nodal":
-            if g_nodal is None:
-                raise InvalidArgumentError(
-                    "nodal moment shortcut needs a LoadVector with g_nodal; "
-                    "pass g_mode='measured' for a bare right-hand side")
-            g = dv.to_dev(g_nodal if isinstance(g_nodal, torch.Tensor)
-                          else np.asarray(g_nodal, dtype=float))
-            counter.add("line4", 0)
-        elif g_mode == "measured":
-            psiq = levels[q].raw("psi")
-            if not isinstance(psiq, PsiWindows):
-                psiq = _psi_dev(levels[q], n, n)
-            bd = dv.to_dev(b)
-            g = dv.empty(N)
-            nat.call("gb_psi_apply", n, n, psiq.lo, psiq.wd, dv.ptr(psiq.vals), dv.ptr(bd),
-                     dv.ptr(g), s)
-            counter.add("line4", 2 * N * psiq.wd * psiq.wd)
+        for ld in loads:
+            if isinstance(ld, LoadVector):
+                b, g_nodal = ld.b, ld.g_nodal
+            else:
+                b, g_nodal = (ld if isinstance(ld, torch.Tensor)
+                              else np.asarray(ld, dtype=float)), None
+            if tuple(b.shape) != (N,):
+                raise InvalidArgumentError(f"load shape {b.shape} does not match N={N}")
+            if g_mode == "nodal":
+                if g_nodal is None:
+                    raise InvalidArgumentError(
+                        "nodal moment shortcut needs a LoadVector with g_nodal; "
+                        "pass g_mode='measured' for a bare right-hand side")
+                g = dv.to_dev(g_nodal if isinstance(g_nodal, torch.Tensor)
+                              else np.asarray(g_nodal, dtype=float))
+                counter.add("line4", 0)
+            elif g_mode == "measured":
+                psiq = levels[q].raw("psi")
+                if not isinstance(psiq, PsiWindows):
+                    psiq = _psi_dev(levels[q], n, n)
+                bd = dv.to_dev(b)
+                g = dv.empty(N)
+                nat.call("gb_psi_apply", n, n, psiq.lo, psiq.wd, dv.ptr(psiq.vals), dv.ptr(bd),
+                         dv.ptr(g), s)
+                counter.add("line4", 2 * N * psiq.wd * psiq.wd)
+            else:
+                raise InvalidArgumentError(f"unknown g_mode {g_mode!r}")
+            gs.append(g)
+        records = [[] for _ in gs]
+        if batch:
+            outs = _solve_levels_batch(levels, gs, tree, schedule, tol, counter, records)
         else:
-            raise InvalidArgumentError(f"unknown g_mode {g_mode!r}")
-        g = _solve_levels(levels, g, tree, schedule, tol, counter, records)
+            outs = [_solve_levels(levels, gs[0], tree, schedule, tol, counter, records[0])]
 
-    sol_parts, U1 = g
-    u = dv.to_host(sol_parts["partials"].device(q))
-    solution = MultiresSolution(u=u, u1_coarse=dv.to_host(U1),
-                                subband_coeffs=sol_parts["coeffs"],
-                                increments=sol_parts["increments"],
-                                partials=sol_parts["partials"], records=records)
-    return solution, counter
+    sols = []
+    for (sol_parts, U1), recs in zip(outs, records):
+        u = dv.to_host(sol_parts["partials"].device(q))
+        sols.append(MultiresSolution(u=u, u1_coarse=dv.to_host(U1),
+                                     subband_coeffs=sol_parts["coeffs"],
+                                     increments=sol_parts["increments"],
+                                     partials=sol_parts["partials"], records=recs))
+    return (sols if batch else sols[0]), counter
 
 
 class _LevelSolver:
@@ -1356,12 +1372,23 @@ class _LevelSolver:
         return lvl, B, R
 
     def subband(self, k, g, pipelined=False, engine=None, psi=None):
+        op, sB, rhs = self.subband_rhs(k, g, pipelined)
+        if engine is not None:
+            zp, its, rel, conv, brk = engine(op, op.pad(rhs), self.tol)
+        else:
+            with dv.phase("subband_cg"):
+                zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), self.tol)
+            dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
+                                                         + 12 * 8 * op.n))
+        self.subband_finish(k, op, sB, zp, its, rel, conv, brk, psi)
+
+    def subband_rhs(self, k, g, pipelined=False):
+        """(operator, s_B, rhs = s (W g)) of level k (gamblet_fast.py:717-722)."""
         lvl = self.levels[k]
         op = getattr(lvl, "_krylov_op", None) if pipelined else None
         if op is None:  # B^(k) must be on the level (a lean level hands its operator over)
             lvl, B, _ = self._check(k, need_r=not pipelined)
         s = dv.stream()
-        counter = self.counter
         sB = lvl.raw("subband_scale")
         if not isinstance(sB, torch.Tensor):
             sB = dv.empty(B.rows)
@@ -1370,17 +1397,20 @@ class _LevelSolver:
         w12 = w_template(lvl.w_variant or "orthonormal").ctypes.data
         if op is None:
             op = getattr(lvl, "_op", None) or _POp(B, sB)
+            lvl._op = op  # the Krylov copy is kept for repeat solves
         Lp, J = op.L, op.n
         rhs = dv.empty(J)
         nat.call("gb_apply_w", Lp, w12, dv.ptr(g), dv.ptr(sB), dv.ptr(rhs), s)
-        counter.add("line8", 8 * J + J)
-        if engine is not None:
-            zp, its, rel, conv, brk = engine(op, op.pad(rhs), self.tol)
-        else:
-            with dv.phase("subband_cg"):
-                zp, its, rel, conv, brk, _ = _pcg(op, op.pad(rhs), self.tol)
-            dv.Prof.add_work("subband_cg", nbytes=its * (op.spmv_bytes + 10 * 8 * op.npad
-                                                         + 12 * 8 * op.n))
+        self.counter.add("line8", 8 * J + J)
+        return op, sB, rhs
+
+    def subband_finish(self, k, op, sB, zp, its, rel, conv, brk, psi=None):
+        """w = s z, the increment psi^T W^T w (gamblet_fast.py:723-745)."""
+        lvl = self.levels[k]
+        s = dv.stream()
+        counter = self.counter
+        Lp, J = op.L, op.n
+        w12 = w_template(lvl.w_variant or "orthonormal").ctypes.data
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0 "
                                  "(matrix is not SPD)")
@@ -1470,6 +1500,72 @@ def _solve_levels(levels, g, tree, schedule, tol, counter, records):
         g = sv.restrict(k, g)
     sv.coarse(g)
     return sv.finish()
+
+
+def _pcg2(op, b0, b1, rel_tol):
+    """Two block-Jacobi PCG solves on one operator in lockstep, sharing every
+    S B S pass (gb_bjcg_solve2); each result is bitwise _pcg's.  Returns the
+    two _pcg tuples."""
+    max_iter = min(max(200, 2 * op.n), MAX_ITER_CAP)
+    inv = op.bj_inv()
+    st = dv.stream()
+    vecs, krs = [], []
+    for b in (b0, b1):
+        kr = _Krylov(op.npad)
+        x, r, p, Ap, z = (op.vec() for _ in range(5))
+        nat.call("gb_state_reset", dv.ptr(kr.state), max_iter, st)
+        nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(b), None, None, 1.0, dv.ptr(x), dv.ptr(r),
+                 dv.ptr(p), dv.ptr(z), dv.ptr(inv), float(rel_tol), int(max_iter),
+                 dv.ptr(kr.state), dv.ptr(kr.part), st)
+        vecs.append((x, r, p, Ap, z))
+        krs.append(kr)
+    P2 = nat.ctypes.c_void_p * 2
+    arr = lambda i: P2(*(dv.ptr(v[i]) for v in vecs))  # noqa: E731
+    nat.call("gb_bjcg_solve2", op.L, op.w, dv.ptr(op.BsT), dv.ptr(inv), arr(0), arr(1),
+             arr(2), arr(3), arr(4), P2(*(dv.ptr(kr.state) for kr in krs)),
+             P2(*(dv.ptr(kr.part) for kr in krs)), P2(*(kr.host.data_ptr() for kr in krs)),
+             128, st)
+    out = []
+    for (x, *_), kr in zip(vecs, krs):
+        h = kr.host_view()
+        rel = float(h["rnorm"] / h["bnorm"]) if h["bnorm"] > 0 else 0.0
+        out.append((x, int(h["it"]), rel, bool(h["converged"]), int(h["breakdown"]), h))
+    return out
+
+
+def _solve_levels_batch(levels, gs, tree, schedule, tol, counter, records):
+    """The sequential solve phase for several loads at once: per level, the
+    subband PCGs run two at a time through the dual-vector symmetric SpMV
+    (one stream of S B^(k) S per pass for both loads); every other step is
+    the single-load arithmetic.  Each result is bitwise the single solve's."""
+    svs = [_LevelSolver(levels, tree, tol, counter, recs) for recs in records]
+    gs = list(gs)
+    for k in range(tree.q, 1, -1):
+        prep = [sv.subband_rhs(k, g) for sv, g in zip(svs, gs)]
+        op = prep[0][0]
+        i = 0
+        while i < len(svs):
+            if i + 1 < len(svs) and op.layout == 1 and op.nr == 3:
+                with dv.phase("subband_cg2"):
+                    res = _pcg2(op, op.pad(prep[i][2]), op.pad(prep[i + 1][2]), tol)
+                its = max(r[1] for r in res)
+                dv.Prof.add_work("subband_cg2", nbytes=its * (op.matrix_bytes
+                                                              + 2 * (3 * 8 * op.npad
+                                                                     + 10 * 8 * op.npad)))
+                for j, (zp, it, rel, conv, brk, _) in enumerate(res):
+                    svs[i + j].subband_finish(k, op, prep[i + j][1], zp, it, rel, conv, brk)
+                i += 2
+            else:
+                with dv.phase("subband_cg"):
+                    zp, it, rel, conv, brk, _ = _pcg(op, op.pad(prep[i][2]), tol)
+                svs[i].subband_finish(k, op, prep[i][1], zp, it, rel, conv, brk)
+                i += 1
+        gs = [sv.restrict(k, g) for sv, g in zip(svs, gs)]
+    out = []
+    for sv, g in zip(svs, gs):
+        sv.coarse(g)
+        out.append(sv.finish())
+    return out
 
 
 # ---------------------------------------------------------------------------
