@@ -259,7 +259,8 @@ int gb_bjcg_solve(int L, int w, const double* BsT, const float* inv, double* x, 
  * pass (batched repeat solves of solve_with_transform, gamblet_fast.py:
  * 717-760): each argument is a 2-array (vector 0, vector 1), both initialised
  * by gb_bjcg_init; each result is bitwise the single solve's.  Symmetric band
- * layout only (GB_ERR_INVALID otherwise). */
+ * layout with the warp-specialized pass for one and two vectors only
+ * (GB_ERR_INVALID otherwise). */
 int gb_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* const* x,
                    double* const* r, double* const* p, double* const* Ap, double* const* z,
                    void* const* state, double* const* partials, void* const* host_state,
@@ -370,6 +371,49 @@ int gb_dense_build_p(int Lk, double* out, double scale, void* stream);
 
 /* ---- FP64 peak probes (DFMA / DMMA) used for the roofline denominators --- */
 int gb_fp64_peak_probe(int kind, int iters, double* sink, void* stream);
+
+
+/* ---- config 4 (BASELINE.json configs[4]): the 3-D localized transform on
+ *      3-D box stencils (csrc/gb_3d.cu); the reference is 2-D only, the
+ *      algorithm is gamblet_fast.py:464-775 in d = 3 (8 children, 7 Helmert
+ *      W rows per parent, pibar = pi/8), restated by
+ *      oracle/gamblets_oracle_nd.py.  host_w: 7 x 8 row-major W template. */
+int gb3_csr_to_box(int L, int w, const int32_t* indptr, const int32_t* indices,
+                   const double* data, double* box, int64_t* status, void* stream);
+int gb3_box_scale(int64_t rows, int nr, int w, const double* box, double* s, int64_t* status,
+                  void* stream);
+int gb3_box_sym_drop(int L, int nr, int w, const double* raw, double* out, double* dmin,
+                     double* stats, void* stream);
+int gb3_mass_patches(int L, const double* Ms, const double* s, int rho, int wd, double* psi,
+                     int64_t* status, void* stream);
+int gb3_psi_galerkin(int L, int rho, int wd, const double* psi, const double* A, int wX,
+                     double* X, int wR, double* raw, void* stream);
+int gb3_level_blocks(int Lk, int wA, const double* A, const double* host_w, int wB, double* Braw,
+                     double* G, double* PAPt, void* stream);
+size_t gb3_correction_workspace(int Lp, int rho, int ctas);
+int gb3_correction_patches(int Lp, int wB, const double* B, const double* sB, const double* G,
+                           int rho, double* Dt, int64_t* status, double* workspace, int ctas,
+                           void* stream);
+int gb3_restriction(int Lp, int rho, const double* Dt, const double* host_w, double* R,
+                    void* stream);
+int gb3_triple(int Lp, int wB, const double* B, const double* G, const double* PAPt, int rho,
+               const double* Dt, int wBD, double* BD, int wGD, double* GtD, int wA2, double* raw,
+               void* stream);
+int gb3_apply_w(int Lp, const double* host_w, const double* g, const double* s, double* out,
+                void* stream);
+int gb3_apply_wt(int Lp, const double* host_w, const double* w, double* v, void* stream);
+int gb3_apply_r(int Lp, int rho, const double* R, const double* g, double* out, void* stream);
+int gb3_apply_rt(int Lp, int rho, const double* R, const double* u, double* out, void* stream);
+int gb3_psi_t_apply(int L, int rho, int wd, const double* psi, const double* v, double* out,
+                    void* stream);
+int gb3_apply(int L, int nr, int w, const double* B, const double* s, const double* x, double* y,
+              void* stream);
+int gb3_cg_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* r,
+                 double* p, double* Ap, void* state, double* partials, void* host_state,
+                 int max_chunk, void* stream);
+int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* y,
+                  double tol, void* state, double* partials, void* host_state, int max_chunk,
+                  void* stream);
 
 #ifdef __cplusplus
 }

@@ -129,6 +129,25 @@ _SIGS = {
     "gb_csr_to_dense": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "gb_eye": ([_I, _P, _P], _I),
     "gb_fp64_peak_probe": ([_I, _I, _P, _P], _I),
+    # config 4: 3-D box stencils (csrc/gb_3d.cu)
+    "gb3_csr_to_box": ([_I, _I, _P, _P, _P, _P, _P, _P], _I),
+    "gb3_box_scale": ([_L, _I, _I, _P, _P, _P, _P], _I),
+    "gb3_box_sym_drop": ([_I, _I, _I, _P, _P, _P, _P, _P], _I),
+    "gb3_mass_patches": ([_I, _P, _P, _I, _I, _P, _P, _P], _I),
+    "gb3_psi_galerkin": ([_I, _I, _I, _P, _P, _I, _P, _I, _P, _P], _I),
+    "gb3_level_blocks": ([_I, _I, _P, _P, _I, _P, _P, _P, _P], _I),
+    "gb3_correction_workspace": ([_I, _I, _I], _Z),
+    "gb3_correction_patches": ([_I, _I, _P, _P, _P, _I, _P, _P, _P, _I, _P], _I),
+    "gb3_restriction": ([_I, _I, _P, _P, _P, _P], _I),
+    "gb3_triple": ([_I, _I, _P, _P, _P, _I, _P, _I, _P, _I, _P, _I, _P, _P], _I),
+    "gb3_apply_w": ([_I, _P, _P, _P, _P, _P], _I),
+    "gb3_apply_wt": ([_I, _P, _P, _P, _P], _I),
+    "gb3_apply_r": ([_I, _I, _P, _P, _P, _P], _I),
+    "gb3_apply_rt": ([_I, _I, _P, _P, _P, _P], _I),
+    "gb3_psi_t_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "gb3_apply": ([_I, _I, _I, _P, _P, _P, _P, _P], _I),
+    "gb3_cg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
+    "gb3_pow_solve": ([_I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
 }
 
 EXPORTED = tuple(_SIGS)

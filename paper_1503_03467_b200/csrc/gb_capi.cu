@@ -45,7 +45,7 @@ static int invalid(const char* msg) {
 
 extern "C" {
 
-int gb_abi_version(void) { return 4; }
+int gb_abi_version(void) { return 5; }
 unsigned long long gb_launch_count(void) { return g_launches.load(); }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
@@ -612,6 +612,116 @@ int gb_eye(int n, double* out, void* stream) {
 int gb_fp64_peak_probe(int kind, int iters, double* sink, void* stream) {
   COUNT(1);
   return wrap(gbk_fp64_peak_probe(kind, iters, sink, ST(stream)), "fp64_peak_probe");
+}
+
+
+/* ---- config 4: 3-D box stencils (gb_3d.cu) ------------------------------ */
+int gb3_csr_to_box(int L, int w, const int32_t* indptr, const int32_t* indices,
+                   const double* data, double* box, int64_t* status, void* stream) {
+  if (L <= 0 || w < 0) return invalid("gb3_csr_to_box: bad geometry");
+  COUNT(1);
+  return wrap(gbk3_csr_to_box(L, w, indptr, indices, data, box, LL(status), ST(stream)),
+              "gb3_csr_to_box");
+}
+int gb3_box_scale(int64_t rows, int nr, int w, const double* box, double* s, int64_t* status,
+                  void* stream) {
+  COUNT(1);
+  return wrap(gbk3_box_scale(rows, nr, w, box, s, LL(status), ST(stream)), "gb3_box_scale");
+}
+int gb3_box_sym_drop(int L, int nr, int w, const double* raw, double* out, double* dmin,
+                     double* stats, void* stream) {
+  if (raw == out) return invalid("gb3_box_sym_drop: in-place not supported");
+  COUNT(2);
+  return wrap(gbk3_box_sym_drop(L, nr, w, raw, out, dmin, stats, ST(stream)), "gb3_box_sym_drop");
+}
+int gb3_mass_patches(int L, const double* Ms, const double* s, int rho, int wd, double* psi,
+                     int64_t* status, void* stream) {
+  COUNT(1);
+  const int rc = gbk3_mass_patches(L, Ms, s, rho, wd, psi, LL(status), ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("gb3_mass_patches: patch exceeds shared memory");
+  return wrap(rc, "gb3_mass_patches");
+}
+int gb3_psi_galerkin(int L, int rho, int wd, const double* psi, const double* A, int wX,
+                     double* X, int wR, double* raw, void* stream) {
+  COUNT(2);
+  return wrap(gbk3_psi_galerkin(L, rho, wd, psi, A, wX, X, wR, raw, ST(stream)),
+              "gb3_psi_galerkin");
+}
+int gb3_level_blocks(int Lk, int wA, const double* A, const double* host_w, int wB, double* Braw,
+                     double* G, double* PAPt, void* stream) {
+  if (!host_w || Lk < 2) return invalid("gb3_level_blocks: bad arguments");
+  COUNT(1);
+  return wrap(gbk3_level_blocks(Lk, wA, A, host_w, wB, Braw, G, PAPt, ST(stream)),
+              "gb3_level_blocks");
+}
+size_t gb3_correction_workspace(int Lp, int rho, int ctas) {
+  return gbk3_correction_workspace(Lp, rho, ctas);
+}
+int gb3_correction_patches(int Lp, int wB, const double* B, const double* sB, const double* G,
+                           int rho, double* Dt, int64_t* status, double* workspace, int ctas,
+                           void* stream) {
+  if (!workspace || ctas <= 0) return invalid("gb3_correction_patches: no workspace");
+  COUNT(1);
+  return wrap(gbk3_correction_patches(Lp, wB, B, sB, G, rho, Dt, LL(status), workspace, ctas,
+                                      ST(stream)),
+              "gb3_correction_patches");
+}
+int gb3_restriction(int Lp, int rho, const double* Dt, const double* host_w, double* R,
+                    void* stream) {
+  COUNT(1);
+  return wrap(gbk3_restriction(Lp, rho, Dt, host_w, R, ST(stream)), "gb3_restriction");
+}
+int gb3_triple(int Lp, int wB, const double* B, const double* G, const double* PAPt, int rho,
+               const double* Dt, int wBD, double* BD, int wGD, double* GtD, int wA2, double* raw,
+               void* stream) {
+  COUNT(3);
+  return wrap(gbk3_triple(Lp, wB, B, G, PAPt, rho, Dt, wBD, BD, wGD, GtD, wA2, raw, ST(stream)),
+              "gb3_triple");
+}
+int gb3_apply_w(int Lp, const double* host_w, const double* g, const double* s, double* out,
+                void* stream) {
+  COUNT(1);
+  return wrap(gbk3_apply_w(Lp, host_w, g, s, out, ST(stream)), "gb3_apply_w");
+}
+int gb3_apply_wt(int Lp, const double* host_w, const double* w, double* v, void* stream) {
+  COUNT(1);
+  return wrap(gbk3_apply_wt(Lp, host_w, w, v, ST(stream)), "gb3_apply_wt");
+}
+int gb3_apply_r(int Lp, int rho, const double* R, const double* g, double* out, void* stream) {
+  COUNT(1);
+  return wrap(gbk3_apply_r(Lp, rho, R, g, out, ST(stream)), "gb3_apply_r");
+}
+int gb3_apply_rt(int Lp, int rho, const double* R, const double* u, double* out, void* stream) {
+  COUNT(1);
+  return wrap(gbk3_apply_rt(Lp, rho, R, u, out, ST(stream)), "gb3_apply_rt");
+}
+int gb3_psi_t_apply(int L, int rho, int wd, const double* psi, const double* v, double* out,
+                    void* stream) {
+  COUNT(1);
+  return wrap(gbk3_psi_t_apply(L, rho, wd, psi, v, out, ST(stream)), "gb3_psi_t_apply");
+}
+int gb3_apply(int L, int nr, int w, const double* B, const double* s, const double* x, double* y,
+              void* stream) {
+  COUNT(1);
+  return wrap(gbk3_apply(L, nr, w, B, s, x, y, ST(stream)), "gb3_apply");
+}
+int gb3_cg_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* r,
+                 double* p, double* Ap, void* state, double* partials, void* host_state,
+                 int max_chunk, void* stream) {
+  long long n = 0;
+  const int e = gbk3_cg_solve(L, nr, w, B, s, x, r, p, Ap, state, partials, host_state,
+                              max_chunk, ST(stream), &n);
+  COUNT(n);
+  return wrap(e, "gb3_cg_solve");
+}
+int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* y,
+                  double tol, void* state, double* partials, void* host_state, int max_chunk,
+                  void* stream) {
+  long long n = 0;
+  const int e = gbk3_pow_solve(L, nr, w, B, s, x, y, tol, state, partials, host_state,
+                               max_chunk, ST(stream), &n);
+  COUNT(n);
+  return wrap(e, "gb3_pow_solve");
 }
 
 }  // extern "C"

@@ -200,3 +200,45 @@ size_t gbk_quad_part_elems();
 int gbk_box_quadform(int L, int w, const double* box, const double* x, double* part, double* out,
                      cudaStream_t s);
 int gbk_max_abs(long long n, const double* x, double* part, double* out, cudaStream_t s);
+
+// gb_3d.cu (config 4, 3-D box stencils) and the 3-D operator of gb_krylov.cu
+int gbk3_csr_to_box(int L, int w, const int32_t* indptr, const int32_t* indices,
+                    const double* data, double* box, long long* status, cudaStream_t s);
+int gbk3_box_scale(long long rows, int nr, int w, const double* box, double* sv,
+                   long long* status, cudaStream_t s);
+int gbk3_box_sym_drop(int L, int nr, int w, const double* raw, double* out, double* dmin,
+                      double* stats, cudaStream_t s);
+size_t gbk3_mass_smem(int rho);
+int gbk3_mass_patches(int L, const double* M, const double* sv, int rho, int wd, double* psi,
+                      long long* status, cudaStream_t s);
+int gbk3_psi_galerkin(int L, int rho, int wd, const double* psi, const double* A, int wX,
+                      double* X, int wR, double* raw, cudaStream_t s);
+int gbk3_level_blocks(int Lk, int wA, const double* A, const double* host_w, int wB,
+                      double* Braw, double* G, double* PAPt, cudaStream_t s);
+int gbk3_correction_ld(int rho);
+size_t gbk3_correction_workspace(int Lp, int rho, int ctas);
+int gbk3_correction_patches(int Lp, int wB, const double* B, const double* sB, const double* G,
+                            int rho, double* Dt, long long* status, double* ws, int ctas,
+                            cudaStream_t s);
+int gbk3_restriction(int Lp, int rho, const double* Dt, const double* host_w, double* Rv,
+                     cudaStream_t s);
+int gbk3_triple(int Lp, int wB, const double* B, const double* G, const double* PAPt, int rho,
+                const double* Dt, int wBD, double* BD, int wGD, double* GtD, int wA2,
+                double* raw, cudaStream_t s);
+int gbk3_apply_w(int Lp, const double* host_w, const double* g, const double* sv, double* out,
+                 cudaStream_t s);
+int gbk3_apply_wt(int Lp, const double* host_w, const double* w, double* v, cudaStream_t s);
+int gbk3_apply_r(int Lp, int rho, const double* Rv, const double* g, double* out,
+                 cudaStream_t s);
+int gbk3_apply_rt(int Lp, int rho, const double* Rv, const double* u, double* out,
+                  cudaStream_t s);
+int gbk3_psi_t_apply(int L, int rho, int wd, const double* psi, const double* v, double* out,
+                     cudaStream_t s);
+int gbk3_apply(int L, int nr, int w, const double* B, const double* sv, const double* x,
+               double* y, cudaStream_t s);
+int gbk3_cg_solve(int L, int nr, int w, const double* B, const double* sv, double* x, double* r,
+                  double* p, double* Ap, void* st, double* part, void* host_state, int max_chunk,
+                  cudaStream_t s, long long* launches);
+int gbk3_pow_solve(int L, int nr, int w, const double* B, const double* sv, double* x,
+                   double* y, double tol, void* st, double* part, void* host_state,
+                   int max_chunk, cudaStream_t s, long long* launches);

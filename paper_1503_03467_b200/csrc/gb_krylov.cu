@@ -2179,7 +2179,12 @@ int gbk_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* c
                     double* const* r, double* const* p, double* const* Ap, double* const* z,
                     void* const* st, double* const* part, void* const* host_state,
                     int max_chunk, cudaStream_t s, long long* launches) {
-  if (!use_sym(1, L, 3, w)) return GB_UNSUPPORTED;
+  // bitwise equality with the single solve needs the same phase-1 kernel
+  // family for one and two vectors (the warp-specialized one; the dot
+  // partials of the register-pipelined fallback are formed in another order)
+  if (!use_sym(1, L, 3, w) || !GB_SYM_WS || symb_ws_smem(w, 1) > 226 * 1024 ||
+      symb_ws_smem(w, 2) > 226 * 1024)
+    return GB_UNSUPPORTED;
   const int Lpad = L + 2 * w;
   const long long npad = (long long)Lpad * Lpad * 3;
   const int gv = grid_for(npad, 256, kRedBlocks);
@@ -2279,6 +2284,140 @@ int gbk_csr_pow_solve(long long n, const int32_t* indptr, const int32_t* indices
   for (;;) {
     for (int i = 0; i < chunk; ++i) {
       k_csr_apply<<<csr_grid(n), 256, 0, s>>>(n, indptr, indices, data, x, y, k, part, 1);
+      k_pow_step<<<gv, 256, 0, s>>>(n, x, y, tol, k, part);
+      k_pow_scale<<<gv, 256, 0, s>>>(n, x, y, k);
+    }
+    *launches += 3LL * chunk;
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    e = read_state(st, h, s);
+    if (e) return e;
+    if (h->done) return 0;
+    chunk = chunk * 2 < max_chunk ? chunk * 2 : max_chunk;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3-D box operator (config 4): y = (S B S) x with the materialized
+// congruence's entry ((B_rc s_r) s_c) (gamblet_fast.py:123-139) on an L^3 grid
+// with nr components, half-width w; one warp per row, reductions as
+// k_csr_apply (mode 0: CG pAp/alpha, 1: power x.y, |y|, 2: none)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
+                                                   const double* __restrict__ B,
+                                                   const double* __restrict__ sv,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y, KState* st,
+                                                   double* part, int mode) {
+  __shared__ double sh[32];
+  if (mode != 2 && st->done) return;
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long rows = (long long)L * L * L * nr;
+  const int W3 = 2 * w + 1;
+  const int S = W3 * W3 * W3 * nr;
+  double xy = 0.0, yy = 0.0;
+  for (long long r = wid; r < rows; r += nwarps) {
+    const long long p = r / nr;
+    const int pz = (int)(p % L), py = (int)((p / L) % L), px = (int)(p / ((long long)L * L));
+    const double sr = sv[r];
+    const double* row = B + r * S;
+    double acc = 0.0;
+    for (int sl = lane; sl < S; sl += 32) {
+      const double bv = row[sl];
+      if (bv == 0.0) continue;
+      const int c = sl % nr;
+      int t = sl / nr;
+      const int dz = t % W3 - w;
+      t /= W3;
+      const int dy = t % W3 - w, dx = t / W3 - w;
+      const long long col = ((((long long)(px + dx) * L) + (py + dy)) * L + (pz + dz)) * nr + c;
+      acc += (bv * sr) * sv[col] * x[col];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      y[r] = acc;
+      xy += x[r] * acc;
+      yy += acc * acc;
+    }
+  }
+  if (mode == 2) return;
+  xy = block_sum(xy, sh);
+  yy = block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = xy;
+    part[2 * blockIdx.x + 1] = yy;
+  }
+  if (last_block(&st->counter)) {
+    double a, b;
+    final_sum2(part, gridDim.x, &a, &b, sh);
+    if (threadIdx.x == 0) {
+      st->counter = 0;
+      if (mode == 0) {
+        st->pAp = a;
+        if (!(a > 0.0)) {
+          st->breakdown = st->it + 1;
+          st->done = 1;
+        } else {
+          st->alpha = st->rs / a;
+        }
+      } else {
+        st->lam = a;
+        st->ynorm = sqrt(b);
+        if (st->ynorm == 0.0) {
+          st->lam = 0.0;
+          st->done = 1;
+        }
+      }
+    }
+  }
+}
+
+static inline int box3_grid(long long rows) { return grid_for(rows * 32, 256, kRedBlocks); }
+
+int gbk3_apply(int L, int nr, int w, const double* B, const double* sv, const double* x,
+               double* y, cudaStream_t s) {
+  const long long rows = (long long)L * L * L * nr;
+  k3_box_apply<<<box3_grid(rows), 256, 0, s>>>(L, nr, w, B, sv, x, y, nullptr, nullptr, 2);
+  return (int)cudaGetLastError();
+}
+
+int gbk3_cg_solve(int L, int nr, int w, const double* B, const double* sv, double* x, double* r,
+                  double* p, double* Ap, void* st, double* part, void* host_state, int max_chunk,
+                  cudaStream_t s, long long* launches) {
+  KState* h = (KState*)host_state;
+  KState* k = (KState*)st;
+  const long long n = (long long)L * L * L * nr;
+  const int gv = grid_for(n, 256, kRedBlocks);
+  int chunk = 8;
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      k3_box_apply<<<box3_grid(n), 256, 0, s>>>(L, nr, w, B, sv, p, Ap, k, part, 0);
+      k_cg_update<<<gv, 256, 0, s>>>(n, x, r, p, Ap, k, part);
+      k_cg_dir<<<gv, 256, 0, s>>>(n, r, p, k);
+    }
+    *launches += 3LL * chunk;
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    e = read_state(st, h, s);
+    if (e) return e;
+    if (h->done) return 0;
+    chunk = chunk * 2 < max_chunk ? chunk * 2 : max_chunk;
+  }
+}
+
+int gbk3_pow_solve(int L, int nr, int w, const double* B, const double* sv, double* x,
+                   double* y, double tol, void* st, double* part, void* host_state,
+                   int max_chunk, cudaStream_t s, long long* launches) {
+  KState* h = (KState*)host_state;
+  KState* k = (KState*)st;
+  const long long n = (long long)L * L * L * nr;
+  const int gv = grid_for(n, 256, kRedBlocks);
+  int chunk = 8;
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      k3_box_apply<<<box3_grid(n), 256, 0, s>>>(L, nr, w, B, sv, x, y, k, part, 1);
       k_pow_step<<<gv, 256, 0, s>>>(n, x, y, tol, k, part);
       k_pow_scale<<<gv, 256, 0, s>>>(n, x, y, k);
     }

@@ -1545,9 +1545,14 @@ def _solve_levels_batch(levels, gs, tree, schedule, tol, counter, records):
         op = prep[0][0]
         i = 0
         while i < len(svs):
+            res = None
             if i + 1 < len(svs) and op.layout == 1 and op.nr == 3:
-                with dv.phase("subband_cg2"):
-                    res = _pcg2(op, op.pad(prep[i][2]), op.pad(prep[i + 1][2]), tol)
+                try:
+                    with dv.phase("subband_cg2"):
+                        res = _pcg2(op, op.pad(prep[i][2]), op.pad(prep[i + 1][2]), tol)
+                except InvalidArgumentError:  # no bitwise-equal pair kernel at this w
+                    res = None
+            if res is not None:
                 its = max(r[1] for r in res)
                 dv.Prof.add_work("subband_cg2", nbytes=its * (op.matrix_bytes
                                                               + 2 * (3 * 8 * op.npad

@@ -164,13 +164,13 @@ def test_tree_and_schedule_guards():
 def test_library_exports_every_header_symbol():
     from paper_1503_03467_b200 import _native
     header = (ROOT / "include" / "gamblets_b200.h").read_text()
-    declared = set(re.findall(r"^(?:int|size_t|const char\*|unsigned long long)\s+(gb_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^(?:int|size_t|const char\*|unsigned long long)\s+(gb3?_\w+)\(", header, re.M))
     assert len(declared) > 40
     lib = ctypes.CDLL(str(_native.LIB_PATH))
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.EXPORTED)
-    assert lib.gb_abi_version() == 4
+    assert lib.gb_abi_version() == 5
 
 
 def _lanczos_ab(A, v0, m):
