@@ -37,12 +37,15 @@ CONFIGS = {
     "c1": dict(q=7, coeff="example1"),
     "c2": dict(q=10, coeff="checker"),
     "c3": dict(q=12, coeff="checker"),
+    "c4": dict(q=7, coeff="example3d", d=3),
 }
+RHO3 = 2
 EPS, RHO, CTOL = 1e-13, 3, 1e-6
 METRIC = "fine-DOF/s for gamblet setup+solve (fp64)"
 # CPU sample of configs 1-3: the oracle's complete tight-mode pipeline on a
 # 2^CPU_WINDOW_Q x 2^CPU_WINDOW_Q block of the config's own instance
 CPU_WINDOW_Q = 7
+CPU_WINDOW_Q3 = 3
 
 
 def instance_seeds(rank):
@@ -235,6 +238,14 @@ def workload_config(name, q, world):
         return {"workload": f"{name}: q={q}, N={N} fine DOFs, exact (global) gamblets, "
                             "tight mode tol 1e-14", "q": q, "fine_dofs": N,
                 "parallelism": "single GPU" if world == 1 else f"{world} replicas"}
+    if cfg.get("d") == 3:
+        N = 8 ** q
+        return {"workload": f"{name}: 3-D unit cube, q={q} ({1 << q}^3 = {N} fine DOFs), "
+                            f"Q1 trilinear 27-point, example coefficient, localized gamblets "
+                            f"rho={RHO3}, tight mode eps={EPS}",
+                "q": q, "d": 3, "fine_dofs": N, "rho": RHO3, "epsilon": EPS,
+                "parallelism": "single GPU" if world == 1 else f"{world} replicas",
+                "l2": "working set > 126 MB L2 (operators tens of GB), no flush needed"}
     return {"workload": f"{name}: q={q}, N={N} fine DOFs, {cfg['coeff']}, "
                         f"localized gamblets rho={RHO}, tight mode eps={EPS}",
             "q": q, "fine_dofs": N, "rho": RHO, "epsilon": EPS,
@@ -316,6 +327,116 @@ def run_exact(args, rank, world, local_rank):
                 "value is measured through the public call with host inputs",
         "clocks": clk.summary(), "step_ms": [round(t, 2) for t in ts],
     }
+
+
+def build_inputs_3d(q, rank=0):
+    from paper_1503_03467_b200 import gamblet_3d as g3
+    grid = g3.build_grid_3d(q)
+    _, sg = instance_seeds(rank)
+    c = g3.coefficient_example_3d(grid)
+    M = g3.assemble_mass_3d(grid)
+    A = g3.assemble_stiffness_3d(grid, c)
+    g = g3.gaussian_load_3d(grid, sg)
+    return grid, M, A, g
+
+
+def run_3d(args, rank, world, local_rank):
+    """BASELINE configs[4]: 3-D unit cube 128^3 (q = 7), Q1 trilinear,
+    example coefficient, Gaussian nodal load (seed 1), rho = 2, tight mode.
+    value: M, A as device boxes and g in HBM; e2e: fast_solve_3d with host
+    scipy CSR M, A and host g, uploads and the u download inside the step."""
+    import torch
+    from paper_1503_03467_b200 import _native as nat, device as dv, gamblet_3d as g3
+    torch.cuda.set_device(local_rank)
+    q = args.q or CONFIGS[args.config]["q"]
+    N = 8 ** q
+    grid, M, A, g = build_inputs_3d(q, rank)
+    Md, Ad = g3.box3_from_csr(M, 1 << q), g3.box3_from_csr(A, 1 << q)
+    gd = dv.to_dev(g)
+
+    def step():
+        return g3.fast_solve_3d(Md, Ad, gd, q, EPS, uniform_rho=RHO3)
+
+    for _ in range(args.warmup):
+        res = step()
+        res = None
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = nat.query("gb_launch_count")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            res = None
+            res = step()
+            torch.cuda.synchronize()
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = nat.query("gb_launch_count") - launches0
+    ms = reduce_max(ev0.elapsed_time(ev1) / args.steps, world, "cuda")
+    iters = dict(res.iterations)
+    res = None
+    e2e_ms = []
+    dv.Traffic.reset()
+    for _ in range(max(1, min(args.steps, 2))):
+        res = None
+        torch.cuda.synchronize()
+        dv.Traffic.reset()
+        t0 = time.perf_counter()
+        res = g3.fast_solve_3d(M, A, g, q, EPS, uniform_rho=RHO3)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d, d2h = dv.Traffic.h2d, dv.Traffic.d2h
+    e2e = reduce_max(float(np.median(e2e_ms)), world, "cuda")
+    if rank != 0:
+        return None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample_3d(q, os.cpu_count() or 1, 0)
+    return {
+        "metric": METRIC, "value": round(whole_job_rate(N, world, ms), 1), "unit": "fine-DOF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (3-D example coefficient of BASELINE configs[4], Gaussian nodal "
+                "load seed 1)",
+        "config": workload_config(args.config, q, world),
+        "e2e": {"value": round(whole_job_rate(N, world, e2e), 1), "unit": "fine-DOF/s",
+                "ms_per_step": round(e2e, 3), "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches), "roofline": None,
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+        "krylov_iterations": {str(k): v for k, v in iters.items()},
+    }
+
+
+def cpu_sample_3d(q, threads, index):
+    """The 3-D restatement (oracle/gamblets_oracle_nd.py, tight mode, rho=2)
+    on one 2^m-per-axis window of the config's own instance."""
+    from threadpoolctl import threadpool_limits
+    from oracle import gamblets_oracle_nd as ND
+    from paper_1503_03467_b200 import gamblet_3d as g3
+    m = min(q, CPU_WINDOW_Q3)
+    grid = g3.build_grid_3d(q)
+    c = g3.coefficient_example_3d(grid).reshape((grid.n + 1,) * 3)
+    g = g3.gaussian_load_3d(grid, 1).reshape((grid.n,) * 3)
+    w = 1 << m
+    nb = grid.n // w
+    bi, bj, bk = np.unravel_index(int(index) % (nb ** 3), (nb,) * 3)
+    gw = g3.build_grid_3d(m)
+    cw = c[bi * w:bi * w + w + 1, bj * w:bj * w + w + 1, bk * w:bk * w + w + 1].ravel().copy()
+    M = g3.assemble_mass_3d(gw)
+    A = g3.assemble_stiffness_3d(gw, cw)
+    gv = g[bi * w:(bi + 1) * w, bj * w:(bj + 1) * w, bk * w:(bk + 1) * w].ravel().copy()
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        ND.fast_solve(M, A, gv, m, 3, EPS, uniform_rho=RHO3)
+        dt = time.perf_counter() - t0
+    return {"value": round(8 ** m / dt, 2), "unit": "fine-DOF/s", "cores": threads,
+            "kind": "port",
+            "sample": f"oracle/gamblets_oracle_nd.fast_solve (d=3, tight mode, rho={RHO3}) on "
+                      f"window {(int(bi), int(bj), int(bk))} ({w}^3 nodes = {8 ** m} DOFs) of "
+                      f"this config's own q={q} instance, {dt:.1f} s"}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -603,6 +724,31 @@ def run_reference(args, rank, world):
     cfg = CONFIGS[args.config]
     q = args.q or cfg["q"]
     threads = os.cpu_count() or 1
+    if cfg.get("d") == 3:  # config 4: windows of the 3-D instance, 3-D restatement
+        times, wins = [], []
+        m = min(q, CPU_WINDOW_Q3)
+        for i in range(args.warmup + args.steps):
+            r = cpu_sample_3d(q, threads, i)
+            if i >= args.warmup:
+                times.append(8 ** m / r["value"])
+                wins.append(r["sample"])
+        dt = float(np.mean(times))
+        value = 8 ** m / dt
+        return {
+            "impl": "reference", "metric": METRIC, "value": round(value, 2),
+            "unit": "fine-DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same instance as the GPU arm)",
+            "config": workload_config(args.config, q, world),
+            "cpu_baseline": {"value": round(value, 2), "unit": "fine-DOF/s", "cores": threads,
+                             "kind": "port",
+                             "sample": f"oracle/gamblets_oracle_nd.fast_solve (d=3, the "
+                                       f"reference has no 3-D) on one {1 << m}^3-node window "
+                                       f"of the config's own q={q} instance per step"},
+            "e2e": {"value": round(value, 2), "unit": "fine-DOF/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
     if cfg.get("exact"):  # config 0: the whole q=5 exact sweep fits a CPU step
         grid, M, A, load, tree = build_inputs(q, cfg["coeff"])
         times = []
@@ -675,7 +821,8 @@ def main():
             import torch
             torch.cuda.set_device(local_rank)
             torch.distributed.init_process_group("nccl")
-        runner = run_exact if CONFIGS[args.config].get("exact") else run_ours
+        cfg = CONFIGS[args.config]
+        runner = run_exact if cfg.get("exact") else run_3d if cfg.get("d") == 3 else run_ours
         out = runner(args, rank, world, local_rank)
         if world > 1:
             import torch

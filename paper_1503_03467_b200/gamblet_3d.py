@@ -50,7 +50,8 @@ from .sparse_core import as_csr
 
 __all__ = ["Grid3D", "build_grid_3d", "coefficient_example_3d", "coefficient_checkerboard_3d",
            "gaussian_load_3d", "assemble_mass_3d", "assemble_stiffness_3d",
-           "assemble_load_3d", "w_template_3d", "fast_solve_3d", "Level3D", "FastResult3D"]
+           "assemble_load_3d", "w_template_3d", "fast_solve_3d", "Level3D", "FastResult3D",
+           "box3_from_csr"]
 
 D = 3
 NCH = 8        # children per aggregate
@@ -421,7 +422,17 @@ def _sym_drop(L, nr, w, raw, what):
     return out, rep
 
 
+def box3_from_csr(mat, L, w=1):
+    """Upload a canonical 27-point CSR on the L^3 grid into the 3-D box
+    layout (a device tensor, reusable as fast_solve_3d input)."""
+    return _csr3_to_box(mat, L, w)
+
+
 def _csr3_to_box(mat, L, w=1):
+    if isinstance(mat, torch.Tensor):  # already a device box
+        if mat.numel() != L ** 3 * slots3(w, 1):
+            raise InvalidArgumentError("device box input has the wrong size")
+        return mat
     mat = as_csr(mat)
     box = dv.empty(L ** 3 * slots3(w, 1))
     st = dv.zeros(2, torch.int64)
@@ -526,8 +537,11 @@ def _correction_ctas(Lp, rho):
 
 def fast_transform_3d(M, A, q, radii):
     """Levels q..1 (dict k -> Level3D) and the Krylov operators of k >= 2."""
-    if M.shape != (8 ** q, 8 ** q) or A.shape != M.shape:
-        raise InvalidArgumentError(f"M, A must be {8 ** q} x {8 ** q} for q={q} in 3-D")
+    for X in (M, A):
+        ok = (X.numel() == 8 ** q * 27) if isinstance(X, torch.Tensor) else \
+            (X.shape == (8 ** q, 8 ** q))
+        if not ok:
+            raise InvalidArgumentError(f"M, A must be {8 ** q} x {8 ** q} for q={q} in 3-D")
     W = w_template_3d()
     levels = {q: Level3D(q, q)}
     psi, Aq, wR, rep = _level_q(M, A, q, radii[q - 1])

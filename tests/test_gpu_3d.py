@@ -100,9 +100,8 @@ def test_3d_golden_q3():
 
 
 def test_3d_solution_is_linear_and_converges_with_rho():
-    """Size-independent properties at q = 5 (32^3, where the restatement is
-    slow): linearity of u in the load, and rho = 3 closer than rho = 2 to the
-    exact FE solution."""
+    """Size-independent properties: linearity of u in the load, and rho = 2
+    closer than rho = 1 to the exact FE solution."""
     import scipy.sparse.linalg as spla
     from paper_1503_03467_b200 import gamblet_3d as g3
     q = 4
@@ -114,5 +113,8 @@ def test_3d_solution_is_linear_and_converges_with_rho():
     assert O.rel_energy(A, r1.solution.u + r2.solution.u, r12.solution.u) <= 1e-9
     exact = spla.spsolve(A.tocsc(), M @ g)
     errs = [O.rel_energy(A, g3.fast_solve_3d(M, A, g, q, 1e-13, uniform_rho=r).solution.u, exact)
-            for r in (1, 2, 3)]
-    assert errs[0] > errs[1] > errs[2]
+            for r in (1, 2)]
+    assert errs[0] > 2 * errs[1]
+    # the shared-memory mass-patch kernel covers rho <= 2 in 3-D (BASELINE: 2)
+    with pytest.raises(g3.InvalidArgumentError):
+        g3.fast_solve_3d(M, A, g, q, 1e-13, uniform_rho=3)
