@@ -179,7 +179,9 @@ int gb_wpsi(int n, int Lk, int lo, int wd, const double* host_w12, const double*
 int gb_products_mode(int mma);
 /* launch tuning (tests and tools only): what = 0 -> total CTAs of the v2
  * correction-patch grid (0 = auto); 1 -> correction kernel (1 = v3, default;
- * 0 = v2); 2 -> mass patches (0 = banded, default; 1 = dense tiled).  value
+ * 0 = v2); 2 -> mass patches (0 = banded, default; 1 = dense tiled); 3 -> CTA cap
+ * of the persistent symmetric-band SpMV pass (0 = one per SM); 4 -> mass patches by
+ * clip type when M is translation invariant (1, default; 0 = every patch).  value
  * < 0 queries.  Returns the previous value (-1: unknown key). */
 int gb_tune(int what, int value);
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,

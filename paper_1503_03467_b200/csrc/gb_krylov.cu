@@ -1821,6 +1821,7 @@ static inline bool use_sym(int layout, int L, int nr, int w) {
 #ifndef GB_SYM_WS
 #define GB_SYM_WS 1  // warp-specialized bulk-copy phase 1 (0: register-pipelined)
 #endif
+int g_sym_ws_ctas = 0;  // gb_tune(3): CTA cap of the warp-specialized phase 1 (0: 148)
 static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, double* y0,
                        KState* s0, double* p0, int r0, const double* x1, double* y1,
                        KState* s1, double* p1, int r1, cudaStream_t s) {
@@ -1830,7 +1831,10 @@ static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, 
   static size_t attr[2][3] = {{0, 0, 0}, {0, 0, 0}};
   const bool ws = GB_SYM_WS && symb_ws_smem(w, nv) <= 226 * 1024;
   if (ws) {
-    const int gp = nt < 148 ? nt : 148;  // persistent: one CTA per SM
+    // persistent: one CTA per SM, at most g_sym_ws_ctas (the HBM stream
+    // saturates on fewer SMs; the rest stay free for the concurrent setup)
+    const int cap = g_sym_ws_ctas > 0 && g_sym_ws_ctas < 148 ? g_sym_ws_ctas : 148;
+    const int gp = nt < cap ? nt : cap;
     const size_t sm = symb_ws_smem(w, nv);
     if (sm > attr[1][nv]) {
       if (nv == 2)

@@ -503,9 +503,26 @@ __global__ void __launch_bounds__(128) k_mass_patches_v2(
 // ---------------------------------------------------------------------------
 constexpr int kBandMaxM = 49, kBandMaxB = 8, kBandW = kBandMaxB + 1, kBandWarps = 4;
 
+// type representative of a fine coordinate: rows whose ball is unclipped
+// share the patch of coordinate rho (at most (2 rho + 1)^2
+// distinct S M S patches when M is translation invariant)
+__host__ __device__ __forceinline__ int mass_type_rep(int c, int n, int rho) {
+  return (c < rho || c > n - 1 - rho) ? c : rho;
+}
+// rep list entry l of the (2 rho + 1)^2 representatives: coordinates
+// 0..rho (rho = the interior type) then n - rho .. n - 1 per axis
+__device__ __forceinline__ int mass_rep_coord(int l, int n, int rho) {
+  return l <= rho ? l : n - (2 * rho + 1) + l;
+}
+
 __global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
     int n, const double* __restrict__ M, const double* __restrict__ s, int rho, int wd,
-    double* __restrict__ psi, long long* status, long long p0, long long p1) {
+    double* __restrict__ psi, long long* status, long long p0, long long p1,
+    const int* __restrict__ flag = nullptr, int mode = 0) {
+  // mode 0: patches [p0, p1); 1: the type representatives only (index l in
+  // [p0, p1) of the rep list); 2: [p0, p1) only when *flag != 0 (M is not
+  // translation invariant, the representatives cannot stand in)
+  if (mode == 2 && *flag == 0) return;
   __shared__ double sLb[kBandWarps][kBandMaxM * kBandW];
   __shared__ double sSl[kBandWarps][kBandMaxM];
   __shared__ double sX[kBandWarps][kBandMaxM];
@@ -532,7 +549,11 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
   }
   // patches [p0, p1) (node order; a row strip of the fine grid)
   const long long nwarps = (long long)gridDim.x * kBandWarps;
-  for (long long i = p0 + (long long)blockIdx.x * kBandWarps + wi; i < p1; i += nwarps) {
+  const int R = 2 * rho + 1;
+  for (long long ii = p0 + (long long)blockIdx.x * kBandWarps + wi; ii < p1; ii += nwarps) {
+    const long long i = mode == 1 ? (long long)mass_rep_coord((int)(ii / R), n, rho) * n +
+                                        mass_rep_coord((int)(ii % R), n, rho)
+                                  : ii;
     const int si = (int)(i / n), ti = (int)(i % n);
     const int s0 = imax(0, si - rho), s1 = imin(n - 1, si + rho);
     const int t0 = imax(0, ti - rho), t1 = imin(n - 1, ti + rho);
@@ -623,6 +644,40 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_mass_patches_band(
     __syncwarp();
   }
 }
+// M translation invariant (every in-domain box entry of every row equals the
+// interior representative's, bit for bit) -> *flag stays 0
+__global__ void k_mass_invariance(int n, const double* __restrict__ M, int* flag) {
+  const long long N = (long long)n * n;
+  const long long c = (long long)(n / 2) * n + n / 2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int si = (int)(i / n), ti = (int)(i % n);
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+      const int ds = d / 3 - 1, dt = d % 3 - 1;
+      const bool in = si + ds >= 0 && si + ds < n && ti + dt >= 0 && ti + dt < n;
+      if (in && __double_as_longlong(M[i * 9 + d]) != __double_as_longlong(M[c * 9 + d]))
+        bad = true;
+    }
+    if (bad) atomicOr(flag, 1);
+  }
+}
+
+// psi row i = psi row of its type representative (window content identical)
+__global__ void k_mass_broadcast(int n, int rho, int wd, double* __restrict__ psi,
+                                 const int* __restrict__ flag) {
+  if (*flag != 0) return;
+  const long long W2 = (long long)wd * wd;
+  const long long total = (long long)n * n * W2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / W2;
+    const int si = (int)(i / n), ti = (int)(i % n);
+    const long long r = (long long)mass_type_rep(si, n, rho) * n + mass_type_rep(ti, n, rho);
+    if (r != i) psi[e] = psi[r * W2 + (e - i * W2)];
+  }
+}
 }  // namespace gb
 
 #include "gb_patch_l2.cuh"
@@ -697,9 +752,15 @@ int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB,
 static int g_patch_grid = 0;
 static int g_patch_v3 = 1;
 static int g_mass_dense = 0;
+static int g_mass_types = 1;
 int gbk_tune(int what, int value) {
-  int* slot = what == 0 ? &g_patch_grid : what == 1 ? &g_patch_v3 : what == 2 ? &g_mass_dense
-                                                                                : nullptr;
+  extern int g_sym_ws_ctas;
+  int* slot = what == 0   ? &g_patch_grid
+              : what == 1 ? &g_patch_v3
+              : what == 2 ? &g_mass_dense
+              : what == 3 ? &g_sym_ws_ctas
+              : what == 4 ? &g_mass_types
+                          : nullptr;
   if (!slot) return -1;
   const int old = *slot;
   if (value >= 0) *slot = value;
@@ -777,6 +838,31 @@ int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int r
   if (r0 == r1) return 0;
   const int nmax = (2 * rho + 1) * (2 * rho + 1);
   const int Tmax = (nmax + 7) / 8;
+  if (wM == 1 && rho <= 3 && !g_mass_dense && r0 == 0 && r1 == n && n >= 2 * rho + 2 &&
+      g_mass_types) {
+    // whole level: factor the (2 rho + 1)^2 type representatives, broadcast
+    // their rows; the general pass runs only if M is not translation invariant
+    int* d_flag = nullptr;  // stream-ordered, so concurrent transforms never share it
+    cudaError_t e = cudaMallocAsync((void**)&d_flag, sizeof(int), st);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return (int)e;
+    const long long N = (long long)n * n;
+    k_mass_invariance<<<(int)((N + 255) / 256 < 148 * 8 ? (N + 255) / 256 : 148 * 8), 256, 0,
+                        st>>>(n, M, d_flag);
+    const int R = 2 * rho + 1;
+    k_mass_patches_band<<<(R * R + kBandWarps - 1) / kBandWarps, 32 * kBandWarps, 0, st>>>(
+        n, M, s, rho, wd, psi, status, 0, (long long)R * R, d_flag, 1);
+    k_mass_broadcast<<<148 * 16, 256, 0, st>>>(n, rho, wd, psi, d_flag);
+    const long long warps = 148LL * 16 * 4;
+    const long long g = (N + kBandWarps - 1) / kBandWarps;
+    k_mass_patches_band<<<(int)(g < warps / kBandWarps ? g : warps / kBandWarps),
+                          32 * kBandWarps, 0, st>>>(n, M, s, rho, wd, psi, status, 0, N,
+                                                    d_flag, 2);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaFreeAsync(d_flag, st);
+  }
   if (wM == 1 && rho <= 3 && !g_mass_dense) {  // banded warp solver (rho = 3: b <= 8)
     const long long warps = 148LL * 16 * 4;
     const long long np = (long long)(r1 - r0) * n;
