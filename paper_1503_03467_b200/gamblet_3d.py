@@ -459,7 +459,9 @@ def _level_q(M, A, q, rho):
     rho = int(min(rho, L - 1))
     wd = min(2 * rho + 1, L)
     psi = dv.empty(N * wd ** 3)
-    nat.call("gb3_mass_patches", L, dv.ptr(Mb), dv.ptr(sM), rho, wd, dv.ptr(psi), dv.ptr(st), s)
+    with dv.phase("3d_mass_patches"):
+        nat.call("gb3_mass_patches", L, dv.ptr(Mb), dv.ptr(sM), rho, wd, dv.ptr(psi),
+                 dv.ptr(st), s)
     _check(st, "mass patches")
     del Mb
     Ab = _csr3_to_box(A, L)
@@ -467,8 +469,9 @@ def _level_q(M, A, q, rho):
     wR = min(2 * rho + 1, L - 1)
     X = dv.empty(N * slots3(wX, 1))
     raw = dv.empty(N * slots3(wR, 1))
-    nat.call("gb3_psi_galerkin", L, rho, wd, dv.ptr(psi), dv.ptr(Ab), wX, dv.ptr(X), wR,
-             dv.ptr(raw), s)
+    with dv.phase("3d_psi_A_psiT"):
+        nat.call("gb3_psi_galerkin", L, rho, wd, dv.ptr(psi), dv.ptr(Ab), wX, dv.ptr(X), wR,
+                 dv.ptr(raw), s)
     del X, Ab
     Aq, rep = _sym_drop(L, 1, wR, raw, "A^(q),loc")
     return (psi, rho, wd), Aq, wR, rep
@@ -488,9 +491,10 @@ def _level_step(lv, nxt, rho, W, ctas):
     Braw = dv.empty(J * slots3(wB, NSUB))
     G = dv.empty(J * slots3(wB, 1))
     PAPt = dv.empty(P * slots3(wB, 1))
-    nat.call("gb3_level_blocks", Lk, wA, dv.ptr(lv._A), w8, wB, dv.ptr(Braw), dv.ptr(G),
-             dv.ptr(PAPt), s)
-    B, rep_b = _sym_drop(Lp, NSUB, wB, Braw, f"B^({k}),loc")
+    with dv.phase("3d_level_blocks"):
+        nat.call("gb3_level_blocks", Lk, wA, dv.ptr(lv._A), w8, wB, dv.ptr(Braw), dv.ptr(G),
+                 dv.ptr(PAPt), s)
+        B, rep_b = _sym_drop(Lp, NSUB, wB, Braw, f"B^({k}),loc")
     del Braw
     sB = dv.empty(J)
     st = dv.zeros(2, torch.int64)
@@ -499,14 +503,16 @@ def _level_step(lv, nxt, rho, W, ctas):
     lv._B, lv.wB, lv.subband_scale_dev = B, wB, sB
     lv.symmetry_repair = max(lv.symmetry_repair, rep_b)
     op = _Op3(B, Lp, NSUB, wB, sB)
-    lv.lambda_min_subband, lv.lambda_max_subband = op.eig_extremes(tol=0.1)
+    with dv.phase("3d_spectral"):
+        lv.lambda_min_subband, lv.lambda_max_subband = op.eig_extremes(tol=0.1)
     # correction patches -> D^T (row-tail trim fused)
     R3 = (2 * rho + 1) ** 3
     Dt = dv.empty(P * R3 * NSUB)
     nb = nat.query("gb3_correction_workspace", Lp, rho, ctas)
     ws = dv.empty(nb // 8)
-    nat.call("gb3_correction_patches", Lp, wB, dv.ptr(B), dv.ptr(sB), dv.ptr(G), rho,
-             dv.ptr(Dt), dv.ptr(st), dv.ptr(ws), ctas, s)
+    with dv.phase("3d_correction_patches"):
+        nat.call("gb3_correction_patches", Lp, wB, dv.ptr(B), dv.ptr(sB), dv.ptr(G), rho,
+                 dv.ptr(Dt), dv.ptr(st), dv.ptr(ws), ctas, s)
     _check(st, f"correction patches, level {k}")
     del ws
     Rv = dv.empty(P * R3 * NCH)
@@ -519,10 +525,11 @@ def _level_step(lv, nxt, rho, W, ctas):
     BD = dv.empty(J * slots3(wBD, 1))
     GtD = dv.empty(P * slots3(wGD, 1))
     raw = dv.empty(P * slots3(wA2, 1))
-    nat.call("gb3_triple", Lp, wB, dv.ptr(B), dv.ptr(G), dv.ptr(PAPt), rho, dv.ptr(Dt), wBD,
-             dv.ptr(BD), wGD, dv.ptr(GtD), wA2, dv.ptr(raw), s)
-    del BD, GtD, G, PAPt
-    An, rep_a = _sym_drop(Lp, 1, wA2, raw, f"A^({k - 1}),loc")
+    with dv.phase("3d_triple_product"):
+        nat.call("gb3_triple", Lp, wB, dv.ptr(B), dv.ptr(G), dv.ptr(PAPt), rho, dv.ptr(Dt),
+                 wBD, dv.ptr(BD), wGD, dv.ptr(GtD), wA2, dv.ptr(raw), s)
+        del BD, GtD, G, PAPt
+        An, rep_a = _sym_drop(Lp, 1, wA2, raw, f"A^({k - 1}),loc")
     nxt._A, nxt.wA = An, wA2
     nxt.symmetry_repair = rep_a
     return op
@@ -580,7 +587,8 @@ def solve_with_transform_3d(levels, ops, g_nodal, q, tol):
         Lp = 1 << (k - 1)
         rhs = dv.empty(op.n)
         nat.call("gb3_apply_w", Lp, w8, dv.ptr(g), dv.ptr(lv.subband_scale_dev), dv.ptr(rhs), s)
-        z, its, conv, brk = op.cg(rhs, tol)
+        with dv.phase("3d_subband_cg"):
+            z, its, conv, brk = op.cg(rhs, tol)
         if brk:
             raise NumericalError(f"CG breakdown at iteration {brk}: p^T A p <= 0")
         if not conv:
