@@ -177,9 +177,19 @@ __global__ void k3_box_sym_drop(int L, int nr, int w, const double* __restrict__
 // ---------------------------------------------------------------------------
 constexpr int k3MassThreads = 128;
 
+__device__ __forceinline__ int type_rep3(int c, int L, int rho) {
+  return (c < rho || c > L - 1 - rho) ? c : rho;
+}
+__device__ __forceinline__ int rep_coord3(int l, int L, int rho) {
+  return l <= rho ? l : L - (2 * rho + 1) + l;
+}
+
+// mode 0: every fine node; 1: the (2 rho + 1)^3 clip-type representatives;
+// 2: every node, only when *flag != 0 (M not translation invariant)
 __global__ void __launch_bounds__(k3MassThreads) k3_mass_patches(
     int L, const double* __restrict__ M, const double* __restrict__ s, int rho, int wd,
-    double* __restrict__ psi, long long* status) {
+    double* __restrict__ psi, long long* status, int mode, const int* __restrict__ flag) {
+  if (mode == 2 && *flag == 0) return;
   extern __shared__ double sm[];
   const int R = 2 * rho + 1;
   const int mmax = R * R * R;
@@ -189,9 +199,17 @@ __global__ void __launch_bounds__(k3MassThreads) k3_mass_patches(
   const int tid = threadIdx.x;
   const long long N = (long long)L * L * L;
   const long long SM = slots3(1, 1);
-  for (long long i = blockIdx.x; i < N; i += gridDim.x) {
+  const long long cnt = mode == 1 ? (long long)R * R * R : N;
+  for (long long ii = blockIdx.x; ii < cnt; ii += gridDim.x) {
     int x, y, z;
-    unflat3(i, L, &x, &y, &z);
+    if (mode == 1) {
+      x = rep_coord3((int)(ii / (R * R)), L, rho);
+      y = rep_coord3((int)((ii / R) % R), L, rho);
+      z = rep_coord3((int)(ii % R), L, rho);
+    } else {
+      unflat3(ii, L, &x, &y, &z);
+    }
+    const long long i = flat3(x, y, z, L);
     if (tid == 0) {
       bx0 = imax(x - rho, 0);
       by0 = imax(y - rho, 0);
@@ -284,6 +302,43 @@ __global__ void __launch_bounds__(k3MassThreads) k3_mass_patches(
       row[e] = val;
     }
     __syncthreads();
+  }
+}
+
+// M translation invariant: every in-domain stencil entry of every row equals
+// the interior representative's, bit for bit (else *flag = 1)
+__global__ void k3_mass_invariance(int L, const double* __restrict__ M, int* flag) {
+  const long long N = (long long)L * L * L;
+  const long long c = flat3(L / 2, L / 2, L / 2, L);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x, y, z;
+    unflat3(i, L, &x, &y, &z);
+    bool bad = false;
+    for (int d = 0; d < 27; ++d) {
+      const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+      if (inside3(x + dx, y + dy, z + dz, L) &&
+          __double_as_longlong(M[i * 27 + d]) != __double_as_longlong(M[c * 27 + d]))
+        bad = true;
+    }
+    if (bad) atomicOr(flag, 1);
+  }
+}
+
+// psi row i = the row of its clip-type representative (same window content)
+__global__ void k3_mass_broadcast(int L, int rho, int wd, double* __restrict__ psi,
+                                  const int* __restrict__ flag) {
+  if (*flag != 0) return;
+  const long long W3w = (long long)wd * wd * wd;
+  const long long total = (long long)L * L * L * W3w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / W3w;
+    int x, y, z;
+    unflat3(i, L, &x, &y, &z);
+    const long long r =
+        flat3(type_rep3(x, L, rho), type_rep3(y, L, rho), type_rep3(z, L, rho), L);
+    if (r != i) psi[e] = psi[r * W3w + (e - i * W3w)];
   }
 }
 
@@ -448,7 +503,8 @@ __global__ void k3_level_blocks(int Lk, int wA, const double* __restrict__ A, W7
 // carried through the panels, back substitution, D^T row i = s z with the
 // 1e-11 row-tail trim.  One launch per level, CTAs stride over the parents.
 // ---------------------------------------------------------------------------
-constexpr int k3PB = 32;  // panel width
+constexpr int k3PB = 64;    // panel width
+constexpr int k3TLD = 68;   // leading dimension of the staged operand blocks (4 mod 16)
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile(
@@ -461,8 +517,11 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB,
     const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status,
     double* __restrict__ ws, int ld) {
-  __shared__ double D11[k3PB][k3PB + 1];
-  __shared__ double y1[k3PB];
+  extern __shared__ double dsm3[];
+  double (*D11)[k3PB + 1] = reinterpret_cast<double (*)[k3PB + 1]>(dsm3);  // 64 x 65
+  double* y1 = dsm3 + k3PB * (k3PB + 1);                                 // 64
+  double* As = y1 + k3PB;                                                // 64 x k3TLD
+  double* Bs = As + k3PB * k3TLD;                                        // 64 x k3TLD
   __shared__ int bx0, by0, bz0, nx, ny, nz, bad;
   __shared__ double sh[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -518,7 +577,7 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
     __syncthreads();
     for (int j0 = 0; j0 < m; j0 += k3PB) {
       const int jb = imin(k3PB, m - j0);
-      // (a) diagonal block: factor in shared memory, carry the rhs
+      // (a) diagonal block: factor in shared memory (warp 0), carry the rhs
       for (int e = tid; e < jb * jb; e += blockDim.x) {
         const int a = e / jb, b = e - a * jb;
         D11[a][b] = b <= a ? K[(long long)(j0 + a) * ld + j0 + b] : 0.0;
@@ -535,12 +594,13 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
           __syncwarp();
           for (int a = j + 1 + lane; a < jb; a += 32) D11[a][j] /= d;
           __syncwarp();
-          for (int a = j + 1 + lane; a < jb; a += 32)
-            for (int b = j + 1; b <= a; ++b) D11[a][b] -= D11[a][j] * D11[b][j];
+          for (int a = j + 1 + lane; a < jb; a += 32) {
+            const double laj = D11[a][j];
+            for (int b = j + 1; b <= a; ++b) D11[a][b] -= laj * D11[b][j];
+          }
           __syncwarp();
         }
-        // y1 = L11^-1 v1
-        for (int j = 0; j < jb; ++j) {
+        for (int j = 0; j < jb; ++j) {  // y1 = L11^-1 v1
           if (lane == 0) y1[j] /= D11[j][j];
           __syncwarp();
           for (int a = j + 1 + lane; a < jb; a += 32) y1[a] -= D11[a][j] * y1[j];
@@ -554,51 +614,88 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
         if (b <= a) K[(long long)(j0 + a) * ld + j0 + b] = D11[a][b];
       }
       if (tid < jb) v[j0 + tid] = y1[tid];
-      // (b) panel rows below: x L11^T = a (warp per row), rhs update
+      // (b) panel rows below: x L11^T = a (warp per row, 2 columns per lane),
+      // then v[r] -= L21[r, :] y1
       const int r0 = j0 + jb;
       for (int r = r0 + warp; r < m; r += 8) {
         double* ar = K + (long long)r * ld + j0;
-        double a = lane < jb ? ar[lane] : 0.0;
+        double a0 = lane < jb ? ar[lane] : 0.0;
+        double a1 = lane + 32 < jb ? ar[lane + 32] : 0.0;
         for (int c = 0; c < jb; ++c) {
-          const double xc = __shfl_sync(0xffffffffu, a, c) / D11[c][c];
-          if (lane == c) a = xc;
-          if (lane > c && lane < jb) a -= xc * D11[lane][c];
+          const double src = __shfl_sync(0xffffffffu, c < 32 ? a0 : a1, c & 31);
+          const double xc = src / D11[c][c];
+          if (c < 32) {
+            if (lane == c) a0 = xc;
+            if (lane > c && lane < jb) a0 -= xc * D11[lane][c];
+            if (lane + 32 < jb) a1 -= xc * D11[lane + 32][c];
+          } else {
+            if (lane + 32 == c) a1 = xc;
+            if (lane + 32 > c && lane + 32 < jb) a1 -= xc * D11[lane + 32][c];
+          }
         }
-        if (lane < jb) ar[lane] = a;
-        double t = lane < jb ? a * y1[lane] : 0.0;
+        if (lane < jb) ar[lane] = a0;
+        if (lane + 32 < jb) ar[lane + 32] = a1;
+        double t = (lane < jb ? a0 * y1[lane] : 0.0) + (lane + 32 < jb ? a1 * y1[lane + 32] : 0.0);
         t = warp_sum(t);
         if (lane == 0) v[r] -= t;
       }
       __syncthreads();
-      // (c) trailing update K22 -= L21 L21^T on 8x8 tiles (lower), DMMA
-      const int nt = (m - r0 + 7) / 8;
-      const long long ntiles = (long long)nt * (nt + 1) / 2;
-      const int fr = lane >> 2, fk = lane & 3;
-      for (long long tt = warp; tt < ntiles; tt += 8) {
-        int ti = (int)((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
-        while ((long long)ti * (ti + 1) / 2 > tt) --ti;
-        while ((long long)(ti + 1) * (ti + 2) / 2 <= tt) ++ti;
-        const int tj = (int)(tt - (long long)ti * (ti + 1) / 2);
-        const int rr = r0 + ti * 8 + fr;  // A row of this lane
-        const int cc = r0 + tj * 8 + fr;  // B column of this lane
-        double c0 = 0.0, c1 = 0.0;
-        const int ccol = r0 + tj * 8 + 2 * fk;
-        if (rr < m) {
-          if (ccol < m) c0 = K[(long long)rr * ld + ccol];
-          if (ccol + 1 < m) c1 = K[(long long)rr * ld + ccol + 1];
+      // (c) trailing update K22 -= L21 L21^T (lower), 64 x 64 output blocks:
+      // the two L21 row blocks staged k-major in shared memory, warp (wm, wn)
+      // of a 2 x 4 grid owns 32 x 16 = 4 x 2 DMMA m8n8k4 accumulators
+      const int nbk = (m - r0 + 63) / 64;
+      const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fk = lane & 3;
+      for (int bi = 0; bi < nbk; ++bi) {
+        const int ib = r0 + bi * 64;
+        for (int e = tid; e < 64 * k3PB; e += blockDim.x) {  // A rows block
+          const int rr = e / k3PB, kk = e - rr * k3PB;
+          As[kk * k3TLD + rr] =
+              (ib + rr < m && kk < jb) ? K[(long long)(ib + rr) * ld + j0 + kk] : 0.0;
         }
-        for (int k4 = 0; k4 < jb; k4 += 4) {
-          const int kk = j0 + k4 + fk;
-          const double av = (rr < m && k4 + fk < jb) ? -K[(long long)rr * ld + kk] : 0.0;
-          const double bv = (cc < m && k4 + fk < jb) ? K[(long long)cc * ld + kk] : 0.0;
-          dmma_884(c0, c1, av, bv);
+        for (int bj = 0; bj <= bi; ++bj) {
+          const int jbase = r0 + bj * 64;
+          __syncthreads();
+          if (bj == bi) {
+            for (int e = tid; e < 64 * k3TLD; e += blockDim.x) Bs[e] = As[e];
+          } else {
+            for (int e = tid; e < 64 * k3PB; e += blockDim.x) {
+              const int rr = e / k3PB, kk = e - rr * k3PB;
+              Bs[kk * k3TLD + rr] =
+                  (jbase + rr < m && kk < jb) ? K[(long long)(jbase + rr) * ld + j0 + kk] : 0.0;
+            }
+          }
+          __syncthreads();
+          double acc[4][2][2];
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) acc[ii][jj][0] = acc[ii][jj][1] = 0.0;
+          for (int k4 = 0; k4 < jb; k4 += 4) {
+            double af[4], bf[2];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) af[ii] = As[(k4 + fk) * k3TLD + wm * 32 + ii * 8 + fr];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) bf[jj] = Bs[(k4 + fk) * k3TLD + wn * 16 + jj * 8 + fr];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj) dmma_884(acc[ii][jj][0], acc[ii][jj][1], af[ii], bf[jj]);
+          }
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int gr = ib + wm * 32 + ii * 8 + fr;
+            if (gr >= m) continue;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const int gc = jbase + wn * 16 + jj * 8 + 2 * fk + e2;
+                if (gc < m && gc <= gr) K[(long long)gr * ld + gc] -= acc[ii][jj][e2];
+              }
+          }
         }
-        if (rr < m) {
-          if (ccol < m && ccol <= rr) K[(long long)rr * ld + ccol] = c0;
-          if (ccol + 1 < m && ccol + 1 <= rr) K[(long long)rr * ld + ccol + 1] = c1;
-        }
+        __syncthreads();
       }
-      __syncthreads();
     }
     if (bad) {
       if (tid == 0) raise_status(status, ST_NOT_SPD, i);
@@ -959,8 +1056,26 @@ int gbk3_mass_patches(int L, const double* M, const double* sv, int rho, int wd,
   if (e != cudaSuccess) return (int)e;
   const long long N = (long long)L * L * L;
   const int g = (int)(N < 148LL * 8 ? N : 148LL * 8);
-  k3_mass_patches<<<g, k3MassThreads, smem, s>>>(L, M, sv, rho, wd, psi, status);
-  return (int)cudaGetLastError();
+  if (L < 2 * rho + 2) {  // no interior type: every patch
+    k3_mass_patches<<<g, k3MassThreads, smem, s>>>(L, M, sv, rho, wd, psi, status, 0, nullptr);
+    return (int)cudaGetLastError();
+  }
+  // the (2 rho + 1)^3 clip types when M is translation invariant (checked
+  // on the device), else every patch; the flag is stream-ordered
+  int* flag = nullptr;
+  e = cudaMallocAsync((void**)&flag, sizeof(int), s);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaMemsetAsync(flag, 0, sizeof(int), s);
+  if (e != cudaSuccess) return (int)e;
+  k3_mass_invariance<<<grid3(N, 256), 256, 0, s>>>(L, M, flag);
+  const int R = 2 * rho + 1;
+  k3_mass_patches<<<R * R * R, k3MassThreads, smem, s>>>(L, M, sv, rho, wd, psi, status, 1,
+                                                        flag);
+  k3_mass_broadcast<<<grid3(N * wd * wd * wd, 256), 256, 0, s>>>(L, rho, wd, psi, flag);
+  k3_mass_patches<<<g, k3MassThreads, smem, s>>>(L, M, sv, rho, wd, psi, status, 2, flag);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaFreeAsync(flag, s);
 }
 int gbk3_psi_galerkin(int L, int rho, int wd, const double* psi, const double* A, int wX,
                       double* X, int wR, double* raw, cudaStream_t s) {
@@ -989,8 +1104,12 @@ int gbk3_correction_patches(int Lp, int wB, const double* B, const double* sB, c
                             cudaStream_t s) {
   const long long P = (long long)Lp * Lp * Lp;
   const int g = (int)(P < ctas ? P : ctas);
-  k3_correction_patches<<<g, 256, 0, s>>>(Lp, wB, B, sB, G, rho, Dt, status, ws,
-                                          gbk3_correction_ld(rho));
+  const size_t smem = ((size_t)k3PB * (k3PB + 1) + k3PB + 2 * (size_t)k3PB * k3TLD) * 8;
+  cudaError_t e = cudaFuncSetAttribute(k3_correction_patches,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  k3_correction_patches<<<g, 256, smem, s>>>(Lp, wB, B, sB, G, rho, Dt, status, ws,
+                                             gbk3_correction_ld(rho));
   return (int)cudaGetLastError();
 }
 int gbk3_restriction(int Lp, int rho, const double* Dt, const double* host_w, double* Rv,

@@ -2328,16 +2328,15 @@ __global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
     const double sr = sv[r];
     const double* row = B + r * S;
     double acc = 0.0;
-    for (int sl = lane; sl < S; sl += 32) {
-      const double bv = row[sl];
-      if (bv == 0.0) continue;
-      const int c = sl % nr;
-      int t = sl / nr;
-      const int dz = t % W3 - w;
-      t /= W3;
-      const int dy = t % W3 - w, dx = t / W3 - w;
-      const long long col = ((((long long)(px + dx) * L) + (py + dy)) * L + (pz + dz)) * nr + c;
-      acc += (bv * sr) * sv[col] * x[col];
+    // pencils (dx, dy): the (dz, c') run is contiguous in the row and in x
+    const int RUN = W3 * nr;
+    const int e0 = (imax(-w, -pz) + w) * nr, e1 = (imin(w, L - 1 - pz) + w + 1) * nr;
+    for (int pc = 0; pc < W3 * W3; ++pc) {
+      const int dx = pc / W3 - w, dy = pc - (pc / W3) * W3 - w;
+      if ((unsigned)(px + dx) >= (unsigned)L || (unsigned)(py + dy) >= (unsigned)L) continue;
+      const long long xb = ((((long long)(px + dx) * L) + (py + dy)) * L + pz - w) * nr;
+      const double* rp = row + (long long)pc * RUN;
+      for (int e = e0 + lane; e < e1; e += 32) acc += (rp[e] * sr) * sv[xb + e] * x[xb + e];
     }
     acc = warp_sum(acc);
     if (lane == 0) {

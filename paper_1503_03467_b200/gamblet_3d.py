@@ -536,10 +536,10 @@ def _level_step(lv, nxt, rho, W, ctas):
 
 
 def _correction_ctas(Lp, rho):
-    """CTAs of the correction-patch launch: 4 per SM, bounded so their
-    dense workspaces stay below ~8 GB."""
+    """CTAs of the correction-patch launch: 2 per SM (103 KB of shared
+    memory each), bounded so their dense workspaces stay below ~8 GB."""
     ld = nat.query("gb3_correction_workspace", Lp, rho, 1)
-    return int(max(1, min(148 * 4, (8 << 30) // max(ld, 1), Lp ** 3)))
+    return int(max(1, min(148 * 2, (8 << 30) // max(ld, 1), Lp ** 3)))
 
 
 def fast_transform_3d(M, A, q, radii):
