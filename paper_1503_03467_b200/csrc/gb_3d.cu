@@ -520,7 +520,8 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
   extern __shared__ double dsm3[];
   double (*D11)[k3PB + 1] = reinterpret_cast<double (*)[k3PB + 1]>(dsm3);  // 64 x 65
   double* y1 = dsm3 + k3PB * (k3PB + 1);                                 // 64
-  double* As = y1 + k3PB;                                                // 64 x k3TLD
+  double* dinv = y1 + k3PB;                                              // 64: 1 / L_jj
+  double* As = dinv + k3PB;                                              // 64 x k3TLD
   double* Bs = As + k3PB * k3TLD;                                        // 64 x k3TLD
   __shared__ int bx0, by0, bz0, nx, ny, nz, bad;
   __shared__ double sh[32];
@@ -584,31 +585,44 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
       }
       if (tid < jb) y1[tid] = v[j0 + tid];
       __syncthreads();
-      if (warp == 0) {
-        for (int j = 0; j < jb; ++j) {
-          double d = D11[j][j];
-          if (lane == 0 && !(d > 0.0)) bad = 1;
-          d = sqrt(d);
-          __syncwarp();
-          if (lane == 0) D11[j][j] = d;
-          __syncwarp();
-          for (int a = j + 1 + lane; a < jb; a += 32) D11[a][j] /= d;
-          __syncwarp();
-          for (int a = j + 1 + lane; a < jb; a += 32) {
-            const double laj = D11[a][j];
-            for (int b = j + 1; b <= a; ++b) D11[a][b] -= laj * D11[b][j];
-          }
-          __syncwarp();
+      // right-looking over the block's columns, all warps: column scale,
+      // then the rank-1 update of the trailing triangle (pairs over threads)
+      for (int j = 0; j < jb; ++j) {
+        const double d = D11[j][j];
+        if (!(d > 0.0)) {
+          if (tid == 0) bad = 1;
+          break;  // uniform: every thread read the same pivot
         }
+        const double l = sqrt(d);
+        const double il = 1.0 / l;
+        __syncthreads();
+        if (tid == 0) {
+          D11[j][j] = l;
+          dinv[j] = il;
+        }
+        for (int a = j + 1 + tid; a < jb; a += blockDim.x) D11[a][j] *= il;
+        __syncthreads();
+        const int t = jb - j - 1;
+        for (int e = tid; e < t * (t + 1) / 2; e += blockDim.x) {
+          int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+          while (a * (a + 1) / 2 > e) --a;
+          while ((a + 1) * (a + 2) / 2 <= e) ++a;
+          const int b = e - a * (a + 1) / 2;
+          D11[a + j + 1][b + j + 1] -= D11[a + j + 1][j] * D11[b + j + 1][j];
+        }
+        __syncthreads();
+      }
+      __syncthreads();
+      if (bad) break;
+      if (warp == 0) {
         for (int j = 0; j < jb; ++j) {  // y1 = L11^-1 v1
-          if (lane == 0) y1[j] /= D11[j][j];
+          if (lane == 0) y1[j] *= dinv[j];
           __syncwarp();
           for (int a = j + 1 + lane; a < jb; a += 32) y1[a] -= D11[a][j] * y1[j];
           __syncwarp();
         }
       }
       __syncthreads();
-      if (bad) break;
       for (int e = tid; e < jb * jb; e += blockDim.x) {
         const int a = e / jb, b = e - a * jb;
         if (b <= a) K[(long long)(j0 + a) * ld + j0 + b] = D11[a][b];
@@ -623,7 +637,7 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
         double a1 = lane + 32 < jb ? ar[lane + 32] : 0.0;
         for (int c = 0; c < jb; ++c) {
           const double src = __shfl_sync(0xffffffffu, c < 32 ? a0 : a1, c & 31);
-          const double xc = src / D11[c][c];
+          const double xc = src * dinv[c];
           if (c < 32) {
             if (lane == c) a0 = xc;
             if (lane > c && lane < jb) a0 -= xc * D11[lane][c];
@@ -1104,7 +1118,7 @@ int gbk3_correction_patches(int Lp, int wB, const double* B, const double* sB, c
                             cudaStream_t s) {
   const long long P = (long long)Lp * Lp * Lp;
   const int g = (int)(P < ctas ? P : ctas);
-  const size_t smem = ((size_t)k3PB * (k3PB + 1) + k3PB + 2 * (size_t)k3PB * k3TLD) * 8;
+  const size_t smem = ((size_t)k3PB * (k3PB + 1) + 2 * k3PB + 2 * (size_t)k3PB * k3TLD) * 8;
   cudaError_t e = cudaFuncSetAttribute(k3_correction_patches,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;

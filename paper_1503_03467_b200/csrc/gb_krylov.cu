@@ -2327,17 +2327,32 @@ __global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
     const int pz = (int)(p % L), py = (int)((p / L) % L), px = (int)(p / ((long long)L * L));
     const double sr = sv[r];
     const double* row = B + r * S;
-    double acc = 0.0;
-    // pencils (dx, dy): the (dz, c') run is contiguous in the row and in x
+    // pencils (dx, dy): the (dz, c') run is contiguous in the row and in x.
+    // The lanes walk the row's slots with stride 32, tracking (pencil,
+    // offset) incrementally; four independent partial sums
     const int RUN = W3 * nr;
     const int e0 = (imax(-w, -pz) + w) * nr, e1 = (imin(w, L - 1 - pz) + w + 1) * nr;
-    for (int pc = 0; pc < W3 * W3; ++pc) {
-      const int dx = pc / W3 - w, dy = pc - (pc / W3) * W3 - w;
-      if ((unsigned)(px + dx) >= (unsigned)L || (unsigned)(py + dy) >= (unsigned)L) continue;
-      const long long xb = ((((long long)(px + dx) * L) + (py + dy)) * L + pz - w) * nr;
-      const double* rp = row + (long long)pc * RUN;
-      for (int e = e0 + lane; e < e1; e += 32) acc += (rp[e] * sr) * sv[xb + e] * x[xb + e];
+    double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+    int pc = lane / RUN, off = lane - pc * RUN;
+    int dx = pc / W3 - w, dy = pc - (pc / W3) * W3 - w;
+    int u = 0;
+    for (int e = lane; e < S; e += 32) {
+      if (off >= e0 && off < e1 && (unsigned)(px + dx) < (unsigned)L &&
+          (unsigned)(py + dy) < (unsigned)L) {
+        const long long col = ((((long long)(px + dx) * L) + (py + dy)) * L + pz - w) * nr + off;
+        acc4[u] += (row[e] * sr) * sv[col] * x[col];
+      }
+      u = (u + 1) & 3;
+      off += 32;
+      while (off >= RUN) {
+        off -= RUN;
+        if (++dy > w) {
+          dy = -w;
+          ++dx;
+        }
+      }
     }
+    double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
     acc = warp_sum(acc);
     if (lane == 0) {
       y[r] = acc;
