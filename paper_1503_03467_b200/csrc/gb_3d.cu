@@ -547,22 +547,35 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
     }
     __syncthreads();
     const int m = nx * ny * nz * 7;
-    // gather (lower triangle and diagonal; row-major, ld) and the rhs
-    for (long long e = tid; e < (long long)m * m; e += blockDim.x) {
-      const int a = (int)(e / m), b = (int)(e - (long long)a * m);
-      if (b > a) continue;
-      const int pa = a / 7, ca = a - 7 * pa, pb = b / 7, cb = b - 7 * pb;
+    // gather (lower triangle and diagonal; row-major, ld): one thread per
+    // (parent a, parent b <= a) pair, the 7 x 7 component block inside (the
+    // 7 columns of a B row for fixed (a, c_a) are contiguous)
+    const int np = nx * ny * nz;
+    for (long long e = tid; e < (long long)np * np; e += blockDim.x) {
+      const int pa = (int)(e / np), pb = (int)(e - (long long)pa * np);
+      if (pb > pa) continue;
       const int az = pa % nz, ay = (pa / nz) % ny, ax = pa / (nz * ny);
       const int bz = pb % nz, by = (pb / nz) % ny, bxx = pb / (nz * ny);
       const int dx = bxx - ax, dy = by - ay, dz = bz - az;
-      double val = 0.0;
-      if (abs(dx) <= wB && abs(dy) <= wB && abs(dz) <= wB) {
-        const long long qa = flat3(bx0 + ax, by0 + ay, bz0 + az, Lp);
-        const long long qb = flat3(bx0 + bxx, by0 + by, bz0 + bz, Lp);
-        const long long ra = qa * 7 + ca, rb = qb * 7 + cb;
-        val = (B[ra * SB + slot3(wB, 7, dx, dy, dz, cb)] * sB[ra]) * sB[rb];
+      const bool in = abs(dx) <= wB && abs(dy) <= wB && abs(dz) <= wB;
+      const long long qa = flat3(bx0 + ax, by0 + ay, bz0 + az, Lp);
+      const long long qb = flat3(bx0 + bxx, by0 + by, bz0 + bz, Lp);
+      const int sl = in ? slot3(wB, 7, dx, dy, dz, 0) : 0;
+      double sb[7];
+#pragma unroll
+      for (int cb = 0; cb < 7; ++cb) sb[cb] = sB[qb * 7 + cb];
+#pragma unroll
+      for (int ca = 0; ca < 7; ++ca) {
+        const long long ra = qa * 7 + ca;
+        const double sa = sB[ra];
+        double* krow = K + (long long)(7 * pa + ca) * ld + 7 * pb;
+        const double* brow = B + ra * SB + sl;
+#pragma unroll
+        for (int cb = 0; cb < 7; ++cb) {
+          if (pb == pa && cb > ca) break;
+          krow[cb] = in ? (brow[cb] * sa) * sb[cb] : 0.0;
+        }
       }
-      K[(long long)a * ld + b] = val;
     }
     for (int a = tid; a < m; a += blockDim.x) {
       const int pa = a / 7, ca = a - 7 * pa;
@@ -628,32 +641,80 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
         if (b <= a) K[(long long)(j0 + a) * ld + j0 + b] = D11[a][b];
       }
       if (tid < jb) v[j0 + tid] = y1[tid];
-      // (b) panel rows below: x L11^T = a (warp per row, 2 columns per lane),
-      // then v[r] -= L21[r, :] y1
       const int r0 = j0 + jb;
-      for (int r = r0 + warp; r < m; r += 8) {
-        double* ar = K + (long long)r * ld + j0;
-        double a0 = lane < jb ? ar[lane] : 0.0;
-        double a1 = lane + 32 < jb ? ar[lane + 32] : 0.0;
-        for (int c = 0; c < jb; ++c) {
-          const double src = __shfl_sync(0xffffffffu, c < 32 ? a0 : a1, c & 31);
-          const double xc = src * dinv[c];
-          if (c < 32) {
-            if (lane == c) a0 = xc;
-            if (lane > c && lane < jb) a0 -= xc * D11[lane][c];
-            if (lane + 32 < jb) a1 -= xc * D11[lane + 32][c];
-          } else {
-            if (lane + 32 == c) a1 = xc;
-            if (lane + 32 > c && lane + 32 < jb) a1 -= xc * D11[lane + 32][c];
+      // (b) panel rows below: L21 = A21 L11^-T as a DMMA GEMM with the
+      // explicit inverse T = L11^-1 (4 threads per column, forward
+      // substitution), then v[r] -= L21[r, :] y1
+      {
+        double* T = Bs;  // T[c][k] stored as Bs[k * k3TLD + c] (the GEMM's B)
+        for (int e = tid; e < k3PB * k3TLD; e += blockDim.x) T[e] = 0.0;
+        __syncthreads();
+        // column col = tid / 4 (8 per warp), its 4 threads split the sums;
+        // every lane of a warp runs the same i range so the shuffles converge:
+        // x_i = (delta_ic - sum_{col <= k < i} L_ik x_k) / L_ii for i >= col
+        const int col = tid >> 2, q4 = tid & 3;
+        for (int i = 8 * warp; i < jb; ++i) {
+          const bool act = col < jb && col <= i;
+          double part = 0.0;
+          if (act)
+            for (int k = col + q4; k < i; k += 4) part += D11[i][k] * T[k * k3TLD + col];
+          part += __shfl_xor_sync(0xffffffffu, part, 1);
+          part += __shfl_xor_sync(0xffffffffu, part, 2);
+          if (act && q4 == 0) T[i * k3TLD + col] = ((i == col ? 1.0 : 0.0) - part) * dinv[i];
+          __syncwarp();
+        }
+        __syncthreads();
+        // T holds (row i, column c) of L11^-1 at T[i * TLD + c]; the GEMM's B
+        // operand is B[k][n] = T[n][k] (L21[r][n] = sum_k A21[r][k] T[n][k])
+        const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fk = lane & 3;
+        for (int rb = r0; rb < m; rb += 64) {
+          for (int e = tid; e < 64 * k3PB; e += blockDim.x) {
+            const int rr = e / k3PB, kk = e - rr * k3PB;
+            As[kk * k3TLD + rr] =
+                (rb + rr < m && kk < jb) ? K[(long long)(rb + rr) * ld + j0 + kk] : 0.0;
+          }
+          __syncthreads();
+          double acc[4][2][2];
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) acc[ii][jj][0] = acc[ii][jj][1] = 0.0;
+          for (int k4 = 0; k4 < jb; k4 += 4) {
+            double af[4], bf[2];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) af[ii] = As[(k4 + fk) * k3TLD + wm * 32 + ii * 8 + fr];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+              bf[jj] = T[(wn * 16 + jj * 8 + fr) * k3TLD + k4 + fk];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj) dmma_884(acc[ii][jj][0], acc[ii][jj][1], af[ii], bf[jj]);
+          }
+          __syncthreads();  // As is reused by the next row block
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int gr = rb + wm * 32 + ii * 8 + fr;
+            if (gr >= m) continue;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const int gc = wn * 16 + jj * 8 + 2 * fk + e2;
+                if (gc < jb) K[(long long)gr * ld + j0 + gc] = acc[ii][jj][e2];
+              }
           }
         }
-        if (lane < jb) ar[lane] = a0;
-        if (lane + 32 < jb) ar[lane + 32] = a1;
-        double t = (lane < jb ? a0 * y1[lane] : 0.0) + (lane + 32 < jb ? a1 * y1[lane + 32] : 0.0);
-        t = warp_sum(t);
-        if (lane == 0) v[r] -= t;
+        __syncthreads();
+        for (int r = r0 + warp; r < m; r += 8) {
+          const double* ar = K + (long long)r * ld + j0;
+          double t = (lane < jb ? ar[lane] * y1[lane] : 0.0) +
+                     (lane + 32 < jb ? ar[lane + 32] * y1[lane + 32] : 0.0);
+          t = warp_sum(t);
+          if (lane == 0) v[r] -= t;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       // (c) trailing update K22 -= L21 L21^T (lower), 64 x 64 output blocks:
       // the two L21 row blocks staged k-major in shared memory, warp (wm, wn)
       // of a 2 x 4 grid owns 32 x 16 = 4 x 2 DMMA m8n8k4 accumulators

@@ -1036,10 +1036,22 @@ int gbk_restriction(int Lp, int rho, const double* Dt, const double* w12, double
   return (int)cudaGetLastError();
 }
 
-static int box_gemm_grid(int Lp, int TB, int wOut) {
+// Persistent tile loops run one wave: the grid is the number of CTAs that
+// are resident at once, so the tiles in flight are consecutive (row blocks
+// next to each other share their operand rows in L2).  A grid larger than
+// one wave would interleave far-apart tiles (CTA b runs b, b + G, ...) and
+// thrash L2 with the operand gathers.
+template <class Kern>
+static int resident_grid(Kern kern, int block, long long ntiles) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, block, 0) != cudaSuccess || nb < 1)
+    nb = 1;
+  const long long g = 148LL * nb;
+  return (int)(ntiles < g ? ntiles : g);
+}
+static long long box_gemm_tiles(int Lp, int TB, int wOut) {
   const long long nb = (Lp + TB - 1) / TB, side = 2 * ((wOut + TB - 1) / TB) + 1;
-  const long long nt = nb * nb * side * side;
-  return (int)(nt < 148LL * 48 ? nt : 148LL * 48);
+  return nb * nb * side * side;
 }
 
 int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
@@ -1049,7 +1061,8 @@ int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
     const size_t bytes = (size_t)Lp * Lp * 3 * box_slots(wBD, 1) * sizeof(double);
     cudaError_t e = cudaMemsetAsync(BD, 0, bytes, s);
     if (e != cudaSuccess) return (int)e;
-    k_box_gemm<3><<<box_gemm_grid(Lp, TB, wBD), 128, 0, s>>>(
+    auto kern = k_box_gemm<3, OpBrows, OpDtRowsB, StoreBox>;
+    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wBD)), 128, 0, s>>>(
         Lp, TB, wB, rho, wBD, OpBrows{B, Lp, wB, box_slots(wB, 3)},
         OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{BD, Lp, 3, wBD, box_slots(wBD, 1)});
     return (int)cudaGetLastError();
@@ -1066,7 +1079,8 @@ int gbk_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
     const size_t bytes = (size_t)Lp * Lp * box_slots(wGD, 1) * sizeof(double);
     cudaError_t e = cudaMemsetAsync(GtD, 0, bytes, s);
     if (e != cudaSuccess) return (int)e;
-    k_box_gemm<1><<<box_gemm_grid(Lp, TB, wGD), 128, 0, s>>>(
+    auto kern = k_box_gemm<1, OpGcols, OpDtRowsB, StoreBox>;
+    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wGD)), 128, 0, s>>>(
         Lp, TB, wG, rho, wGD, OpGcols{G, Lp, wG, box_slots(wG, 1)},
         OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{GtD, Lp, 1, wGD, box_slots(wGD, 1)});
     return (int)cudaGetLastError();
@@ -1084,7 +1098,8 @@ int gbk_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* Gt
     const size_t bytes = (size_t)Lp * Lp * box_slots(wA2, 1) * sizeof(double);
     cudaError_t e = cudaMemsetAsync(raw, 0, bytes, s);
     if (e != cudaSuccess) return (int)e;
-    k_box_gemm<1><<<box_gemm_grid(Lp, TB, wA2), 128, 0, s>>>(
+    auto kern = k_box_gemm<1, OpDtRowsA, OpBDrows, StoreRaw>;
+    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wA2)), 128, 0, s>>>(
         Lp, TB, rho, wBD, wA2, OpDtRowsA{Dt, Lp, rho, box_slots(rho, 3)},
         OpBDrows{BD, Lp, wBD, box_slots(wBD, 1)}, StoreRaw{raw, PAPt, GtD, Lp, wB, wGD, wA2});
     return (int)cudaGetLastError();
@@ -1125,7 +1140,7 @@ int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, 
     const long long nb = (Lp + TB - 1) / TB;
     const long long nrb = (r1 + TB - 1) / TB - r0 / TB;
     const long long nt = nrb * nb * nfs * nft;
-    const int g = (int)(nt < 148LL * 64 ? nt : 148LL * 64);
+    const int g = resident_grid(k_psi_next_mma, 128, nt);
     k_psi_next_mma<<<g, 128, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out, psi_next, rowmax, TB,
                                      nfs, nft, r0, r1);
   } else {
