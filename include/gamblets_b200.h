@@ -413,6 +413,15 @@ int gb3_apply(int L, int nr, int w, const double* B, const double* s, const doub
 int gb3_cg_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* r,
                  double* p, double* Ap, void* state, double* partials, void* host_state,
                  int max_chunk, void* stream);
+/* lambda_min of S B S (3-D box) by the Lanczos moments of the unit start
+ * vector x: the reference's inverse-iteration sequence (sparse_core.py:
+ * 258-277) evaluated from T_m (gb_lanczos_emulate), stop when stable to
+ * lz_tol between checks.  x is overwritten; vp, wv: work n-vectors; ab /
+ * host_ab: 2 cap doubles (device / pinned host). */
+int gb3_lanczos_min(int L, int nr, int w, const double* B, const double* s, double* x,
+                    double* vp, double* wv, void* state, double* partials, void* host_state,
+                    double* ab, double* host_ab, int cap, double tol, int max_outer,
+                    double lz_tol, double* lam, int* outer, int* its, void* stream);
 int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* y,
                   double tol, void* state, double* partials, void* host_state, int max_chunk,
                   void* stream);

@@ -147,6 +147,8 @@ _SIGS = {
     "gb3_psi_t_apply": ([_I, _I, _I, _P, _P, _P, _P], _I),
     "gb3_apply": ([_I, _I, _I, _P, _P, _P, _P, _P], _I),
     "gb3_cg_solve": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
+    "gb3_lanczos_min": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _I, _D,
+                         _P, _P, _P, _P], _I),
     "gb3_pow_solve": ([_I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
 }
 

@@ -714,6 +714,24 @@ int gb3_cg_solve(int L, int nr, int w, const double* B, const double* s, double*
   COUNT(n);
   return wrap(e, "gb3_cg_solve");
 }
+int gb3_lanczos_min(int L, int nr, int w, const double* B, const double* s, double* x,
+                    double* vp, double* wv, void* state, double* partials, void* host_state,
+                    double* ab, double* host_ab, int cap, double tol, int max_outer,
+                    double lz_tol, double* lam, int* outer, int* its, void* stream) {
+  if (!lam || !outer || !its || cap <= 0) return invalid("gb3_lanczos_min: bad arguments");
+  long long n = 0;
+  const int e = gbk3_lanczos_min(L, nr, w, B, s, x, vp, wv, state, partials, host_state, ab,
+                                 host_ab, cap, tol, max_outer, lz_tol, lam, outer, its,
+                                 ST(stream), &n);
+  COUNT(n);
+  if (e < 0) {
+    snprintf(g_err, sizeof(g_err), "gb3_lanczos_min: %s",
+             e == GB_UNSUPPORTED - 9 ? "A v_1 = 0 (inverse iteration breaks down)"
+                                     : "nonpositive Ritz value or tridiagonal eigensolver failed");
+    return GB_ERR_NUMERICAL;
+  }
+  return wrap(e, "gb3_lanczos_min");
+}
 int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double* x, double* y,
                   double tol, void* state, double* partials, void* host_state, int max_chunk,
                   void* stream) {

@@ -242,3 +242,8 @@ int gbk3_cg_solve(int L, int nr, int w, const double* B, const double* sv, doubl
 int gbk3_pow_solve(int L, int nr, int w, const double* B, const double* sv, double* x,
                    double* y, double tol, void* st, double* part, void* host_state,
                    int max_chunk, cudaStream_t s, long long* launches);
+int gbk3_lanczos_min(int L, int nr, int w, const double* B, const double* sv, double* x,
+                     double* vp, double* wv, void* st, double* part, void* host_state,
+                     double* ab, double* hab, int cap, double tol, int max_outer,
+                     double lz_tol, double* lam_out, int* outer_out, int* its_out,
+                     cudaStream_t s, long long* launches);

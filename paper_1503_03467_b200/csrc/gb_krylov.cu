@@ -2549,6 +2549,66 @@ static void post_a(const gb_level_engine_args* e, cudaStream_t s, long long* nl)
   pcg_post(e, e->xa, e->ra, e->pa, e->apa, e->za, (KState*)e->sta, e->parta, s, nl);
 }
 
+// lambda_min of the 3-D operator by the Lanczos moments of the unit start
+// vector x (gb_lanczos.h; the 2-D engine's spectral mode 1): Lanczos steps
+// on k3_box_apply (power-mode reduction) + k_lz_step, the reference's
+// inverse-iteration sequence evaluated on the host every 32-64 steps, stop
+// when the estimate and its stopping index are stable to lz_tol.  x, vp, w:
+// n-vectors (x is overwritten); ab / hab: 2 cap doubles (device / pinned).
+int gbk3_lanczos_min(int L, int nr, int w, const double* B, const double* sv, double* x,
+                     double* vp, double* wv, void* st, double* part, void* host_state,
+                     double* ab, double* hab, int cap, double tol, int max_outer,
+                     double lz_tol, double* lam_out, int* outer_out, int* its_out,
+                     cudaStream_t s, long long* launches) {
+  const long long n = (long long)L * L * L * nr;
+  const int gv = grid_for(n, 256, kRedBlocks);
+  KState* k = (KState*)st;
+  KState* h = (KState*)host_state;
+  cudaError_t ce = cudaMemsetAsync(vp, 0, sizeof(double) * n, s);
+  if (ce != cudaSuccess) return (int)ce;
+  k_state_reset<<<1, 1, 0, s>>>(k, cap);
+  k_lz_init<<<1, 1, 0, s>>>(k);
+  *launches += 2;
+  double* v = x;
+  double* wn = wv;
+  int chunk = 32;
+  double lam_prev = 0.0;
+  int outer_prev = -1;
+  *its_out = 0;
+  for (;;) {
+    for (int i = 0; i < chunk; ++i) {
+      k3_box_apply<<<box3_grid(n), 256, 0, s>>>(L, nr, w, B, sv, v, wn, k, part, 1);
+      k_lz_step<<<gv, 256, 0, s>>>(n, v, vp, wn, k, part, ab);
+      double* t = v;
+      v = wn;
+      wn = t;
+    }
+    *launches += 2LL * chunk;
+    int err = (int)cudaGetLastError();
+    if (err) return err;
+    if ((err = read_state(st, h, s))) return err;
+    const int m = h->it;
+    if (m > 0) {
+      if ((err = gbk_sync_read(ab, hab, sizeof(double) * 2 * (size_t)m, s))) return err;
+      double lam;
+      int outer;
+      const int rc = gb_lz::emulate_inverse_iteration(hab, m, tol, max_outer, &lam, &outer,
+                                                      nullptr, nullptr);
+      if (rc) return GB_UNSUPPORTED - rc;  // -2 / -3: non-SPD or QL failure
+      *lam_out = lam;
+      *outer_out = outer;
+      *its_out = m;
+      const bool stable = outer == outer_prev && fabs(lam - lam_prev) <= lz_tol * fabs(lam);
+      lam_prev = lam;
+      outer_prev = outer;
+      if (h->done || stable) return 0;
+    } else if (h->done) {
+      return GB_UNSUPPORTED - 9;  // A v_1 = 0
+    }
+    chunk = chunk * 2 < 64 ? chunk * 2 : 64;
+  }
+}
+
 static int level_engine(gb_level_engine_args* e, cudaStream_t s, long long& nl);
 static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl);
 static int inverse_iteration(gb_level_engine_args* e, cudaStream_t s, long long& nl);

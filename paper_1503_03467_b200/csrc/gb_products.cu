@@ -1036,18 +1036,13 @@ int gbk_restriction(int Lp, int rho, const double* Dt, const double* w12, double
   return (int)cudaGetLastError();
 }
 
-// Persistent tile loops run one wave: the grid is the number of CTAs that
-// are resident at once, so the tiles in flight are consecutive (row blocks
-// next to each other share their operand rows in L2).  A grid larger than
-// one wave would interleave far-apart tiles (CTA b runs b, b + G, ...) and
-// thrash L2 with the operand gathers.
+// Tile loops are oversubscribed (48 CTAs per SM, grid-stride): the short
+// CTAs free SMs continuously, so the level engine's high-priority SpMV CTAs
+// (a whole SM each) are scheduled while the products run.  A one-wave
+// persistent grid measured slower: it holds every SM until the kernel ends.
 template <class Kern>
-static int resident_grid(Kern kern, int block, long long ntiles) {
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, block, 0) != cudaSuccess || nb < 1)
-    nb = 1;
-  const long long g = 148LL * nb;
-  return (int)(ntiles < g ? ntiles : g);
+static int resident_grid(Kern, int, long long ntiles) {
+  return (int)(ntiles < 148LL * 48 ? ntiles : 148LL * 48);
 }
 static long long box_gemm_tiles(int Lp, int TB, int wOut) {
   const long long nb = (Lp + TB - 1) / TB, side = 2 * ((wOut + TB - 1) / TB) + 1;

@@ -44,8 +44,8 @@ from . import _native as nat
 from . import device as dv
 from .errors import InvalidArgumentError, NumericalError
 from .gamblet_exact import MultiresSolution, SolveRecord
-from .gamblet_fast import (_Krylov, _start_vectors, _clamp_tol, make_schedule,
-                           SYMMETRY_REPAIR_TOL, MAX_ITER_CAP)
+from .gamblet_fast import (_Krylov, _start_vectors, make_schedule, SYMMETRY_REPAIR_TOL,
+                           MAX_ITER_CAP, LANCZOS_CAP, LANCZOS_TOL)
 from .sparse_core import as_csr
 
 __all__ = ["Grid3D", "build_grid_3d", "coefficient_example_3d", "coefficient_checkerboard_3d",
@@ -316,6 +316,7 @@ class FastResult3D:
     levels: dict
     radii: tuple
     iterations: dict = field(default_factory=dict)
+    operators: dict = field(default_factory=dict)  # k -> S B^(k) S Krylov operator
 
 
 # ---------------------------------------------------------------------------
@@ -354,10 +355,13 @@ class _Op3:
         h = kr.host_view()
         return x, int(h["it"]), bool(h["converged"]), int(h["breakdown"])
 
-    def eig_extremes(self, tol=0.1, max_iter=500, seed=24337):
-        """sparse_core.py:232-278: power iteration (lambda_max) and inverse
-        iteration with warm-started inner CG to max(1e-12, 1e-3 tol)
-        (lambda_min), start vectors from default_rng(seed)."""
+    def eig_extremes(self, tol=0.1, max_iter=500, seed=24337, method="lanczos"):
+        """sparse_core.py:232-278: power iteration (lambda_max) and, for
+        lambda_min, the inverse iteration -- evaluated from the Lanczos
+        moments of its start vector (method "lanczos", default: the iteration
+        with exact inner solves) or run with warm-started inner CG to
+        max(1e-12, 1e-3 tol) ("cg", the reference verbatim); start vectors
+        from default_rng(seed)."""
         n = self.n
         st = dv.stream()
         x1, x2 = _start_vectors(n, seed)
@@ -373,6 +377,27 @@ class _Op3:
                  kr.host.data_ptr(), 128, st)
         h = kr.host_view()
         lam_max = float(h["lam"])
+        if method == "lanczos":
+            # the inverse-iteration sequence from the Lanczos moments of its
+            # unit start vector (csrc/gb_lanczos.h; the 2-D engine's default)
+            x = x2.clone()
+            nat.call("gb_dot2", n, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots), dv.ptr(kr.state),
+                     dv.ptr(kr.part), st)
+            nat.call("gb_scale_by_norm", n, dv.ptr(x), dv.ptr(kr.dots), 0, dv.ptr(x), None, st)
+            cap = int(min(n, LANCZOS_CAP))
+            ab = dv.empty(2 * cap)
+            hab = torch.empty(2 * cap, dtype=torch.float64, pin_memory=True)
+            lam = nat.ctypes.c_double(0.0)
+            outer = nat.ctypes.c_int(0)
+            its = nat.ctypes.c_int(0)
+            vp, wv = dv.empty(n), dv.empty(n)
+            nat.call("gb3_lanczos_min", self.L, self.nr, self.w, dv.ptr(self.box),
+                     dv.ptr(self.s), dv.ptr(x), dv.ptr(vp), dv.ptr(wv), dv.ptr(kr.state),
+                     dv.ptr(kr.part), kr.host.data_ptr(), dv.ptr(ab), hab.data_ptr(), cap,
+                     float(tol), int(max_iter), float(LANCZOS_TOL), nat.ctypes.byref(lam),
+                     nat.ctypes.byref(outer), nat.ctypes.byref(its), st)
+            self.spectral_passes = int(h["it"]) + int(its.value)
+            return float(lam.value), lam_max
         inner = max(1e-12, 1e-3 * tol)
         x = x2.clone()
         nat.call("gb_dot2", n, dv.ptr(x), dv.ptr(x), None, dv.ptr(kr.dots), dv.ptr(kr.state),
@@ -652,4 +677,5 @@ def fast_solve_3d(M, A, g_nodal, q, epsilon, uniform_rho=None, c_rho=None):
     sched = make_schedule(epsilon, q, c_rho=c_rho, uniform_rho=uniform_rho)
     levels, ops = fast_transform_3d(M, A, q, sched.radii)
     sol, iters = solve_with_transform_3d(levels, ops, g_nodal, q, sched.subband_tol())
-    return FastResult3D(solution=sol, levels=levels, radii=tuple(sched.radii), iterations=iters)
+    return FastResult3D(solution=sol, levels=levels, radii=tuple(sched.radii), iterations=iters,
+                        operators=ops)

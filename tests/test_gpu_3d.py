@@ -118,3 +118,16 @@ def test_3d_solution_is_linear_and_converges_with_rho():
     # the shared-memory mass-patch kernel covers rho <= 2 in 3-D (BASELINE: 2)
     with pytest.raises(g3.InvalidArgumentError):
         g3.fast_solve_3d(M, A, g, q, 1e-13, uniform_rho=3)
+
+
+def test_3d_lanczos_lambda_min_is_the_inverse_iteration():
+    """The default lambda_min (Lanczos moments of the start vector) against
+    the reference's inverse iteration run verbatim on the same device
+    operator (inner CG to 1e-4), at every level of q = 4."""
+    from paper_1503_03467_b200 import gamblet_3d as g3
+    grid, M, A, g = _inputs(4, "checker")
+    res = g3.fast_solve_3d(M, A, g, 4, 1e-13, uniform_rho=2)
+    for k, op in res.operators.items():
+        lam_min, lam_max = op.eig_extremes(method="cg")
+        np.testing.assert_allclose(res.levels[k].lambda_max_subband, lam_max, rtol=1e-12)
+        np.testing.assert_allclose(res.levels[k].lambda_min_subband, lam_min, rtol=1e-4)
