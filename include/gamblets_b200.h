@@ -181,7 +181,9 @@ int gb_products_mode(int mma);
  * correction-patch grid (0 = auto); 1 -> correction kernel (1 = v3, default;
  * 0 = v2); 2 -> mass patches (0 = banded, default; 1 = dense tiled); 3 -> CTA cap
  * of the persistent symmetric-band SpMV pass (0 = one per SM); 4 -> mass patches by
- * clip type when M is translation invariant (1, default; 0 = every patch).  value
+ * clip type when M is translation invariant (1, default; 0 = every patch); 5 -> phase-1
+ * kernel of the symmetric-band SpMV (1 = warp-specialized, default; 0 =
+ * register-pipelined).  value
  * < 0 queries.  Returns the previous value (-1: unknown key). */
 int gb_tune(int what, int value);
 int gb_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,

@@ -1822,6 +1822,7 @@ static inline bool use_sym(int layout, int L, int nr, int w) {
 #define GB_SYM_WS 1  // warp-specialized bulk-copy phase 1 (0: register-pipelined)
 #endif
 int g_sym_ws_ctas = 0;  // gb_tune(3): CTA cap of the warp-specialized phase 1 (0: 148)
+int g_sym_ws_on = 1;    // gb_tune(5): 0 = register-pipelined phase 1 (smaller CTAs)
 static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, double* y0,
                        KState* s0, double* p0, int r0, const double* x1, double* y1,
                        KState* s1, double* p1, int r1, cudaStream_t s) {
@@ -1829,7 +1830,7 @@ static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, 
   // dynamic shared memory attribute raised to what a launch needs (the
   // kernels also have static shared memory, so the 227 KB cap is not usable)
   static size_t attr[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  const bool ws = GB_SYM_WS && symb_ws_smem(w, nv) <= 226 * 1024;
+  const bool ws = GB_SYM_WS && g_sym_ws_on && symb_ws_smem(w, nv) <= 226 * 1024;
   if (ws) {
     // persistent: one CTA per SM, at most g_sym_ws_ctas (the HBM stream
     // saturates on fewer SMs; the rest stay free for the concurrent setup)
@@ -2186,7 +2187,7 @@ int gbk_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* c
   // bitwise equality with the single solve needs the same phase-1 kernel
   // family for one and two vectors (the warp-specialized one; the dot
   // partials of the register-pipelined fallback are formed in another order)
-  if (!use_sym(1, L, 3, w) || !GB_SYM_WS || symb_ws_smem(w, 1) > 226 * 1024 ||
+  if (!use_sym(1, L, 3, w) || !GB_SYM_WS || !g_sym_ws_on || symb_ws_smem(w, 1) > 226 * 1024 ||
       symb_ws_smem(w, 2) > 226 * 1024)
     return GB_UNSUPPORTED;
   const int Lpad = L + 2 * w;

@@ -21,13 +21,16 @@ ap.add_argument("--q", type=int, default=10)
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--workers", default="2,3,4")
 ap.add_argument("--ctas", default="0,96,74")
+ap.add_argument("--ws", default="1", help="phase-1 kernel: 1 warp-specialized, 0 register-pipelined")
 a = ap.parse_args()
 grid, M, A, load, tree = build_inputs(a.q, "checker")
 sched = gb.make_schedule(EPS, a.q, uniform_rho=RHO)
 Md, Ad = dv.DeviceCSR.from_scipy(M), dv.DeviceCSR.from_scipy(A)
 gd = dv.to_dev(load.g_nodal)
 lib = nat.load()
-for w in map(int, a.workers.split(",")):
+for ws in map(int, a.ws.split(",")):
+  lib.gb_tune(5, ws)
+  for w in map(int, a.workers.split(",")):
     gf.SPECTRAL_WORKERS = w
     if gf._LevelTasks._pool is not None:
         gf._LevelTasks._pool.shutdown(wait=True)
@@ -45,5 +48,6 @@ for w in map(int, a.workers.split(",")):
             out = None
             if i >= 2:
                 ts.append(e0.elapsed_time(e1))
-        print(json.dumps({"workers": w, "sym_ctas": c, "ms": round(float(np.median(ts)), 2),
+        print(json.dumps({"ws": ws, "workers": w, "sym_ctas": c,
+                          "ms": round(float(np.median(ts)), 2),
                           "all": [round(t, 1) for t in ts]}), flush=True)
