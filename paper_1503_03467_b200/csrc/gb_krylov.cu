@@ -2314,6 +2314,9 @@ __global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
                                                    const double* __restrict__ x,
                                                    double* __restrict__ y, KState* st,
                                                    double* part, int mode) {
+  // slot tables (shared): column offset of slot e relative to the row's
+  // point, and its packed (dx, dy, dz) + w for the domain test
+  extern __shared__ int k3tab[];
   __shared__ double sh[32];
   if (mode != 2 && st->done) return;
   const int lane = threadIdx.x & 31;
@@ -2322,38 +2325,56 @@ __global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
   const long long rows = (long long)L * L * L * nr;
   const int W3 = 2 * w + 1;
   const int S = W3 * W3 * W3 * nr;
+  int* toff = k3tab;
+  int* tpk = k3tab + S;
+  for (int e = threadIdx.x; e < S; e += blockDim.x) {
+    const int c = e % nr;
+    int t = e / nr;
+    const int dz = t % W3;
+    t /= W3;
+    const int dy = t % W3, dx = t / W3;
+    toff[e] = (((dx - w) * L + (dy - w)) * L + (dz - w)) * nr + c;
+    tpk[e] = (dx << 16) | (dy << 8) | dz;
+  }
+  __syncthreads();
   double xy = 0.0, yy = 0.0;
   for (long long r = wid; r < rows; r += nwarps) {
     const long long p = r / nr;
     const int pz = (int)(p % L), py = (int)((p / L) % L), px = (int)(p / ((long long)L * L));
+    // in-domain offset ranges (+ w): [lo, hi] per axis
+    const int xlo = imax(w - px, 0), xhi = imin(w + L - 1 - px, 2 * w);
+    const int ylo = imax(w - py, 0), yhi = imin(w + L - 1 - py, 2 * w);
+    const int zlo = imax(w - pz, 0), zhi = imin(w + L - 1 - pz, 2 * w);
     const double sr = sv[r];
     const double* row = B + r * S;
-    // pencils (dx, dy): the (dz, c') run is contiguous in the row and in x.
-    // The lanes walk the row's slots with stride 32, tracking (pencil,
-    // offset) incrementally; four independent partial sums
-    const int RUN = W3 * nr;
-    const int e0 = (imax(-w, -pz) + w) * nr, e1 = (imin(w, L - 1 - pz) + w + 1) * nr;
-    double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-    int pc = lane / RUN, off = lane - pc * RUN;
-    int dx = pc / W3 - w, dy = pc - (pc / W3) * W3 - w;
-    int u = 0;
-    for (int e = lane; e < S; e += 32) {
-      if (off >= e0 && off < e1 && (unsigned)(px + dx) < (unsigned)L &&
-          (unsigned)(py + dy) < (unsigned)L) {
-        const long long col = ((((long long)(px + dx) * L) + (py + dy)) * L + pz - w) * nr + off;
-        acc4[u] += (row[e] * sr) * sv[col] * x[col];
+    const long long base = p * nr;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int e = lane;
+    for (; e + 96 < S; e += 128) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int eu = e + 32 * u;
+        const int pk = tpk[eu];
+        const int dx = pk >> 16, dy = (pk >> 8) & 255, dz = pk & 255;
+        const bool in = dx >= xlo && dx <= xhi && dy >= ylo && dy <= yhi && dz >= zlo && dz <= zhi;
+        const long long col = base + toff[eu];
+        v[u] = in ? (row[eu] * sr) * sv[col] * x[col] : 0.0;
       }
-      u = (u + 1) & 3;
-      off += 32;
-      while (off >= RUN) {
-        off -= RUN;
-        if (++dy > w) {
-          dy = -w;
-          ++dx;
-        }
+      a0 += v[0];
+      a1 += v[1];
+      a2 += v[2];
+      a3 += v[3];
+    }
+    for (; e < S; e += 32) {
+      const int pk = tpk[e];
+      const int dx = pk >> 16, dy = (pk >> 8) & 255, dz = pk & 255;
+      if (dx >= xlo && dx <= xhi && dy >= ylo && dy <= yhi && dz >= zlo && dz <= zhi) {
+        const long long col = base + toff[e];
+        a0 += (row[e] * sr) * sv[col] * x[col];
       }
     }
-    double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+    double acc = (a0 + a1) + (a2 + a3);
     acc = warp_sum(acc);
     if (lane == 0) {
       y[r] = acc;
@@ -2393,12 +2414,23 @@ __global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
   }
 }
 
+static inline size_t box3_smem(int w, int nr) {
+  const size_t b = (size_t)2 * (2 * w + 1) * (2 * w + 1) * (2 * w + 1) * nr * sizeof(int);
+  static size_t attr = 48 * 1024;  // raised once to what a launch needs
+  if (b > attr && b <= 200 * 1024) {
+    cudaFuncSetAttribute(k3_box_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    attr = b;
+  }
+  return b;
+}
+
 static inline int box3_grid(long long rows) { return grid_for(rows * 32, 256, kRedBlocks); }
 
 int gbk3_apply(int L, int nr, int w, const double* B, const double* sv, const double* x,
                double* y, cudaStream_t s) {
   const long long rows = (long long)L * L * L * nr;
-  k3_box_apply<<<box3_grid(rows), 256, 0, s>>>(L, nr, w, B, sv, x, y, nullptr, nullptr, 2);
+  k3_box_apply<<<box3_grid(rows), 256, box3_smem(w, nr), s>>>(L, nr, w, B, sv, x, y, nullptr,
+                                                               nullptr, 2);
   return (int)cudaGetLastError();
 }
 
@@ -2412,7 +2444,8 @@ int gbk3_cg_solve(int L, int nr, int w, const double* B, const double* sv, doubl
   int chunk = 8;
   for (;;) {
     for (int i = 0; i < chunk; ++i) {
-      k3_box_apply<<<box3_grid(n), 256, 0, s>>>(L, nr, w, B, sv, p, Ap, k, part, 0);
+      k3_box_apply<<<box3_grid(n), 256, box3_smem(w, nr), s>>>(L, nr, w, B, sv, p, Ap, k, part,
+                                                               0);
       k_cg_update<<<gv, 256, 0, s>>>(n, x, r, p, Ap, k, part);
       k_cg_dir<<<gv, 256, 0, s>>>(n, r, p, k);
     }
@@ -2436,7 +2469,8 @@ int gbk3_pow_solve(int L, int nr, int w, const double* B, const double* sv, doub
   int chunk = 8;
   for (;;) {
     for (int i = 0; i < chunk; ++i) {
-      k3_box_apply<<<box3_grid(n), 256, 0, s>>>(L, nr, w, B, sv, x, y, k, part, 1);
+      k3_box_apply<<<box3_grid(n), 256, box3_smem(w, nr), s>>>(L, nr, w, B, sv, x, y, k, part,
+                                                               1);
       k_pow_step<<<gv, 256, 0, s>>>(n, x, y, tol, k, part);
       k_pow_scale<<<gv, 256, 0, s>>>(n, x, y, k);
     }
@@ -2578,7 +2612,8 @@ int gbk3_lanczos_min(int L, int nr, int w, const double* B, const double* sv, do
   *its_out = 0;
   for (;;) {
     for (int i = 0; i < chunk; ++i) {
-      k3_box_apply<<<box3_grid(n), 256, 0, s>>>(L, nr, w, B, sv, v, wn, k, part, 1);
+      k3_box_apply<<<box3_grid(n), 256, box3_smem(w, nr), s>>>(L, nr, w, B, sv, v, wn, k, part,
+                                                               1);
       k_lz_step<<<gv, 256, 0, s>>>(n, v, vp, wn, k, part, ab);
       double* t = v;
       v = wn;
