@@ -428,6 +428,84 @@ int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double
                   double tol, void* state, double* partials, void* host_state, int max_chunk,
                   void* stream);
 
+/* ---- Row strips (multi-GPU spatial partition) --------------
+ * Every `_rows` entry computes the grid rows [r0, r1) of its output only and
+ * reads its inputs at global indices, so a rank passes the same base pointers
+ * as the whole-level call and provides the halo rows named in each comment
+ * (exchanged by paper_1503_03467_b200/comm.py).  The whole-level entry points
+ * are the [0, L) instances: the union of a partition's strips is bitwise the
+ * whole level.  Patches are independent given the level operator
+ * (gamblet_fast.py:464-498, 546-580).
+ * The `gb_dist_*` entries are the rank-local pieces of the distributed
+ * block-Jacobi PCG / power iteration / Lanczos recurrence on a strip of a
+ * tiled level (rows multiples of 4): every reduction stops at the strip's
+ * partial sum, the caller all-reduces it, a commit entry applies it to the
+ * iteration state (sparse_core.py:126-165, 232-278 split at the reductions). */
+/* grid rows [r0, r1) of a box from the CSR slice of exactly those matrix rows (local indptr, global columns) */
+int gb_csr_to_box_rows(int n, int w, const int32_t* indptr, const int32_t* indices, const double* data, double* box, int64_t* status, int r0, int r1, void* stream);
+/* gb_box_sym_drop on the grid rows [r0, r1); reads raw rows within w of the strip */
+int gb_box_sym_drop_rows(int L, int nr, int w, const double* raw, double* out, const double* dmin, double* stats, int r0, int r1, void* stream);
+/* X = psi A, fine rows [r0, r1); reads A rows within rho */
+int gb_psi_stencil_rows(int n, int lo, int wd, int rho, const double* psi, int wA, const double* A, int wX, double* X, int r0, int r1, void* stream);
+/* raw = X psi^T, fine rows [r0, r1); reads psi rows within wR */
+int gb_psi_galerkin_t_rows(int n, int lo, int wd, int rho, const double* psi, int wX, const double* X, int wR, double* raw, double* work, int r0, int r1, void* stream);
+/* diag(B) of the parents in rows [r0, r1) and their running minimum */
+int gb_level_diag_rows(int Lk, int wA, const double* A, const double* host_w12, double* bdiag, double* dmin, int r0, int r1, void* stream);
+/* B, G, P A P^T rows of the parents in rows [r0, r1); reads A rows of parents within wB, bdiag within wB */
+int gb_level_blocks_rows(int Lk, int wA, const double* A, const double* host_w12, int wB, const double* bdiag, const double* dmin, double* B, double* G, double* PAPt, double* stats, int r0, int r1, void* stream);
+/* R rows [r0, r1) from the same rows of D^T */
+int gb_restriction_rows(int Lp, int rho, const double* Dt, const double* host_w12, double* R, int r0, int r1, void* stream);
+/* B D rows [r0, r1); reads D^T rows within wBD */
+int gb_bd_rows(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD, double* BD, int r0, int r1, void* stream);
+/* G^T D rows [r0, r1); reads G rows within wG and D^T rows within wGD */
+int gb_gtd_rows(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD, double* GtD, int r0, int r1, void* stream);
+/* raw A^(k-1) rows [r0, r1); reads G^T D rows within wGD and B D rows within rho */
+int gb_coarse_raw_rows(int Lp, int wB, const double* PAPt, int wGD, const double* GtD, int rho, const double* Dt, int wBD, const double* BD, int wA2, double* raw, int r0, int r1, void* stream);
+/* W psi rows of the parents in rows [r0, r1), window points with fine row in [f0, f1) only */
+int gb_wpsi_rows(int n, int Lk, int lo, int wd, const double* host_w12, const double* psi, int wdw, double* Wpsi, int r0, int r1, int f0, int f1, void* stream);
+/* raw psi^(k-1) rows [r0, r1) and their maxima, window points with fine row in [f0, f1) only (no drop) */
+int gb_psi_next_raw_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw, const double* Wpsi, int rho, const double* Dt, int lo2, int wd2, double* psi_next, double* rowmax, int r0, int r1, int f0, int f1, void* stream);
+/* the row-tail drop of psi rows [r0, r1) given their (all-reduced) maxima */
+int gb_psi_drop_rows(int n, int Lp, int lo2, int wd2, double* psi_next, const double* rowmax, int r0, int r1, int f0, int f1, void* stream);
+/* gb_pad on grid rows [r0, r1) */
+int gb_pad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst, int r0, int r1, void* stream);
+/* gb_unpad on grid rows [r0, r1) */
+int gb_unpad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst, int r0, int r1, void* stream);
+/* gb_apply_w on parent rows [r0, r1) */
+int gb_apply_w_rows(int Lp, const double* host_w12, const double* g, const double* s, double* out, int r0, int r1, void* stream);
+/* gb_apply_wt on parent rows [r0, r1) */
+int gb_apply_wt_rows(int Lp, const double* host_w12, const double* w, double* v, int r0, int r1, void* stream);
+/* gb_apply_r on parent rows [r0, r1); reads g within 2 rho + 1 child rows */
+int gb_apply_r_rows(int Lp, int rho, const double* R, const double* g, double* out, int r0, int r1, void* stream);
+/* fine rows [F0, F1) of psi^T v summed over the psi rows in grid rows [j_lo, j_hi) only */
+int gb_psi_t_apply_rows(int n, int L, int lo, int wd, const double* psi, const double* v, double* inc, int F0, int F1, int j_lo, int j_hi, void* stream);
+/* block-Jacobi inverses of the 2x2-parent blocks in rows [r0, r1) */
+int gb_bj_setup_rows(int L, int w, const double* B, const double* s, float* inv, int r0, int r1, void* stream);
+/* rows [r0, r1) of the symmetric band copy of S B S; reads s within w rows below */
+int gb_scale_box_symT_rows(int L, int w, const double* B, const double* s, double* UsT, int r0, int r1, void* stream);
+/* phase 1 of the symmetric SpMV on the strip's tiles for nv vectors; red[v] = strip partial of x_v.(A x_v) */
+int gb_dist_apply(int L, int w, const double* UsT, int nv, const double* x0, double* y0, void* st0, double* part0, const double* x1, double* y1, void* st1, double* part1, double* red, int r0, int r1, void* stream);
+/* x = 0, r = b, z = p = Minv r on the strip; out = (r.r, r.z, b.b) partials */
+int gb_dist_pcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z, const float* inv, void* st, double* part, double* out, int r0, int r1, void* stream);
+/* all-reduced init sums -> iteration state */
+int gb_dist_pcg_init_commit(void* st, const double* out, double rel_tol, int max_iter, void* stream);
+/* PCG update on the strip with alpha = rs / red[0]; out = (r.r, r.z) partials */
+int gb_dist_pcg_update(int L, int w, double* x, double* r, const double* p, const double* Ap, double* z, const float* inv, void* st, const double* red, double* part, double* out, int r0, int r1, void* stream);
+/* all-reduced sums -> state (convergence, beta), then p = z + beta p on the strip */
+int gb_dist_pcg_commit_dir(int L, int w, void* st, const double* red, const double* out, const double* z, double* p, int r0, int r1, void* stream);
+/* y += spill-over on the strip; out[0] = y.y partial */
+int gb_dist_fix_yy(int L, int w, double* y, void* st, double* part, double* out, int r0, int r1, void* stream);
+/* power iteration between its reductions (stage 0: lam, ynorm, residual partial; stage 1: test, x = y / ynorm) */
+int gb_dist_pow_step(int L, int w, double* x, const double* y, void* st, const double* red, const double* out_yy, double* out_res, double* part, double tol, int r0, int r1, int stage, void* stream);
+/* Lanczos recurrence on the strip; out[0] = |u|^2 partial */
+int gb_dist_lz_update(int L, int w, const double* x, double* y, double* vp, void* st, const double* red, double* part, double* out, int r0, int r1, void* stream);
+/* all-reduced |u|^2 -> (alpha_j, beta_j) appended, state advanced */
+int gb_dist_lz_commit(void* st, const double* red, const double* out, double* ab, void* stream);
+/* reset the state for a Lanczos sequence of at most cap steps */
+int gb_dist_lz_begin(void* st, int cap, void* stream);
+/* out[0] = a.b over n contiguous elements (strip partial) */
+int gb_dist_dot(int64_t n, const double* a, const double* b, void* st, double* part, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -150,6 +150,39 @@ _SIGS = {
     "gb3_lanczos_min": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _I, _D,
                          _P, _P, _P, _P], _I),
     "gb3_pow_solve": ([_I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
+    # row strips and the distributed Krylov pieces (multi-GPU partition)
+    "gb_csr_to_box_rows": ([_I, _I, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_box_sym_drop_rows": ([_I, _I, _I, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_psi_stencil_rows": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P], _I),
+    "gb_psi_galerkin_t_rows": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _I, _P], _I),
+    "gb_level_diag_rows": ([_I, _I, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_level_blocks_rows": ([_I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_restriction_rows": ([_I, _I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_bd_rows": ([_I, _I, _P, _I, _P, _I, _P, _I, _I, _P], _I),
+    "gb_gtd_rows": ([_I, _I, _P, _I, _P, _I, _P, _I, _I, _P], _I),
+    "gb_coarse_raw_rows": ([_I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P, _I, _I, _P], _I),
+    "gb_wpsi_rows": ([_I, _I, _I, _I, _P, _P, _I, _P, _I, _I, _I, _I, _P], _I),
+    "gb_psi_next_raw_rows": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P, _P, _I, _I, _I, _I, _P], _I),
+    "gb_psi_drop_rows": ([_I, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P], _I),
+    "gb_pad_rows": ([_I, _I, _I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_unpad_rows": ([_I, _I, _I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_apply_w_rows": ([_I, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_apply_wt_rows": ([_I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_apply_r_rows": ([_I, _I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_psi_t_apply_rows": ([_I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _P], _I),
+    "gb_bj_setup_rows": ([_I, _I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_scale_box_symT_rows": ([_I, _I, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_apply": ([_I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_pcg_init": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_pcg_init_commit": ([_P, _P, _D, _I, _P], _I),
+    "gb_dist_pcg_update": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_pcg_commit_dir": ([_I, _I, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_fix_yy": ([_I, _I, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_pow_step": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _D, _I, _I, _I, _P], _I),
+    "gb_dist_lz_update": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "gb_dist_lz_commit": ([_P, _P, _P, _P, _P], _I),
+    "gb_dist_lz_begin": ([_P, _I, _P], _I),
+    "gb_dist_dot": ([_L, _P, _P, _P, _P, _P, _P], _I),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -104,13 +104,16 @@ __global__ void k_csr_halfwidth(int n, const int32_t* __restrict__ indptr,
 __global__ void k_csr_to_box(int n, int w, const int32_t* __restrict__ indptr,
                              const int32_t* __restrict__ indices,
                              const double* __restrict__ data,
-                             double* __restrict__ box, long long* status) {
-  const long long N = (long long)n * n;
+                             double* __restrict__ box, long long* status, long long row0,
+                             long long nrows) {
+  // indptr holds nrows + 1 entries of the rows [row0, row0 + nrows); column
+  // indices and the box are global
   const int S = box_slots(w, 1);
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < N;
-       r += (long long)gridDim.x * blockDim.x) {
+  for (long long lr = blockIdx.x * (long long)blockDim.x + threadIdx.x; lr < nrows;
+       lr += (long long)gridDim.x * blockDim.x) {
+    const long long r = row0 + lr;
     const int rs = (int)(r / n), rt = (int)(r % n);
-    for (int e = indptr[r]; e < indptr[r + 1]; ++e) {
+    for (int e = indptr[lr]; e < indptr[lr + 1]; ++e) {
       const int c = indices[e];
       const int ds = c / n - rs, dt = c % n - rt;
       if (ds < -w || ds > w || dt < -w || dt > w) {
@@ -172,12 +175,11 @@ __global__ void k_box_diag_min(long long rows, int nr, int w,
 __global__ void k_box_sym_drop(int L, int nr, int w, const double* __restrict__ raw,
                                double* __restrict__ out,
                                const double* __restrict__ dmin,
-                               double* __restrict__ stats) {
+                               double* __restrict__ stats, long long e0, long long e1) {
   const int S = box_slots(w, nr);
-  const long long total = (long long)L * L * nr * S;
   const bool do_drop = *dmin > 0.0;
   double mdiff = 0.0, mabs = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long r = e / S;
     const int sl = (int)(e - r * S);
@@ -386,7 +388,20 @@ int gbk_csr_to_box(int n, int w, const int32_t* indptr, const int32_t* indices,
                    cudaStream_t s) {
   const long long N = (long long)n * n;
   k_csr_to_box<<<grid_for(N, 256), 256, 0, s>>>(n, w, indptr, indices, data, box,
-                                                status);
+                                                status, 0, N);
+  return (int)cudaGetLastError();
+}
+
+// grid rows [r0, r1) from the CSR slice of exactly those matrix rows (local
+// indptr starting at 0, global column indices) into the global box
+int gbk_csr_to_box_rows(int n, int w, const int32_t* indptr, const int32_t* indices,
+                        const double* data, double* box, long long* status, int r0, int r1,
+                        cudaStream_t s) {
+  if (r0 < 0 || r1 > n || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long nrows = (long long)(r1 - r0) * n;
+  k_csr_to_box<<<grid_for(nrows, 256), 256, 0, s>>>(n, w, indptr, indices, data, box, status,
+                                                    (long long)r0 * n, nrows);
   return (int)cudaGetLastError();
 }
 
@@ -404,9 +419,17 @@ int gbk_box_diag_min(long long rows, int nr, int w, const double* box,
 
 int gbk_box_sym_drop(int L, int nr, int w, const double* raw, double* out,
                      const double* dmin, double* stats, cudaStream_t s) {
-  const long long total = (long long)L * L * nr * box_slots(w, nr);
-  k_box_sym_drop<<<grid_for(total, 256), 256, 0, s>>>(L, nr, w, raw, out, dmin,
-                                                      stats);
+  return gbk_box_sym_drop_rows(L, nr, w, raw, out, dmin, stats, 0, L, s);
+}
+
+// grid rows [r0, r1) of the output; reads raw rows within w of the strip
+int gbk_box_sym_drop_rows(int L, int nr, int w, const double* raw, double* out,
+                          const double* dmin, double* stats, int r0, int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > L || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)L * nr * box_slots(w, nr);
+  k_box_sym_drop<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(L, nr, w, raw, out, dmin, stats,
+                                                               r0 * per, r1 * per);
   return (int)cudaGetLastError();
 }
 

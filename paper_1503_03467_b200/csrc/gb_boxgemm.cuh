@@ -28,7 +28,8 @@ constexpr int BG_KC = 32, BG_LDA = 36, BG_LDB = 20;
 // warp w: n-tile w & 1, m-tiles (w >> 1) + 2 j, j < MC.
 template <int MC, class AOp, class BOp, class OutOp>
 __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb, int wOut,
-                                                  AOp aop, BOp bop, OutOp out) {
+                                                  AOp aop, BOp bop, OutOp out, int rb0,
+                                                  int rb1) {
   // double-buffered: chunk c + 1 is gathered into registers while chunk c is
   // multiplied (the operand gathers are L2-latency bound)
   __shared__ double As[2][16 * MC * BG_LDA];
@@ -39,13 +40,14 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
   const int nb = (Lp + TB - 1) / TB;
   const int nbo = (wOut + TB - 1) / TB;
   const int side = 2 * nbo + 1;
-  const long long ntiles = (long long)nb * nb * side * side;
+  // row blocks [rb0, rb1) of the output only (row strips; whole level: [0, nb))
+  const long long ntiles = (long long)(rb1 - rb0) * nb * side * side;
   const double* Ab = aop.base();
   const double* Bb = bop.base();
   const int wA = aop.hw(), wB_ = bop.hw();
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long mb = t / (side * side);
-    const int ob = (int)(t - mb * side * side);
+    const long long mb = t / (side * side) + (long long)rb0 * nb;
+    const int ob = (int)(t % (side * side));
     const int mbs = (int)(mb / nb), mbt = (int)(mb % nb);
     const int nbs = mbs + ob / side - nbo, nbt = mbt + ob % side - nbo;
     if (nbs < 0 || nbs >= nb || nbt < 0 || nbt >= nb) continue;  // CTA-uniform

@@ -45,7 +45,7 @@ static int invalid(const char* msg) {
 
 extern "C" {
 
-int gb_abi_version(void) { return 5; }
+int gb_abi_version(void) { return 6; }
 unsigned long long gb_launch_count(void) { return g_launches.load(); }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
@@ -740,6 +740,200 @@ int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double
                                max_chunk, ST(stream), &n);
   COUNT(n);
   return wrap(e, "gb3_pow_solve");
+}
+
+// ---- row-strip entry points (multi-GPU partition) and the distributed Krylov pieces ----
+int gb_csr_to_box_rows(int n, int w, const int32_t* indptr, const int32_t* indices, const double* data, double* box, int64_t* status, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_csr_to_box_rows(n, w, indptr, indices, data, box, LL(status), r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("csr_to_box_rows: bad row range or unsupported configuration");
+  return wrap(rc, "csr_to_box_rows");
+}
+int gb_box_sym_drop_rows(int L, int nr, int w, const double* raw, double* out, const double* dmin, double* stats, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_box_sym_drop_rows(L, nr, w, raw, out, dmin, stats, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("box_sym_drop_rows: bad row range or unsupported configuration");
+  return wrap(rc, "box_sym_drop_rows");
+}
+int gb_psi_stencil_rows(int n, int lo, int wd, int rho, const double* psi, int wA, const double* A, int wX, double* X, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_psi_stencil_rows(n, lo, wd, rho, psi, wA, A, wX, X, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("psi_stencil_rows: bad row range or unsupported configuration");
+  return wrap(rc, "psi_stencil_rows");
+}
+int gb_psi_galerkin_t_rows(int n, int lo, int wd, int rho, const double* psi, int wX, const double* X, int wR, double* raw, double* work, int r0, int r1, void* stream) {
+  COUNT(3);
+  const int rc = gbk_psi_galerkin_t_rows(n, lo, wd, rho, psi, wX, X, wR, raw, work, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("psi_galerkin_t_rows: bad row range or unsupported configuration");
+  return wrap(rc, "psi_galerkin_t_rows");
+}
+int gb_level_diag_rows(int Lk, int wA, const double* A, const double* host_w12, double* bdiag, double* dmin, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_level_diag_rows(Lk, wA, A, host_w12, bdiag, dmin, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("level_diag_rows: bad row range or unsupported configuration");
+  return wrap(rc, "level_diag_rows");
+}
+int gb_level_blocks_rows(int Lk, int wA, const double* A, const double* host_w12, int wB, const double* bdiag, const double* dmin, double* B, double* G, double* PAPt, double* stats, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_level_blocks_rows(Lk, wA, A, host_w12, wB, bdiag, dmin, B, G, PAPt, stats, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("level_blocks_rows: bad row range or unsupported configuration");
+  return wrap(rc, "level_blocks_rows");
+}
+int gb_restriction_rows(int Lp, int rho, const double* Dt, const double* host_w12, double* R, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_restriction_rows(Lp, rho, Dt, host_w12, R, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("restriction_rows: bad row range or unsupported configuration");
+  return wrap(rc, "restriction_rows");
+}
+int gb_bd_rows(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD, double* BD, int r0, int r1, void* stream) {
+  COUNT(2);
+  const int rc = gbk_bd_rows(Lp, wB, B, rho, Dt, wBD, BD, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("bd_rows: bad row range or unsupported configuration");
+  return wrap(rc, "bd_rows");
+}
+int gb_gtd_rows(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD, double* GtD, int r0, int r1, void* stream) {
+  COUNT(2);
+  const int rc = gbk_gtd_rows(Lp, wG, G, rho, Dt, wGD, GtD, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("gtd_rows: bad row range or unsupported configuration");
+  return wrap(rc, "gtd_rows");
+}
+int gb_coarse_raw_rows(int Lp, int wB, const double* PAPt, int wGD, const double* GtD, int rho, const double* Dt, int wBD, const double* BD, int wA2, double* raw, int r0, int r1, void* stream) {
+  COUNT(2);
+  const int rc = gbk_coarse_raw_rows(Lp, wB, PAPt, wGD, GtD, rho, Dt, wBD, BD, wA2, raw, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("coarse_raw_rows: bad row range or unsupported configuration");
+  return wrap(rc, "coarse_raw_rows");
+}
+int gb_wpsi_rows(int n, int Lk, int lo, int wd, const double* host_w12, const double* psi, int wdw, double* Wpsi, int r0, int r1, int f0, int f1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_wpsi_rows(n, Lk, lo, wd, host_w12, psi, wdw, Wpsi, r0, r1, f0, f1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("wpsi_rows: bad row range or unsupported configuration");
+  return wrap(rc, "wpsi_rows");
+}
+int gb_psi_next_raw_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw, const double* Wpsi, int rho, const double* Dt, int lo2, int wd2, double* psi_next, double* rowmax, int r0, int r1, int f0, int f1, void* stream) {
+  COUNT(2);
+  const int rc = gbk_psi_next_raw_rows(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2, psi_next, rowmax, r0, r1, f0, f1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("psi_next_raw_rows: bad row range or unsupported configuration");
+  return wrap(rc, "psi_next_raw_rows");
+}
+int gb_psi_drop_rows(int n, int Lp, int lo2, int wd2, double* psi_next, const double* rowmax, int r0, int r1, int f0, int f1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_psi_drop_rows(n, Lp, lo2, wd2, psi_next, rowmax, r0, r1, f0, f1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("psi_drop_rows: bad row range or unsupported configuration");
+  return wrap(rc, "psi_drop_rows");
+}
+int gb_pad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_pad_rows(L, nr, w, src, scale, dst, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("pad_rows: bad row range or unsupported configuration");
+  return wrap(rc, "pad_rows");
+}
+int gb_unpad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_unpad_rows(L, nr, w, src, scale, dst, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("unpad_rows: bad row range or unsupported configuration");
+  return wrap(rc, "unpad_rows");
+}
+int gb_apply_w_rows(int Lp, const double* host_w12, const double* g, const double* s, double* out, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_apply_w_rows(Lp, host_w12, g, s, out, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("apply_w_rows: bad row range or unsupported configuration");
+  return wrap(rc, "apply_w_rows");
+}
+int gb_apply_wt_rows(int Lp, const double* host_w12, const double* w, double* v, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_apply_wt_rows(Lp, host_w12, w, v, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("apply_wt_rows: bad row range or unsupported configuration");
+  return wrap(rc, "apply_wt_rows");
+}
+int gb_apply_r_rows(int Lp, int rho, const double* R, const double* g, double* out, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_apply_r_rows(Lp, rho, R, g, out, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("apply_r_rows: bad row range or unsupported configuration");
+  return wrap(rc, "apply_r_rows");
+}
+int gb_psi_t_apply_rows(int n, int L, int lo, int wd, const double* psi, const double* v, double* inc, int F0, int F1, int j_lo, int j_hi, void* stream) {
+  COUNT(1);
+  const int rc = gbk_psi_t_apply_rows(n, L, lo, wd, psi, v, inc, F0, F1, j_lo, j_hi, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("psi_t_apply_rows: bad row range or unsupported configuration");
+  return wrap(rc, "psi_t_apply_rows");
+}
+int gb_bj_setup_rows(int L, int w, const double* B, const double* s, float* inv, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_bj_setup_rows(L, w, B, s, inv, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("bj_setup_rows: bad row range or unsupported configuration");
+  return wrap(rc, "bj_setup_rows");
+}
+int gb_scale_box_symT_rows(int L, int w, const double* B, const double* s, double* UsT, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_scale_box_symT_rows(L, w, B, s, UsT, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("scale_box_symT_rows: bad row range or unsupported configuration");
+  return wrap(rc, "scale_box_symT_rows");
+}
+int gb_dist_apply(int L, int w, const double* UsT, int nv, const double* x0, double* y0, void* st0, double* part0, const double* x1, double* y1, void* st1, double* part1, double* red, int r0, int r1, void* stream) {
+  COUNT(2);
+  const int rc = gbk_dist_apply(L, w, UsT, nv, x0, y0, st0, part0, x1, y1, st1, part1, red, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_apply: bad row range or unsupported configuration");
+  return wrap(rc, "dist_apply");
+}
+int gb_dist_pcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z, const float* inv, void* st, double* part, double* out, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_pcg_init(L, w, b, x, r, p, z, inv, st, part, out, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_pcg_init: bad row range or unsupported configuration");
+  return wrap(rc, "dist_pcg_init");
+}
+int gb_dist_pcg_init_commit(void* st, const double* out, double rel_tol, int max_iter, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_pcg_init_commit(st, out, rel_tol, max_iter, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_pcg_init_commit: bad row range or unsupported configuration");
+  return wrap(rc, "dist_pcg_init_commit");
+}
+int gb_dist_pcg_update(int L, int w, double* x, double* r, const double* p, const double* Ap, double* z, const float* inv, void* st, const double* red, double* part, double* out, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_pcg_update(L, w, x, r, p, Ap, z, inv, st, red, part, out, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_pcg_update: bad row range or unsupported configuration");
+  return wrap(rc, "dist_pcg_update");
+}
+int gb_dist_pcg_commit_dir(int L, int w, void* st, const double* red, const double* out, const double* z, double* p, int r0, int r1, void* stream) {
+  COUNT(2);
+  const int rc = gbk_dist_pcg_commit_dir(L, w, st, red, out, z, p, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_pcg_commit_dir: bad row range or unsupported configuration");
+  return wrap(rc, "dist_pcg_commit_dir");
+}
+int gb_dist_fix_yy(int L, int w, double* y, void* st, double* part, double* out, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_fix_yy(L, w, y, st, part, out, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_fix_yy: bad row range or unsupported configuration");
+  return wrap(rc, "dist_fix_yy");
+}
+int gb_dist_pow_step(int L, int w, double* x, const double* y, void* st, const double* red, const double* out_yy, double* out_res, double* part, double tol, int r0, int r1, int stage, void* stream) {
+  COUNT(2);
+  const int rc = gbk_dist_pow_step(L, w, x, y, st, red, out_yy, out_res, part, tol, r0, r1, stage, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_pow_step: bad row range or unsupported configuration");
+  return wrap(rc, "dist_pow_step");
+}
+int gb_dist_lz_update(int L, int w, const double* x, double* y, double* vp, void* st, const double* red, double* part, double* out, int r0, int r1, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_lz_update(L, w, x, y, vp, st, red, part, out, r0, r1, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_lz_update: bad row range or unsupported configuration");
+  return wrap(rc, "dist_lz_update");
+}
+int gb_dist_lz_commit(void* st, const double* red, const double* out, double* ab, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_lz_commit(st, red, out, ab, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_lz_commit: bad row range or unsupported configuration");
+  return wrap(rc, "dist_lz_commit");
+}
+int gb_dist_lz_begin(void* st, int cap, void* stream) {
+  COUNT(2);
+  const int rc = gbk_dist_lz_begin(st, cap, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_lz_begin: bad row range or unsupported configuration");
+  return wrap(rc, "dist_lz_begin");
+}
+int gb_dist_dot(int64_t n, const double* a, const double* b, void* st, double* part, double* out, void* stream) {
+  COUNT(1);
+  const int rc = gbk_dist_dot(n, a, b, st, part, out, ST(stream));
+  if (rc == GB_UNSUPPORTED) return invalid("dist_dot: bad row range or unsupported configuration");
+  return wrap(rc, "dist_dot");
 }
 
 }  // extern "C"

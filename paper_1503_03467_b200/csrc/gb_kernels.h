@@ -186,6 +186,40 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
 int gbk_products_mode(int mma);
 int gbk_tune(int what, int value);
 
+// row-strip variants (gb_box.cu, gb_products.cu, gb_krylov.cu) and gb_dist.cuh launchers
+int gbk_csr_to_box_rows(int n, int w, const int32_t* indptr, const int32_t* indices, const double* data, double* box, long long* status, int r0, int r1, cudaStream_t st_);
+int gbk_box_sym_drop_rows(int L, int nr, int w, const double* raw, double* out, const double* dmin, double* stats, int r0, int r1, cudaStream_t st_);
+int gbk_psi_stencil_rows(int n, int lo, int wd, int rho, const double* psi, int wA, const double* A, int wX, double* X, int r0, int r1, cudaStream_t st_);
+int gbk_psi_galerkin_t_rows(int n, int lo, int wd, int rho, const double* psi, int wX, const double* X, int wR, double* raw, double* work, int r0, int r1, cudaStream_t st_);
+int gbk_level_diag_rows(int Lk, int wA, const double* A, const double* host_w12, double* bdiag, double* dmin, int r0, int r1, cudaStream_t st_);
+int gbk_level_blocks_rows(int Lk, int wA, const double* A, const double* host_w12, int wB, const double* bdiag, const double* dmin, double* B, double* G, double* PAPt, double* stats, int r0, int r1, cudaStream_t st_);
+int gbk_restriction_rows(int Lp, int rho, const double* Dt, const double* host_w12, double* R, int r0, int r1, cudaStream_t st_);
+int gbk_bd_rows(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD, double* BD, int r0, int r1, cudaStream_t st_);
+int gbk_gtd_rows(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD, double* GtD, int r0, int r1, cudaStream_t st_);
+int gbk_coarse_raw_rows(int Lp, int wB, const double* PAPt, int wGD, const double* GtD, int rho, const double* Dt, int wBD, const double* BD, int wA2, double* raw, int r0, int r1, cudaStream_t st_);
+int gbk_wpsi_rows(int n, int Lk, int lo, int wd, const double* host_w12, const double* psi, int wdw, double* Wpsi, int r0, int r1, int f0, int f1, cudaStream_t st_);
+int gbk_psi_next_raw_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw, const double* Wpsi, int rho, const double* Dt, int lo2, int wd2, double* psi_next, double* rowmax, int r0, int r1, int f0, int f1, cudaStream_t st_);
+int gbk_psi_drop_rows(int n, int Lp, int lo2, int wd2, double* psi_next, const double* rowmax, int r0, int r1, int f0, int f1, cudaStream_t st_);
+int gbk_pad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst, int r0, int r1, cudaStream_t st_);
+int gbk_unpad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst, int r0, int r1, cudaStream_t st_);
+int gbk_apply_w_rows(int Lp, const double* host_w12, const double* g, const double* s, double* out, int r0, int r1, cudaStream_t st_);
+int gbk_apply_wt_rows(int Lp, const double* host_w12, const double* w, double* v, int r0, int r1, cudaStream_t st_);
+int gbk_apply_r_rows(int Lp, int rho, const double* R, const double* g, double* out, int r0, int r1, cudaStream_t st_);
+int gbk_psi_t_apply_rows(int n, int L, int lo, int wd, const double* psi, const double* v, double* inc, int F0, int F1, int j_lo, int j_hi, cudaStream_t st_);
+int gbk_bj_setup_rows(int L, int w, const double* B, const double* s, float* inv, int r0, int r1, cudaStream_t st_);
+int gbk_scale_box_symT_rows(int L, int w, const double* B, const double* s, double* UsT, int r0, int r1, cudaStream_t st_);
+int gbk_dist_apply(int L, int w, const double* UsT, int nv, const double* x0, double* y0, void* st0, double* part0, const double* x1, double* y1, void* st1, double* part1, double* red, int r0, int r1, cudaStream_t st_);
+int gbk_dist_pcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z, const float* inv, void* st, double* part, double* out, int r0, int r1, cudaStream_t st_);
+int gbk_dist_pcg_init_commit(void* st, const double* out, double rel_tol, int max_iter, cudaStream_t st_);
+int gbk_dist_pcg_update(int L, int w, double* x, double* r, const double* p, const double* Ap, double* z, const float* inv, void* st, const double* red, double* part, double* out, int r0, int r1, cudaStream_t st_);
+int gbk_dist_pcg_commit_dir(int L, int w, void* st, const double* red, const double* out, const double* z, double* p, int r0, int r1, cudaStream_t st_);
+int gbk_dist_fix_yy(int L, int w, double* y, void* st, double* part, double* out, int r0, int r1, cudaStream_t st_);
+int gbk_dist_pow_step(int L, int w, double* x, const double* y, void* st, const double* red, const double* out_yy, double* out_res, double* part, double tol, int r0, int r1, int stage, cudaStream_t st_);
+int gbk_dist_lz_update(int L, int w, const double* x, double* y, double* vp, void* st, const double* red, double* part, double* out, int r0, int r1, cudaStream_t st_);
+int gbk_dist_lz_commit(void* st, const double* red, const double* out, double* ab, cudaStream_t st_);
+int gbk_dist_lz_begin(void* st, int cap, cudaStream_t st_);
+int gbk_dist_dot(long long n, const double* a, const double* b, void* st, double* part, double* out, cudaStream_t st_);
+
 // gb_diag.cu
 int gbk_cell_energies(int n, const double* v, const double* coef, const double* host_e16,
                       double* out, cudaStream_t s);

@@ -451,10 +451,10 @@ __global__ void k_scale_box(int L, int nr, int w, const double* __restrict__ B,
 }
 
 __global__ void k_pad(int L, int nr, int w, const double* __restrict__ src,
-                      const double* __restrict__ scale, double* __restrict__ dst) {
-  const long long n = (long long)L * L * nr;
+                      const double* __restrict__ scale, double* __restrict__ dst, long long e0,
+                      long long e1) {
   const int Lpad = L + 2 * w;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+  for (long long r = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < e1;
        r += (long long)gridDim.x * blockDim.x) {
     const long long p = r / nr;
     const int c = (int)(r - p * nr);
@@ -464,10 +464,10 @@ __global__ void k_pad(int L, int nr, int w, const double* __restrict__ src,
 }
 
 __global__ void k_unpad(int L, int nr, int w, const double* __restrict__ src,
-                        const double* __restrict__ scale, double* __restrict__ dst) {
-  const long long n = (long long)L * L * nr;
+                        const double* __restrict__ scale, double* __restrict__ dst,
+                        long long e0, long long e1) {
   const int Lpad = L + 2 * w;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+  for (long long r = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < e1;
        r += (long long)gridDim.x * blockDim.x) {
     const long long p = r / nr;
     const int c = (int)(r - p * nr);
@@ -871,7 +871,9 @@ __global__ void __launch_bounds__(192) k_tbox_apply_tiled(int L, int w,
 // state is done is skipped.  Block arrival is counted on A's state.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void finish_reduction(KState* st, int mode, double a, double b) {
-  if (mode == 0) {
+  if (mode == 3) {  // raw partial sum of a row strip (gb_dist.cuh all-reduces it)
+    st->pAp = a;
+  } else if (mode == 0) {
     st->pAp = a;
     if (!(a > 0.0)) {
       st->breakdown = st->it + 1;
@@ -1094,13 +1096,14 @@ __device__ __forceinline__ long long bj_row_pad(int L, int w, int b, int l) {
 
 // inverse of each 12x12 diagonal block of S B S (Gauss-Jordan, one warp per block)
 __global__ void k_bj_setup(int L, int w, const double* __restrict__ B,
-                           const double* __restrict__ s, float* __restrict__ inv) {
+                           const double* __restrict__ s, float* __restrict__ inv, int blk0,
+                           int blk1) {
   __shared__ double M[8][12][25];
   __shared__ double colk[8][12];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int Lb = L >> 1, nb = Lb * Lb;
+  const int Lb = L >> 1;
   const int S = box_slots(w, 3);
-  for (int b = blockIdx.x * 8 + wl; b < nb; b += gridDim.x * 8) {
+  for (int b = blk0 + blockIdx.x * 8 + wl; b < blk1; b += gridDim.x * 8) {
     const int bs = b / Lb, bt = b - bs * Lb;
     double (*m)[25] = M[wl];
     for (int e = lane; e < 144; e += 32) {
@@ -1486,10 +1489,10 @@ __global__ void __launch_bounds__(192) k_bjcg_init(int L, int w, const double* _
 // ---------------------------------------------------------------------------
 // out[(p,c)] = s[(p,c)] * sum_a W[c][a] g[child_a(p)]   (s may be null)
 __global__ void k_apply_w(int Lp, WTemplate W, const double* __restrict__ g,
-                          const double* __restrict__ s, double* __restrict__ out) {
-  const long long P = (long long)Lp * Lp;
+                          const double* __restrict__ s, double* __restrict__ out,
+                          long long e0, long long e1) {
   const int Lk = 2 * Lp;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+  for (long long p = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < e1;
        p += (long long)gridDim.x * blockDim.x) {
     const int ps = (int)(p / Lp), pt = (int)(p % Lp);
     double gv[4];
@@ -1509,10 +1512,9 @@ __global__ void k_apply_w(int Lp, WTemplate W, const double* __restrict__ g,
 
 // v[child_a(p)] = sum_c W[c][a] w[(p,c)]   (W^T w, csc scatter order)
 __global__ void k_apply_wt(int Lp, WTemplate W, const double* __restrict__ w,
-                           double* __restrict__ v) {
-  const long long P = (long long)Lp * Lp;
+                           double* __restrict__ v, long long e0, long long e1) {
   const int Lk = 2 * Lp;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+  for (long long p = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < e1;
        p += (long long)gridDim.x * blockDim.x) {
     const int ps = (int)(p / Lp), pt = (int)(p % Lp);
     const double w0 = w[p * 3], w1 = w[p * 3 + 1], w2 = w[p * 3 + 2];
@@ -1529,11 +1531,11 @@ __global__ void k_apply_wt(int Lp, WTemplate W, const double* __restrict__ w,
 
 // g'[i] = sum over R row i in ascending column order (ds, alpha, dt, beta)
 __global__ void k_apply_r(int Lp, int rho, const double* __restrict__ R,
-                          const double* __restrict__ g, double* __restrict__ out) {
-  const long long P = (long long)Lp * Lp;
+                          const double* __restrict__ g, double* __restrict__ out,
+                          long long e0, long long e1) {
   const int W2 = 2 * rho + 1, Lk = 2 * Lp;
   const int S = W2 * W2 * 4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
+  for (long long i = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e1;
        i += (long long)gridDim.x * blockDim.x) {
     const int is = (int)(i / Lp), it = (int)(i % Lp);
     const double* row = R + i * S;
@@ -1559,13 +1561,13 @@ __global__ void k_apply_r(int Lp, int rho, const double* __restrict__ R,
 
 // inc[f] = sum_{j asc} psi[j][f] v[j]   (psi^T v, csc scatter order)
 __global__ void k_psi_t_apply(int n, int L, int lo, int wd, const double* __restrict__ psi,
-                              const double* __restrict__ v, double* __restrict__ inc) {
-  const long long N = (long long)n * n;
+                              const double* __restrict__ v, double* __restrict__ inc,
+                              int F0, int F1, int j_lo, int j_hi) {
   const int h = n / L;
   const int hi = lo + wd - 1;  // only meaningful when the window is unclipped
   const long long per = (long long)wd * wd;
-  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < N;
-       f += (long long)gridDim.x * blockDim.x) {
+  for (long long f = (long long)F0 * n + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       f < (long long)F1 * n; f += (long long)gridDim.x * blockDim.x) {
     const int fs = (int)(f / n), ft = (int)(f % n);
     // rows j whose window covers f; windows are monotone in j, use a safe range
     int j0s, j1s, j0t, j1t;
@@ -1575,6 +1577,8 @@ __global__ void k_psi_t_apply(int n, int L, int lo, int wd, const double* __rest
       j0s = imax(0, (fs - hi) / h - 1); j1s = imin(L - 1, (fs - lo) / h + 1);
       j0t = imax(0, (ft - hi) / h - 1); j1t = imin(L - 1, (ft - lo) / h + 1);
     }
+    j0s = imax(j0s, j_lo);
+    j1s = imin(j1s, j_hi - 1);
     double acc = 0.0;
     for (int js = j0s; js <= j1s; ++js) {
       const int ls = fs - clampi(js * h + lo, 0, n - wd);
@@ -1634,6 +1638,8 @@ __global__ void k_vadd(long long n, const double* __restrict__ a, const double* 
        i += (long long)gridDim.x * blockDim.x)
     out[i] = a[i] + b[i];
 }
+
+#include "gb_dist.cuh"
 
 }  // namespace gb
 
@@ -1721,12 +1727,28 @@ int gbk_scale_box(int L, int nr, int w, const double* B, const double* sv, doubl
 }
 int gbk_pad(int L, int nr, int w, const double* src, const double* scale, double* dst,
             cudaStream_t s) {
-  k_pad<<<grid_for((long long)L * L * nr, 256, 148 * 16), 256, 0, s>>>(L, nr, w, src, scale, dst);
+  return gbk_pad_rows(L, nr, w, src, scale, dst, 0, L, s);
+}
+int gbk_pad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst,
+                 int r0, int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > L || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)L * nr;
+  k_pad<<<grid_for((r1 - r0) * per, 256, 148 * 16), 256, 0, s>>>(L, nr, w, src, scale, dst,
+                                                                 r0 * per, r1 * per);
   return (int)cudaGetLastError();
 }
 int gbk_unpad(int L, int nr, int w, const double* src, const double* scale, double* dst,
               cudaStream_t s) {
-  k_unpad<<<grid_for((long long)L * L * nr, 256, 148 * 16), 256, 0, s>>>(L, nr, w, src, scale, dst);
+  return gbk_unpad_rows(L, nr, w, src, scale, dst, 0, L, s);
+}
+int gbk_unpad_rows(int L, int nr, int w, const double* src, const double* scale, double* dst,
+                   int r0, int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > L || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)L * nr;
+  k_unpad<<<grid_for((r1 - r0) * per, 256, 148 * 16), 256, 0, s>>>(L, nr, w, src, scale, dst,
+                                                                   r0 * per, r1 * per);
   return (int)cudaGetLastError();
 }
 static inline size_t off_smem(int nr, int w) {
@@ -1825,8 +1847,10 @@ int g_sym_ws_ctas = 0;  // gb_tune(3): CTA cap of the warp-specialized phase 1 (
 int g_sym_ws_on = 1;    // gb_tune(5): 0 = register-pipelined phase 1 (smaller CTAs)
 static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, double* y0,
                        KState* s0, double* p0, int r0, const double* x1, double* y1,
-                       KState* s1, double* p1, int r1, cudaStream_t s) {
-  const int nt = (int)symb_ntile(L);
+                       KState* s1, double* p1, int r1, cudaStream_t s, long long t0 = 0,
+                       long long t1 = -1) {
+  if (t1 < 0) t1 = symb_ntile(L);
+  const int nt = (int)(t1 - t0);
   // dynamic shared memory attribute raised to what a launch needs (the
   // kernels also have static shared memory, so the 227 KB cap is not usable)
   static size_t attr[2][3] = {{0, 0, 0}, {0, 0, 0}};
@@ -1848,10 +1872,10 @@ static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, 
     }
     if (nv == 2)
       k_symb_apply_ws<2><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1,
-                                                          s1, p1, r1);
+                                                          s1, p1, r1, t0, t1);
     else
       k_symb_apply_ws<1><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr,
-                                                          nullptr, nullptr, nullptr, 0);
+                                                          nullptr, nullptr, nullptr, 0, t0, t1);
     return;
   }
   const int gp = nt < kRedBlocks ? nt : kRedBlocks;
@@ -1864,10 +1888,11 @@ static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, 
     attr[0][nv] = sm;
   }
   if (nv == 2)
-    k_symb_apply<2><<<gp, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1, s1, p1, r1);
+    k_symb_apply<2><<<gp, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1, s1, p1, r1,
+                                                 t0, t1);
   else
     k_symb_apply<1><<<gp, kSymThreads, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr, nullptr,
-                                                 nullptr, nullptr, 0);
+                                                 nullptr, nullptr, 0, t0, t1);
 }
 // phase 2 alone (spill-over + reductions of mode m_v) for nv vectors
 static void sym_phase2(int L, int w, int nv, const double* x0, double* y0, KState* s0,
@@ -1946,8 +1971,15 @@ int gbk_tbox_apply(int L, int nr, int w, const double* BsT, const double* x, dou
 // ---- block-Jacobi PCG launchers ----
 int gbk_bj_setup(int L, int w, const double* B, const double* sv, float* inv,
                  cudaStream_t s) {
-  const int nb = (L / 2) * (L / 2);
-  k_bj_setup<<<grid_for(nb, 8, 148 * 16), 256, 0, s>>>(L, w, B, sv, inv);
+  return gbk_bj_setup_rows(L, w, B, sv, inv, 0, L, s);
+}
+// the 2x2-parent blocks of grid rows [r0, r1) (both even)
+int gbk_bj_setup_rows(int L, int w, const double* B, const double* sv, float* inv, int r0,
+                      int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > L || r0 > r1 || (r0 & 1) || (r1 & 1)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const int Lb = L / 2, b0 = (r0 / 2) * Lb, b1 = (r1 / 2) * Lb;
+  k_bj_setup<<<grid_for(b1 - b0, 8, 148 * 16), 256, 0, s>>>(L, w, B, sv, inv, b0, b1);
   return (int)cudaGetLastError();
 }
 static inline int bj_grid(int L) {
@@ -2016,28 +2048,54 @@ int gbk_box_apply(int L, int nr, int w, const double* B, const double* sv, int m
 
 int gbk_apply_w(int Lp, const double* w12, const double* g, const double* sv, double* out,
                 cudaStream_t s) {
-  const long long P = (long long)Lp * Lp;
-  k_apply_w<<<grid_for(P, 256, 148 * 16), 256, 0, s>>>(Lp, mkW(w12), g, sv, out);
+  return gbk_apply_w_rows(Lp, w12, g, sv, out, 0, Lp, s);
+}
+int gbk_apply_w_rows(int Lp, const double* w12, const double* g, const double* sv, double* out,
+                     int r0, int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > Lp || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  k_apply_w<<<grid_for((long long)(r1 - r0) * Lp, 256, 148 * 16), 256, 0, s>>>(
+      Lp, mkW(w12), g, sv, out, (long long)r0 * Lp, (long long)r1 * Lp);
   return (int)cudaGetLastError();
 }
 
 int gbk_apply_wt(int Lp, const double* w12, const double* w, double* v, cudaStream_t s) {
-  const long long P = (long long)Lp * Lp;
-  k_apply_wt<<<grid_for(P, 256, 148 * 16), 256, 0, s>>>(Lp, mkW(w12), w, v);
+  return gbk_apply_wt_rows(Lp, w12, w, v, 0, Lp, s);
+}
+int gbk_apply_wt_rows(int Lp, const double* w12, const double* w, double* v, int r0, int r1,
+                      cudaStream_t s) {
+  if (r0 < 0 || r1 > Lp || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  k_apply_wt<<<grid_for((long long)(r1 - r0) * Lp, 256, 148 * 16), 256, 0, s>>>(
+      Lp, mkW(w12), w, v, (long long)r0 * Lp, (long long)r1 * Lp);
   return (int)cudaGetLastError();
 }
 
 int gbk_apply_r(int Lp, int rho, const double* R, const double* g, double* out,
                 cudaStream_t s) {
-  const long long P = (long long)Lp * Lp;
-  k_apply_r<<<grid_for(P, 128, 148 * 16), 128, 0, s>>>(Lp, rho, R, g, out);
+  return gbk_apply_r_rows(Lp, rho, R, g, out, 0, Lp, s);
+}
+int gbk_apply_r_rows(int Lp, int rho, const double* R, const double* g, double* out, int r0,
+                     int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > Lp || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  k_apply_r<<<grid_for((long long)(r1 - r0) * Lp, 128, 148 * 16), 128, 0, s>>>(
+      Lp, rho, R, g, out, (long long)r0 * Lp, (long long)r1 * Lp);
   return (int)cudaGetLastError();
 }
 
 int gbk_psi_t_apply(int n, int L, int lo, int wd, const double* psi, const double* v,
                     double* inc, cudaStream_t s) {
-  const long long N = (long long)n * n;
-  k_psi_t_apply<<<grid_for(N, 128, 148 * 32), 128, 0, s>>>(n, L, lo, wd, psi, v, inc);
+  return gbk_psi_t_apply_rows(n, L, lo, wd, psi, v, inc, 0, n, 0, L, s);
+}
+// fine rows [F0, F1) of inc from the psi rows in grid rows [j_lo, j_hi) only
+// (a rank's partial increment; the whole level is (0, n, 0, L))
+int gbk_psi_t_apply_rows(int n, int L, int lo, int wd, const double* psi, const double* v,
+                         double* inc, int F0, int F1, int j_lo, int j_hi, cudaStream_t s) {
+  if (F0 < 0 || F1 > n || F0 > F1 || j_lo < 0 || j_hi > L || j_lo > j_hi) return GB_UNSUPPORTED;
+  if (F0 == F1) return 0;
+  k_psi_t_apply<<<grid_for((long long)(F1 - F0) * n, 128, 148 * 32), 128, 0, s>>>(
+      n, L, lo, wd, psi, v, inc, F0, F1, j_lo, j_hi);
   return (int)cudaGetLastError();
 }
 
@@ -2241,8 +2299,17 @@ size_t gbk_sym_overflow_elems(int L, int w) {
 int gbk_sym_supported(int L, int nr, int w) { return use_sym(1, L, nr, w) ? 1 : 0; }
 int gbk_scale_box_symT(int L, int w, const double* B, const double* sv, double* UsT,
                        cudaStream_t s) {
-  const long long total = (long long)gbk_boxsym_elems(L, w);
-  k_scale_box_symb<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(L, w, B, sv, UsT);
+  return gbk_scale_box_symT_rows(L, w, B, sv, UsT, 0, L, s);
+}
+// grid rows [r0, r1) of the symmetric band copy (rows are whole 32-parent
+// blocks: L % 64 == 0); reads s within w rows below the strip
+int gbk_scale_box_symT_rows(int L, int w, const double* B, const double* sv, double* UsT,
+                            int r0, int r1, cudaStream_t s) {
+  if (r0 < 0 || r1 > L || r0 > r1 || L % 32) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)L * symb_ns(w);
+  k_scale_box_symb<<<grid_for((r1 - r0) * per, 256, 148 * 16), 256, 0, s>>>(
+      L, w, B, sv, UsT, r0 * per, r1 * per);
   return (int)cudaGetLastError();
 }
 
@@ -2905,4 +2972,114 @@ static int inverse_iteration(gb_level_engine_args* e, cudaStream_t s, long long&
     lam_prev = lam;
   }
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Row-strip Krylov launchers (gb_dist.cuh): rank-local pieces of the
+// distributed block-Jacobi PCG / power iteration / Lanczos recurrence on the
+// grid rows [r0, r1) of a tiled level.  The caller (gamblet_dist.py) exchanges
+// halos and all-reduces the partial sums between them.
+// ---------------------------------------------------------------------------
+static inline bool dist_rows_ok(int L, int r0, int r1) {
+  return r0 >= 0 && r1 <= L && r0 < r1 && r0 % kSymTH == 0 && r1 % kSymTH == 0 &&
+         L % kSymTW == 0;
+}
+static inline int dist_bj_grid(int nblk) { return grid_for(nblk, 16, kRedBlocks); }
+
+// phase 1 of y_v = (S B S) x_v on the strip's tiles for nv = 1, 2 vectors with
+// the strip partials of x_v . (A x_v) formed by linearity -> red[0], red[1]
+int gbk_dist_apply(int L, int w, const double* U, int nv, const double* x0, double* y0,
+                   void* st0, double* part0, const double* x1, double* y1, void* st1,
+                   double* part1, double* red, int r0, int r1, cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1) || (nv != 1 && nv != 2)) return GB_UNSUPPORTED;
+  const long long tpr = L / kSymTW;
+  sym_phase1(L, w, U, nv, x0, y0, (KState*)st0, part0, 2, x1, y1, (KState*)st1, part1, 2, s,
+             (r0 / kSymTH) * tpr, (r1 / kSymTH) * tpr);
+  k_dist_pack<<<1, 1, 0, s>>>((KState*)st0, nv == 2 ? (KState*)st1 : nullptr, red);
+  return (int)cudaGetLastError();
+}
+
+int gbk_dist_pcg_init(int L, int w, const double* b, double* x, double* r, double* p, double* z,
+                      const float* inv, void* st, double* part, double* out, int r0, int r1,
+                      cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1)) return GB_UNSUPPORTED;
+  const int Lb = L / 2, b0 = (r0 / 2) * Lb, b1 = (r1 / 2) * Lb;
+  k_dist_pcg_init<<<dist_bj_grid(b1 - b0), 192, 0, s>>>(L, w, b, x, r, p, z, inv, (KState*)st,
+                                                        part, out, b0, b1);
+  return (int)cudaGetLastError();
+}
+int gbk_dist_pcg_init_commit(void* st, const double* out, double rel_tol, int max_iter,
+                             cudaStream_t s) {
+  k_dist_pcg_init_commit<<<1, 1, 0, s>>>((KState*)st, out, rel_tol, max_iter);
+  return (int)cudaGetLastError();
+}
+int gbk_dist_pcg_update(int L, int w, double* x, double* r, const double* p, const double* Ap,
+                        double* z, const float* inv, void* st, const double* red, double* part,
+                        double* out, int r0, int r1, cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1)) return GB_UNSUPPORTED;
+  const int Lb = L / 2, b0 = (r0 / 2) * Lb, b1 = (r1 / 2) * Lb;
+  k_dist_pcg_update<<<dist_bj_grid(b1 - b0), 192, 0, s>>>(L, w, x, r, p, Ap, z, inv, (KState*)st,
+                                                          red, part, out, b0, b1);
+  return (int)cudaGetLastError();
+}
+// all-reduced sums -> state, then p = z + beta p on the strip
+int gbk_dist_pcg_commit_dir(int L, int w, void* st, const double* red, const double* out,
+                            const double* z, double* p, int r0, int r1, cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1)) return GB_UNSUPPORTED;
+  const long long Lpad = L + 2 * w, off = (long long)(r0 + w) * Lpad * 3,
+                  n = (long long)(r1 - r0) * Lpad * 3;
+  k_dist_pcg_commit<<<1, 1, 0, s>>>((KState*)st, red, out);
+  k_cg_dir<<<grid_for(n, 256, kRedBlocks), 256, 0, s>>>(n, z + off, p + off, (KState*)st);
+  return (int)cudaGetLastError();
+}
+int gbk_dist_fix_yy(int L, int w, double* y, void* st, double* part, double* out, int r0, int r1,
+                    cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1)) return GB_UNSUPPORTED;
+  const long long n = (long long)(r1 - r0) * L * 3;
+  k_dist_fix_yy<<<grid_for(n, 256, kRedBlocks), 256, 0, s>>>(L, w, y, (KState*)st, part, out, r0,
+                                                            r1);
+  return (int)cudaGetLastError();
+}
+// power iteration between the reductions: stage 0 (x.y and y.y all-reduced)
+// sets lam, ynorm and forms the residual partial; stage 1 (residual
+// all-reduced) tests convergence and rescales x = y / ynorm on the strip
+int gbk_dist_pow_step(int L, int w, double* x, const double* y, void* st, const double* red,
+                      const double* out_yy, double* out_res, double* part, double tol, int r0,
+                      int r1, int stage, cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1)) return GB_UNSUPPORTED;
+  const long long Lpad = L + 2 * w, off = (long long)(r0 + w) * Lpad * 3,
+                  n = (long long)(r1 - r0) * Lpad * 3;
+  const int g = grid_for(n, 256, kRedBlocks);
+  if (stage == 0) {
+    k_dist_pow_commit1<<<1, 1, 0, s>>>((KState*)st, red, out_yy);
+    k_dist_pow_res<<<g, 256, 0, s>>>(n, x + off, y + off, (KState*)st, part, out_res);
+  } else {
+    k_dist_pow_commit2<<<1, 1, 0, s>>>((KState*)st, out_res, tol);
+    k_pow_scale<<<g, 256, 0, s>>>(n, x + off, y + off, (KState*)st);
+  }
+  return (int)cudaGetLastError();
+}
+int gbk_dist_lz_update(int L, int w, const double* x, double* y, double* vp, void* st,
+                       const double* red, double* part, double* out, int r0, int r1,
+                       cudaStream_t s) {
+  if (!dist_rows_ok(L, r0, r1)) return GB_UNSUPPORTED;
+  const long long n = (long long)(r1 - r0) * L * 3;
+  k_dist_lz_update<<<grid_for(n, 256, kRedBlocks), 256, 0, s>>>(L, w, x, y, vp, (KState*)st, red,
+                                                               part, out, r0, r1);
+  return (int)cudaGetLastError();
+}
+int gbk_dist_lz_commit(void* st, const double* red, const double* out, double* ab,
+                       cudaStream_t s) {
+  k_dist_lz_commit<<<1, 1, 0, s>>>((KState*)st, red, out, ab);
+  return (int)cudaGetLastError();
+}
+int gbk_dist_lz_begin(void* st, int cap, cudaStream_t s) {
+  k_state_reset<<<1, 1, 0, s>>>((KState*)st, cap);
+  k_lz_init<<<1, 1, 0, s>>>((KState*)st);
+  return (int)cudaGetLastError();
+}
+int gbk_dist_dot(long long n, const double* a, const double* b, void* st, double* part,
+                 double* out, cudaStream_t s) {
+  k_dist_dot<<<grid_for(n, 256, kRedBlocks), 256, 0, s>>>(n, a, b, (KState*)st, part, out);
+  return (int)cudaGetLastError();
 }

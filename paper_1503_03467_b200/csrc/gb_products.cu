@@ -32,11 +32,10 @@ struct PsiWin {
 // ---------------------------------------------------------------------------
 __global__ void k_psi_stencil(PsiWin pw, int rho, const double* __restrict__ psi,
                               int wA, const double* __restrict__ A, int wX,
-                              double* __restrict__ X) {
+                              double* __restrict__ X, long long e0, long long e1) {
   const int n = pw.n;
   const int SX = box_slots(wX, 1), SA = box_slots(wA, 1);
-  const long long total = (long long)n * n * SX;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / SX;
     const int sl = (int)(e - i * SX);
@@ -67,11 +66,10 @@ __global__ void k_psi_stencil(PsiWin pw, int rho, const double* __restrict__ psi
 // K2b: raw[i][j] = sum_m X[i][m] psi[j][m], box half-width wR = wX + rho
 __global__ void k_psi_galerkin(PsiWin pw, int rho, const double* __restrict__ psi,
                                int wX, const double* __restrict__ X, int wR,
-                               double* __restrict__ raw) {
+                               double* __restrict__ raw, long long e0, long long e1) {
   const int n = pw.n;
   const int SX = box_slots(wX, 1), SR = box_slots(wR, 1);
-  const long long total = (long long)n * n * SR;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / SR;
     const int sl = (int)(e - i * SR);
@@ -109,7 +107,7 @@ __global__ void k_psi_galerkin(PsiWin pw, int rho, const double* __restrict__ ps
 // output block is staged in shared memory and written contiguously.
 // ---------------------------------------------------------------------------
 __global__ void k_transpose_f64(long long R, int C, const double* __restrict__ in,
-                                double* __restrict__ out) {
+                                double* __restrict__ out, long long ldo) {
   __shared__ double t[32][33];
   const long long r0 = (long long)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
@@ -122,7 +120,7 @@ __global__ void k_transpose_f64(long long R, int C, const double* __restrict__ i
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int c = c0 + k;
     const long long r = r0 + threadIdx.x;
-    if (r < R && c < C) out[(long long)c * R + r] = t[threadIdx.x][k];
+    if (r < R && c < C) out[(long long)c * ldo + r] = t[threadIdx.x][k];
   }
 }
 
@@ -131,14 +129,16 @@ constexpr int GT_THREADS = 256;
 __global__ void __launch_bounds__(GT_THREADS) k_psi_galerkin_t(PsiWin pw, int rho,
                                                                const double* __restrict__ psiT,
                                                                int wX, const double* __restrict__ XT,
-                                                               int wR, double* __restrict__ raw) {
+                                                               int wR, double* __restrict__ raw,
+                                                               int s0, int s1) {
   extern __shared__ double ob[];  // 32 x SR
   const int n = pw.n;
   const long long N = (long long)n * n;
   const int SR = box_slots(wR, 1), WR = 2 * wR + 1, WX = 2 * wX + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ncb = (n + 31) / 32;
-  for (long long cta = blockIdx.x; cta < (long long)n * ncb; cta += gridDim.x) {
+  for (long long cta = (long long)s0 * ncb + blockIdx.x; cta < (long long)s1 * ncb;
+       cta += gridDim.x) {
     const int si = (int)(cta / ncb), ti0 = (int)(cta - (long long)si * ncb) * 32;
     const int ti = ti0 + lane;
     const bool live = ti < n;
@@ -244,11 +244,10 @@ __device__ __forceinline__ void block_products(const WTemplate& W, const Blk& t,
 
 __global__ void k_level_diag(int Lk, int wA, const double* __restrict__ A,
                              WTemplate W, double* __restrict__ bdiag,
-                             double* __restrict__ dmin) {
+                             double* __restrict__ dmin, long long e0, long long e1) {
   const int Lp = Lk / 2;
-  const long long P = (long long)Lp * Lp;
   double m = __longlong_as_double(0x7ff0000000000000ll);
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+  for (long long p = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < e1;
        p += (long long)gridDim.x * blockDim.x) {
     const int ps = (int)(p / Lp), pt = (int)(p % Lp);
     Blk t;
@@ -282,14 +281,13 @@ __global__ void k_level_blocks(int Lk, int wA, const double* __restrict__ A,
                                const double* __restrict__ dmin,
                                double* __restrict__ B, double* __restrict__ G,
                                double* __restrict__ PAPt,
-                               double* __restrict__ stats) {
+                               double* __restrict__ stats, long long e0, long long e1) {
   const int Lp = Lk / 2;
   const int W2 = 2 * wB + 1, NB = W2 * W2;
-  const long long total = (long long)Lp * Lp * NB;
   const bool do_drop = *dmin > 0.0;
   const int SB = NB * 9 / 3;  // slots per B row: NB * 3
   double mdiff = 0.0, mabs = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long p = e / NB;
     const int bs = (int)(e - p * NB);
@@ -353,10 +351,10 @@ __global__ void k_level_blocks(int Lk, int wA, const double* __restrict__ A,
 // K6: R = 0.25 P + Dt W.  R box on the parent grid, nc = 4 children, w = rho.
 // ---------------------------------------------------------------------------
 __global__ void k_restriction(int Lp, int rho, const double* __restrict__ Dt,
-                              WTemplate W, double* __restrict__ R) {
+                              WTemplate W, double* __restrict__ R, long long e0,
+                              long long e1) {
   const int W2 = 2 * rho + 1, NB = W2 * W2;
-  const long long total = (long long)Lp * Lp * NB;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / NB;
     const int bs = (int)(e - i * NB);
@@ -384,10 +382,10 @@ __global__ void k_restriction(int Lp, int rho, const double* __restrict__ Dt,
 
 // BD[(p,c)][j] = sum_{r' asc} B[(p,c)][r'] * Dt[j][(p'-j, c')],  w = wB + rho
 __global__ void k_bd(int Lp, int wB, const double* __restrict__ B, int rho,
-                     const double* __restrict__ Dt, int wBD, double* __restrict__ BD) {
+                     const double* __restrict__ Dt, int wBD, double* __restrict__ BD,
+                     long long e0, long long e1) {
   const int SB = box_slots(wB, 3), SD = box_slots(rho, 3), SBD = box_slots(wBD, 1);
-  const long long total = (long long)Lp * Lp * 3 * SBD;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long r = e / SBD;
     const int sl = (int)(e - r * SBD);
@@ -418,10 +416,10 @@ __global__ void k_bd(int Lp, int wB, const double* __restrict__ B, int rho,
 
 // GtD[i][j] = sum_{r asc} G[r][i] * Dt[j][r],  box nr=nc=1, w = wG + rho
 __global__ void k_gtd(int Lp, int wG, const double* __restrict__ G, int rho,
-                      const double* __restrict__ Dt, int wGD, double* __restrict__ GtD) {
+                      const double* __restrict__ Dt, int wGD, double* __restrict__ GtD,
+                      long long e0, long long e1) {
   const int SG = box_slots(wG, 1), SD = box_slots(rho, 3), SO = box_slots(wGD, 1);
-  const long long total = (long long)Lp * Lp * SO;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / SO;
     const int sl = (int)(e - i * SO);
@@ -455,11 +453,10 @@ __global__ void k_coarse_raw(int Lp, int wB, const double* __restrict__ PAPt,
                              int wGD, const double* __restrict__ GtD, int rho,
                              const double* __restrict__ Dt, int wBD,
                              const double* __restrict__ BD, int wA2,
-                             double* __restrict__ raw) {
+                             double* __restrict__ raw, long long e0, long long e1) {
   const int SP = box_slots(wB, 1), SGD = box_slots(wGD, 1), SD = box_slots(rho, 3),
             SBD = box_slots(wBD, 1), SO = box_slots(wA2, 1);
-  const long long total = (long long)Lp * Lp * SO;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / SO;
     const int sl = (int)(e - i * SO);
@@ -506,18 +503,20 @@ __global__ void k_coarse_raw(int Lp, int wB, const double* __restrict__ PAPt,
 // with parent spacing 2h.
 // ---------------------------------------------------------------------------
 __global__ void k_wpsi(PsiWin child, WTemplate W, const double* __restrict__ psi,
-                       PsiWin par, double* __restrict__ Wpsi) {
-  // par.L = child.L / 2, par.lo = child.lo, par.wd = wdw
+                       PsiWin par, double* __restrict__ Wpsi, long long e0, long long e1,
+                       int f0, int f1) {
+  // par.L = child.L / 2, par.lo = child.lo, par.wd = wdw; only window points
+  // whose fine row lies in [f0, f1) are computed (column strips of psi)
   const int Lp = par.L;
   const long long per = (long long)par.wd * par.wd;
-  const long long total = (long long)Lp * Lp * per;
   const long long cper = (long long)child.wd * child.wd;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long p = e / per;
     const int f = (int)(e - p * per);
     const int ps = (int)(p / Lp), pt = (int)(p % Lp);
     const int fs = par.origin(ps) + f / par.wd, ft = par.origin(pt) + f % par.wd;
+    if (fs < f0 || fs >= f1) continue;
     double cv[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -546,7 +545,7 @@ __global__ void k_psi_next(PsiWin child, const double* __restrict__ psi,
                            double* __restrict__ psi_next) {
   const int Lp = out.L;
   const long long per = (long long)out.wd * out.wd;
-  const long long total = (long long)Lp * Lp * per;
+  const long long total = (long long)Lp * Lp * per;  // (whole level only)
   const long long cper = (long long)child.wd * child.wd;
   const long long wper = (long long)par.wd * par.wd;
   const int SD = box_slots(rho, 3);
@@ -625,7 +624,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
                                                       int rho, const double* __restrict__ Dt,
                                                       PsiWin out, double* __restrict__ psi_next,
                                                       double* __restrict__ rowmax, int TB, int nfs,
-                                                      int nft, int r0, int r1) {
+                                                      int nft, int r0, int r1, int f0, int f1) {
   // double-buffered: chunk c + 1 is gathered into registers while chunk c
   // is multiplied (the gathers are L2-latency bound)
   __shared__ double As[2][16 * PN_LDA];
@@ -660,6 +659,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     const int ut0 = out.origin(bi_t), ut1 = out.origin(bi_t + nrt - 1) + out.wd - 1;
     const int F0s = us0 + (tt / nft) * 8, F0t = ut0 + (tt % nft) * 4;
     if (F0s > us1 || F0t > ut1) continue;  // (uniform across the CTA)
+    if (F0s + 7 < f0 || F0s >= f1) continue;  // no fine row of the column strip [f0, f1)
     // parents in some ball whose Wpsi support [2ph+lo, 2ph+h+hi] meets F
     int ps0 = imax(bi_s - rho, 0), ps1 = imin(bi_s + nrs - 1 + rho, Lp - 1);
     int pt0 = imax(bi_t - rho, 0), pt1 = imin(bi_t + nrt - 1 + rho, Lp - 1);
@@ -773,6 +773,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
           const int fs = F0s + (n >> 2), ft = F0t + (n & 3);
           const int ls = fs - os, lt = ft - ot;
           if (ls < 0 || ls >= out.wd || lt < 0 || lt >= out.wd) continue;
+          if (fs < f0 || fs >= f1) continue;
           double pv = 0.0;
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
@@ -818,6 +819,29 @@ __global__ void k_drop_by_rowmax(long long rows, long long S, double* __restrict
   for (long long b = blockIdx.x; b < rows * nch; b += gridDim.x) {
     const long long r = b / nch, j0 = (b - r * nch) * RT_CHUNK;
     const long long j1 = j0 + RT_CHUNK < S ? j0 + RT_CHUNK : S;
+    const double thr = 1e-11 * rowmax[r];
+    for (long long j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      const double x = v[r * S + j];
+      if (!(fabs(x) >= thr)) v[r * S + j] = 0.0;
+    }
+  }
+}
+
+// the same drop restricted to the window rows whose fine row lies in
+// [f0, f1) (column strips of psi: the other window rows belong to other ranks)
+__global__ void k_drop_by_rowmax_cols(PsiWin out, long long row0, long long rows,
+                                      double* __restrict__ v, const double* __restrict__ rowmax,
+                                      int f0, int f1) {
+  const long long S = (long long)out.wd * out.wd;
+  const long long nch = (S + RT_CHUNK - 1) / RT_CHUNK;
+  for (long long b = blockIdx.x; b < rows * nch; b += gridDim.x) {
+    const long long r = row0 + b / nch;
+    const int os = out.origin((int)(r / out.L));
+    const long long ja = (long long)imax(f0 - os, 0) * out.wd;
+    const long long jb = (long long)imin(f1 - os, out.wd) * out.wd;
+    long long j0 = (b % nch) * RT_CHUNK, j1 = j0 + RT_CHUNK < S ? j0 + RT_CHUNK : S;
+    j0 = j0 > ja ? j0 : ja;
+    j1 = j1 < jb ? j1 : jb;
     const double thr = 1e-11 * rowmax[r];
     for (long long j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
       const double x = v[r * S + j];
@@ -973,67 +997,118 @@ static inline WTemplate mkW(const double* w12) {
   return W;
 }
 
+// Row-range launchers (multi-GPU strips, partition.py): [r0, r1) are grid rows
+// of the OUTPUT's row grid; only those rows are written, inputs are read at
+// global indices (the caller provides the halo rows).  The whole-level entry
+// points are the [0, L) instances, so a partition's strips reproduce the whole
+// level bitwise.
+static inline bool bad_rows(int r0, int r1, int L) { return r0 < 0 || r1 > L || r0 > r1; }
+
+int gbk_psi_stencil_rows(int n, int lo, int wd, int rho, const double* psi, int wA,
+                         const double* A, int wX, double* X, int r0, int r1, cudaStream_t s) {
+  if (bad_rows(r0, r1, n)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  PsiWin pw{n, n, lo, wd, -lo};
+  const long long per = (long long)n * box_slots(wX, 1);
+  k_psi_stencil<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(pw, rho, psi, wA, A, wX, X,
+                                                              r0 * per, r1 * per);
+  return (int)cudaGetLastError();
+}
 int gbk_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                     const double* A, int wX, double* X, cudaStream_t s) {
-  PsiWin pw{n, n, lo, wd, -lo};
-  const long long total = (long long)n * n * box_slots(wX, 1);
-  k_psi_stencil<<<grid_for(total, 256), 256, 0, s>>>(pw, rho, psi, wA, A, wX, X);
-  return (int)cudaGetLastError();
+  return gbk_psi_stencil_rows(n, lo, wd, rho, psi, wA, A, wX, X, 0, n, s);
 }
 
 size_t gbk_psi_galerkin_workspace(int n, int wd, int wX) {
   return (size_t)n * n * ((size_t)wd * wd + (size_t)box_slots(wX, 1)) * sizeof(double);
 }
 
-int gbk_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,
-                       const double* X, int wR, double* raw, double* work, cudaStream_t s) {
+// fine rows [r0, r1) of raw: psi rows within wR of the strip and the strip's X
+// rows are transposed into their global plane-major positions of `work`
+int gbk_psi_galerkin_t_rows(int n, int lo, int wd, int rho, const double* psi, int wX,
+                            const double* X, int wR, double* raw, double* work, int r0, int r1,
+                            cudaStream_t s) {
+  if (bad_rows(r0, r1, n)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
   PsiWin pw{n, n, lo, wd, -lo};
   const long long N = (long long)n * n;
   const int SX = box_slots(wX, 1), SR = box_slots(wR, 1);
   double* psiT = work;
   double* XT = work + N * wd * wd;
   const dim3 tb(32, 8);
-  k_transpose_f64<<<dim3((unsigned)((N + 31) / 32), (wd * wd + 31) / 32), tb, 0, s>>>(
-      N, wd * wd, psi, psiT);
-  k_transpose_f64<<<dim3((unsigned)((N + 31) / 32), (SX + 31) / 32), tb, 0, s>>>(N, SX, X, XT);
+  const int h0 = imax(r0 - wR, 0), h1 = imin(r1 + wR, n);
+  const long long pa = (long long)h0 * n, pn = (long long)(h1 - h0) * n;
+  k_transpose_f64<<<dim3((unsigned)((pn + 31) / 32), (wd * wd + 31) / 32), tb, 0, s>>>(
+      pn, wd * wd, psi + pa * wd * wd, psiT + pa, N);
+  const long long xa = (long long)r0 * n, xn = (long long)(r1 - r0) * n;
+  k_transpose_f64<<<dim3((unsigned)((xn + 31) / 32), (SX + 31) / 32), tb, 0, s>>>(
+      xn, SX, X + xa * SX, XT + xa, N);
   const size_t smem = (size_t)32 * SR * sizeof(double);
-  if (smem > 200 * 1024) return 1;
-  cudaFuncSetAttribute(k_psi_galerkin_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const long long nct = (long long)n * ((n + 31) / 32);
+  if (smem > 200 * 1024) return GB_UNSUPPORTED;
+  cudaError_t e = cudaFuncSetAttribute(k_psi_galerkin_t,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  const long long nct = (long long)(r1 - r0) * ((n + 31) / 32);
   const int g = (int)(nct < 148LL * 8 ? nct : 148LL * 8);
-  k_psi_galerkin_t<<<g, GT_THREADS, smem, s>>>(pw, rho, psiT, wX, XT, wR, raw);
+  k_psi_galerkin_t<<<g, GT_THREADS, smem, s>>>(pw, rho, psiT, wX, XT, wR, raw, r0, r1);
   return (int)cudaGetLastError();
+}
+int gbk_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,
+                       const double* X, int wR, double* raw, double* work, cudaStream_t s) {
+  return gbk_psi_galerkin_t_rows(n, lo, wd, rho, psi, wX, X, wR, raw, work, 0, n, s);
 }
 
 int gbk_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,
                      const double* X, int wR, double* raw, cudaStream_t s) {
   PsiWin pw{n, n, lo, wd, -lo};
   const long long total = (long long)n * n * box_slots(wR, 1);
-  k_psi_galerkin<<<grid_for(total, 256), 256, 0, s>>>(pw, rho, psi, wX, X, wR, raw);
+  k_psi_galerkin<<<grid_for(total, 256), 256, 0, s>>>(pw, rho, psi, wX, X, wR, raw, 0, total);
   return (int)cudaGetLastError();
 }
 
+int gbk_level_diag_rows(int Lk, int wA, const double* A, const double* w12, double* bdiag,
+                        double* dmin, int r0, int r1, cudaStream_t s) {
+  const int Lp = Lk / 2;
+  if (bad_rows(r0, r1, Lp)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  k_level_diag<<<grid_for((long long)(r1 - r0) * Lp, 128), 128, 0, s>>>(
+      Lk, wA, A, mkW(w12), bdiag, dmin, (long long)r0 * Lp, (long long)r1 * Lp);
+  return (int)cudaGetLastError();
+}
 int gbk_level_diag(int Lk, int wA, const double* A, const double* w12,
                    double* bdiag, double* dmin, cudaStream_t s) {
-  const long long P = (long long)(Lk / 2) * (Lk / 2);
-  k_level_diag<<<grid_for(P, 128), 128, 0, s>>>(Lk, wA, A, mkW(w12), bdiag, dmin);
-  return (int)cudaGetLastError();
+  return gbk_level_diag_rows(Lk, wA, A, w12, bdiag, dmin, 0, Lk / 2, s);
 }
 
+int gbk_level_blocks_rows(int Lk, int wA, const double* A, const double* w12, int wB,
+                          const double* bdiag, const double* dmin, double* B, double* G,
+                          double* PAPt, double* stats, int r0, int r1, cudaStream_t s) {
+  const int Lp = Lk / 2;
+  if (bad_rows(r0, r1, Lp)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)Lp * box_slots(wB, 1);
+  k_level_blocks<<<grid_for((r1 - r0) * per, 128), 128, 0, s>>>(
+      Lk, wA, A, mkW(w12), wB, bdiag, dmin, B, G, PAPt, stats, r0 * per, r1 * per);
+  return (int)cudaGetLastError();
+}
 int gbk_level_blocks(int Lk, int wA, const double* A, const double* w12, int wB,
                      const double* bdiag, const double* dmin, double* B, double* G,
                      double* PAPt, double* stats, cudaStream_t s) {
-  const long long total = (long long)(Lk / 2) * (Lk / 2) * box_slots(wB, 1);
-  k_level_blocks<<<grid_for(total, 128), 128, 0, s>>>(Lk, wA, A, mkW(w12), wB, bdiag,
-                                                      dmin, B, G, PAPt, stats);
-  return (int)cudaGetLastError();
+  return gbk_level_blocks_rows(Lk, wA, A, w12, wB, bdiag, dmin, B, G, PAPt, stats, 0, Lk / 2, s);
 }
 
+int gbk_restriction_rows(int Lp, int rho, const double* Dt, const double* w12, double* R,
+                         int r0, int r1, cudaStream_t s) {
+  if (bad_rows(r0, r1, Lp)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)Lp * box_slots(rho, 1);
+  k_restriction<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(Lp, rho, Dt, mkW(w12), R,
+                                                              r0 * per, r1 * per);
+  return (int)cudaGetLastError();
+}
 int gbk_restriction(int Lp, int rho, const double* Dt, const double* w12, double* R,
                     cudaStream_t s) {
-  const long long total = (long long)Lp * Lp * box_slots(rho, 1);
-  k_restriction<<<grid_for(total, 256), 256, 0, s>>>(Lp, rho, Dt, mkW(w12), R);
-  return (int)cudaGetLastError();
+  return gbk_restriction_rows(Lp, rho, Dt, w12, R, 0, Lp, s);
 }
 
 // Tile loops are oversubscribed (48 CTAs per SM, grid-stride): the short
@@ -1044,89 +1119,139 @@ template <class Kern>
 static int resident_grid(Kern, int, long long ntiles) {
   return (int)(ntiles < 148LL * 48 ? ntiles : 148LL * 48);
 }
-static long long box_gemm_tiles(int Lp, int TB, int wOut) {
+// tiles of the row blocks [rb0, rb1) of the TB x TB blocking
+static long long box_gemm_tiles(int Lp, int TB, int wOut, int rb0, int rb1) {
   const long long nb = (Lp + TB - 1) / TB, side = 2 * ((wOut + TB - 1) / TB) + 1;
-  return nb * nb * side * side;
+  return (long long)(rb1 - rb0) * nb * side * side;
+}
+// the tensor-core tile kernels own whole TB-row blocks: a strip must start and
+// end on a block boundary (or the grid edge)
+static inline bool rows_block_aligned(int r0, int r1, int Lp, int TB) {
+  return r0 % TB == 0 && (r1 % TB == 0 || r1 == Lp);
 }
 
+int gbk_bd_rows(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
+                double* BD, int r0, int r1, cudaStream_t s) {
+  if (bad_rows(r0, r1, Lp)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)Lp * 3 * box_slots(wBD, 1);
+  const int TB = Lp < 4 ? Lp : 4;
+  if (products_use_mma && rows_block_aligned(r0, r1, Lp, TB)) {
+    cudaError_t e = cudaMemsetAsync(BD + r0 * per, 0, (r1 - r0) * per * sizeof(double), s);
+    if (e != cudaSuccess) return (int)e;
+    const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
+    auto kern = k_box_gemm<3, OpBrows, OpDtRowsB, StoreBox>;
+    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wBD, rb0, rb1)), 128, 0, s>>>(
+        Lp, TB, wB, rho, wBD, OpBrows{B, Lp, wB, box_slots(wB, 3)},
+        OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{BD, Lp, 3, wBD, box_slots(wBD, 1)},
+        rb0, rb1);
+    return (int)cudaGetLastError();
+  }
+  if (products_use_mma) return GB_UNSUPPORTED;  // same arithmetic as the whole level only
+  k_bd<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD, r0 * per,
+                                                     r1 * per);
+  return (int)cudaGetLastError();
+}
 int gbk_bd(int Lp, int wB, const double* B, int rho, const double* Dt, int wBD,
            double* BD, cudaStream_t s) {
-  if (products_use_mma) {
-    const int TB = Lp < 4 ? Lp : 4;
-    const size_t bytes = (size_t)Lp * Lp * 3 * box_slots(wBD, 1) * sizeof(double);
-    cudaError_t e = cudaMemsetAsync(BD, 0, bytes, s);
-    if (e != cudaSuccess) return (int)e;
-    auto kern = k_box_gemm<3, OpBrows, OpDtRowsB, StoreBox>;
-    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wBD)), 128, 0, s>>>(
-        Lp, TB, wB, rho, wBD, OpBrows{B, Lp, wB, box_slots(wB, 3)},
-        OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{BD, Lp, 3, wBD, box_slots(wBD, 1)});
-    return (int)cudaGetLastError();
-  }
-  const long long total = (long long)Lp * Lp * 3 * box_slots(wBD, 1);
-  k_bd<<<grid_for(total, 256), 256, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD);
-  return (int)cudaGetLastError();
+  return gbk_bd_rows(Lp, wB, B, rho, Dt, wBD, BD, 0, Lp, s);
 }
 
+int gbk_gtd_rows(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
+                 double* GtD, int r0, int r1, cudaStream_t s) {
+  if (bad_rows(r0, r1, Lp)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)Lp * box_slots(wGD, 1);
+  const int TB = Lp < 4 ? Lp : 4;
+  if (products_use_mma && rows_block_aligned(r0, r1, Lp, TB)) {
+    cudaError_t e = cudaMemsetAsync(GtD + r0 * per, 0, (r1 - r0) * per * sizeof(double), s);
+    if (e != cudaSuccess) return (int)e;
+    const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
+    auto kern = k_box_gemm<1, OpGcols, OpDtRowsB, StoreBox>;
+    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wGD, rb0, rb1)), 128, 0, s>>>(
+        Lp, TB, wG, rho, wGD, OpGcols{G, Lp, wG, box_slots(wG, 1)},
+        OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{GtD, Lp, 1, wGD, box_slots(wGD, 1)},
+        rb0, rb1);
+    return (int)cudaGetLastError();
+  }
+  if (products_use_mma) return GB_UNSUPPORTED;
+  k_gtd<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(Lp, wG, G, rho, Dt, wGD, GtD, r0 * per,
+                                                      r1 * per);
+  return (int)cudaGetLastError();
+}
 int gbk_gtd(int Lp, int wG, const double* G, int rho, const double* Dt, int wGD,
             double* GtD, cudaStream_t s) {
-  if (products_use_mma) {
-    const int TB = Lp < 4 ? Lp : 4;
-    const size_t bytes = (size_t)Lp * Lp * box_slots(wGD, 1) * sizeof(double);
-    cudaError_t e = cudaMemsetAsync(GtD, 0, bytes, s);
-    if (e != cudaSuccess) return (int)e;
-    auto kern = k_box_gemm<1, OpGcols, OpDtRowsB, StoreBox>;
-    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wGD)), 128, 0, s>>>(
-        Lp, TB, wG, rho, wGD, OpGcols{G, Lp, wG, box_slots(wG, 1)},
-        OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{GtD, Lp, 1, wGD, box_slots(wGD, 1)});
-    return (int)cudaGetLastError();
-  }
-  const long long total = (long long)Lp * Lp * box_slots(wGD, 1);
-  k_gtd<<<grid_for(total, 256), 256, 0, s>>>(Lp, wG, G, rho, Dt, wGD, GtD);
-  return (int)cudaGetLastError();
+  return gbk_gtd_rows(Lp, wG, G, rho, Dt, wGD, GtD, 0, Lp, s);
 }
 
+int gbk_coarse_raw_rows(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
+                        int rho, const double* Dt, int wBD, const double* BD, int wA2,
+                        double* raw, int r0, int r1, cudaStream_t s) {
+  if (bad_rows(r0, r1, Lp)) return GB_UNSUPPORTED;
+  if (r0 == r1) return 0;
+  const long long per = (long long)Lp * box_slots(wA2, 1);
+  const int TB = Lp < 4 ? Lp : 4;
+  if (products_use_mma && rows_block_aligned(r0, r1, Lp, TB)) {
+    cudaError_t e = cudaMemsetAsync(raw + r0 * per, 0, (r1 - r0) * per * sizeof(double), s);
+    if (e != cudaSuccess) return (int)e;
+    const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
+    auto kern = k_box_gemm<1, OpDtRowsA, OpBDrows, StoreRaw>;
+    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wA2, rb0, rb1)), 128, 0, s>>>(
+        Lp, TB, rho, wBD, wA2, OpDtRowsA{Dt, Lp, rho, box_slots(rho, 3)},
+        OpBDrows{BD, Lp, wBD, box_slots(wBD, 1)}, StoreRaw{raw, PAPt, GtD, Lp, wB, wGD, wA2},
+        rb0, rb1);
+    return (int)cudaGetLastError();
+  }
+  if (products_use_mma) return GB_UNSUPPORTED;
+  k_coarse_raw<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt,
+                                                             wBD, BD, wA2, raw, r0 * per,
+                                                             r1 * per);
+  return (int)cudaGetLastError();
+}
 int gbk_coarse_raw(int Lp, int wB, const double* PAPt, int wGD, const double* GtD,
                    int rho, const double* Dt, int wBD, const double* BD, int wA2,
                    double* raw, cudaStream_t s) {
-  if (products_use_mma) {
-    const int TB = Lp < 4 ? Lp : 4;
-    const size_t bytes = (size_t)Lp * Lp * box_slots(wA2, 1) * sizeof(double);
-    cudaError_t e = cudaMemsetAsync(raw, 0, bytes, s);
-    if (e != cudaSuccess) return (int)e;
-    auto kern = k_box_gemm<1, OpDtRowsA, OpBDrows, StoreRaw>;
-    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wA2)), 128, 0, s>>>(
-        Lp, TB, rho, wBD, wA2, OpDtRowsA{Dt, Lp, rho, box_slots(rho, 3)},
-        OpBDrows{BD, Lp, wBD, box_slots(wBD, 1)}, StoreRaw{raw, PAPt, GtD, Lp, wB, wGD, wA2});
-    return (int)cudaGetLastError();
-  }
-  const long long total = (long long)Lp * Lp * box_slots(wA2, 1);
-  k_coarse_raw<<<grid_for(total, 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt,
-                                                    wBD, BD, wA2, raw);
-  return (int)cudaGetLastError();
+  return gbk_coarse_raw_rows(Lp, wB, PAPt, wGD, GtD, rho, Dt, wBD, BD, wA2, raw, 0, Lp, s);
 }
 
+// Wpsi rows of the parents in grid rows [r0, r1); only window points whose
+// fine row is in [f0, f1) are written (column strips of the coarse levels)
+int gbk_wpsi_rows(int n, int Lk, int lo, int wd, const double* w12, const double* psi,
+                  int wdw, double* Wpsi, int r0, int r1, int f0, int f1, cudaStream_t s) {
+  const int Lp = Lk / 2;
+  if (bad_rows(r0, r1, Lp) || f0 < 0 || f1 > n || f0 > f1) return GB_UNSUPPORTED;
+  if (r0 == r1 || f0 == f1) return 0;
+  PsiWin child{n, Lk, lo, wd, 0}, par{n, Lp, lo, wdw, 0};
+  const long long per = (long long)Lp * wdw * wdw;
+  k_wpsi<<<grid_for((r1 - r0) * per, 256), 256, 0, s>>>(child, mkW(w12), psi, par, Wpsi,
+                                                       r0 * per, r1 * per, f0, f1);
+  return (int)cudaGetLastError();
+}
 int gbk_wpsi(int n, int Lk, int lo, int wd, const double* w12, const double* psi,
              int wdw, double* Wpsi, cudaStream_t s) {
-  PsiWin child{n, Lk, lo, wd, 0}, par{n, Lk / 2, lo, wdw, 0};
-  const long long total = (long long)(Lk / 2) * (Lk / 2) * wdw * wdw;
-  k_wpsi<<<grid_for(total, 256), 256, 0, s>>>(child, mkW(w12), psi, par, Wpsi);
-  return (int)cudaGetLastError();
+  return gbk_wpsi_rows(n, Lk, lo, wd, w12, psi, wdw, Wpsi, 0, Lk / 2, 0, n, s);
 }
 
 // output parent rows [r0, r1) only (tensor-core mode required for a proper
-// strip, returns 1 otherwise): rows outside are not written
-int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
-                      const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
-                      double* psi_next, double* rowmax, int r0, int r1, cudaStream_t s) {
+// strip, GB_UNSUPPORTED otherwise): rows outside are not written.  Raw rows and
+// their row maxima; window points with a fine row outside [f0, f1) are
+// neither computed nor written (column strips: the caller max-reduces rowmax
+// over the column owners before the drop).
+int gbk_psi_next_raw_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                          const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                          double* psi_next, double* rowmax, int r0, int r1, int f0, int f1,
+                          cudaStream_t s) {
   PsiWin child{n, Lk, lo, wd, hi}, par{n, Lk / 2, lo, wdw, 0}, out{n, Lk / 2, lo2, wd2, 0};
   const int Lp = Lk / 2;
-  if (r0 < 0 || r1 > Lp || r0 > r1) return GB_UNSUPPORTED;
+  if (r0 < 0 || r1 > Lp || r0 > r1 || f0 < 0 || f1 > n || f0 > f1) return GB_UNSUPPORTED;
   if (r0 == r1) return 0;
-  if (!products_use_mma && (r0 != 0 || r1 != Lp)) return GB_UNSUPPORTED;
+  const bool whole = r0 == 0 && r1 == Lp && f0 == 0 && f1 == n;
+  if (!products_use_mma && !whole) return GB_UNSUPPORTED;
   const long long S = (long long)wd2 * wd2;
   const long long rows = (long long)(r1 - r0) * Lp, roff = (long long)r0 * Lp;
   cudaError_t e = cudaMemsetAsync(rowmax + roff, 0, rows * sizeof(double), s);
   if (e != cudaSuccess) return (int)e;
+  if (f0 == f1) return 0;
   if (products_use_mma) {
     const int TB = Lp < 4 ? Lp : 4;
     const int hp = n / Lp;  // output row spacing (fine units)
@@ -1137,7 +1262,7 @@ int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, 
     const long long nt = nrb * nb * nfs * nft;
     const int g = resident_grid(k_psi_next_mma, 128, nt);
     k_psi_next_mma<<<g, 128, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out, psi_next, rowmax, TB,
-                                     nfs, nft, r0, r1);
+                                     nfs, nft, r0, r1, f0, f1);
   } else {
     const long long total = rows * S;
     k_psi_next<<<grid_for(total, 256), 256, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out,
@@ -1146,10 +1271,35 @@ int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, 
     k_rowmax_chunks<<<(int)(nch < 148LL * 32 ? nch : 148LL * 32), 256, 0, s>>>(rows, S, psi_next,
                                                                               rowmax);
   }
-  const long long nch = rows * ((S + RT_CHUNK - 1) / RT_CHUNK);
-  k_drop_by_rowmax<<<(int)(nch < 148LL * 32 ? nch : 148LL * 32), 256, 0, s>>>(
-      rows, S, psi_next + roff * S, rowmax + roff);
   return (int)cudaGetLastError();
+}
+
+// the row-tail drop of psi rows [r0, r1) given their maxima; window rows with
+// a fine row outside [f0, f1) are left alone
+int gbk_psi_drop_rows(int n, int Lp, int lo2, int wd2, double* psi_next, const double* rowmax,
+                      int r0, int r1, int f0, int f1, cudaStream_t s) {
+  if (r0 < 0 || r1 > Lp || r0 > r1 || f0 < 0 || f1 > n || f0 > f1) return GB_UNSUPPORTED;
+  if (r0 == r1 || f0 == f1) return 0;
+  const long long S = (long long)wd2 * wd2;
+  const long long rows = (long long)(r1 - r0) * Lp, roff = (long long)r0 * Lp;
+  const long long nch = rows * ((S + RT_CHUNK - 1) / RT_CHUNK);
+  const int g = (int)(nch < 148LL * 32 ? nch : 148LL * 32);
+  if (f0 == 0 && f1 == n) {
+    k_drop_by_rowmax<<<g, 256, 0, s>>>(rows, S, psi_next + roff * S, rowmax + roff);
+  } else {
+    PsiWin out{n, Lp, lo2, wd2, 0};
+    k_drop_by_rowmax_cols<<<g, 256, 0, s>>>(out, roff, rows, psi_next, rowmax, f0, f1);
+  }
+  return (int)cudaGetLastError();
+}
+
+int gbk_psi_next_rows(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
+                      const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,
+                      double* psi_next, double* rowmax, int r0, int r1, cudaStream_t s) {
+  const int rc = gbk_psi_next_raw_rows(n, Lk, lo, hi, wd, psi, wdw, Wpsi, rho, Dt, lo2, wd2,
+                                       psi_next, rowmax, r0, r1, 0, n, s);
+  if (rc != 0) return rc;
+  return gbk_psi_drop_rows(n, Lk / 2, lo2, wd2, psi_next, rowmax, r0, r1, 0, n, s);
 }
 int gbk_psi_next(int n, int Lk, int lo, int hi, int wd, const double* psi, int wdw,
                  const double* Wpsi, int rho, const double* Dt, int lo2, int wd2,

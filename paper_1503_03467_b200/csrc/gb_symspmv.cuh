@@ -54,10 +54,10 @@ __host__ __device__ __forceinline__ void symb_offset(int w, int e, int* ds, int*
 // (S B S) upper blocks from the unscaled box, entry by entry the reference's
 // materialized congruence (x * s_i) * s_j (gamblet_fast.py:136)
 __global__ void k_scale_box_symb(int L, int w, const double* __restrict__ B,
-                                 const double* __restrict__ s, double* __restrict__ U) {
+                                 const double* __restrict__ s, double* __restrict__ U,
+                                 long long e0, long long e1) {
   const int S = (2 * w + 1) * (2 * w + 1) * 3, NS = symb_ns(w), npos = symb_npos(w);
-  const long long total = (long long)L * L * NS;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const long long blk = e / (32LL * NS);
     const int rem = (int)(e - blk * 32LL * NS);
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
     int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
     double* __restrict__ y0, KState* s0, double* part0, int red0,
     const double* __restrict__ x1, double* __restrict__ y1, KState* s1, double* part1,
-    int red1) {
+    int red1, long long tile0, long long tile1) {
   extern __shared__ double dyn[];
   __shared__ double sh[32];
   const bool live0 = !(s0 && s0->done);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
   const int XW = (kSymTH + w) * WC * 3;                 // x window doubles
   const int AC = 32 + 2 * w, AREG = (w + 1) * AC * 3;  // per-warp accumulator
   const int RW = WC * 3, RG = symb_region(w);
-  const long long npad = (long long)Lpad * Lpad * 3, ntile = symb_ntile(L);
+  const long long npad = (long long)Lpad * Lpad * 3;
   int* xoff = reinterpret_cast<int*>(dyn);
   int* aoff = xoff + npos;
   double* xs = dyn + ((2 * npos + 1) >> 1) + 1;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
   double dot[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) dot[v] = 0.0;
-  for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+  for (long long t = tile0 + blockIdx.x; t < tile1; t += gridDim.x) {
     const int I = (int)(t / tpr), J = (int)(t % tpr);
     const int ps0 = I * kSymTH, pt0 = J * kSymTW;
     // stage x windows: the tile's own rows and the w rows below (padded rows
@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(kSymThreads, 2) k_symb_apply(
       double a = 0.0;
       for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) a += part[2 * k];
       a = block_sum(a, sh);
-      if (threadIdx.x == 0) finish_reduction(v == 0 ? s0 : s1, 0, a, 0.0);
+      if (threadIdx.x == 0)
+        finish_reduction(v == 0 ? s0 : s1, (v == 0 ? red0 : red1) == 2 ? 3 : 0, a, 0.0);
     }
     if (threadIdx.x == 0) cs->counter = 0;
   }
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
     int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
     double* __restrict__ y0, KState* s0, double* part0, int red0,
     const double* __restrict__ x1, double* __restrict__ y1, KState* s1, double* part1,
-    int red1) {
+    int red1, long long tile0, long long tile1) {
   constexpr int NS = symb_ws_stages<NV>();
   constexpr int NW = 2 * kSymTH;  // consumer warps
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
   const int XW = (kSymTH + w) * WC * 3;
   const int AC = 32 + 2 * w, AREG = (w + 1) * AC * 3;
   const int RW = WC * 3, RG = symb_region(w);
-  const long long npad = (long long)Lpad * Lpad * 3, ntile = symb_ntile(L);
+  const long long npad = (long long)Lpad * Lpad * 3;
   const int tpr = L / kSymTW;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(dsm);
   unsigned long long* empty = full + NS;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
     // ---- producer: chunk g = (tile iteration, k) -> stage g % NS ----
     if (lane == 0) {
       long long g = 0;
-      for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+      for (long long t = tile0 + blockIdx.x; t < tile1; t += gridDim.x) {
         const int I = (int)(t / tpr), J = (int)(t % tpr);
         for (int k = 0; k < nch; ++k, ++g) {
           const int st = (int)(g % NS);
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
   } else {
     // ---- consumers ----
     long long g = 0;
-    for (long long t = blockIdx.x; t < ntile; t += gridDim.x) {
+    for (long long t = tile0 + blockIdx.x; t < tile1; t += gridDim.x) {
       const int I = (int)(t / tpr), J = (int)(t % tpr);
       const int ps0 = I * kSymTH, pt0 = J * kSymTW;
       // x windows, 8 independent loads in flight per thread (L2 latency)
@@ -548,7 +549,8 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
       double a = 0.0;
       for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) a += part[2 * k];
       a = block_sum(a, sh);
-      if (threadIdx.x == 0) finish_reduction(v == 0 ? s0 : s1, 0, a, 0.0);
+      if (threadIdx.x == 0)
+        finish_reduction(v == 0 ? s0 : s1, (v == 0 ? red0 : red1) == 2 ? 3 : 0, a, 0.0);
     }
     if (threadIdx.x == 0) cs->counter = 0;
   }

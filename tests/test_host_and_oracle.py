@@ -170,7 +170,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.EXPORTED)
-    assert lib.gb_abi_version() == 5
+    assert lib.gb_abi_version() == 6
 
 
 def _lanczos_ab(A, v0, m):
