@@ -441,6 +441,8 @@ int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double
  * tiled level (rows multiples of 4): every reduction stops at the strip's
  * partial sum, the caller all-reduces it, a commit entry applies it to the
  * iteration state (sparse_core.py:126-165, 232-278 split at the reductions). */
+/* bytes of the gb_psi_galerkin_t_rows workspace for the strip [r0, r1) */
+size_t gb_psi_galerkin_workspace_rows(int n, int wd, int wX, int wR, int r0, int r1);
 /* grid rows [r0, r1) of a box from the CSR slice of exactly those matrix rows (local indptr, global columns) */
 int gb_csr_to_box_rows(int n, int w, const int32_t* indptr, const int32_t* indices, const double* data, double* box, int64_t* status, int r0, int r1, void* stream);
 /* gb_box_sym_drop on the grid rows [r0, r1); reads raw rows within w of the strip */

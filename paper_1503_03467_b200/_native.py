@@ -151,6 +151,7 @@ _SIGS = {
                          _P, _P, _P, _P], _I),
     "gb3_pow_solve": ([_I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _I, _P], _I),
     # row strips and the distributed Krylov pieces (multi-GPU partition)
+    "gb_psi_galerkin_workspace_rows": ([_I, _I, _I, _I, _I, _I], _Z),
     "gb_csr_to_box_rows": ([_I, _I, _P, _P, _P, _P, _P, _I, _I, _P], _I),
     "gb_box_sym_drop_rows": ([_I, _I, _I, _P, _P, _P, _P, _I, _I, _P], _I),
     "gb_psi_stencil_rows": ([_I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P], _I),

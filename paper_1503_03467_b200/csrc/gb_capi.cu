@@ -743,6 +743,9 @@ int gb3_pow_solve(int L, int nr, int w, const double* B, const double* s, double
 }
 
 // ---- row-strip entry points (multi-GPU partition) and the distributed Krylov pieces ----
+size_t gb_psi_galerkin_workspace_rows(int n, int wd, int wX, int wR, int r0, int r1) {
+  return gbk_psi_galerkin_workspace_rows(n, wd, wX, wR, r0, r1);
+}
 int gb_csr_to_box_rows(int n, int w, const int32_t* indptr, const int32_t* indices, const double* data, double* box, int64_t* status, int r0, int r1, void* stream) {
   COUNT(1);
   const int rc = gbk_csr_to_box_rows(n, w, indptr, indices, data, box, LL(status), r0, r1, ST(stream));

@@ -50,6 +50,7 @@ int gbk_correction_patches(int Lp, int wB, const double* B, const double* sB, in
 int gbk_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
                     const double* A, int wX, double* X, cudaStream_t s);
 size_t gbk_psi_galerkin_workspace(int n, int wd, int wX);
+size_t gbk_psi_galerkin_workspace_rows(int n, int wd, int wX, int wR, int r0, int r1);
 int gbk_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,
                        const double* X, int wR, double* raw, double* work, cudaStream_t s);
 int gbk_psi_galerkin(int n, int lo, int wd, int rho, const double* psi, int wX,

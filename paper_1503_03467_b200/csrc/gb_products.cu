@@ -130,10 +130,10 @@ __global__ void __launch_bounds__(GT_THREADS) k_psi_galerkin_t(PsiWin pw, int rh
                                                                const double* __restrict__ psiT,
                                                                int wX, const double* __restrict__ XT,
                                                                int wR, double* __restrict__ raw,
-                                                               int s0, int s1) {
+                                                               int s0, int s1, long long ld) {
   extern __shared__ double ob[];  // 32 x SR
   const int n = pw.n;
-  const long long N = (long long)n * n;
+  const long long N = ld;  // plane stride of psiT / XT (the node count they hold)
   const int SR = box_slots(wR, 1), WR = 2 * wR + 1, WX = 2 * wX + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ncb = (n + 31) / 32;
@@ -1022,6 +1022,12 @@ int gbk_psi_stencil(int n, int lo, int wd, int rho, const double* psi, int wA,
 size_t gbk_psi_galerkin_workspace(int n, int wd, int wX) {
   return (size_t)n * n * ((size_t)wd * wd + (size_t)box_slots(wX, 1)) * sizeof(double);
 }
+// workspace of the strip [r0, r1): planes over the nodes of the strip's rows
+// widened by wR (psi) -- X uses the same plane stride
+size_t gbk_psi_galerkin_workspace_rows(int n, int wd, int wX, int wR, int r0, int r1) {
+  const int h0 = imax(r0 - wR, 0), h1 = imin(r1 + wR, n);
+  return (size_t)(h1 - h0) * n * ((size_t)wd * wd + (size_t)box_slots(wX, 1)) * sizeof(double);
+}
 
 // fine rows [r0, r1) of raw: psi rows within wR of the strip and the strip's X
 // rows are transposed into their global plane-major positions of `work`
@@ -1033,16 +1039,20 @@ int gbk_psi_galerkin_t_rows(int n, int lo, int wd, int rho, const double* psi, i
   PsiWin pw{n, n, lo, wd, -lo};
   const long long N = (long long)n * n;
   const int SX = box_slots(wX, 1), SR = box_slots(wR, 1);
-  double* psiT = work;
-  double* XT = work + N * wd * wd;
   const dim3 tb(32, 8);
   const int h0 = imax(r0 - wR, 0), h1 = imin(r1 + wR, n);
   const long long pa = (long long)h0 * n, pn = (long long)(h1 - h0) * n;
+  // planes hold the nodes [pa, pa + pn) only (plane stride pn); psiT / XT are
+  // the bases shifted so that a global node index addresses them (whole
+  // level: pa = 0, pn = N)
+  (void)N;
+  double* psiT = work - pa;
+  double* XT = work + pn * wd * wd - pa;
   k_transpose_f64<<<dim3((unsigned)((pn + 31) / 32), (wd * wd + 31) / 32), tb, 0, s>>>(
-      pn, wd * wd, psi + pa * wd * wd, psiT + pa, N);
+      pn, wd * wd, psi + pa * wd * wd, psiT + pa, pn);
   const long long xa = (long long)r0 * n, xn = (long long)(r1 - r0) * n;
   k_transpose_f64<<<dim3((unsigned)((xn + 31) / 32), (SX + 31) / 32), tb, 0, s>>>(
-      xn, SX, X + xa * SX, XT + xa, N);
+      xn, SX, X + xa * SX, XT + xa, pn);
   const size_t smem = (size_t)32 * SR * sizeof(double);
   if (smem > 200 * 1024) return GB_UNSUPPORTED;
   cudaError_t e = cudaFuncSetAttribute(k_psi_galerkin_t,
@@ -1050,7 +1060,7 @@ int gbk_psi_galerkin_t_rows(int n, int lo, int wd, int rho, const double* psi, i
   if (e != cudaSuccess) return (int)e;
   const long long nct = (long long)(r1 - r0) * ((n + 31) / 32);
   const int g = (int)(nct < 148LL * 8 ? nct : 148LL * 8);
-  k_psi_galerkin_t<<<g, GT_THREADS, smem, s>>>(pw, rho, psiT, wX, XT, wR, raw, r0, r1);
+  k_psi_galerkin_t<<<g, GT_THREADS, smem, s>>>(pw, rho, psiT, wX, XT, wR, raw, r0, r1, pn);
   return (int)cudaGetLastError();
 }
 int gbk_psi_galerkin_t(int n, int lo, int wd, int rho, const double* psi, int wX,

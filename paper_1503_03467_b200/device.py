@@ -9,6 +9,7 @@ cached on the host.
 
 from __future__ import annotations
 
+import threading
 from contextlib import contextmanager
 
 import numpy as np
@@ -78,12 +79,15 @@ class Traffic:
 # DMA) -- a pageable copy is bounded by one driver memcpy thread
 _STAGE_MIN_BYTES = 4 << 20
 _STAGE_THREADS = 8
+# the staging ring is one per process: in-process ranks (comm.ThreadComm) take turns
+_STAGE_LOCK = threading.Lock()
 
 
 def _staged_copy(t):
     out = torch.empty(t.shape, dtype=t.dtype, device=device())
-    nat.call("gb_h2d_staged", out.data_ptr(), t.data_ptr(), t.numel() * t.element_size(),
-             _STAGE_THREADS, stream())
+    with _STAGE_LOCK:
+        nat.call("gb_h2d_staged", out.data_ptr(), t.data_ptr(), t.numel() * t.element_size(),
+                 _STAGE_THREADS, stream())
     return out
 
 
@@ -94,8 +98,9 @@ def _index_to_dev(idx):
     if idx.dtype == np.int64 and idx.nbytes >= _STAGE_MIN_BYTES and torch.cuda.is_available():
         out = torch.empty(idx.shape, dtype=torch.int32, device=device())
         Traffic.h2d += idx.size * 4
-        nat.call("gb_h2d_staged_i64_i32", out.data_ptr(), idx.ctypes.data, idx.size,
-                 _STAGE_THREADS, stream())
+        with _STAGE_LOCK:
+            nat.call("gb_h2d_staged_i64_i32", out.data_ptr(), idx.ctypes.data, idx.size,
+                     _STAGE_THREADS, stream())
         return out
     return to_dev(idx.astype(np.int32, copy=False))
 

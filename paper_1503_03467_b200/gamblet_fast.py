@@ -269,6 +269,7 @@ class _Ctx:
         self.cap = n_slots
         self.labels = []
         self.repair_of = {}
+        self.comm = None  # comm.Comm of a spatially partitioned transform
 
     def slot(self, kind, what, detail=None):
         if self.n >= self.cap:
@@ -296,7 +297,11 @@ class _Ctx:
         self._check(raise_=True)
 
     def _check(self, raise_=False):
-        if _STRIPS is not None and _STRIPS.distributed and _STRIPS.world > 1:
+        if self.comm is not None and self.comm.world > 1:
+            # every rank sees every strip's status words and repair statistics
+            self.comm.allreduce(self.status[: 2 * self.n], "max")
+            self.comm.allreduce(self.stats[: 2 * self.n], "max")
+        elif _STRIPS is not None and _STRIPS.distributed and _STRIPS.world > 1:
             # every rank raises together: a non-SPD patch on one strip poisons
             # the rows the others received from it
             import torch.distributed as dist
@@ -1049,9 +1054,15 @@ def local_mass_inverse(M, tree, rho, tol, counter=None, dense_cutoff=DENSE_PATCH
 
 def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAULT_C_TOL,
                      counter=None, dense_cutoff=DENSE_PATCH_CUTOFF, _ctx=None, _spool=None,
-                     _g=None, _lean=False):
+                     _g=None, _lean=False, _cols=None):
     """One localized downward step k -> k-1 (gamblet_fast.py:501-632).
-    Mutates `level` (W, B, s_B, D, R, lambdas, repair) and returns level k-1."""
+    Mutates `level` (W, B, s_B, D, R, lambdas, repair) and returns level k-1.
+
+    _cols = (f0, f1, comm): column strips of psi (gamblet_dist.py, the
+    replicated coarse levels of a partitioned transform): this rank holds and
+    computes only the window points of psi^(k), W psi and psi^(k-1) whose fine
+    row lies in [f0, f1); the row maxima of the tail drop are max-reduced
+    over the ranks."""
     k = level.k
     if k < 2:
         raise InvalidArgumentError(f"level step needs k >= 2, got k={k}")
@@ -1172,11 +1183,23 @@ def local_level_step(level, tree, schedule, w_variant="orthonormal", c_tol=DEFAU
             wd2 = PsiWindows.window(n, lo2, hi2)
             pv = dv.empty(P * wd2 * wd2)
             with dv.phase("psi_next"):
-                nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
-                         dv.ptr(Wpsi), s)
                 rmax = dv.empty(P)
                 strips_done = False
-                if _STRIPS is not None:  # row strips of the parent grid (multi-GPU block)
+                if _cols is not None:
+                    cf0, cf1, ccomm = _cols
+                    nat.call("gb_wpsi_rows", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
+                             dv.ptr(Wpsi), 0, Lp, cf0, cf1, s)
+                    nat.call("gb_psi_next_raw_rows", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
+                             dv.ptr(Wpsi), rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax),
+                             0, Lp, cf0, cf1, s)
+                    ccomm.allreduce(rmax, "max")
+                    nat.call("gb_psi_drop_rows", n, Lp, lo2, wd2, dv.ptr(pv), dv.ptr(rmax),
+                             0, Lp, cf0, cf1, s)
+                    strips_done = True
+                else:
+                    nat.call("gb_wpsi", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw,
+                             dv.ptr(Wpsi), s)
+                if _STRIPS is not None and not strips_done:  # row strips of the parent grid (multi-GPU block)
                     try:
                         part.run_strips(_STRIPS, Lp, Lp * wd2 * wd2, pv, lambda r0, r1: nat.call(
                             "gb_psi_next_rows", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw,
@@ -1358,6 +1381,22 @@ class _LevelSolver:
         self.n = 1 << tree.q
         self.N = self.n * self.n
         self.coeffs, self.incs = HostDict(), HostDict()
+        # (f0, f1): increments on these fine rows only (column strips of psi,
+        # gamblet_dist.py); the other entries of an increment stay zero
+        self.fine_rows = None
+
+    def _psi_t(self, L, psi, v):
+        """inc = psi^T v over the fine grid (or its fine_rows strip)."""
+        if self.fine_rows is None:
+            inc = dv.empty(self.N)
+            nat.call("gb_psi_t_apply", self.n, L, psi.lo, psi.wd, dv.ptr(psi.vals), dv.ptr(v),
+                     dv.ptr(inc), dv.stream())
+            return inc
+        f0, f1 = self.fine_rows
+        inc = dv.zeros(self.N)
+        nat.call("gb_psi_t_apply_rows", self.n, L, psi.lo, psi.wd, dv.ptr(psi.vals), dv.ptr(v),
+                 dv.ptr(inc), f0, f1, 0, L, dv.stream())
+        return inc
 
     def _check(self, k, need_r=True):
         lvl = self.levels[k]
@@ -1428,9 +1467,7 @@ class _LevelSolver:
             psi = lvl.raw("psi")
         if not isinstance(psi, PsiWindows):
             psi = _psi_dev(lvl, self.n, 2 * Lp)
-        inc = dv.empty(self.N)
-        nat.call("gb_psi_t_apply", self.n, 2 * Lp, psi.lo, psi.wd, dv.ptr(psi.vals),
-                 dv.ptr(v), dv.ptr(inc), s)
+        inc = self._psi_t(2 * Lp, psi, v)
         psi.vals.record_stream(torch.cuda.current_stream())
         counter.add("line10", 8 * J + 2 * (4 * Lp * Lp) * psi.wd * psi.wd)
         self.incs[k] = inc
@@ -1470,9 +1507,7 @@ class _LevelSolver:
         psi1 = coarse.raw("psi")
         if not isinstance(psi1, PsiWindows):
             psi1 = _psi_dev(coarse, self.n, 2)
-        inc1 = dv.empty(self.N)
-        nat.call("gb_psi_t_apply", self.n, 2, psi1.lo, psi1.wd, dv.ptr(psi1.vals), dv.ptr(U1),
-                 dv.ptr(inc1), s)
+        inc1 = self._psi_t(2, psi1, U1)
         counter.add("line17", 2 * 4 * psi1.wd * psi1.wd)
         self.incs[1] = inc1
         self.U1 = U1
