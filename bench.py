@@ -13,8 +13,11 @@ subband solves and the reassembly of u.
          host->device uploads and the device->host copy of u inside the step
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-        (N > 1: one process per GPU via torch.distributed.run; each rank solves
-        its own replica -- weak scaling, no domain decomposition yet)
+        N > 1 (one process per GPU via torch.distributed.run, NCCL): BASELINE
+        configs[3] (q = 12, 16.8 M DOFs) split spatially into N row strips --
+        gamblet_dist.fast_solve_dist: per-rank strips of every level operator,
+        neighbour halo exchanges, distributed PCG (strong scaling).  Configs 0
+        and 4 run N replicas.
 """
 
 from __future__ import annotations
@@ -704,6 +707,120 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
+def run_dist(args, rank, world, local_rank):
+    """N > 1: the spatially partitioned solve (gamblet_dist.fast_solve_dist)
+    of ONE instance -- BASELINE configs[3] unless --config says otherwise --
+    over `world` ranks: strong scaling, value = N fine DOFs / step time (max
+    over ranks, device-timed).  value: M, A device-assembled boxes (9 values
+    per row, replicated) and g in HBM; e2e: host scipy M, A and host g in,
+    u back on the host, on every rank."""
+    import torch
+    import torch.distributed as dist
+    import paper_1503_03467_b200 as gb
+    from paper_1503_03467_b200 import _native as nat, device as dv, gamblet_dist as gd
+    torch.cuda.set_device(local_rank)
+    name = args.config if args.config_given else "c3"
+    cfg = CONFIGS[name]
+    q = args.q or cfg["q"]
+    N = 4 ** q
+    comm = gb.TorchComm()
+    if rank == 0:
+        print(f"[bench] partitioned run: world {world}, backend {comm.backend}, q={q}; "
+              f"one {comm.backend} communicator over ranks 0..{world - 1}"
+              + (" (NCCL_DEBUG=INFO prints its channels)" if comm.backend == "nccl" else ""),
+              file=sys.stderr)
+    grid, M, A, load, tree = build_inputs(q, cfg["coeff"], 0)  # the one shared instance
+    c = (gb.coefficient_example1(grid) if cfg["coeff"] == "example1"
+         else gb.coefficient_checkerboard(grid, 1e4, instance_seeds(0)[0]))
+    Mb = gb.assemble_mass(grid, device=True)
+    Ab = gb.assemble_stiffness(grid, c, device=True)
+    gd_dev = dv.to_dev(load.g_nodal)
+
+    def step():
+        return gd.fast_solve_dist(comm, Mb, Ab, gd_dev, tree, EPS, uniform_rho=RHO)
+
+    for _ in range(args.warmup):
+        res = step()
+        res = None
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    gd.DIST_TIMING = {"n": 3 * 4 ** (q - 1), "cap": 64, "ms": []}
+    launches0 = nat.query("gb_launch_count")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            res = None
+            res = step()
+            torch.cuda.synchronize()
+        ev1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches = nat.query("gb_launch_count") - launches0
+    timing, gd.DIST_TIMING = gd.DIST_TIMING, None
+    ms = reduce_max(ev0.elapsed_time(ev1) / args.steps, world, "cuda")
+    peak = reduce_max(res.peak_bytes, world, "cuda")
+    halo = reduce_max(res.halo_bytes, world, "cuda")
+    its, lams, first_rep, passes = res.iterations, res.lambdas, res.first_replicated, \
+        res.krylov_passes
+    res = None
+    # e2e: host inputs in, u on the host out, every step
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        dist.barrier()
+        dv.Traffic.reset()
+        t0 = time.perf_counter()
+        r2 = gd.fast_solve_dist(comm, M, A, load.g_nodal, tree, EPS, uniform_rho=RHO)
+        u = dv.to_host(r2.u)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d, d2h = dv.Traffic.h2d, dv.Traffic.d2h
+        r2 = None
+    e2e = reduce_max(float(np.median(e2e_ms)), world, "cuda")
+    if rank != 0:
+        return None
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs") or 6650.0
+    roof = None
+    if timing.get("ms"):
+        dual_ms = float(np.mean(timing["ms"]))
+        nbytes = timing["matrix_bytes"] + timing["vector_bytes"]
+        ach = nbytes / (dual_ms * 1e-3) / 1e9
+        roof = {"kernel": "k_symb_apply_ws<2> on the rank's tile rows (finest level, strip of "
+                          "the symmetric band S B S, PCG + spectral vectors)",
+                "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "traffic": None,
+                "bytes_per_launch": int(nbytes), "ms_per_launch": round(dual_ms, 4),
+                "launches_timed": len(timing["ms"]),
+                "timing": "CUDA events on rank 0's stream around its first 64 dual launches "
+                          "of the finest level in every timed step (per GPU)"}
+    cfgo = workload_config(name, q, world)
+    cfgo["parallelism"] = (f"spatial row strips over {world} GPUs: levels with >= "
+                           f"{gd.min_distributed_rows(world)} parent rows distributed (halo "
+                           f"exchange + all-reduce over NCCL), coarser levels replicated with "
+                           f"column strips of psi; first replicated level {first_rep}")
+    return {
+        "metric": METRIC, "value": round(N / (ms * 1e-3), 1), "unit": "fine-DOF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded reference generators, one instance shared by all ranks)",
+        "config": cfgo,
+        "e2e": {"value": round(N / (e2e * 1e-3), 1), "unit": "fine-DOF/s",
+                "ms_per_step": round(e2e, 3), "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": None,
+        "clocks": clk.summary(),
+        "per_rank_peak_bytes": int(peak), "per_rank_halo_bytes_per_step": int(halo),
+        "subband_iterations": {str(k): v for k, v in sorted(its.items())},
+        "krylov_passes": {str(k): list(v) for k, v in passes.items()},
+        "lambdas": {str(k): list(v) for k, v in sorted(lams.items())},
+    }
+
+
 def run_reference(args, rank, world):
     """Reference arm: the CPU oracle port (numpy/scipy restatement of the
     reference, tight mode, direct patch solves; the reference itself is pure
@@ -797,16 +914,19 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--q", type=int, default=None, help="override the config's q")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timeline", action="store_true")
     ap.add_argument("--repeat-solves", type=int, default=4,
                     help="loads of the repeat-solve leg (0: skip)")
     args = ap.parse_args()
+    args.config_given = args.config is not None
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    # N = 1: configs[2]; N > 1: configs[3] split over the GPUs (both arms)
+    args.config = args.config or ("c3" if world > 1 else "c2")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if (args.q or CONFIGS[args.config]["q"]) >= 12:
@@ -819,10 +939,18 @@ def main():
     else:
         if world > 1:
             import torch
+            # GB_DIST_BACKEND=gloo: functional runs of the N > 1 path on fewer
+            # GPUs than ranks (ranks share devices, rows staged through the
+            # host) -- never a measurement
+            backend = os.environ.get("GB_DIST_BACKEND", "nccl")
+            if backend != "nccl":
+                local_rank = local_rank % max(1, torch.cuda.device_count())
             torch.cuda.set_device(local_rank)
-            torch.distributed.init_process_group("nccl")
+            torch.distributed.init_process_group(backend)
         cfg = CONFIGS[args.config]
         runner = run_exact if cfg.get("exact") else run_3d if cfg.get("d") == 3 else run_ours
+        if world > 1 and runner is run_ours:
+            runner = run_dist
         out = runner(args, rank, world, local_rank)
         if world > 1:
             import torch

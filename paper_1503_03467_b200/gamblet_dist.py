@@ -57,6 +57,13 @@ from .hierarchy import w_template
 
 __all__ = ["fast_solve_dist", "Rows", "DistResult", "min_distributed_rows"]
 
+# live timing of the strip's dual-vector operator passes (bench.py): {"n": rows
+# of the level to time, "cap": launches} -> CUDA events on the launching stream
+# around the first `cap` two-vector gb_dist_apply calls of that level; their
+# durations (ms) are appended to DIST_TIMING["ms"], the strip's matrix bytes
+# are stored under "matrix_bytes" and the vector bytes under "vector_bytes"
+DIST_TIMING = None
+
 
 def min_distributed_rows(world):
     """Smallest parent grid side that is split into strips: strips must be
@@ -252,6 +259,8 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
     comm.allreduce(outa, "sum")
     nat.call("gb_dist_pcg_init_commit", dv.ptr(ka.state), dv.ptr(outa), float(tol), int(max_a), s)
     passes = [0, 0]
+    timing = DIST_TIMING if (DIST_TIMING is not None and DIST_TIMING.get("n") == n) else None
+    evs = []
 
     def a_post():
         nat.call("gb_dist_pcg_update", L, w, dv.ptr(xa), dv.ptr(ra), dv.ptr(pa), dv.ptr(apa),
@@ -266,9 +275,16 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
         """One pass over the strip's rows of S B S for the live halves."""
         if a_live and xb is not None:
             op.halo_x(pa, xb)
+            timed = timing is not None and len(evs) < int(timing.get("cap", 64))
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
             nat.call("gb_dist_apply", L, w, U, 2, dv.ptr(pa), dv.ptr(apa), dv.ptr(ka.state),
                      dv.ptr(ka.part), dv.ptr(xb), dv.ptr(yb), dv.ptr(kb.state), dv.ptr(kb.part),
                      dv.ptr(red), p0, p1, s)
+            if timed:
+                e1.record()
+                evs.append((e0, e1))
             op.halo_spill(apa, yb)
             passes[0] += 1
         elif a_live:
@@ -396,6 +412,11 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
                              "(matrix is not SPD)")
     if ha["aux0"] != 0.0:  # zero right-hand side: the solution is zero
         xa.zero_()
+    if timing is not None and evs:
+        evs[-1][1].synchronize()
+        timing.setdefault("ms", []).extend(a.elapsed_time(b) for a, b in evs)
+        timing["matrix_bytes"] = op.matrix_bytes
+        timing["vector_bytes"] = 4 * 8 * (p1 - p0 + w) * Lpad * 3
     rel = float(ha["rnorm"] / ha["bnorm"]) if ha["bnorm"] > 0 else 0.0
     out.update(x=xa, its=int(ha["it"]), rel=rel, conv=bool(ha["converged"]),
                passes=tuple(passes))

@@ -53,7 +53,8 @@ def _check_rows(name, k, ref, rows_list, L, row_elems):
 
 @pytest.mark.parametrize("q,world,coeff", [(7, 2, "checker"), (7, 4, "example1"),
                                            (8, 8, "checker"), (9, 2, "checker"),
-                                           (9, 4, "checker")])
+                                           (9, 4, "checker"), (10, 2, "checker"),
+                                           (10, 8, "checker")])
 def test_partitioned_transform_bitwise_and_solution(q, world, coeff):
     from paper_1503_03467_b200 import comm as cm, device as dv
     grid, M, A, g, tree = _inputs(q, coeff)
@@ -149,3 +150,51 @@ def test_per_rank_memory_shrinks_with_world():
             one = held[0] * world
         # strips + halos: within 35% of an even split of the same operators
         assert max(held) <= 1.35 * one / world, (world, held, one)
+
+
+def _proc_worker(rank, world, port, q, out_dir):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1503_03467_b200 as gb
+    grid, M, A, g, tree = _inputs(q)
+    res = gb.fast_solve_dist(gb.TorchComm(), M, A, g, tree, EPS, uniform_rho=RHO, keep=True)
+    L = 1 << q
+    p0, p1 = L * rank // world, L * (rank + 1) // world
+    np.save(f"{out_dir}/u_{rank}.npy", res.u.cpu().numpy())
+    np.save(f"{out_dir}/A_{rank}.npy", res.strips[q]["A"].rows(p0, p1).cpu().numpy())
+    np.save(f"{out_dir}/meta_{rank}.npy", np.array([res.first_replicated, res.halo_bytes]))
+    dist.destroy_process_group()
+
+
+def test_two_processes_gloo_share_the_gpu(tmp_path):
+    """The real multi-process path (torch.distributed, one process per rank):
+    two gloo ranks on the one GPU run the partitioned solve on q = 8 level
+    data (rows staged through the host) and reproduce the single-GPU result."""
+    import socket
+    import torch.multiprocessing as mp
+    q, world = 8, 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    # the children allocate on the same device: hand the cached blocks back first
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    mp.spawn(_proc_worker, args=(world, port, q, str(tmp_path)), nprocs=world, join=True)
+    grid, M, A, g, tree = _inputs(q)
+    levels, u_ref, _ = _single(M, A, g, tree)
+    us = [np.load(tmp_path / f"u_{r}.npy") for r in range(world)]
+    assert np.array_equal(us[0], us[1])
+    ur = u_ref.cpu().numpy()
+    assert np.linalg.norm(us[0] - ur) <= 1e-9 * np.linalg.norm(ur)
+    Aq = levels[q].raw("stiffness")
+    got = np.concatenate([np.load(tmp_path / f"A_{r}.npy") for r in range(world)])
+    assert np.array_equal(got, Aq.vals.cpu().numpy())
+    meta = np.load(tmp_path / "meta_0.npy")
+    assert meta[0] < q and meta[1] > 0
