@@ -77,6 +77,11 @@ class Comm:
     def halo_add(self, buf, L, row_elems, up, down):
         return
 
+    def halo_many(self, items):
+        """Several halos [(buf, L, row_elems, up, down)] as one exchange."""
+        for it in items:
+            self.halo(*it)
+
     def allreduce(self, t, op="sum"):
         return t
 
@@ -111,25 +116,31 @@ class TorchComm(Comm):
 
     def _exchange(self, buf, sends, recvs, row_elems, add=False):
         """sends / recvs: [(peer, a, b)] row ranges of buf."""
+        self._exchange_many([(buf, sends, recvs, row_elems)], add)
+
+    def _exchange_many(self, jobs, add=False):
+        """jobs: [(buf, sends, recvs, row_elems)] -- one batch of P2P ops (one
+        NCCL group): the order of the jobs is the same on every rank, so the
+        messages of a pair of ranks match in order."""
         dist = self.dist
-        ops, landing = [], []
-        for peer, a, b in recvs:
-            view = buf[a * row_elems:b * row_elems]
-            if add or self._stage(buf):
-                tmp = torch.empty(view.shape, dtype=buf.dtype,
-                                  device="cpu" if self._stage(buf) else buf.device)
-                landing.append((view, tmp))
-                ops.append(dist.P2POp(dist.irecv, tmp, peer, self.group))
-            else:
-                ops.append(dist.P2POp(dist.irecv, view, peer, self.group))
-        keep = []
-        for peer, a, b in sends:
-            view = buf[a * row_elems:b * row_elems]
-            if self._stage(buf):
-                view = view.cpu()
-                keep.append(view)
-            self.bytes_sent += view.numel() * view.element_size()
-            ops.append(dist.P2POp(dist.isend, view, peer, self.group))
+        ops, landing, keep = [], [], []
+        for buf, sends, recvs, row_elems in jobs:
+            for peer, a, b in recvs:
+                view = buf[a * row_elems:b * row_elems]
+                if add or self._stage(buf):
+                    tmp = torch.empty(view.shape, dtype=buf.dtype,
+                                      device="cpu" if self._stage(buf) else buf.device)
+                    landing.append((view, tmp))
+                    ops.append(dist.P2POp(dist.irecv, tmp, peer, self.group))
+                else:
+                    ops.append(dist.P2POp(dist.irecv, view, peer, self.group))
+            for peer, a, b in sends:
+                view = buf[a * row_elems:b * row_elems]
+                if self._stage(buf):
+                    view = view.cpu()
+                    keep.append(view)
+                self.bytes_sent += view.numel() * view.element_size()
+                ops.append(dist.P2POp(dist.isend, view, peer, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
@@ -140,13 +151,23 @@ class TorchComm(Comm):
             else:
                 view.copy_(src)
 
-    def halo(self, buf, L, row_elems, up, down):
-        if self.world == 1 or (up <= 0 and down <= 0):
-            return
+    def _halo_job(self, buf, L, row_elems, up, down):
         recvs = self._wanted(L, up, down, self.rank)
         sends = [(peer, a, b) for peer in range(self.world) if peer != self.rank
                  for (src, a, b) in self._wanted(L, up, down, peer) if src == self.rank]
-        self._exchange(buf, sends, recvs, row_elems)
+        return (buf, sends, recvs, row_elems)
+
+    def halo(self, buf, L, row_elems, up, down):
+        if self.world == 1 or (up <= 0 and down <= 0):
+            return
+        self._exchange_many([self._halo_job(buf, L, row_elems, up, down)])
+
+    def halo_many(self, items):
+        if self.world == 1:
+            return
+        jobs = [self._halo_job(*it) for it in items if it[3] > 0 or it[4] > 0]
+        if jobs:
+            self._exchange_many(jobs)
 
     def halo_add(self, buf, L, row_elems, up, down):
         if self.world == 1 or (up <= 0 and down <= 0):

@@ -195,13 +195,13 @@ class _StripOp:
     # the operator input needs the w rows below the strip
     def halo_x(self, *vecs):
         re = self.Lpad * 3
-        for v in vecs:
-            self.comm.halo(_PaddedView(v, self.w, self.L, re), self.L, re, 0, self.w)
+        self.comm.halo_many([(_PaddedView(v, self.w, self.L, re), self.L, re, 0, self.w)
+                             for v in vecs])
 
     # the neighbour above sends the spill-over of its last KI tile rows
     def halo_spill(self, *vecs):
-        for v in vecs:
-            self.comm.halo(v[self.npad:], self.tile_rows, self.tile_row_elems, self.KI, 0)
+        self.comm.halo_many([(v[self.npad:], self.tile_rows, self.tile_row_elems, self.KI, 0)
+                             for v in vecs])
 
 
 class _PaddedView:
@@ -250,8 +250,9 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
     ka = _KState()
     xa, ra, pa, apa, za = (op.vec() for _ in range(5))
     red = dv.zeros(2)       # all-reduced after phase 1: (p.Ap, x.y of the B half)
-    outa = dv.zeros(3)      # all-reduced after the updates: A (rr, rz[, bb])
-    outb = dv.zeros(1)      # B: y.y / |u|^2
+    outs = dv.zeros(4)      # all-reduced after the updates, one message:
+    outa = outs[0:3]        #   A (rr, rz[, bb at the start])
+    outb = outs[3:4]        #   B: y.y / |u|^2
     outr = dv.zeros(1)      # B: power residual
     max_a = min(max(200, 2 * n), gf.MAX_ITER_CAP)
     nat.call("gb_dist_pcg_init", L, w, dv.ptr(rhs_pad), dv.ptr(xa), dv.ptr(ra), dv.ptr(pa),
@@ -330,8 +331,7 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
                     a_post()
                 nat.call("gb_dist_fix_yy", L, w, dv.ptr(yb), dv.ptr(kb.state), dv.ptr(kb.part),
                          dv.ptr(outb), p0, p1, s)
-                comm.allreduce(outa, "sum")
-                comm.allreduce(outb, "sum")
+                comm.allreduce(outs, "sum")
                 if a_live:
                     a_commit()
                 nat.call("gb_dist_pow_step", L, w, dv.ptr(xb), dv.ptr(yb), dv.ptr(kb.state),
@@ -366,8 +366,7 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
                     a_post()
                 nat.call("gb_dist_lz_update", L, w, dv.ptr(v), dv.ptr(wv), dv.ptr(vp),
                          dv.ptr(kb.state), dv.ptr(red), dv.ptr(kb.part), dv.ptr(outb), p0, p1, s)
-                comm.allreduce(outa, "sum")
-                comm.allreduce(outb, "sum")
+                comm.allreduce(outs, "sum")
                 if a_live:
                     a_commit()
                 nat.call("gb_dist_lz_commit", dv.ptr(kb.state), dv.ptr(red), dv.ptr(outb),
@@ -499,7 +498,7 @@ def fast_solve_dist(comm: Comm, M, A, g_nodal, tree, epsilon, uniform_rho=None, 
         # nothing to split at this size: the single-GPU program on every rank
         # (world == 1, or a grid too small for strips)
         levels, parts, U1, _ = gf._fast_solve_device(Mb, Ab, gfull, tree, sched,
-                                                     w_variant=w_variant, lean=False)
+                                                     w_variant=w_variant, lean=q >= 12)
         res.u = parts["partials"].device(q)
         res.levels = levels
         res.first_replicated = q
