@@ -1871,8 +1871,8 @@ static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, 
       attr[1][nv] = sm;
     }
     if (nv == 2)
-      k_symb_apply_ws<2><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1, y1,
-                                                          s1, p1, r1, t0, t1);
+      k_symb_apply_ws<2><<<gp, 2 * kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1,
+                                                              y1, s1, p1, r1, t0, t1);
     else
       k_symb_apply_ws<1><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr,
                                                           nullptr, nullptr, nullptr, 0, t0, t1);

@@ -336,14 +336,24 @@ static inline size_t symb_ws_smem(int w, int nv) {
          (size_t)2 * npos * 4;                                        // offset tables
 }
 
+// the consumer warps of one vector only (named barrier 1 + vec)
+__device__ __forceinline__ void group_sync(int vec) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + vec), "r"(kSymThreads) : "memory");
+}
+
+// NV vectors = NV groups of 8 consumer warps: group v applies the tile's U
+// blocks (read from the shared ring by every group) to vector v, so a second
+// vector adds warps -- latency hiding -- instead of lengthening every warp's
+// dependent shared-memory chains.  Each group runs exactly the single-vector
+// arithmetic (same order), the groups are independent between ring stages.
 template <int NV>
-__global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
+__global__ void __launch_bounds__(NV * kSymThreads + 32, 1) k_symb_apply_ws(
     int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
     double* __restrict__ y0, KState* s0, double* part0, int red0,
     const double* __restrict__ x1, double* __restrict__ y1, KState* s1, double* part1,
     int red1, long long tile0, long long tile1) {
   constexpr int NS = symb_ws_stages<NV>();
-  constexpr int NW = 2 * kSymTH;  // consumer warps
+  constexpr int NW = 2 * kSymTH;  // consumer warps per vector
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ double sh[32];
   const bool live0 = !(s0 && s0->done);
@@ -360,15 +370,15 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
   unsigned long long* full = reinterpret_cast<unsigned long long*>(dsm);
   unsigned long long* empty = full + NS;
   double2* ring = reinterpret_cast<double2*>(dsm + 2 * NS * 8);
-  double* xs = reinterpret_cast<double*>(ring + NS * NW * kSymWsPairs * 32);
-  double* acc = xs + NV * XW;
-  int* xoff = reinterpret_cast<int*>(acc + NV * NW * AREG);
+  double* xs_all = reinterpret_cast<double*>(ring + NS * NW * kSymWsPairs * 32);
+  double* acc_all = xs_all + NV * XW;
+  int* xoff = reinterpret_cast<int*>(acc_all + NV * NW * AREG);
   int* aoff = xoff + npos;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int st = 0; st < NS; ++st) {
       mbar_init(full + st, 1);
-      mbar_init(empty + st, NW);
+      mbar_init(empty + st, NV * NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -379,10 +389,9 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
     aoff[e] = (ds * AC + dt) * 3;
   }
   __syncthreads();
-  double dot[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) dot[v] = 0.0;
-  if (warp == NW) {
+  double dot = 0.0;
+  const int vec = warp / NW;  // NV for the producer warp
+  if (warp == NV * NW) {
     // ---- producer: chunk g = (tile iteration, k) -> stage g % NS ----
     if (lane == 0) {
       long long g = 0;
@@ -407,52 +416,61 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
       }
     }
   } else {
-    // ---- consumers ----
-    long long g = 0;
+    // ---- consumers: group `vec`, warp cw of the tile, thread gt of the group ----
+    const int cw = warp - vec * NW, gt = tid - vec * kSymThreads;
+    const bool live = vec == 0 ? live0 : live1;
+    const bool rd = vec == 0 ? rd0 : rd1;
+    const double* __restrict__ x = vec == 0 ? x0 : x1;
+    double* __restrict__ y = vec == 0 ? y0 : y1;
+    double* xs = xs_all + vec * XW;
+    double* acc = acc_all + vec * NW * AREG;
+    int st = 0;          // ring stage of the next chunk and its phase parity
+    unsigned ph = 0;
     for (long long t = tile0 + blockIdx.x; t < tile1; t += gridDim.x) {
       const int I = (int)(t / tpr), J = (int)(t % tpr);
       const int ps0 = I * kSymTH, pt0 = J * kSymTW;
-      // x windows, 8 independent loads in flight per thread (L2 latency)
-      for (int e0 = tid; e0 < XW; e0 += 8 * kSymThreads) {
-        double va[8], vb[8];
+      if (!live) {  // a finished vector: keep the ring moving, no arithmetic
+        for (int k = 0; k < nch; ++k) {
+          mbar_wait(full + st, ph);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + st);
+          if (++st == NS) st = 0, ph ^= 1;
+        }
+        continue;
+      }
+      // x window, 8 independent loads in flight per thread (L2 latency)
+      for (int e0 = gt; e0 < XW; e0 += 8 * kSymThreads) {
+        double va[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = e0 + u * kSymThreads;
-          va[u] = vb[u] = 0.0;
+          va[u] = 0.0;
           if (e < XW) {
             const int wr = e / (WC * 3), rem = e - wr * (WC * 3);
-            const long long gi = ((long long)(ps0 + w + wr) * Lpad + pt0) * 3 + rem;
-            va[u] = x0[gi];
-            if (NV == 2) vb[u] = x1[gi];
+            va[u] = x[((long long)(ps0 + w + wr) * Lpad + pt0) * 3 + rem];
           }
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = e0 + u * kSymThreads;
-          if (e < XW) {
-            xs[e] = va[u];
-            if (NV == 2) xs[XW + e] = vb[u];
-          }
+          if (e < XW) xs[e] = va[u];
         }
       }
-      for (int e = tid; e < NV * NW * AREG; e += kSymThreads) acc[e] = 0.0;
-      consumer_sync();
-      const int h = warp >> 1, j = (warp & 1) * 32 + lane;
+      for (int e = gt; e < NW * AREG; e += kSymThreads) acc[e] = 0.0;
+      group_sync(vec);
+      const int h = cw >> 1, j = (cw & 1) * 32 + lane;
       const int xo = (h * WC + (j + w)) * 3;
       const int ao = (lane + w) * 3;
-      double xa[NV][3], gg[NV][3];
+      double xa[3], gg[3];
 #pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          xa[v][c] = xs[v * XW + xo + c];
-          gg[v][c] = 0.0;
-        }
-      double* aw = acc + warp * AREG;
-      for (int k = 0; k < nch; ++k, ++g) {
-        const int st = (int)(g % NS);
-        mbar_wait(full + st, (unsigned)((g / NS) & 1));
-        const double2* sb = ring + ((long long)st * NW + warp) * kSymWsPairs * 32 + lane;
+      for (int c = 0; c < 3; ++c) {
+        xa[c] = xs[xo + c];
+        gg[c] = 0.0;
+      }
+      double* aw = acc + cw * AREG;
+      for (int k = 0; k < nch; ++k) {
+        mbar_wait(full + st, ph);
+        const double2* sb = ring + (st * NW + cw) * (kSymWsPairs * 32) + lane;
         if (k < nch - 1) {
 #pragma unroll
           for (int ee = 0; ee < 2; ++ee) {
@@ -464,19 +482,15 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
               ub[i] = (m & 1) ? d.y : d.x;
             }
             const int e = 2 * k + ee;
-            const int xe = xo + xoff[e], ae = ao + aoff[e];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              const double* xw = xs + v * XW + xe;
-              const double n0 = xw[0], n1 = xw[1], n2 = xw[2];
-              gg[v][0] = fma(ub[0], n0, fma(ub[1], n1, fma(ub[2], n2, gg[v][0])));
-              gg[v][1] = fma(ub[3], n0, fma(ub[4], n1, fma(ub[5], n2, gg[v][1])));
-              gg[v][2] = fma(ub[6], n0, fma(ub[7], n1, fma(ub[8], n2, gg[v][2])));
-              double* a = aw + v * NW * AREG + ae;
-              a[0] += fma(ub[0], xa[v][0], fma(ub[3], xa[v][1], ub[6] * xa[v][2]));
-              a[1] += fma(ub[1], xa[v][0], fma(ub[4], xa[v][1], ub[7] * xa[v][2]));
-              a[2] += fma(ub[2], xa[v][0], fma(ub[5], xa[v][1], ub[8] * xa[v][2]));
-            }
+            const double* xw = xs + xo + xoff[e];
+            const double n0 = xw[0], n1 = xw[1], n2 = xw[2];
+            gg[0] = fma(ub[0], n0, fma(ub[1], n1, fma(ub[2], n2, gg[0])));
+            gg[1] = fma(ub[3], n0, fma(ub[4], n1, fma(ub[5], n2, gg[1])));
+            gg[2] = fma(ub[6], n0, fma(ub[7], n1, fma(ub[8], n2, gg[2])));
+            double* a = aw + ao + aoff[e];
+            a[0] += fma(ub[0], xa[0], fma(ub[3], xa[1], ub[6] * xa[2]));
+            a[1] += fma(ub[1], xa[0], fma(ub[4], xa[1], ub[7] * xa[2]));
+            a[2] += fma(ub[2], xa[0], fma(ub[5], xa[1], ub[8] * xa[2]));
             __syncwarp();
           }
         } else {  // diagonal block
@@ -487,49 +501,40 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
             u[2 * i] = d.x;
             u[2 * i + 1] = d.y;
           }
+          double* a = aw + ao;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            double* a = aw + v * NW * AREG + ao;
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              a[c] += fma(u[3 * c], xa[v][0], fma(u[3 * c + 1], xa[v][1],
-                                                 fma(u[3 * c + 2], xa[v][2], gg[v][c])));
-          }
+          for (int c = 0; c < 3; ++c)
+            a[c] += fma(u[3 * c], xa[0], fma(u[3 * c + 1], xa[1], fma(u[3 * c + 2], xa[2], gg[c])));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + st);
+        if (++st == NS) st = 0, ph ^= 1;
       }
-      consumer_sync();
+      group_sync(vec);
       // combine: region row rr outer (uniform warp-row range), the thread's
       // column/component fixed, so no index division in the loop
-      if (tid < RW) {
-        const int cc = tid / 3 - w, c = tid - 3 * (tid / 3);
+      if (gt < RW) {
+        const int cc = gt / 3 - w, c = gt - 3 * (gt / 3);
         const int lc0 = cc + w, lc1 = cc - 32 + w;
         const bool in0 = lc0 < AC, in1 = lc1 >= 0;
         const bool own_col = cc >= 0 && cc < kSymTW;
         for (int rr = 0; rr < kSymTH + w; ++rr) {
           const int h0 = rr - w > 0 ? rr - w : 0, h1 = rr < kSymTH - 1 ? rr : kSymTH - 1;
-          const int idx = rr * RW + tid;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            if (v == 0 ? !live0 : !live1) continue;
-            const double* av = acc + v * NW * AREG;
-            double sm = 0.0;
-            for (int hh = h0; hh <= h1; ++hh) {
-              const int ro = ((rr - hh) * AC) * 3 + c;
-              if (in0) sm += av[(2 * hh) * AREG + ro + lc0 * 3];
-              if (in1) sm += av[(2 * hh + 1) * AREG + ro + lc1 * 3];
-            }
-            double* y = v == 0 ? y0 : y1;
-            if (rr < kSymTH && own_col)
-              y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = sm;
-            else
-              y[npad + t * RG + idx] = sm;
-            if (v == 0 ? rd0 : rd1) dot[v] = fma(xs[v * XW + idx], sm, dot[v]);
+          const int idx = rr * RW + gt;
+          double sm = 0.0;
+          for (int hh = h0; hh <= h1; ++hh) {
+            const int ro = ((rr - hh) * AC) * 3 + c;
+            if (in0) sm += acc[(2 * hh) * AREG + ro + lc0 * 3];
+            if (in1) sm += acc[(2 * hh + 1) * AREG + ro + lc1 * 3];
           }
+          if (rr < kSymTH && own_col)
+            y[((long long)(ps0 + rr + w) * Lpad + pt0 + cc + w) * 3 + c] = sm;
+          else
+            y[npad + t * RG + idx] = sm;
+          if (rd) dot = fma(xs[idx], sm, dot);
         }
       }
-      consumer_sync();
+      group_sync(vec);
     }
   }
   __syncthreads();
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__(kSymThreads + 32, 1) k_symb_apply_ws(
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (!(v == 0 ? rd0 : rd1)) continue;
-    const double a = block_sum(dot[v], sh);
+    const double a = block_sum(vec == v ? dot : 0.0, sh);
     if (threadIdx.x == 0) (v == 0 ? part0 : part1)[2 * blockIdx.x] = a;
   }
   if (last_block(&cs->counter)) {
