@@ -726,8 +726,10 @@ def run_dist(args, rank, world, local_rank):
     of ONE instance -- BASELINE configs[3] unless --config says otherwise --
     over `world` ranks: strong scaling, value = N fine DOFs / step time (max
     over ranks, device-timed).  value: M, A device-assembled boxes (9 values
-    per row, replicated) and g in HBM; e2e: host scipy M, A and host g in,
-    u back on the host, on every rank."""
+    per row, replicated) and g in HBM; e2e: the host coefficient cells and the
+    host nodal load in (on-device Q1 assembly, grid_fem.assemble_*(device=True):
+    bitwise the reference's CSR values), u back on the host, on every rank --
+    no rank builds the 150 M-entry scipy matrices of q = 12."""
     import torch
     import torch.distributed as dist
     import paper_1503_03467_b200 as gb
@@ -743,12 +745,19 @@ def run_dist(args, rank, world, local_rank):
               f"one {comm.backend} communicator over ranks 0..{world - 1}"
               + (" (NCCL_DEBUG=INFO prints its channels)" if comm.backend == "nccl" else ""),
               file=sys.stderr)
-    grid, M, A, load, tree = build_inputs(q, cfg["coeff"], 0)  # the one shared instance
-    c = (gb.coefficient_example1(grid) if cfg["coeff"] == "example1"
-         else gb.coefficient_checkerboard(grid, 1e4, instance_seeds(0)[0]))
+    # the one instance every rank shares (rank-0 seeds of BASELINE's config)
+    grid = gb.build_grid(q)
+    tree = gb.build_hierarchy(grid)
+    if cfg["coeff"] == "example1":
+        c = gb.coefficient_example1(grid)
+        g_host = gb.example_load(grid)
+    else:
+        sa, sg = instance_seeds(0)
+        c = gb.coefficient_checkerboard(grid, 1e4, sa)
+        g_host = np.random.default_rng(sg).standard_normal(grid.num_nodes)
     Mb = gb.assemble_mass(grid, device=True)
     Ab = gb.assemble_stiffness(grid, c, device=True)
-    gd_dev = dv.to_dev(load.g_nodal)
+    gd_dev = dv.to_dev(g_host)
 
     def step():
         return gd.fast_solve_dist(comm, Mb, Ab, gd_dev, tree, EPS, uniform_rho=RHO)
@@ -787,12 +796,14 @@ def run_dist(args, rank, world, local_rank):
         dist.barrier()
         dv.Traffic.reset()
         t0 = time.perf_counter()
-        r2 = gd.fast_solve_dist(comm, M, A, load.g_nodal, tree, EPS, uniform_rho=RHO)
+        M2 = gb.assemble_mass(grid, device=True)
+        A2 = gb.assemble_stiffness(grid, c, device=True)   # uploads the cell values
+        r2 = gd.fast_solve_dist(comm, M2, A2, g_host, tree, EPS, uniform_rho=RHO)
         u = dv.to_host(r2.u)
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h2d, d2h = dv.Traffic.h2d, dv.Traffic.d2h
-        r2 = None
+        r2 = M2 = A2 = None
     e2e = reduce_max(float(np.median(e2e_ms)), world, "cuda")
     if rank != 0:
         return None

@@ -614,6 +614,11 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
 }
 
 constexpr int PN_LDA = 36, PN_LDB = 36, PN_KC = 32;
+// fine-point tile of one CTA: PN_FR rows x PN_FC consecutive columns (32 points)
+#ifndef GB_PN_FC
+#define GB_PN_FC 4
+#endif
+constexpr int PN_FC = GB_PN_FC, PN_FR = 32 / PN_FC;
 
 __device__ __forceinline__ int floordiv(int a, int b) {  // b > 0
   return a >= 0 ? a / b : -((-a + b - 1) / b);
@@ -657,16 +662,16 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     // union of the block rows' windows (origins are monotone in the row)
     const int us0 = out.origin(bi_s), us1 = out.origin(bi_s + nrs - 1) + out.wd - 1;
     const int ut0 = out.origin(bi_t), ut1 = out.origin(bi_t + nrt - 1) + out.wd - 1;
-    const int F0s = us0 + (tt / nft) * 8, F0t = ut0 + (tt % nft) * 4;
+    const int F0s = us0 + (tt / nft) * PN_FR, F0t = ut0 + (tt % nft) * PN_FC;
     if (F0s > us1 || F0t > ut1) continue;  // (uniform across the CTA)
-    if (F0s + 7 < f0 || F0s >= f1) continue;  // no fine row of the column strip [f0, f1)
+    if (F0s + PN_FR - 1 < f0 || F0s >= f1) continue;  // no fine row of the column strip [f0, f1)
     // parents in some ball whose Wpsi support [2ph+lo, 2ph+h+hi] meets F
     int ps0 = imax(bi_s - rho, 0), ps1 = imin(bi_s + nrs - 1 + rho, Lp - 1);
     int pt0 = imax(bi_t - rho, 0), pt1 = imin(bi_t + nrt - 1 + rho, Lp - 1);
     ps0 = imax(ps0, floordiv(F0s - h - hi, 2 * h));
-    ps1 = imin(ps1, floordiv(F0s + 7 - lo, 2 * h));
+    ps1 = imin(ps1, floordiv(F0s + PN_FR - 1 - lo, 2 * h));
     pt0 = imax(pt0, floordiv(F0t - h - hi, 2 * h));
-    pt1 = imin(pt1, floordiv(F0t + 3 - lo, 2 * h));
+    pt1 = imin(pt1, floordiv(F0t + PN_FC - 1 - lo, 2 * h));
     const int nps = ps1 - ps0 + 1, npt = pt1 - pt0 + 1;
     const int K = (nps > 0 && npt > 0) ? nps * npt * 3 : 0;
     double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -677,7 +682,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     const bool arow = am < TB * TB && ams < nrs && amt < nrt && ais >= r0 && ais < r1;
     const double* drow = Dt + ((long long)ais * Lp + ait) * SD;
     const int n_ = threadIdx.x & 31;
-    const int bfs = F0s + (n_ >> 2), bft = F0t + (n_ & 3);
+    const int bfs = F0s + n_ / PN_FC, bft = F0t + n_ % PN_FC;
     // chunk metadata (threads < PN_KC) into buffer u
     const int arowoff = ((ais - rho) * side + (ait - rho)) * 3;
     const long long bfsw = (long long)bfs * par.wd + bft;
@@ -770,7 +775,7 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int n = warp * 8 + 2 * (lane & 3) + j;
-          const int fs = F0s + (n >> 2), ft = F0t + (n & 3);
+          const int fs = F0s + n / PN_FC, ft = F0t + n % PN_FC;
           const int ls = fs - os, lt = ft - ot;
           if (ls < 0 || ls >= out.wd || lt < 0 || lt >= out.wd) continue;
           if (fs < f0 || fs >= f1) continue;
@@ -1266,7 +1271,7 @@ int gbk_psi_next_raw_rows(int n, int Lk, int lo, int hi, int wd, const double* p
     const int TB = Lp < 4 ? Lp : 4;
     const int hp = n / Lp;  // output row spacing (fine units)
     const int span = imin(wd2 + (TB - 1) * hp, n);
-    const int nfs = (span + 7) / 8, nft = (span + 3) / 4;
+    const int nfs = (span + PN_FR - 1) / PN_FR, nft = (span + PN_FC - 1) / PN_FC;
     const long long nb = (Lp + TB - 1) / TB;
     const long long nrb = (r1 + TB - 1) / TB - r0 / TB;
     const long long nt = nrb * nb * nfs * nft;

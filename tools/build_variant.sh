@@ -7,7 +7,7 @@ name=$1; shift
 out=build/variants/$name; mkdir -p $out
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC"
 objs=""
-for s in gb_box gb_patch gb_products gb_krylov gb_dense gb_diag gb_capi; do
+for s in gb_box gb_patch gb_products gb_krylov gb_dense gb_diag gb_3d gb_capi; do
   nvcc $F "$@" -c paper_1503_03467_b200/csrc/$s.cu -o $out/$s.o &
   objs="$objs $out/$s.o"
 done
