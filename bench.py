@@ -823,6 +823,15 @@ def run_dist(args, rank, world, local_rank):
                 "launches_timed": len(timing["ms"]),
                 "timing": "CUDA events on rank 0's stream around its first 64 dual launches "
                           "of the finest level in every timed step (per GPU)"}
+    # the same configuration on ONE GPU (the N = 1 bench line is configs[2]):
+    # the committed single-GPU measurement of this config, for a like-for-like
+    # parallel efficiency
+    single = None
+    sf = ROOT / "profiles" / f"r02_bench_{name}.json"
+    if sf.exists() and not args.q:
+        sd = json.loads(sf.read_text())
+        single = {"value": sd["value"], "unit": sd["unit"], "ms_per_step": sd["ms_per_step"],
+                  "source": f"profiles/{sf.name} (bench.py --config {name} on one B200)"}
     cfgo = workload_config(name, q, world)
     cfgo["parallelism"] = (f"spatial row strips over {world} GPUs: levels with >= "
                            f"{gd.min_distributed_rows(world)} parent rows distributed (halo "
@@ -839,6 +848,7 @@ def run_dist(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": None,
         "clocks": clk.summary(),
+        "single_gpu_same_config": single,
         "per_rank_peak_bytes": int(peak), "per_rank_halo_bytes_per_step": int(halo),
         "subband_iterations": {str(k): v for k, v in sorted(its.items())},
         "krylov_passes": {str(k): list(v) for k, v in passes.items()},

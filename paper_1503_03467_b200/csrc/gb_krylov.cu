@@ -1645,7 +1645,10 @@ __global__ void k_vadd(long long n, const double* __restrict__ a, const double* 
 
 using namespace gb;
 
-static const int kRedBlocks = 148 * 8;  // 8 per SM on 148 SMs; partials sized by the caller
+#ifndef GB_RED_BLOCKS
+#define GB_RED_BLOCKS (148 * 8)
+#endif
+static const int kRedBlocks = GB_RED_BLOCKS;  // 8 per SM on 148 SMs; partials sized by the caller
 
 static inline int grid_for(long long work, int block, int cap) {
   long long g = (work + block - 1) / block;
@@ -2719,20 +2722,28 @@ int gbk_level_engine(gb_level_engine_args* e, cudaStream_t s, long long* launche
   long long nl = 0;
   e->n_dual = e->n_single = 0;
   e->ev_n = 0;
-  std::vector<cudaEvent_t> ev;
-  if (e->ev_cap > 0 && e->ev_ms) {
-    ev.resize(2 * (size_t)e->ev_cap);
-    for (auto& x : ev) cudaEventCreate(&x);
+  // timing events come from a per-thread pool that only grows (an engine
+  // runs on one worker thread): no event is created or destroyed in a
+  // steady-state step
+  static thread_local std::vector<cudaEvent_t> ev;
+  const bool timing = e->ev_cap > 0 && e->ev_ms;
+  if (timing) {
+    const size_t need = 2 * (size_t)e->ev_cap;
+    while (ev.size() < need) {
+      cudaEvent_t x;
+      if (cudaEventCreate(&x) != cudaSuccess) break;
+      ev.push_back(x);
+    }
+    if (ev.size() < need) e->ev_cap = (int)(ev.size() / 2);
     e->ev_events = ev.data();
   } else {
     e->ev_events = nullptr;
   }
   int rc = level_engine(e, s, nl);
-  if (!ev.empty()) {
+  if (timing) {
     const cudaError_t se = e->ev_n > 0 ? cudaEventSynchronize(ev[2 * e->ev_n - 1]) : cudaSuccess;
     for (int i = 0; i < e->ev_n && se == cudaSuccess; ++i)
       cudaEventElapsedTime(&e->ev_ms[i], ev[2 * i], ev[2 * i + 1]);
-    for (auto& x : ev) cudaEventDestroy(x);
     e->ev_events = nullptr;
     if (!rc && se != cudaSuccess) rc = (int)se;
   }
