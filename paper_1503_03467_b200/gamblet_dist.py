@@ -449,7 +449,8 @@ class _InlineTasks(gf._LevelTasks):
 
 
 def fast_solve_dist(comm: Comm, M, A, g_nodal, tree, epsilon, uniform_rho=None, c_rho=None,
-                    w_variant="orthonormal", lean=True, keep=False, spectral=True):
+                    w_variant="orthonormal", lean=True, keep=False, spectral=True,
+                    force_strips=False):
     """gamblet_fast.fast_solve (nodal load) on `comm.world` ranks, this rank's
     part.  M, A: the whole mass / stiffness matrix on every rank (BoxMatrix
     from grid_fem.assemble_*(device=True), DeviceCSR or canonical scipy CSR:
@@ -457,7 +458,9 @@ def fast_solve_dist(comm: Comm, M, A, g_nodal, tree, epsilon, uniform_rho=None, 
 
     Returns a DistResult; `u` is the whole solution on every rank.  keep=True
     retains this rank's strips of every distributed level (parity tests);
-    lean=True releases each operator once consumed."""
+    lean=True releases each operator once consumed.  force_strips=True runs the
+    strip program even on one rank (a single strip, no exchange): the
+    single-GPU measurement of the partitioned code path."""
     comm = comm if comm is not None else SelfComm()
     q = tree.q
     n = 1 << q
@@ -493,7 +496,7 @@ def fast_solve_dist(comm: Comm, M, A, g_nodal, tree, epsilon, uniform_rho=None, 
     # ------------------------------------------------------------------
     # level q: psi^(q) by mass patches, A^(q) = psi A psi^T (gamblet_fast._level_q)
     # ------------------------------------------------------------------
-    dist_q = world > 1 and n // 2 >= Lmin
+    dist_q = (world > 1 or force_strips) and n // 2 >= Lmin
     if not dist_q:
         # nothing to split at this size: the single-GPU program on every rank
         # (world == 1, or a grid too small for strips)

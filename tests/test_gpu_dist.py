@@ -198,3 +198,21 @@ def test_two_processes_gloo_share_the_gpu(tmp_path):
     assert np.array_equal(got, Aq.vals.cpu().numpy())
     meta = np.load(tmp_path / "meta_0.npy")
     assert meta[0] < q and meta[1] > 0
+
+
+def test_strip_program_on_one_rank_matches_the_pipeline():
+    """force_strips: the partitioned code path with a single strip (no
+    exchange) -- same transform bits, same solution to the solver tolerance."""
+    from paper_1503_03467_b200 import comm as cm, gamblet_dist as gd
+    q = 7
+    grid, M, A, g, tree = _inputs(q)
+    levels, u_ref, _ = _single(M, A, g, tree)
+    res = gd.fast_solve_dist(cm.SelfComm(), M, A, g, tree, EPS, uniform_rho=RHO, keep=True,
+                             force_strips=True)
+    assert res.first_replicated < q
+    for k in range(q, res.first_replicated - 1, -1):
+        L = 1 << k
+        assert torch.equal(res.strips[k]["A"].rows(0, L), levels[k].raw("stiffness").vals), k
+        assert torch.equal(res.strips[k]["psi"].rows(0, L), levels[k].raw("psi").vals), k
+    err = float((res.u - u_ref).norm() / u_ref.norm())
+    assert err <= 1e-9, err
