@@ -1857,28 +1857,47 @@ static void sym_phase1(int L, int w, const double* U, int nv, const double* x0, 
   // dynamic shared memory attribute raised to what a launch needs (the
   // kernels also have static shared memory, so the 227 KB cap is not usable)
   static size_t attr[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  const bool ws = GB_SYM_WS && g_sym_ws_on && symb_ws_smem(w, nv) <= 226 * 1024;
+  static size_t attr2[3] = {0, 0, 0};  // the 2-stage instances
+  const int st_pref = nv == 1 ? symb_ws_stages<1>() : symb_ws_stages<2>();
+#ifndef GB_SYM_MIN_STAGES
+#define GB_SYM_MIN_STAGES 2
+#endif
+  const int st = symb_ws_smem(w, nv, st_pref) <= 226 * 1024 ? st_pref : GB_SYM_MIN_STAGES;
+  const bool ws = GB_SYM_WS && g_sym_ws_on && symb_ws_smem(w, nv, st) <= 226 * 1024;
   if (ws) {
     // persistent: one CTA per SM, at most g_sym_ws_ctas (the HBM stream
     // saturates on fewer SMs; the rest stay free for the concurrent setup)
     const int cap = g_sym_ws_ctas > 0 && g_sym_ws_ctas < 148 ? g_sym_ws_ctas : 148;
     const int gp = nt < cap ? nt : cap;
-    const size_t sm = symb_ws_smem(w, nv);
-    if (sm > attr[1][nv]) {
-      if (nv == 2)
-        cudaFuncSetAttribute(k_symb_apply_ws<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t sm = symb_ws_smem(w, nv, st);
+    size_t& have = st == st_pref ? attr[1][nv] : attr2[nv];
+    if (sm > have) {
+      if (nv == 2 && st == 3)
+        cudaFuncSetAttribute(k_symb_apply_ws<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+      else if (nv == 2)
+        cudaFuncSetAttribute(k_symb_apply_ws<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+      else if (st == 4)
+        cudaFuncSetAttribute(k_symb_apply_ws<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sm);
       else
-        cudaFuncSetAttribute(k_symb_apply_ws<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_symb_apply_ws<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sm);
-      attr[1][nv] = sm;
+      have = sm;
     }
-    if (nv == 2)
-      k_symb_apply_ws<2><<<gp, 2 * kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1,
-                                                              y1, s1, p1, r1, t0, t1);
+    if (nv == 2 && st == 3)
+      k_symb_apply_ws<2, 3><<<gp, 2 * kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1,
+                                                                 y1, s1, p1, r1, t0, t1);
+    else if (nv == 2)
+      k_symb_apply_ws<2, 2><<<gp, 2 * kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, x1,
+                                                                 y1, s1, p1, r1, t0, t1);
+    else if (st == 4)
+      k_symb_apply_ws<1, 4><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr,
+                                                             nullptr, nullptr, nullptr, 0, t0, t1);
     else
-      k_symb_apply_ws<1><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr,
-                                                          nullptr, nullptr, nullptr, 0, t0, t1);
+      k_symb_apply_ws<1, 2><<<gp, kSymThreads + 32, sm, s>>>(L, w, U, x0, y0, s0, p0, r0, nullptr,
+                                                             nullptr, nullptr, nullptr, 0, t0, t1);
     return;
   }
   const int gp = nt < kRedBlocks ? nt : kRedBlocks;
@@ -2248,8 +2267,8 @@ int gbk_bjcg_solve2(int L, int w, const double* BsT, const float* inv, double* c
   // bitwise equality with the single solve needs the same phase-1 kernel
   // family for one and two vectors (the warp-specialized one; the dot
   // partials of the register-pipelined fallback are formed in another order)
-  if (!use_sym(1, L, 3, w) || !GB_SYM_WS || !g_sym_ws_on || symb_ws_smem(w, 1) > 226 * 1024 ||
-      symb_ws_smem(w, 2) > 226 * 1024)
+  if (!use_sym(1, L, 3, w) || !GB_SYM_WS || !g_sym_ws_on ||
+      symb_ws_smem(w, 1, 2) > 226 * 1024 || symb_ws_smem(w, 2, 2) > 226 * 1024)
     return GB_UNSUPPORTED;
   const int Lpad = L + 2 * w;
   const long long npad = (long long)Lpad * Lpad * 3;

@@ -323,12 +323,13 @@ __device__ __forceinline__ void consumer_sync() {  // the 8 consumer warps only
   asm volatile("bar.sync 1, %0;" ::"r"(kSymThreads) : "memory");
 }
 
+// preferred ring depth; wide stencils (w >= 5 with two vectors) fall back to
+// 2 stages so that the kernel still fits in shared memory
 template <int NV>
 __host__ __device__ constexpr int symb_ws_stages() { return NV == 1 ? 4 : 3; }
 
-static inline size_t symb_ws_smem(int w, int nv) {
+static inline size_t symb_ws_smem(int w, int nv, int st) {
   const int npos = symb_npos(w), WC = kSymTW + 2 * w, nwarp = 2 * kSymTH;
-  const int st = nv == 1 ? symb_ws_stages<1>() : symb_ws_stages<2>();
   return (size_t)2 * st * 8 +                                        // full/empty barriers
          (size_t)st * nwarp * kSymWsPairs * 32 * 16 +                 // U ring
          (size_t)nv * (kSymTH + w) * WC * 3 * 8 +                     // x windows
@@ -346,13 +347,12 @@ __device__ __forceinline__ void group_sync(int vec) {
 // vector adds warps -- latency hiding -- instead of lengthening every warp's
 // dependent shared-memory chains.  Each group runs exactly the single-vector
 // arithmetic (same order), the groups are independent between ring stages.
-template <int NV>
+template <int NV, int NS>
 __global__ void __launch_bounds__(NV * kSymThreads + 32, 1) k_symb_apply_ws(
     int L, int w, const double* __restrict__ U, const double* __restrict__ x0,
     double* __restrict__ y0, KState* s0, double* part0, int red0,
     const double* __restrict__ x1, double* __restrict__ y1, KState* s1, double* part1,
     int red1, long long tile0, long long tile1) {
-  constexpr int NS = symb_ws_stages<NV>();
   constexpr int NW = 2 * kSymTH;  // consumer warps per vector
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ double sh[32];
