@@ -513,15 +513,69 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
       : "d"(a), "d"(b));
 }
 
+// 16-byte global -> shared copy (LDGSTS, L2 only) and its completion wait
+__device__ __forceinline__ void k3_cp16(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void k3_cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// stage the 64 x 64 block K[row0 + rr][j0 + kk] (rr, kk < 64) row-major into
+// dst[rr * k3TLD + kk], zero beyond row m / column jb; asynchronous 16-byte
+// copies (ld and j0 are even, so every pair is aligned) -- the caller waits
+// (k3_cp_wait) before its barrier
+__device__ __forceinline__ void k3_stage(double* dst, const double* __restrict__ K, int ld,
+                                         int row0, int j0, int jb, int m, int tid) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int c = tid + 256 * u;
+    const int rr = c >> 5, kc = (c & 31) << 1;
+    double* d = dst + rr * k3TLD + kc;
+    const double* src = K + (long long)(row0 + rr) * ld + j0 + kc;
+    if (row0 + rr < m && kc + 2 <= jb) {
+      k3_cp16(d, src);
+    } else {
+      const bool r = row0 + rr < m;
+      d[0] = (r && kc < jb) ? src[0] : 0.0;
+      d[1] = (r && kc + 1 < jb) ? src[1] : 0.0;
+    }
+  }
+}
+
+// one 64 x 64 x jb block product on the FP64 tensor cores: acc[ii][jj] of
+// warp (wm, wn) += A[wm 32 + 8 ii + ., k] B[wn 16 + 8 jj + ., k] over k < jb,
+// both operands row-major (row, k) with leading dimension k3TLD
+__device__ __forceinline__ void k3_block_mma(const double* __restrict__ As,
+                                             const double* __restrict__ Bs, int jb, int wm,
+                                             int wn, int fr, int fk, double acc[4][2][2]) {
+  const double* ap = As + (wm * 32 + fr) * k3TLD + fk;
+  const double* bp = Bs + (wn * 16 + fr) * k3TLD + fk;
+  for (int k4 = 0; k4 < jb; k4 += 4) {
+    double af[4], bf[2];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) af[ii] = ap[ii * 8 * k3TLD + k4];
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) bf[jj] = bp[jj * 8 * k3TLD + k4];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) dmma_884(acc[ii][jj][0], acc[ii][jj][1], af[ii], bf[jj]);
+  }
+}
+
 __global__ void __launch_bounds__(256) k3_correction_patches(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB,
     const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status,
     double* __restrict__ ws, int ld) {
-  extern __shared__ double dsm3[];
+  extern __shared__ __align__(16) double dsm3[];
+  // region 0 (64 x k3TLD doubles): the diagonal block D11 (64 x 65), y1 and
+  // dinv behind it -- free during the trailing update, where it is the second
+  // B-operand buffer
   double (*D11)[k3PB + 1] = reinterpret_cast<double (*)[k3PB + 1]>(dsm3);  // 64 x 65
   double* y1 = dsm3 + k3PB * (k3PB + 1);                                 // 64
   double* dinv = y1 + k3PB;                                              // 64: 1 / L_jj
-  double* As = dinv + k3PB;                                              // 64 x k3TLD
+  double* Bs2 = dsm3;                                                    // alias of region 0
+  double* As = dsm3 + k3PB * k3TLD;                                      // 64 x k3TLD
   double* Bs = As + k3PB * k3TLD;                                        // 64 x k3TLD
   __shared__ int bx0, by0, bz0, nx, ny, nz, bad;
   __shared__ double sh[32];
@@ -615,13 +669,26 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
         }
         for (int a = j + 1 + tid; a < jb; a += blockDim.x) D11[a][j] *= il;
         __syncthreads();
-        const int t = jb - j - 1;
-        for (int e = tid; e < t * (t + 1) / 2; e += blockDim.x) {
-          int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-          while (a * (a + 1) / 2 > e) --a;
-          while ((a + 1) * (a + 2) / 2 <= e) ++a;
-          const int b = e - a * (a + 1) / 2;
-          D11[a + j + 1][b + j + 1] -= D11[a + j + 1][j] * D11[b + j + 1][j];
+        // rank-1 update of the trailing triangle: thread (ty, tx) of a 16 x 16
+        // grid owns the entries (a, b) = (ty + 16 i, tx + 16 i2), b <= a
+        {
+          const int ty = tid >> 4, tx = tid & 15;
+          double ca[4], cb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            ca[i] = D11[ty + 16 * i][j];
+            cb[i] = D11[tx + 16 * i][j];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int a = ty + 16 * i;
+            if (a <= j || a >= jb) continue;
+#pragma unroll
+            for (int i2 = 0; i2 < 4; ++i2) {
+              const int b = tx + 16 * i2;
+              if (b > j && b <= a) D11[a][b] -= ca[i] * cb[i2];
+            }
+          }
         }
         __syncthreads();
       }
@@ -668,29 +735,15 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
         // operand is B[k][n] = T[n][k] (L21[r][n] = sum_k A21[r][k] T[n][k])
         const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fk = lane & 3;
         for (int rb = r0; rb < m; rb += 64) {
-          for (int e = tid; e < 64 * k3PB; e += blockDim.x) {
-            const int rr = e / k3PB, kk = e - rr * k3PB;
-            As[kk * k3TLD + rr] =
-                (rb + rr < m && kk < jb) ? K[(long long)(rb + rr) * ld + j0 + kk] : 0.0;
-          }
+          k3_stage(As, K, ld, rb, j0, jb, m, tid);
+          k3_cp_wait();
           __syncthreads();
           double acc[4][2][2];
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) acc[ii][jj][0] = acc[ii][jj][1] = 0.0;
-          for (int k4 = 0; k4 < jb; k4 += 4) {
-            double af[4], bf[2];
-#pragma unroll
-            for (int ii = 0; ii < 4; ++ii) af[ii] = As[(k4 + fk) * k3TLD + wm * 32 + ii * 8 + fr];
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-              bf[jj] = T[(wn * 16 + jj * 8 + fr) * k3TLD + k4 + fk];
-#pragma unroll
-            for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-              for (int jj = 0; jj < 2; ++jj) dmma_884(acc[ii][jj][0], acc[ii][jj][1], af[ii], bf[jj]);
-          }
+          k3_block_mma(As, T, jb, wm, wn, fr, fk, acc);
           __syncthreads();  // As is reused by the next row block
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
@@ -716,46 +769,45 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
         __syncthreads();
       }
       // (c) trailing update K22 -= L21 L21^T (lower), 64 x 64 output blocks:
-      // the two L21 row blocks staged k-major in shared memory, warp (wm, wn)
-      // of a 2 x 4 grid owns 32 x 16 = 4 x 2 DMMA m8n8k4 accumulators
+      // the row block of L21 (A operand) staged once per block row, the
+      // column blocks (B operand) streamed through two buffers (the next one
+      // copied asynchronously while the current one is multiplied); warp
+      // (wm, wn) of a 2 x 4 grid owns 32 x 16 = 4 x 2 DMMA m8n8k4
+      // accumulators.  The K entries a thread updates are loaded before its
+      // products, so their latency overlaps the tensor-core work.
       const int nbk = (m - r0 + 63) / 64;
       const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fk = lane & 3;
       for (int bi = 0; bi < nbk; ++bi) {
         const int ib = r0 + bi * 64;
-        for (int e = tid; e < 64 * k3PB; e += blockDim.x) {  // A rows block
-          const int rr = e / k3PB, kk = e - rr * k3PB;
-          As[kk * k3TLD + rr] =
-              (ib + rr < m && kk < jb) ? K[(long long)(ib + rr) * ld + j0 + kk] : 0.0;
-        }
+        __syncthreads();  // every warp is done with the buffers of block row bi - 1
+        k3_stage(As, K, ld, ib, j0, jb, m, tid);
+        if (bi > 0) k3_stage(Bs, K, ld, r0, j0, jb, m, tid);  // column block 0
         for (int bj = 0; bj <= bi; ++bj) {
           const int jbase = r0 + bj * 64;
-          __syncthreads();
-          if (bj == bi) {
-            for (int e = tid; e < 64 * k3TLD; e += blockDim.x) Bs[e] = As[e];
-          } else {
-            for (int e = tid; e < 64 * k3PB; e += blockDim.x) {
-              const int rr = e / k3PB, kk = e - rr * k3PB;
-              Bs[kk * k3TLD + rr] =
-                  (jbase + rr < m && kk < jb) ? K[(long long)(jbase + rr) * ld + j0 + kk] : 0.0;
+          const double* Bc = bj == bi ? As : ((bj & 1) ? Bs2 : Bs);
+          k3_cp_wait();
+          __syncthreads();  // block bj (and As) landed; buffer (bj + 1) & 1 is free
+          if (bj + 1 < bi) k3_stage((bj & 1) ? Bs : Bs2, K, ld, jbase + 64, j0, jb, m, tid);
+          double kold[4][2][2];
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int gr = ib + wm * 32 + ii * 8 + fr;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int gc = jbase + wn * 16 + jj * 8 + 2 * fk;
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2)
+                kold[ii][jj][e2] = (gr < m && gc + e2 < m && gc + e2 <= gr)
+                                       ? __ldcg(K + (long long)gr * ld + gc + e2)
+                                       : 0.0;
             }
           }
-          __syncthreads();
           double acc[4][2][2];
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) acc[ii][jj][0] = acc[ii][jj][1] = 0.0;
-          for (int k4 = 0; k4 < jb; k4 += 4) {
-            double af[4], bf[2];
-#pragma unroll
-            for (int ii = 0; ii < 4; ++ii) af[ii] = As[(k4 + fk) * k3TLD + wm * 32 + ii * 8 + fr];
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) bf[jj] = Bs[(k4 + fk) * k3TLD + wn * 16 + jj * 8 + fr];
-#pragma unroll
-            for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-              for (int jj = 0; jj < 2; ++jj) dmma_884(acc[ii][jj][0], acc[ii][jj][1], af[ii], bf[jj]);
-          }
+          k3_block_mma(As, Bc, jb, wm, wn, fr, fk, acc);
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
             const int gr = ib + wm * 32 + ii * 8 + fr;
@@ -765,24 +817,48 @@ __global__ void __launch_bounds__(256) k3_correction_patches(
 #pragma unroll
               for (int e2 = 0; e2 < 2; ++e2) {
                 const int gc = jbase + wn * 16 + jj * 8 + 2 * fk + e2;
-                if (gc < m && gc <= gr) K[(long long)gr * ld + gc] -= acc[ii][jj][e2];
+                if (gc < m && gc <= gr)
+                  K[(long long)gr * ld + gc] = kold[ii][jj][e2] - acc[ii][jj][e2];
               }
           }
         }
-        __syncthreads();
       }
+      __syncthreads();
     }
     if (bad) {
       if (tid == 0) raise_status(status, ST_NOT_SPD, i);
       __syncthreads();
       continue;
     }
-    // back substitution L^T z = y (row j of L is contiguous)
-    for (int j = m - 1; j >= 0; --j) {
-      if (tid == 0) v[j] /= K[(long long)j * ld + j];
+    // back substitution L^T z = y in blocks of 64 rows (row j of L is
+    // contiguous): the block's own triangle by one warp on a shared-memory
+    // copy, then v[a] -= sum_j L[j][a] z_j for every a above the block (one
+    // thread per a, coalesced over a, no barrier inside)
+    for (int jb0 = ((m - 1) / k3PB) * k3PB; jb0 >= 0; jb0 -= k3PB) {
+      const int nb = imin(k3PB, m - jb0);
+      for (int e = tid; e < nb * nb; e += blockDim.x) {
+        const int a = e / nb, b = e - a * nb;
+        D11[a][b] = b <= a ? K[(long long)(jb0 + a) * ld + jb0 + b] : 0.0;
+      }
+      if (tid < nb) y1[tid] = v[jb0 + tid];
       __syncthreads();
-      const double zj = v[j];
-      for (int a = tid; a < j; a += blockDim.x) v[a] -= K[(long long)j * ld + a] * zj;
+      if (warp == 0) {
+        for (int j = nb - 1; j >= 0; --j) {
+          if (lane == 0) y1[j] /= D11[j][j];
+          __syncwarp();
+          const double zj = y1[j];
+          for (int a = lane; a < j; a += 32) y1[a] -= D11[j][a] * zj;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (tid < nb) v[jb0 + tid] = y1[tid];
+      for (int a = tid; a < jb0; a += blockDim.x) {
+        double acc = 0.0;
+        for (int j = nb - 1; j >= 0; --j)
+          acc = fma(__ldcg(K + (long long)(jb0 + j) * ld + a), y1[j], acc);
+        v[a] -= acc;
+      }
       __syncthreads();
     }
     // D^T row i = s z, row-tail trim (1e-11 rowmax), box slots (ball offset, c)
@@ -1168,7 +1244,12 @@ int gbk3_level_blocks(int Lk, int wA, const double* A, const double* host_w, int
   k3_level_blocks<<<grid3(work, 128), 128, 0, s>>>(Lk, wA, A, w7x8(host_w), wB, Braw, G, PAPt);
   return (int)cudaGetLastError();
 }
-int gbk3_correction_ld(int rho) { return 7 * (2 * rho + 1) * (2 * rho + 1) * (2 * rho + 1); }
+// leading dimension of a patch workspace: the largest patch size rounded up to a
+// multiple of 4 (16-byte aligned row pairs for the asynchronous staging copies)
+int gbk3_correction_ld(int rho) {
+  const int m = 7 * (2 * rho + 1) * (2 * rho + 1) * (2 * rho + 1);
+  return (m + 3) & ~3;
+}
 size_t gbk3_correction_workspace(int Lp, int rho, int ctas) {
   const long long ld = gbk3_correction_ld(rho);
   (void)Lp;
@@ -1179,7 +1260,7 @@ int gbk3_correction_patches(int Lp, int wB, const double* B, const double* sB, c
                             cudaStream_t s) {
   const long long P = (long long)Lp * Lp * Lp;
   const int g = (int)(P < ctas ? P : ctas);
-  const size_t smem = ((size_t)k3PB * (k3PB + 1) + 2 * k3PB + 2 * (size_t)k3PB * k3TLD) * 8;
+  const size_t smem = 3 * (size_t)k3PB * k3TLD * 8;  // region 0 (D11 / B buffer 2), As, Bs
   cudaError_t e = cudaFuncSetAttribute(k3_correction_patches,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
