@@ -563,7 +563,7 @@ __device__ __forceinline__ void k3_block_mma(const double* __restrict__ As,
   }
 }
 
-__global__ void __launch_bounds__(256) k3_correction_patches(
+__global__ void __launch_bounds__(256, 2) k3_correction_patches(
     int Lp, int wB, const double* __restrict__ B, const double* __restrict__ sB,
     const double* __restrict__ G, int rho, double* __restrict__ Dt, long long* status,
     double* __restrict__ ws, int ld) {
