@@ -2439,6 +2439,27 @@ __global__ void __launch_bounds__(256) k3_box_apply(int L, int nr, int w,
     const long long base = p * nr;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int e = lane;
+    // rows whose whole stencil is inside the domain (warp-uniform): the same
+    // sums without the per-slot domain tests
+    if (xlo == 0 && xhi == 2 * w && ylo == 0 && yhi == 2 * w && zlo == 0 && zhi == 2 * w) {
+      for (; e + 96 < S; e += 128) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int eu = e + 32 * u;
+          const long long col = base + toff[eu];
+          v[u] = (row[eu] * sr) * sv[col] * x[col];
+        }
+        a0 += v[0];
+        a1 += v[1];
+        a2 += v[2];
+        a3 += v[3];
+      }
+      for (; e < S; e += 32) {
+        const long long col = base + toff[e];
+        a0 += (row[e] * sr) * sv[col] * x[col];
+      }
+    }
     for (; e + 96 < S; e += 128) {
       double v[4];
 #pragma unroll
