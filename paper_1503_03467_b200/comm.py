@@ -88,6 +88,10 @@ class Comm:
     def allgather_rows(self, buf, L, row_elems):
         return
 
+    def broadcast(self, t, src):
+        """t of rank `src` on every rank."""
+        return t
+
     def barrier(self):
         return
 
@@ -207,6 +211,20 @@ class TorchComm(Comm):
                 self.dist.broadcast(view, src=self._global(r), group=self.group)
             if r == self.rank:
                 self.bytes_sent += view.numel() * view.element_size()
+
+    def broadcast(self, t, src):
+        if self.world == 1:
+            return t
+        if self._stage(t):
+            h = t.cpu()
+            self.dist.broadcast(h, src=self._global(src), group=self.group)
+            if src != self.rank:
+                t.copy_(h)
+        else:
+            self.dist.broadcast(t, src=self._global(src), group=self.group)
+        if src == self.rank:
+            self.bytes_sent += t.numel() * t.element_size()
+        return t
 
     def _global(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
@@ -332,6 +350,17 @@ class ThreadComm(Comm):
             self._wait(buf, ev)
             buf[a * row_elems:b * row_elems].copy_(src[a * row_elems:b * row_elems])
         self._retire(buf)
+
+    def broadcast(self, t, src):
+        if self.world == 1:
+            return t
+        self._publish(t)
+        if src != self.rank:
+            buf, ev = self.hub.slot[src]
+            self._wait(t, ev)
+            t.copy_(buf)
+        self._retire(t)
+        return t
 
     def barrier(self):
         self._sync()

@@ -30,7 +30,10 @@ rows above it go to the neighbour, and two small all-reduces carry the CG /
 Lanczos scalars (csrc/gb_dist.cuh).
 
 Coarser levels are *replicated* (every rank runs gamblet_fast's level step on
-the whole small level -- identical bits on every rank) except psi, whose rows
+the whole small level -- identical bits on every rank); their subband systems
+are independent, so each is solved by one owner rank (levels
+dealt round-robin, the owners work concurrently) and broadcast.  The
+exception to replication is psi, whose rows
 get wider as the level gets coarser: there a rank keeps the *column strip* of
 every psi^(k) row (the window points whose fine row it owns), which makes
 psi^(k-1), W psi and the increments psi^T W^T w local; only the row maxima of
@@ -422,30 +425,41 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
     return out
 
 
-class _InlineTasks(gf._LevelTasks):
-    """Level tasks run on the calling thread and stream (the replicated levels
-    of a partitioned run: every rank runs them identically, in order)."""
-
-    def __init__(self, solver):
-        self.futures = []
-        self.solver = solver
-        self._done = []
-
-    @classmethod
-    def _stream(cls):
-        return torch.cuda.current_stream()
+class _NoTasks:
+    """Level-step spool that runs nothing: the replicated levels' solves are
+    assigned to owner ranks afterwards."""
 
     def submit(self, level, op, k, g=None):
-        ev = torch.cuda.Event()
-        ev.record()
-        psi = level.raw("psi") if self.solver is not None else None
-        level._krylov_op = op
-        self._done.append(self._run(level, op, k, g, ev, psi))
+        return
 
     def join(self, counter):
-        done, self._done = self._done, []
-        for calls, (op_n, op_slots, _), _, _ in done:
-            counter.add("spectral", 2 * op_n * op_slots * calls)
+        return
+
+
+def _psi_next_cols(comm, level, psiw, n, k, sched, w12, f0, f1, s):
+    """psi^(k-1) from psi^(k) and the level's D^T on this rank's column strip
+    (the window points with fine row in [f0, f1)): the psi part of
+    gamblet_fast.local_level_step (gamblet_fast.py:615-624), row maxima of the
+    tail drop max-reduced over the ranks."""
+    Lk, Lp = 1 << k, 1 << (k - 1)
+    P, J = Lp * Lp, 3 * Lp * Lp
+    rho = int(min(sched.rho(k - 1), Lp - 1))
+    Dt = level.raw("correction").vals
+    h = n // Lk
+    lo, hi, wd = psiw.lo, psiw.hi, psiw.wd
+    wdw = min(hi - lo + 1 + h, n)
+    Wpsi = dv.empty(J * wdw * wdw)
+    lo2, hi2 = -2 * rho * h + lo, (2 * rho + 1) * h + hi
+    wd2 = PsiWindows.window(n, lo2, hi2)
+    pv = dv.empty(P * wd2 * wd2)
+    rmax = dv.empty(P)
+    nat.call("gb_wpsi_rows", n, Lk, lo, wd, w12, dv.ptr(psiw.vals), wdw, dv.ptr(Wpsi), 0, Lp,
+             f0, f1, s)
+    nat.call("gb_psi_next_raw_rows", n, Lk, lo, hi, wd, dv.ptr(psiw.vals), wdw, dv.ptr(Wpsi),
+             rho, dv.ptr(Dt), lo2, wd2, dv.ptr(pv), dv.ptr(rmax), 0, Lp, f0, f1, s)
+    comm.allreduce(rmax, "max")
+    nat.call("gb_psi_drop_rows", n, Lp, lo2, wd2, dv.ptr(pv), dv.ptr(rmax), 0, Lp, f0, f1, s)
+    return PsiWindows(pv, n, Lp, lo2, hi2)
 
 
 def fast_solve_dist(comm: Comm, M, A, g_nodal, tree, epsilon, uniform_rho=None, c_rho=None,
@@ -697,32 +711,74 @@ def fast_solve_dist(comm: Comm, M, A, g_nodal, tree, epsilon, uniform_rho=None, 
     psifull[psi.a * Lk * per:psi.b * Lk * per].copy_(psi.t)
     if not keep:
         del psi, Ak, gk
-    level = gf.LocalGambletLevel(k, PsiWindows(psifull, n, Lk, psi_lo, psi_hi),
-                                 BoxMatrix(Afull, Lk, 1, wA, 1))
+    # (R1) the operators of the replicated levels -- B^(k), D, R, A^(k-1), no
+    # psi yet: every rank, identical bits (the levels are small)
+    level = gf.LocalGambletLevel(k, None, BoxMatrix(Afull, Lk, 1, wA, 1))
     level._repair_slot_a = -1
     levels = {k: level}
     records = []
     solver = gf._LevelSolver(levels, tree, tol, counter, records)
     solver.fine_rows = (f0, f1)
-    spool = _InlineTasks(solver)
-    gcur = gfull
+    gs = {k: gfull}
     for kk in range(k, 1, -1):
-        level = gf.local_level_step(level, tree, sched, w_variant=w_variant, counter=counter,
-                                    _ctx=ctx, _spool=spool, _g=gcur, _lean=False,
-                                    _cols=(f0, f1, comm))
-        levels[kk - 1] = level
-        gcur = solver.restrict(kk, gcur)
+        levels[kk - 1] = gf.local_level_step(levels[kk], tree, sched, w_variant=w_variant,
+                                             counter=counter, _ctx=ctx, _spool=_NoTasks(),
+                                             _g=None, _lean=False)
+        gs[kk - 1] = solver.restrict(kk, gs[kk])
+    # (R2) the independent subband systems of those levels (SPEC.md:401,
+    # PAPER.md:1515), one owner rank each: the owners solve concurrently,
+    # then every rank receives every w^(k) (and the lambda estimates)
+    prep, sols = {}, {}
+    for kk in range(k, 1, -1):
+        owner = (k - kk) % world
+        op, sBk, rhs = solver.subband_rhs(kk, gs[kk])
+        prep[kk] = (op, sBk)
+        zp = op.vec()
+        sc = dv.zeros(6)
+        if owner == rank:
+            if spectral and gf.PAIRED_ENGINE and gf._engine_ok(op):
+                out = gf._paired_level(op, op.pad(rhs), tol)
+                z, vals = out["x"], (out["its"], out["rel"], out["conv"], out["brk"],
+                                     out["lam_min"], out["lam_max"])
+            else:
+                lmin = lmax = float("nan")
+                if spectral:
+                    lmin, lmax, _ = gf._eig_extremes(op)
+                z, its, rel, conv, brk, _ = gf._pcg(op, op.pad(rhs), tol)
+                vals = (its, rel, conv, brk, lmin, lmax)
+            zp.copy_(z)
+            sc.copy_(torch.tensor([float(v) for v in vals], dtype=torch.float64))
+        sols[kk] = (owner, zp, sc)
+        del rhs
+    for kk in range(k, 1, -1):
+        owner, zp, sc = sols[kk]
+        comm.broadcast(zp, owner)
+        comm.broadcast(sc, owner)
+    # (R3) psi^(k-1) = drop_row(0.25 P psi + D^T W psi) down the replicated
+    # levels on this rank's column strip, each level's increment formed before
+    # its psi^(k) is released
+    psik = PsiWindows(psifull, n, Lk, psi_lo, psi_hi)
+    for kk in range(k, 1, -1):
+        owner, zp, sc = sols[kk]
+        its, rel, conv, brk, lmin, lmax = dv.to_host(sc).tolist()
+        levels[kk].psi = psik
+        if spectral:
+            levels[kk].lambda_min_subband, levels[kk].lambda_max_subband = lmin, lmax
         res.lambdas[kk] = (levels[kk].lambda_min_subband, levels[kk].lambda_max_subband)
+        res.iterations[kk] = int(its)
+        op, sBk = prep[kk]
+        solver.subband_finish(kk, op, sBk, zp, int(its), rel, bool(conv), int(brk), psi=psik)
+        psin = _psi_next_cols(comm, levels[kk], psik, n, kk, sched, w12, f0, f1, s)
         if lean and not keep:
             levels[kk].psi = None
-    spool.join(counter)
-    solver.coarse(gcur)
+        psik = psin
+        del sols[kk], prep[kk]
+    levels[1].psi = psik
+    solver.coarse(gs[1])
     for kk in sorted(solver.incs.keys(), reverse=True):
         inc = solver.incs.device(kk)
         nat.call("gb_vadd", (f1 - f0) * n, dv.ptr(uacc) + f0 * n * 8,
                  inc.data_ptr() + f0 * n * 8, dv.ptr(uacc) + f0 * n * 8, s)
-    for kk, its in zip(range(k, 1, -1), counter.iterations.get("line8", [])):
-        res.iterations[kk] = int(its)
     ctx.check()
     # hand the overhang of the distributed levels' increments to its owners,
     # then every rank collects the whole solution

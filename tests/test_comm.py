@@ -60,6 +60,9 @@ def _exercise(comm, full, L, row_elems):
     g = torch.zeros_like(full)
     g[r0 * row_elems:r1 * row_elems] = full[r0 * row_elems:r1 * row_elems]
     comm.allgather_rows(g, L, row_elems)
+    bc = torch.full((5,), float(comm.rank), dtype=torch.float64)
+    comm.broadcast(bc, comm.world - 1)
+    assert torch.equal(bc, torch.full((5,), comm.world - 1.0, dtype=torch.float64))
     return dict(ok_halo=ok_halo, untouched=untouched, own=own.numpy(), tsum=tsum.numpy(),
                 tmax=tmax.numpy(), tmin=tmin.numpy(), gathered=torch.equal(g, full),
                 strip=(r0, r1))
