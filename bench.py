@@ -367,6 +367,7 @@ def run_3d(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     launches0 = nat.query("gb_launch_count")
+    dv.Prof.reset(enabled=True)  # CUDA-event spans of the phases, live in the timed steps
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         ev0.record()
@@ -377,6 +378,8 @@ def run_3d(args, rank, world, local_rank):
         ev1.record()
         torch.cuda.synchronize()
     launches = nat.query("gb_launch_count") - launches0
+    phase_ms = {k: v / args.steps for k, v in dv.Prof.times_ms().items()}
+    dv.Prof.reset(enabled=False)
     ms = reduce_max(ev0.elapsed_time(ev1) / args.steps, world, "cuda")
     iters = dict(res.iterations)
     res = None
@@ -397,6 +400,32 @@ def run_3d(args, rank, world, local_rank):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample_3d(q, os.cpu_count() or 1, 0)
+    # roofline of the dominant kernel: the correction patches of every level
+    # (k3_correction_patches, batched blocked Cholesky on the FP64 tensor
+    # cores), algorithmic flops sum over patches of m^3/3 + 2 m^2 with
+    # m = 7 x the clipped ball, over the phase's live CUDA-event span
+    roof = None
+    corr_ms = phase_ms.get("3d_correction_patches")
+    if corr_ms:
+        flops = 0.0
+        for k in range(q, 1, -1):
+            Lp = 1 << (k - 1)
+            rho = min(RHO3, Lp - 1)
+            ext = np.minimum(np.arange(Lp), rho) + np.minimum(Lp - 1 - np.arange(Lp), rho) + 1
+            m = 7.0 * np.multiply.outer(np.multiply.outer(ext, ext), ext).ravel()
+            flops += float((m ** 3 / 3.0 + 2.0 * m * m).sum())
+        fp64 = fp64_peak_tflops()
+        peak = max(fp64.values())
+        ach = flops / (corr_ms * 1e-3) / 1e12
+        roof = {"kernel": "k3_correction_patches (all levels: batched blocked Cholesky of the "
+                          "875 x 875 patch matrices, DMMA m8n8k4 trailing updates)",
+                "bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 3),
+                "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": None,
+                "peak_source": "FP64 tensor-core (DMMA) probe measured in-run; "
+                               "MEASURED_PEAKS.json has no fp64 figure",
+                "flops_per_step": flops, "ms_per_step": round(corr_ms, 2),
+                "timing": "CUDA events on the launching stream around the phase in every "
+                          "timed step"}
     return {
         "metric": METRIC, "value": round(whole_job_rate(N, world, ms), 1), "unit": "fine-DOF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
@@ -407,7 +436,8 @@ def run_3d(args, rank, world, local_rank):
         "e2e": {"value": round(whole_job_rate(N, world, e2e), 1), "unit": "fine-DOF/s",
                 "ms_per_step": round(e2e, 3), "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(launches), "roofline": None,
+        "gpu_launches": int(launches), "roofline": roof,
+        "phases_ms": {k: round(v, 2) for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
         "cpu_baseline": cpu, "clocks": clk.summary(),
         "krylov_iterations": {str(k): v for k, v in iters.items()},
     }
