@@ -654,10 +654,15 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
   const long long oper = (long long)out.wd * out.wd;
   const int h = child.h();  // child spacing (fine units); parents 2h
   const int lo = child.lo, hi = child.hi;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long blk = t / tpb;
-    const int tt = (int)(t - blk * tpb);
-    const int bi_s = (rb0 + (int)(blk / nbs)) * TB, bi_t = (int)(blk % nbs) * TB;
+  // h and TB are powers of two (dyadic levels; TB = min(Lp, 4)): the floor
+  // divisions of the tile setup and of the epilogue are shifts
+  const int sh2h = 31 - __clz(2 * h), tbs = 31 - __clz(TB);
+  const unsigned ntl = (unsigned)ntiles;  // (< 2^31 tiles: checked by the launcher)
+  for (unsigned t = blockIdx.x; t < ntl; t += gridDim.x) {
+    const unsigned blk = t / (unsigned)tpb;
+    const int tt = (int)(t - blk * (unsigned)tpb);
+    const unsigned bq = blk / (unsigned)nbs;
+    const int bi_s = (rb0 + (int)bq) << tbs, bi_t = (int)(blk - bq * (unsigned)nbs) << tbs;
     const int nrs = imin(TB, Lp - bi_s), nrt = imin(TB, Lp - bi_t);
     // union of the block rows' windows (origins are monotone in the row)
     const int us0 = out.origin(bi_s), us1 = out.origin(bi_s + nrs - 1) + out.wd - 1;
@@ -668,16 +673,16 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
     // parents in some ball whose Wpsi support [2ph+lo, 2ph+h+hi] meets F
     int ps0 = imax(bi_s - rho, 0), ps1 = imin(bi_s + nrs - 1 + rho, Lp - 1);
     int pt0 = imax(bi_t - rho, 0), pt1 = imin(bi_t + nrt - 1 + rho, Lp - 1);
-    ps0 = imax(ps0, floordiv(F0s - h - hi, 2 * h));
-    ps1 = imin(ps1, floordiv(F0s + PN_FR - 1 - lo, 2 * h));
-    pt0 = imax(pt0, floordiv(F0t - h - hi, 2 * h));
-    pt1 = imin(pt1, floordiv(F0t + PN_FC - 1 - lo, 2 * h));
+    ps0 = imax(ps0, (F0s - h - hi) >> sh2h);  // floor division by 2 h
+    ps1 = imin(ps1, (F0s + PN_FR - 1 - lo) >> sh2h);
+    pt0 = imax(pt0, (F0t - h - hi) >> sh2h);
+    pt1 = imin(pt1, (F0t + PN_FC - 1 - lo) >> sh2h);
     const int nps = ps1 - ps0 + 1, npt = pt1 - pt0 + 1;
     const int K = (nps > 0 && npt > 0) ? nps * npt * 3 : 0;
     double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     // the A rows this thread gathers: m = threadIdx.x / 8 (+ fixed), kk strided
     const int am = threadIdx.x >> 3;  // 0..15
-    const int ams = am / TB, amt = am - (am / TB) * TB;
+    const int ams = am >> tbs, amt = am - (ams << tbs);
     const int ais = bi_s + ams, ait = bi_t + amt;
     const bool arow = am < TB * TB && ams < nrs && amt < nrt && ais >= r0 && ais < r1;
     const double* drow = Dt + ((long long)ais * Lp + ait) * SD;
@@ -766,12 +771,17 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int m = mt * 8 + (lane >> 2);
-      const int ms = m / TB, mtt = m - ms * TB;
+      const int ms = m >> tbs, mtt = m - (ms << tbs);
       const int is = bi_s + ms, it = bi_t + mtt;
       const bool live = m < TB * TB && ms < nrs && mtt < nrt && is >= r0 && is < r1;
       double amax = 0.0;
       if (live) {
         const int os = out.origin(is), ot = out.origin(it);
+        // the four children of row (is, it): window origins and row bases once
+        const int cos0 = child.origin(2 * is), cos1 = child.origin(2 * is + 1);
+        const int cot0 = child.origin(2 * it), cot1 = child.origin(2 * it + 1);
+        const double* cb00 = psi + ((long long)(2 * is) * child.L + 2 * it) * cper;
+        const double* cb10 = cb00 + (long long)child.L * cper;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int n = warp * 8 + 2 * (lane & 3) + j;
@@ -782,10 +792,10 @@ __global__ void __launch_bounds__(128) k_psi_next_mma(PsiWin child, const double
           double pv = 0.0;
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
-            const int cs = 2 * is + (a >> 1), ct = 2 * it + (a & 1);
-            const int ks = fs - child.origin(cs), kt = ft - child.origin(ct);
-            if (ks >= 0 && ks < child.wd && kt >= 0 && kt < child.wd)
-              pv += psi[((long long)cs * child.L + ct) * cper + ks * child.wd + kt];
+            const unsigned ks = (unsigned)(fs - ((a >> 1) ? cos1 : cos0));
+            const unsigned kt = (unsigned)(ft - ((a & 1) ? cot1 : cot0));
+            if (ks < (unsigned)child.wd && kt < (unsigned)child.wd)
+              pv += ((a >> 1) ? cb10 : cb00)[(a & 1) * cper + ks * child.wd + kt];
           }
           const double v = 0.25 * pv + c[mt][j];
           psi_next[((long long)is * Lp + it) * oper + ls * out.wd + lt] = v;
@@ -1275,6 +1285,7 @@ int gbk_psi_next_raw_rows(int n, int Lk, int lo, int hi, int wd, const double* p
     const long long nb = (Lp + TB - 1) / TB;
     const long long nrb = (r1 + TB - 1) / TB - r0 / TB;
     const long long nt = nrb * nb * nfs * nft;
+    if (nt >= (1LL << 31)) return GB_UNSUPPORTED;  // the kernel counts tiles in 32 bits
     const int g = resident_grid(k_psi_next_mma, 128, nt);
     k_psi_next_mma<<<g, 128, 0, s>>>(child, psi, par, Wpsi, rho, Dt, out, psi_next, rowmax, TB,
                                      nfs, nft, r0, r1, f0, f1);
