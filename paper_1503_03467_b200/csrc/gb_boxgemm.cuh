@@ -45,13 +45,19 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
   const double* Ab = aop.base();
   const double* Bb = bop.base();
   const int wA = aop.hw(), wB_ = bop.hw();
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long mb = t / (side * side) + (long long)rb0 * nb;
-    const int ob = (int)(t % (side * side));
-    const int mbs = (int)(mb / nb), mbt = (int)(mb % nb);
-    const int nbs = mbs + ob / side - nbo, nbt = mbt + ob % side - nbo;
+  // TB = min(Lp, 4) is a power of two: the tile-local divisions are shifts;
+  // tiles are counted in 32 bits (the launchers check the count)
+  const int tbs = 31 - __clz(TB);
+  const unsigned ss = (unsigned)(side * side), ntl = (unsigned)ntiles;
+  for (unsigned t = blockIdx.x; t < ntl; t += gridDim.x) {
+    const unsigned mbl = t / ss;
+    const int ob = (int)(t - mbl * ss);
+    const unsigned mb = mbl + (unsigned)rb0 * (unsigned)nb;
+    const int mbs = (int)(mb / (unsigned)nb), mbt = (int)(mb - (unsigned)mbs * (unsigned)nb);
+    const int obs = ob / side;
+    const int nbs = mbs + obs - nbo, nbt = mbt + (ob - obs * side) - nbo;
     if (nbs < 0 || nbs >= nb || nbt < 0 || nbt >= nb) continue;  // CTA-uniform
-    const int i0s = mbs * TB, i0t = mbt * TB, j0s = nbs * TB, j0t = nbt * TB;
+    const int i0s = mbs << tbs, i0t = mbt << tbs, j0s = nbs << tbs, j0t = nbt << tbs;
     const int nis = imin(TB, Lp - i0s), nit = imin(TB, Lp - i0t);
     const int njs = imin(TB, Lp - j0s), njt = imin(TB, Lp - j0t);
     // skip tiles with no (i, j) pair inside the output box
@@ -68,13 +74,13 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
     if (threadIdx.x < 16 * MC) {
       const int m = threadIdx.x;
       const int lm = m / MC, mc = m - lm * MC;
-      const int ls = lm / TB, lt = lm - ls * TB;
+      const int ls = lm >> tbs, lt = lm - (ls << tbs);
       const bool ok = lm < TB * TB && ls < nis && lt < nit;
       arp[m] = ok ? (((i0s + ls) << 16) | (i0t + lt)) : -1;
       aro[m] = ok ? aop.ipart(i0s + ls, i0t + lt, mc) : 0;
     } else if (threadIdx.x >= 64 && threadIdx.x < 80) {
       const int nn = threadIdx.x - 64;
-      const int ls = nn / TB, lt = nn - ls * TB;
+      const int ls = nn >> tbs, lt = nn - (ls << tbs);
       const bool ok = nn < TB * TB && ls < njs && lt < njt;
       bcp[nn] = ok ? (((j0s + ls) << 16) | (j0t + lt)) : -1;
       bco[nn] = ok ? bop.ipart(j0s + ls, j0t + lt, 0) : 0;
@@ -172,13 +178,13 @@ __global__ void __launch_bounds__(128) k_box_gemm(int Lp, int TB, int wa, int wb
       const int mt = (warp >> 1) + 2 * j;
       const int m = mt * 8 + (lane >> 2);
       const int lm = m / MC, mc = m - lm * MC;
-      const int ls = lm / TB, lt = lm - ls * TB;
+      const int ls = lm >> tbs, lt = lm - (ls << tbs);
       if (lm >= TB * TB || ls >= nis || lt >= nit) continue;
       const int is = i0s + ls, it = i0t + lt;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int nn = nt * 8 + 2 * (lane & 3) + h;
-        const int ns = nn / TB, ntt = nn - ns * TB;
+        const int ns = nn >> tbs, ntt = nn - (ns << tbs);
         if (nn >= TB * TB || ns >= njs || ntt >= njt) continue;
         const int js = j0s + ns, jt = j0t + ntt;
         if (js - is > wOut || is - js > wOut || jt - it > wOut || it - jt > wOut) continue;

@@ -1147,7 +1147,9 @@ static int resident_grid(Kern, int, long long ntiles) {
 // tiles of the row blocks [rb0, rb1) of the TB x TB blocking
 static long long box_gemm_tiles(int Lp, int TB, int wOut, int rb0, int rb1) {
   const long long nb = (Lp + TB - 1) / TB, side = 2 * ((wOut + TB - 1) / TB) + 1;
-  return (long long)(rb1 - rb0) * nb * side * side;
+  const long long nt = (long long)(rb1 - rb0) * nb * side * side;
+  // the kernel counts tiles in 32 bits; the largest level (Lp = 2048) has 2.7e7
+  return nt < (1LL << 31) ? nt : 0;
 }
 // the tensor-core tile kernels own whole TB-row blocks: a strip must start and
 // end on a block boundary (or the grid edge)
@@ -1166,7 +1168,9 @@ int gbk_bd_rows(int Lp, int wB, const double* B, int rho, const double* Dt, int 
     if (e != cudaSuccess) return (int)e;
     const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
     auto kern = k_box_gemm<3, OpBrows, OpDtRowsB, StoreBox>;
-    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wBD, rb0, rb1)), 128, 0, s>>>(
+    const long long nt = box_gemm_tiles(Lp, TB, wBD, rb0, rb1);
+    if (nt == 0) return GB_UNSUPPORTED;
+    kern<<<resident_grid(kern, 128, nt), 128, 0, s>>>(
         Lp, TB, wB, rho, wBD, OpBrows{B, Lp, wB, box_slots(wB, 3)},
         OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{BD, Lp, 3, wBD, box_slots(wBD, 1)},
         rb0, rb1);
@@ -1193,7 +1197,9 @@ int gbk_gtd_rows(int Lp, int wG, const double* G, int rho, const double* Dt, int
     if (e != cudaSuccess) return (int)e;
     const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
     auto kern = k_box_gemm<1, OpGcols, OpDtRowsB, StoreBox>;
-    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wGD, rb0, rb1)), 128, 0, s>>>(
+    const long long nt = box_gemm_tiles(Lp, TB, wGD, rb0, rb1);
+    if (nt == 0) return GB_UNSUPPORTED;
+    kern<<<resident_grid(kern, 128, nt), 128, 0, s>>>(
         Lp, TB, wG, rho, wGD, OpGcols{G, Lp, wG, box_slots(wG, 1)},
         OpDtRowsB{Dt, Lp, rho, box_slots(rho, 3)}, StoreBox{GtD, Lp, 1, wGD, box_slots(wGD, 1)},
         rb0, rb1);
@@ -1221,7 +1227,9 @@ int gbk_coarse_raw_rows(int Lp, int wB, const double* PAPt, int wGD, const doubl
     if (e != cudaSuccess) return (int)e;
     const int rb0 = r0 / TB, rb1 = (r1 + TB - 1) / TB;
     auto kern = k_box_gemm<1, OpDtRowsA, OpBDrows, StoreRaw>;
-    kern<<<resident_grid(kern, 128, box_gemm_tiles(Lp, TB, wA2, rb0, rb1)), 128, 0, s>>>(
+    const long long nt = box_gemm_tiles(Lp, TB, wA2, rb0, rb1);
+    if (nt == 0) return GB_UNSUPPORTED;
+    kern<<<resident_grid(kern, 128, nt), 128, 0, s>>>(
         Lp, TB, rho, wBD, wA2, OpDtRowsA{Dt, Lp, rho, box_slots(rho, 3)},
         OpBDrows{BD, Lp, wBD, box_slots(wBD, 1)}, StoreRaw{raw, PAPt, GtD, Lp, wB, wGD, wA2},
         rb0, rb1);
