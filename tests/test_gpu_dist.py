@@ -216,3 +216,38 @@ def test_strip_program_on_one_rank_matches_the_pipeline():
         assert torch.equal(res.strips[k]["psi"].rows(0, L), levels[k].raw("psi").vals), k
     err = float((res.u - u_ref).norm() / u_ref.norm())
     assert err <= 1e-9, err
+
+
+def test_partition_rejects_a_world_that_is_not_a_power_of_two():
+    import paper_1503_03467_b200 as gb
+    from paper_1503_03467_b200 import comm as cm
+    grid, M, A, g, tree = _inputs(6)
+
+    class Three(cm.SelfComm):
+        world = 3
+
+    with pytest.raises(gb.InvalidArgumentError):
+        gb.fast_solve_dist(Three(), M, A, g, tree, EPS, uniform_rho=RHO)
+
+
+def test_non_spd_operator_raises_on_every_rank():
+    """An indefinite stiffness surfaces as NumericalError on all ranks (the
+    status words and repair statistics are all-reduced before the check, the
+    Krylov breakdown flags come from all-reduced sums)."""
+    import paper_1503_03467_b200 as gb
+    from paper_1503_03467_b200 import comm as cm, device as dv
+    q = 8
+    grid, M, A, g, tree = _inputs(q)
+    Aneg = (-A).tocsr()
+    seen = []
+
+    def body(comm):
+        try:
+            gb.fast_solve_dist(comm, M, Aneg, g, tree, EPS, uniform_rho=RHO)
+        except gb.NumericalError as e:
+            seen.append((comm.rank, str(e)))
+            return "raised"
+        return "returned"
+
+    out = cm.run_threads(2, body, device=dv.device())
+    assert out == ["raised", "raised"], (out, seen)
