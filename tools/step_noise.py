@@ -4,6 +4,18 @@ import sys, gc, json, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np, torch
+import os
+if os.environ.get("GB_SPIN"):
+    # cudaDeviceScheduleSpin before the context exists: stream / event waits
+    # poll instead of blocking on an interrupt
+    import ctypes, glob
+    cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart*.so*")) + \
+        glob.glob("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cuda_runtime/lib/libcudart.so*") + \
+        ["/usr/local/cuda/lib64/libcudart.so"]
+    rt = ctypes.CDLL(cands[0])
+    print("cudart:", cands[0])
+    rc = rt.cudaSetDeviceFlags(int(os.environ["GB_SPIN"]))
+    print("cudaSetDeviceFlags ->", rc)
 import paper_1503_03467_b200 as gb
 from paper_1503_03467_b200 import device as dv, gamblet_fast as gf
 from bench import build_inputs, EPS, RHO
