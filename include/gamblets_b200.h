@@ -305,6 +305,14 @@ int gb_level_engine(struct gb_level_engine_args* args, void* stream);
  * extreme Ritz values.  Returns 0, 1 (QL failure), 2 (nonpositive Ritz value). */
 int gb_lanczos_emulate(const double* ab, int m, double tol, int max_outer, double* lam,
                        int* outer, double* ritz_min, double* ritz_max);
+/* host-only: the engines' convergence check after m Lanczos steps.  The same
+ * estimate by the inverse iteration run on T_m itself (LDL^T solves, O(m) per
+ * outer step), and *stop = 1 once the estimates on T_m, T_{m-16}, T_{m-32}
+ * share the stopping index and the geometric tail of their differences is
+ * below lz_tol |lam|.  Returns 0, 1 (bad arguments), 2 (T_m not positive
+ * definite). */
+int gb_lanczos_check(const double* ab, int m, double tol, int max_outer, double lz_tol,
+                     double* lam, int* outer, int* stop);
 
 /* ---- diagnostics on the device (replaces diagnostics.py:40-155) --------
  * cell energies a_c * v_c^T E v_c of a fine vector (diagnostics.py:40-49);
@@ -417,8 +425,7 @@ int gb3_cg_solve(int L, int nr, int w, const double* B, const double* s, double*
                  int max_chunk, void* stream);
 /* lambda_min of S B S (3-D box) by the Lanczos moments of the unit start
  * vector x: the reference's inverse-iteration sequence (sparse_core.py:
- * 258-277) evaluated from T_m (gb_lanczos_emulate), stop when stable to
- * lz_tol between checks.  x is overwritten; vp, wv: work n-vectors; ab /
+ * 258-277) evaluated from T_m, stop by gb_lanczos_check at lz_tol.  x is overwritten; vp, wv: work n-vectors; ab /
  * host_ab: 2 cap doubles (device / pinned host). */
 int gb3_lanczos_min(int L, int nr, int w, const double* B, const double* s, double* x,
                     double* vp, double* wv, void* state, double* partials, void* host_state,

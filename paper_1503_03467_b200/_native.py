@@ -106,6 +106,7 @@ _SIGS = {
     "gb_assemble_q1": ([_I, _P, _D, _P, _P, _P], _I),
     "gb_box1_matvec": ([_I, _P, _P, _P, _P], _I),
     "gb_lanczos_emulate": ([_P, _I, _D, _I, _P, _P, _P, _P], _I),
+    "gb_lanczos_check": ([_P, _I, _D, _I, _D, _P, _P, _P], _I),
     "gb_dot2": ([_L, _P, _P, _P, _P, _P, _P, _P], _I),
     "gb_scale_by_norm": ([_L, _P, _P, _I, _P, _P, _P], _I),
     "gb_box_apply": ([_I, _I, _I, _P, _P, _I, _P, _P, _P], _I),

@@ -45,7 +45,7 @@ static int invalid(const char* msg) {
 
 extern "C" {
 
-int gb_abi_version(void) { return 6; }
+int gb_abi_version(void) { return 7; }
 unsigned long long gb_launch_count(void) { return g_launches.load(); }
 const char* gb_last_error(void) { return g_err; }
 int gb_device_count(void) {
@@ -450,6 +450,11 @@ int gb_lanczos_emulate(const double* ab, int m, double tol, int max_outer, doubl
                        int* outer, double* ritz_min, double* ritz_max) {
   if (!ab || m <= 0 || !lam || !outer) return 1;
   return gb_lz::emulate_inverse_iteration(ab, m, tol, max_outer, lam, outer, ritz_min, ritz_max);
+}
+int gb_lanczos_check(const double* ab, int m, double tol, int max_outer, double lz_tol,
+                     double* lam, int* outer, int* stop) {
+  if (!ab || m <= 0 || !lam || !outer || !stop) return 1;
+  return gb_lz::lanczos_check(ab, m, tol, max_outer, lz_tol, lam, outer, stop);
 }
 int gb_cell_energies(int n, const double* v, const double* coef, const double* host_e16,
                      double* out, void* stream) {

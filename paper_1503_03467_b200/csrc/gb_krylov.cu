@@ -2716,9 +2716,7 @@ int gbk3_lanczos_min(int L, int nr, int w, const double* B, const double* sv, do
   *launches += 2;
   double* v = x;
   double* wn = wv;
-  int chunk = 32;
-  double lam_prev = 0.0;
-  int outer_prev = -1;
+  int chunk = 64;
   *its_out = 0;
   for (;;) {
     for (int i = 0; i < chunk; ++i) {
@@ -2737,21 +2735,17 @@ int gbk3_lanczos_min(int L, int nr, int w, const double* B, const double* sv, do
     if (m > 0) {
       if ((err = gbk_sync_read(ab, hab, sizeof(double) * 2 * (size_t)m, s))) return err;
       double lam;
-      int outer;
-      const int rc = gb_lz::emulate_inverse_iteration(hab, m, tol, max_outer, &lam, &outer,
-                                                      nullptr, nullptr);
-      if (rc) return GB_UNSUPPORTED - rc;  // -2 / -3: non-SPD or QL failure
+      int outer, stable;
+      const int rc = gb_lz::lanczos_check(hab, m, tol, max_outer, lz_tol, &lam, &outer, &stable);
+      if (rc) return GB_UNSUPPORTED - rc;  // -2 / -3: non-SPD or a failed evaluation
       *lam_out = lam;
       *outer_out = outer;
       *its_out = m;
-      const bool stable = outer == outer_prev && fabs(lam - lam_prev) <= lz_tol * fabs(lam);
-      lam_prev = lam;
-      outer_prev = outer;
       if (h->done || stable) return 0;
     } else if (h->done) {
       return GB_UNSUPPORTED - 9;  // A v_1 = 0
     }
-    chunk = chunk * 2 < 64 ? chunk * 2 : 64;
+    chunk = 32;
   }
 }
 
@@ -2872,9 +2866,7 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
   k_state_reset<<<1, 1, 0, s>>>(kb, e->lz_cap);
   k_lz_init<<<1, 1, 0, s>>>(kb);
   nl += 2;
-  int chunk = 32;
-  double lam_prev = 0.0;
-  int outer_prev = -1;
+  int chunk = 64;
   e->lz_its = 0;
   e->lz_rc = 0;
   for (;;) {
@@ -2907,9 +2899,9 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
     if (m > 0) {
       if ((err = gbk_sync_read(e->lz, e->hlz, sizeof(double) * 2 * (size_t)m, s))) return err;
       double lam;
-      int outer;
-      const int rc = gb_lz::emulate_inverse_iteration(e->hlz, m, e->tol, e->max_outer, &lam,
-                                                      &outer, nullptr, nullptr);
+      int outer, stable;
+      const int rc = gb_lz::lanczos_check(e->hlz, m, e->tol, e->max_outer, e->lz_tol, &lam,
+                                          &outer, &stable);
       if (rc) {
         e->lz_rc = rc;
         e->breakdown = -2;
@@ -2918,16 +2910,13 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
       e->lam_min = lam;
       e->n_outer = outer;
       e->lz_its = m;
-      const bool stable = outer == outer_prev && fabs(lam - lam_prev) <= e->lz_tol * fabs(lam);
-      lam_prev = lam;
-      outer_prev = outer;
       if (hb->done || stable) break;
     } else if (hb->done) {  // A v_1 = 0
       e->breakdown = -1;
       return 0;
     }
-    // checks at most 64 steps apart: the stop lands within 64 of convergence
-    chunk = chunk * 2 < 64 ? chunk * 2 : 64;
+    // checks 32 steps apart (the host side of a check is O(m))
+    chunk = 32;
   }
   e->calls += e->lz_its;
   return 0;

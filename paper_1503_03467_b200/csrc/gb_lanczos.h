@@ -136,4 +136,83 @@ inline int emulate_inverse_iteration(const double* ab, int m, double tol, int ma
   return 0;
 }
 
+// The same sequence without the eigen-decomposition: the reference's
+// iteration run on T_m itself from e_1 (x_j = T^{-1} x_{j-1} / |.|,
+// lambda_j = x_j^T T x_j = (y . x_{j-1}) / (y . y) with y = T^{-1} x_{j-1}),
+// each solve two sweeps of the LDL^T factors of the tridiagonal -- O(m) per
+// outer step instead of the O(m^2) QL pass, so the engine can test for
+// convergence often without stalling its stream.  Same stopping test and
+// return codes (2: a nonpositive pivot, T_m is not positive definite).
+inline int emulate_inverse_iteration_ldl(const double* ab, int m, double tol, int max_outer,
+                                         double* lam_out, int* outer_out) {
+  if (m <= 0) return 1;
+  double* piv = (double*)malloc(sizeof(double) * 4 * (size_t)m);
+  double* l = piv + m;
+  double* x = l + m;
+  double* y = x + m;
+  piv[0] = ab[0];
+  for (int i = 0; i + 1 < m; ++i) {
+    if (!(piv[i] > 0.0)) {
+      free(piv);
+      return 2;
+    }
+    l[i] = ab[2 * i + 1] / piv[i];
+    piv[i + 1] = ab[2 * i + 2] - l[i] * ab[2 * i + 1];
+  }
+  if (!(piv[m - 1] > 0.0)) {
+    free(piv);
+    return 2;
+  }
+  for (int i = 0; i < m; ++i) x[i] = (i == 0) ? 1.0 : 0.0;
+  double lam_prev = INFINITY, lam = 0.0;
+  int j;
+  for (j = 1; j <= max_outer; ++j) {
+    y[0] = x[0];
+    for (int i = 0; i + 1 < m; ++i) y[i + 1] = x[i + 1] - l[i] * y[i];
+    y[m - 1] /= piv[m - 1];
+    for (int i = m - 2; i >= 0; --i) y[i] = y[i] / piv[i] - l[i] * y[i + 1];
+    double xy = 0.0, yy = 0.0;
+    for (int i = 0; i < m; ++i) {
+      xy += x[i] * y[i];
+      yy += y[i] * y[i];
+    }
+    lam = xy / yy;
+    const double inv = 1.0 / sqrt(yy);
+    for (int i = 0; i < m; ++i) x[i] = y[i] * inv;
+    if (fabs(lam - lam_prev) <= 0.5 * tol * fabs(lam)) break;
+    lam_prev = lam;
+  }
+  *lam_out = lam;
+  *outer_out = j > max_outer ? max_outer : j;
+  free(piv);
+  return 0;
+}
+
+// Stopping rule of the Lanczos sequence after m steps.  The estimate
+// lam(m) converges geometrically in m (tools/lanczos_convergence.py), and
+// the estimates of fewer steps come for free from the leading blocks of the
+// same T: with d1 = |lam(m-16) - lam(m)|, d2 = |lam(m-32) - lam(m-16)| and
+// rate = d1 / d2, the remaining error is the geometric tail
+// d1 rate / (1 - rate).  Stop when the three stopping indices agree, the
+// differences shrink, and the tail is below lz_tol |lam|.
+constexpr int kCheckBack = 16;
+inline int lanczos_check(const double* ab, int m, double tol, int max_outer, double lz_tol,
+                         double* lam, int* outer, int* stop) {
+  *stop = 0;
+  int rc = emulate_inverse_iteration_ldl(ab, m, tol, max_outer, lam, outer);
+  if (rc || m <= 2 * kCheckBack) return rc;
+  double l1, l2;
+  int o1, o2;
+  if ((rc = emulate_inverse_iteration_ldl(ab, m - kCheckBack, tol, max_outer, &l1, &o1))) return rc;
+  if ((rc = emulate_inverse_iteration_ldl(ab, m - 2 * kCheckBack, tol, max_outer, &l2, &o2)))
+    return rc;
+  if (o1 != *outer || o2 != *outer) return 0;
+  const double d1 = fabs(l1 - *lam), d2 = fabs(l2 - l1);
+  if (d1 > d2) return 0;
+  double rate = d2 > 0.0 ? d1 / d2 : 0.0;
+  if (rate > 0.95) rate = 0.95;
+  *stop = d1 * rate / (1.0 - rate) <= lz_tol * fabs(*lam);
+  return 0;
+}
+
 }  // namespace gb_lz

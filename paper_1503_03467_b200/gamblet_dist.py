@@ -358,9 +358,10 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
         hlz = np.empty(2 * cap)
         v, wv = xs, yb
         nat.call("gb_dist_lz_begin", dv.ptr(kb.state), cap, s)
-        chunk, lam_prev, outer_prev, lam, m = 32, 0.0, -1, None, 0
+        chunk, lam, m = 64, None, 0
         lamc = nat.ctypes.c_double(0.0)
         outc = nat.ctypes.c_int(0)
+        stopc = nat.ctypes.c_int(0)
         while True:
             a_live = not ha["done"]
             for _ in range(chunk):
@@ -380,22 +381,20 @@ def _dist_krylov(op, rhs_pad, tol, spectral=True, eig_tol=0.1, max_outer=500, se
             m = int(hb["it"])
             if m > 0:
                 hlz[:2 * m] = dv.to_host(lz[:2 * m])
-                rc = nat.query("gb_lanczos_emulate", hlz.ctypes.data, m, float(eig_tol),
-                               int(max_outer), nat.ctypes.byref(lamc), nat.ctypes.byref(outc),
-                               None, None)
+                rc = nat.query("gb_lanczos_check", hlz.ctypes.data, m, float(eig_tol),
+                               int(max_outer), float(gf.LANCZOS_TOL), nat.ctypes.byref(lamc),
+                               nat.ctypes.byref(outc), nat.ctypes.byref(stopc))
                 if rc:
                     raise NumericalError(
                         f"Lanczos moments of S B S at n={n}: "
-                        + ("nonpositive Ritz value (matrix is not SPD)" if rc == 2
-                           else "tridiagonal eigensolver failed"))
-                lam, outer = float(lamc.value), int(outc.value)
-                stable = outer == outer_prev and abs(lam - lam_prev) <= gf.LANCZOS_TOL * abs(lam)
-                lam_prev, outer_prev = lam, outer
-                if hb["done"] or stable:
+                        + ("nonpositive pivot (matrix is not SPD)" if rc == 2
+                           else "evaluation failed"))
+                lam = float(lamc.value)
+                if hb["done"] or stopc.value:
                     break
             elif hb["done"]:
                 raise NumericalError("inverse iteration broke down: A^{-1} x = 0")
-            chunk = min(chunk * 2, 64)
+            chunk = 32
         out["lam_min"] = lam
         out["lanczos"] = m
         out["calls"] += m

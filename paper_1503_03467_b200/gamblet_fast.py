@@ -603,6 +603,7 @@ def _eig_extremes(op, tol=0.1, max_iter=500, seed=24337, inner_solver=None):
 
 
 _SPECTRAL_LOG = []
+_LANCZOS_DUMP = None
 
 # live timing of the level engine's dual-vector operator passes (bench.py):
 # {"n": rows of the level to time, "cap": launches per engine} -> the engine
@@ -679,8 +680,8 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
         timing.setdefault("ms", []).extend(ev_ms[:args.ev_n].tolist())
     if args.breakdown == -2:
         raise NumericalError(f"Lanczos moments of S B S at n={n}: "
-                             + ("nonpositive Ritz value (matrix is not SPD)" if args.lz_rc == 2
-                                else "tridiagonal eigensolver failed"))
+                             + ("nonpositive pivot (matrix is not SPD)" if args.lz_rc == 2
+                                else "evaluation failed"))
     if args.breakdown > 0:
         raise NumericalError(f"CG breakdown at iteration {args.breakdown}: p^T A p <= 0 "
                              "(matrix is not SPD)")
@@ -690,6 +691,8 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
     if args.spectral_mode == 1:
         _SPECTRAL_LOG.append({"n": n, "power": int(args.power_its), "outer": int(args.n_outer),
                               "lanczos": int(args.lz_its)})
+        if _LANCZOS_DUMP is not None:  # tools/lanczos_convergence.py
+            _LANCZOS_DUMP.append((n, hlz[:2 * int(args.lz_its)].clone().numpy()))
     else:
         _SPECTRAL_LOG.append({"n": n, "power": int(args.power_its),
                               "inner": [int(args.inner_its[i])
@@ -728,11 +731,12 @@ MAX_ITER_CAP = 100000
 # PCG's operator passes.  Smaller levels run the inverse iteration with PCG.
 SPECTRAL_INNER = "lanczos"
 LANCZOS_CAP = 4096
-# relative change of the emulated lambda_min between two engine checks (32-64
-# Lanczos steps apart) below which the sequence stops.  The quadrature
-# converges fast by then: at q=10 stopping at 1e-4 (416 steps) lands 4e-7 from
-# the 1e-5 stop (480 steps); the reference's own inner solves (rel_tol 1e-4)
-# move its estimate by 3e-4
+# bound on the estimated remaining relative error of the emulated lambda_min
+# at which the Lanczos sequence stops (gb_lanczos.h lanczos_check: every 32
+# steps the estimate is evaluated on T_m, T_{m-16}, T_{m-32} and the geometric
+# tail of the differences compared with this).  At q=10 the sequence stops at
+# 352 steps, 3e-5 from the converged value; the reference's own inner solves
+# (rel_tol 1e-4) move its estimate by 3e-4
 LANCZOS_TOL = 1e-4
 
 

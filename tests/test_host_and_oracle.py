@@ -170,7 +170,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.EXPORTED)
-    assert lib.gb_abi_version() == 6
+    assert lib.gb_abi_version() == 7
 
 
 def _lanczos_ab(A, v0, m):
@@ -240,6 +240,59 @@ def test_lanczos_emulation_flags_indefinite_operator():
         ab = _lanczos_ab(A, np.ones(4), 4)
     rc = _emulate(ab)[0]
     assert rc == 2
+
+
+def _check(ab, lz_tol=1e-4, tol=0.1, max_outer=500):
+    from paper_1503_03467_b200 import _native
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    lam, outer, stop = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+    buf = np.ascontiguousarray(ab, dtype=np.float64)
+    rc = lib.gb_lanczos_check(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(len(ab) // 2),
+                              ctypes.c_double(tol), ctypes.c_int(max_outer),
+                              ctypes.c_double(lz_tol), ctypes.byref(lam), ctypes.byref(outer),
+                              ctypes.byref(stop))
+    return rc, lam.value, outer.value, stop.value
+
+
+def test_lanczos_check_matches_emulation_and_stops_when_converged():
+    """gb_lanczos_check (the engines' convergence test): its O(m) evaluation
+    equals the eigen-decomposition one on every leading T_m, and walking the
+    engine's check points (64, 96, 128, ...) it stops at a point whose
+    estimate is within lz_tol of the converged one, not before the estimates
+    have settled."""
+    rng = np.random.default_rng(11)
+    n = 700
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    ev = np.geomspace(2e-4, 1.0, n)
+    A = (Q * ev) @ Q.T
+    A = 0.5 * (A + A.T)
+    ab = _lanczos_ab(A, rng.standard_normal(n), 640)
+    lam_final = _emulate(ab)[1]
+    for m in (1, 2, 17, 64, 333, 640):
+        rc, lam, outer, _, _ = _emulate(ab[:2 * m])
+        rc2, lam2, outer2, _ = _check(ab[:2 * m])
+        assert rc == 0 and rc2 == 0
+        assert outer2 == outer
+        assert abs(lam2 - lam) <= 1e-11 * lam
+    stops = []
+    for lz_tol in (1e-2, 1e-4, 1e-6):
+        for m in range(64, 641, 32):
+            rc, lam, outer, stop = _check(ab[:2 * m], lz_tol=lz_tol)
+            assert rc == 0
+            if stop:
+                break
+        assert stop, "the sequence converges well inside 640 steps"
+        assert abs(lam - lam_final) <= 2 * lz_tol * lam_final
+        stops.append(m)
+    assert stops[0] < stops[1] < stops[2]
+    assert _check(ab[:2 * 64], lz_tol=1e-6)[3] == 0
+
+
+def test_lanczos_check_flags_indefinite_operator():
+    A = np.diag([-1.0, 1.0, 2.0, 3.0])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ab = _lanczos_ab(A, np.ones(4), 4)
+    assert _check(ab)[0] == 2
 
 
 def test_matrix_market_roundtrip_and_bad_transform_file(tmp_path):
