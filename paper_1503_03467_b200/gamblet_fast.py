@@ -710,7 +710,7 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
 
 # lambda estimates run on side streams (one per worker thread) so they overlap
 # the FP64-bound patch factorizations of the main stream
-SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "2"))
+SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "3"))
 # safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
 # it; converging solves here need < 2000)
 SPECTRAL_PRIORITY = -1
