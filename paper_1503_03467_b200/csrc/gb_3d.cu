@@ -1214,6 +1214,7 @@ int gbk3_mass_patches(int L, const double* M, const double* sv, int rho, int wd,
   // the (2 rho + 1)^3 clip types when M is translation invariant (checked
   // on the device), else every patch; the flag is stream-ordered
   int* flag = nullptr;
+  keep_default_pool();
   e = cudaMallocAsync((void**)&flag, sizeof(int), s);
   if (e != cudaSuccess) return (int)e;
   e = cudaMemsetAsync(flag, 0, sizeof(int), s);

@@ -116,4 +116,21 @@ struct WTemplate {
   double w[3][4];
 };
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// memory pool, whose release threshold is zero unless told otherwise: every
+// synchronize hands the pool's memory back to the driver and the next
+// allocation maps it again -- on this pool's microVM hosts that remap stalls
+// for tens to hundreds of milliseconds now and then.  Keep the pool's memory.
+inline void keep_default_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 }  // namespace gb

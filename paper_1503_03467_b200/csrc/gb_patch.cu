@@ -844,6 +844,7 @@ int gbk_mass_patches_rows(int n, int wM, const double* M, const double* s, int r
     // whole level: factor the (2 rho + 1)^2 type representatives, broadcast
     // their rows; the general pass runs only if M is not translation invariant
     int* d_flag = nullptr;  // stream-ordered, so concurrent transforms never share it
+    keep_default_pool();
     cudaError_t e = cudaMallocAsync((void**)&d_flag, sizeof(int), st);
     if (e != cudaSuccess) return (int)e;
     e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
