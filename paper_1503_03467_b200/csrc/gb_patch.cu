@@ -768,7 +768,7 @@ int gbk_tune(int what, int value) {
   return old;
 }
 
-static constexpr int kV3PerSm = 6;  // smem (36 KB) and register limit of the v3 CTA
+static constexpr int kV3PerSm = GB_V3_MINB;  // smem (36 KB) and register limit of the v3 CTA
 
 static long long v3_grid(int Lp, int r0, int r1) {
   const long long P = (long long)(r1 - r0) * Lp;

@@ -37,15 +37,14 @@ struct V3Smem {
   double* dg;    // 64: diagonal tile, swizzled (warp_chol8_inv layout)
   double* sl;    // 8 Tmax + 8 (scale; 8 scratch doubles after it)
   double* z;     // 8 Tmax
-  long long* rowb;  // 8 Tmax: B offset of local row l minus its key (separable gather)
+  long long* rowb;  // 8 Tmax: (B offset of local row l minus its key) << 16 | a << 8 | b
   int* colk;     // 8 Tmax: key of local column l
-  int* ploc;     // 8 Tmax
   int* flag;
 };
 
 __host__ __device__ __forceinline__ size_t v3_smem_bytes(int Tmax) {
   return ((size_t)2 * (Tmax + 1) * 64 + (size_t)Tmax * 64 + 64 + (8 * Tmax + 8) + 8 * Tmax +
-          8 * Tmax) * 8 + (size_t)16 * Tmax * 4 + 16;
+          8 * Tmax) * 8 + (size_t)8 * Tmax * 4 + 16;
 }
 
 __device__ __forceinline__ V3Smem v3_carve(double* sm, int Tmax) {
@@ -58,8 +57,7 @@ __device__ __forceinline__ V3Smem v3_carve(double* sm, int Tmax) {
   s.rowb = reinterpret_cast<long long*>(s.z + 8 * Tmax);
   int* ip = reinterpret_cast<int*>(s.rowb + 8 * Tmax);
   s.colk = ip;
-  s.ploc = s.colk + 8 * Tmax;
-  s.flag = s.ploc + 8 * Tmax;
+  s.flag = s.colk + 8 * Tmax;
   return s;
 }
 
@@ -88,31 +86,32 @@ __device__ __forceinline__ void v3_cp8(double* dst, const double* src) {
 // and asynchronously (cp.async; the caller waits before its barrier); the
 // reference's congruence (B s_i) s_j (gamblet_fast.py:136) is applied when
 // the update phase first reads the column (v3 step (3)); padding rows hold
-// the unit diagonal and S.sl = 1 there.
+// the unit diagonal and S.sl = 1 there.  One table word per row carries the
+// row's box offset and its parent coordinates (the band test).
 __device__ __forceinline__ void v3_gather(const V3Smem& S, double* col, int kt, int T, int m,
                                           int wB, const double* __restrict__ B, int tl, int nt) {
   const int c = tl & 7;
   const int l2 = 8 * kt + c;
-  const bool cval = l2 < m;
-  const long long ck = cval ? S.colk[l2] : 0;
-  const int p2 = cval ? S.ploc[l2] : 0;
   const int step = nt >> 3;
+  int l1 = 8 * kt + (tl >> 3);
+  double* dst = col + (tl >> 3) * 8 + c;
+  if (l2 < m) {
+    const int p2 = (int)S.rowb[l2];
+    const int a2 = ((p2 >> 8) & 255) + wB, b2 = (p2 & 255) + wB;
+    const unsigned w2 = 2 * wB;
+    const double* Bc = B + S.colk[l2];
 #pragma unroll 4
-  for (int l1 = 8 * kt + (tl >> 3); l1 < 8 * T; l1 += step) {
-    double* dst = col + (l1 - 8 * kt) * 8 + c;
-    bool zero = true;
-    if (l1 < m && cval) {
-      const int p1 = S.ploc[l1];
-      const int ds = (p2 >> 8) - (p1 >> 8), dt = (p2 & 255) - (p1 & 255);
-      if (ds >= -wB && ds <= wB && dt >= -wB && dt <= wB) {
-        v3_cp8(dst, B + S.rowb[l1] + ck);
-        zero = false;
-      }
-    } else if (l1 == l2) {
-      *dst = 1.0;  // padding rows: unit diagonal
-      zero = false;
+    for (; l1 < m; l1 += step, dst += step * 8) {
+      const long long info = S.rowb[l1];
+      const int lo = (int)info;
+      if ((unsigned)(a2 - ((lo >> 8) & 255)) <= w2 && (unsigned)(b2 - (lo & 255)) <= w2)
+        v3_cp8(dst, Bc + (info >> 16));
+      else
+        *dst = 0.0;
     }
-    if (zero) *dst = 0.0;
+    for (; l1 < 8 * T; l1 += step, dst += step * 8) *dst = 0.0;  // padding rows
+  } else {  // padding column: unit diagonal
+    for (; l1 < 8 * T; l1 += step, dst += step * 8) *dst = (l1 == l2) ? 1.0 : 0.0;
   }
   for (int r = tl >> 3; r < 8; r += step) col[(T - kt) * 64 + r * 8 + c] = (r == 0) ? S.z[l2] : 0.0;
 }
@@ -146,9 +145,8 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
         const long long r = ((long long)(s0 + a) * Lp + (t0 + b)) * 3 + c;
         // slot_of(wB, 3, a2 - a1, b2 - b1, c2) = key(l2) - 3 (a1 W2 + b1) + K
         const int key = (a * (2 * wB + 1) + b) * 3;
-        S.rowb[l] = r * SB - key + (wB * (2 * wB + 1) + wB) * 3;
+        S.rowb[l] = ((r * SB - key + (wB * (2 * wB + 1) + wB) * 3) << 16) | (a << 8) | b;
         S.colk[l] = key + c;
-        S.ploc[l] = (a << 8) | b;
         S.sl[l] = sB[r];
         const int ds = si - (s0 + a), dt = ti - (t0 + b);
         double g = 0.0;
@@ -330,9 +328,16 @@ __global__ void __launch_bounds__(32 * kV3Warps, GB_V3_MINB) k_correction_patche
         for (int o = threadIdx.x; o < 8 * it; o += blockDim.x) {
           const int jt = o >> 3, c = o & 7;
           const double* t = row + jt * 64;
+          // the 16 lanes of a half-warp start their sum at different k: the
+          // tile words (c & 3) + 4 k of the fragment order then fall into 16
+          // distinct bank pairs
+          const int rot = 2 * (jt & 1) + (c >> 2);
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc = fma(t[fpos(k, c)], S.sl[8 * Tmax + k], acc);
+          for (int k = 0; k < 8; ++k) {
+            const int kk = (k + rot) & 7;
+            acc = fma(t[fpos(kk, c)], S.sl[8 * Tmax + kk], acc);
+          }
           S.z[o] -= acc;
         }
       }
