@@ -23,6 +23,9 @@
 // reductions.  DRAM moves half the matrix bytes of the full box, every run is
 // bitwise reproducible.
 #pragma once
+#ifndef GB_SYM_L2_STREAM
+#define GB_SYM_L2_STREAM 1
+#endif
 
 #ifndef GB_SYM_TH
 #define GB_SYM_TH 4
@@ -319,6 +322,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
 }
+// the same copy with an L2 evict-first policy: a band larger than L2 is read
+// once per pass, and without the hint its 0.8 GB stream evicts the Krylov
+// vectors the update kernels between two passes re-read
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, unsigned bytes,
+                                                unsigned long long* b, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void consumer_sync() {  // the 8 consumer warps only
   asm volatile("bar.sync 1, %0;" ::"r"(kSymThreads) : "memory");
 }
@@ -395,6 +414,9 @@ __global__ void __launch_bounds__(NV * kSymThreads + 32, 1) k_symb_apply_ws(
     // ---- producer: chunk g = (tile iteration, k) -> stage g % NS ----
     if (lane == 0) {
       long long g = 0;
+      // bands beyond the L2 capacity (levels with >= 256^2 parents) stream
+      const bool streamed = GB_SYM_L2_STREAM && L >= 256;
+      const unsigned long long pol = l2_evict_first_policy();
       for (long long t = tile0 + blockIdx.x; t < tile1; t += gridDim.x) {
         const int I = (int)(t / tpr), J = (int)(t % tpr);
         for (int k = 0; k < nch; ++k, ++g) {
@@ -410,7 +432,10 @@ __global__ void __launch_bounds__(NV * kSymThreads + 32, 1) k_symb_apply_ws(
                 (long long)(I * kSymTH + (cw >> 1)) * L + J * kSymTW + (cw & 1) * 32;
             const double2* src = reinterpret_cast<const double2*>(U) + (p >> 5) * (32LL * NS2) +
                                   (long long)k * kSymWsPairs * 32;
-            bulk_g2s(dst + cw * kSymWsPairs * 32, src, bytes, full + st);
+            if (streamed)
+              bulk_g2s_stream(dst + cw * kSymWsPairs * 32, src, bytes, full + st, pol);
+            else
+              bulk_g2s(dst + cw * kSymWsPairs * 32, src, bytes, full + st);
           }
         }
       }
