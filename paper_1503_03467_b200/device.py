@@ -78,7 +78,7 @@ class Traffic:
 # staging ring (gb_h2d_staged: multi-threaded host copy overlapped with the
 # DMA) -- a pageable copy is bounded by one driver memcpy thread
 _STAGE_MIN_BYTES = 4 << 20
-_STAGE_THREADS = 8
+_STAGE_THREADS = 4
 # the staging ring is one per process: in-process ranks (comm.ThreadComm) take turns
 _STAGE_LOCK = threading.Lock()
 
