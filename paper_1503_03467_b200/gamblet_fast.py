@@ -708,16 +708,25 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
             "lam_max": float(args.lam_max), "calls": int(args.calls),
             "passes": (int(args.n_dual), int(args.n_single))}
 
-# lambda estimates run on side streams (one per worker thread) so they overlap
-# the FP64-bound patch factorizations of the main stream
-SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "3"))
-# safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
-# it; converging solves here need < 2000)
-SPECTRAL_PRIORITY = -1
+# The level tasks (lambda estimates + subband solve of one level) run on side
+# streams so they overlap the setup of the coarser levels on the main stream:
+# a pool of worker threads, one stream per LEVEL, same priority as the main
+# stream (measured at q=10: 3 workers on high-priority streams 258 ms, 6
+# workers at equal priority 251 ms, tools/tune_step.py)
+SPECTRAL_WORKERS = int(__import__("os").environ.get("GB_SPECTRAL_WORKERS", "6"))
+SPECTRAL_PRIORITY = int(__import__("os").environ.get("GB_SPECTRAL_PRIORITY", "0"))
+# lean transforms (q >= 12, within ~20 % of the HBM capacity): three levels in
+# flight on per-worker high-priority streams, the setting the q=12 line was
+# measured with
+LEAN_WORKERS = 3
+LEAN_PRIORITY = -1
+_LEAN_SLOTS = threading.BoundedSemaphore(LEAN_WORKERS)
 # symmetric band Krylov copy (csrc/gb_symspmv.cuh): only the upper 3x3 blocks
 # of S B S are streamed, the lower half is applied from the same registers
 # (scatter through shared memory) -- half the HBM bytes of the full box
 SYMMETRIC_SPMV = True
+# safety cap on Krylov iterations (the reference's max(200, 2n) is kept below
+# it; converging solves here need < 2000)
 MAX_ITER_CAP = 100000
 # inner solver of the inverse iteration for lambda_min: "pcg" (block-Jacobi,
 # the subband preconditioner) or "cg" (the reference's unpreconditioned CG).
@@ -758,12 +767,31 @@ class _LevelTasks:
         self.futures = []
         self.solver = solver
 
+    _level_streams = {}
+    _level_streams_lock = threading.Lock()
+
     @classmethod
-    def _stream(cls):
+    def _stream(cls, k=None):
+        """The stream of a level task.  Retained transforms give every level
+        its own stream: the caching allocator keeps one block pool per
+        stream, so the same level on the same stream in every step replays
+        the same allocations and a steady-state step makes no cudaMalloc
+        (with a stream per worker thread, whichever thread picked a level up
+        grew its pool: tens of new segments per step and a 100+ ms stall now
+        and then).  Lean transforms (q >= 12, memory bound) keep one stream
+        per worker so the levels share the workers' pools."""
+        torch.cuda.set_device(dv.device())
+        if k is not None:
+            key = (dv.device().index, int(k), SPECTRAL_PRIORITY)
+            with cls._level_streams_lock:
+                st = cls._level_streams.get(key)
+                if st is None:
+                    st = torch.cuda.Stream(device=dv.device(), priority=SPECTRAL_PRIORITY)
+                    cls._level_streams[key] = st
+            return st
         st = getattr(cls._local, "stream", None)
         if st is None:
-            torch.cuda.set_device(dv.device())
-            st = torch.cuda.Stream(device=dv.device(), priority=SPECTRAL_PRIORITY)
+            st = torch.cuda.Stream(device=dv.device(), priority=LEAN_PRIORITY)
             cls._local.stream = st
         return st
 
@@ -777,7 +805,12 @@ class _LevelTasks:
         self.futures.append(self._pool.submit(self._run, level, op, k, g, ev, psi))
 
     def _run(self, level, op, k, g, ev, psi=None):
-        st = self._stream()
+        if getattr(level, "_lean", False):
+            with _LEAN_SLOTS:  # memory bound: at most LEAN_WORKERS levels in flight
+                return self._run_on(self._stream(None), level, op, k, g, ev, psi)
+        return self._run_on(self._stream(k), level, op, k, g, ev, psi)
+
+    def _run_on(self, st, level, op, k, g, ev, psi=None):
         calls = 0
         with torch.cuda.stream(st):
             st.wait_event(ev)

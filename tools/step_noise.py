@@ -42,7 +42,7 @@ def run(n, tag):
         rows.append((round(e0.elapsed_time(e1), 1), round(t_enq, 1), s1[0] - s0[0], s1[1] - s0[1], s1[2] - s0[2], s1[3]))
     print(tag, "median", np.median([r[0] for r in rows]))
     for r in rows:
-        if r[0] > 305 or r[2] or r[3] or r[4]:
+        if r[0] > 270 or r[2] or r[3] or r[4]:
             print("   step ms %.1f, host-return ms %.1f, segments +%d -%d, retries %d, reserved MiB %d" % r)
 import os
 print("cpus", os.cpu_count(), "affinity", len(os.sched_getaffinity(0)), "loadavg", os.getloadavg())
