@@ -31,12 +31,29 @@ def emulate(ab, m):
     return rc, lam.value, outer.value
 
 
+def check(ab, m, lz_tol=1e-4):
+    lam, outer, stop = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+    buf = np.ascontiguousarray(ab[:2 * m])
+    rc = lib.gb_lanczos_check(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(m),
+                              ctypes.c_double(0.1), ctypes.c_int(500), ctypes.c_double(lz_tol),
+                              ctypes.byref(lam), ctypes.byref(outer), ctypes.byref(stop))
+    return rc, lam.value, outer.value, stop.value
+
+
 for n, ab in sorted(gf._LANCZOS_DUMP, key=lambda t: -t[0]):
     mtot = len(ab) // 2
     rc, lam_f, out_f = emulate(ab, mtot)
     print(f"n={n} steps={mtot} final lam={lam_f:.12e} outer={out_f}")
+    for m in [64] + list(range(96, mtot + 1, 32)):  # the engine's check points
+        rc, lam, outer, stop = check(ab, m)
+        if stop:
+            print(f"   engine stops at m={m}: lam/lam_final - 1 = {lam / lam_f - 1.0:+.2e}, outer {outer}")
+            break
+    else:
+        print("   engine does not stop within", mtot)
     row = []
     for m in range(16, mtot + 1, 16):
         rc, lam, outer = emulate(ab, m)
         row.append((m, lam / lam_f - 1.0, outer))
-    print("   " + "  ".join(f"{m}:{d:+.1e}/{o}" for m, d, o in row))
+    if "-v" in sys.argv:
+        print("   " + "  ".join(f"{m}:{d:+.1e}/{o}" for m, d, o in row))
