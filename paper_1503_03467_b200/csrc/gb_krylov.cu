@@ -2602,6 +2602,9 @@ int gbk3_pow_solve(int L, int nr, int w, const double* B, const double* sv, doub
 // ---------------------------------------------------------------------------
 #include "gb_engine.h"
 #include "gb_lanczos.h"
+#ifndef GB_LZ_CHECK
+#define GB_LZ_CHECK 32
+#endif
 
 // ---- engine building blocks (count their launches into *nl) ----
 // dual pass: A (subband PCG, mode 0) and B (mode mb) on one sweep of S B S;
@@ -2916,7 +2919,7 @@ static int lanczos_min(gb_level_engine_args* e, cudaStream_t s, long long& nl) {
       return 0;
     }
     // checks 32 steps apart (the host side of a check is O(m))
-    chunk = 32;
+    chunk = GB_LZ_CHECK;
   }
   e->calls += e->lz_its;
   return 0;
