@@ -958,6 +958,89 @@ __global__ void k3_bd(int Lp, int wB, const double* __restrict__ B, int rho,
   }
 }
 
+// The same BD, register tiled: a thread forms the 7 component rows of parent
+// p against a run of K3_JZ consecutive column offsets along z, so a 7 x 7
+// block of B serves K3_JZ columns and a 7-vector of D serves 7 rows (0.4
+// loads per FMA instead of 2).  Every output is still the sequential chain
+// over q ascending, c ascending from 0.0 -- bitwise the per-entry kernel.
+#ifndef GB_K3_JZ
+#define GB_K3_JZ 3
+#endif
+#ifndef GB_K3_C2U
+#define GB_K3_C2U 7
+#endif
+constexpr int K3_JZ = GB_K3_JZ, K3_C2U = GB_K3_C2U;
+__global__ void __launch_bounds__(128) k3_bd_tiled(int Lp, int wB, const double* __restrict__ B,
+                                                   int rho, const double* __restrict__ Dt,
+                                                   int wBD, double* __restrict__ BD) {
+  const long long P = (long long)Lp * Lp * Lp;
+  const int W = 2 * wBD + 1, R = 2 * rho + 1;
+  const int NG = (W + K3_JZ - 1) / K3_JZ;
+  const long long S = (long long)W * W * W;
+  const long long SB = slots3(wB, 7), SD = (long long)R * R * R * 7;
+  const long long per = (long long)W * W * NG;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < P * per;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / per;
+    const int it = (int)(e - p * per);
+    const int g = it % NG, dy = (it / NG) % W - wBD, dx = it / (NG * W) - wBD;
+    const int dz0 = g * K3_JZ - wBD;
+    const int nz = imin(K3_JZ, wBD - dz0 + 1);  // columns of this run inside the box
+    int px, py, pz;
+    unflat3(p, Lp, &px, &py, &pz);
+    const int jx = px + dx, jy = py + dy, jz0 = pz + dz0;
+    double acc[7][K3_JZ];
+#pragma unroll
+    for (int c = 0; c < 7; ++c)
+#pragma unroll
+      for (int u = 0; u < K3_JZ; ++u) acc[c][u] = 0.0;
+    if ((unsigned)jx < (unsigned)Lp && (unsigned)jy < (unsigned)Lp) {
+      const int q0x = imax(imax(px - wB, jx - rho), 0), q1x = imin(imin(px + wB, jx + rho), Lp - 1);
+      const int q0y = imax(imax(py - wB, jy - rho), 0), q1y = imin(imin(py + wB, jy + rho), Lp - 1);
+      const int q0z = imax(imax(pz - wB, jz0 - rho), 0);
+      const int q1z = imin(imin(pz + wB, jz0 + nz - 1 + rho), Lp - 1);
+      const double* brow = B + p * 7 * SB;
+      for (int qx = q0x; qx <= q1x; ++qx)
+        for (int qy = q0y; qy <= q1y; ++qy) {
+          // column j = (jx, jy, jz0 + u): Dt row and the slot of (qx, qy, .)
+          const long long jrow = flat3(jx, jy, 0, Lp);
+          const int dxy = ((qx - jx + rho) * R + (qy - jy + rho)) * R;
+          for (int qz = q0z; qz <= q1z; ++qz) {
+            const int bs = slot3(wB, 7, qx - px, qy - py, qz - pz, 0);
+            bool on[K3_JZ];
+            const double* dp[K3_JZ];
+#pragma unroll
+            for (int u = 0; u < K3_JZ; ++u) {
+              const int jz = jz0 + u;
+              const int dzq = qz - jz;
+              on[u] = u < nz && (unsigned)jz < (unsigned)Lp && dzq >= -rho && dzq <= rho;
+              dp[u] = Dt + (jrow + jz) * SD + (long long)(dxy + dzq + rho) * 7;
+            }
+#pragma unroll K3_C2U
+            for (int c2 = 0; c2 < 7; ++c2) {
+              double dv[K3_JZ];
+#pragma unroll
+              for (int u = 0; u < K3_JZ; ++u) dv[u] = on[u] ? dp[u][c2] : 0.0;
+#pragma unroll
+              for (int c = 0; c < 7; ++c) {
+                const double b = brow[c * SB + bs + c2];
+#pragma unroll
+                for (int u = 0; u < K3_JZ; ++u)
+                  if (on[u]) acc[c][u] += b * dv[u];
+              }
+            }
+          }
+        }
+    }
+    const long long sl0 = ((long long)(dx + wBD) * W + (dy + wBD)) * W + (dz0 + wBD);
+#pragma unroll
+    for (int c = 0; c < 7; ++c)
+#pragma unroll
+      for (int u = 0; u < K3_JZ; ++u)
+        if (u < nz) BD[(p * 7 + c) * S + sl0 + u] = acc[c][u];
+  }
+}
+
 // GtD[i, j], |j - i| <= wGD: sum over (p, c) ascending with G[(p,c), i] and
 // D[(p,c), j] both in their boxes
 __global__ void k3_gtd(int Lp, int wG, const double* __restrict__ G, int rho,
@@ -992,6 +1075,46 @@ __global__ void k3_gtd(int Lp, int wG, const double* __restrict__ G, int rho,
           }
     }
     GtD[e] = acc;
+  }
+}
+
+// The same GtD enumerated by column: a thread takes (j, d) and forms entry
+// (i = j - d, j).  A warp then shares the D row of j (broadcast loads) and its
+// G reads of row (p, c) at the consecutive columns i run through consecutive
+// slots (coalesced); the per-entry kernel walked a private D row per lane.
+// Same sum per entry (p ascending, c ascending, from 0.0).  Entries whose
+// column lies outside the grid are never visited: the caller zeroes GtD first.
+__global__ void k3_gtd_bycol(int Lp, int wG, const double* __restrict__ G, int rho,
+                             const double* __restrict__ Dt, int wGD, double* __restrict__ GtD) {
+  const long long P = (long long)Lp * Lp * Lp;
+  const int W = 2 * wGD + 1, R = 2 * rho + 1;
+  const long long S = (long long)W * W * W;
+  const long long SG = slots3(wG, 1), SD = (long long)R * R * R * 7;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < P * S;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / S;
+    const int sl = (int)(e - j * S);
+    const int dz = sl % W - wGD, dy = (sl / W) % W - wGD, dx = sl / (W * W) - wGD;
+    int jx, jy, jz;
+    unflat3(j, Lp, &jx, &jy, &jz);
+    const int x = jx - dx, y = jy - dy, z = jz - dz;
+    if (!inside3(x, y, z, Lp)) continue;
+    const long long i = flat3(x, y, z, Lp);
+    const int p0x = imax(imax(x - wG, jx - rho), 0), p1x = imin(imin(x + wG, jx + rho), Lp - 1);
+    const int p0y = imax(imax(y - wG, jy - rho), 0), p1y = imin(imin(y + wG, jy + rho), Lp - 1);
+    const int p0z = imax(imax(z - wG, jz - rho), 0), p1z = imin(imin(z + wG, jz + rho), Lp - 1);
+    const double* drow = Dt + j * SD;
+    double acc = 0.0;
+    for (int px = p0x; px <= p1x; ++px)
+      for (int py = p0y; py <= p1y; ++py)
+        for (int pz = p0z; pz <= p1z; ++pz) {
+          const long long pr = flat3(px, py, pz, Lp) * 7;
+          const int gs = slot3(wG, 1, x - px, y - py, z - pz, 0);
+          const int ds = slot3(rho, 7, px - jx, py - jy, pz - jz, 0);
+#pragma unroll
+          for (int c = 0; c < 7; ++c) acc += G[(pr + c) * SG + gs] * drow[ds + c];
+        }
+    GtD[i * S + sl] = acc;
   }
 }
 
@@ -1043,6 +1166,86 @@ __global__ void k3_coarse_raw(int Lp, int wP, const double* __restrict__ PAPt, i
       v = ((0.015625 * pap + g1) + g2) + dbd;
     }
     raw[e] = v;
+  }
+}
+
+// The same raw, a run of K3_JZ consecutive columns along z per thread: the 7
+// correction entries of (i, p) are loaded once per run and the BD entries of
+// the run sit side by side.  Same sums per entry as k3_coarse_raw.
+__global__ void __launch_bounds__(256) k3_coarse_raw_tiled(
+    int Lp, int wP, const double* __restrict__ PAPt, int wGD, const double* __restrict__ GtD,
+    int rho, const double* __restrict__ Dt, int wBD, const double* __restrict__ BD, int wA2,
+    double* __restrict__ raw) {
+  const long long P = (long long)Lp * Lp * Lp;
+  const int W = 2 * wA2 + 1, R = 2 * rho + 1;
+  const int NG = (W + K3_JZ - 1) / K3_JZ;
+  const long long S = (long long)W * W * W;
+  const long long SP = slots3(wP, 1), SGD = slots3(wGD, 1), SBD = slots3(wBD, 1);
+  const long long SD = (long long)R * R * R * 7;
+  const long long per = (long long)W * W * NG;
+  const int WB = 2 * wBD + 1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < P * per;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / per;
+    const int it = (int)(e - i * per);
+    const int g = it % NG, dy = (it / NG) % W - wA2, dx = it / (NG * W) - wA2;
+    const int dz0 = g * K3_JZ - wA2;
+    const int nz = imin(K3_JZ, wA2 - dz0 + 1);
+    int x, y, z;
+    unflat3(i, Lp, &x, &y, &z);
+    const int jx = x + dx, jy = y + dy, jz0 = z + dz0;
+    double dbd[K3_JZ];
+    bool in[K3_JZ];
+#pragma unroll
+    for (int u = 0; u < K3_JZ; ++u) {
+      dbd[u] = 0.0;
+      in[u] = u < nz && inside3(jx, jy, jz0 + u, Lp);
+    }
+    if ((unsigned)jx < (unsigned)Lp && (unsigned)jy < (unsigned)Lp) {
+      const int p0x = imax(imax(x - rho, jx - wBD), 0), p1x = imin(imin(x + rho, jx + wBD), Lp - 1);
+      const int p0y = imax(imax(y - rho, jy - wBD), 0), p1y = imin(imin(y + rho, jy + wBD), Lp - 1);
+      const int p0z = imax(imax(z - rho, jz0 - wBD), 0);
+      const int p1z = imin(imin(z + rho, jz0 + nz - 1 + wBD), Lp - 1);
+      const double* drow = Dt + i * SD;
+      for (int px = p0x; px <= p1x; ++px)
+        for (int py = p0y; py <= p1y; ++py) {
+          const int bxy = ((jx - px + wBD) * WB + (jy - py + wBD)) * WB;
+          for (int pz = p0z; pz <= p1z; ++pz) {
+            const long long pr = flat3(px, py, pz, Lp) * 7;
+            const int ds = slot3(rho, 7, px - x, py - y, pz - z, 0);
+            const int bz0 = jz0 - pz + wBD;  // slot of u = 0 along z
+            bool on[K3_JZ];
+#pragma unroll
+            for (int u = 0; u < K3_JZ; ++u) on[u] = in[u] && (unsigned)(bz0 + u) < (unsigned)WB;
+#pragma unroll
+            for (int c = 0; c < 7; ++c) {
+              const double d = drow[ds + c];
+              const double* bp = BD + (pr + c) * SBD + bxy + bz0;
+#pragma unroll
+              for (int u = 0; u < K3_JZ; ++u)
+                if (on[u]) dbd[u] += d * bp[u];
+            }
+          }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < K3_JZ; ++u) {
+      if (u >= nz) continue;
+      const int dz = dz0 + u;
+      double v = 0.0;
+      if (in[u]) {
+        const long long j = flat3(jx, jy, jz0 + u, Lp);
+        double pap = 0.0, g1 = 0.0, g2 = 0.0;
+        if (abs(dx) <= wP && abs(dy) <= wP && abs(dz) <= wP)
+          pap = PAPt[i * SP + slot3(wP, 1, dx, dy, dz, 0)];
+        if (abs(dx) <= wGD && abs(dy) <= wGD && abs(dz) <= wGD) {
+          g1 = GtD[i * SGD + slot3(wGD, 1, dx, dy, dz, 0)];
+          g2 = GtD[j * SGD + slot3(wGD, 1, -dx, -dy, -dz, 0)];
+        }
+        v = ((0.015625 * pap + g1) + g2) + dbd[u];
+      }
+      raw[i * S + ((long long)(dx + wA2) * W + (dy + wA2)) * W + (dz + wA2)] = v;
+    }
   }
 }
 
@@ -1157,6 +1360,8 @@ __global__ void k3_psi_t_apply(int L, int rho, int wd, const double* __restrict_
 }  // namespace gb
 
 using namespace gb;
+
+int g_k3_tiled = 1;  // gb_tune(6): 0 = per-entry 3-D product kernels (cross-check)
 
 static inline int grid3(long long work, int block) {
   const long long g = (work + block - 1) / block;
@@ -1280,10 +1485,27 @@ int gbk3_triple(int Lp, int wB, const double* B, const double* G, const double* 
                 const double* Dt, int wBD, double* BD, int wGD, double* GtD, int wA2,
                 double* raw, cudaStream_t s) {
   const long long P = (long long)Lp * Lp * Lp;
-  k3_bd<<<grid3(P * 7 * slots3(wBD, 1), 256), 256, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD);
-  k3_gtd<<<grid3(P * slots3(wGD, 1), 256), 256, 0, s>>>(Lp, wB, G, rho, Dt, wGD, GtD);
-  k3_coarse_raw<<<grid3(P * slots3(wA2, 1), 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt,
-                                                                wBD, BD, wA2, raw);
+  if (g_k3_tiled) {
+    // (a D copy by rows, coalesced over the runs, was measured too: no change)
+    const int W = 2 * wBD + 1;
+    const long long items = P * W * W * ((W + K3_JZ - 1) / K3_JZ);
+    k3_bd_tiled<<<grid3(items, 128), 128, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD);
+    cudaError_t e = cudaMemsetAsync(GtD, 0, sizeof(double) * P * slots3(wGD, 1), s);
+    if (e != cudaSuccess) return (int)e;
+    k3_gtd_bycol<<<grid3(P * slots3(wGD, 1), 256), 256, 0, s>>>(Lp, wB, G, rho, Dt, wGD, GtD);
+  } else {
+    k3_bd<<<grid3(P * 7 * slots3(wBD, 1), 256), 256, 0, s>>>(Lp, wB, B, rho, Dt, wBD, BD);
+    k3_gtd<<<grid3(P * slots3(wGD, 1), 256), 256, 0, s>>>(Lp, wB, G, rho, Dt, wGD, GtD);
+  }
+  if (g_k3_tiled) {
+    const int W = 2 * wA2 + 1;
+    const long long items = P * W * W * ((W + K3_JZ - 1) / K3_JZ);
+    k3_coarse_raw_tiled<<<grid3(items, 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt, wBD,
+                                                           BD, wA2, raw);
+  } else {
+    k3_coarse_raw<<<grid3(P * slots3(wA2, 1), 256), 256, 0, s>>>(Lp, wB, PAPt, wGD, GtD, rho, Dt,
+                                                                  wBD, BD, wA2, raw);
+  }
   return (int)cudaGetLastError();
 }
 int gbk3_apply_w(int Lp, const double* host_w, const double* g, const double* sv, double* out,

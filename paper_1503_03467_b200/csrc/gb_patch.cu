@@ -754,13 +754,14 @@ static int g_patch_v3 = 1;
 static int g_mass_dense = 0;
 static int g_mass_types = 1;
 int gbk_tune(int what, int value) {
-  extern int g_sym_ws_ctas, g_sym_ws_on;
+  extern int g_sym_ws_ctas, g_sym_ws_on, g_k3_tiled;
   int* slot = what == 0   ? &g_patch_grid
               : what == 1 ? &g_patch_v3
               : what == 2 ? &g_mass_dense
               : what == 3 ? &g_sym_ws_ctas
               : what == 4 ? &g_mass_types
               : what == 5 ? &g_sym_ws_on
+              : what == 6 ? &g_k3_tiled
                           : nullptr;
   if (!slot) return -1;
   const int old = *slot;

@@ -131,3 +131,25 @@ def test_3d_lanczos_lambda_min_is_the_inverse_iteration():
         lam_min, lam_max = op.eig_extremes(method="cg")
         np.testing.assert_allclose(res.levels[k].lambda_max_subband, lam_max, rtol=1e-12)
         np.testing.assert_allclose(res.levels[k].lambda_min_subband, lam_min, rtol=1e-4)
+
+
+def test_3d_tiled_products_are_bitwise_the_per_entry_kernels():
+    """The register-tiled / column-enumerated split triple product
+    (k3_bd_tiled, k3_gtd_bycol, k3_coarse_raw_tiled; gb_tune(6) = 1, default)
+    keeps every entry's summation order, so A^(k-1) at every level equals the
+    per-entry kernels' bit for bit (clipped patches, odd run lengths: q = 4)."""
+    from paper_1503_03467_b200 import _native as nat, gamblet_3d as g3
+    grid, M, A, g = _inputs(4, "checker")
+    lib = nat.load()
+    old = lib.gb_tune(6, -1)
+    try:
+        lib.gb_tune(6, 0)
+        a = g3.fast_solve_3d(M, A, g, 4, 1e-13, uniform_rho=2)
+        lib.gb_tune(6, 1)
+        b = g3.fast_solve_3d(M, A, g, 4, 1e-13, uniform_rho=2)
+    finally:
+        lib.gb_tune(6, old)
+    for k in range(4, 0, -1):
+        sa, sb = a.levels[k].stiffness, b.levels[k].stiffness
+        assert O.same_pattern(sa, sb) and np.array_equal(sa.data, sb.data), f"A^({k})"
+    assert np.array_equal(a.solution.u, b.solution.u)
