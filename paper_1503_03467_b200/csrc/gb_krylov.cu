@@ -2628,6 +2628,21 @@ static int launch_dual(const gb_level_engine_args* ec, double* xb, double* yb, i
     }
     return (int)cudaGetLastError();
   }
+  if (!use_tiled(e->L, 3, e->w)) {
+    // levels below the tile width (L < 64): the row-per-thread kernels, one
+    // launch per half
+    const int gs = row_grid((long long)e->L * e->L * 3);
+    const size_t sm = off_smem(3, e->w);
+    k_tcg_spmv<3><<<gs, 256, sm, s>>>(e->L, e->w, e->BsT, e->pa, e->apa, (KState*)e->sta,
+                                      e->parta);
+    if (mb == 0)
+      k_tcg_spmv<3><<<gs, 256, sm, s>>>(e->L, e->w, e->BsT, xb, yb, (KState*)e->stb, e->partb);
+    else
+      k_tpow_apply<3><<<gs, 256, sm, s>>>(e->L, e->w, e->BsT, xb, yb, (KState*)e->stb,
+                                          e->partb);
+    *nl += 2;
+    return (int)cudaGetLastError();
+  }
   const int W2 = 2 * e->w + 1;
   const size_t smem = ((size_t)(W2 * W2 * 3 + 2) / 2 + 1) * sizeof(double) +
                       2 * (size_t)W2 * (kTileP + 2 * e->w) * 3 * sizeof(double);
@@ -2658,6 +2673,16 @@ static int launch_single(const gb_level_engine_args* e, const double* x, double*
     }
     return (int)cudaGetLastError();
   }
+  if (!use_tiled(e->L, 3, e->w)) {
+    const int gs = row_grid((long long)e->L * e->L * 3);
+    const size_t sm = off_smem(3, e->w);
+    if (mode == 0)
+      k_tcg_spmv<3><<<gs, 256, sm, s>>>(e->L, e->w, e->BsT, x, y, (KState*)st, part);
+    else
+      k_tpow_apply<3><<<gs, 256, sm, s>>>(e->L, e->w, e->BsT, x, y, (KState*)st, part);
+    *nl += 1;
+    return (int)cudaGetLastError();
+  }
   if (mode == 0)
     k_tcg_spmv_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y,
                                                                       (KState*)st, part);
@@ -2675,7 +2700,11 @@ static int launch_plain(const gb_level_engine_args* e, const double* x, double* 
     return sym_apply(e->L, e->w, e->BsT, 1, x, y, nullptr, nullptr, 2, nullptr, nullptr, nullptr,
                      nullptr, 2, s);
   }
-  k_tbox_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y);
+  if (!use_tiled(e->L, 3, e->w))
+    k_tbox_apply<3><<<row_grid((long long)e->L * e->L * 3), 256, off_smem(3, e->w), s>>>(
+        e->L, e->w, e->BsT, x, y);
+  else
+    k_tbox_apply_tiled<<<tiled_grid(e->L), 192, tiled_smem(e->w), s>>>(e->L, e->w, e->BsT, x, y);
   *nl += 1;
   return (int)cudaGetLastError();
 }

@@ -616,8 +616,23 @@ ENGINE_TIMING = None
 PAIRED_ENGINE = True
 
 
-def _engine_ok(op):
-    return (op.nr == 3 and op.L % 64 == 0 and op.w <= 8)
+# The C level engine on levels below the tile width (L < 64, row-per-thread
+# kernels): used when those levels are the critical path, i.e. for q <=
+# SMALL_ENGINE_MAX_Q (measured: q=7 17.2 -> 14.5 ms; from q=8 on they are hidden
+# behind the finest level and their 64-step Lanczos start only adds GPU work:
+# q=9 69.9 -> 73.2 ms, q=10 254.4 -> 257 ms).  Sides below ENGINE_MIN_L always
+# keep the host-driven inverse iteration (their Krylov spaces are exhausted
+# within the engine's first Lanczos chunk).
+ENGINE_MIN_L = int(os.environ.get("GB_ENGINE_MIN_L", "8"))
+SMALL_ENGINE_MAX_Q = 7
+
+
+def _engine_ok(op, small=False):
+    """Levels the C level engine covers: the tiled / symmetric-band kernels
+    need L % 64 == 0; `small`: also the sides ENGINE_MIN_L <= L < 64."""
+    if op.nr != 3 or op.w > 8:
+        return False
+    return op.L % 64 == 0 or (small and op.L % 2 == 0 and ENGINE_MIN_L <= op.L < 64)
 
 
 def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
@@ -766,6 +781,7 @@ class _LevelTasks:
                 max_workers=SPECTRAL_WORKERS, thread_name_prefix="gb-level")
         self.futures = []
         self.solver = solver
+        self.small_engine = solver is not None and solver.tree.q <= SMALL_ENGINE_MAX_Q
 
     _level_streams = {}
     _level_streams_lock = threading.Lock()
@@ -817,7 +833,7 @@ class _LevelTasks:
             if g is not None:
                 g.record_stream(st)  # main-stream tensor read on this stream
             if (SPECTRAL and PAIRED_ENGINE and self.solver is not None and g is not None
-                    and _engine_ok(op)):
+                    and _engine_ok(op, self.small_engine)):
                 box = {}
 
                 def run_engine(op_, rhs_pad, tol):
