@@ -698,6 +698,11 @@ __device__ __forceinline__ double trow_apply(const double* __restrict__ BsT, lon
   return acc0 + acc1;
 }
 
+// Operators with fewer rows than this run the split form of tbox_pass (a CTA
+// per 32-row block, its 8 warps each a slice of the slots): with a thread per
+// row a 3 072-row level keeps 12 CTAs busy for 49 us per pass
+constexpr long long kSplitMaxRows = 148LL * 256;
+
 // y = BsT x over padded vectors for rows [0, R); returns partial dots x.y, y.y
 template <int NR>
 __device__ __forceinline__ void tbox_pass(int L, int w, const double* __restrict__ BsT,
@@ -706,6 +711,46 @@ __device__ __forceinline__ void tbox_pass(int L, int w, const double* __restrict
   const int W2 = 2 * w + 1, S = W2 * W2 * NR, Lpad = L + 2 * w;
   const long long R = (long long)L * L * NR;
   double d0 = 0.0, d1 = 0.0;
+  if (R < kSplitMaxRows) {  // (uniform; the launchers size the grid to match)
+    __shared__ double red[256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int Sp = S + (S & 1), M = Sp >> 1;
+    const int per = (M + nw - 1) / nw;
+    const int m0 = imin(warp * per, M), m1 = imin(m0 + per, M);
+    const long long nblk = (R + 31) >> 5;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+      const long long r = blk * 32 + lane;
+      double acc0 = 0.0, acc1 = 0.0;
+      long long yr = 0;
+      if (r < R) {
+        const long long p = r / NR;
+        const int c = (int)(r - p * NR);
+        const int ps = (int)(p / L), pt = (int)(p % L);
+        const long long xb = ((long long)ps * Lpad + pt) * NR;
+        yr = ((long long)(ps + w) * Lpad + pt + w) * NR + c;
+        const double2* a = reinterpret_cast<const double2*>(BsT + blk * (32LL * Sp)) + lane;
+#pragma unroll 4
+        for (int m = m0; m < m1; ++m) {
+          const double2 v = __ldg(a + 32 * m);
+          acc0 = fma(v.x, __ldg(x + xb + off[2 * m]), acc0);
+          acc1 = fma(v.y, __ldg(x + xb + off[2 * m + 1]), acc1);
+        }
+      }
+      red[threadIdx.x] = acc0 + acc1;
+      __syncthreads();
+      if (warp == 0 && r < R) {
+        double v = red[lane];
+        for (int j = 1; j < nw; ++j) v += red[j * 32 + lane];  // slices in order
+        y[yr] = v;
+        d0 += x[yr] * v;
+        d1 += v * v;
+      }
+      __syncthreads();
+    }
+    *xy = d0;
+    *yy = d1;
+    return;
+  }
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
        r += (long long)gridDim.x * blockDim.x) {
     const long long p = r / NR;
@@ -1804,7 +1849,11 @@ int gbk_pbox_apply(int L, int nr, int w, const double* Bs, const double* x, doub
 
 
 // ---- v3 (slot-major) launchers ----
-static inline int row_grid(long long R) { return grid_for(R, 256, kRedBlocks); }
+static inline int row_grid(long long R) {
+  // small operators: a CTA per 32-row block (tbox_pass, split form)
+  if (R < kSplitMaxRows) return grid_for((R + 31) / 32 * 256, 256, kRedBlocks);
+  return grid_for(R, 256, kRedBlocks);
+}
 static inline bool use_tiled(int L, int nr, int w) {
   return nr == 3 && L % kTileP == 0 && w <= 8;
 }

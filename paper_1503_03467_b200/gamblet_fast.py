@@ -620,19 +620,19 @@ PAIRED_ENGINE = True
 # kernels): used when those levels are the critical path, i.e. for q <=
 # SMALL_ENGINE_MAX_Q (measured: q=7 17.2 -> 14.5 ms; from q=8 on they are hidden
 # behind the finest level and their 64-step Lanczos start only adds GPU work:
-# q=9 69.9 -> 73.2 ms, q=10 254.4 -> 257 ms).  Sides below ENGINE_MIN_L always
-# keep the host-driven inverse iteration (their Krylov spaces are exhausted
-# within the engine's first Lanczos chunk).
-ENGINE_MIN_L = int(os.environ.get("GB_ENGINE_MIN_L", "8"))
+# q=9 69.9 -> 73.2 ms, q=10 254.4 -> 257 ms).  Sides below LANCZOS_MIN_L run
+# the engine's inverse iteration (PCG inner solves, the host-driven path's
+# algorithm): their Krylov spaces are exhausted within the first Lanczos chunk.
+LANCZOS_MIN_L = int(os.environ.get("GB_LANCZOS_MIN_L", "8"))
 SMALL_ENGINE_MAX_Q = 7
 
 
 def _engine_ok(op, small=False):
     """Levels the C level engine covers: the tiled / symmetric-band kernels
-    need L % 64 == 0; `small`: also the sides ENGINE_MIN_L <= L < 64."""
+    need L % 64 == 0; `small`: also the even sides below 64."""
     if op.nr != 3 or op.w > 8:
         return False
-    return op.L % 64 == 0 or (small and op.L % 2 == 0 and ENGINE_MIN_L <= op.L < 64)
+    return op.L % 64 == 0 or (small and op.L % 2 == 0 and op.L < 64)
 
 
 def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
@@ -675,7 +675,7 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
         hdots=kb.hdots.data_ptr(), tol=tol, inner_tol=max(1e-12, 1e-3 * tol),
         inner_max_iter=min(max(200, 2 * n), MAX_ITER_CAP),
         inner_pcg=int(SPECTRAL_INNER != "cg"), cz=dv.ptr(cz), layout=op.layout)
-    if SPECTRAL_INNER == "lanczos":
+    if SPECTRAL_INNER == "lanczos" and op.L >= LANCZOS_MIN_L:
         cap = int(min(n, LANCZOS_CAP))
         lz = dv.empty(2 * cap)
         hlz = torch.empty(2 * cap, dtype=torch.float64, pin_memory=True)
