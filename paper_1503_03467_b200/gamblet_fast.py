@@ -434,6 +434,13 @@ class _POp:
         layout, so any vector can be an SpMV output)."""
         return dv.zeros(self.npad + self.vtail)
 
+    def vecs(self, count):
+        """`count` zero padded vectors carved out of one allocation (one fill
+        kernel; each starts on a 256-byte boundary)."""
+        stride = (self.npad + self.vtail + 31) // 32 * 32
+        buf = dv.zeros(count * stride)
+        return [buf[i * stride:i * stride + self.npad + self.vtail] for i in range(count)]
+
     def pad(self, x, scale=None):
         out = self.vec()
         nat.call("gb_pad", self.L, self.nr, self.w, dv.ptr(x), dv.ptr(scale), dv.ptr(out),
@@ -645,7 +652,7 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
     # A: initialised PCG
     inv = op.bj_inv()
     ka = _Krylov(op.npad)
-    xa, ra, pa, apa, za = (op.vec() for _ in range(5))
+    xa, ra, pa, apa, za, yb, xn, ax, cx, cr, cp, cap, cz = op.vecs(13)
     max_a = min(max(200, 2 * n), MAX_ITER_CAP)
     nat.call("gb_state_reset", dv.ptr(ka.state), max_a, st)
     nat.call("gb_bjcg_init", op.L, op.w, dv.ptr(rhs_pad), None, None, 1.0, dv.ptr(xa), dv.ptr(ra),
@@ -663,7 +670,6 @@ def _paired_level(op, rhs_pad, tol_a, tol=0.1, max_iter=500, seed=24337):
              dv.ptr(kb.state), dv.ptr(kb.part), st)
     nat.call("gb_scale_by_norm", op.npad, dv.ptr(xs), dv.ptr(kb.dots), 0, dv.ptr(xs), None, st)
     nat.call("gb_state_reset", dv.ptr(kb.state), max_iter, st)
-    yb, xn, ax, cx, cr, cp, cap, cz = (op.vec() for _ in range(8))
     dots = dv.empty(4)
     args = LevelEngineArgs(
         L=op.L, w=op.w, max_chunk=128, max_outer=max_iter, BsT=dv.ptr(op.BsT),
